@@ -1,0 +1,82 @@
+"""Assembled Schur-system problem per parameter set (oracle; test infra only).
+
+The system of the north star (Eq.(2)) on Γ after eliminating the bulk:
+    S = K S_unit + γ F,   S_unit = A^ii - A^i0 (A^00)^-1 A^0i,   F = L_h^{-1/2}
+(PAPER.md:107-122, 146-148, 178-180, 219-221), preconditioned by the RA of
+S_Γ^-1 = (K L^{1/2} + γ L^{-1/2})^-1.
+
+Two tiers:
+  DenseProblem  — dense S_unit by elimination of the assembled stiffness, dense F by the
+                  generalised eigendecomposition; any dim, small/moderate N.
+  ModeProblem2D — 2D only, full config sizes: the same operators applied in the
+                  orthonormal sine basis of Γ (scipy.fft DST-I), with S_unit's mode values
+                  from the mode-wise layer elimination and the pair's mode values from the
+                  assembled tridiagonal entries; pinned to DenseProblem in tests.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import fem, ra, schur, spectral
+
+
+class DenseProblem:
+    def __init__(self, dim: int, N: int, method: str = "layers"):
+        self.dim, self.N = dim, N
+        self.S_unit = schur.schur_layers(dim, N) if method == "layers" else schur.schur_bruteforce(dim, N)
+        self.A_g, self.M_g = fem.trace_pair(dim, N)
+        self.gevp = spectral.GEVP(self.A_g, self.M_g)
+        self.F = self.gevp.power(-0.5)
+        self.n_gamma = self.S_unit.shape[0]
+
+    def S(self, K, gamma):
+        return K * self.S_unit + gamma * self.F
+
+    def apply_S(self, K, gamma, X):
+        return K * (self.S_unit @ X) + gamma * (self.F @ X)
+
+    def apply_P_ra(self, c0, poles, residues, X):
+        return ra.apply_ra(self.A_g, self.M_g, c0, poles, residues, X)
+
+    def apply_P_exact(self, K, gamma, X):
+        return ra.apply_exact_precond(self.gevp, K, gamma, X)
+
+    def spectrum(self):
+        return self.gevp.lam
+
+
+class ModeProblem2D:
+    def __init__(self, N: int):
+        self.dim, self.N = 2, N
+        n = N - 1
+        self.n_gamma = n
+        a_d, a_o, m_d, m_o = fem.trace_pair_1d(N)
+        # uniform mesh: constant Toeplitz entries; mode value = diag + 2 off cos θ_b
+        assert np.allclose(a_d, a_d[0]) and np.allclose(m_d, m_d[0])
+        c = schur._cos_theta(n)
+        ao = a_o[0] if n > 1 else 0.0
+        mo = m_o[0] if n > 1 else 0.0
+        self.alpha = a_d[0] + 2.0 * ao * c          # A_Γ mode values
+        self.mu = m_d[0] + 2.0 * mo * c             # M_Γ mode values
+        self.lam = self.alpha / self.mu             # generalised eigenvalues of (A_Γ, M_Γ)
+        self.s = schur.schur_modes_2d(N)            # S_unit mode values
+        self.f = self.mu * self.lam ** -0.5         # F mode values: (MU) Λ^-1/2 (MU)^T
+        self.band = (a_d, a_o, m_d, m_o)
+
+    def apply_S(self, K, gamma, X):
+        Xh = schur.dst_ortho(X, axis=0)
+        w = (K * self.s + gamma * self.f)
+        return schur.dst_ortho(w[:, None] * Xh if X.ndim == 2 else w * Xh, axis=0)
+
+    def apply_P_ra(self, c0, poles, residues, X):
+        """Parity form: banded Cholesky solves of the assembled tridiagonal pair."""
+        a_d, a_o, m_d, m_o = self.band
+        return ra.apply_ra_banded_tri(a_d, a_o, m_d, m_o, c0, poles, residues, X)
+
+    def apply_P_exact(self, K, gamma, X):
+        Xh = schur.dst_ortho(X, axis=0)
+        w = 1.0 / (self.mu * (K * self.lam ** 0.5 + gamma * self.lam ** -0.5))
+        return schur.dst_ortho(w[:, None] * Xh if X.ndim == 2 else w * Xh, axis=0)
+
+    def spectrum(self):
+        return np.sort(self.lam)

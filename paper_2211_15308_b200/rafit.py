@@ -1,0 +1,146 @@
+"""Host-side rational-approximation fit (setup data for `dd_setup`; not on the GPU path).
+
+PAPER.md:188-199 (footnote, Eq.(8)): the preconditioner S_Γ^-1 = (K L^{1/2} + γ L^{-1/2})^-1
+is realised as  c0 M^-1 + Σ_k c_k (L + p_k M)^-1  from a rational approximation f_RA of
+f(x) = (K x^{1/2} + γ x^{-1/2})^-1 on the spectral interval; "the number of poles m does
+not depend on the dimensionality of Q_h and is instead determined by the accuracy ε_RA".
+The paper defers the construction to its references; this module's
+choice (reading A9'):
+
+ 1. g(x) = x^{-1/2} on [λ_min, λ_max] by Zolotarev's best relative rational approximation
+    of type (n, n) (closed form in Jacobi elliptic functions, evaluated with mpmath at 50
+    digits): g_RA(x) = d0 Π_l (x + c_{2l}) / Π_l (x + c_{2l-1}),
+    c_j = sn^2(jK'/(2n+1); k') / cn^2(jK'/(2n+1); k'), k'^2 = 1 - λ_min/λ_max,
+    with x scaled to [1, λ_max/λ_min] and d0 set so the relative error equioscillates.
+    All poles are real and negative and all residues positive (Stieltjes function).
+ 2. f(x) = x g(x) / (K (x + γ/K)) exactly, expanded in partial fractions; this adds the pole
+    -γ/K and keeps the relative error of g (f_RA/f = g_RA/g).
+ Poles are returned with the sign convention of reading A7: r(x) = c0 + Σ c_k/(x - p_k),
+ p_k < 0, and the library forms A_Γ - p_k M_Γ.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class RationalApprox:
+    c0: float
+    poles: np.ndarray        # p_k < 0
+    residues: np.ndarray     # c_k (may be negative after step 2)
+    lam_min: float
+    lam_max: float
+    K: float
+    gamma: float
+    n_zolo: int
+    rel_err: float = float("nan")      # max |r/f - 1| on a 2e4-point geometric grid
+    cancel: float = float("nan")       # κ_c of reading A11
+
+    @property
+    def m(self) -> int:
+        return len(self.poles)
+
+    def __call__(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        out = np.full_like(x, self.c0)
+        for p, c in zip(self.poles, self.residues):
+            out = out + c / (x - p)
+        return out
+
+    def to_json(self):
+        return {"c0": self.c0, "poles": list(map(float, self.poles)),
+                "residues": list(map(float, self.residues)), "lam_min": self.lam_min,
+                "lam_max": self.lam_max, "K": self.K, "gamma": self.gamma,
+                "n_zolo": self.n_zolo, "rel_err": self.rel_err, "cancel": self.cancel}
+
+
+def _zolotarev_invsqrt(kappa: float, n: int, dps: int = 50):
+    """Type-(n,n) Zolotarev approximation of x^{-1/2} on [1, kappa] in pole-residue form.
+
+    Returns (d0, q, r) as mpmath numbers: g(x) = d0 + Σ_l r_l / (x - q_l), q_l < 0."""
+    import mpmath as mp
+    with mp.workdps(dps):
+        kappa = mp.mpf(kappa)
+        m = 1 - 1 / kappa                     # parameter k'^2
+        Kp = mp.ellipk(m)
+        c = []
+        for j in range(1, 2 * n + 1):
+            u = j * Kp / (2 * n + 1)
+            sn = mp.ellipfun("sn", u, m=m)
+            cn = mp.ellipfun("cn", u, m=m)
+            c.append((sn / cn) ** 2)
+        num = [c[2 * l + 1] for l in range(n)]     # c_2, c_4, ..., c_2n
+        den = [c[2 * l] for l in range(n)]         # c_1, c_3, ..., c_2n-1
+        # equioscillation constant: extrema of sqrt(x) g0(x) on [1, kappa] are attained
+        # at the endpoints and at interior alternation points; sample densely in log x.
+        def g0(x):
+            v = mp.mpf(1)
+            for a in num:
+                v *= (x + a)
+            for b in den:
+                v /= (x + b)
+            return v
+        xs = [mp.power(kappa, mp.mpf(t) / 4000) for t in range(4001)]
+        vals = [mp.sqrt(x) * g0(x) for x in xs]
+        d0 = 2 / (max(vals) + min(vals))
+        q, r = [], []
+        for l, b in enumerate(den):
+            pole = -b
+            res = d0
+            for a in num:
+                res *= (pole + a)
+            for j, b2 in enumerate(den):
+                if j != l:
+                    res /= (pole + b2)
+            q.append(pole); r.append(res)
+        return d0, q, r
+
+
+def fit_ra(K: float, gamma: float, lam_min: float, lam_max: float, n_poles: int) -> RationalApprox:
+    """RA of f(x) = 1/(K x^{1/2} + γ x^{-1/2}) on [lam_min, lam_max] with `n_poles` poles in
+    total (n_poles - 1 from the Zolotarev fit of x^{-1/2}, plus -γ/K when γ > 0)."""
+    import mpmath as mp
+    if not (K > 0 and gamma >= 0 and 0 < lam_min < lam_max and np.isfinite(lam_max)):
+        raise ValueError("need K > 0, gamma >= 0, 0 < lam_min < lam_max")
+    nz = n_poles - 1 if gamma > 0 else n_poles
+    if nz < 1:
+        raise ValueError("n_poles too small")
+    with mp.workdps(50):
+        d0, q, r = _zolotarev_invsqrt(lam_max / lam_min, nz)
+        lm = mp.mpf(lam_min)
+        C0 = d0 / mp.sqrt(lm)                      # λ^{-1/2} ≈ C0 + Σ R_l/(λ - P_l)
+        P = [ql * lm for ql in q]
+        R = [rl * mp.sqrt(lm) for rl in r]
+        Kq, a = mp.mpf(K), mp.mpf(gamma) / mp.mpf(K)
+        c0 = C0 / Kq
+        poles, res = [], []
+        for Pl, Rl in zip(P, R):
+            poles.append(Pl)
+            res.append(Rl * Pl / ((Pl + a) * Kq))
+        if gamma > 0:
+            poles.append(-a)
+            res.append((-C0 * a + sum(Rl * a / (a + Pl) for Pl, Rl in zip(P, R))) / Kq)
+        order = sorted(range(len(poles)), key=lambda i: float(poles[i]))[::-1]  # p closest to 0 first
+        ra = RationalApprox(float(c0), np.array([float(poles[i]) for i in order]),
+                            np.array([float(res[i]) for i in order]), float(lam_min),
+                            float(lam_max), float(K), float(gamma), nz)
+    xs = np.geomspace(lam_min, lam_max, 20000)
+    f = 1.0 / (K * np.sqrt(xs) + gamma / np.sqrt(xs))
+    ra.rel_err = float(np.max(np.abs(ra(xs) / f - 1.0)))
+    acc = np.full_like(xs, abs(ra.c0))
+    for p, c in zip(ra.poles, ra.residues):
+        acc += np.abs(c / (xs - p))
+    ra.cancel = float(np.max(acc / f))
+    return ra
+
+
+def interval_1d(N: int):
+    """Spectral interval of the 1D P1 pair on Γ with Dirichlet ends, closed form
+    λ_k = (6/h^2)(1 - cos θ_k)/(2 + cos θ_k), θ_k = kπ/N, k = 1..N-1 (north star)."""
+    h = 1.0 / N
+    def lam(k):
+        s2 = np.sin(0.5 * np.pi * k / N) ** 2          # (1 - cos θ)/2 without cancellation
+        return (6.0 / h ** 2) * (2.0 * s2) / (3.0 - 2.0 * s2)
+    return float(lam(1)), float(lam(N - 1))

@@ -1,0 +1,367 @@
+"""Pins of the CPU oracle against things other than itself (CPU only, `-m "not gpu"`).
+
+Each test names the fact it checks: a closed form of the mathematics, a textbook
+matrix, a brute-force computation on tiny inputs, a library routine, or a claim of the
+paper.  A plausible slip in the oracle (dropped term, wrong sign/index, transposed
+operand) fails at least one of them.  See DESIGN.md §"Oracle pins".
+"""
+import numpy as np
+import pytest
+
+from oracle import fem, pcg, problem, ra, schur, spectral
+from paper_2211_15308_b200 import rafit
+
+
+# --------------------------------------------------------------------------- meshes
+@pytest.mark.parametrize("N", [1, 2, 4])
+def test_square_mesh_counts_and_area(N):
+    # SPEC.md "build_unit_square_mesh": (n+1)^2 vertices, 2n^2 triangles, area 1.
+    coords, cells = fem.square_mesh(N)
+    assert coords.shape[0] == (N + 1) ** 2 and cells.shape[0] == 2 * N * N
+    area = sum(fem._p1_element(coords[c])[2] for c in cells)
+    assert abs(area - 1.0) < 1e-14
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_cube_mesh_counts_and_volume(N):
+    # SPEC.md "build_unit_cube_mesh": Kuhn split, 6n^3 tets, volume 1.
+    coords, cells = fem.cube_mesh(N)
+    assert coords.shape[0] == (N + 1) ** 3 and cells.shape[0] == 6 * N ** 3
+    vol = sum(fem._p1_element(coords[c])[2] for c in cells)
+    assert abs(vol - 1.0) < 1e-14
+
+
+def _row(P, node_lattice):
+    """Row of the assembled free-node stiffness at a lattice node, as {offset: value}."""
+    N = P.N
+    lat = np.rint(P.coords * N).astype(int)
+    i = np.nonzero(np.all(lat == node_lattice, axis=1))[0][0]
+    row = P.A.getrow(i).toarray().ravel()
+    out = {}
+    for j in np.nonzero(np.abs(row) > 1e-14)[0]:
+        out[tuple(lat[j] - lat[i])] = row[j]
+    return out
+
+
+def test_bulk_stencil_2d():
+    # V1: P1 on the Freudenthal mesh reproduces the 5-point Laplacian [4; -1 x4] (textbook),
+    # independent of h; on Γ (x=0): diagonal 2, Γ-neighbours -1/2, interior neighbour -1.
+    P = fem.BulkProblem(2, 6)
+    assert _row(P, (3, 3)) == pytest.approx({(0, 0): 4.0, (1, 0): -1.0, (-1, 0): -1.0, (0, 1): -1.0, (0, -1): -1.0})
+    assert _row(P, (0, 3)) == pytest.approx({(0, 0): 2.0, (0, 1): -0.5, (0, -1): -0.5, (1, 0): -1.0})
+
+
+def test_bulk_stencil_3d():
+    # V2: Kuhn P1 stiffness is h * 7-point [6; -1 x6]; Γ-face row: 3h, -h/2 in-face, -h normal.
+    N = 4; h = 1.0 / N
+    P = fem.BulkProblem(3, N)
+    interior = {(0, 0, 0): 6 * h}
+    for ax in range(3):
+        for s in (1, -1):
+            e = [0, 0, 0]; e[ax] = s; interior[tuple(e)] = -h
+    assert _row(P, (2, 2, 2)) == pytest.approx(interior)
+    face = {(0, 0, 0): 3 * h, (1, 0, 0): -h, (0, 1, 0): -h / 2, (0, -1, 0): -h / 2, (0, 0, 1): -h / 2, (0, 0, -1): -h / 2}
+    assert _row(P, (0, 2, 2)) == pytest.approx(face)
+
+
+@pytest.mark.parametrize("N", [2, 5, 9])
+def test_trace_pair_1d_textbook(N):
+    # The 1D P1 pair with Dirichlet ends: A = (1/h) tridiag(-1,2,-1), M = (h/6) tridiag(1,4,1).
+    h = 1.0 / N; n = N - 1
+    A, M = fem.trace_pair(2, N)
+    T = lambda d, o: d * np.eye(n) + o * (np.eye(n, k=1) + np.eye(n, k=-1))
+    assert np.allclose(A, T(2 / h, -1 / h), rtol=0, atol=1e-12)
+    assert np.allclose(M, T(4 * h / 6, h / 6), rtol=0, atol=1e-15)
+    a_d, a_o, m_d, m_o = fem.trace_pair_1d(N)
+    assert np.allclose(np.diag(A), a_d) and np.allclose(np.diag(M), m_d)
+    if n > 1:
+        assert np.allclose(np.diag(A, 1), a_o) and np.allclose(np.diag(M, 1), m_o)
+
+
+def test_face_pair_3d():
+    # V5: face stiffness = 5-point [4; -1 x4] (independent of h); consistent P1 mass of the
+    # Kuhn trace = (h^2/12)[6; 1 at (±1,0),(0,±1),(1,1),(-1,-1)]; each full mass row sums to
+    # ∫ hat = h^2 (6 triangles of area h^2/2, 1/3 each).
+    N = 5; h = 1.0 / N; n = N - 1
+    A, M = fem.trace_pair(3, N)
+    idx = lambda j, k: (j - 1) * n + (k - 1)
+    r = idx(2, 2)
+    nzA = {(j - 2, k - 2): A[r, idx(j, k)] for j in range(1, n + 1) for k in range(1, n + 1) if abs(A[r, idx(j, k)]) > 1e-14}
+    assert nzA == pytest.approx({(0, 0): 4, (1, 0): -1, (-1, 0): -1, (0, 1): -1, (0, -1): -1})
+    nzM = {(j - 2, k - 2): M[r, idx(j, k)] * 12 / h ** 2 for j in range(1, n + 1) for k in range(1, n + 1) if abs(M[r, idx(j, k)]) > 1e-16}
+    assert nzM == pytest.approx({(0, 0): 6, (1, 0): 1, (-1, 0): 1, (0, 1): 1, (0, -1): 1, (1, 1): 1, (-1, -1): 1})
+    assert M[r].sum() == pytest.approx(h * h, rel=1e-13)
+
+
+# --------------------------------------------------------------------------- Schur
+def test_schur_hand_2x2():
+    # SPEC.md exact_schur_oracle: blocks [[2,1],[1,2]] -> Σ = 2 - 1*(1/2)*1 = 1.5.
+    S = schur.schur_of(np.array([[2.0, 1.0], [1.0, 2.0]]), [1])
+    assert S.shape == (1, 1) and S[0, 0] == pytest.approx(1.5, abs=1e-15)
+
+
+@pytest.mark.parametrize("N", [2, 4, 7, 16])
+def test_schur_tiers_agree_2d(N):
+    # brute-force elimination (tier 1) = layer elimination (tier 2) = mode-wise elimination (3)
+    a = schur.schur_bruteforce(2, N)
+    b = schur.schur_layers(2, N)
+    n = N - 1
+    Q = schur.dst_ortho(np.eye(n))
+    c = Q @ np.diag(schur.schur_modes_2d(N)) @ Q
+    assert np.abs(a - b).max() < 1e-14 * max(1, np.abs(a).max()) * N
+    assert np.abs(a - c).max() < 1e-13
+
+
+@pytest.mark.parametrize("N", [2, 3, 4, 6])
+def test_schur_tiers_agree_3d(N):
+    a = schur.schur_bruteforce(3, N)
+    b = schur.schur_layers(3, N)
+    n = N - 1
+    Q = schur.dst_ortho(np.eye(n)); QQ = np.kron(Q, Q)
+    c = QQ @ np.diag(schur.schur_modes_3d(N).ravel()) @ QQ
+    assert np.abs(a - b).max() < 1e-14
+    assert np.abs(a - c).max() < 1e-14
+
+
+def test_schur_spd_and_symmetric():
+    S = schur.schur_bruteforce(2, 12)
+    assert np.allclose(S, S.T, atol=1e-15)
+    assert np.linalg.eigvalsh(S).min() > 0
+
+
+def test_schur_continuum_dtn_limit():
+    # V9: the Dirichlet-to-Neumann map of the unit square (Dirichlet on the other sides)
+    # acts on sin(bπy) by bπ coth(bπ); the FE Schur complement's mode value divided by h
+    # converges to it at O(h^2).
+    errs = []
+    for N in (64, 128, 256):
+        s = schur.schur_modes_2d(N)
+        errs.append([abs(s[b - 1] * N - b * np.pi / np.tanh(b * np.pi)) for b in (1, 2)])
+    errs = np.array(errs)
+    assert errs[-1, 0] < 2e-4
+    ratio = errs[:-1] / errs[1:]
+    assert np.all(ratio > 3.5) and np.all(ratio < 4.5)
+
+
+# --------------------------------------------------------------------------- spectral
+@pytest.mark.parametrize("N", [8, 32])
+def test_closed_form_generalised_eigenvalues(N):
+    # North-star fixed point: λ_k = (6/h^2)(1 - cos θ_k)/(2 + cos θ_k), θ_k = kπ/(m+1), m+1 = N.
+    h = 1.0 / N
+    A, M = fem.trace_pair(2, N)
+    lam = spectral.GEVP(A, M).lam
+    k = np.arange(1, N)
+    th = k * np.pi / N
+    closed = (6 / h ** 2) * (1 - np.cos(th)) / (2 + np.cos(th))
+    assert np.allclose(lam, closed, rtol=1e-12, atol=0)
+    assert np.allclose(np.sort(problem.ModeProblem2D(N).lam), closed, rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("dim,N", [(2, 9), (3, 5)])
+def test_gevp_invariants(dim, N):
+    # SPEC.md spectral: U^T M U = I; L U = M U Λ; L^0 = M; L^1 = L; L^½ M^-1 L^½ = L.
+    A, M = fem.trace_pair(dim, N)
+    G = spectral.GEVP(A, M)
+    assert np.allclose(G.U.T @ M @ G.U, np.eye(len(G.lam)), atol=1e-10)
+    assert np.abs(A @ G.U - M @ G.U * G.lam).max() < 1e-9 * np.abs(A).max()
+    assert np.allclose(G.power(0.0), M, atol=1e-13)
+    assert np.allclose(G.power(1.0), A, atol=1e-9 * np.abs(A).max())
+    H = G.power(0.5)
+    assert np.allclose(H @ np.linalg.solve(M, H), A, atol=1e-8 * np.abs(A).max())
+
+
+@pytest.mark.parametrize("N", [8, 32])
+def test_fractional_term_closed_form_2d(N):
+    # V4: F = S_dst diag(μ_k λ_k^{-1/2}) S_dst with μ_k = (h/6)(4 + 2cos θ_k), built from the
+    # explicit sine matrix (not from any oracle routine).
+    h = 1.0 / N; n = N - 1
+    A, M = fem.trace_pair(2, N)
+    F = spectral.fractional_term(A, M, -0.5)
+    j = np.arange(1, n + 1)
+    Sd = np.sqrt(2.0 / N) * np.sin(np.outer(j, j) * np.pi / N)
+    th = j * np.pi / N
+    mu = (h / 6) * (4 + 2 * np.cos(th))
+    lam = (6 / h ** 2) * (1 - np.cos(th)) / (2 + np.cos(th))
+    assert np.abs(F - Sd @ np.diag(mu * lam ** -0.5) @ Sd).max() < 1e-13
+
+
+def test_dst_ortho_is_explicit_sine_matrix():
+    n = 13
+    j = np.arange(1, n + 1)
+    Sd = np.sqrt(2.0 / (n + 1)) * np.sin(np.outer(j, j) * np.pi / (n + 1))
+    assert np.allclose(schur.dst_ortho(np.eye(n)), Sd, atol=1e-15)
+
+
+# --------------------------------------------------------------------------- problems
+@pytest.mark.parametrize("N", [6, 33])
+def test_mode_problem_matches_dense(N):
+    rng = np.random.default_rng(1)
+    D = problem.DenseProblem(2, N)
+    Mo = problem.ModeProblem2D(N)
+    X = rng.uniform(-1, 1, size=(N - 1, 3))
+    for K, g in [(1.0, 0.0), (1.0, 1e2), (1e-4, 1e6)]:
+        a, b = D.apply_S(K, g, X), Mo.apply_S(K, g, X)
+        assert np.abs(a - b).max() < 1e-12 * np.abs(a).max()
+        a, b = D.apply_P_exact(K, g, X), Mo.apply_P_exact(K, g, X)
+        assert np.abs(a - b).max() < 1e-12 * np.abs(a).max()
+    poles, res = [-0.5, -30.0, -1e4], [0.3, -0.1, 2.0]
+    a, b = D.apply_P_ra(0.7, poles, res, X), Mo.apply_P_ra(0.7, poles, res, X)
+    assert np.abs(a - b).max() < 1e-12 * np.abs(a).max()
+
+
+# --------------------------------------------------------------------------- RA
+@pytest.mark.parametrize("dim,N", [(2, 17), (3, 5)])
+def test_ra_parity_form_equals_eigen_form(dim, N):
+    # banded / sparse-direct shifted solves (parity form) = U diag(r(λ)) U^T (eigen form)
+    A, M = fem.trace_pair(dim, N)
+    G = spectral.GEVP(A, M)
+    rng = np.random.default_rng(2)
+    B = rng.uniform(-1, 1, size=(A.shape[0], 4))
+    c0, poles, res = 0.25, [-0.3, -7.0, -900.0], [1.5, -0.2, 40.0]
+    a = ra.apply_ra(A, M, c0, poles, res, B)
+    b = ra.apply_ra_eigen(G, c0, poles, res, B)
+    assert np.abs(a - b).max() < 1e-11 * np.abs(a).max()
+
+
+def test_ra_trivial_cases():
+    # SPEC.md apply_ra: m = 0, c0 = 1 -> M^-1 b; linear; symmetric.
+    A, M = fem.trace_pair(2, 12)
+    rng = np.random.default_rng(3)
+    b1, b2 = rng.standard_normal((2, 11))
+    assert np.allclose(ra.apply_ra(A, M, 1.0, [], [], b1), np.linalg.solve(M, b1), atol=1e-12)
+    P = lambda b: ra.apply_ra(A, M, 0.1, [-2.0, -50.0], [1.0, 3.0], b)
+    assert np.allclose(P(b1 + 2 * b2), P(b1) + 2 * P(b2), atol=1e-13)
+    assert abs(P(b1) @ b2 - b1 @ P(b2)) < 1e-12 * abs(P(b1) @ b2)
+
+
+def test_ra_eigenvector_input():
+    # b = M v_k for an eigenvector v_k -> r(λ_k) v_k.
+    A, M = fem.trace_pair(2, 20)
+    G = spectral.GEVP(A, M)
+    c0, poles, res = 0.1, [-2.0, -50.0], [1.0, 3.0]
+    for k in (0, 7, 18):
+        v = G.U[:, k]
+        z = ra.apply_ra(A, M, c0, poles, res, M @ v)
+        assert np.allclose(z, ra.r_eval(G.lam[k], c0, poles, res) * v, rtol=1e-11, atol=1e-13)
+
+
+@pytest.mark.parametrize("N,m,bound", [(32, 12, 1e-9), (1024, 16, 1e-7), (2048, 20, 1e-8), (4096, 24, 1e-9)])
+def test_ra_fit_error_bound_on_spectrum(N, m, bound):
+    # North-star fixed point: the RA error bound on the spectral interval, evaluated at the
+    # closed-form discrete eigenvalues (oracle's own r/f evaluation); all poles real < 0.
+    lo, hi = rafit.interval_1d(N)
+    k = np.arange(1, N); h = 1.0 / N
+    one_m_cos = 2 * np.sin(k * np.pi / (2 * N)) ** 2      # 1 - cos θ without cancellation
+    lam = (6 / h ** 2) * one_m_cos / (3 - one_m_cos)
+    assert lo == pytest.approx(lam.min(), rel=1e-12) and hi == pytest.approx(lam.max(), rel=1e-12)
+    for K, g in [(1.0, 1.0), (1.0, 1e4), (1e-2, 1e2)]:
+        fit = rafit.fit_ra(K, g, lo, hi, m)
+        assert np.all(fit.poles < 0) and fit.m == m
+        err = ra.ra_rel_error(fit.c0, fit.poles, fit.residues, K, g, lam)
+        assert err <= bound
+        assert err <= 1.01 * fit.rel_err + 1e-15 * fit.cancel
+        # dropping a pole must make it worse (SPEC.md verify_ra)
+        worse = ra.ra_rel_error(fit.c0, fit.poles[1:], fit.residues[1:], K, g, lam)
+        assert worse > 10 * err
+
+
+def test_ra_preconditioner_close_to_exact():
+    # ||P_RA b - P_exact b||_M <= ε ||P_exact b||_M in the eigen calculus (1D pair).
+    N = 64
+    A, M = fem.trace_pair(2, N)
+    G = spectral.GEVP(A, M)
+    lo, hi = rafit.interval_1d(N)
+    rng = np.random.default_rng(4)
+    b = rng.uniform(-1, 1, N - 1)
+    for K, g in [(1.0, 1e2), (1e-4, 1e6)]:
+        fit = rafit.fit_ra(K, g, lo, hi, 12)
+        x_ra = ra.apply_ra(A, M, fit.c0, fit.poles, fit.residues, b)
+        x_ex = ra.apply_exact_precond(G, K, g, b)
+        d = x_ra - x_ex
+        assert np.sqrt(d @ M @ d) <= (fit.rel_err + 1e-14 * fit.cancel) * np.sqrt(x_ex @ M @ x_ex) * 1.01
+
+
+# --------------------------------------------------------------------------- PCG
+def test_pcg_exact_preconditioner_one_iteration():
+    # SPEC.md pcg: B = A^-1 converges in 1 iteration.
+    D = problem.DenseProblem(2, 12)
+    S = D.S(1.0, 1e2)
+    b = np.random.default_rng(5).uniform(-1, 1, 11)
+    x, it, rel, hist, conv = pcg.pcg(lambda v: S @ v, lambda v: np.linalg.solve(S, v), b)
+    assert conv and it == 1
+    assert np.allclose(S @ x, b, atol=1e-12)
+
+
+def test_pcg_three_distinct_eigenvalues():
+    # Krylov finite termination: 3 distinct eigenvalues, B = I -> <= 3 iterations.
+    d = np.repeat([1.0, 5.0, 20.0], 7)
+    b = np.random.default_rng(6).uniform(-1, 1, d.size)
+    x, it, rel, hist, conv = pcg.pcg(lambda v: d * v, lambda v: v, b, rtol=1e-12)
+    assert conv and it <= 3
+    assert np.allclose(x, b / d, atol=1e-12)
+
+
+def test_pcg_indefinite_raises():
+    d = np.array([1.0, -2.0, 3.0])
+    with pytest.raises(pcg.NotSPD):
+        pcg.pcg(lambda v: d * v, lambda v: v, np.array([0.0, 1.0, 0.0]))
+
+
+def test_pcg_zero_rhs_and_batch_equals_single():
+    D = problem.DenseProblem(2, 10)
+    S = D.S(1.0, 10.0)
+    rng = np.random.default_rng(7)
+    B = rng.uniform(-1, 1, (9, 4)); B[:, 2] = 0.0
+    P = lambda X: D.apply_P_exact(1.0, 10.0, X) * 1.0 + 0.05 * X
+    X, its, rel, hist = pcg.pcg_batch(lambda X, c: S @ X, lambda X, c: P(X), B)
+    for c in range(4):
+        x, it, r, h, conv = pcg.pcg(lambda v: S @ v, lambda v: P(v[:, None])[:, 0], B[:, c])
+        assert it == its[c]
+        assert np.allclose(x, X[:, c], rtol=1e-12, atol=1e-14)
+    assert its[2] == 0 and np.all(X[:, 2] == 0)
+
+
+def _robust_iters(N, K, g, exact=True, m=16):
+    Mo = problem.ModeProblem2D(N)
+    b = np.random.default_rng(0).uniform(-1, 1, N - 1)
+    if exact:
+        P = lambda v: Mo.apply_P_exact(K, g, v)
+    else:
+        lo, hi = rafit.interval_1d(N)
+        f = rafit.fit_ra(K, g, lo, hi, m)
+        P = lambda v: Mo.apply_P_ra(f.c0, f.poles, f.residues, v)
+    x, it, rel, hist, conv = pcg.pcg(lambda v: Mo.apply_S(K, g, v), P, b)
+    assert conv
+    return it, Mo
+
+
+def test_preconditioned_spectrum_bound_2d():
+    # Closed-form robustness bound (SURVEY §8c PCG iii): S and S_Γ are simultaneously
+    # diagonal in the sine basis; the preconditioned eigenvalues are convex combinations
+    # of 1 and the DtN/L^½ ratio s_b/(μ_b λ_b^½) ∈ [1, √6].
+    for N in (32, 1024):
+        Mo = problem.ModeProblem2D(N)
+        ratio = Mo.s / (Mo.mu * np.sqrt(Mo.lam))
+        assert ratio.min() > 0.99 and ratio.max() < np.sqrt(6.0)
+        for K, g in [(1.0, 1.0), (1e-6, 1e6), (1.0, 1e6)]:
+            ev = (K * Mo.s + g * Mo.f) / (Mo.mu * (K * Mo.lam ** 0.5 + g * Mo.lam ** -0.5))
+            assert ev.min() > 0.99 and ev.max() < np.sqrt(6.0)
+
+
+def test_pcg_iterations_bounded_mesh_independent():
+    # PAPER.md:235-236 "PCG convergence is in general bounded in mesh size ... and the
+    # perturbation strength"; κ <= √6 gives k <= 16 by 2ρ^k√κ <= 1e-10 (allow 17).
+    for K, g in [(1.0, 1.0), (1.0, 1e2), (1.0, 1e4), (1.0, 1e6), (1e-6, 1e6)]:
+        its = [_robust_iters(N, K, g)[0] for N in (32, 256, 1024, 4096)]
+        assert max(its) <= 17
+        # mesh independence once h^-2 >> γ/K resolves both terms (coarse meshes where the
+        # γ term dominates the whole spectrum converge faster, e.g. 5/12/15/16 for γ=1e6)
+        assert abs(its[-1] - its[-2]) <= 1, (K, g, its)
+
+
+def test_pcg_ra_matches_exact_iterations():
+    # PAPER.md:236-238 "iteration counts with RA realization ... practically match the exact inverse".
+    for K, g in [(1.0, 1.0), (1.0, 1e4), (1e-4, 1e6)]:
+        a = _robust_iters(1024, K, g, exact=True)[0]
+        b = _robust_iters(1024, K, g, exact=False, m=16)[0]
+        assert abs(a - b) <= 1
