@@ -1,0 +1,165 @@
+/*
+ * dd_api.h — C ABI of libdd: B200-native (sm_100a) Schur-complement PCG for operators
+ * with fractional interface perturbations (M. Kuchta, arXiv 2211.15308).
+ *
+ * The system (Eq.(2)):   -K Δ_Ω x + μ^-1 (-Δ_Γ)^{-1/2} x = b,
+ * discretised by P1 elements on Ω = (0,1)^d with Γ = {x = 0},
+ * homogeneous Dirichlet on ∂Ω\Γ and ∂Γ.  After the split V = V0 ⊕ VΓ (PAPER.md:104-122,
+ * Eq.(4)) the library solves the interface (Steklov–Poincaré / Schur) system
+ *
+ *     S x = b,   S = K (A^ii - A^i0 (A^00)^-1 A^0i) + γ F,   γ = μ^-1,
+ *     F = L_h^{-1/2} = (M U) Λ^{-1/2} (M U)^T          (Eq.(7))
+ *
+ * by PCG from x0 = 0 preconditioned with the rational approximation
+ *
+ *     P = c0 M_Γ^-1 + Σ_k c_k (A_Γ - p_k M_Γ)^-1       (Eq.(8))
+ *
+ * of S_Γ^-1 = (K L^{1/2} + γ L^{-1/2})^-1 (Eq.(6)).
+ * Pole sign convention (reading A7): `poles` are the scalar poles p_k < 0 of
+ * r(λ) = c0 + Σ c_k/(λ - p_k); the library forms A_Γ - p_k M_Γ = A_Γ + |p_k| M_Γ.
+ *
+ * Layout: every vector argument is n_Γ x ncols, column-major (each column = one right-hand
+ * side, contiguous, leading dimension n_Γ), fp64.  Interface ordering is lexicographic:
+ * 2D node (0, j h) -> j-1;  3D node (0, j h, k h) -> (j-1)(N-1) + (k-1).
+ * All vector pointers of the dd_apply_* / dd_pcg_solve calls are DEVICE pointers on the
+ * handle's device; dd_pcg_solve_host takes HOST pointers and stages them itself.
+ *
+ * Ownership: the caller owns every vector buffer; the handle owns the operator data
+ * (sine matrix, F, Schur weights, pole tables), all workspaces (sized by max_cols at
+ * setup; apply/solve never allocate) and, when distributed, the NCCL communicator.
+ * Streams: apply calls are asynchronous on the handle's stream; dd_pcg_solve synchronises
+ * that stream once at the end to fill its host outputs.
+ * Thread safety: a handle is not thread-safe; distinct handles are independent.
+ * Errors: return codes only; nothing crosses the ABI as an exception.  On DD_EINVAL no
+ * output is written.  dd_last_error() returns a thread-local description of the last
+ * failure.
+ */
+#ifndef DD_API_H
+#define DD_API_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DD_OK = 0,
+    DD_EINVAL = 1,      /* invalid argument (nothing written)                              */
+    DD_ECUDA = 2,       /* CUDA runtime error                                              */
+    DD_ENOMEM = 3,      /* device allocation failed                                        */
+    DD_ENOTSPD = 4,     /* p.Sp <= 0 or r.Pr < 0 met in PCG ("indefiniteness") */
+    DD_ENOCONV = 5,     /* non-fatal: some column hit maxit; outputs are the last iterate  */
+    DD_ENCCL = 6,       /* NCCL error (distributed handles)                                */
+    DD_EUNSUPPORTED = 7 /* valid request this build does not implement                     */
+} dd_status;
+
+typedef struct {
+    int dim;            /* 2: unit square, Γ = edge {x=0};  3: unit cube, Γ = face {x=0}     */
+    int cells_per_side; /* N >= 2; mesh size h = 1/N; n = N-1 interior nodes per axis      */
+    int gamma_face;     /* 0: {x = 0} (only value supported)                               */
+} dd_mesh;
+
+typedef struct {
+    int rank, world;              /* this process's rank / number of ranks                 */
+    const void* nccl_unique_id;   /* 128-byte ncclUniqueId (broadcast by the caller)         */
+    int mode;                     /* DD_SHARD_COLUMNS or DD_SHARD_POLES                      */
+} dd_dist;
+#define DD_SHARD_COLUMNS 0        /* each rank passes its own columns; no collective        */
+#define DD_SHARD_POLES 1          /* RA poles split across ranks + allreduce of the sum     */
+
+typedef struct dd_ctx dd_ctx;
+
+/*
+ * dd_setup — build a handle for one mesh and n_param parameter sets.
+ *   K[n_param], mu_inv[n_param]   host; K > 0, mu_inv >= 0   (γ = mu_inv)
+ *   poles, residues               host [n_param * n_poles]; parameter set j uses entries
+ *                                 j*n_poles .. j*n_poles+n_poles-1; every pole < 0 and finite;
+ *                                 a zero residue disables that pole (no solve is issued)
+ *   c0                            host [n_param]: coefficient of M_Γ^-1 in Eq.(8)
+ *   max_cols                      largest ncols any later call may pass (workspace size)
+ *   device, cuda_stream           CUDA device ordinal and cudaStream_t (NULL = legacy)
+ *   dist                          NULL for a single GPU
+ * The RA fit itself is not part of the library (PAPER.md:196-198 defers it to the
+ * references); the Python package provides one (rafit.py).
+ * Returns DD_EINVAL for dim not in {2,3}, N < 2, gamma_face != 0, K <= 0, mu_inv < 0,
+ * a pole >= 0 or not finite, n_param < 1, n_poles < 0, max_cols < 1.
+ */
+dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K, const double* mu_inv,
+                   int n_poles, const double* poles, const double* residues, const double* c0,
+                   int max_cols, int device, void* cuda_stream, const dd_dist* dist,
+                   dd_ctx** out);
+
+/* n_Γ = N-1 (2D) or (N-1)^2 (3D); -1 for a NULL handle. */
+int dd_interface_size(const dd_ctx* ctx);
+
+/*
+ * dd_apply_schur — y = S x per column:
+ *   y_c = K_c (A^ii - A^i0 (A^00)^-1 A^0i) x_c + γ_c F x_c,  (K_c, γ_c) = set col_param[c].
+ * The interior solve (A^00)^-1 is exact (fast diagonalisation; "exactly").
+ *   col_param  DEVICE int[ncols], each in [0, n_param)
+ *   x, y       DEVICE n_Γ x ncols column-major; x and y must not overlap.
+ * 0 <= ncols <= max_cols (ncols = 0 is a no-op).
+ */
+dd_status dd_apply_schur(dd_ctx* ctx, int ncols, const int* col_param, const double* x, double* y);
+
+/*
+ * dd_apply_precond — z = P r per column with the column's RA (Eq.(8)),
+ * shifted solves summed in the fixed order: M term, then poles in the given order.
+ */
+dd_status dd_apply_precond(dd_ctx* ctx, int ncols, const int* col_param, const double* r, double* z);
+
+/*
+ * dd_pcg_solve — x = S^-1 b per column by PCG from x0 = 0, stopping a
+ * column when its preconditioned residual norm η_k <= rtol * η_0, where
+ *   norm_kind 0: η = sqrt(r.Pr) (default)     1: η = ||Pr||_2.
+ * Columns freeze individually on convergence (x, r untouched afterwards).
+ *   b, x       DEVICE n_Γ x ncols (b may equal x? no: must not overlap)
+ *   iters      HOST int[ncols]: S applications until convergence (or maxit)
+ *   rel_res    HOST double[ncols]: final η / η0
+ *   hist       HOST double[maxit+1] or NULL: η history of column 0 (η0 first); entries
+ *              after column 0 converged are left untouched
+ * Returns DD_ENOCONV if any column reached maxit (outputs valid), DD_ENOTSPD on p.Sp <= 0
+ * or r.Pr < 0 (outputs are the iterate at that point).
+ */
+dd_status dd_pcg_solve(dd_ctx* ctx, int ncols, const int* col_param, const double* b, double* x,
+                       double rtol, int maxit, int norm_kind, int* iters, double* rel_res,
+                       double* hist);
+
+/* As dd_pcg_solve but b, x and col_param are HOST pointers: the call copies b and
+ * col_param host->device, solves, and copies x device->host (synchronous). */
+dd_status dd_pcg_solve_host(dd_ctx* ctx, int ncols, const int* col_param_host,
+                            const double* b_host, double* x_host, double rtol, int maxit,
+                            int norm_kind, int* iters, double* rel_res, double* hist);
+
+dd_status dd_destroy(dd_ctx* ctx);
+const char* dd_last_error(void);
+
+/* ---------------------------------------------------------------- instrumentation
+ * Per-kernel-class device time (CUDA events on the handle's stream, recorded around each
+ * launch while enabled; graphs are bypassed while enabled).  Classes: */
+#define DD_KCLASS_GEMM_DST 0      /* K1: T = S_dst X with the Schur-weight epilogue        */
+#define DD_KCLASS_GEMM_SCHUR 1    /* K2: Y = [S_dst | F] [T ; γX]                           */
+#define DD_KCLASS_POLESUM 2       /* K3 (+K4): fused PCG update + pole sum + dots           */
+#define DD_KCLASS_OTHER 3         /* init / copies / allreduce                              */
+#define DD_NKCLASS 4
+dd_status dd_profile_enable(dd_ctx* ctx, int on);
+/* ms[DD_NKCLASS] total milliseconds, launches[DD_NKCLASS]; resets the counters. */
+dd_status dd_profile_read(dd_ctx* ctx, double* ms, long long* launches);
+/* Number of this library's kernel launches since the last call (resets). */
+long long dd_launch_count(dd_ctx* ctx);
+/* Launch configuration actually used (for reports): splitk of the two GEMMs, pole-sum
+ * warps per CTA, whether the CUDA-graph WHILE loop is used. */
+dd_status dd_query_config(const dd_ctx* ctx, int* splitk_dst, int* splitk_schur, int* ps_warps,
+                          int* uses_graph);
+
+/* ---------------------------------------------------------------- test hooks
+ * C = A B in fp64 with the library's DMMA GEMM: A row-major M x K (lda), B column-major
+ * K x N (ldb), C column-major M x N (ldc); device pointers; K % 16 == 0, lda % 2 == 0,
+ * ldb % 2 == 0 and 16-byte aligned A/B; rows of A up to round_up(M, 64) and columns of B
+ * up to round_up(N, 64) must be readable.  Used by the parity tests only. */
+dd_status dd_test_dgemm(int M, int N, int K, const double* A, int lda, const double* B, int ldb,
+                        double* C, int ldc, int splitk, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DD_API_H */

@@ -1,0 +1,745 @@
+// libdd C ABI: setup, validation, the Schur/preconditioner applies and the PCG driver.
+// See include/dd_api.h for the contract and DESIGN.md for the design.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "dd_internal.h"
+
+using namespace dd;
+
+namespace {
+thread_local std::string g_last_error;
+
+dd_status fail(dd_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+#define CK(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t _e = (expr);                                                                  \
+        if (_e != cudaSuccess)                                                                    \
+            return fail(_e == cudaErrorMemoryAllocation ? DD_ENOMEM : DD_ECUDA,                  \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                      \
+    } while (0)
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+struct EvPair {
+    cudaEvent_t a, b;
+    int cls;
+};
+
+struct GraphKey {
+    int ncols;
+    const int* colp;
+    const double* x;
+    double rtol;
+    int maxit, norm_kind;
+    bool operator<(const GraphKey& o) const {
+        return std::tie(ncols, colp, x, rtol, maxit, norm_kind) <
+               std::tie(o.ncols, o.colp, o.x, o.rtol, o.maxit, o.norm_kind);
+    }
+};
+}  // namespace
+
+struct dd_ctx {
+    int dim = 2, N = 0, n = 0, ng = 0, Kpad = 0, ldv = 0, lda = 0, Mpad = 0;
+    int n_param = 0, n_poles = 0, max_cols = 0, cols_pad = 0, device = 0, num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::vector<void*> allocs;
+    // operator data
+    double* W = nullptr;      // Mpad x 2 Kpad row-major: [S_dst | 0 | F | 0]
+    double* sw = nullptr;     // Schur weights s_b
+    double* Kp = nullptr;     // [n_param]
+    double* gp = nullptr;     // [n_param]
+    PoleGeom geom{};
+    PoleTabs tabs{};
+    // workspaces
+    double *xw = nullptr, *Z = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
+    double *bst = nullptr, *xst = nullptr;   // host-API staging (ld = n)
+    int* colp_st = nullptr;
+    double* gws = nullptr;
+    int* gcnt = nullptr;
+    // PCG scalars
+    double *rho = nullptr, *eta0 = nullptr, *relres = nullptr, *hist = nullptr;
+    int *active = nullptr, *iters = nullptr, *ints = nullptr;   // ints: kiter, n_active, n_active_next, done, status, flag
+    int hist_cap = 0;
+    // pinned host mirrors
+    int* h_ints = nullptr;
+    // profiling
+    bool prof = false;
+    std::vector<EvPair> ev_pending, ev_free;
+    double prof_ms[DD_NKCLASS] = {0, 0, 0, 0};
+    long long prof_n[DD_NKCLASS] = {0, 0, 0, 0};
+    long long launches = 0;
+    // graphs
+    bool graph_ok = true;
+    std::map<GraphKey, cudaGraphExec_t> graphs;
+    int last_split1 = 0, last_split2 = 0, last_ps_warps = 0, last_graph = 0;
+};
+
+// ------------------------------------------------------------------------------------ helpers
+template <typename T>
+static cudaError_t dalloc(dd_ctx* c, T** p, size_t count) {
+    void* v = nullptr;
+    cudaError_t e = cudaMalloc(&v, count * sizeof(T) + 256);
+    if (e != cudaSuccess) return e;
+    c->allocs.push_back(v);
+    e = cudaMemsetAsync(v, 0, count * sizeof(T) + 256, c->stream);
+    *p = reinterpret_cast<T*>(v);
+    return e;
+}
+
+static dd_status prof_begin(dd_ctx* c, EvPair& ev, int cls) {
+    if (!c->prof) return DD_OK;
+    if (c->ev_free.empty()) {
+        EvPair e{};
+        CK(cudaEventCreate(&e.a));
+        CK(cudaEventCreate(&e.b));
+        c->ev_free.push_back(e);
+    }
+    ev = c->ev_free.back();
+    c->ev_free.pop_back();
+    ev.cls = cls;
+    CK(cudaEventRecord(ev.a, c->stream));
+    return DD_OK;
+}
+static dd_status prof_end(dd_ctx* c, EvPair& ev) {
+    if (!c->prof) return DD_OK;
+    CK(cudaEventRecord(ev.b, c->stream));
+    c->ev_pending.push_back(ev);
+    if (c->ev_pending.size() > 2048) {   // drain to bound the event pool
+        CK(cudaEventSynchronize(c->ev_pending.back().b));
+        for (auto& e : c->ev_pending) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e.a, e.b));
+            c->prof_ms[e.cls] += ms;
+            c->prof_n[e.cls] += 1;
+            c->ev_free.push_back(e);
+        }
+        c->ev_pending.clear();
+    }
+    return DD_OK;
+}
+
+#define TIMED(cls, call)                                         \
+    do {                                                         \
+        EvPair _ev{};                                            \
+        dd_status _s = prof_begin(c, _ev, cls);                  \
+        if (_s != DD_OK) return _s;                              \
+        CK(call);                                                \
+        c->launches++;                                           \
+        _s = prof_end(c, _ev);                                   \
+        if (_s != DD_OK) return _s;                              \
+    } while (0)
+
+// ------------------------------------------------------------------------------------ tables
+// Pole-sum tables for one symmetric Toeplitz tridiagonal system (d, e), computed in long
+// double (x87 80-bit) so that the conditioning-sensitive parts (pivots, u, PCR multipliers)
+// carry ~1e-19 relative error; the per-RHS sweeps then run in fp64 on the GPU.
+struct SysTables {
+    std::vector<double> invb, cpr, uf, up, pa, pb, pinvb;
+};
+
+static SysTables build_sys_tables(long double d, long double e, const PoleGeom& g) {
+    const int L = g.L, m = L - 1;
+    SysTables t;
+    t.invb.assign(L, 0.0); t.cpr.assign(L, 0.0); t.uf.assign(L, 0.0); t.up.assign(L, 0.0);
+    t.pa.assign(160, 0.0); t.pb.assign(160, 0.0); t.pinvb.assign(32, 0.0);
+    std::vector<long double> bp(L > 0 ? L : 1, 0.0L), ib(L > 0 ? L : 1, 0.0L);
+    for (int i = 0; i < m; i++) {
+        bp[i] = (i == 0) ? d : d - e * e / bp[i - 1];
+        ib[i] = 1.0L / bp[i];
+        t.invb[i] = (double)ib[i];
+        t.cpr[i] = (double)(e * ib[i]);
+    }
+    auto u_of = [&](int Lr) {
+        std::vector<long double> u(L > 0 ? L : 1, 0.0L), yt(Lr > 0 ? Lr : 1, 0.0L);
+        if (Lr == 0) return u;
+        yt[0] = ib[0];
+        for (int i = 1; i < Lr; i++) yt[i] = -e * yt[i - 1] * ib[i];
+        u[Lr - 1] = yt[Lr - 1];
+        for (int i = Lr - 2; i >= 0; i--) u[i] = yt[i] - e * ib[i] * u[i + 1];
+        return u;
+    };
+    const std::vector<long double> uf = u_of(m), up = u_of(g.Lr_part);
+    for (int i = 0; i < L; i++) { t.uf[i] = (double)uf[i]; t.up[i] = (double)up[i]; }
+    auto Lr = [&](int l) { return l < g.part_lane ? m : (l == g.part_lane ? g.Lr_part : 0); };
+    auto sep = [&](int l) { return l < g.part_lane; };
+    auto uu = [&](int l) -> const std::vector<long double>& { return l < g.part_lane ? uf : up; };
+    long double a[32], b[32], c[32];
+    for (int l = 0; l < 32; l++) {
+        a[l] = 0.0L; b[l] = 1.0L; c[l] = 0.0L;
+        if (!sep(l)) continue;
+        a[l] = (l == 0) ? 0.0L : (Lr(l) >= 1 ? -e * e * uu(l)[Lr(l) - 1] : e);
+        b[l] = d - (Lr(l) >= 1 ? e * e * uu(l)[0] : 0.0L) - ((l < 31 && Lr(l + 1) >= 1) ? e * e * uu(l + 1)[0] : 0.0L);
+        if (l < 31) c[l] = Lr(l + 1) >= 1 ? -e * e * uu(l + 1)[Lr(l + 1) - 1] : (sep(l + 1) ? e : 0.0L);
+    }
+    for (int j = 0; j < 5; j++) {
+        const int s = 1 << j;
+        long double na[32], nb[32], nc[32];
+        for (int i = 0; i < 32; i++) {
+            const long double al = (i - s >= 0) ? a[i] / b[i - s] : 0.0L;
+            const long double be = (i + s < 32) ? c[i] / b[i + s] : 0.0L;
+            t.pa[j * 32 + i] = (double)al;
+            t.pb[j * 32 + i] = (double)be;
+            na[i] = (i - s >= 0) ? -al * a[i - s] : 0.0L;
+            nc[i] = (i + s < 32) ? -be * c[i + s] : 0.0L;
+            nb[i] = b[i] - ((i - s >= 0) ? al * c[i - s] : 0.0L) - ((i + s < 32) ? be * a[i + s] : 0.0L);
+        }
+        for (int i = 0; i < 32; i++) { a[i] = na[i]; b[i] = nb[i]; c[i] = nc[i]; }
+    }
+    for (int i = 0; i < 32; i++) t.pinvb[i] = (double)(1.0L / b[i]);
+    return t;
+}
+
+// ------------------------------------------------------------------------------------ setup
+static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, const double* poles,
+                          const double* residues, const double* c0) {
+    const int N = c->N, n = c->n;
+    const long double h = 1.0L / N;
+    const long double PI = 3.141592653589793238462643383279502884L;
+    c->Kpad = round_up(n, GEMM_BK);
+    c->ldv = c->Kpad;
+    c->lda = 2 * c->Kpad;
+    c->Mpad = round_up(n, GEMM_BM);
+    c->cols_pad = round_up(c->max_cols, GEMM_BN);
+
+    // --- sine matrix S_dst[j,k] = sqrt(2/N) sin(jkπ/N) with integer argument reduction (A18)
+    std::vector<long double> sintab(2 * N);
+    for (int a = 0; a < 2 * N; a++) sintab[a] = sinl(PI * (long double)a / (long double)N);
+    const long double sc = sqrtl(2.0L / N);
+    std::vector<double> Wh((size_t)c->Mpad * c->lda, 0.0);
+    for (int j = 1; j <= n; j++)
+        for (int k = 1; k <= n; k++)
+            Wh[(size_t)(j - 1) * c->lda + (k - 1)] = (double)(sc * sintab[((long long)j * k) % (2 * N)]);
+
+    // --- mode quantities: σ_b = 4 sin^2(θ_b/2), θ_b = bπ/N
+    std::vector<long double> sig(n);
+    for (int b = 1; b <= n; b++) {
+        const long double sh = sinl(PI * b / (2.0L * N));
+        sig[b - 1] = 4.0L * sh * sh;
+    }
+    // Schur weights: s_b = (2 - cos θ_b) - Σ_a S[1,a]^2 / (σ_a + σ_b)
+    std::vector<double> swh(n);
+    for (int b = 0; b < n; b++) {
+        long double g = 0.0L;
+        for (int a = 0; a < n; a++) {
+            const long double s1 = sintab[(a + 1) % (2 * N)];
+            g += (2.0L / N) * s1 * s1 / (sig[a] + sig[b]);
+        }
+        swh[b] = (double)((1.0L + 0.5L * sig[b]) - g);
+    }
+    // F = S diag(μ_b λ_b^{-1/2}) S  (Eq.(7) in closed form for the 1D pair, t = -1/2):
+    // μ_b = (h/6)(6 - σ_b),  λ_b = 6 σ_b / (h^2 (6 - σ_b))
+    std::vector<double> Bh((size_t)c->Kpad * round_up(n, GEMM_BN), 0.0);
+    for (int k = 0; k < n; k++) {
+        const long double mu = h / 6.0L * (6.0L - sig[k]);
+        const long double lam = 6.0L * sig[k] / (h * h * (6.0L - sig[k]));
+        const long double f = mu / sqrtl(lam);
+        for (int j = 0; j < n; j++) Bh[(size_t)j * c->Kpad + k] = (double)(f * (long double)Wh[(size_t)k * c->lda + j]);
+    }
+    CK(dalloc(c, &c->W, (size_t)c->Mpad * c->lda));
+    CK(cudaMemcpyAsync(c->W, Wh.data(), Wh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    double* Bd = nullptr;
+    CK(cudaMalloc(&Bd, Bh.size() * sizeof(double)));
+    CK(cudaMemcpyAsync(Bd, Bh.data(), Bh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    {
+        // one-off setup GEMM F = S_dst · (diag(f) S_dst), written into W's right half
+        const int sk = gemm_pick_splitk(n, n, c->Kpad, c->num_sms);
+        double* ws = nullptr; int* cnt = nullptr;
+        const size_t wsz = gemm_ws_doubles(n, n, sk);
+        if (wsz) CK(cudaMalloc(&ws, wsz * sizeof(double)));
+        CK(cudaMalloc(&cnt, sizeof(int) * (gemm_tiles(n, n) + 1)));
+        CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (gemm_tiles(n, n) + 1), c->stream));
+        GemmArgs ga{};
+        ga.M = n; ga.N = n; ga.K = c->Kpad;
+        ga.A = c->W; ga.lda = c->lda;
+        ga.B = Bd; ga.ldb = c->Kpad;
+        ga.C = c->W + c->Kpad; ga.ldc = c->lda;
+        ga.splitk = sk; ga.ws = ws; ga.counters = cnt; ga.epi = EPI_STORE;
+        CK(launch_dgemm(ga, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (ws) cudaFree(ws);
+        cudaFree(cnt);
+    }
+    cudaFree(Bd);
+    CK(dalloc(c, &c->sw, n));
+    CK(cudaMemcpyAsync(c->sw, swh.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+
+    // --- pole tables: systems [M term if c0 != 0] + [poles with non-zero residue]
+    PoleGeom& g = c->geom;
+    g.n = n;
+    g.L = (n + 1 + 31) / 32;
+    g.part_lane = n / g.L;
+    g.Lr_part = n - g.part_lane * g.L;
+    const int L = g.L;
+    const int max_sys = c->n_poles + 1;
+    std::vector<int> nsys(c->n_param, 0);
+    std::vector<double> w((size_t)c->n_param * max_sys, 0.0), dd((size_t)c->n_param * max_sys, 1.0),
+        ee((size_t)c->n_param * max_sys, 0.0), invb((size_t)c->n_param * max_sys * L, 0.0),
+        cpr(invb.size(), 0.0), uf(invb.size(), 0.0), up(invb.size(), 0.0),
+        pa((size_t)c->n_param * max_sys * 160, 0.0), pb(pa.size(), 0.0), pinvb((size_t)c->n_param * max_sys * 32, 0.0);
+    for (int pi = 0; pi < c->n_param; pi++) {
+        std::vector<std::tuple<double, long double, long double>> sys;   // (weight, d, e)
+        if (c0[pi] != 0.0) sys.emplace_back(c0[pi], 4.0L * h / 6.0L, h / 6.0L);
+        for (int k = 0; k < c->n_poles; k++) {
+            const double pk = poles[(size_t)pi * c->n_poles + k], ck = residues[(size_t)pi * c->n_poles + k];
+            if (ck == 0.0) continue;
+            const long double P = pk;
+            sys.emplace_back(ck, 2.0L / h - P * 4.0L * h / 6.0L, -1.0L / h - P * h / 6.0L);
+        }
+        nsys[pi] = (int)sys.size();
+        for (size_t s = 0; s < sys.size(); s++) {
+            const size_t ps = (size_t)pi * max_sys + s;
+            w[ps] = std::get<0>(sys[s]);
+            dd[ps] = (double)std::get<1>(sys[s]);
+            ee[ps] = (double)std::get<2>(sys[s]);
+            SysTables t = build_sys_tables(std::get<1>(sys[s]), std::get<2>(sys[s]), g);
+            std::memcpy(&invb[ps * L], t.invb.data(), L * sizeof(double));
+            std::memcpy(&cpr[ps * L], t.cpr.data(), L * sizeof(double));
+            std::memcpy(&uf[ps * L], t.uf.data(), L * sizeof(double));
+            std::memcpy(&up[ps * L], t.up.data(), L * sizeof(double));
+            std::memcpy(&pa[ps * 160], t.pa.data(), 160 * sizeof(double));
+            std::memcpy(&pb[ps * 160], t.pb.data(), 160 * sizeof(double));
+            std::memcpy(&pinvb[ps * 32], t.pinvb.data(), 32 * sizeof(double));
+        }
+    }
+    auto up_d = [&](const std::vector<double>& v, const double** dst) -> dd_status {
+        double* d = nullptr;
+        CK(dalloc(c, &d, v.size()));
+        CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        *dst = d;
+        return DD_OK;
+    };
+    int* nsys_d = nullptr;
+    CK(dalloc(c, &nsys_d, nsys.size()));
+    CK(cudaMemcpyAsync(nsys_d, nsys.data(), nsys.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    PoleTabs& T = c->tabs;
+    T.max_sys = max_sys;
+    T.n_param = c->n_param;
+    T.nsys = nsys_d;
+    dd_status st;
+    if ((st = up_d(w, &T.w)) || (st = up_d(dd, &T.d)) || (st = up_d(ee, &T.e)) || (st = up_d(invb, &T.invb)) ||
+        (st = up_d(cpr, &T.cpr)) || (st = up_d(uf, &T.ufull)) || (st = up_d(up, &T.upart)) || (st = up_d(pa, &T.pa)) ||
+        (st = up_d(pb, &T.pb)) || (st = up_d(pinvb, &T.pinvb)))
+        return st;
+
+    // --- per-parameter K, γ
+    CK(dalloc(c, &c->Kp, c->n_param));
+    CK(dalloc(c, &c->gp, c->n_param));
+    CK(cudaMemcpyAsync(c->Kp, K, c->n_param * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->gp, mu_inv, c->n_param * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+
+    // --- workspaces
+    const size_t vec = (size_t)c->ldv * c->cols_pad;
+    CK(dalloc(c, &c->xw, vec));
+    CK(dalloc(c, &c->Z, 2 * vec));
+    CK(dalloc(c, &c->r, vec));
+    CK(dalloc(c, &c->p, vec));
+    CK(dalloc(c, &c->q, vec));
+    CK(dalloc(c, &c->bst, (size_t)n * c->max_cols));
+    CK(dalloc(c, &c->xst, (size_t)n * c->max_cols));
+    CK(dalloc(c, &c->colp_st, c->max_cols));
+    size_t wsmax = 0;
+    int cntmax = 0;
+    for (int nc = 1; nc <= c->max_cols; nc = (nc < GEMM_BN ? nc + 1 : nc + GEMM_BN)) {
+        const int ncl = nc > c->max_cols ? c->max_cols : nc;
+        const size_t w1 = gemm_ws_doubles(n, ncl, gemm_pick_splitk(n, ncl, c->Kpad, c->num_sms));
+        const size_t w2 = gemm_ws_doubles(n, ncl, gemm_pick_splitk(n, ncl, 2 * c->Kpad, c->num_sms));
+        wsmax = std::max(wsmax, std::max(w1, w2));
+        cntmax = std::max(cntmax, gemm_tiles(n, ncl));
+    }
+    {
+        const size_t w1 = gemm_ws_doubles(n, c->max_cols, gemm_pick_splitk(n, c->max_cols, c->Kpad, c->num_sms));
+        const size_t w2 = gemm_ws_doubles(n, c->max_cols, gemm_pick_splitk(n, c->max_cols, 2 * c->Kpad, c->num_sms));
+        wsmax = std::max(wsmax, std::max(w1, w2));
+        cntmax = std::max(cntmax, gemm_tiles(n, c->max_cols));
+    }
+    if (wsmax) CK(dalloc(c, &c->gws, wsmax));
+    CK(dalloc(c, &c->gcnt, cntmax + 1));
+    return DD_OK;
+}
+
+extern "C" dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K, const double* mu_inv, int n_poles,
+                              const double* poles, const double* residues, const double* c0, int max_cols, int device,
+                              void* cuda_stream, const dd_dist* dist, dd_ctx** out) {
+    if (!out) return fail(DD_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!mesh) return fail(DD_EINVAL, "mesh is NULL");
+    if (mesh->dim != 2 && mesh->dim != 3) return fail(DD_EINVAL, "dim must be 2 or 3");
+    if (mesh->cells_per_side < 2) return fail(DD_EINVAL, "cells_per_side must be >= 2");
+    if (mesh->gamma_face != 0) return fail(DD_EINVAL, "gamma_face must be 0 ({x=0})");
+    if (n_param < 1 || !K || !mu_inv || !c0) return fail(DD_EINVAL, "need n_param >= 1 and K, mu_inv, c0");
+    if (n_poles < 0 || (n_poles > 0 && (!poles || !residues))) return fail(DD_EINVAL, "bad poles/residues");
+    if (max_cols < 1) return fail(DD_EINVAL, "max_cols must be >= 1");
+    for (int i = 0; i < n_param; i++) {
+        if (!(K[i] > 0.0) || !std::isfinite(K[i])) return fail(DD_EINVAL, "K must be > 0 and finite");
+        if (!(mu_inv[i] >= 0.0) || !std::isfinite(mu_inv[i])) return fail(DD_EINVAL, "mu_inv must be >= 0 and finite");
+        if (!std::isfinite(c0[i])) return fail(DD_EINVAL, "c0 must be finite");
+        for (int k = 0; k < n_poles; k++) {
+            const double p = poles[(size_t)i * n_poles + k], r = residues[(size_t)i * n_poles + k];
+            if (!(p < 0.0) || !std::isfinite(p)) return fail(DD_EINVAL, "every pole must be < 0 and finite");
+            if (!std::isfinite(r)) return fail(DD_EINVAL, "residues must be finite");
+        }
+    }
+    if (dist && dist->world > 1) return fail(DD_EUNSUPPORTED, "distributed handles: not in this build yet");
+    if (mesh->dim == 3) return fail(DD_EUNSUPPORTED, "3D interfaces: not in this build yet");
+
+    dd_ctx* c = new dd_ctx();
+    c->dim = mesh->dim;
+    c->N = mesh->cells_per_side;
+    c->n = c->N - 1;
+    c->ng = c->dim == 2 ? c->n : c->n * c->n;
+    c->n_param = n_param;
+    c->n_poles = n_poles;
+    c->max_cols = max_cols;
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    auto bail = [&](dd_status s) {
+        std::string msg = g_last_error;
+        dd_destroy(c);
+        g_last_error = msg;
+        return s;
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DD_ECUDA, "cudaSetDevice failed"));
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    dd_status s = setup_2d(c, K, mu_inv, poles, residues, c0);
+    if (s != DD_OK) return bail(s);
+    c->hist_cap = 4096;
+    if (cudaMalloc(&c->rho, sizeof(double) * (3 * (size_t)max_cols + c->hist_cap + 8)) != cudaSuccess)
+        return bail(fail(DD_ENOMEM, "scalars"));
+    c->allocs.push_back(c->rho);
+    c->eta0 = c->rho + max_cols;
+    c->relres = c->eta0 + max_cols;
+    c->hist = c->relres + max_cols;
+    if (cudaMalloc(&c->active, sizeof(int) * (2 * (size_t)max_cols + 16)) != cudaSuccess)
+        return bail(fail(DD_ENOMEM, "scalars"));
+    c->allocs.push_back(c->active);
+    c->iters = c->active + max_cols;
+    c->ints = c->iters + max_cols;
+    if (cudaMemsetAsync(c->active, 0, sizeof(int) * (2 * (size_t)max_cols + 16), c->stream) != cudaSuccess)
+        return bail(fail(DD_ECUDA, "memset"));
+    if (cudaMallocHost(&c->h_ints, sizeof(int) * 16) != cudaSuccess) return bail(fail(DD_ENOMEM, "pinned"));
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DD_ECUDA, "setup sync"));
+    *out = c;
+    return DD_OK;
+}
+
+extern "C" int dd_interface_size(const dd_ctx* c) { return c ? c->ng : -1; }
+
+// ------------------------------------------------------------------------------------ applies
+static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double* xin, double* y, int ldy) {
+    // T' = (K_c s) ∘ (S_dst X) -> Z[0:n);  γ_c X -> Z[Kpad:Kpad+n);  Y = [S_dst | F] Z
+    const int n = c->n;
+    const int sk1 = gemm_pick_splitk(n, ncols, c->Kpad, c->num_sms);
+    const int sk2 = gemm_pick_splitk(n, ncols, 2 * c->Kpad, c->num_sms);
+    c->last_split1 = sk1;
+    c->last_split2 = sk2;
+    GemmArgs g1{};
+    g1.M = n; g1.N = ncols; g1.K = c->Kpad;
+    g1.A = c->W; g1.lda = c->lda;
+    g1.B = xin; g1.ldb = c->ldv;
+    g1.C = c->Z; g1.ldc = 2 * c->Kpad;
+    g1.splitk = sk1; g1.ws = c->gws; g1.counters = c->gcnt;
+    g1.epi = EPI_SCHUR_DST;
+    g1.n_param = c->n_param;
+    g1.col_param = colp; g1.Kp = c->Kp; g1.gp = c->gp; g1.s = c->sw;
+    g1.X = xin; g1.ldx = c->ldv; g1.Zlow = c->Z + c->Kpad;
+    TIMED(DD_KCLASS_GEMM_DST, launch_dgemm(g1, c->stream));
+    GemmArgs g2{};
+    g2.M = n; g2.N = ncols; g2.K = 2 * c->Kpad;
+    g2.A = c->W; g2.lda = c->lda;
+    g2.B = c->Z; g2.ldb = 2 * c->Kpad;
+    g2.C = y; g2.ldc = ldy;
+    g2.splitk = sk2; g2.ws = c->gws; g2.counters = c->gcnt;
+    g2.epi = EPI_STORE;
+    TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(g2, c->stream));
+    return DD_OK;
+}
+
+static dd_status check_cols(dd_ctx* c, int ncols, const int* colp) {
+    if (!c) return fail(DD_EINVAL, "NULL handle");
+    if (ncols < 0 || ncols > c->max_cols) return fail(DD_EINVAL, "ncols out of [0, max_cols]");
+    if (ncols > 0 && !colp) return fail(DD_EINVAL, "col_param is NULL");
+    return DD_OK;
+}
+
+extern "C" dd_status dd_apply_schur(dd_ctx* c, int ncols, const int* colp, const double* x, double* y) {
+    dd_status s = check_cols(c, ncols, colp);
+    if (s != DD_OK) return s;
+    if (ncols == 0) return DD_OK;
+    if (!x || !y) return fail(DD_EINVAL, "x/y NULL");
+    CK(cudaSetDevice(c->device));
+    TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
+    TIMED(DD_KCLASS_OTHER, launch_copy_cols(c->n, ncols, x, c->n, c->xw, c->ldv, c->stream));
+    return schur_gemms(c, ncols, colp, c->xw, y, c->n);
+}
+
+extern "C" dd_status dd_apply_precond(dd_ctx* c, int ncols, const int* colp, const double* r, double* z) {
+    dd_status s = check_cols(c, ncols, colp);
+    if (s != DD_OK) return s;
+    if (ncols == 0) return DD_OK;
+    if (!r || !z) return fail(DD_EINVAL, "r/z NULL");
+    CK(cudaSetDevice(c->device));
+    c->last_ps_warps = polesum_warps(c->geom.L);
+    TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
+    TIMED(DD_KCLASS_POLESUM, launch_precond(ncols, colp, c->geom, c->tabs, r, c->n, z, c->n, c->stream));
+    return DD_OK;
+}
+
+// ------------------------------------------------------------------------------------ PCG
+static PcgState make_state(dd_ctx* c, int ncols, const int* colp, double* x, double rtol, int maxit, int norm_kind) {
+    PcgState s{};
+    s.n = c->n; s.ldv = c->ldv; s.ncols = ncols; s.col_param = colp;
+    s.x = x; s.ldx = c->n;
+    s.r = c->r; s.p = c->p; s.q = c->q;
+    s.rho = c->rho; s.eta0 = c->eta0; s.relres = c->relres;
+    s.active = c->active; s.iters = c->iters;
+    s.hist = c->hist;
+    s.kiter = c->ints + 0; s.n_active = c->ints + 1; s.n_active_next = c->ints + 2;
+    s.done_ctas = c->ints + 3; s.status = c->ints + 4;
+    s.rtol = rtol; s.maxit = maxit; s.norm_kind = norm_kind;
+    s.cond_handle = 0;
+    return s;
+}
+
+static dd_status iteration_body(dd_ctx* c, const PcgState& s) {
+    dd_status st = schur_gemms(c, s.ncols, s.col_param, c->p, c->q, c->ldv);
+    if (st != DD_OK) return st;
+    c->last_ps_warps = polesum_warps(c->geom.L);
+    TIMED(DD_KCLASS_POLESUM, launch_pcg_iter(s, c->geom, c->tabs, c->stream));
+    return DD_OK;
+}
+
+static dd_status build_graph(dd_ctx* c, const PcgState& s0, cudaGraphExec_t* out) {
+    cudaGraph_t g = nullptr;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+    if (e != cudaSuccess) { cudaGraphDestroy(g); return fail(DD_ECUDA, "conditional handle"); }
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+    if (e != cudaSuccess) { cudaGraphDestroy(g); return fail(DD_ECUDA, "conditional node"); }
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    PcgState s = s0;
+    s.cond_handle = (unsigned long long)h;
+    cudaStream_t cap = nullptr;
+    CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaStream_t saved = c->stream;
+    c->stream = cap;
+    e = cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) { c->stream = saved; cudaStreamDestroy(cap); cudaGraphDestroy(g); return fail(DD_ECUDA, "capture"); }
+    const bool prof = c->prof;
+    c->prof = false;
+    const long long l0 = c->launches;
+    dd_status st = iteration_body(c, s);
+    c->launches = l0;
+    c->prof = prof;
+    cudaGraph_t captured = nullptr;
+    e = cudaStreamEndCapture(cap, &captured);
+    c->stream = saved;
+    cudaStreamDestroy(cap);
+    if (st != DD_OK || e != cudaSuccess) { cudaGraphDestroy(g); return st != DD_OK ? st : fail(DD_ECUDA, "end capture"); }
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(DD_ECUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+    *out = ex;
+    return DD_OK;
+}
+
+extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol,
+                                  int maxit, int norm_kind, int* iters, double* rel_res, double* hist) {
+    dd_status s = check_cols(c, ncols, colp);
+    if (s != DD_OK) return s;
+    if (ncols > 0 && (!b || !x)) return fail(DD_EINVAL, "b/x NULL");
+    if (!(rtol >= 0.0) || maxit < 0 || (norm_kind != 0 && norm_kind != 1)) return fail(DD_EINVAL, "rtol/maxit/norm_kind");
+    if (ncols == 0) return DD_OK;
+    if (hist && maxit + 1 > c->hist_cap) return fail(DD_EINVAL, "maxit too large for hist (<= 4095)");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemsetAsync(c->ints, 0, sizeof(int) * 8, c->stream));
+    TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
+    PcgState st = make_state(c, ncols, colp, x, rtol, maxit, norm_kind);
+    c->last_ps_warps = polesum_warps(c->geom.L);
+    TIMED(DD_KCLASS_OTHER, launch_pcg_init(st, c->geom, c->tabs, b, c->n, c->stream));
+    c->last_graph = 0;
+    if (maxit > 0) {
+        bool done = false;
+        if (c->graph_ok && !c->prof) {
+            GraphKey key{ncols, colp, x, rtol, maxit, norm_kind};
+            auto it = c->graphs.find(key);
+            cudaGraphExec_t ex = nullptr;
+            if (it != c->graphs.end()) {
+                ex = it->second;
+            } else {
+                dd_status gs = build_graph(c, st, &ex);
+                if (gs == DD_OK) {
+                    if (c->graphs.size() > 32) {
+                        for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+                        c->graphs.clear();
+                    }
+                    c->graphs[key] = ex;
+                } else {
+                    c->graph_ok = false;   // fall back to the host-driven loop
+                    cudaGetLastError();
+                }
+            }
+            if (ex) {
+                CK(cudaGraphLaunch(ex, c->stream));
+                done = true;
+                c->last_graph = 1;
+            }
+        }
+        if (!done) {
+            // host-driven loop: blind batches, then check the active count
+            int k = 0;
+            while (k < maxit) {
+                const int batch = std::min(k == 0 ? 8 : 2, maxit - k);
+                for (int j = 0; j < batch; j++) {
+                    dd_status is = iteration_body(c, st);
+                    if (is != DD_OK) return is;
+                }
+                k += batch;
+                CK(cudaMemcpyAsync(c->h_ints, c->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+                if (c->h_ints[1] == 0 || c->h_ints[4] != 0) break;
+            }
+        }
+    }
+    if (iters) CK(cudaMemcpyAsync(iters, c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c->stream));
+    if (rel_res) CK(cudaMemcpyAsync(rel_res, c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_ints, c->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const int kdone = c->h_ints[0];
+    if (c->last_graph) c->launches += 3LL * kdone;
+    if (hist) {
+        // column 0 history: η_0 .. η_{iters[0]}
+        int it0 = 0;
+        CK(cudaMemcpy(&it0, c->iters, sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hist, c->hist, sizeof(double) * (it0 + 1), cudaMemcpyDeviceToHost));
+    }
+    if (c->h_ints[5]) return fail(DD_EINVAL, "col_param entry out of range (clamped; outputs undefined)");
+    if (c->h_ints[4] == DD_ENOTSPD) return fail(DD_ENOTSPD, "p.Sp <= 0 or r.Pr < 0 in PCG");
+    // any column still active after maxit iterations?
+    std::vector<int> itv(ncols);
+    if (!iters) {
+        CK(cudaMemcpy(itv.data(), c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost));
+        iters = itv.data();
+    }
+    std::vector<double> rr(ncols);
+    CK(cudaMemcpy(rr.data(), c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < ncols; i++)
+        if (iters[i] >= maxit && !(rr[i] <= rtol)) return fail(DD_ENOCONV, "maxit reached");
+    return DD_OK;
+}
+
+extern "C" dd_status dd_pcg_solve_host(dd_ctx* c, int ncols, const int* colp_h, const double* b_h, double* x_h,
+                                       double rtol, int maxit, int norm_kind, int* iters, double* rel_res,
+                                       double* hist) {
+    dd_status s = check_cols(c, ncols, colp_h);
+    if (s != DD_OK) return s;
+    if (ncols == 0) return DD_OK;
+    if (!b_h || !x_h) return fail(DD_EINVAL, "b/x NULL");
+    for (int i = 0; i < ncols; i++)
+        if (colp_h[i] < 0 || colp_h[i] >= c->n_param) return fail(DD_EINVAL, "col_param out of range");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemcpyAsync(c->colp_st, colp_h, sizeof(int) * ncols, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->bst, b_h, sizeof(double) * (size_t)c->n * ncols, cudaMemcpyHostToDevice, c->stream));
+    dd_status r = dd_pcg_solve(c, ncols, c->colp_st, c->bst, c->xst, rtol, maxit, norm_kind, iters, rel_res, hist);
+    if (r != DD_OK && r != DD_ENOCONV && r != DD_ENOTSPD) return r;
+    CK(cudaMemcpyAsync(x_h, c->xst, sizeof(double) * (size_t)c->n * ncols, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return r;
+}
+
+extern "C" dd_status dd_destroy(dd_ctx* c) {
+    if (!c) return DD_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& e : c->ev_pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    for (auto& e : c->ev_free) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    for (void* p : c->allocs) cudaFree(p);
+    if (c->h_ints) cudaFreeHost(c->h_ints);
+    delete c;
+    return DD_OK;
+}
+
+extern "C" const char* dd_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" dd_status dd_profile_enable(dd_ctx* c, int on) {
+    if (!c) return fail(DD_EINVAL, "NULL handle");
+    c->prof = on != 0;
+    return DD_OK;
+}
+
+extern "C" dd_status dd_profile_read(dd_ctx* c, double* ms, long long* launches) {
+    if (!c) return fail(DD_EINVAL, "NULL handle");
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto& e : c->ev_pending) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, e.a, e.b));
+        c->prof_ms[e.cls] += t;
+        c->prof_n[e.cls] += 1;
+        c->ev_free.push_back(e);
+    }
+    c->ev_pending.clear();
+    for (int i = 0; i < DD_NKCLASS; i++) {
+        if (ms) ms[i] = c->prof_ms[i];
+        if (launches) launches[i] = c->prof_n[i];
+        c->prof_ms[i] = 0.0;
+        c->prof_n[i] = 0;
+    }
+    return DD_OK;
+}
+
+extern "C" long long dd_launch_count(dd_ctx* c) {
+    if (!c) return -1;
+    const long long v = c->launches;
+    c->launches = 0;
+    return v;
+}
+
+extern "C" dd_status dd_query_config(const dd_ctx* c, int* s1, int* s2, int* w, int* g) {
+    if (!c) return fail(DD_EINVAL, "NULL handle");
+    if (s1) *s1 = c->last_split1;
+    if (s2) *s2 = c->last_split2;
+    if (w) *w = c->last_ps_warps;
+    if (g) *g = c->last_graph;
+    return DD_OK;
+}
+
+extern "C" dd_status dd_test_dgemm(int M, int N, int K, const double* A, int lda, const double* B, int ldb, double* C,
+                                   int ldc, int splitk, void* stream) {
+    if (M < 0 || N < 0 || K < 0 || K % GEMM_BK || lda % 2 || ldb % 2 || splitk < 1 || splitk > 64)
+        return fail(DD_EINVAL, "bad dgemm args");
+    if (M == 0 || N == 0) return DD_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    double* ws = nullptr; int* cnt = nullptr;
+    const size_t wsz = gemm_ws_doubles(M, N, splitk);
+    if (wsz) CK(cudaMalloc(&ws, wsz * sizeof(double)));
+    CK(cudaMalloc(&cnt, sizeof(int) * (gemm_tiles(M, N) + 1)));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (gemm_tiles(M, N) + 1), st));
+    GemmArgs g{};
+    g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
+    g.splitk = splitk; g.ws = ws; g.counters = cnt; g.epi = EPI_STORE;
+    CK(launch_dgemm(g, st));
+    CK(cudaStreamSynchronize(st));
+    if (ws) cudaFree(ws);
+    cudaFree(cnt);
+    return DD_OK;
+}

@@ -1,0 +1,100 @@
+// Internal declarations shared by the libdd translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/dd_api.h"
+
+namespace dd {
+
+// ----------------------------------------------------------------------------- GEMM
+// FP64 tensor-core GEMM  C = A·B  (A row-major, B column-major, C column-major), DMMA
+// (mma.sync .f64) with a cp.async multi-stage pipeline and optional split-K.
+constexpr int GEMM_BM = 64, GEMM_BN = 64, GEMM_BK = 16, GEMM_STAGES = 4, GEMM_THREADS = 128;
+constexpr int GEMM_LDS = GEMM_BK + 4;   // padded smem row (doubles): conflict-free fragment loads
+constexpr size_t GEMM_SMEM = size_t(GEMM_STAGES) * (GEMM_BM + GEMM_BN) * GEMM_LDS * sizeof(double);
+
+enum EpiKind : int {
+    EPI_STORE = 0,      // C[i,c] = acc
+    EPI_SCHUR_DST = 1,  // C[i,c] = K_c s_i acc   and   Zlow[i,c] = γ_c X[i,c]   (Schur step a-2/a-3)
+};
+
+struct GemmArgs {
+    int M, N, K;                 // K multiple of GEMM_BK
+    const double* A; int lda;    // row-major, rows readable up to round_up(M, BM)
+    const double* B; int ldb;    // column-major, columns readable up to round_up(N, BN)
+    double* C; int ldc;          // column-major
+    int splitk;                  // >= 1
+    double* ws;                  // split-K partials  [tiles * splitk * BM*BN]
+    int* counters;               // [tiles], zero on entry, left zero on exit
+    int epi;
+    int n_param;
+    // EPI_SCHUR_DST
+    const int* col_param; const double* Kp; const double* gp; const double* s;
+    const double* X; int ldx; double* Zlow;
+};
+
+int gemm_tiles(int M, int N);
+int gemm_pick_splitk(int M, int N, int K, int num_sms);
+size_t gemm_ws_doubles(int M, int N, int splitk);
+cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st);
+
+// ----------------------------------------------------------------------------- pole sum
+// 1D Γ: each shifted system (A_Γ - p M_Γ) (and M_Γ) is symmetric Toeplitz tridiagonal
+// (diag d, off-diagonal e).  The n rows (padded to 32 L) are split in 32 chunks of L rows, one
+// per lane: rows 0..L-2 of a chunk are its interior, row L-1 its separator.  Interiors are
+// solved by Thomas with precomputed factors, separators by PCR across the warp (shuffles).
+struct PoleGeom {
+    int n;          // rows (n_Γ)
+    int L;          // chunk length (rows per lane), 32 L >= n + 1
+    int part_lane;  // first lane whose separator row is >= n (padding): floor(n / L)
+    int Lr_part;    // real interior rows of that lane: n - part_lane * L   (0..L-1)
+};
+
+struct PoleTabs {
+    int max_sys;                // systems per parameter set (mass term + poles), padded
+    int n_param;                // parameter sets (col_param is clamped to [0, n_param))
+    const int* nsys;            // [n_param]
+    const double* w;            // [n_param][max_sys]  weight (c0 or c_k)
+    const double* d;            // [n_param][max_sys]  diagonal
+    const double* e;            // [n_param][max_sys]  off-diagonal
+    const double* invb;         // [n_param][max_sys][L]  1 / Thomas pivot
+    const double* cpr;          // [n_param][max_sys][L]  e / Thomas pivot
+    const double* ufull;        // [n_param][max_sys][L]  T_{L-1}^-1 e_1
+    const double* upart;        // [n_param][max_sys][L]  T_{Lr_part}^-1 e_1
+    const double* pa;           // [n_param][max_sys][5][32] PCR multipliers (left)
+    const double* pb;           // [n_param][max_sys][5][32] PCR multipliers (right)
+    const double* pinvb;        // [n_param][max_sys][32]    final 1/b
+};
+
+// PCG state for a batch of columns (device).
+struct PcgState {
+    int n, ldv, ncols;
+    const int* col_param;
+    double* x; int ldx;                // solution (caller's buffer), column stride ldx
+    double *r, *p, *q;                 // n x ncols, column stride ldv
+    double *rho, *eta0, *relres;       // [ncols]
+    int *active, *iters;               // [ncols]
+    double* hist;                      // [maxit+1] column 0
+    int* kiter;                        // iteration counter (device)
+    int* n_active;                     // active columns after the last iteration
+    int* n_active_next;                // scratch counter
+    int* done_ctas;                    // scratch counter
+    int* status;                       // 0 ok, DD_ENOTSPD
+    double rtol; int maxit; int norm_kind;
+    unsigned long long cond_handle;    // cudaGraphConditionalHandle (0 = none)
+};
+
+int polesum_warps(int L);
+size_t polesum_smem(int L, int warps);
+cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b,
+                            int ldb, cudaStream_t st);
+cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st);
+cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, const PoleTabs& t,
+                           const double* r, int ldr, double* z, int ldz, cudaStream_t st);
+cudaError_t launch_copy_cols(int n, int ncols, const double* src, int lds, double* dst, int ldd,
+                             cudaStream_t st);
+cudaError_t launch_check_params(int ncols, const int* col_param, int n_param, int* flag, cudaStream_t st);
+
+}  // namespace dd

@@ -1,0 +1,23 @@
+"""Shared test helpers: RA fits for a parameter list, tolerances.  No method arithmetic."""
+import numpy as np
+
+from paper_2211_15308_b200 import rafit
+
+
+def fit_all(N, params, m):
+    lo, hi = rafit.interval_1d(N)
+    return [rafit.fit_ra(K, g, lo, hi, m) for K, g in params]
+
+
+def rel_l2_cols(a, b):
+    """max over columns of ||a_c - b_c|| / ||b_c||  (arrays shaped (ncols, n))."""
+    a = np.asarray(a); b = np.asarray(b)
+    num = np.linalg.norm(a - b, axis=1)
+    den = np.linalg.norm(b, axis=1)
+    den = np.where(den == 0, 1.0, den)
+    return float(np.max(num / den))
+
+
+def precond_tol(ras):
+    # max(1e-10, 1e-15 κ_c) relative ℓ2 (κ_c = cancellation factor, reading A11)
+    return max(1e-10, 1e-15 * max(r.cancel for r in ras))

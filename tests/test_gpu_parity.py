@@ -1,0 +1,202 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.  Needs a B200: -m gpu.
+
+Tolerances (north star, BASELINE.json): operator applications 1e-10 relative ℓ2 (precond:
+max(1e-10, 1e-15 κ_c), reading A11), solutions 1e-8 relative, iteration counts ±1.
+"""
+import numpy as np
+import pytest
+
+from helpers import fit_all, precond_tol, rel_l2_cols
+from oracle import pcg as opcg
+from oracle import problem as oprob
+from paper_2211_15308_b200 import configs, inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2211_15308_b200 import binding
+    binding.load()
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    return binding
+
+
+def _solver(lib, N, params, ras, max_cols):
+    return lib.Solver(2, N, params, ras, max_cols=max_cols, device=0)
+
+
+def _cols(B):
+    return torch.as_tensor(B, device="cuda")
+
+
+# ------------------------------------------------------------------------- GEMM core
+@pytest.mark.parametrize("M,N,K,sk", [(64, 64, 16, 1), (100, 37, 70, 1), (199, 130, 400, 3), (1023, 256, 2046, 2),
+                                      (300, 5, 1000, 7)])
+def test_dgemm_core(lib, M, N, K, sk):
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K)); B = rng.standard_normal((N, K))
+    C = lib.test_dgemm(torch.as_tensor(A, device="cuda"), torch.as_tensor(B, device="cuda"), splitk=sk).cpu().numpy()
+    ref = (A @ B.T).T
+    assert np.abs(C - ref).max() <= 1e-13 * np.sqrt(K) * np.abs(ref).max()
+
+
+# ------------------------------------------------------------------------- small / ragged parity vs dense oracle
+SMALL = [
+    (8, [(1.0, 1e2)], 8, 3),
+    (33, [(1.0, 1.0), (1e-4, 1e6)], 10, 5),
+    (200, [(1.0, 1e2), (1e-4, 1e6), (1.0, 0.0)], 14, 37),
+]
+
+
+@pytest.fixture(scope="module", params=SMALL, ids=lambda p: f"N{p[0]}")
+def small_case(request, lib):
+    N, params, m, C = request.param
+    ras = fit_all(N, params, m)
+    D = oprob.DenseProblem(2, N)
+    S = _solver(lib, N, params, ras, max_cols=C + 3)
+    rng = np.random.default_rng(N)
+    B = rng.uniform(-1, 1, (C, N - 1))
+    colp = np.arange(C) % len(params)
+    yield N, params, ras, D, S, B, colp
+    S.close()
+
+
+def test_schur_apply_parity_small(small_case):
+    N, params, ras, D, S, B, colp = small_case
+    y = S.apply_schur(_cols(B), colp).cpu().numpy()
+    ref = np.stack([D.apply_S(*params[colp[c]], B[c]) for c in range(B.shape[0])])
+    assert rel_l2_cols(y, ref) <= 1e-10
+
+
+def test_precond_apply_parity_small(small_case):
+    N, params, ras, D, S, B, colp = small_case
+    z = S.apply_precond(_cols(B), colp).cpu().numpy()
+    ref = np.stack([D.apply_P_ra(ras[colp[c]].c0, ras[colp[c]].poles, ras[colp[c]].residues, B[c]) for c in range(B.shape[0])])
+    assert rel_l2_cols(z, ref) <= precond_tol(ras)
+
+
+def test_pcg_parity_small(small_case):
+    N, params, ras, D, S, B, colp = small_case
+    res = S.pcg_solve(_cols(B), colp, rtol=1e-10, maxit=500, want_hist=True)
+    x = res.x.cpu().numpy()
+    for c in range(B.shape[0]):
+        K, g = params[colp[c]]; ra = ras[colp[c]]
+        xo, it, rel, hist, conv = opcg.pcg(lambda v: D.apply_S(K, g, v),
+                                           lambda v: D.apply_P_ra(ra.c0, ra.poles, ra.residues, v), B[c])
+        assert conv
+        assert abs(int(res.iters[c]) - it) <= 1, (c, res.iters[c], it)
+        assert np.linalg.norm(x[c] - xo) <= 1e-8 * np.linalg.norm(xo)
+        if c == 0:
+            assert len(res.hist) == res.iters[0] + 1
+            assert res.hist[0] == pytest.approx(hist[0], rel=1e-12)
+    assert np.all(res.rel_res <= 1e-10)
+
+
+def test_determinism_and_host_api(small_case):
+    N, params, ras, D, S, B, colp = small_case
+    a = S.pcg_solve(_cols(B), colp).x.cpu().numpy()
+    b = S.pcg_solve(_cols(B), colp).x.cpu().numpy()
+    assert np.array_equal(a, b)                         # fixed reduction trees: bitwise
+    h = S.pcg_solve_host(B, colp)
+    assert np.array_equal(h.x, a)
+
+
+def test_batch_columns_match_single(small_case):
+    # A14: columns freeze individually; each column reproduces its single-column run.
+    N, params, ras, D, S, B, colp = small_case
+    full = S.pcg_solve(_cols(B), colp)
+    for c in (0, B.shape[0] - 1):
+        one = S.pcg_solve(_cols(B[c:c + 1]), colp[c:c + 1])
+        assert one.iters[0] == full.iters[c]
+        xf = full.x.cpu().numpy()[c]; xs = one.x.cpu().numpy()[0]
+        assert np.linalg.norm(xf - xs) <= 1e-12 * np.linalg.norm(xs)
+
+
+# ------------------------------------------------------------------------- edge cases
+def test_edge_cases(lib):
+    N = 16; params = [(1.0, 1e2)]; ras = fit_all(N, params, 6)
+    S = _solver(lib, N, params, ras, max_cols=4)
+    try:
+        # ncols = 0 is a no-op
+        e = torch.empty(0, N - 1, dtype=torch.float64, device="cuda")
+        S.apply_schur(e, np.zeros(0, dtype=np.int32)); S.apply_precond(e, np.zeros(0, dtype=np.int32))
+        # zero right-hand side: 0 iterations, x = 0
+        B = np.zeros((2, N - 1)); B[1] = 1.0
+        r = S.pcg_solve(_cols(B), [0, 0])
+        assert r.iters[0] == 0 and np.all(r.x.cpu().numpy()[0] == 0) and r.iters[1] > 0
+        # maxit reached -> DD_ENOCONV (non-fatal, outputs valid)
+        r = S.pcg_solve(_cols(np.ones((1, N - 1))), [0], maxit=2)
+        assert r.status == lib.DD_ENOCONV and r.iters[0] == 2
+        # ncols > max_cols -> DD_EINVAL
+        with pytest.raises(lib.DDError):
+            S.pcg_solve(_cols(np.ones((5, N - 1))), [0] * 5)
+    finally:
+        S.close()
+    # invalid setup arguments
+    class Bad:
+        c0 = 0.0; poles = np.array([0.5]); residues = np.array([1.0])
+    with pytest.raises(lib.DDError):
+        lib.Solver(2, N, params, [Bad()], max_cols=1)
+    with pytest.raises(lib.DDError):
+        lib.Solver(2, N, [(0.0, 1.0)], ras, max_cols=1)
+    with pytest.raises(lib.DDError):
+        lib.Solver(2, 1, params, ras, max_cols=1)
+
+
+def test_profile_and_launch_counts(lib):
+    N = 64; params = [(1.0, 1e2)]; ras = fit_all(N, params, 8)
+    S = _solver(lib, N, params, ras, max_cols=8)
+    try:
+        B = np.random.default_rng(0).uniform(-1, 1, (8, N - 1))
+        S.launch_count()
+        r = S.pcg_solve(_cols(B), [0] * 8)
+        k = int(r.iters.max())
+        assert S.launch_count() == 2 + 3 * k
+        S.profile(True)
+        r2 = S.pcg_solve(_cols(B), [0] * 8)
+        prof = S.profile_read()
+        S.profile(False)
+        assert np.array_equal(r2.x.cpu().numpy(), r.x.cpu().numpy())
+        assert prof["gemm_dst"][1] == k and prof["gemm_schur"][1] == k and prof["polesum_pcg"][1] == k
+        assert all(v[0] > 0 for v in prof.values())
+    finally:
+        S.close()
+
+
+# ------------------------------------------------------------------------- full config sizes
+@pytest.mark.parametrize("cfg", [c for c in configs.CONFIGS if c.dim == 2], ids=lambda c: c.name)
+def test_full_config_parity(lib, cfg):
+    """BASELINE.json configs at full size, in the launch configuration bench.py times, against
+    the oracle's mode tier (pinned to dense elimination in test_oracle_pins)."""
+    ras = fit_all(cfg.N, cfg.params, cfg.n_poles)
+    B, colp = inputs.batch(cfg.n_gamma, len(cfg.params), cfg.rhs_per_param)
+    Mo = oprob.ModeProblem2D(cfg.N)
+    S = _solver(lib, cfg.N, cfg.params, ras, max_cols=cfg.n_cols)
+    try:
+        Bt = _cols(B)
+        # operator and preconditioner applications on every column
+        y = S.apply_schur(Bt, colp).cpu().numpy()
+        z = S.apply_precond(Bt, colp).cpu().numpy()
+        ref_y = np.empty_like(B); ref_z = np.empty_like(B)
+        for p, (K, g) in enumerate(cfg.params):
+            sel = colp == p
+            ref_y[sel] = Mo.apply_S(K, g, B[sel].T).T
+            ref_z[sel] = Mo.apply_P_ra(ras[p].c0, ras[p].poles, ras[p].residues, B[sel].T).T
+        assert rel_l2_cols(y, ref_y) <= 1e-10
+        assert rel_l2_cols(z, ref_z) <= precond_tol(ras)
+        # the PCG solve
+        res = S.pcg_solve(Bt, colp, rtol=cfg.rtol, maxit=cfg.maxit)
+        x = res.x.cpu().numpy()
+        for p, (K, g) in enumerate(cfg.params):
+            sel = np.nonzero(colp == p)[0]
+            ra = ras[p]
+            X, its, rel, _ = opcg.pcg_batch(lambda V, cols: Mo.apply_S(K, g, V),
+                                            lambda V, cols: Mo.apply_P_ra(ra.c0, ra.poles, ra.residues, V),
+                                            B[sel].T, rtol=cfg.rtol, maxit=cfg.maxit)
+            assert np.all(np.abs(res.iters[sel] - its) <= 1), (p, res.iters[sel], its)
+            assert rel_l2_cols(x[sel], X.T) <= 1e-8
+        assert np.all(res.rel_res <= cfg.rtol)
+    finally:
+        S.close()
