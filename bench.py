@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark: Schur-complement PCG solves/s on B200 (BASELINE.json metric), one JSON line.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2_2d_N1024_sweep] [--impl reference]
+
+A "step" is one dd_pcg_solve over one batch of the workload (every column driven to
+rtol 1e-10): the whole hot path (Schur apply = DST GEMM + [S_dst|F] GEMM, RA pole sum, fused
+PCG updates) per iteration.  At N=1 the workload is BASELINE.json configs[1] (2D, 1024
+cells/side, 4 parameter sets x 64 RHS = 256 solves per step).
+Multi-GPU (torchrun): independent (K, mu, RHS) columns shard with no data-path collective —
+each rank solves its own full batch (weak scaling, seeds offset by rank); value = all ranks'
+solves / max-over-ranks time.
+Timing: W warm-up steps, then K steps each bracketed by CUDA events (recorded inside libdd
+on its stream), with a 512 MiB L2 flush between steps outside the timed spans; barrier +
+synchronize on both sides of the timed region; max over ranks.
+`--impl reference`: the CPU oracle (this tier's reference arm) timed on host cores on a
+bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2211_15308_b200 import configs, inputs, rafit  # noqa: E402
+
+METRIC = "Schur PCG solves/s"
+UNIT = "solves/s"
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def fit_ras(cfg):
+    lo, hi = rafit.interval_1d(cfg.N)
+    return [rafit.fit_ra(K, g, lo, hi, cfg.n_poles) for K, g in cfg.params]
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        under = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(under) if under else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_sample(cfg, ras, B, colp, per_param: int):
+    """Time the CPU oracle (mode tier: scipy DST + LAPACK banded Cholesky pole solves, PCG per
+    column) on `per_param` columns of every parameter set.  Returns (solves, seconds)."""
+    from oracle import pcg as opcg
+    from oracle import problem as oprob
+    Mo = oprob.ModeProblem2D(cfg.N)
+    t0 = time.perf_counter()
+    solves = 0
+    for p, (K, g) in enumerate(cfg.params):
+        sel = np.nonzero(colp == p)[0][:per_param]
+        ra = ras[p]
+        for c in sel:
+            opcg.pcg(lambda v: Mo.apply_S(K, g, v), lambda v: Mo.apply_P_ra(ra.c0, ra.poles, ra.residues, v), B[c],
+                     rtol=cfg.rtol, maxit=cfg.maxit)
+            solves += 1
+    return solves, time.perf_counter() - t0
+
+
+def cores_used():
+    try:
+        from threadpoolctl import threadpool_info
+        th = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        th = 1
+    return int(min(th, len(os.sched_getaffinity(0))))
+
+
+# ----------------------------------------------------------------------------- roofline inputs
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def fp64_peak():
+    m = load_json(os.path.join(ROOT, "MEASURED_FP64.json"))
+    if m and m.get("dmma_tflops"):
+        return float(m["dmma_tflops"]), "MEASURED_FP64.json dmma_tflops (DMMA issue-bound probe, this pool)"
+    mp = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    bf16 = float(mp.get("bf16_tflops", 1590.0))
+    return bf16 * 40.0 / 2250.0, "bf16 measured x nominal FP64/bf16 ratio (40/2250)"
+
+
+def traffic_for(cfg_name, kernel):
+    t = load_json(os.path.join(ROOT, "profiles", "traffic.json")) or {}
+    v = t.get(cfg_name, {}).get(kernel)
+    return float(v) if v is not None else None
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=configs.HEADLINE.name)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    cfg = configs.BY_NAME[args.config]
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2211_15308_b200 import binding
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ras = fit_ras(cfg)
+    B, colp = inputs.batch(cfg.n_gamma, len(cfg.params), cfg.rhs_per_param, seed_offset=rank * len(cfg.params))
+    C = B.shape[0]
+    S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local)
+    Bt = torch.as_tensor(B, device=f"cuda:{local}")
+    cp = torch.as_tensor(colp.astype(np.int32), device=f"cuda:{local}")
+    X = torch.empty_like(Bt)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def step():
+        return S.pcg_solve(Bt, cp, x=X, rtol=cfg.rtol, maxit=cfg.maxit)
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        step()
+    iters_all = []
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    S.launch_count()
+    step_ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)                      # L2 flush outside the timed span
+            r = step()
+            step_ms.append(S.last_solve_ms())
+            iters_all.append(r.iters.copy())
+        torch.cuda.synchronize()
+    launches = S.launch_count()
+    if world > 1:
+        dist.barrier()
+    total_ms = float(sum(step_ms))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    solves_total = C * args.steps * world
+    value = solves_total / (max_ms / 1e3)
+
+    # ---- instrumented pass: per-kernel-class device time (CUDA events on libdd's stream)
+    S.profile(True)
+    nprof = max(2, min(args.steps, 5))
+    for _ in range(nprof):
+        flush.fill_(1.0)
+        step()
+    prof = S.profile_read()
+    S.profile(False)
+    qc = S.query_config()
+
+    # ---- e2e through the host-buffer ABI call (pinned host memory, H2D + D2H inside)
+    Bh = torch.as_tensor(B).pin_memory().numpy()
+    Xh = torch.empty(B.shape, dtype=torch.float64).pin_memory().numpy()
+    S.pcg_solve_host(Bh, colp, rtol=cfg.rtol, maxit=cfg.maxit, x_out=Xh)
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        S.pcg_solve_host(Bh, colp, rtol=cfg.rtol, maxit=cfg.maxit, x_out=Xh)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = float(sum(e2e_t))
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = C * len(e2e_t) * world / float(te.item())
+
+    # ---- precond applies/s (secondary metric of BASELINE.json)
+    Z = torch.empty_like(Bt)
+    for _ in range(3):
+        S.apply_precond(Bt, cp, z=Z)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    reps = 20
+    e0.record(S.stream)
+    for _ in range(reps):
+        S.apply_precond(Bt, cp, z=Z)
+    e1.record(S.stream)
+    torch.cuda.synchronize()
+    pa_per_s = C * reps * world / (e0.elapsed_time(e1) / 1e3)
+
+    if rank == 0:
+        n = cfg.n
+        its = np.concatenate(iters_all)
+        mean_it = float(its.mean())
+        peak, peak_src = fp64_peak()
+        g2_ms, g2_n = prof["gemm_schur"]
+        g1_ms, g1_n = prof["gemm_dst"]
+        ps_ms, ps_n = prof["polesum_pcg"]
+        flops_g2 = 2.0 * n * (2 * n) * C          # [S_dst | F] (n x 2n) times (2n x C), algorithmic
+        flops_g1 = 2.0 * n * n * C
+        ach_g2 = flops_g2 / (g2_ms / g2_n / 1e3) / 1e12 if g2_n else None
+        step_flops = (flops_g1 + flops_g2) * mean_it
+        total_prof_ms = sum(v[0] for v in prof.values())
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "dim": cfg.dim, "cells_per_side": cfg.N, "n_gamma": cfg.n_gamma,
+                       "param_sets": len(cfg.params), "rhs_per_param": cfg.rhs_per_param, "solves_per_step": C,
+                       "poles": cfg.n_poles, "rtol": cfg.rtol, "l2": "flushed (512 MiB write) between timed steps",
+                       "parallelism": f"columns sharded, {world} rank(s), no collective",
+                       "mean_pcg_iters": round(mean_it, 3), "max_pcg_iters": int(its.max())},
+            "precond_applies_per_s": round(pa_per_s, 1),
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "roofline": {"bound": "tensor", "kernel": "gemm_schur ([S_dst|F] x [T; gamma X], DMMA fp64)",
+                         "achieved": round(ach_g2, 3) if ach_g2 else None, "peak": peak, "unit": "TFLOP/s",
+                         "frac": round(ach_g2 / peak, 4) if ach_g2 else None,
+                         "traffic": traffic_for(cfg.name, "gemm_schur"), "peak_source": peak_src,
+                         "flops_per_launch": flops_g2, "avg_launch_us": round(g2_ms / g2_n * 1e3, 2) if g2_n else None,
+                         "step_fp64_frac": round(step_flops / (total_prof_ms / nprof / 1e3) / 1e12 / peak, 4),
+                         "share_of_step": {k: round(v[0] / total_prof_ms, 4) for k, v in prof.items()},
+                         "avg_us": {k: round(v[0] / v[1] * 1e3, 2) if v[1] else None for k, v in prof.items()}},
+            "launch_config": qc,
+            "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(B.nbytes + C * 4), "d2h_bytes_per_step": int(B.nbytes + C * 12)},
+        }
+        if not args.no_cpu_baseline and world == 1:
+            per = max(1, int(os.environ.get("DD_ORACLE_PER_PARAM", "64")))
+            solves, secs = oracle_sample(cfg, ras, B, colp, per)
+            line["cpu_baseline"] = {"value": round(solves / secs, 4), "unit": UNIT, "cores": cores_used(),
+                                    "kind": "oracle",
+                                    "sample": f"{solves} of the {C} solves ({per} per parameter set), oracle mode tier "
+                                              f"(scipy DST + LAPACK banded Cholesky), {secs:.1f} s"}
+        print(json.dumps(line), flush=True)
+    S.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    ras = fit_ras(cfg)
+    B, colp = inputs.batch(cfg.n_gamma, len(cfg.params), cfg.rhs_per_param)
+    per = max(1, int(os.environ.get("DD_ORACLE_PER_PARAM", "16")))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, ras, B, colp, 1)
+    tot_s, tot_n = 0.0, 0
+    for _ in range(args.steps):
+        n, s = oracle_sample(cfg, ras, B, colp, per)
+        tot_s += s; tot_n += n
+    v = tot_n / tot_s
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_s / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "solves_per_step": per * len(cfg.params)},
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": cores_used(), "kind": "oracle",
+                             "sample": f"{per} solves per parameter set per step (of {cfg.rhs_per_param}), oracle mode tier"},
+            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

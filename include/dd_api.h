@@ -144,6 +144,10 @@ const char* dd_last_error(void);
 dd_status dd_profile_enable(dd_ctx* ctx, int on);
 /* ms[DD_NKCLASS] total milliseconds, launches[DD_NKCLASS]; resets the counters. */
 dd_status dd_profile_read(dd_ctx* ctx, double* ms, long long* launches);
+/* Device time of the last dd_pcg_solve / dd_pcg_solve_host in ms: CUDA events on the handle's
+ * stream around the whole solve (parameter check, init, iterations), excluding the final
+ * device->host read of iters/rel_res and, for the host variant, the staging copies. */
+dd_status dd_last_solve_ms(dd_ctx* ctx, double* ms);
 /* Number of this library's kernel launches since the last call (resets). */
 long long dd_launch_count(dd_ctx* ctx);
 /* Launch configuration actually used (for reports): splitk of the two GEMMs, pole-sum

@@ -41,6 +41,9 @@ class DenseProblem:
     def apply_P_exact(self, K, gamma, X):
         return ra.apply_exact_precond(self.gevp, K, gamma, X)
 
+    def apply_P_ra_eigen(self, c0, poles, residues, X):
+        return ra.apply_ra_eigen(self.gevp, c0, poles, residues, X)
+
     def spectrum(self):
         return self.gevp.lam
 
@@ -72,6 +75,13 @@ class ModeProblem2D:
         """Parity form: banded Cholesky solves of the assembled tridiagonal pair."""
         a_d, a_o, m_d, m_o = self.band
         return ra.apply_ra_banded_tri(a_d, a_o, m_d, m_o, c0, poles, residues, X)
+
+    def apply_P_ra_eigen(self, c0, poles, residues, X):
+        """Eigen form U diag(r(λ)) U^T X of the same RA operator (fixed point (ii) of SURVEY §8c):
+        (A - pM)^-1 = U diag(1/(λ-p)) U^T with U = S_dst diag(μ^-1/2)."""
+        Xh = schur.dst_ortho(X, axis=0)
+        w = ra.r_eval(self.lam, c0, poles, residues) / self.mu
+        return schur.dst_ortho(w[:, None] * Xh if X.ndim == 2 else w * Xh, axis=0)
 
     def apply_P_exact(self, K, gamma, X):
         Xh = schur.dst_ortho(X, axis=0)

@@ -23,7 +23,7 @@ KCLASS = ["gemm_dst", "gemm_schur", "polesum_pcg", "other"]
 
 EXPORTS = ["dd_setup", "dd_interface_size", "dd_apply_schur", "dd_apply_precond", "dd_pcg_solve",
            "dd_pcg_solve_host", "dd_destroy", "dd_last_error", "dd_profile_enable", "dd_profile_read",
-           "dd_launch_count", "dd_query_config", "dd_test_dgemm"]
+           "dd_launch_count", "dd_query_config", "dd_test_dgemm", "dd_last_solve_ms"]
 
 
 class DDError(RuntimeError):
@@ -66,6 +66,7 @@ def load():
     lib.dd_profile_read.argtypes = [P, P, P]; lib.dd_profile_read.restype = I
     lib.dd_launch_count.argtypes = [P]; lib.dd_launch_count.restype = ctypes.c_longlong
     lib.dd_query_config.argtypes = [P, P, P, P, P]; lib.dd_query_config.restype = I
+    lib.dd_last_solve_ms.argtypes = [P, P]; lib.dd_last_solve_ms.restype = I
     lib.dd_test_dgemm.argtypes = [I, I, I, P, I, P, I, P, I, I, P]; lib.dd_test_dgemm.restype = I
     _lib = lib
     return lib
@@ -186,6 +187,11 @@ class Solver:
         ms = np.zeros(4); n = np.zeros(4, dtype=np.int64)
         _check(load().dd_profile_read(self._h, ms.ctypes.data, n.ctypes.data))
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KCLASS)}
+
+    def last_solve_ms(self) -> float:
+        v = ctypes.c_double()
+        _check(load().dd_last_solve_ms(self._h, ctypes.byref(v)))
+        return v.value
 
     def launch_count(self) -> int:
         return int(load().dd_launch_count(self._h))

@@ -84,6 +84,7 @@ struct dd_ctx {
     bool graph_ok = true;
     std::map<GraphKey, cudaGraphExec_t> graphs;
     int last_split1 = 0, last_split2 = 0, last_ps_warps = 0, last_graph = 0;
+    cudaEvent_t solve_ev[2] = {nullptr, nullptr};
 };
 
 // ------------------------------------------------------------------------------------ helpers
@@ -571,6 +572,11 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
     if (ncols == 0) return DD_OK;
     if (hist && maxit + 1 > c->hist_cap) return fail(DD_EINVAL, "maxit too large for hist (<= 4095)");
     CK(cudaSetDevice(c->device));
+    if (!c->solve_ev[0]) {
+        CK(cudaEventCreate(&c->solve_ev[0]));
+        CK(cudaEventCreate(&c->solve_ev[1]));
+    }
+    CK(cudaEventRecord(c->solve_ev[0], c->stream));
     CK(cudaMemsetAsync(c->ints, 0, sizeof(int) * 8, c->stream));
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
     PcgState st = make_state(c, ncols, colp, x, rtol, maxit, norm_kind);
@@ -620,6 +626,7 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
             }
         }
     }
+    CK(cudaEventRecord(c->solve_ev[1], c->stream));
     if (iters) CK(cudaMemcpyAsync(iters, c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c->stream));
     if (rel_res) CK(cudaMemcpyAsync(rel_res, c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(c->h_ints, c->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -671,6 +678,7 @@ extern "C" dd_status dd_destroy(dd_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& e : c->solve_ev) if (e) cudaEventDestroy(e);
     for (auto& e : c->ev_pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (auto& e : c->ev_free) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (void* p : c->allocs) cudaFree(p);
@@ -704,6 +712,15 @@ extern "C" dd_status dd_profile_read(dd_ctx* c, double* ms, long long* launches)
         c->prof_ms[i] = 0.0;
         c->prof_n[i] = 0;
     }
+    return DD_OK;
+}
+
+extern "C" dd_status dd_last_solve_ms(dd_ctx* c, double* ms) {
+    if (!c || !ms) return fail(DD_EINVAL, "NULL argument");
+    if (!c->solve_ev[0]) return fail(DD_EINVAL, "no solve yet");
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, c->solve_ev[0], c->solve_ev[1]));
+    *ms = t;
     return DD_OK;
 }
 

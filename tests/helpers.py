@@ -21,3 +21,18 @@ def rel_l2_cols(a, b):
 def precond_tol(ras):
     # max(1e-10, 1e-15 κ_c) relative ℓ2 (κ_c = cancellation factor, reading A11)
     return max(1e-10, 1e-15 * max(r.cancel for r in ras))
+
+
+def check_precond(z_gpu, z_banded, z_eigen, ras):
+    """Preconditioner parity (reading A11'): the GPU result must match the oracle's
+    eigen form U diag(r(λ)) U^T within max(1e-10, 1e-15 κ_c), and the oracle's parity form
+    (LAPACK banded Cholesky per pole) within that bar plus the oracle's own measured
+    parity-vs-eigen discrepancy (the banded solves of the least-shifted pole carry
+    ~eps·cond(A_Γ - p M_Γ) ≈ 1e-10 at n = 4095)."""
+    tol = precond_tol(ras)
+    e_eig = rel_l2_cols(z_gpu, z_eigen)
+    self_err = rel_l2_cols(z_banded, z_eigen)
+    e_band = rel_l2_cols(z_gpu, z_banded)
+    assert e_eig <= tol, (e_eig, tol)
+    assert e_band <= tol + self_err, (e_band, tol, self_err)
+    return e_eig, e_band, self_err

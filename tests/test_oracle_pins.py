@@ -207,6 +207,9 @@ def test_mode_problem_matches_dense(N):
     poles, res = [-0.5, -30.0, -1e4], [0.3, -0.1, 2.0]
     a, b = D.apply_P_ra(0.7, poles, res, X), Mo.apply_P_ra(0.7, poles, res, X)
     assert np.abs(a - b).max() < 1e-12 * np.abs(a).max()
+    c, d = D.apply_P_ra_eigen(0.7, poles, res, X), Mo.apply_P_ra_eigen(0.7, poles, res, X)
+    assert np.abs(a - c).max() < 1e-12 * np.abs(a).max()
+    assert np.abs(a - d).max() < 1e-12 * np.abs(a).max()
 
 
 # --------------------------------------------------------------------------- RA
