@@ -25,8 +25,9 @@ struct GemmArgs {
     const double* A; int lda;    // row-major, rows readable up to round_up(M, BM)
     const double* B; int ldb;    // column-major, columns readable up to round_up(N, BN)
     double* C; int ldc;          // column-major
-    int splitk;                  // >= 1
-    double* ws;                  // split-K partials  [tiles * splitk * BM*BN]
+    int splitk;                  // 0: stream-K; 1..8: cluster split-K
+    int num_sms;
+    double* ws;                  // stream-K partials (gemm_ws_doubles)
     int* counters;               // [tiles], zero on entry, left zero on exit
     int epi;
     int n_param;
@@ -36,8 +37,8 @@ struct GemmArgs {
 };
 
 int gemm_tiles(int M, int N);
-int gemm_pick_splitk(int M, int N, int K, int num_sms);
-size_t gemm_ws_doubles(int M, int N, int splitk);
+int gemm_pick_splitk(int M, int N, int K, int num_sms);   // 0 = stream-K
+size_t gemm_ws_doubles(int M, int N, int num_sms);
 cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st);
 
 // ----------------------------------------------------------------------------- pole sum
@@ -87,7 +88,7 @@ struct PcgState {
 };
 
 int polesum_warps(int L);
-size_t polesum_smem(int L, int warps);
+size_t polesum_smem(int L, int warps, int max_sys);
 cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b,
                             int ldb, cudaStream_t st);
 cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st);

@@ -1,0 +1,459 @@
+// FP64 DMMA GEMM tile template (sm_100a), shared by libdd and tools/gemm_lab.cu.
+//
+//   C = A · B,  A row-major (lda), B column-major (ldb) — both K-contiguous ("TN").
+//
+// CTA tile BM x BN, K-step BK, WM x WN warps each owning (BM/WM) x (BN/WN) as m16n8k4 fragments
+// (mma.sync.aligned.m16n8k4 .f64 -> SASS DMMA.8x8x4; tcgen05 has no f64 kind).  Operands are
+// staged by a STAGES-deep cp.async (LDGSTS) ring in padded smem rows (BK+4 doubles: the
+// fragment loads of a warp hit distinct bank pairs).  Split-K: gridDim.y = S CTAs of one output
+// tile form a thread-block cluster (1, S, 1); after the main loop each CTA parks its
+// accumulators in its own shared memory and, after a cluster barrier, CTA q reduces the
+// accumulator registers r ≡ q (mod S) of all S CTAs over DSMEM in fixed order s = 0..S-1
+// (bitwise deterministic, no global partials, no serial tail) and runs the epilogue on them.
+#pragma once
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+namespace dd {
+namespace cg = cooperative_groups;
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_>
+struct DgemmCfg {
+    static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
+    static constexpr int THREADS = WM * WN * 32;
+    static constexpr int LDS = BK + 4;
+    static constexpr int TM = BM / WM, TN = BN / WN;        // warp tile
+    static constexpr int MI = TM / 16, NI = TN / 8;         // fragments per warp
+    static constexpr int NREG = MI * NI * 4;                // accumulators per thread
+    static constexpr size_t SMEM_PIPE = size_t(STAGES) * (BM + BN) * LDS * sizeof(double);
+    static constexpr size_t SMEM_RED = size_t(NREG) * THREADS * sizeof(double);
+    static constexpr size_t SMEM = SMEM_PIPE > SMEM_RED ? SMEM_PIPE : SMEM_RED;
+    static_assert(TM % 16 == 0 && TN % 8 == 0 && BK % 4 == 0, "tile shape");
+    static_assert((BM * BK / 2) % THREADS == 0 && (BN * BK / 2) % THREADS == 0, "load mapping");
+};
+
+struct DgemmProblem {
+    int M, N, K;                 // K multiple of BK
+    const double* A; int lda;    // rows readable up to round_up(M, BM)
+    const double* B; int ldb;    // columns readable up to round_up(N, BN)
+};
+
+__device__ __forceinline__ void dg_cp_async16(void* smem, const void* gmem) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void dg_cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void dg_cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dg_mma(double (&c)[4], double a0, double a1, double b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+        : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+        : "d"(a0), "d"(a1), "d"(b));
+}
+
+// Row / column of accumulator register r of this thread within the CTA tile.
+template <class C>
+__device__ __forceinline__ void dg_coord(int r, int tid, int& row, int& col) {
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wm = warp % C::WM, wn = warp / C::WM;
+    const int f = r >> 2, q = r & 3;
+    const int mi = f / C::NI, ni = f % C::NI;
+    row = wm * C::TM + mi * 16 + (lane >> 2) + (q >> 1) * 8;
+    col = wn * C::TN + ni * 8 + (lane & 3) * 2 + (q & 1);
+}
+
+// Epi: functor  __device__ void operator()(int row, int col, double v) const  (row < M, col < N checked)
+template <class C, class Epi>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem g, Epi epi) {
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;
+    double* Bs = smem + C::STAGES * C::BM * C::LDS;
+
+    const int tiles_m = (g.M + C::BM - 1) / C::BM;
+    const int m0 = (blockIdx.x % tiles_m) * C::BM;
+    const int n0 = (blockIdx.x / tiles_m) * C::BN;
+    const int S = gridDim.y, split = blockIdx.y;
+    const int ktiles = g.K / C::BK;
+    const int per = (ktiles + S - 1) / S;
+    const int kt0 = split * per;
+    const int nkt = max(0, min(per, ktiles - kt0));
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = warp % C::WM, wn = warp / C::WM;
+    const int gq = lane >> 2, tq = lane & 3;
+
+    double acc[C::MI][C::NI][4];
+#pragma unroll
+    for (int i = 0; i < C::MI; i++)
+#pragma unroll
+        for (int j = 0; j < C::NI; j++)
+#pragma unroll
+            for (int r = 0; r < 4; r++) acc[i][j][r] = 0.0;
+
+    auto load_stage = [&](int stage, int kt) {
+        const int k0 = kt * C::BK;
+        constexpr int CPR = C::BK / 2;   // 16-byte chunks per row
+#pragma unroll
+        for (int j = 0; j < (C::BM * CPR) / C::THREADS; j++) {
+            const int c = tid + C::THREADS * j;
+            const int row = c / CPR, kc = (c % CPR) * 2;
+            dg_cp_async16(&As[(stage * C::BM + row) * C::LDS + kc], g.A + (size_t)(m0 + row) * g.lda + k0 + kc);
+        }
+#pragma unroll
+        for (int j = 0; j < (C::BN * CPR) / C::THREADS; j++) {
+            const int c = tid + C::THREADS * j;
+            const int row = c / CPR, kc = (c % CPR) * 2;
+            dg_cp_async16(&Bs[(stage * C::BN + row) * C::LDS + kc], g.B + (size_t)(n0 + row) * g.ldb + k0 + kc);
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < C::STAGES - 1; s++) {
+        if (s < nkt) load_stage(s, kt0 + s);
+        dg_cp_commit();
+    }
+    for (int it = 0; it < nkt; it++) {
+        dg_cp_wait<C::STAGES - 2>();
+        __syncthreads();
+        const int nk = it + C::STAGES - 1;
+        if (nk < nkt) load_stage(nk % C::STAGES, kt0 + nk);
+        dg_cp_commit();
+        const double* as = As + (it % C::STAGES) * C::BM * C::LDS + (wm * C::TM + gq) * C::LDS + tq;
+        const double* bs = Bs + (it % C::STAGES) * C::BN * C::LDS + (wn * C::TN + gq) * C::LDS + tq;
+#pragma unroll
+        for (int kk = 0; kk < C::BK; kk += 4) {
+            double a[C::MI][2], b[C::NI];
+#pragma unroll
+            for (int mi = 0; mi < C::MI; mi++) {
+                a[mi][0] = as[(mi * 16) * C::LDS + kk];
+                a[mi][1] = as[(mi * 16 + 8) * C::LDS + kk];
+            }
+#pragma unroll
+            for (int ni = 0; ni < C::NI; ni++) b[ni] = bs[(ni * 8) * C::LDS + kk];
+#pragma unroll
+            for (int mi = 0; mi < C::MI; mi++)
+#pragma unroll
+                for (int ni = 0; ni < C::NI; ni++) dg_mma(acc[mi][ni], a[mi][0], a[mi][1], b[ni]);
+        }
+    }
+    dg_cp_wait<0>();
+
+    if (S == 1) {
+#pragma unroll
+        for (int mi = 0; mi < C::MI; mi++)
+#pragma unroll
+            for (int ni = 0; ni < C::NI; ni++)
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    int row, col;
+                    dg_coord<C>((mi * C::NI + ni) * 4 + q, tid, row, col);
+                    row += m0; col += n0;
+                    if (row < g.M && col < g.N) epi(row, col, acc[mi][ni][q]);
+                }
+        return;
+    }
+
+    // ---- split-K: deterministic reduction across the cluster over DSMEM
+    cg::cluster_group cluster = cg::this_cluster();
+    __syncthreads();   // pipeline smem is free now
+    double* red = smem;
+#pragma unroll
+    for (int mi = 0; mi < C::MI; mi++)
+#pragma unroll
+        for (int ni = 0; ni < C::NI; ni++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) red[((mi * C::NI + ni) * 4 + q) * C::THREADS + tid] = acc[mi][ni][q];
+    cluster.sync();
+    const int rank = (int)cluster.block_rank();
+    // CTA `rank` owns registers r = rank + j*S; source-CTA-outer / register-inner so the DSMEM
+    // loads of one source are in flight together; the sum order over sources is fixed.
+    constexpr int JMAX = C::NREG;
+    double v[JMAX];
+#pragma unroll
+    for (int j = 0; j < JMAX; j++) v[j] = 0.0;
+    for (int s = 0; s < S; s++) {
+        const double* rs = cluster.map_shared_rank(red, s);
+#pragma unroll
+        for (int j = 0; j < JMAX; j++) {
+            const int r = rank + j * S;
+            if (r < C::NREG) v[j] += rs[r * C::THREADS + tid];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < JMAX; j++) {
+        const int r = rank + j * S;
+        if (r < C::NREG) {
+            int row, col;
+            dg_coord<C>(r, tid, row, col);
+            row += m0; col += n0;
+            if (row < g.M && col < g.N) epi(row, col, v[j]);
+        }
+    }
+    cluster.sync();   // keep every CTA's smem alive until all remote reads are done
+}
+
+// ----------------------------------------------------------------------------------- stream-K
+// Work units = (output tile, k-tile) pairs in tile-major, k-minor order; CTA b of G takes
+// units [floor(bU/G), floor((b+1)U/G)) — every SM gets the same amount of MMA work whatever
+// the tile count.  A tile whose k-range is cut by CTA boundaries is produced in segments; each
+// segment's CTA parks its partial accumulators in a global slot (tile-local segment index),
+// and the last CTA to finish a segment of that tile (per-tile arrival counter) sums all
+// segments in segment order (its own from registers) and runs the epilogue.  Fixed partition
+// + fixed order = bitwise deterministic; no CTA ever waits on another.
+struct StreamK {
+    double* ws;       // [slots][BM*BN] partials (slot = seg_base[tile] + seg)
+    int* counters;    // [tiles], zero on entry, reset by the reducing CTA
+    int G;            // CTAs in the grid
+};
+
+__device__ __forceinline__ long long sk_unit_begin(int b, long long U, int G) { return (long long)b * U / G; }
+// CTA whose range contains unit u
+__device__ __forceinline__ int sk_cta_of(long long u, long long U, int G) {
+    int b = (int)((u * G) / U);
+    while (b + 1 < G && sk_unit_begin(b + 1, U, G) <= u) b++;
+    while (b > 0 && sk_unit_begin(b, U, G) > u) b--;
+    return b;
+}
+
+template <class C, class Epi>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProblem g, Epi epi, StreamK sk) {
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;
+    double* Bs = smem + C::STAGES * C::BM * C::LDS;
+    __shared__ int s_last;
+
+    const int tiles_m = (g.M + C::BM - 1) / C::BM;
+    const int tiles = tiles_m * ((g.N + C::BN - 1) / C::BN);
+    const int KT = g.K / C::BK;
+    const long long U = (long long)tiles * KT;
+    const int b = blockIdx.x;
+    const long long u0 = sk_unit_begin(b, U, sk.G), u1 = sk_unit_begin(b + 1, U, sk.G);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = warp % C::WM, wn = warp / C::WM;
+    const int gq = lane >> 2, tq = lane & 3;
+
+    long long u = u0;
+    while (u < u1) {
+        const int t = (int)(u / KT);
+        const int ks = (int)(u % KT);
+        const int ke = (int)min((long long)KT, (long long)ks + (u1 - u));
+        const int m0 = (t % tiles_m) * C::BM;
+        const int n0 = (t / tiles_m) * C::BN;
+        const int nkt = ke - ks;
+
+        double acc[C::MI][C::NI][4];
+#pragma unroll
+        for (int i = 0; i < C::MI; i++)
+#pragma unroll
+            for (int j = 0; j < C::NI; j++)
+#pragma unroll
+                for (int r = 0; r < 4; r++) acc[i][j][r] = 0.0;
+
+        auto load_stage = [&](int stage, int kt) {
+            const int k0 = kt * C::BK;
+            constexpr int CPR = C::BK / 2;
+#pragma unroll
+            for (int j = 0; j < (C::BM * CPR) / C::THREADS; j++) {
+                const int c = tid + C::THREADS * j;
+                const int row = c / CPR, kc = (c % CPR) * 2;
+                dg_cp_async16(&As[(stage * C::BM + row) * C::LDS + kc], g.A + (size_t)(m0 + row) * g.lda + k0 + kc);
+            }
+#pragma unroll
+            for (int j = 0; j < (C::BN * CPR) / C::THREADS; j++) {
+                const int c = tid + C::THREADS * j;
+                const int row = c / CPR, kc = (c % CPR) * 2;
+                dg_cp_async16(&Bs[(stage * C::BN + row) * C::LDS + kc], g.B + (size_t)(n0 + row) * g.ldb + k0 + kc);
+            }
+        };
+        __syncthreads();   // previous segment's smem reads are finished
+#pragma unroll
+        for (int s = 0; s < C::STAGES - 1; s++) {
+            if (s < nkt) load_stage(s, ks + s);
+            dg_cp_commit();
+        }
+        for (int it = 0; it < nkt; it++) {
+            dg_cp_wait<C::STAGES - 2>();
+            __syncthreads();
+            const int nk = it + C::STAGES - 1;
+            if (nk < nkt) load_stage(nk % C::STAGES, ks + nk);
+            dg_cp_commit();
+            const double* as = As + (it % C::STAGES) * C::BM * C::LDS + (wm * C::TM + gq) * C::LDS + tq;
+            const double* bs = Bs + (it % C::STAGES) * C::BN * C::LDS + (wn * C::TN + gq) * C::LDS + tq;
+#pragma unroll
+            for (int kk = 0; kk < C::BK; kk += 4) {
+                double a[C::MI][2], bb[C::NI];
+#pragma unroll
+                for (int mi = 0; mi < C::MI; mi++) {
+                    a[mi][0] = as[(mi * 16) * C::LDS + kk];
+                    a[mi][1] = as[(mi * 16 + 8) * C::LDS + kk];
+                }
+#pragma unroll
+                for (int ni = 0; ni < C::NI; ni++) bb[ni] = bs[(ni * 8) * C::LDS + kk];
+#pragma unroll
+                for (int mi = 0; mi < C::MI; mi++)
+#pragma unroll
+                    for (int ni = 0; ni < C::NI; ni++) dg_mma(acc[mi][ni], a[mi][0], a[mi][1], bb[ni]);
+            }
+        }
+        dg_cp_wait<0>();
+
+        bool emit = true;
+        if (!(ks == 0 && ke == KT)) {
+            // segmented tile: park the partial, count arrivals, last arriver reduces
+            const long long tu0 = (long long)t * KT;
+            const int bfirst = sk_cta_of(tu0, U, sk.G);
+            const int blast = sk_cta_of(tu0 + KT - 1, U, sk.G);
+            const int nseg = blast - bfirst + 1;
+            const int seg = b - bfirst;
+            // slot base of tile t = Σ_{t'<t} (nseg(t') - 1) ... use a closed form: bfirst + t
+            double* slot = sk.ws + ((size_t)(bfirst + t) + seg) * (C::BM * C::BN);
+#pragma unroll
+            for (int mi = 0; mi < C::MI; mi++)
+#pragma unroll
+                for (int ni = 0; ni < C::NI; ni++)
+#pragma unroll
+                    for (int q = 0; q < 4; q++) __stcg(&slot[((mi * C::NI + ni) * 4 + q) * C::THREADS + tid], acc[mi][ni][q]);
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) s_last = (atomicAdd(&sk.counters[t], 1) == nseg - 1);
+            __syncthreads();
+            emit = s_last;
+            if (emit) {
+                __threadfence();
+                const double* base = sk.ws + (size_t)(bfirst + t) * (C::BM * C::BN);
+                // segment-outer / register-inner: each segment's loads are independent and in
+                // flight together; the sum order (segment 0, 1, ...) is fixed.
+                double sum[C::NREG];
+#pragma unroll
+                for (int r = 0; r < C::NREG; r++) sum[r] = 0.0;
+                for (int s2 = 0; s2 < nseg; s2++) {
+                    if (s2 == seg) {
+#pragma unroll
+                        for (int mi = 0; mi < C::MI; mi++)
+#pragma unroll
+                            for (int ni = 0; ni < C::NI; ni++)
+#pragma unroll
+                                for (int q = 0; q < 4; q++) sum[(mi * C::NI + ni) * 4 + q] += acc[mi][ni][q];
+                    } else {
+                        const double* src = base + (size_t)s2 * (C::BM * C::BN) + tid;
+                        double tmp[C::NREG];
+#pragma unroll
+                        for (int r = 0; r < C::NREG; r++) tmp[r] = __ldcg(&src[r * C::THREADS]);
+#pragma unroll
+                        for (int r = 0; r < C::NREG; r++) sum[r] += tmp[r];
+                    }
+                }
+#pragma unroll
+                for (int mi = 0; mi < C::MI; mi++)
+#pragma unroll
+                    for (int ni = 0; ni < C::NI; ni++)
+#pragma unroll
+                        for (int q = 0; q < 4; q++) acc[mi][ni][q] = sum[(mi * C::NI + ni) * 4 + q];
+                if (tid == 0) sk.counters[t] = 0;
+            }
+        }
+        if (emit) {
+#pragma unroll
+            for (int mi = 0; mi < C::MI; mi++)
+#pragma unroll
+                for (int ni = 0; ni < C::NI; ni++)
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        int row, col;
+                        dg_coord<C>((mi * C::NI + ni) * 4 + q, tid, row, col);
+                        row += m0; col += n0;
+                        if (row < g.M && col < g.N) epi(row, col, acc[mi][ni][q]);
+                    }
+        }
+        u += nkt;
+    }
+}
+
+// Stream-K sizing: grid = resident CTAs (SMs x occupancy, capped by the unit count).
+template <class C>
+inline int dgemm_streamk_grid(int M, int N, int K, int num_sms, int occ) {
+    const long long tiles = ((M + C::BM - 1) / C::BM) * (long long)((N + C::BN - 1) / C::BN);
+    const long long U = tiles * (K / C::BK);
+    long long G = (long long)num_sms * occ;
+    if (G > U) G = U;
+    return (int)(G < 1 ? 1 : G);
+}
+// workspace: slot index bfirst(t) + t + seg <= (G - 1) + (tiles - 1) + nseg <= G + 2 tiles
+template <class C>
+inline size_t dgemm_streamk_ws_doubles(int M, int N, int G) {
+    const size_t tiles = size_t((M + C::BM - 1) / C::BM) * size_t((N + C::BN - 1) / C::BN);
+    return (size_t(G) + 2 * tiles + 2) * C::BM * C::BN;
+}
+
+template <class C, class Epi>
+inline cudaError_t dgemm_launch_streamk(const DgemmProblem& g, int G, const StreamK& sk, const Epi& epi, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_dgemm_streamk<C, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+    StreamK s = sk;
+    s.G = G;
+    k_dgemm_streamk<C, Epi><<<G, C::THREADS, C::SMEM, st>>>(g, epi, s);
+    return cudaGetLastError();
+}
+
+template <class C>
+inline int dgemm_tiles(int M, int N) {
+    return ((M + C::BM - 1) / C::BM) * ((N + C::BN - 1) / C::BN);
+}
+
+template <class C, class Epi>
+inline cudaError_t dgemm_launch(const DgemmProblem& g, int splitk, const Epi& epi, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_dgemm_tile<C, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        if (e != cudaSuccess) return e;
+        if (C::SMEM > 100 * 1024) cudaFuncSetAttribute(k_dgemm_tile<C, Epi>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+    if (splitk < 1) splitk = 1;
+    if (splitk > 8) splitk = 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(dgemm_tiles<C>(g.M, g.N), splitk, 1);
+    cfg.blockDim = dim3(C::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = splitk;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = splitk > 1 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_dgemm_tile<C, Epi>, g, epi);
+}
+
+// Pick split-K S (1..8) for a tile count so that S * tiles fills the SM slots evenly.
+template <class C>
+inline int dgemm_pick_splitk(int M, int N, int K, int num_sms, int ctas_per_sm) {
+    const int tiles = dgemm_tiles<C>(M, N);
+    const int ktiles = K / C::BK;
+    const int slots = num_sms * ctas_per_sm;
+    int best = 1;
+    double best_t = 1e30;
+    for (int s = 1; s <= 8; s++) {
+        if (s > 1 && ktiles / s < 4) break;
+        const int ctas = tiles * s;
+        // time ~ (work per CTA) x (CTAs on the busiest SM), plus a small per-split reduction cost
+        const double per_cta = double((ktiles + s - 1) / s) + 2.0;
+        const int waves = (ctas + slots - 1) / slots;
+        const int busiest = (ctas + num_sms - 1) / num_sms;   // CTAs per SM when spread
+        const double t = per_cta * (double)busiest * (waves > 1 ? 1.0 : 1.0) + (s > 1 ? 1.5 : 0.0);
+        if (t < best_t - 1e-9) { best_t = t; best = s; }
+    }
+    return best;
+}
+
+}  // namespace dd

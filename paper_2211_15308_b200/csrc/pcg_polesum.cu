@@ -128,6 +128,120 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Register-resident fast path for chunk length L <= LMAX <= 32 (n_Γ <= 1023).
+// Every lane keeps its chunk (y) and its share of the pole sum (z) in registers; sweeps are fully
+// unrolled so the table loads (shared memory, broadcast) are hoisted off the FMA chain.  Warp w
+// accumulates systems k = w, w+W, ... in registers; the W partial sums are combined in fixed
+// warp order at the end (deterministic).  Tables of all systems are staged in shared memory
+// once per CTA: [k][invb | cpr | ufull | upart] x L.
+template <int LMAX>
+__device__ void block_polesum_reg(const PoleTabs& t, const PoleGeom& g, int param, const double* R, double* Z,
+                                  double* scratch) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int W = blockDim.x >> 5;
+    const int L = g.L;
+    const int tot = L * 33;
+    const int nsys = t.nsys[param];
+    double* Zw = scratch;                          // [W][tot]
+    double* tab = scratch + (size_t)W * tot;       // [nsys][4][L]
+    const size_t pbase = (size_t)param * t.max_sys;
+    for (int idx = threadIdx.x; idx < nsys * 4 * L; idx += blockDim.x) {
+        const int k = idx / (4 * L), rem = idx - k * 4 * L, which = rem / L, i = rem - which * L;
+        const double* src = which == 0 ? t.invb : (which == 1 ? t.cpr : (which == 2 ? t.ufull : t.upart));
+        tab[idx] = src[(pbase + k) * L + i];
+    }
+    __syncthreads();
+
+    const int Lr = lane < g.part_lane ? L - 1 : (lane == g.part_lane ? g.Lr_part : 0);
+    const int Lr_next = (lane + 1) < g.part_lane ? L - 1 : ((lane + 1) == g.part_lane ? g.Lr_part : 0);
+    const bool sep_real = lane < g.part_lane;
+    double z[LMAX];
+#pragma unroll
+    for (int i = 0; i < LMAX; i++) z[i] = 0.0;
+
+    for (int k = warp; k < nsys; k += W) {
+        const double* ib = tab + (size_t)k * 4 * L;
+        const double* cp = ib + L;
+        const double* u = lane < g.part_lane ? ib + 2 * L : ib + 3 * L;
+        const double e = t.e[pbase + k], wk = t.w[pbase + k];
+        const double* pa = t.pa + (pbase + k) * 160;
+        const double* pb = t.pb + (pbase + k) * 160;
+        double pav[5], pbv[5];
+#pragma unroll
+        for (int j = 0; j < 5; j++) { pav[j] = __ldg(&pa[j * 32 + lane]); pbv[j] = __ldg(&pb[j * 32 + lane]); }
+        const double pinv = __ldg(&t.pinvb[(pbase + k) * 32 + lane]);
+        double y[LMAX];
+        // forward:  ỹ_i = r_i/b'_i - (e/b'_i) ỹ_{i-1}
+        double prev = 0.0, y_last = 0.0;   // y_last = ỹ_{Lr-1} = y_{Lr-1} (untouched by the back sweep)
+#pragma unroll
+        for (int i = 0; i < LMAX; i++) {
+            if (i < L - 1) {
+                const double v = fma(-cp[i], prev, R[TI(i, lane)] * ib[i]);
+                y[i] = i < Lr ? v : 0.0;
+                if (i < Lr) y_last = v;
+                prev = y[i];
+            } else {
+                y[i] = 0.0;
+            }
+        }
+        // backward:  y_i = ỹ_i - (e/b'_i) y_{i+1}
+        double next = 0.0;
+#pragma unroll
+        for (int i = LMAX - 1; i >= 0; i--) {
+            if (i < L - 1) {
+                y[i] = fma(-cp[i], next, y[i]);
+                next = y[i];
+            }
+        }
+        double y_first = y[0];
+        if (Lr == 0) y_first = 0.0;
+        const double y_first_next = __shfl_down_sync(0xffffffffu, y_first, 1);
+        double rs = 0.0;
+        if (sep_real) {
+            rs = R[TI(L - 1, lane)];
+            if (Lr > 0) rs -= e * y_last;
+            if (lane < 31 && Lr_next > 0) rs -= e * y_first_next;
+        }
+#pragma unroll
+        for (int j = 0; j < 5; j++) {
+            const int s = 1 << j;
+            double rm = __shfl_up_sync(0xffffffffu, rs, s);
+            double rp = __shfl_down_sync(0xffffffffu, rs, s);
+            if (lane < s) rm = 0.0;
+            if (lane + s > 31) rp = 0.0;
+            rs = rs - pav[j] * rm - pbv[j] * rp;
+        }
+        const double gsep = sep_real ? rs * pinv : 0.0;
+        double gleft = __shfl_up_sync(0xffffffffu, gsep, 1);
+        if (lane == 0) gleft = 0.0;
+        const double eg0 = e * gleft, eg1 = e * gsep;
+#pragma unroll
+        for (int i = 0; i < LMAX; i++) {
+            if (i < L - 1 && i < Lr) {
+                const double x = y[i] - eg0 * u[i] - eg1 * u[Lr - 1 - i];
+                z[i] = fma(wk, x, z[i]);
+            }
+        }
+        // separator row (in-chunk index L-1)
+#pragma unroll
+        for (int i = 0; i < LMAX; i++)
+            if (i == L - 1) z[i] = fma(wk, gsep, z[i]);
+    }
+    // fixed-order combine of the W warp partials
+#pragma unroll
+    for (int i = 0; i < LMAX; i++)
+        if (i < L) Zw[(size_t)warp * tot + TI(i, lane)] = z[i];
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+        if ((idx % 33) == 32) continue;
+        double acc = 0.0;
+        for (int w = 0; w < W; w++) acc += Zw[(size_t)w * tot + idx];
+        Z[idx] = acc;
+    }
+    __syncthreads();
+}
+
 // Deterministic block reduction of two values (fixed tree).
 __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -151,7 +265,15 @@ __device__ __forceinline__ int clamp_param(int p, int n_param) { return p < 0 ? 
 // rows of the column in natural order <-> transposed smem index
 __device__ __forceinline__ int tpos(int row, int L) { return TI(row % L, row / L); }
 
+template <int LMAX>
+__device__ __forceinline__ void polesum_dispatch(const PoleTabs& t, const PoleGeom& g, int param, const double* R,
+                                                 double* Z, double* Xb) {
+    if constexpr (LMAX > 0) block_polesum_reg<LMAX>(t, g, param, R, Z, Xb);
+    else block_polesum(t, g, param, R, Z, Xb);
+}
+
 // ---------------------------------------------------------------------------- kernels
+template <int LMAX>
 __global__ void k_precond(int ncols, const int* __restrict__ col_param, PoleGeom g, PoleTabs t,
                           const double* __restrict__ r, int ldr, double* __restrict__ z, int ldz) {
     extern __shared__ __align__(16) double sm[];
@@ -162,7 +284,7 @@ __global__ void k_precond(int ncols, const int* __restrict__ col_param, PoleGeom
     for (int i = threadIdx.x; i < 32 * L; i += blockDim.x)
         R[tpos(i, L)] = i < g.n ? r[(size_t)c * ldr + i] : 0.0;
     __syncthreads();
-    block_polesum(t, g, clamp_param(col_param[c], t.n_param), R, Z, Xb);
+    polesum_dispatch<LMAX>(t, g, clamp_param(col_param[c], t.n_param), R, Z, Xb);
     for (int i = threadIdx.x; i < g.n; i += blockDim.x) z[(size_t)c * ldz + i] = Z[tpos(i, L)];
 }
 
@@ -192,6 +314,7 @@ __device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_a
     }
 }
 
+template <int LMAX>
 __global__ void k_pcg_init(PcgState s, PoleGeom g, PoleTabs t, const double* __restrict__ b, int ldb) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
@@ -206,7 +329,7 @@ __global__ void k_pcg_init(PcgState s, PoleGeom g, PoleTabs t, const double* __r
     }
     __syncthreads();
     const int param = clamp_param(s.col_param[c], t.n_param);
-    block_polesum(t, g, param, R, Z, Xb);
+    polesum_dispatch<LMAX>(t, g, param, R, Z, Xb);
     double rz = 0.0, zz = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double zi = Z[tpos(i, L)];
@@ -238,6 +361,7 @@ __global__ void k_pcg_init(PcgState s, PoleGeom g, PoleTabs t, const double* __r
     }
 }
 
+template <int LMAX>
 __global__ void k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
@@ -279,7 +403,7 @@ __global__ void k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
             }
             __syncthreads();
             const int param = clamp_param(s.col_param[c], t.n_param);
-            block_polesum(t, g, param, R, Z, Xb);
+            polesum_dispatch<LMAX>(t, g, param, R, Z, Xb);
             double rz = 0.0, zz = 0.0;
             for (int i = threadIdx.x; i < n; i += blockDim.x) {
                 const double zi = Z[tpos(i, L)];
@@ -328,50 +452,84 @@ __global__ void k_check_params(int ncols, const int* col_param, int n_param, int
 }
 
 // ---------------------------------------------------------------------------- host side
+// Launch shape of the pole-sum kernels: register fast path (LMAX = L rounded up to a power of
+// two, L <= 32) with 4-8 warps, or the shared-memory path for longer chunks.
+static int lmax_of(int L) {
+    if (L <= 1) return 1;
+    if (L <= 2) return 2;
+    if (L <= 4) return 4;
+    if (L <= 8) return 8;
+    if (L <= 16) return 16;
+    if (L <= 32) return 32;
+    return 0;
+}
+
 int polesum_warps(int L) {
+    if (lmax_of(L) > 0) return L >= 32 ? 4 : 8;
     const size_t buf = (size_t)L * 33 * sizeof(double);
     const size_t budget = 200 * 1024;
     int w = (int)(budget / buf) - 2;
     return w < 1 ? 1 : (w > 8 ? 8 : w);
 }
 
-size_t polesum_smem(int L, int warps) { return (size_t)(2 + warps) * L * 33 * sizeof(double); }
+size_t polesum_smem(int L, int warps, int max_sys) {
+    size_t d = (size_t)(2 + warps) * L * 33;
+    if (lmax_of(L) > 0) d += (size_t)max_sys * 4 * L;
+    return d * sizeof(double);
+}
 
 template <typename K>
 static cudaError_t set_smem(K kern, size_t bytes) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+#define DD_LMAX_SWITCH(L, ...)                  \
+    switch (lmax_of(L)) {                        \
+        case 1: { constexpr int LM = 1; __VA_ARGS__; } break;   \
+        case 2: { constexpr int LM = 2; __VA_ARGS__; } break;   \
+        case 4: { constexpr int LM = 4; __VA_ARGS__; } break;   \
+        case 8: { constexpr int LM = 8; __VA_ARGS__; } break;   \
+        case 16: { constexpr int LM = 16; __VA_ARGS__; } break; \
+        case 32: { constexpr int LM = 32; __VA_ARGS__; } break; \
+        default: { constexpr int LM = 0; __VA_ARGS__; } break;  \
+    }
+
 cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b, int ldb,
                             cudaStream_t st) {
     if (s.ncols <= 0) return cudaSuccess;
     const int W = polesum_warps(g.L);
-    const size_t smem = polesum_smem(g.L, W);
-    cudaError_t e = set_smem(k_pcg_init, smem);
-    if (e != cudaSuccess) return e;
-    k_pcg_init<<<s.ncols, 32 * W, smem, st>>>(s, g, t, b, ldb);
-    return cudaGetLastError();
+    const size_t smem = polesum_smem(g.L, W, t.max_sys);
+    cudaError_t e = cudaSuccess;
+    DD_LMAX_SWITCH(g.L, {
+        e = set_smem(k_pcg_init<LM>, smem);
+        if (e == cudaSuccess) k_pcg_init<LM><<<s.ncols, 32 * W, smem, st>>>(s, g, t, b, ldb);
+    });
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st) {
     if (s.ncols <= 0) return cudaSuccess;
     const int W = polesum_warps(g.L);
-    const size_t smem = polesum_smem(g.L, W);
-    cudaError_t e = set_smem(k_pcg_iter, smem);
-    if (e != cudaSuccess) return e;
-    k_pcg_iter<<<s.ncols, 32 * W, smem, st>>>(s, g, t);
-    return cudaGetLastError();
+    const size_t smem = polesum_smem(g.L, W, t.max_sys);
+    cudaError_t e = cudaSuccess;
+    DD_LMAX_SWITCH(g.L, {
+        e = set_smem(k_pcg_iter<LM>, smem);
+        if (e == cudaSuccess) k_pcg_iter<LM><<<s.ncols, 32 * W, smem, st>>>(s, g, t);
+    });
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, const PoleTabs& t, const double* r,
                            int ldr, double* z, int ldz, cudaStream_t st) {
     if (ncols <= 0) return cudaSuccess;
     const int W = polesum_warps(g.L);
-    const size_t smem = polesum_smem(g.L, W);
-    cudaError_t e = set_smem(k_precond, smem);
-    if (e != cudaSuccess) return e;
-    k_precond<<<ncols, 32 * W, smem, st>>>(ncols, col_param, g, t, r, ldr, z, ldz);
-    return cudaGetLastError();
+    const size_t smem = polesum_smem(g.L, W, t.max_sys);
+    cudaError_t e = cudaSuccess;
+    DD_LMAX_SWITCH(g.L, {
+        e = set_smem(k_precond<LM>, smem);
+        if (e == cudaSuccess) k_precond<LM><<<ncols, 32 * W, smem, st>>>(ncols, col_param, g, t, r, ldr, z, ldz);
+    });
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_copy_cols(int n, int ncols, const double* src, int lds, double* dst, int ldd, cudaStream_t st) {

@@ -33,7 +33,8 @@ def _cols(B):
 
 # ------------------------------------------------------------------------- GEMM core
 @pytest.mark.parametrize("M,N,K,sk", [(64, 64, 16, 1), (100, 37, 70, 1), (199, 130, 400, 3), (1023, 256, 2046, 2),
-                                      (300, 5, 1000, 7)])
+                                      (300, 5, 1000, 7), (64, 64, 16, 0), (199, 130, 400, 0), (1023, 256, 2046, 0),
+                                      (2047, 100, 4094, 0), (300, 5, 1000, 0)])
 def test_dgemm_core(lib, M, N, K, sk):
     rng = np.random.default_rng(M + N + K)
     A = rng.standard_normal((M, K)); B = rng.standard_normal((N, K))
