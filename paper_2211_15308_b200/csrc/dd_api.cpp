@@ -152,10 +152,10 @@ struct SysTables {
 };
 
 static SysTables build_sys_tables(long double d, long double e, const PoleGeom& g) {
-    const int L = g.L, m = L - 1;
+    const int L = g.LL, m = L - 1, T = g.T, J = g.J;
     SysTables t;
     t.invb.assign(L, 0.0); t.cpr.assign(L, 0.0); t.uf.assign(L, 0.0); t.up.assign(L, 0.0);
-    t.pa.assign(160, 0.0); t.pb.assign(160, 0.0); t.pinvb.assign(32, 0.0);
+    t.pa.assign((size_t)J * T, 0.0); t.pb.assign((size_t)J * T, 0.0); t.pinvb.assign(T, 0.0);
     std::vector<long double> bp(L > 0 ? L : 1, 0.0L), ib(L > 0 ? L : 1, 0.0L);
     for (int i = 0; i < m; i++) {
         bp[i] = (i == 0) ? d : d - e * e / bp[i - 1];
@@ -174,32 +174,33 @@ static SysTables build_sys_tables(long double d, long double e, const PoleGeom& 
     };
     const std::vector<long double> uf = u_of(m), up = u_of(g.Lr_part);
     for (int i = 0; i < L; i++) { t.uf[i] = (double)uf[i]; t.up[i] = (double)up[i]; }
-    auto Lr = [&](int l) { return l < g.part_lane ? m : (l == g.part_lane ? g.Lr_part : 0); };
-    auto sep = [&](int l) { return l < g.part_lane; };
-    auto uu = [&](int l) -> const std::vector<long double>& { return l < g.part_lane ? uf : up; };
-    long double a[32], b[32], c[32];
-    for (int l = 0; l < 32; l++) {
-        a[l] = 0.0L; b[l] = 1.0L; c[l] = 0.0L;
+    auto Lr = [&](int l) { return l < g.part ? m : (l == g.part ? g.Lr_part : 0); };
+    auto sep = [&](int l) { return l < g.part; };
+    auto uu = [&](int l) -> const std::vector<long double>& { return l < g.part ? uf : up; };
+    // reduced (separator) system: row l couples g_{l-1}, g_l, g_{l+1}
+    std::vector<long double> a(T, 0.0L), b(T, 1.0L), c(T, 0.0L);
+    for (int l = 0; l < T; l++) {
         if (!sep(l)) continue;
         a[l] = (l == 0) ? 0.0L : (Lr(l) >= 1 ? -e * e * uu(l)[Lr(l) - 1] : e);
-        b[l] = d - (Lr(l) >= 1 ? e * e * uu(l)[0] : 0.0L) - ((l < 31 && Lr(l + 1) >= 1) ? e * e * uu(l + 1)[0] : 0.0L);
-        if (l < 31) c[l] = Lr(l + 1) >= 1 ? -e * e * uu(l + 1)[Lr(l + 1) - 1] : (sep(l + 1) ? e : 0.0L);
+        b[l] = d - (Lr(l) >= 1 ? e * e * uu(l)[0] : 0.0L) - ((l < T - 1 && Lr(l + 1) >= 1) ? e * e * uu(l + 1)[0] : 0.0L);
+        if (l < T - 1) c[l] = Lr(l + 1) >= 1 ? -e * e * uu(l + 1)[Lr(l + 1) - 1] : (sep(l + 1) ? e : 0.0L);
     }
-    for (int j = 0; j < 5; j++) {
+    // parallel cyclic reduction multipliers, step j has stride 2^j
+    for (int j = 0; j < J; j++) {
         const int s = 1 << j;
-        long double na[32], nb[32], nc[32];
-        for (int i = 0; i < 32; i++) {
+        std::vector<long double> na(T), nb(T), nc(T);
+        for (int i = 0; i < T; i++) {
             const long double al = (i - s >= 0) ? a[i] / b[i - s] : 0.0L;
-            const long double be = (i + s < 32) ? c[i] / b[i + s] : 0.0L;
-            t.pa[j * 32 + i] = (double)al;
-            t.pb[j * 32 + i] = (double)be;
+            const long double be = (i + s < T) ? c[i] / b[i + s] : 0.0L;
+            t.pa[(size_t)j * T + i] = (double)al;
+            t.pb[(size_t)j * T + i] = (double)be;
             na[i] = (i - s >= 0) ? -al * a[i - s] : 0.0L;
-            nc[i] = (i + s < 32) ? -be * c[i + s] : 0.0L;
-            nb[i] = b[i] - ((i - s >= 0) ? al * c[i - s] : 0.0L) - ((i + s < 32) ? be * a[i + s] : 0.0L);
+            nc[i] = (i + s < T) ? -be * c[i + s] : 0.0L;
+            nb[i] = b[i] - ((i - s >= 0) ? al * c[i - s] : 0.0L) - ((i + s < T) ? be * a[i + s] : 0.0L);
         }
-        for (int i = 0; i < 32; i++) { a[i] = na[i]; b[i] = nb[i]; c[i] = nc[i]; }
+        a.swap(na); b.swap(nb); c.swap(nc);
     }
-    for (int i = 0; i < 32; i++) t.pinvb[i] = (double)(1.0L / b[i]);
+    for (int i = 0; i < T; i++) t.pinvb[i] = (double)(1.0L / b[i]);
     return t;
 }
 
@@ -279,17 +280,17 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
 
     // --- pole tables: systems [M term if c0 != 0] + [poles with non-zero residue]
     PoleGeom& g = c->geom;
-    g.n = n;
-    g.L = (n + 1 + 31) / 32;
-    g.part_lane = n / g.L;
-    g.Lr_part = n - g.part_lane * g.L;
-    const int L = g.L;
+    g = make_pole_geom(n);
+    if (!pole_geom_supported(g)) return fail(DD_EUNSUPPORTED, "interface too large for the 1D pole-sum kernels");
+    const int L = g.LL;
+    const size_t JT = (size_t)g.J * g.T;
     const int max_sys = c->n_poles + 1;
     std::vector<int> nsys(c->n_param, 0);
     std::vector<double> w((size_t)c->n_param * max_sys, 0.0), dd((size_t)c->n_param * max_sys, 1.0),
         ee((size_t)c->n_param * max_sys, 0.0), invb((size_t)c->n_param * max_sys * L, 0.0),
         cpr(invb.size(), 0.0), uf(invb.size(), 0.0), up(invb.size(), 0.0),
-        pa((size_t)c->n_param * max_sys * 160, 0.0), pb(pa.size(), 0.0), pinvb((size_t)c->n_param * max_sys * 32, 0.0);
+        pa((size_t)c->n_param * max_sys * JT, 0.0), pb(pa.size(), 0.0),
+        pinvb((size_t)c->n_param * max_sys * g.T, 0.0);
     for (int pi = 0; pi < c->n_param; pi++) {
         std::vector<std::tuple<double, long double, long double>> sys;   // (weight, d, e)
         if (c0[pi] != 0.0) sys.emplace_back(c0[pi], 4.0L * h / 6.0L, h / 6.0L);
@@ -310,9 +311,9 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
             std::memcpy(&cpr[ps * L], t.cpr.data(), L * sizeof(double));
             std::memcpy(&uf[ps * L], t.uf.data(), L * sizeof(double));
             std::memcpy(&up[ps * L], t.up.data(), L * sizeof(double));
-            std::memcpy(&pa[ps * 160], t.pa.data(), 160 * sizeof(double));
-            std::memcpy(&pb[ps * 160], t.pb.data(), 160 * sizeof(double));
-            std::memcpy(&pinvb[ps * 32], t.pinvb.data(), 32 * sizeof(double));
+            std::memcpy(&pa[ps * JT], t.pa.data(), JT * sizeof(double));
+            std::memcpy(&pb[ps * JT], t.pb.data(), JT * sizeof(double));
+            std::memcpy(&pinvb[ps * g.T], t.pinvb.data(), g.T * sizeof(double));
         }
     }
     auto up_d = [&](const std::vector<double>& v, const double** dst) -> dd_status {
@@ -493,7 +494,7 @@ extern "C" dd_status dd_apply_precond(dd_ctx* c, int ncols, const int* colp, con
     if (ncols == 0) return DD_OK;
     if (!r || !z) return fail(DD_EINVAL, "r/z NULL");
     CK(cudaSetDevice(c->device));
-    c->last_ps_warps = polesum_warps(c->geom.L);
+    c->last_ps_warps = polesum_warps(c->geom);
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
     TIMED(DD_KCLASS_POLESUM, launch_precond(ncols, colp, c->geom, c->tabs, r, c->n, z, c->n, c->stream));
     return DD_OK;
@@ -518,7 +519,7 @@ static PcgState make_state(dd_ctx* c, int ncols, const int* colp, double* x, dou
 static dd_status iteration_body(dd_ctx* c, const PcgState& s) {
     dd_status st = schur_gemms(c, s.ncols, s.col_param, c->p, c->q, c->ldv);
     if (st != DD_OK) return st;
-    c->last_ps_warps = polesum_warps(c->geom.L);
+    c->last_ps_warps = polesum_warps(c->geom);
     TIMED(DD_KCLASS_POLESUM, launch_pcg_iter(s, c->geom, c->tabs, c->stream));
     return DD_OK;
 }
@@ -582,7 +583,7 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
     CK(cudaMemsetAsync(c->ints, 0, sizeof(int) * 8, c->stream));
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
     PcgState st = make_state(c, ncols, colp, x, rtol, maxit, norm_kind);
-    c->last_ps_warps = polesum_warps(c->geom.L);
+    c->last_ps_warps = polesum_warps(c->geom);
     TIMED(DD_KCLASS_OTHER, launch_pcg_init(st, c->geom, c->tabs, b, c->n, c->stream));
     c->last_graph = 0;
     if (maxit > 0) {

@@ -43,14 +43,18 @@ cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st);
 
 // ----------------------------------------------------------------------------- pole sum
 // 1D Γ: each shifted system (A_Γ - p M_Γ) (and M_Γ) is symmetric Toeplitz tridiagonal
-// (diag d, off-diagonal e).  The n rows (padded to 32 L) are split in 32 chunks of L rows, one
-// per lane: rows 0..L-2 of a chunk are its interior, row L-1 its separator.  Interiors are
-// solved by Thomas with precomputed factors, separators by PCR across the warp (shuffles).
+// (diag d, off-diagonal e).  The n rows (padded to T LL) are split in T = 32 G chunks of LL <= 32
+// rows, one per thread of a G-warp group: rows 0..LL-2 of a chunk are its interior, row LL-1 its
+// separator.  Interiors: Thomas with precomputed factors in registers; separators: PCR over the
+// group (shuffles for G = 1, shared memory for G > 1).
 struct PoleGeom {
     int n;          // rows (n_Γ)
-    int L;          // chunk length (rows per lane), 32 L >= n + 1
-    int part_lane;  // first lane whose separator row is >= n (padding): floor(n / L)
-    int Lr_part;    // real interior rows of that lane: n - part_lane * L   (0..L-1)
+    int LL;         // chunk length (rows per thread), T LL >= n + 1
+    int G;          // warps per system group (1, 2, 4, 8)
+    int T;          // separators = 32 G
+    int J;          // PCR steps = log2 T
+    int part;       // first thread whose separator row is >= n (padding): floor(n / LL)
+    int Lr_part;    // real interior rows of that thread: n - part * LL   (0..LL-1)
 };
 
 struct PoleTabs {
@@ -60,13 +64,13 @@ struct PoleTabs {
     const double* w;            // [n_param][max_sys]  weight (c0 or c_k)
     const double* d;            // [n_param][max_sys]  diagonal
     const double* e;            // [n_param][max_sys]  off-diagonal
-    const double* invb;         // [n_param][max_sys][L]  1 / Thomas pivot
-    const double* cpr;          // [n_param][max_sys][L]  e / Thomas pivot
-    const double* ufull;        // [n_param][max_sys][L]  T_{L-1}^-1 e_1
-    const double* upart;        // [n_param][max_sys][L]  T_{Lr_part}^-1 e_1
-    const double* pa;           // [n_param][max_sys][5][32] PCR multipliers (left)
-    const double* pb;           // [n_param][max_sys][5][32] PCR multipliers (right)
-    const double* pinvb;        // [n_param][max_sys][32]    final 1/b
+    const double* invb;         // [n_param][max_sys][LL]  1 / Thomas pivot
+    const double* cpr;          // [n_param][max_sys][LL]  e / Thomas pivot
+    const double* ufull;        // [n_param][max_sys][LL]  T_{LL-1}^-1 e_1
+    const double* upart;        // [n_param][max_sys][LL]  T_{Lr_part}^-1 e_1
+    const double* pa;           // [n_param][max_sys][J][T] PCR multipliers (left)
+    const double* pb;           // [n_param][max_sys][J][T] PCR multipliers (right)
+    const double* pinvb;        // [n_param][max_sys][T]    final 1/b
 };
 
 // PCG state for a batch of columns (device).
@@ -87,8 +91,11 @@ struct PcgState {
     unsigned long long cond_handle;    // cudaGraphConditionalHandle (0 = none)
 };
 
-int polesum_warps(int L);
-size_t polesum_smem(int L, int warps, int max_sys);
+PoleGeom make_pole_geom(int n);
+bool pole_geom_supported(const PoleGeom& g);
+int polesum_groups(const PoleGeom& g);
+int polesum_warps(const PoleGeom& g);
+size_t polesum_smem(const PoleGeom& g, int max_sys);
 cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b,
                             int ldb, cudaStream_t st);
 cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st);

@@ -2,182 +2,115 @@
 //
 // Preconditioner (Eq.(8)):
 //     z = c0 M_Γ^-1 r + Σ_k c_k (A_Γ - p_k M_Γ)^-1 r
-// 1D Γ: every system is symmetric Toeplitz tridiagonal (d, e) and SPD, strictly diagonally
-// dominant for p < 0 (no pivoting).  One CTA owns one column; its W warps each solve one
-// system per round with a chunked Thomas + warp-PCR scheme:
-//   lane l owns rows [lL, lL+L): interior rows lL..lL+L-2 and separator row lL+L-1;
-//   interiors: y = T^-1 r_int (Thomas, precomputed pivots), x_int = y - e g_{l-1} u - e g_l Ju;
-//   separators: 32-row reduced tridiagonal system solved by PCR over __shfl (precomputed
-//   multipliers, 5 steps).
-// Rows >= n are padding with x = 0 (equivalent to the Dirichlet end of Γ).
-// All per-column vectors live in shared memory in a transposed, padded layout
-// [row-in-chunk][lane] (stride 33) so both the per-lane sweeps and the coalesced global
-// loads are bank-conflict free.  Systems are summed in fixed order (round-major over warps)
-// and every dot product is a fixed-order tree: results are bitwise reproducible.
+// 1D Γ: every system is symmetric Toeplitz tridiagonal (d, e), SPD and diagonally dominant for
+// p < 0 (no pivoting).  Partitioned solve ("group" = G warps = T = 32G threads per system):
+//   thread τ owns rows [τ LL, (τ+1) LL): interior rows τLL .. τLL+LL-2, separator row τLL+LL-1;
+//   interiors, in registers:  y = T^-1 r_int by Thomas with precomputed pivots (fully unrolled,
+//   LL <= 32), then x_int = y - e g_{τ-1} u - e g_τ J u  (u = T^-1 e_1, precomputed);
+//   separators: the T-row reduced tridiagonal system by parallel cyclic reduction — warp
+//   shuffles when G = 1, a double-buffered shared-memory exchange with one named barrier per
+//   step when G > 1 (log2 T steps, precomputed multipliers).
+// Rows >= n are padding with x = 0 (the Dirichlet end of Γ).  The pivots, u and PCR multipliers
+// are computed on the host in long double (dd_api.cpp), so the fp64 sweeps keep ~1e-15 accuracy
+// even for the nearly singular pole closest to 0.
+// A CTA owns one column; its NG groups take systems k ≡ group (mod NG), accumulate their share of
+// the pole sum in registers, and the NG partial sums are combined in fixed group order:
+// bitwise reproducible.
 //
-// PCG: one fused kernel per iteration after the
-// two GEMMs: α = ρ/(p·q); x += αp; r -= αq; z = P r; ρ' = r·z; η test; β = ρ'/ρ; p = z + βp.
+// PCG: one fused kernel per iteration after the two
+// GEMMs: α = ρ/(p·q); x += αp; r -= αq; z = P r; ρ' = r·z; η test; β = ρ'/ρ; p = z + βp.
 #include "dd_internal.h"
 
 namespace dd {
 
-#define TI(i, l) ((i) * 33 + (l))
+// transposed, padded layout of a column in shared memory: [row-in-chunk i][thread τ], stride T+1
+__device__ __forceinline__ int tix(int i, int tau, int T) { return i * (T + 1) + tau; }
+__device__ __forceinline__ int clamp_param(int p, int n_param) { return p < 0 ? 0 : (p >= n_param ? n_param - 1 : p); }
 
-struct SysView {
-    double w, d, e;
-    const double *invb, *cpr, *ufull, *upart, *pa, *pb, *pinvb;
-};
-
-__device__ __forceinline__ SysView sys_view(const PoleTabs& t, int param, int k, int L) {
-    SysView v;
-    const size_t ps = (size_t)param * t.max_sys + k;
-    v.w = t.w[ps]; v.d = t.d[ps]; v.e = t.e[ps];
-    v.invb = t.invb + ps * L;
-    v.cpr = t.cpr + ps * L;
-    v.ufull = t.ufull + ps * L;
-    v.upart = t.upart + ps * L;
-    v.pa = t.pa + ps * 160;
-    v.pb = t.pb + ps * 160;
-    v.pinvb = t.pinvb + ps * 32;
-    return v;
+template <int G>
+__device__ __forceinline__ void group_sync(int group) {
+    if constexpr (G == 1) {
+        __syncwarp();
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(32 * G) : "memory");
+    }
 }
 
-// One warp solves (tridiag(e, d, e)) x = r for the column held in R (transposed layout) into X.
-__device__ void warp_tridiag_solve(const SysView& S, const PoleGeom& g, const double* __restrict__ R,
-                                   double* __restrict__ X, int lane) {
-    const int L = g.L;
-    const int Lr = lane < g.part_lane ? L - 1 : (lane == g.part_lane ? g.Lr_part : 0);
-    const bool sep_real = lane < g.part_lane;
-    const double* u = lane < g.part_lane ? S.ufull : S.upart;
-    const double e = S.e;
-
-    // forward elimination  ỹ_i = (r_i - e ỹ_{i-1}) / b'_i
-    double prev = 0.0;
-    for (int i = 0; i < Lr; i++) {
-        const double ib = __ldg(&S.invb[i]);
-        const double yt = R[TI(i, lane)] * ib - (e * ib) * prev;
-        X[TI(i, lane)] = yt;
-        prev = yt;
+// Value of `v` held by thread τ+d of the group (0 outside [0, T)).  G = 1: shuffles.
+template <int G>
+__device__ __forceinline__ double group_shift(double v, int d, int tau, double* xb, int group) {
+    constexpr int T = 32 * G;
+    if constexpr (G == 1) {
+        double r = d > 0 ? __shfl_down_sync(0xffffffffu, v, d) : __shfl_up_sync(0xffffffffu, v, -d);
+        const int src = tau + d;
+        return (src < 0 || src >= T) ? 0.0 : r;
+    } else {
+        xb[tau] = v;
+        group_sync<G>(group);
+        const int src = tau + d;
+        const double r = (src < 0 || src >= T) ? 0.0 : xb[src];
+        group_sync<G>(group);
+        return r;
     }
-    // back substitution  y_i = ỹ_i - (e / b'_i) y_{i+1}
-    double next = 0.0;
-    for (int i = Lr - 1; i >= 0; i--) {
-        const double y = X[TI(i, lane)] - __ldg(&S.cpr[i]) * next;
-        X[TI(i, lane)] = y;
-        next = y;
-    }
-    const double y_first = Lr > 0 ? X[TI(0, lane)] : 0.0;
-    const double y_last = Lr > 0 ? X[TI(Lr - 1, lane)] : 0.0;
-    const double y_first_next = __shfl_down_sync(0xffffffffu, y_first, 1);
-    const int Lr_next = (lane + 1) < g.part_lane ? L - 1 : ((lane + 1) == g.part_lane ? g.Lr_part : 0);
-
-    // reduced right-hand side at this lane's separator
-    double rs = 0.0;
-    if (sep_real) {
-        rs = R[TI(L - 1, lane)];
-        if (Lr > 0) rs -= e * y_last;
-        if (lane < 31 && Lr_next > 0) rs -= e * y_first_next;
-    }
-    // PCR over the 32 separators (precomputed multipliers)
-#pragma unroll
-    for (int j = 0; j < 5; j++) {
-        const int s = 1 << j;
-        double rm = __shfl_up_sync(0xffffffffu, rs, s);
-        double rp = __shfl_down_sync(0xffffffffu, rs, s);
-        if (lane < s) rm = 0.0;
-        if (lane + s > 31) rp = 0.0;
-        rs = rs - __ldg(&S.pa[j * 32 + lane]) * rm - __ldg(&S.pb[j * 32 + lane]) * rp;
-    }
-    const double gsep = sep_real ? rs * __ldg(&S.pinvb[lane]) : 0.0;
-    double gleft = __shfl_up_sync(0xffffffffu, gsep, 1);
-    if (lane == 0) gleft = 0.0;
-
-    // interior reconstruction
-    const double eg0 = e * gleft, eg1 = e * gsep;
-    for (int i = 0; i < Lr; i++) {
-        X[TI(i, lane)] = X[TI(i, lane)] - eg0 * __ldg(&u[i]) - eg1 * __ldg(&u[Lr - 1 - i]);
-    }
-    for (int i = Lr; i < L - 1; i++) X[TI(i, lane)] = 0.0;
-    X[TI(L - 1, lane)] = gsep;
 }
 
-// z = P r for the CTA's column: R (input, transposed) -> Z (output, transposed).  Xb: W buffers.
+// z = P r for the CTA's column.  R: input (transposed), Z: output (transposed, written by every
+// thread for its own chunk after the fixed-order combine).  sm: scratch.
+template <int LMAX, int G, int NG>
 __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, const double* R, double* Z,
-                              double* Xb) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int W = blockDim.x >> 5;
-    const int L = g.L;
-    const int tot = L * 33;
+                              double* scratch) {
+    constexpr int T = 32 * G;
+    const int LL = g.LL;
+    const int tot = LL * (T + 1);
+    const int tid = threadIdx.x;
+    const int group = tid / T, tau = tid % T;
     const int nsys = t.nsys[param];
-    for (int i = threadIdx.x; i < tot; i += blockDim.x) Z[i] = 0.0;
-    for (int r0 = 0; r0 < nsys; r0 += W) {
-        const int k = r0 + warp;
-        if (k < nsys) {
-            SysView S = sys_view(t, param, k, L);
-            warp_tridiag_solve(S, g, R, Xb + (size_t)warp * tot, lane);
-        }
-        __syncthreads();
-        const int nw = min(W, nsys - r0);
-        for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-            if ((i % 33) == 32) continue;
-            double acc = Z[i];
-            for (int w = 0; w < nw; w++) acc += t.w[(size_t)param * t.max_sys + r0 + w] * Xb[(size_t)w * tot + i];
-            Z[i] = acc;
-        }
-        __syncthreads();
-    }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Register-resident fast path for chunk length L <= LMAX <= 32 (n_Γ <= 1023).
-// Every lane keeps its chunk (y) and its share of the pole sum (z) in registers; sweeps are fully
-// unrolled so the table loads (shared memory, broadcast) are hoisted off the FMA chain.  Warp w
-// accumulates systems k = w, w+W, ... in registers; the W partial sums are combined in fixed
-// warp order at the end (deterministic).  Tables of all systems are staged in shared memory
-// once per CTA: [k][invb | cpr | ufull | upart] x L.
-template <int LMAX>
-__device__ void block_polesum_reg(const PoleTabs& t, const PoleGeom& g, int param, const double* R, double* Z,
-                                  double* scratch) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int W = blockDim.x >> 5;
-    const int L = g.L;
-    const int tot = L * 33;
-    const int nsys = t.nsys[param];
-    double* Zw = scratch;                          // [W][tot]
-    double* tab = scratch + (size_t)W * tot;       // [nsys][4][L]
     const size_t pbase = (size_t)param * t.max_sys;
-    for (int idx = threadIdx.x; idx < nsys * 4 * L; idx += blockDim.x) {
-        const int k = idx / (4 * L), rem = idx - k * 4 * L, which = rem / L, i = rem - which * L;
-        const double* src = which == 0 ? t.invb : (which == 1 ? t.cpr : (which == 2 ? t.ufull : t.upart));
-        tab[idx] = src[(pbase + k) * L + i];
+    double* tab = scratch;                                     // [nsys][4][LL]
+    double* xbuf = scratch + (size_t)t.max_sys * 4 * LL;       // [NG][2][T] PCR exchange (G > 1)
+    double* Zw = xbuf + 2 * NG * T;                            // [NG - 1][tot] partial sums of groups 1..NG-1
+
+    // stage the interior tables of this parameter set's systems (coalesced, unrolled)
+    {
+        const int tot_tab = nsys * 4 * LL;
+        for (int idx = tid; idx < tot_tab; idx += blockDim.x) {
+            const int k = idx / (4 * LL), rem = idx - k * 4 * LL, which = rem / LL, i = rem - which * LL;
+            const double* src = which == 0 ? t.invb : (which == 1 ? t.cpr : (which == 2 ? t.ufull : t.upart));
+            tab[idx] = __ldg(&src[(pbase + k) * LL + i]);
+        }
     }
     __syncthreads();
 
-    const int Lr = lane < g.part_lane ? L - 1 : (lane == g.part_lane ? g.Lr_part : 0);
-    const int Lr_next = (lane + 1) < g.part_lane ? L - 1 : ((lane + 1) == g.part_lane ? g.Lr_part : 0);
-    const bool sep_real = lane < g.part_lane;
+    const int Lr = tau < g.part ? LL - 1 : (tau == g.part ? g.Lr_part : 0);
+    const int Lr_next = (tau + 1) < g.part ? LL - 1 : ((tau + 1) == g.part ? g.Lr_part : 0);
+    const bool sep_real = tau < g.part;
+    double* xb = xbuf + (size_t)group * 2 * T;
     double z[LMAX];
 #pragma unroll
     for (int i = 0; i < LMAX; i++) z[i] = 0.0;
 
-    for (int k = warp; k < nsys; k += W) {
-        const double* ib = tab + (size_t)k * 4 * L;
-        const double* cp = ib + L;
-        const double* u = lane < g.part_lane ? ib + 2 * L : ib + 3 * L;
-        const double e = t.e[pbase + k], wk = t.w[pbase + k];
-        const double* pa = t.pa + (pbase + k) * 160;
-        const double* pb = t.pb + (pbase + k) * 160;
-        double pav[5], pbv[5];
+    for (int k = group; k < nsys; k += NG) {
+        const double* ib = tab + (size_t)k * 4 * LL;
+        const double* cp = ib + LL;
+        const double* u = tau < g.part ? ib + 2 * LL : ib + 3 * LL;
+        const double e = __ldg(&t.e[pbase + k]), wk = __ldg(&t.w[pbase + k]);
+        const double* pa = t.pa + (pbase + k) * (size_t)g.J * T;
+        const double* pb = t.pb + (pbase + k) * (size_t)g.J * T;
+        double pav[8], pbv[8];
 #pragma unroll
-        for (int j = 0; j < 5; j++) { pav[j] = __ldg(&pa[j * 32 + lane]); pbv[j] = __ldg(&pb[j * 32 + lane]); }
-        const double pinv = __ldg(&t.pinvb[(pbase + k) * 32 + lane]);
-        double y[LMAX];
+        for (int j = 0; j < 8; j++) {
+            pav[j] = j < g.J ? __ldg(&pa[j * T + tau]) : 0.0;
+            pbv[j] = j < g.J ? __ldg(&pb[j * T + tau]) : 0.0;
+        }
+        const double pinv = __ldg(&t.pinvb[(pbase + k) * T + tau]);
+
         // forward:  ỹ_i = r_i/b'_i - (e/b'_i) ỹ_{i-1}
-        double prev = 0.0, y_last = 0.0;   // y_last = ỹ_{Lr-1} = y_{Lr-1} (untouched by the back sweep)
+        double y[LMAX];
+        double prev = 0.0, y_last = 0.0;
 #pragma unroll
         for (int i = 0; i < LMAX; i++) {
-            if (i < L - 1) {
-                const double v = fma(-cp[i], prev, R[TI(i, lane)] * ib[i]);
+            if (i < LL - 1) {
+                const double v = fma(-cp[i], prev, R[tix(i, tau, T)] * ib[i]);
                 y[i] = i < Lr ? v : 0.0;
                 if (i < Lr) y_last = v;
                 prev = y[i];
@@ -189,55 +122,82 @@ __device__ void block_polesum_reg(const PoleTabs& t, const PoleGeom& g, int para
         double next = 0.0;
 #pragma unroll
         for (int i = LMAX - 1; i >= 0; i--) {
-            if (i < L - 1) {
+            if (i < LL - 1) {
                 y[i] = fma(-cp[i], next, y[i]);
                 next = y[i];
             }
         }
-        double y_first = y[0];
-        if (Lr == 0) y_first = 0.0;
-        const double y_first_next = __shfl_down_sync(0xffffffffu, y_first, 1);
+        const double y_first = Lr > 0 ? y[0] : 0.0;
+        const double y_first_next = group_shift<G>(y_first, 1, tau, xb, group);
         double rs = 0.0;
         if (sep_real) {
-            rs = R[TI(L - 1, lane)];
+            rs = R[tix(LL - 1, tau, T)];
             if (Lr > 0) rs -= e * y_last;
-            if (lane < 31 && Lr_next > 0) rs -= e * y_first_next;
+            if (tau < T - 1 && Lr_next > 0) rs -= e * y_first_next;
         }
+        // parallel cyclic reduction over the T separators
+        if constexpr (G == 1) {
 #pragma unroll
-        for (int j = 0; j < 5; j++) {
-            const int s = 1 << j;
-            double rm = __shfl_up_sync(0xffffffffu, rs, s);
-            double rp = __shfl_down_sync(0xffffffffu, rs, s);
-            if (lane < s) rm = 0.0;
-            if (lane + s > 31) rp = 0.0;
-            rs = rs - pav[j] * rm - pbv[j] * rp;
+            for (int j = 0; j < 5; j++) {
+                const int s = 1 << j;
+                double rm = __shfl_up_sync(0xffffffffu, rs, s);
+                double rp = __shfl_down_sync(0xffffffffu, rs, s);
+                if (tau < s) rm = 0.0;
+                if (tau + s > T - 1) rp = 0.0;
+                rs = rs - pav[j] * rm - pbv[j] * rp;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                if (j < g.J) {
+                    const int s = 1 << j;
+                    double* buf = xb + (j & 1) * T;
+                    buf[tau] = rs;
+                    group_sync<G>(group);
+                    const double rm = (tau >= s) ? buf[tau - s] : 0.0;
+                    const double rp = (tau + s < T) ? buf[tau + s] : 0.0;
+                    rs = rs - pav[j] * rm - pbv[j] * rp;
+                }
+            }
+            group_sync<G>(group);
         }
         const double gsep = sep_real ? rs * pinv : 0.0;
-        double gleft = __shfl_up_sync(0xffffffffu, gsep, 1);
-        if (lane == 0) gleft = 0.0;
+        const double gleft = group_shift<G>(gsep, -1, tau, xb, group);
         const double eg0 = e * gleft, eg1 = e * gsep;
 #pragma unroll
         for (int i = 0; i < LMAX; i++) {
-            if (i < L - 1 && i < Lr) {
+            if (i < LL - 1 && i < Lr) {
                 const double x = y[i] - eg0 * u[i] - eg1 * u[Lr - 1 - i];
                 z[i] = fma(wk, x, z[i]);
             }
         }
-        // separator row (in-chunk index L-1)
 #pragma unroll
         for (int i = 0; i < LMAX; i++)
-            if (i == L - 1) z[i] = fma(wk, gsep, z[i]);
+            if (i == LL - 1) z[i] = fma(wk, gsep, z[i]);
     }
-    // fixed-order combine of the W warp partials
+
+    // fixed-order combine of the NG group partials: Z = z_0 + z_1 + ... + z_{NG-1}
+    if constexpr (NG > 1) {
+        if (group > 0) {
 #pragma unroll
-    for (int i = 0; i < LMAX; i++)
-        if (i < L) Zw[(size_t)warp * tot + TI(i, lane)] = z[i];
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-        if ((idx % 33) == 32) continue;
-        double acc = 0.0;
-        for (int w = 0; w < W; w++) acc += Zw[(size_t)w * tot + idx];
-        Z[idx] = acc;
+            for (int i = 0; i < LMAX; i++)
+                if (i < LL) Zw[(size_t)(group - 1) * tot + tix(i, tau, T)] = z[i];
+        }
+        __syncthreads();
+        if (group == 0) {
+#pragma unroll
+            for (int i = 0; i < LMAX; i++) {
+                if (i < LL) {
+                    double acc = z[i];
+                    for (int gg = 1; gg < NG; gg++) acc += Zw[(size_t)(gg - 1) * tot + tix(i, tau, T)];
+                    Z[tix(i, tau, T)] = acc;
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < LMAX; i++)
+            if (i < LL) Z[tix(i, tau, T)] = z[i];
     }
     __syncthreads();
 }
@@ -260,32 +220,31 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
     __syncthreads();
 }
 
-__device__ __forceinline__ int clamp_param(int p, int n_param) { return p < 0 ? 0 : (p >= n_param ? n_param - 1 : p); }
+// smem index of natural row ρ of the column
+__device__ __forceinline__ int tpos(int row, const PoleGeom& g) { return tix(row % g.LL, row / g.LL, g.T); }
 
-// rows of the column in natural order <-> transposed smem index
-__device__ __forceinline__ int tpos(int row, int L) { return TI(row % L, row / L); }
-
-template <int LMAX>
-__device__ __forceinline__ void polesum_dispatch(const PoleTabs& t, const PoleGeom& g, int param, const double* R,
-                                                 double* Z, double* Xb) {
-    if constexpr (LMAX > 0) block_polesum_reg<LMAX>(t, g, param, R, Z, Xb);
-    else block_polesum(t, g, param, R, Z, Xb);
+struct Smem {
+    double *R, *Z, *scratch;
+};
+__device__ __forceinline__ Smem carve(double* sm, const PoleGeom& g) {
+    const int tot = g.LL * (g.T + 1);
+    return Smem{sm, sm + tot, sm + 2 * tot};
 }
 
 // ---------------------------------------------------------------------------- kernels
-template <int LMAX>
-__global__ void k_precond(int ncols, const int* __restrict__ col_param, PoleGeom g, PoleTabs t,
-                          const double* __restrict__ r, int ldr, double* __restrict__ z, int ldz) {
+template <int LMAX, int G, int NG>
+__global__ void __launch_bounds__(32 * G * NG) k_precond(int ncols, const int* __restrict__ col_param, PoleGeom g,
+                                                         PoleTabs t, const double* __restrict__ r, int ldr,
+                                                         double* __restrict__ z, int ldz) {
     extern __shared__ __align__(16) double sm[];
     const int c = blockIdx.x;
     if (c >= ncols) return;
-    const int L = g.L, tot = L * 33;
-    double* R = sm; double* Z = sm + tot; double* Xb = sm + 2 * tot;
-    for (int i = threadIdx.x; i < 32 * L; i += blockDim.x)
-        R[tpos(i, L)] = i < g.n ? r[(size_t)c * ldr + i] : 0.0;
+    Smem S = carve(sm, g);
+    const int npad = g.T * g.LL;
+    for (int i = threadIdx.x; i < npad; i += blockDim.x) S.R[tpos(i, g)] = i < g.n ? r[(size_t)c * ldr + i] : 0.0;
     __syncthreads();
-    polesum_dispatch<LMAX>(t, g, clamp_param(col_param[c], t.n_param), R, Z, Xb);
-    for (int i = threadIdx.x; i < g.n; i += blockDim.x) z[(size_t)c * ldz + i] = Z[tpos(i, L)];
+    block_polesum<LMAX, G, NG>(t, g, clamp_param(col_param[c], t.n_param), S.R, S.Z, S.scratch);
+    for (int i = threadIdx.x; i < g.n; i += blockDim.x) z[(size_t)c * ldz + i] = S.Z[tpos(i, g)];
 }
 
 __device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_active) {
@@ -314,26 +273,26 @@ __device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_a
     }
 }
 
-template <int LMAX>
-__global__ void k_pcg_init(PcgState s, PoleGeom g, PoleTabs t, const double* __restrict__ b, int ldb) {
+template <int LMAX, int G, int NG>
+__global__ void __launch_bounds__(32 * G * NG) k_pcg_init(PcgState s, PoleGeom g, PoleTabs t,
+                                                          const double* __restrict__ b, int ldb) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
     const int c = blockIdx.x;
-    const int L = g.L, tot = L * 33, n = g.n;
-    double* R = sm; double* Z = sm + tot; double* Xb = sm + 2 * tot;
+    const int n = g.n, npad = g.T * g.LL;
+    Smem S = carve(sm, g);
     const size_t off = (size_t)c * s.ldv;
-    for (int i = threadIdx.x; i < 32 * L; i += blockDim.x) {
+    for (int i = threadIdx.x; i < npad; i += blockDim.x) {
         const double v = i < n ? b[(size_t)c * ldb + i] : 0.0;
-        R[tpos(i, L)] = v;
+        S.R[tpos(i, g)] = v;
         if (i < n) { s.r[off + i] = v; s.x[(size_t)c * s.ldx + i] = 0.0; }
     }
     __syncthreads();
-    const int param = clamp_param(s.col_param[c], t.n_param);
-    polesum_dispatch<LMAX>(t, g, param, R, Z, Xb);
+    block_polesum<LMAX, G, NG>(t, g, clamp_param(s.col_param[c], t.n_param), S.R, S.Z, S.scratch);
     double rz = 0.0, zz = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const double zi = Z[tpos(i, L)];
-        rz += R[tpos(i, L)] * zi;
+        const double zi = S.Z[tpos(i, g)];
+        rz += S.R[tpos(i, g)] * zi;
         zz += zi * zi;
         s.p[off + i] = zi;
     }
@@ -361,28 +320,39 @@ __global__ void k_pcg_init(PcgState s, PoleGeom g, PoleTabs t, const double* __r
     }
 }
 
-template <int LMAX>
-__global__ void k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
+// rows of thread tid: ρ = tid + j NT, j < RPT (coalesced); RPT = ceil(T LL / NT) <= ceil(LMAX / NG)
+template <int LMAX, int G, int NG>
+__global__ void __launch_bounds__(32 * G * NG) k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
+    constexpr int NT = 32 * G * NG;
+    constexpr int RPT = (LMAX + NG - 1) / NG;
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
-    __shared__ double s_alpha;
     __shared__ int s_work;
     const int c = blockIdx.x;
-    const int L = g.L, tot = L * 33, n = g.n;
-    double* R = sm; double* Z = sm + tot; double* Xb = sm + 2 * tot;
+    const int n = g.n;
+    Smem S = carve(sm, g);
     const size_t off = (size_t)c * s.ldv;
+    const size_t offx = (size_t)c * s.ldx;
     if (threadIdx.x == 0) s_work = s.active[c];
     __syncthreads();
     bool still = false;
     if (s_work) {
         const int k = *s.kiter + 1;
-        // π = p·q
+        // one pass over p, q, x, r: all loads in flight together
+        double pv[RPT], qv[RPT], xv[RPT], rv[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; j++) {
+            const int i = threadIdx.x + j * NT;
+            const bool ok = i < n;
+            pv[j] = ok ? s.p[off + i] : 0.0;
+            qv[j] = ok ? s.q[off + i] : 0.0;
+            xv[j] = ok ? s.x[offx + i] : 0.0;
+            rv[j] = ok ? s.r[off + i] : 0.0;
+        }
         double pq = 0.0, dummy = 0.0;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) pq += s.p[off + i] * s.q[off + i];
+#pragma unroll
+        for (int j = 0; j < RPT; j++) pq = fma(pv[j], qv[j], pq);
         block_sum2(pq, dummy, red);
-        if (threadIdx.x == 0) s_alpha = pq > 0.0 ? s.rho[c] / pq : 0.0;
-        __syncthreads();
-        const double alpha = s_alpha;
         if (!(pq > 0.0)) {
             if (threadIdx.x == 0) {
                 atomicExch(s.status, (int)DD_ENOTSPD);
@@ -390,25 +360,34 @@ __global__ void k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
                 s.iters[c] = k;
             }
         } else {
-            // x += α p ; r -= α q
-            for (int i = threadIdx.x; i < 32 * L; i += blockDim.x) {
-                double ri = 0.0;
+            const double alpha = s.rho[c] / pq;
+#pragma unroll
+            for (int j = 0; j < RPT; j++) {
+                const int i = threadIdx.x + j * NT;
                 if (i < n) {
-                    const double pi = s.p[off + i];
-                    s.x[(size_t)c * s.ldx + i] += alpha * pi;
-                    ri = s.r[off + i] - alpha * s.q[off + i];
+                    s.x[offx + i] = fma(alpha, pv[j], xv[j]);
+                    const double ri = fma(-alpha, qv[j], rv[j]);
                     s.r[off + i] = ri;
+                    S.R[tpos(i, g)] = ri;
+                } else if (i < g.T * g.LL) {
+                    S.R[tpos(i, g)] = 0.0;
                 }
-                R[tpos(i, L)] = ri;
             }
+            for (int i = threadIdx.x + RPT * NT; i < g.T * g.LL; i += NT) S.R[tpos(i, g)] = 0.0;
             __syncthreads();
-            const int param = clamp_param(s.col_param[c], t.n_param);
-            polesum_dispatch<LMAX>(t, g, param, R, Z, Xb);
+            block_polesum<LMAX, G, NG>(t, g, clamp_param(s.col_param[c], t.n_param), S.R, S.Z, S.scratch);
             double rz = 0.0, zz = 0.0;
-            for (int i = threadIdx.x; i < n; i += blockDim.x) {
-                const double zi = Z[tpos(i, L)];
-                rz += R[tpos(i, L)] * zi;
-                zz += zi * zi;
+            double zv[RPT];
+#pragma unroll
+            for (int j = 0; j < RPT; j++) {
+                const int i = threadIdx.x + j * NT;
+                zv[j] = 0.0;
+                if (i < n) {
+                    const int ps = tpos(i, g);
+                    zv[j] = S.Z[ps];
+                    rz = fma(S.R[ps], zv[j], rz);
+                    zz = fma(zv[j], zv[j], zz);
+                }
             }
             block_sum2(rz, zz, red);
             const double eta = s.norm_kind == 0 ? sqrt(fmax(rz, 0.0)) : sqrt(zz);
@@ -424,8 +403,17 @@ __global__ void k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
                 if (threadIdx.x == 0) s.active[c] = 0;
             } else {
                 const double beta = rz / s.rho[c];
-                for (int i = threadIdx.x; i < n; i += blockDim.x)
-                    s.p[off + i] = Z[tpos(i, L)] + beta * s.p[off + i];
+                double pn[RPT];
+#pragma unroll
+                for (int j = 0; j < RPT; j++) {
+                    const int i = threadIdx.x + j * NT;
+                    pn[j] = i < n ? s.p[off + i] : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < RPT; j++) {
+                    const int i = threadIdx.x + j * NT;
+                    if (i < n) s.p[off + i] = fma(beta, pn[j], zv[j]);
+                }
                 __syncthreads();
                 if (threadIdx.x == 0) s.rho[c] = rz;
                 still = true;
@@ -452,29 +440,45 @@ __global__ void k_check_params(int ncols, const int* col_param, int n_param, int
 }
 
 // ---------------------------------------------------------------------------- host side
-// Launch shape of the pole-sum kernels: register fast path (LMAX = L rounded up to a power of
-// two, L <= 32) with 4-8 warps, or the shared-memory path for longer chunks.
+PoleGeom make_pole_geom(int n) {
+    PoleGeom g{};
+    g.n = n;
+    int G = 1;
+    while (32 * G * 32 < n + 1 && G < 8) G *= 2;
+    g.G = G;
+    g.T = 32 * G;
+    g.J = 0;
+    while ((1 << g.J) < g.T) g.J++;
+    g.LL = (n + 1 + g.T - 1) / g.T;
+    g.part = n / g.LL;
+    g.Lr_part = n - g.part * g.LL;
+    return g;
+}
+
+bool pole_geom_supported(const PoleGeom& g) { return g.LL <= 32; }
+
 static int lmax_of(int L) {
-    if (L <= 1) return 1;
-    if (L <= 2) return 2;
-    if (L <= 4) return 4;
-    if (L <= 8) return 8;
-    if (L <= 16) return 16;
-    if (L <= 32) return 32;
-    return 0;
+    int m = 1;
+    while (m < L) m *= 2;
+    return m;
 }
 
-int polesum_warps(int L) {
-    if (lmax_of(L) > 0) return L >= 32 ? 4 : 8;
-    const size_t buf = (size_t)L * 33 * sizeof(double);
-    const size_t budget = 200 * 1024;
-    int w = (int)(budget / buf) - 2;
-    return w < 1 ? 1 : (w > 8 ? 8 : w);
+int polesum_groups(const PoleGeom& g) {
+    if (g.G >= 8) return 1;
+    if (g.G == 4) return 2;
+    if (g.G == 2) return 4;
+    return lmax_of(g.LL) >= 16 ? 4 : 8;
 }
 
-size_t polesum_smem(int L, int warps, int max_sys) {
-    size_t d = (size_t)(2 + warps) * L * 33;
-    if (lmax_of(L) > 0) d += (size_t)max_sys * 4 * L;
+int polesum_warps(const PoleGeom& g) { return g.G * polesum_groups(g); }
+
+size_t polesum_smem(const PoleGeom& g, int max_sys) {
+    const int NG = polesum_groups(g);
+    const size_t tot = (size_t)g.LL * (g.T + 1);
+    size_t d = 2 * tot                          // R, Z
+               + (size_t)max_sys * 4 * g.LL     // tables
+               + 2 * (size_t)NG * g.T           // PCR exchange
+               + (size_t)(NG - 1) * tot;        // group partials
     return d * sizeof(double);
 }
 
@@ -483,38 +487,40 @@ static cudaError_t set_smem(K kern, size_t bytes) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-#define DD_LMAX_SWITCH(L, ...)                  \
-    switch (lmax_of(L)) {                        \
-        case 1: { constexpr int LM = 1; __VA_ARGS__; } break;   \
-        case 2: { constexpr int LM = 2; __VA_ARGS__; } break;   \
-        case 4: { constexpr int LM = 4; __VA_ARGS__; } break;   \
-        case 8: { constexpr int LM = 8; __VA_ARGS__; } break;   \
-        case 16: { constexpr int LM = 16; __VA_ARGS__; } break; \
-        case 32: { constexpr int LM = 32; __VA_ARGS__; } break; \
-        default: { constexpr int LM = 0; __VA_ARGS__; } break;  \
-    }
+// Instantiated shapes (LMAX, G, NG): n <= 1023 with G = 1, and LL = 32 chunks with G = 2, 4, 8.
+#define DD_POLE_SWITCH(g, ...)                                                                   \
+    do {                                                                                         \
+        const int _lm = lmax_of((g).LL), _G = (g).G;                                             \
+        if (_G == 1 && _lm == 1) { constexpr int LM = 1, GG = 1, NGG = 8; __VA_ARGS__; }         \
+        else if (_G == 1 && _lm == 2) { constexpr int LM = 2, GG = 1, NGG = 8; __VA_ARGS__; }    \
+        else if (_G == 1 && _lm == 4) { constexpr int LM = 4, GG = 1, NGG = 8; __VA_ARGS__; }    \
+        else if (_G == 1 && _lm == 8) { constexpr int LM = 8, GG = 1, NGG = 8; __VA_ARGS__; }    \
+        else if (_G == 1 && _lm == 16) { constexpr int LM = 16, GG = 1, NGG = 4; __VA_ARGS__; }  \
+        else if (_G == 1) { constexpr int LM = 32, GG = 1, NGG = 4; __VA_ARGS__; }               \
+        else if (_G == 2) { constexpr int LM = 32, GG = 2, NGG = 4; __VA_ARGS__; }               \
+        else if (_G == 4) { constexpr int LM = 32, GG = 4, NGG = 2; __VA_ARGS__; }               \
+        else { constexpr int LM = 32, GG = 8, NGG = 1; __VA_ARGS__; }                            \
+    } while (0)
 
 cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b, int ldb,
                             cudaStream_t st) {
     if (s.ncols <= 0) return cudaSuccess;
-    const int W = polesum_warps(g.L);
-    const size_t smem = polesum_smem(g.L, W, t.max_sys);
+    const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
-    DD_LMAX_SWITCH(g.L, {
-        e = set_smem(k_pcg_init<LM>, smem);
-        if (e == cudaSuccess) k_pcg_init<LM><<<s.ncols, 32 * W, smem, st>>>(s, g, t, b, ldb);
+    DD_POLE_SWITCH(g, {
+        e = set_smem(k_pcg_init<LM, GG, NGG>, smem);
+        if (e == cudaSuccess) k_pcg_init<LM, GG, NGG><<<s.ncols, 32 * GG * NGG, smem, st>>>(s, g, t, b, ldb);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st) {
     if (s.ncols <= 0) return cudaSuccess;
-    const int W = polesum_warps(g.L);
-    const size_t smem = polesum_smem(g.L, W, t.max_sys);
+    const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
-    DD_LMAX_SWITCH(g.L, {
-        e = set_smem(k_pcg_iter<LM>, smem);
-        if (e == cudaSuccess) k_pcg_iter<LM><<<s.ncols, 32 * W, smem, st>>>(s, g, t);
+    DD_POLE_SWITCH(g, {
+        e = set_smem(k_pcg_iter<LM, GG, NGG>, smem);
+        if (e == cudaSuccess) k_pcg_iter<LM, GG, NGG><<<s.ncols, 32 * GG * NGG, smem, st>>>(s, g, t);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -522,12 +528,12 @@ cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs
 cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, const PoleTabs& t, const double* r,
                            int ldr, double* z, int ldz, cudaStream_t st) {
     if (ncols <= 0) return cudaSuccess;
-    const int W = polesum_warps(g.L);
-    const size_t smem = polesum_smem(g.L, W, t.max_sys);
+    const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
-    DD_LMAX_SWITCH(g.L, {
-        e = set_smem(k_precond<LM>, smem);
-        if (e == cudaSuccess) k_precond<LM><<<ncols, 32 * W, smem, st>>>(ncols, col_param, g, t, r, ldr, z, ldz);
+    DD_POLE_SWITCH(g, {
+        e = set_smem(k_precond<LM, GG, NGG>, smem);
+        if (e == cudaSuccess)
+            k_precond<LM, GG, NGG><<<ncols, 32 * GG * NGG, smem, st>>>(ncols, col_param, g, t, r, ldr, z, ldz);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
 }

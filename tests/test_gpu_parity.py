@@ -168,6 +168,39 @@ def test_profile_and_launch_counts(lib):
         S.close()
 
 
+# ------------------------------------------------------------------------- ragged large sizes (G = 2, 4 groups)
+@pytest.mark.parametrize("N,C", [(1500, 13), (3001, 7), (2049, 3)])
+def test_ragged_large_parity(lib, N, C):
+    """Interfaces whose chunking uses 2- and 4-warp groups with a partial last chunk, and column
+    counts that leave ragged GEMM tiles; against the oracle's mode tier."""
+    params = [(1.0, 1e2), (1e-3, 1e5)]
+    ras = fit_all(N, params, 18)
+    Mo = oprob.ModeProblem2D(N)
+    rng = np.random.default_rng(N)
+    B = rng.uniform(-1, 1, (C, N - 1))
+    colp = np.arange(C) % 2
+    S = _solver(lib, N, params, ras, max_cols=C)
+    try:
+        y = S.apply_schur(_cols(B), colp).cpu().numpy()
+        z = S.apply_precond(_cols(B), colp).cpu().numpy()
+        ref_y = np.stack([Mo.apply_S(*params[colp[c]], B[c]) for c in range(C)])
+        ra = lambda c: ras[colp[c]]
+        zb = np.stack([Mo.apply_P_ra(ra(c).c0, ra(c).poles, ra(c).residues, B[c]) for c in range(C)])
+        ze = np.stack([Mo.apply_P_ra_eigen(ra(c).c0, ra(c).poles, ra(c).residues, B[c]) for c in range(C)])
+        assert rel_l2_cols(y, ref_y) <= 1e-10
+        check_precond(z, zb, ze, ras)
+        res = S.pcg_solve(_cols(B), colp)
+        x = res.x.cpu().numpy()
+        for c in range(C):
+            K, g = params[colp[c]]
+            xo, it, rel, hist, conv = opcg.pcg(lambda v: Mo.apply_S(K, g, v),
+                                               lambda v: Mo.apply_P_ra(ra(c).c0, ra(c).poles, ra(c).residues, v), B[c])
+            assert abs(int(res.iters[c]) - it) <= 1
+            assert np.linalg.norm(x[c] - xo) <= 1e-8 * np.linalg.norm(xo)
+    finally:
+        S.close()
+
+
 # ------------------------------------------------------------------------- full config sizes
 @pytest.mark.parametrize("cfg", [c for c in configs.CONFIGS if c.dim == 2], ids=lambda c: c.name)
 def test_full_config_parity(lib, cfg):
