@@ -84,7 +84,8 @@ struct dd_ctx {
     // graphs
     bool graph_ok = true;
     std::map<GraphKey, cudaGraphExec_t> graphs;
-    int last_split1 = 0, last_split2 = 0, last_ps_warps = 0, last_graph = 0;
+    int last_split1 = 0, last_split2 = 0, last_ps_warps = 0, last_graph = 0, last_small = 0;
+    bool small_ok = true;     // persistent single-launch PCG for n <= 63 (DD_NO_SMALL=1 disables)
     cudaEvent_t solve_ev[2] = {nullptr, nullptr};
 };
 
@@ -414,6 +415,7 @@ extern "C" dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K,
         return s;
     };
     if (const char* ng = std::getenv("DD_NO_GRAPH")) c->graph_ok = !(ng[0] == '1');   // profiling: host loop
+    if (const char* ns = std::getenv("DD_NO_SMALL")) c->small_ok = !(ns[0] == '1');
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DD_ECUDA, "cudaSetDevice failed"));
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     dd_status s = setup_2d(c, K, mu_inv, poles, residues, c0);
@@ -584,8 +586,15 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
     PcgState st = make_state(c, ncols, colp, x, rtol, maxit, norm_kind);
     c->last_ps_warps = polesum_warps(c->geom);
-    TIMED(DD_KCLASS_OTHER, launch_pcg_init(st, c->geom, c->tabs, b, c->n, c->stream));
     c->last_graph = 0;
+    c->last_small = 0;
+    if (c->small_ok && pcg_small_supported(c->n)) {
+        // whole PCG in one persistent launch (small interfaces)
+        c->last_small = 1;
+        TIMED(DD_KCLASS_POLESUM, launch_pcg_small(st, c->geom, c->tabs, b, c->n, c->W, c->lda, c->Kpad, c->sw, c->Kp,
+                                                  c->gp, c->stream));
+    } else {
+    TIMED(DD_KCLASS_OTHER, launch_pcg_init(st, c->geom, c->tabs, b, c->n, c->stream));
     if (maxit > 0) {
         bool done = false;
         if (c->graph_ok && !c->prof) {
@@ -628,6 +637,7 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
                 if (c->h_ints[1] == 0 || c->h_ints[4] != 0) break;
             }
         }
+    }
     }
     CK(cudaEventRecord(c->solve_ev[1], c->stream));
     if (iters) CK(cudaMemcpyAsync(iters, c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c->stream));
@@ -739,7 +749,7 @@ extern "C" dd_status dd_query_config(const dd_ctx* c, int* s1, int* s2, int* w, 
     if (s1) *s1 = c->last_split1;
     if (s2) *s2 = c->last_split2;
     if (w) *w = c->last_ps_warps;
-    if (g) *g = c->last_graph;
+    if (g) *g = c->last_small ? 2 : c->last_graph;   // 0 host loop, 1 graph WHILE loop, 2 persistent kernel
     return DD_OK;
 }
 

@@ -101,6 +101,11 @@ cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs
 cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st);
 cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, const PoleTabs& t,
                            const double* r, int ldr, double* z, int ldz, cudaStream_t st);
+// whole PCG in one launch for n <= 63 (one CTA per column, operators in shared memory)
+bool pcg_small_supported(int n);
+cudaError_t launch_pcg_small(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b, int ldb,
+                             const double* W, int lda, int Kpad, const double* sw, const double* Kp, const double* gp,
+                             cudaStream_t st);
 cudaError_t launch_copy_cols(int n, int ncols, const double* src, int lds, double* dst, int ldd,
                              cudaStream_t st);
 cudaError_t launch_check_params(int ncols, const int* col_param, int n_param, int* flag, cudaStream_t st);

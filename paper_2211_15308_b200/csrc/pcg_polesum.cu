@@ -54,8 +54,28 @@ __device__ __forceinline__ double group_shift(double v, int d, int tau, double* 
     }
 }
 
+// Asynchronously stage this parameter set's interior tables (4 contiguous blocks of nsys x LL
+// doubles) into scratch with cp.async (LDGSTS); block_polesum waits for them.  Called at kernel
+// entry so the copies overlap the vector passes.
+__device__ __forceinline__ void stage_tables(const PoleTabs& t, const PoleGeom& g, int param, double* scratch) {
+    const int LL = g.LL;
+    const int cnt = t.nsys[param] * LL;
+    const size_t tstride = (size_t)t.max_sys * LL;
+    const size_t src0 = (size_t)param * t.max_sys * LL;
+#pragma unroll
+    for (int which = 0; which < 4; which++) {
+        const double* src = (which == 0 ? t.invb : (which == 1 ? t.cpr : (which == 2 ? t.ufull : t.upart))) + src0;
+        double* dst = scratch + which * tstride;
+        for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + idx));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + idx));
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+
 // z = P r for the CTA's column.  R: input (transposed), Z: output (transposed, written by every
-// thread for its own chunk after the fixed-order combine).  sm: scratch.
+// thread for its own chunk after the fixed-order combine).  sm: scratch (tables already staged).
 template <int LMAX, int G, int NG>
 __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, const double* R, double* Z,
                               double* scratch) {
@@ -66,19 +86,11 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
     const int group = tid / T, tau = tid % T;
     const int nsys = t.nsys[param];
     const size_t pbase = (size_t)param * t.max_sys;
-    double* tab = scratch;                                     // [nsys][4][LL]
-    double* xbuf = scratch + (size_t)t.max_sys * 4 * LL;       // [NG][2][T] PCR exchange (G > 1)
+    const size_t tstride = (size_t)t.max_sys * LL;             // tables: [which][k][i], staged by stage_tables()
+    double* tab = scratch;
+    double* xbuf = scratch + 4 * tstride;                      // [NG][2][T] PCR exchange (G > 1)
     double* Zw = xbuf + 2 * NG * T;                            // [NG - 1][tot] partial sums of groups 1..NG-1
-
-    // stage the interior tables of this parameter set's systems (coalesced, unrolled)
-    {
-        const int tot_tab = nsys * 4 * LL;
-        for (int idx = tid; idx < tot_tab; idx += blockDim.x) {
-            const int k = idx / (4 * LL), rem = idx - k * 4 * LL, which = rem / LL, i = rem - which * LL;
-            const double* src = which == 0 ? t.invb : (which == 1 ? t.cpr : (which == 2 ? t.ufull : t.upart));
-            tab[idx] = __ldg(&src[(pbase + k) * LL + i]);
-        }
-    }
+    asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 
     const int Lr = tau < g.part ? LL - 1 : (tau == g.part ? g.Lr_part : 0);
@@ -90,9 +102,9 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
     for (int i = 0; i < LMAX; i++) z[i] = 0.0;
 
     for (int k = group; k < nsys; k += NG) {
-        const double* ib = tab + (size_t)k * 4 * LL;
-        const double* cp = ib + LL;
-        const double* u = tau < g.part ? ib + 2 * LL : ib + 3 * LL;
+        const double* ib = tab + (size_t)k * LL;
+        const double* cp = ib + tstride;
+        const double* u = tau < g.part ? ib + 2 * tstride : ib + 3 * tstride;
         const double e = __ldg(&t.e[pbase + k]), wk = __ldg(&t.w[pbase + k]);
         const double* pa = t.pa + (pbase + k) * (size_t)g.J * T;
         const double* pb = t.pb + (pbase + k) * (size_t)g.J * T;
@@ -241,9 +253,11 @@ __global__ void __launch_bounds__(32 * G * NG) k_precond(int ncols, const int* _
     if (c >= ncols) return;
     Smem S = carve(sm, g);
     const int npad = g.T * g.LL;
+    const int param = clamp_param(col_param[c], t.n_param);
+    stage_tables(t, g, param, S.scratch);
     for (int i = threadIdx.x; i < npad; i += blockDim.x) S.R[tpos(i, g)] = i < g.n ? r[(size_t)c * ldr + i] : 0.0;
     __syncthreads();
-    block_polesum<LMAX, G, NG>(t, g, clamp_param(col_param[c], t.n_param), S.R, S.Z, S.scratch);
+    block_polesum<LMAX, G, NG>(t, g, param, S.R, S.Z, S.scratch);
     for (int i = threadIdx.x; i < g.n; i += blockDim.x) z[(size_t)c * ldz + i] = S.Z[tpos(i, g)];
 }
 
@@ -282,13 +296,15 @@ __global__ void __launch_bounds__(32 * G * NG) k_pcg_init(PcgState s, PoleGeom g
     const int n = g.n, npad = g.T * g.LL;
     Smem S = carve(sm, g);
     const size_t off = (size_t)c * s.ldv;
+    const int param = clamp_param(s.col_param[c], t.n_param);
+    stage_tables(t, g, param, S.scratch);
     for (int i = threadIdx.x; i < npad; i += blockDim.x) {
         const double v = i < n ? b[(size_t)c * ldb + i] : 0.0;
         S.R[tpos(i, g)] = v;
         if (i < n) { s.r[off + i] = v; s.x[(size_t)c * s.ldx + i] = 0.0; }
     }
     __syncthreads();
-    block_polesum<LMAX, G, NG>(t, g, clamp_param(s.col_param[c], t.n_param), S.R, S.Z, S.scratch);
+    block_polesum<LMAX, G, NG>(t, g, param, S.R, S.Z, S.scratch);
     double rz = 0.0, zz = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double zi = S.Z[tpos(i, g)];
@@ -338,6 +354,8 @@ __global__ void __launch_bounds__(32 * G * NG) k_pcg_iter(PcgState s, PoleGeom g
     bool still = false;
     if (s_work) {
         const int k = *s.kiter + 1;
+        const int param = clamp_param(s.col_param[c], t.n_param);
+        stage_tables(t, g, param, S.scratch);
         // one pass over p, q, x, r: all loads in flight together
         double pv[RPT], qv[RPT], xv[RPT], rv[RPT];
 #pragma unroll
@@ -375,7 +393,7 @@ __global__ void __launch_bounds__(32 * G * NG) k_pcg_iter(PcgState s, PoleGeom g
             }
             for (int i = threadIdx.x + RPT * NT; i < g.T * g.LL; i += NT) S.R[tpos(i, g)] = 0.0;
             __syncthreads();
-            block_polesum<LMAX, G, NG>(t, g, clamp_param(s.col_param[c], t.n_param), S.R, S.Z, S.scratch);
+            block_polesum<LMAX, G, NG>(t, g, param, S.R, S.Z, S.scratch);
             double rz = 0.0, zz = 0.0;
             double zv[RPT];
 #pragma unroll
@@ -421,6 +439,119 @@ __global__ void __launch_bounds__(32 * G * NG) k_pcg_iter(PcgState s, PoleGeom g
         }
     }
     finish_iteration(s, still);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Persistent whole-PCG kernel for small interfaces (n <= 63): one CTA per column
+// keeps [S_dst | F], the vectors and the pole-sum state in shared memory and runs every PCG
+// iteration in one launch — the Schur apply as two fixed-order matvecs (same operator as the
+// GEMM path: q = S_dst (K s ∘ S_dst p) + γ F p), the pole sum and the updates as in k_pcg_iter.
+template <int LMAX, int NG>
+__global__ void __launch_bounds__(32 * NG) k_pcg_small(PcgState s, PoleGeom g, PoleTabs t, const double* __restrict__ b,
+                                                       int ldb, const double* __restrict__ W, int lda, int Kpad,
+                                                       const double* __restrict__ sw, const double* __restrict__ Kp,
+                                                       const double* __restrict__ gp) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[64];
+    const int c = blockIdx.x;
+    const int n = g.n, npad = g.T * g.LL;
+    const int ldw = 2 * Kpad;
+    double* Ws = sm;                                   // n x 2Kpad
+    double* pv = Ws + (size_t)n * ldw;                 // p, T, x : 64 each
+    double* Tv = pv + 64;
+    double* xv = Tv + 64;
+    double* psm = xv + 64;
+    Smem S = carve(psm, g);
+    const int param = clamp_param(s.col_param[c], t.n_param);
+    stage_tables(t, g, param, S.scratch);
+    for (int idx = threadIdx.x; idx < n * ldw; idx += blockDim.x) Ws[idx] = W[(size_t)(idx / ldw) * lda + idx % ldw];
+    const double Kc = Kp[param], gc = gp[param];
+    for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+        const double v = i < n ? b[(size_t)c * ldb + i] : 0.0;
+        S.R[tpos(i, g)] = v;
+        if (i < 64) xv[i] = 0.0;
+    }
+    __syncthreads();
+    block_polesum<LMAX, 1, NG>(t, g, param, S.R, S.Z, S.scratch);
+    double rz = 0.0, zz = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double zi = S.Z[tpos(i, g)];
+        rz += S.R[tpos(i, g)] * zi;
+        zz += zi * zi;
+        pv[i] = zi;
+    }
+    block_sum2(rz, zz, red);
+    const double eta0 = s.norm_kind == 0 ? sqrt(fmax(rz, 0.0)) : sqrt(zz);
+    double rho = rz;
+    int k = 0;
+    double rel = eta0 > 0.0 ? 1.0 : 0.0;
+    if (threadIdx.x == 0 && c == 0 && s.hist) s.hist[0] = eta0;
+    if (rz < 0.0 && threadIdx.x == 0) atomicExch(s.status, (int)DD_ENOTSPD);
+    bool run = eta0 > 0.0 && rz >= 0.0;
+    while (run && k < s.maxit) {
+        k++;
+        // q = S_dst (K s ∘ (S_dst p)) + γ F p
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const double* wr = Ws + (size_t)i * ldw;
+            double a = 0.0;
+            for (int j = 0; j < n; j++) a = fma(wr[j], pv[j], a);
+            Tv[i] = Kc * sw[i] * a;
+        }
+        __syncthreads();
+        // n <= 63 < blockDim: thread i owns row i
+        double pq = 0.0, dummy = 0.0, qi = 0.0;
+        const int i = threadIdx.x;
+        if (i < n) {
+            const double* wr = Ws + (size_t)i * ldw;
+            double a = 0.0, f = 0.0;
+            for (int j = 0; j < n; j++) {
+                a = fma(wr[j], Tv[j], a);
+                f = fma(wr[Kpad + j], pv[j], f);
+            }
+            qi = fma(gc, f, a);
+            pq = pv[i] * qi;
+        }
+        block_sum2(pq, dummy, red);
+        if (!(pq > 0.0)) {
+            if (threadIdx.x == 0) atomicExch(s.status, (int)DD_ENOTSPD);
+            break;
+        }
+        const double alpha = rho / pq;
+        if (i < n) {
+            xv[i] = fma(alpha, pv[i], xv[i]);
+            const int ps = tpos(i, g);
+            S.R[ps] = fma(-alpha, qi, S.R[ps]);
+        }
+        __syncthreads();
+        block_polesum<LMAX, 1, NG>(t, g, param, S.R, S.Z, S.scratch);
+        rz = 0.0; zz = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const double zi = S.Z[tpos(i, g)];
+            rz = fma(S.R[tpos(i, g)], zi, rz);
+            zz = fma(zi, zi, zz);
+        }
+        block_sum2(rz, zz, red);
+        const double eta = s.norm_kind == 0 ? sqrt(fmax(rz, 0.0)) : sqrt(zz);
+        rel = eta / eta0;
+        if (threadIdx.x == 0 && c == 0 && s.hist) s.hist[k] = eta;
+        if (rz < 0.0) {
+            if (threadIdx.x == 0) atomicExch(s.status, (int)DD_ENOTSPD);
+            break;
+        }
+        if (eta <= s.rtol * eta0) break;
+        const double beta = rz / rho;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) pv[i] = fma(beta, pv[i], S.Z[tpos(i, g)]);
+        __syncthreads();
+        rho = rz;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s.x[(size_t)c * s.ldx + i] = xv[i];
+    if (threadIdx.x == 0) {
+        s.iters[c] = k;
+        s.relres[c] = rel;
+        s.eta0[c] = eta0;
+        s.active[c] = 0;
+        atomicMax(s.kiter, k);
+    }
 }
 
 __global__ void k_copy_cols(int n, int ncols, const double* __restrict__ src, int lds, double* __restrict__ dst,
@@ -535,6 +666,28 @@ cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, c
         if (e == cudaSuccess)
             k_precond<LM, GG, NGG><<<ncols, 32 * GG * NGG, smem, st>>>(ncols, col_param, g, t, r, ldr, z, ldz);
     });
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+bool pcg_small_supported(int n) { return n <= 63; }
+
+cudaError_t launch_pcg_small(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b, int ldb,
+                             const double* W, int lda, int Kpad, const double* sw, const double* Kp, const double* gp,
+                             cudaStream_t st) {
+    if (s.ncols <= 0) return cudaSuccess;
+    if (!pcg_small_supported(g.n) || g.G != 1) return cudaErrorInvalidValue;
+    const size_t smem = ((size_t)g.n * 2 * Kpad + 192) * sizeof(double) + polesum_smem(g, t.max_sys);
+    cudaError_t e = cudaSuccess;
+    switch (lmax_of(g.LL)) {
+        case 1: {
+            e = set_smem(k_pcg_small<1, 8>, smem);
+            if (e == cudaSuccess) k_pcg_small<1, 8><<<s.ncols, 256, smem, st>>>(s, g, t, b, ldb, W, lda, Kpad, sw, Kp, gp);
+        } break;
+        default: {
+            e = set_smem(k_pcg_small<2, 8>, smem);
+            if (e == cudaSuccess) k_pcg_small<2, 8><<<s.ncols, 256, smem, st>>>(s, g, t, b, ldb, W, lda, Kpad, sw, Kp, gp);
+        } break;
+    }
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 

@@ -148,8 +148,27 @@ def test_edge_cases(lib):
         lib.Solver(2, 1, params, ras, max_cols=1)
 
 
+@pytest.mark.parametrize("N", [32, 48, 64])
+def test_small_persistent_kernel_matches_general_path(lib, N, monkeypatch):
+    # n <= 63 runs the whole PCG in one launch (K7); it must agree with the GEMM/graph path.
+    params = [(1.0, 1e2), (1e-4, 1e6)]; ras = fit_all(N, params, 12)
+    B = np.random.default_rng(N).uniform(-1, 1, (5, N - 1)); colp = [0, 1, 0, 1, 1]
+    S1 = _solver(lib, N, params, ras, max_cols=5)
+    monkeypatch.setenv("DD_NO_SMALL", "1")
+    S2 = _solver(lib, N, params, ras, max_cols=5)
+    try:
+        a = S1.pcg_solve(_cols(B), colp, want_hist=True); ca = S1.query_config()
+        b = S2.pcg_solve(_cols(B), colp, want_hist=True); cb = S2.query_config()
+        assert ca["graph_while"] == 2 and cb["graph_while"] != 2
+        assert np.array_equal(a.iters, b.iters)
+        assert rel_l2_cols(a.x.cpu().numpy(), b.x.cpu().numpy()) <= 1e-12
+        assert np.allclose(a.hist, b.hist, rtol=1e-10)
+    finally:
+        S1.close(); S2.close()
+
+
 def test_profile_and_launch_counts(lib):
-    N = 64; params = [(1.0, 1e2)]; ras = fit_all(N, params, 8)
+    N = 96; params = [(1.0, 1e2)]; ras = fit_all(N, params, 8)
     S = _solver(lib, N, params, ras, max_cols=8)
     try:
         B = np.random.default_rng(0).uniform(-1, 1, (8, N - 1))
