@@ -446,11 +446,14 @@ inline int dgemm_pick_splitk(int M, int N, int K, int num_sms, int ctas_per_sm) 
     for (int s = 1; s <= 8; s++) {
         if (s > 1 && ktiles / s < 4) break;
         const int ctas = tiles * s;
-        // time ~ (work per CTA) x (CTAs on the busiest SM), plus a small per-split reduction cost
+        // time ~ (work per CTA) x (CTAs on the busiest SM) / (SM efficiency at that residency):
+        // one 4-warp CTA alone keeps the DMMA pipe ~60% busy, two or more ~100% (gemm_lab).
         const double per_cta = double((ktiles + s - 1) / s) + 2.0;
         const int waves = (ctas + slots - 1) / slots;
-        const int busiest = (ctas + num_sms - 1) / num_sms;   // CTAs per SM when spread
-        const double t = per_cta * (double)busiest * (waves > 1 ? 1.0 : 1.0) + (s > 1 ? 1.5 : 0.0);
+        int busiest = (ctas + num_sms - 1) / num_sms;   // CTAs per SM when spread
+        if (busiest > ctas_per_sm) busiest = ctas_per_sm;
+        const double eff = busiest >= 2 ? 1.0 : 0.6;
+        const double t = per_cta * (double)busiest / eff * (double)waves + (s > 1 ? 1.5 : 0.0);
         if (t < best_t - 1e-9) { best_t = t; best = s; }
     }
     return best;

@@ -3,7 +3,7 @@
 //   K2  Y  = [S_dst | F] [T' ; γX]                        (EPI_STORE)
 // on the DMMA tile template of dgemm_tile.cuh.  Two work decompositions, picked per launch from
 // the work per CTA (tools/gemm_lab.cu measurements, profiles/):
-//   * stream-K over 2 CTAs/SM when every CTA gets >= 24 (tile, k-tile) units — balanced to
+//   * stream-K over 2 CTAs/SM when every CTA gets >= 64 (tile, k-tile) units — balanced to
 //     within one unit on any shape (large configs: 30-32 TFLOP/s, cuBLAS-level);
 //   * cluster split-K (DSMEM reduction) for small problems (config 2), where stream-K's
 //     segment fix-ups cost more than the imbalance they remove.
@@ -16,7 +16,7 @@ namespace dd {
 using CfgC = DgemmCfg<64, 64, 16, 2, 2, 4, 2>;   // cluster split-K: 4-stage ring, 2 CTAs/SM
 using CfgS = DgemmCfg<64, 64, 16, 2, 2, 3, 3>;   // stream-K: 3-stage ring, run at 2 CTAs/SM
 constexpr int OCC_C = 2, OCC_S = 2;
-constexpr int SK_MIN_UNITS = 24;
+constexpr int SK_MIN_UNITS = 64;   // below this the segment fix-ups outweigh the balance gain
 
 struct EpiStore {
     double* C; int ldc;

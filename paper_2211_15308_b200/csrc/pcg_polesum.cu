@@ -89,7 +89,11 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
     const size_t tstride = (size_t)t.max_sys * LL;             // tables: [which][k][i], staged by stage_tables()
     double* tab = scratch;
     double* xbuf = scratch + 4 * tstride;                      // [NG][2][T] PCR exchange (G > 1)
-    double* Zw = xbuf + 2 * NG * T;                            // [NG - 1][tot] partial sums of groups 1..NG-1
+    double* Zw = xbuf + 2 * NG * T;                            // [NG][tot] per-group partial sums
+    double* zg = Zw + (size_t)group * tot;
+#pragma unroll
+    for (int i = 0; i < LMAX; i++)
+        if (i < LL) zg[tix(i, tau, T)] = 0.0;
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 
@@ -97,9 +101,6 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
     const int Lr_next = (tau + 1) < g.part ? LL - 1 : ((tau + 1) == g.part ? g.Lr_part : 0);
     const bool sep_real = tau < g.part;
     double* xb = xbuf + (size_t)group * 2 * T;
-    double z[LMAX];
-#pragma unroll
-    for (int i = 0; i < LMAX; i++) z[i] = 0.0;
 
     for (int k = group; k < nsys; k += NG) {
         const double* ib = tab + (size_t)k * LL;
@@ -180,36 +181,22 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
         for (int i = 0; i < LMAX; i++) {
             if (i < LL - 1 && i < Lr) {
                 const double x = y[i] - eg0 * u[i] - eg1 * u[Lr - 1 - i];
-                z[i] = fma(wk, x, z[i]);
+                const int ix = tix(i, tau, T);
+                zg[ix] = fma(wk, x, zg[ix]);
             }
         }
-#pragma unroll
-        for (int i = 0; i < LMAX; i++)
-            if (i == LL - 1) z[i] = fma(wk, gsep, z[i]);
+        if (LL >= 1) {
+            const int ix = tix(LL - 1, tau, T);
+            zg[ix] = fma(wk, gsep, zg[ix]);
+        }
     }
 
     // fixed-order combine of the NG group partials: Z = z_0 + z_1 + ... + z_{NG-1}
-    if constexpr (NG > 1) {
-        if (group > 0) {
-#pragma unroll
-            for (int i = 0; i < LMAX; i++)
-                if (i < LL) Zw[(size_t)(group - 1) * tot + tix(i, tau, T)] = z[i];
-        }
-        __syncthreads();
-        if (group == 0) {
-#pragma unroll
-            for (int i = 0; i < LMAX; i++) {
-                if (i < LL) {
-                    double acc = z[i];
-                    for (int gg = 1; gg < NG; gg++) acc += Zw[(size_t)(gg - 1) * tot + tix(i, tau, T)];
-                    Z[tix(i, tau, T)] = acc;
-                }
-            }
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < LMAX; i++)
-            if (i < LL) Z[tix(i, tau, T)] = z[i];
+    __syncthreads();
+    for (int idx = tid; idx < tot; idx += blockDim.x) {
+        double acc = Zw[idx];
+        for (int gg = 1; gg < NG; gg++) acc += Zw[(size_t)gg * tot + idx];
+        Z[idx] = acc;
     }
     __syncthreads();
 }
@@ -245,7 +232,7 @@ __device__ __forceinline__ Smem carve(double* sm, const PoleGeom& g) {
 
 // ---------------------------------------------------------------------------- kernels
 template <int LMAX, int G, int NG>
-__global__ void __launch_bounds__(32 * G * NG) k_precond(int ncols, const int* __restrict__ col_param, PoleGeom g,
+__global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_precond(int ncols, const int* __restrict__ col_param, PoleGeom g,
                                                          PoleTabs t, const double* __restrict__ r, int ldr,
                                                          double* __restrict__ z, int ldz) {
     extern __shared__ __align__(16) double sm[];
@@ -288,7 +275,7 @@ __device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_a
 }
 
 template <int LMAX, int G, int NG>
-__global__ void __launch_bounds__(32 * G * NG) k_pcg_init(PcgState s, PoleGeom g, PoleTabs t,
+__global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_pcg_init(PcgState s, PoleGeom g, PoleTabs t,
                                                           const double* __restrict__ b, int ldb) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
@@ -338,7 +325,7 @@ __global__ void __launch_bounds__(32 * G * NG) k_pcg_init(PcgState s, PoleGeom g
 
 // rows of thread tid: ρ = tid + j NT, j < RPT (coalesced); RPT = ceil(T LL / NT) <= ceil(LMAX / NG)
 template <int LMAX, int G, int NG>
-__global__ void __launch_bounds__(32 * G * NG) k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
+__global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
     constexpr int NT = 32 * G * NG;
     constexpr int RPT = (LMAX + NG - 1) / NG;
     extern __shared__ __align__(16) double sm[];
@@ -598,7 +585,7 @@ int polesum_groups(const PoleGeom& g) {
     if (g.G >= 8) return 1;
     if (g.G == 4) return 2;
     if (g.G == 2) return 4;
-    return lmax_of(g.LL) >= 16 ? 4 : 8;
+    return 8;
 }
 
 int polesum_warps(const PoleGeom& g) { return g.G * polesum_groups(g); }
@@ -609,7 +596,7 @@ size_t polesum_smem(const PoleGeom& g, int max_sys) {
     size_t d = 2 * tot                          // R, Z
                + (size_t)max_sys * 4 * g.LL     // tables
                + 2 * (size_t)NG * g.T           // PCR exchange
-               + (size_t)(NG - 1) * tot;        // group partials
+               + (size_t)NG * tot;              // group partials
     return d * sizeof(double);
 }
 
@@ -626,8 +613,8 @@ static cudaError_t set_smem(K kern, size_t bytes) {
         else if (_G == 1 && _lm == 2) { constexpr int LM = 2, GG = 1, NGG = 8; __VA_ARGS__; }    \
         else if (_G == 1 && _lm == 4) { constexpr int LM = 4, GG = 1, NGG = 8; __VA_ARGS__; }    \
         else if (_G == 1 && _lm == 8) { constexpr int LM = 8, GG = 1, NGG = 8; __VA_ARGS__; }    \
-        else if (_G == 1 && _lm == 16) { constexpr int LM = 16, GG = 1, NGG = 4; __VA_ARGS__; }  \
-        else if (_G == 1) { constexpr int LM = 32, GG = 1, NGG = 4; __VA_ARGS__; }               \
+        else if (_G == 1 && _lm == 16) { constexpr int LM = 16, GG = 1, NGG = 8; __VA_ARGS__; }  \
+        else if (_G == 1) { constexpr int LM = 32, GG = 1, NGG = 8; __VA_ARGS__; }               \
         else if (_G == 2) { constexpr int LM = 32, GG = 2, NGG = 4; __VA_ARGS__; }               \
         else if (_G == 4) { constexpr int LM = 32, GG = 4, NGG = 2; __VA_ARGS__; }               \
         else { constexpr int LM = 32, GG = 8, NGG = 1; __VA_ARGS__; }                            \
