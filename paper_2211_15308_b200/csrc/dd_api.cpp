@@ -11,97 +11,25 @@
 #include <tuple>
 #include <vector>
 
+#include "dd_ctx.h"
 #include "dd_internal.h"
 
 using namespace dd;
 
 namespace {
 thread_local std::string g_last_error;
+}  // namespace
 
-dd_status fail(dd_status s, const std::string& msg) {
+dd_status dd::set_error(dd_status s, const std::string& msg) {
     g_last_error = msg;
     return s;
 }
-
-#define CK(expr)                                                                                  \
-    do {                                                                                          \
-        cudaError_t _e = (expr);                                                                  \
-        if (_e != cudaSuccess)                                                                    \
-            return fail(_e == cudaErrorMemoryAllocation ? DD_ENOMEM : DD_ECUDA,                  \
-                        std::string(#expr) + ": " + cudaGetErrorString(_e));                      \
-    } while (0)
-
-int round_up(int a, int b) { return (a + b - 1) / b * b; }
-
-struct EvPair {
-    cudaEvent_t a, b;
-    int cls;
-};
-
-struct GraphKey {
-    int ncols;
-    const int* colp;
-    const double* x;
-    double rtol;
-    int maxit, norm_kind;
-    bool operator<(const GraphKey& o) const {
-        return std::tie(ncols, colp, x, rtol, maxit, norm_kind) <
-               std::tie(o.ncols, o.colp, o.x, o.rtol, o.maxit, o.norm_kind);
-    }
-};
-}  // namespace
-
-struct dd_ctx {
-    int dim = 2, N = 0, n = 0, ng = 0, Kpad = 0, ldv = 0, lda = 0, Mpad = 0;
-    int n_param = 0, n_poles = 0, max_cols = 0, cols_pad = 0, device = 0, num_sms = 148;
-    cudaStream_t stream = nullptr;
-    std::vector<void*> allocs;
-    // operator data
-    double* W = nullptr;      // Mpad x 2 Kpad row-major: [S_dst | 0 | F | 0]
-    double* sw = nullptr;     // Schur weights s_b
-    double* Kp = nullptr;     // [n_param]
-    double* gp = nullptr;     // [n_param]
-    PoleGeom geom{};
-    PoleTabs tabs{};
-    // workspaces
-    double *xw = nullptr, *Z = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
-    double *bst = nullptr, *xst = nullptr;   // host-API staging (ld = n)
-    int* colp_st = nullptr;
-    double* gws = nullptr;
-    int* gcnt = nullptr;
-    // PCG scalars
-    double *rho = nullptr, *eta0 = nullptr, *relres = nullptr, *hist = nullptr;
-    int *active = nullptr, *iters = nullptr, *ints = nullptr;   // ints: kiter, n_active, n_active_next, done, status, flag
-    int hist_cap = 0;
-    // pinned host mirrors
-    int* h_ints = nullptr;
-    // profiling
-    bool prof = false;
-    std::vector<EvPair> ev_pending, ev_free;
-    double prof_ms[DD_NKCLASS] = {0, 0, 0, 0};
-    long long prof_n[DD_NKCLASS] = {0, 0, 0, 0};
-    long long launches = 0;
-    // graphs
-    bool graph_ok = true;
-    std::map<GraphKey, cudaGraphExec_t> graphs;
-    int last_split1 = 0, last_split2 = 0, last_ps_warps = 0, last_graph = 0, last_small = 0;
-    bool small_ok = true;     // persistent single-launch PCG for n <= 63 (DD_NO_SMALL=1 disables)
-    cudaEvent_t solve_ev[2] = {nullptr, nullptr};
-};
+static dd_status fail(dd_status s, const std::string& msg) { return set_error(s, msg); }
+#define CK(expr) DD_CK(expr)
+#define TIMED(cls, call) DD_TIMED(cls, call)
 
 // ------------------------------------------------------------------------------------ helpers
-template <typename T>
-static cudaError_t dalloc(dd_ctx* c, T** p, size_t count) {
-    void* v = nullptr;
-    cudaError_t e = cudaMalloc(&v, count * sizeof(T) + 256);
-    if (e != cudaSuccess) return e;
-    c->allocs.push_back(v);
-    e = cudaMemsetAsync(v, 0, count * sizeof(T) + 256, c->stream);
-    *p = reinterpret_cast<T*>(v);
-    return e;
-}
-
-static dd_status prof_begin(dd_ctx* c, EvPair& ev, int cls) {
+dd_status dd::prof_begin(dd_ctx* c, EvPair& ev, int cls) {
     if (!c->prof) return DD_OK;
     if (c->ev_free.empty()) {
         EvPair e{};
@@ -115,7 +43,7 @@ static dd_status prof_begin(dd_ctx* c, EvPair& ev, int cls) {
     CK(cudaEventRecord(ev.a, c->stream));
     return DD_OK;
 }
-static dd_status prof_end(dd_ctx* c, EvPair& ev) {
+dd_status dd::prof_end(dd_ctx* c, EvPair& ev) {
     if (!c->prof) return DD_OK;
     CK(cudaEventRecord(ev.b, c->stream));
     c->ev_pending.push_back(ev);
@@ -132,17 +60,6 @@ static dd_status prof_end(dd_ctx* c, EvPair& ev) {
     }
     return DD_OK;
 }
-
-#define TIMED(cls, call)                                         \
-    do {                                                         \
-        EvPair _ev{};                                            \
-        dd_status _s = prof_begin(c, _ev, cls);                  \
-        if (_s != DD_OK) return _s;                              \
-        CK(call);                                                \
-        c->launches++;                                           \
-        _s = prof_end(c, _ev);                                   \
-        if (_s != DD_OK) return _s;                              \
-    } while (0)
 
 // ------------------------------------------------------------------------------------ tables
 // Pole-sum tables for one symmetric Toeplitz tridiagonal system (d, e), computed in long

@@ -1,0 +1,150 @@
+// Host-only definition of the libdd handle and shared host helpers (dd_api.cpp, dd3d.cpp).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "dd_internal.h"
+
+namespace dd {
+
+dd_status set_error(dd_status s, const std::string& msg);
+
+#define DD_CK(expr)                                                                               \
+    do {                                                                                          \
+        cudaError_t _e = (expr);                                                                  \
+        if (_e != cudaSuccess)                                                                    \
+            return ::dd::set_error(_e == cudaErrorMemoryAllocation ? DD_ENOMEM : DD_ECUDA,       \
+                                   std::string(#expr) + ": " + cudaGetErrorString(_e));          \
+    } while (0)
+
+inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+struct EvPair {
+    cudaEvent_t a, b;
+    int cls;
+};
+
+struct GraphKey {
+    int ncols;
+    const int* colp;
+    const double* x;
+    double rtol;
+    int maxit, norm_kind;
+    bool operator<(const GraphKey& o) const {
+        return std::tie(ncols, colp, x, rtol, maxit, norm_kind) <
+               std::tie(o.ncols, o.colp, o.x, o.rtol, o.maxit, o.norm_kind);
+    }
+};
+
+// 3D (face interface) state
+struct Face3 {
+    int n = 0, n2 = 0, ldf = 0;
+    long long NP = 0;                 // padded face size ldf^2
+    double* S = nullptr;              // sine matrix, round_up(n,64) x ldf row-major, zero padded
+    double* sw = nullptr;             // Schur weights s_ab, NP (padded layout)
+    double* F = nullptr;              // dense fractional term, rows round_up(NP,128) x NP row-major
+    double* Kcol = nullptr;           // per-column K (gathered from col_param)
+    // outer vectors [cols_pad][NP]
+    double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr, *U1 = nullptr, *U2 = nullptr;
+    // pole systems of this rank: coefficients of A and M, weight, sine-diagonal preconditioner
+    int nsys = 0;                     // systems handled by this rank
+    int nsys_total = 0;
+    std::vector<int> sys_ids;         // global system ids of this rank
+    double *sys_a = nullptr, *sys_b = nullptr, *sys_w = nullptr, *pdiag = nullptr;   // pdiag [nsys][NP]
+    // inner PCG pairs [nsys * max_cols][NP]
+    double *ix = nullptr, *ir = nullptr, *ip = nullptr, *iq = nullptr, *iz = nullptr, *T1 = nullptr, *T2 = nullptr;
+    double *irho = nullptr, *irho0 = nullptr;
+    int* iactive = nullptr;
+    double inner_rtol = 1e-13;        // reading A12
+    int inner_maxit = 400;
+    int last_inner_iters = 0;
+    double* fx_ws = nullptr;
+    int* fx_cnt = nullptr;
+    double lam_min = 0.0, lam_max = 0.0;   // spectrum of the face pair (from the setup gevp)
+    void* nccl = nullptr;             // ncclComm_t when the poles are split across ranks
+    int rank = 0, world = 1;
+};
+
+}  // namespace dd
+
+struct dd_ctx {
+    int dim = 2, N = 0, n = 0, ng = 0, Kpad = 0, ldv = 0, lda = 0, Mpad = 0;
+    int n_param = 0, n_poles = 0, max_cols = 0, cols_pad = 0, device = 0, num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::vector<void*> allocs;
+    // operator data (2D)
+    double* W = nullptr;      // Mpad x 2 Kpad row-major: [S_dst | 0 | F | 0]
+    double* sw = nullptr;     // Schur weights s_b
+    double* Kp = nullptr;     // [n_param]
+    double* gp = nullptr;     // [n_param]
+    dd::PoleGeom geom{};
+    dd::PoleTabs tabs{};
+    // workspaces
+    double *xw = nullptr, *Z = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
+    double *bst = nullptr, *xst = nullptr;   // host-API staging (ld = n_Γ)
+    int* colp_st = nullptr;
+    double* gws = nullptr;
+    int* gcnt = nullptr;
+    // PCG scalars
+    double *rho = nullptr, *eta0 = nullptr, *relres = nullptr, *hist = nullptr;
+    int *active = nullptr, *iters = nullptr, *ints = nullptr;   // ints: kiter, n_active, n_active_next, done, status, flag
+    int hist_cap = 0;
+    // pinned host mirrors
+    int* h_ints = nullptr;
+    // profiling
+    bool prof = false;
+    std::vector<dd::EvPair> ev_pending, ev_free;
+    double prof_ms[DD_NKCLASS] = {0, 0, 0, 0};
+    long long prof_n[DD_NKCLASS] = {0, 0, 0, 0};
+    long long launches = 0;
+    // graphs
+    bool graph_ok = true;
+    std::map<dd::GraphKey, cudaGraphExec_t> graphs;
+    int last_split1 = 0, last_split2 = 0, last_ps_warps = 0, last_graph = 0, last_small = 0;
+    bool small_ok = true;     // persistent single-launch PCG for n <= 63 (DD_NO_SMALL=1 disables)
+    cudaEvent_t solve_ev[2] = {nullptr, nullptr};
+    // 3D
+    dd::Face3 f3;
+};
+
+namespace dd {
+
+template <typename T>
+inline cudaError_t dalloc(dd_ctx* c, T** p, size_t count) {
+    void* v = nullptr;
+    cudaError_t e = cudaMalloc(&v, count * sizeof(T) + 256);
+    if (e != cudaSuccess) return e;
+    c->allocs.push_back(v);
+    e = cudaMemsetAsync(v, 0, count * sizeof(T) + 256, c->stream);
+    *p = reinterpret_cast<T*>(v);
+    return e;
+}
+
+dd_status prof_begin(dd_ctx* c, EvPair& ev, int cls);
+dd_status prof_end(dd_ctx* c, EvPair& ev);
+
+#define DD_TIMED(cls, call)                                      \
+    do {                                                         \
+        ::dd::EvPair _ev{};                                      \
+        dd_status _s = ::dd::prof_begin(c, _ev, cls);            \
+        if (_s != DD_OK) return _s;                              \
+        DD_CK(call);                                             \
+        c->launches++;                                           \
+        _s = ::dd::prof_end(c, _ev);                             \
+        if (_s != DD_OK) return _s;                              \
+    } while (0)
+
+// 3D entry points (dd3d.cpp)
+dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const double* poles, const double* residues,
+                   const double* c0, const dd_dist* dist);
+dd_status schur_3d(dd_ctx* c, int ncols, const int* colp, const double* xin, double* yout, bool user_layout);
+dd_status precond_3d(dd_ctx* c, int ncols, const int* colp, const double* rin, double* zout, bool user_layout);
+dd_status pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
+                 int norm_kind);
+void destroy_3d(dd_ctx* c);
+
+}  // namespace dd

@@ -28,14 +28,18 @@ struct DgemmCfg {
     static constexpr size_t SMEM_PIPE = size_t(STAGES) * (BM + BN) * LDS * sizeof(double);
     static constexpr size_t SMEM_RED = size_t(NREG) * THREADS * sizeof(double);
     static constexpr size_t SMEM = SMEM_PIPE > SMEM_RED ? SMEM_PIPE : SMEM_RED;
+    static constexpr int CPR = BK / 2;                      // 16-byte chunks per smem row
+    static constexpr int ACH = BM * CPR, BCH = BN * CPR;    // chunks per stage
     static_assert(TM % 16 == 0 && TN % 8 == 0 && BK % 4 == 0, "tile shape");
-    static_assert((BM * BK / 2) % THREADS == 0 && (BN * BK / 2) % THREADS == 0, "load mapping");
 };
 
+// Batched problem: gridDim.z = batch; slab b uses A + b*sA, B + b*sB and the epilogue gets b.
 struct DgemmProblem {
     int M, N, K;                 // K multiple of BK
     const double* A; int lda;    // rows readable up to round_up(M, BM)
     const double* B; int ldb;    // columns readable up to round_up(N, BN)
+    long long sA = 0, sB = 0;    // batch strides (elements)
+    int batch = 1;
 };
 
 __device__ __forceinline__ void dg_cp_async16(void* smem, const void* gmem) {
@@ -64,12 +68,38 @@ __device__ __forceinline__ void dg_coord(int r, int tid, int& row, int& col) {
     col = wn * C::TN + ni * 8 + (lane & 3) * 2 + (q & 1);
 }
 
-// Epi: functor  __device__ void operator()(int row, int col, double v) const  (row < M, col < N checked)
+// Issue the cp.async copies of one K-stage (A: BM rows, B: BN columns of BK doubles each).
+template <class C>
+__device__ __forceinline__ void dg_load_stage(double* As, double* Bs, const double* A, int lda, const double* B, int ldb,
+                                              int m0, int n0, int k0, int tid) {
+#pragma unroll
+    for (int j = 0; j < (C::ACH + C::THREADS - 1) / C::THREADS; j++) {
+        const int c = tid + C::THREADS * j;
+        if (C::ACH % C::THREADS == 0 || c < C::ACH) {
+            const int row = c / C::CPR, kc = (c % C::CPR) * 2;
+            dg_cp_async16(&As[row * C::LDS + kc], A + (size_t)(m0 + row) * lda + k0 + kc);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < (C::BCH + C::THREADS - 1) / C::THREADS; j++) {
+        const int c = tid + C::THREADS * j;
+        if (C::BCH % C::THREADS == 0 || c < C::BCH) {
+            const int row = c / C::CPR, kc = (c % C::CPR) * 2;
+            dg_cp_async16(&Bs[row * C::LDS + kc], B + (size_t)(n0 + row) * ldb + k0 + kc);
+        }
+    }
+}
+
+// Epi: functor  __device__ void operator()(int b, int row, int col, double v) const
+// (b = batch index; row < M, col < N checked)
 template <class C, class Epi>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem g, Epi epi) {
     extern __shared__ __align__(16) double smem[];
     double* As = smem;
     double* Bs = smem + C::STAGES * C::BM * C::LDS;
+    const int bz = blockIdx.z;
+    g.A += (size_t)bz * g.sA;
+    g.B += (size_t)bz * g.sB;
 
     const int tiles_m = (g.M + C::BM - 1) / C::BM;
     const int m0 = (blockIdx.x % tiles_m) * C::BM;
@@ -93,20 +123,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
             for (int r = 0; r < 4; r++) acc[i][j][r] = 0.0;
 
     auto load_stage = [&](int stage, int kt) {
-        const int k0 = kt * C::BK;
-        constexpr int CPR = C::BK / 2;   // 16-byte chunks per row
-#pragma unroll
-        for (int j = 0; j < (C::BM * CPR) / C::THREADS; j++) {
-            const int c = tid + C::THREADS * j;
-            const int row = c / CPR, kc = (c % CPR) * 2;
-            dg_cp_async16(&As[(stage * C::BM + row) * C::LDS + kc], g.A + (size_t)(m0 + row) * g.lda + k0 + kc);
-        }
-#pragma unroll
-        for (int j = 0; j < (C::BN * CPR) / C::THREADS; j++) {
-            const int c = tid + C::THREADS * j;
-            const int row = c / CPR, kc = (c % CPR) * 2;
-            dg_cp_async16(&Bs[(stage * C::BN + row) * C::LDS + kc], g.B + (size_t)(n0 + row) * g.ldb + k0 + kc);
-        }
+        dg_load_stage<C>(As + stage * C::BM * C::LDS, Bs + stage * C::BN * C::LDS, g.A, g.lda, g.B, g.ldb, m0, n0,
+                         kt * C::BK, tid);
     };
 
 #pragma unroll
@@ -150,7 +168,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
                     int row, col;
                     dg_coord<C>((mi * C::NI + ni) * 4 + q, tid, row, col);
                     row += m0; col += n0;
-                    if (row < g.M && col < g.N) epi(row, col, acc[mi][ni][q]);
+                    if (row < g.M && col < g.N) epi(bz, row, col, acc[mi][ni][q]);
                 }
         return;
     }
@@ -188,7 +206,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
             int row, col;
             dg_coord<C>(r, tid, row, col);
             row += m0; col += n0;
-            if (row < g.M && col < g.N) epi(row, col, v[j]);
+            if (row < g.M && col < g.N) epi(bz, row, col, v[j]);
         }
     }
     cluster.sync();   // keep every CTA's smem alive until all remote reads are done
@@ -253,20 +271,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProb
                 for (int r = 0; r < 4; r++) acc[i][j][r] = 0.0;
 
         auto load_stage = [&](int stage, int kt) {
-            const int k0 = kt * C::BK;
-            constexpr int CPR = C::BK / 2;
-#pragma unroll
-            for (int j = 0; j < (C::BM * CPR) / C::THREADS; j++) {
-                const int c = tid + C::THREADS * j;
-                const int row = c / CPR, kc = (c % CPR) * 2;
-                dg_cp_async16(&As[(stage * C::BM + row) * C::LDS + kc], g.A + (size_t)(m0 + row) * g.lda + k0 + kc);
-            }
-#pragma unroll
-            for (int j = 0; j < (C::BN * CPR) / C::THREADS; j++) {
-                const int c = tid + C::THREADS * j;
-                const int row = c / CPR, kc = (c % CPR) * 2;
-                dg_cp_async16(&Bs[(stage * C::BN + row) * C::LDS + kc], g.B + (size_t)(n0 + row) * g.ldb + k0 + kc);
-            }
+            dg_load_stage<C>(As + stage * C::BM * C::LDS, Bs + stage * C::BN * C::LDS, g.A, g.lda, g.B, g.ldb, m0, n0,
+                             kt * C::BK, tid);
         };
         __syncthreads();   // previous segment's smem reads are finished
 #pragma unroll
@@ -365,7 +371,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProb
                         int row, col;
                         dg_coord<C>((mi * C::NI + ni) * 4 + q, tid, row, col);
                         row += m0; col += n0;
-                        if (row < g.M && col < g.N) epi(row, col, acc[mi][ni][q]);
+                        if (row < g.M && col < g.N) epi(0, row, col, acc[mi][ni][q]);
                     }
         }
         u += nkt;
@@ -421,7 +427,7 @@ inline cudaError_t dgemm_launch(const DgemmProblem& g, int splitk, const Epi& ep
     if (splitk < 1) splitk = 1;
     if (splitk > 8) splitk = 8;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(dgemm_tiles<C>(g.M, g.N), splitk, 1);
+    cfg.gridDim = dim3(dgemm_tiles<C>(g.M, g.N), splitk, g.batch < 1 ? 1 : g.batch);
     cfg.blockDim = dim3(C::THREADS, 1, 1);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;

@@ -1,0 +1,439 @@
+// 3D path (Γ = face {x = 0} of the unit cube, SURVEY §8(a) rows a-2..a-6 for config 4).
+//
+// Face vectors live in a padded layout: column c, node (j, k) (1-based grid indices j, k <= n)
+// at c*NP + (j-1)*ldf + (k-1), ldf = round_up(n, 16), NP = ldf^2, padding zero.
+//
+// * Interior solve (row a-2): the 2D sine transform of a face slab, X̂ = S X S, is two batched
+//   DMMA GEMM passes Out = (Y S^T)^T (dgemm_tile.cuh, batch = columns); the Schur weights
+//   s_ab = h(3 - cos θ_a - cos θ_b) - h Σ_m S[1,m]^2/(σ_m + σ_a + σ_b) scale X̂ in the second
+//   pass's epilogue, and two more passes transform back.
+// * Fractional term (row a-3): q = γ F p + (back transform) as one stream-K DMMA GEMM with
+//   BN = 8 columns (HBM-bound: F is read once per apply).
+// * Pole sum (row a-4, 2D Γ): every system (A_Γ - p_k M_Γ) (5-point A, 7-point consistent mass)
+//   and M_Γ is solved by batched preconditioned CG over all (system, column) pairs; the
+//   preconditioner is the sine-diagonal part of the pair, 1/(α_ab - p μ̃_ab) with
+//   α = σ_a + σ_b and μ̃ = (h^2/12)(6 + 2c_a + 2c_b + 2 c_a c_b) (spectrally equivalent, κ <= 3,
+//   SURVEY V10), applied with the same slab transforms.  Converged pairs freeze.
+//   The weighted sum over systems runs in fixed system order; across ranks (pole split) the
+//   partial sums are added by one NCCL allreduce (row a-6, in dd_api.cpp).
+#include "dd_internal.h"
+#include "dgemm_tile.cuh"
+
+namespace dd {
+
+using CfgSlab = DgemmCfg<64, 64, 16, 2, 2, 4, 2>;
+using CfgFv = DgemmCfg<128, 8, 16, 4, 1, 4, 2>;   // F x for a handful of columns: 128 rows x 8 cols
+constexpr int OCC_FV = 2;
+
+// ------------------------------------------------------------------------------------ epilogues
+struct EpiSlabStore {          // Out[b] (col-major, ldc = ldf) = v
+    double* out; long long sC; int ldf;
+    __device__ __forceinline__ void operator()(int b, int row, int col, double v) const {
+        out[(size_t)b * sC + row + (size_t)col * ldf] = v;
+    }
+};
+struct EpiSlabScale {          // Out[b] = v * scale(b) * w[b's table][row + col ldf]
+    double* out; long long sC; int ldf;
+    const double* w; long long sW;          // weight table per slab group (sW = 0: shared)
+    int group;                              // slabs b share table b / group
+    const double* colscale;                 // per slab scalar (or null)
+    __device__ __forceinline__ void operator()(int b, int row, int col, double v) const {
+        const size_t i = row + (size_t)col * ldf;
+        double s = w[(size_t)(b / group) * sW + i];
+        if (colscale) s *= colscale[b];
+        out[(size_t)b * sC + i] = v * s;
+    }
+};
+struct EpiFaceFx {             // q[c] = γ_c v + D[c]  (padded face layout)
+    double* q; const double* D; long long ldq; const int* col_param; int n_param; const double* gp;
+    __device__ __forceinline__ void operator()(int, int row, int col, double v) const {
+        int p = col_param[col];
+        p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
+        const size_t i = row + (size_t)col * ldq;
+        q[i] = fma(gp[p], v, D[i]);
+    }
+};
+struct EpiFaceScatter {        // dense n^2 x n^2 product -> padded NP x NP row-major matrix
+    double* F; int n, ldf; long long NP;
+    __device__ __forceinline__ void operator()(int, int row, int col, double v) const {
+        const size_t r = (size_t)(row / n) * ldf + row % n;
+        const size_t c = (size_t)(col / n) * ldf + col % n;
+        F[r * NP + c] = v;
+    }
+};
+
+cudaError_t face_slab_pass(const double* in, double* out, int nslab, int n, int ldf, const double* S, cudaStream_t st) {
+    DgemmProblem g{n, n, ldf, in, ldf, S, ldf};
+    g.sA = (long long)ldf * ldf;
+    g.sB = 0;
+    g.batch = nslab;
+    return dgemm_launch<CfgSlab>(g, 1, EpiSlabStore{out, (long long)ldf * ldf, ldf}, st);
+}
+
+cudaError_t face_slab_pass_scaled(const double* in, double* out, int nslab, int n, int ldf, const double* S,
+                                  const double* w, long long sW, int group, const double* colscale, cudaStream_t st) {
+    DgemmProblem g{n, n, ldf, in, ldf, S, ldf};
+    g.sA = (long long)ldf * ldf;
+    g.sB = 0;
+    g.batch = nslab;
+    return dgemm_launch<CfgSlab>(g, 1, EpiSlabScale{out, (long long)ldf * ldf, ldf, w, sW, group, colscale}, st);
+}
+
+// q = γ F p + D over ncols columns (F: NP x NP row-major padded; vectors NP per column).
+size_t face_fx_ws_doubles(long long NP, int ncols, int num_sms) {
+    return dgemm_streamk_ws_doubles<CfgFv>((int)NP, ncols, num_sms * OCC_FV);
+}
+cudaError_t face_fx(const double* F, long long NP, const double* p, double* q, const double* D, int ncols,
+                    const int* col_param, int n_param, const double* gp, double* ws, int* counters, int num_sms,
+                    cudaStream_t st) {
+    DgemmProblem g{(int)NP, ncols, (int)NP, F, (int)NP, p, (int)NP};
+    StreamK sk{ws, counters, 0};
+    const int G = dgemm_streamk_grid<CfgFv>((int)NP, ncols, (int)NP, num_sms, OCC_FV);
+    return dgemm_launch_streamk<CfgFv>(g, G, sk, EpiFaceFx{q, D, NP, col_param, n_param, gp}, st);
+}
+int face_fx_tiles(long long NP, int ncols) { return dgemm_tiles<CfgFv>((int)NP, ncols); }
+
+// F = B B^T scattered into the padded layout (B: n2 x n2 row-major, n2 = n^2, K padded to kp).
+cudaError_t face_gram_scatter(const double* B, int n2, int kp, double* F, int n, int ldf, long long NP,
+                              int num_sms, cudaStream_t st) {
+    DgemmProblem g{n2, n2, kp, B, kp, B, kp};
+    const int sk = dgemm_pick_splitk<CfgSlab>(n2, n2, kp, num_sms, 2);
+    return dgemm_launch<CfgSlab>(g, sk, EpiFaceScatter{F, n, ldf, NP}, st);
+}
+
+// ------------------------------------------------------------------------------------ layouts
+__global__ void k_face_copy_in(int n, int ldf, long long NP, int ncols, const double* __restrict__ src, int lds,
+                               double* __restrict__ dst) {
+    const long long n2 = (long long)n * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n2 * ncols;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long c = idx / n2, i = idx % n2;
+        dst[c * NP + (i / n) * ldf + i % n] = src[c * lds + i];
+    }
+}
+__global__ void k_face_copy_out(int n, int ldf, long long NP, int ncols, const double* __restrict__ src,
+                                double* __restrict__ dst, int ldd) {
+    const long long n2 = (long long)n * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n2 * ncols;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long c = idx / n2, i = idx % n2;
+        dst[c * ldd + i] = src[c * NP + (i / n) * ldf + i % n];
+    }
+}
+cudaError_t face_copy_in(int n, int ldf, long long NP, int ncols, const double* src, int lds, double* dst,
+                         cudaStream_t st) {
+    k_face_copy_in<<<1184, 256, 0, st>>>(n, ldf, NP, ncols, src, lds, dst);
+    return cudaGetLastError();
+}
+cudaError_t face_copy_out(int n, int ldf, long long NP, int ncols, const double* src, double* dst, int ldd,
+                          cudaStream_t st) {
+    k_face_copy_out<<<1184, 256, 0, st>>>(n, ldf, NP, ncols, src, dst, ldd);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------ stencils
+// Face pair (SURVEY §8 "verified stencils", oracle pin test_face_pair_3d):
+//   A_Γ = [4; -1 at (±1,0),(0,±1)],  M_Γ = (h^2/12)[6; 1 at (±1,0),(0,±1),(1,1),(-1,-1)].
+__device__ __forceinline__ double face_at(const double* v, int j, int k, int n, int ldf) {
+    return (j < 0 || k < 0 || j >= n || k >= n) ? 0.0 : v[j * ldf + k];
+}
+// y = a A v + b M v on one padded slab (0-based j, k)
+__device__ __forceinline__ double face_op(const double* v, int j, int k, int n, int ldf, double a, double bm) {
+    const double c = v[j * ldf + k];
+    const double nb = face_at(v, j - 1, k, n, ldf) + face_at(v, j + 1, k, n, ldf) + face_at(v, j, k - 1, n, ldf) +
+                      face_at(v, j, k + 1, n, ldf);
+    const double dg = face_at(v, j + 1, k + 1, n, ldf) + face_at(v, j - 1, k - 1, n, ldf);
+    return a * (4.0 * c - nb) + bm * (6.0 * c + nb + dg);
+}
+
+// M applied to the columns of a dense column-major n2 x ncol matrix (setup: B = M V).
+__global__ void k_face_mass_cols(int n, double hh12, const double* __restrict__ V, double* __restrict__ out, int n2,
+                                 int ncol, int ldo) {
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n2 * ncol;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int col = (int)(idx / n2), i = (int)(idx % n2);
+        const int j = i / n, k = i % n;
+        const double* v = V + (size_t)col * n2;
+        out[(size_t)col * ldo + i] = face_op(v, j, k, n, n, 0.0, hh12);
+    }
+}
+// dense assembly of the face pair (setup only, for the generalised eigensolver)
+__global__ void k_face_dense(int n, double hh12, double* __restrict__ A, double* __restrict__ M) {
+    const int n2 = n * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n2;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)idx, j = i / n, k = i % n;
+        auto setp = [&](int jj, int kk, double av, double mv) {
+            if (jj < 0 || kk < 0 || jj >= n || kk >= n) return;
+            const size_t col = (size_t)jj * n + kk;
+            A[col * n2 + i] = av;   // column-major (symmetric anyway)
+            M[col * n2 + i] = mv;
+        };
+        setp(j, k, 4.0, 6.0 * hh12);
+        setp(j - 1, k, -1.0, hh12); setp(j + 1, k, -1.0, hh12);
+        setp(j, k - 1, -1.0, hh12); setp(j, k + 1, -1.0, hh12);
+        setp(j + 1, k + 1, 0.0, hh12); setp(j - 1, k - 1, 0.0, hh12);
+    }
+}
+// scale columns and transpose: Out (row-major n2 x kp) = (V diag(w))^T^T ... Out[i][j] = V[i + j n2] w[j]
+__global__ void k_scale_transpose(const double* __restrict__ V, const double* __restrict__ w, int n2, double* __restrict__ out,
+                                  int kp) {
+    __shared__ double tile[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int j = by + r, i = bx + threadIdx.x;   // read V[i + j n2] (coalesced in i)
+        tile[r][threadIdx.x] = (i < n2 && j < n2) ? V[(size_t)j * n2 + i] * w[j] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = bx + r, j = by + threadIdx.x;   // write out[i][j] (coalesced in j)
+        if (i < n2 && j < kp) out[(size_t)i * kp + j] = (j < n2) ? tile[threadIdx.x][r] : 0.0;
+    }
+}
+
+cudaError_t face_dense_pair(int n, double hh12, double* A, double* M, cudaStream_t st) {
+    k_face_dense<<<1184, 256, 0, st>>>(n, hh12, A, M);
+    return cudaGetLastError();
+}
+cudaError_t face_mass_cols(int n, double hh12, const double* V, double* out, int ncol, int ldo, cudaStream_t st) {
+    k_face_mass_cols<<<1184, 256, 0, st>>>(n, hh12, V, out, n * n, ncol, ldo);
+    return cudaGetLastError();
+}
+cudaError_t scale_transpose(const double* V, const double* w, int n2, double* out, int kp, cudaStream_t st) {
+    dim3 grid((n2 + 31) / 32, (kp + 31) / 32);
+    k_scale_transpose<<<grid, dim3(32, 8), 0, st>>>(V, w, n2, out, kp);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------ inner PCG
+// Pair layout: pair q = s * C + c (system s of this rank, column c); vectors NP each.
+struct InnerArgs {
+    int n, ldf; long long NP;
+    int npair, C;                 // pairs, columns
+    double hh12;
+    const double* sys_a;          // [npair / C] coefficient of A (1 for poles, 0 for the mass term)
+    const double* sys_b;          // [npair / C] coefficient of M (-p for poles, 1 for the mass term)
+    double *x, *r, *p, *q, *z;    // [npair][NP]
+    double *rho, *rho0;           // [npair]
+    int* active;                  // [npair]
+    double rtol;
+};
+
+// deterministic block reduction
+__device__ __forceinline__ double block_sum(double a, double* red) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = a;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < W; w++) s += red[w];
+    __syncthreads();
+    return s;
+}
+
+// init: r = b_c, x = 0 (z, ρ set after the first preconditioner application)
+__global__ void k_inner_init(InnerArgs a, const double* __restrict__ b) {
+    const int pq = blockIdx.x;
+    const int c = pq % a.C;
+    const size_t off = (size_t)pq * a.NP;
+    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) {
+        a.r[off + i] = b[(size_t)c * a.NP + i];
+        a.x[off + i] = 0.0;
+    }
+}
+// after z = P0 r: ρ = r·z, ρ0 = ρ, p = z, active
+__global__ void k_inner_start(InnerArgs a) {
+    __shared__ double red[32];
+    const int pq = blockIdx.x;
+    const size_t off = (size_t)pq * a.NP;
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) {
+        s = fma(a.r[off + i], a.z[off + i], s);
+        a.p[off + i] = a.z[off + i];
+    }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) {
+        a.rho[pq] = s;
+        a.rho0[pq] = s;
+        a.active[pq] = s > 0.0 ? 1 : 0;
+    }
+}
+// q = (a A + b M) p, then α = ρ/(p·q), x += αp, r -= αq   (one CTA per pair)
+__global__ void k_inner_step1(InnerArgs a) {
+    __shared__ double red[32];
+    const int pq = blockIdx.x;
+    if (!a.active[pq]) return;
+    const int s = pq / a.C;
+    const double ca = a.sys_a[s], cb = a.sys_b[s] * a.hh12;
+    const size_t off = (size_t)pq * a.NP;
+    const double* pv = a.p + off;
+    double d = 0.0;
+    for (int i = threadIdx.x; i < a.n * a.ldf; i += blockDim.x) {
+        const int j = i / a.ldf, k = i % a.ldf;
+        if (k >= a.n) continue;
+        const double qi = face_op(pv, j, k, a.n, a.ldf, ca, cb);
+        a.q[off + i] = qi;
+        d = fma(pv[i], qi, d);
+    }
+    d = block_sum(d, red);
+    const double alpha = d > 0.0 ? a.rho[pq] / d : 0.0;
+    for (int i = threadIdx.x; i < a.n * a.ldf; i += blockDim.x) {
+        if (i % a.ldf >= a.n) continue;
+        a.x[off + i] = fma(alpha, pv[i], a.x[off + i]);
+        a.r[off + i] = fma(-alpha, a.q[off + i], a.r[off + i]);
+    }
+}
+// after z = P0 r: ρ' = r·z; converged if sqrt(ρ'/ρ0) <= rtol; else p = z + (ρ'/ρ) p
+__global__ void k_inner_step2(InnerArgs a, int* n_active) {
+    __shared__ double red[32];
+    const int pq = blockIdx.x;
+    if (!a.active[pq]) return;
+    const size_t off = (size_t)pq * a.NP;
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) s = fma(a.r[off + i], a.z[off + i], s);
+    s = block_sum(s, red);
+    if (!(s > a.rtol * a.rtol * a.rho0[pq])) {
+        if (threadIdx.x == 0) a.active[pq] = 0;
+        return;
+    }
+    const double beta = s / a.rho[pq];
+    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) a.p[off + i] = fma(beta, a.p[off + i], a.z[off + i]);
+    if (threadIdx.x == 0) {
+        a.rho[pq] = s;
+        atomicAdd(n_active, 1);
+    }
+}
+// z_c = Σ_s w_s x_{s,c}  in fixed system order (rank-local partial sum)
+__global__ void k_inner_combine(InnerArgs a, const double* __restrict__ w, int nsys, double* __restrict__ zout) {
+    const long long tot = a.NP * a.C;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long c = idx / a.NP, i = idx % a.NP;
+        double acc = 0.0;
+        for (int s = 0; s < nsys; s++) acc = fma(w[s], a.x[((size_t)s * a.C + c) * a.NP + i], acc);
+        zout[idx] = acc;
+    }
+}
+
+cudaError_t inner_init(const InnerArgs& a, const double* b, cudaStream_t st) {
+    k_inner_init<<<a.npair, 256, 0, st>>>(a, b);
+    return cudaGetLastError();
+}
+cudaError_t inner_start(const InnerArgs& a, cudaStream_t st) {
+    k_inner_start<<<a.npair, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t inner_step1(const InnerArgs& a, cudaStream_t st) {
+    k_inner_step1<<<a.npair, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t inner_step2(const InnerArgs& a, int* n_active, cudaStream_t st) {
+    k_inner_step2<<<a.npair, 256, 0, st>>>(a, n_active);
+    return cudaGetLastError();
+}
+cudaError_t inner_combine(const InnerArgs& a, const double* w, int nsys, double* zout, cudaStream_t st) {
+    k_inner_combine<<<1184, 256, 0, st>>>(a, w, nsys, zout);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------ outer PCG (3D)
+struct Pcg3 {
+    long long NP; int ncols;
+    double *x, *r, *p, *q, *z;   // padded face vectors [ncols][NP]
+    double *rho, *eta0, *relres;
+    int *active, *iters;
+    double* hist;
+    double rtol; int norm_kind;
+    int* status;
+};
+// k = 0: r = b (already in r), z given: ρ = r·z, η0, p = z, x = 0
+__global__ void k3_pcg_start(Pcg3 s) {
+    __shared__ double red[32];
+    const int c = blockIdx.x;
+    const size_t off = (size_t)c * s.NP;
+    double rz = 0.0, zz = 0.0;
+    for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) {
+        const double zi = s.z[off + i];
+        rz = fma(s.r[off + i], zi, rz);
+        zz = fma(zi, zi, zz);
+        s.p[off + i] = zi;
+        s.x[off + i] = 0.0;
+    }
+    rz = block_sum(rz, red);
+    zz = block_sum(zz, red);
+    if (threadIdx.x == 0) {
+        const double eta0 = s.norm_kind == 0 ? sqrt(fmax(rz, 0.0)) : sqrt(zz);
+        s.rho[c] = rz; s.eta0[c] = eta0; s.iters[c] = 0; s.relres[c] = eta0 > 0.0 ? 1.0 : 0.0;
+        s.active[c] = (eta0 > 0.0 && rz >= 0.0) ? 1 : 0;
+        if (rz < 0.0) atomicExch(s.status, (int)DD_ENOTSPD);
+        if (c == 0 && s.hist) s.hist[0] = eta0;
+    }
+}
+// α = ρ/(p·q); x += αp; r -= αq
+__global__ void k3_pcg_alpha(Pcg3 s) {
+    __shared__ double red[32];
+    const int c = blockIdx.x;
+    if (!s.active[c]) return;
+    const size_t off = (size_t)c * s.NP;
+    double pq = 0.0;
+    for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) pq = fma(s.p[off + i], s.q[off + i], pq);
+    pq = block_sum(pq, red);
+    if (!(pq > 0.0)) {
+        if (threadIdx.x == 0) { atomicExch(s.status, (int)DD_ENOTSPD); s.active[c] = 0; }
+        return;
+    }
+    const double alpha = s.rho[c] / pq;
+    for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) {
+        s.x[off + i] = fma(alpha, s.p[off + i], s.x[off + i]);
+        s.r[off + i] = fma(-alpha, s.q[off + i], s.r[off + i]);
+    }
+}
+// ρ' = r·z; η test; β; p = z + βp
+__global__ void k3_pcg_beta(Pcg3 s, int k, int maxit, int* n_active) {
+    __shared__ double red[32];
+    const int c = blockIdx.x;
+    if (!s.active[c]) return;
+    const size_t off = (size_t)c * s.NP;
+    double rz = 0.0, zz = 0.0;
+    for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) {
+        const double zi = s.z[off + i];
+        rz = fma(s.r[off + i], zi, rz);
+        zz = fma(zi, zi, zz);
+    }
+    rz = block_sum(rz, red);
+    zz = block_sum(zz, red);
+    const double eta = s.norm_kind == 0 ? sqrt(fmax(rz, 0.0)) : sqrt(zz);
+    const bool conv = eta <= s.rtol * s.eta0[c];
+    if (threadIdx.x == 0) {
+        s.iters[c] = k;
+        s.relres[c] = eta / s.eta0[c];
+        if (c == 0 && s.hist) s.hist[k] = eta;
+        if (rz < 0.0) atomicExch(s.status, (int)DD_ENOTSPD);
+    }
+    if (conv || rz < 0.0 || k >= maxit) {
+        if (threadIdx.x == 0) s.active[c] = 0;
+        return;
+    }
+    const double beta = rz / s.rho[c];
+    for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) s.p[off + i] = fma(beta, s.p[off + i], s.z[off + i]);
+    if (threadIdx.x == 0) {
+        s.rho[c] = rz;
+        atomicAdd(n_active, 1);
+    }
+}
+cudaError_t pcg3_start(const Pcg3& s, cudaStream_t st) {
+    k3_pcg_start<<<s.ncols, 512, 0, st>>>(s);
+    return cudaGetLastError();
+}
+cudaError_t pcg3_alpha(const Pcg3& s, cudaStream_t st) {
+    k3_pcg_alpha<<<s.ncols, 512, 0, st>>>(s);
+    return cudaGetLastError();
+}
+cudaError_t pcg3_beta(const Pcg3& s, int k, int maxit, int* n_active, cudaStream_t st) {
+    k3_pcg_beta<<<s.ncols, 512, 0, st>>>(s, k, maxit, n_active);
+    return cudaGetLastError();
+}
+
+}  // namespace dd

@@ -20,7 +20,7 @@ constexpr int SK_MIN_UNITS = 64;   // below this the segment fix-ups outweigh th
 
 struct EpiStore {
     double* C; int ldc;
-    __device__ __forceinline__ void operator()(int row, int col, double v) const { C[row + (size_t)col * ldc] = v; }
+    __device__ __forceinline__ void operator()(int, int row, int col, double v) const { C[row + (size_t)col * ldc] = v; }
 };
 
 struct EpiSchurDst {
@@ -29,7 +29,7 @@ struct EpiSchurDst {
     const double* X; int ldx;
     const int* col_param; int n_param;
     const double *Kp, *gp, *s;
-    __device__ __forceinline__ void operator()(int row, int col, double v) const {
+    __device__ __forceinline__ void operator()(int, int row, int col, double v) const {
         int p = col_param[col];
         p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
         C[row + (size_t)col * ldc] = Kp[p] * s[row] * v;

@@ -14,7 +14,7 @@ using namespace dd;
 
 struct StoreEpi {
     double* C; int ldc;
-    __device__ void operator()(int row, int col, double v) const { C[row + (size_t)col * ldc] = v; }
+    __device__ void operator()(int, int row, int col, double v) const { C[row + (size_t)col * ldc] = v; }
 };
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)

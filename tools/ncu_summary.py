@@ -42,7 +42,9 @@ def launches(path):
 def full(path, name=None):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
-    h = rows[0]
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0,
+             "msecond": 1e3}
     out = []
     for r in rows[2:]:
         rec = {"kernel": r[h.index("Kernel Name")][:120]}
@@ -50,9 +52,13 @@ def full(path, name=None):
             continue
         for k in KEYS:
             if k in h:
-                v = r[h.index(k)].replace(",", "")
+                j = h.index(k)
+                v = r[j].replace(",", "")
                 try:
-                    rec[k] = float(v)
+                    f = float(v) * scale.get(units[j], 1.0)
+                    key = k + (" [bytes]" if units[j] in ("byte", "Kbyte", "Mbyte", "Gbyte") else
+                               " [us]" if units[j] in ("nsecond", "usecond", "msecond") else "")
+                    rec[key] = f
                 except ValueError:
                     rec[k] = v
         out.append(rec)
