@@ -133,6 +133,11 @@ dd_status dd_pcg_solve_host(dd_ctx* ctx, int ncols, const int* col_param_host,
 dd_status dd_destroy(dd_ctx* ctx);
 const char* dd_last_error(void);
 
+/* 128-byte ncclUniqueId for dd_dist (rank 0 calls it and broadcasts the bytes). */
+dd_status dd_nccl_unique_id(void* out128);
+/* 3D handles: inner (shifted face system) CG iterations of the last preconditioner apply. */
+dd_status dd_inner_iterations(const dd_ctx* ctx, int* iters);
+
 /* ---------------------------------------------------------------- instrumentation
  * Per-kernel-class device time (CUDA events on the handle's stream, recorded around each
  * launch while enabled; graphs are bypassed while enabled).  Classes: */

@@ -23,7 +23,8 @@ KCLASS = ["gemm_dst", "gemm_schur", "polesum_pcg", "other"]
 
 EXPORTS = ["dd_setup", "dd_interface_size", "dd_apply_schur", "dd_apply_precond", "dd_pcg_solve",
            "dd_pcg_solve_host", "dd_destroy", "dd_last_error", "dd_profile_enable", "dd_profile_read",
-           "dd_launch_count", "dd_query_config", "dd_test_dgemm", "dd_last_solve_ms"]
+           "dd_launch_count", "dd_query_config", "dd_test_dgemm", "dd_last_solve_ms", "dd_nccl_unique_id",
+           "dd_inner_iterations"]
 
 
 class DDError(RuntimeError):
@@ -67,6 +68,8 @@ def load():
     lib.dd_launch_count.argtypes = [P]; lib.dd_launch_count.restype = ctypes.c_longlong
     lib.dd_query_config.argtypes = [P, P, P, P, P]; lib.dd_query_config.restype = I
     lib.dd_last_solve_ms.argtypes = [P, P]; lib.dd_last_solve_ms.restype = I
+    lib.dd_nccl_unique_id.argtypes = [P]; lib.dd_nccl_unique_id.restype = I
+    lib.dd_inner_iterations.argtypes = [P, P]; lib.dd_inner_iterations.restype = I
     lib.dd_test_dgemm.argtypes = [I, I, I, P, I, P, I, P, I, I, P]; lib.dd_test_dgemm.restype = I
     _lib = lib
     return lib
@@ -103,7 +106,9 @@ class Solver:
     zero residues).
     """
 
-    def __init__(self, dim: int, N: int, params, ras, max_cols: int, device: int = 0, stream=None):
+    def __init__(self, dim: int, N: int, params, ras, max_cols: int, device: int = 0, stream=None, dist=None):
+        """dist: None, or (rank, world, mode, unique_id_bytes) with mode DD_SHARD_COLUMNS (0) or
+        DD_SHARD_POLES (1); the 128-byte unique id comes from nccl_unique_id() on rank 0."""
         import torch
         self._torch = torch
         lib = load()
@@ -120,9 +125,15 @@ class Solver:
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         mesh = _Mesh(dim, N, 0)
         h = ctypes.c_void_p()
+        dptr = None
+        if dist is not None:
+            rank, world, mode, uid = dist
+            self._uid = ctypes.create_string_buffer(bytes(uid) if uid is not None else bytes(128), 128)
+            self._dist = _Dist(int(rank), int(world), ctypes.cast(self._uid, ctypes.c_void_p), int(mode))
+            dptr = ctypes.byref(self._dist)
         st = lib.dd_setup(ctypes.byref(mesh), self.n_param, K.ctypes.data, mu.ctypes.data, m, poles.ctypes.data,
                           res.ctypes.data, c0.ctypes.data, int(max_cols), int(device),
-                          ctypes.c_void_p(self.stream.cuda_stream), None, ctypes.byref(h))
+                          ctypes.c_void_p(self.stream.cuda_stream), dptr, ctypes.byref(h))
         _check(st)
         self._h = h
         self.max_cols = int(max_cols)
@@ -193,6 +204,11 @@ class Solver:
         _check(load().dd_last_solve_ms(self._h, ctypes.byref(v)))
         return v.value
 
+    def inner_iterations(self) -> int:
+        v = ctypes.c_int()
+        _check(load().dd_inner_iterations(self._h, ctypes.byref(v)))
+        return v.value
+
     def launch_count(self) -> int:
         return int(load().dd_launch_count(self._h))
 
@@ -212,6 +228,12 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().dd_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
 
 
 def test_dgemm(A, B, splitk=1):

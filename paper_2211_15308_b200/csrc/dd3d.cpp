@@ -1,0 +1,345 @@
+// libdd, 3D interfaces (Γ = face {x = 0} of the unit cube; BASELINE.json config 4).
+// Setup: sine matrix, Schur weights, the dense fractional term
+// F = (M U) Λ^{-1/2} (M U)^T of the consistent P1 face pair from a generalised eigensolve
+// (cuSOLVER Dsygvd — setup only, Eq.(7)), pole systems and their sine-diagonal
+// preconditioners, and (pole split) the NCCL communicator.  Applies: see face3d.cu.
+#include <cusolverDn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "dd_ctx.h"
+
+namespace dd {
+
+static const long double PI_L = 3.141592653589793238462643383279502884L;
+
+#define SK(expr)                                                                                          \
+    do {                                                                                                  \
+        cusolverStatus_t _s = (expr);                                                                     \
+        if (_s != CUSOLVER_STATUS_SUCCESS) return set_error(DD_ECUDA, std::string(#expr) + " failed");    \
+    } while (0)
+#define NK(expr)                                                                                                  \
+    do {                                                                                                          \
+        ncclResult_t _r = (expr);                                                                                 \
+        if (_r != ncclSuccess) return set_error(DD_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));   \
+    } while (0)
+
+dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const double* poles, const double* residues,
+                   const double* c0, const dd_dist* dist) {
+    (void)K; (void)mu_inv;
+    Face3& f = c->f3;
+    const int N = c->N, n = c->n;
+    if (c->n_param != 1) return set_error(DD_EUNSUPPORTED, "3D handles take one parameter set");
+    f.n = n;
+    f.n2 = n * n;
+    f.ldf = round_up(n, 16);
+    f.NP = (long long)f.ldf * f.ldf;
+    const long double h = 1.0L / N;
+    const double hh12 = (double)(h * h / 12.0L);
+    const int Srows = std::max(round_up(n, 64), f.ldf);
+    const size_t slack = (size_t)64 * f.ldf;   // slab GEMM tiles may read up to 64 rows past a slab
+
+    // --- sine matrix and Schur weights s_ab = h(1 + (σ_a+σ_b)/2 - Σ_m (2/N) sin^2(mπ/N)/(σ_m+σ_a+σ_b))
+    std::vector<long double> sintab(2 * N), sig(n);
+    for (int a = 0; a < 2 * N; a++) sintab[a] = sinl(PI_L * a / N);
+    for (int a = 1; a <= n; a++) {
+        const long double sh = sinl(PI_L * a / (2.0L * N));
+        sig[a - 1] = 4.0L * sh * sh;
+    }
+    const long double sc = sqrtl(2.0L / N);
+    std::vector<double> Sh((size_t)Srows * f.ldf, 0.0), swh(f.NP, 0.0);
+    for (int q = 1; q <= n; q++)
+        for (int r = 1; r <= n; r++) Sh[(size_t)(q - 1) * f.ldf + (r - 1)] = (double)(sc * sintab[((long long)q * r) % (2 * N)]);
+    for (int a = 0; a < n; a++)
+        for (int b = 0; b < n; b++) {
+            long double g = 0.0L;
+            for (int m = 0; m < n; m++) {
+                const long double s1 = sintab[m + 1];
+                g += (2.0L / N) * s1 * s1 / (sig[m] + sig[a] + sig[b]);
+            }
+            swh[(size_t)a * f.ldf + b] = (double)(h * (1.0L + 0.5L * (sig[a] + sig[b]) - g));
+        }
+    DD_CK(dalloc(c, &f.S, Sh.size()));
+    DD_CK(cudaMemcpyAsync(f.S, Sh.data(), Sh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    DD_CK(dalloc(c, &f.sw, (size_t)f.NP));
+    DD_CK(cudaMemcpyAsync(f.sw, swh.data(), swh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+
+    // --- dense fractional term via the generalised eigenproblem A_Γ U = M_Γ U Λ, U^T M U = I
+    {
+        const int n2 = f.n2;
+        const int kp = round_up(n2, 16);
+        const size_t big = (size_t)round_up(n2, 64) * kp + 1024;
+        double *dA = nullptr, *dM = nullptr, *dW = nullptr, *work = nullptr;
+        int* info = nullptr;
+        DD_CK(cudaMalloc(&dA, big * sizeof(double)));
+        DD_CK(cudaMalloc(&dM, big * sizeof(double)));
+        DD_CK(cudaMalloc(&dW, (size_t)n2 * sizeof(double)));
+        DD_CK(cudaMalloc(&info, sizeof(int)));
+        DD_CK(cudaMemsetAsync(dA, 0, big * sizeof(double), c->stream));
+        DD_CK(cudaMemsetAsync(dM, 0, big * sizeof(double), c->stream));
+        DD_CK(face_dense_pair(n, hh12, dA, dM, c->stream));
+        cusolverDnHandle_t hs = nullptr;
+        SK(cusolverDnCreate(&hs));
+        SK(cusolverDnSetStream(hs, c->stream));
+        int lwork = 0;
+        SK(cusolverDnDsygvd_bufferSize(hs, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n2, dA,
+                                       n2, dM, n2, dW, &lwork));
+        DD_CK(cudaMalloc(&work, (size_t)lwork * sizeof(double)));
+        SK(cusolverDnDsygvd(hs, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n2, dA, n2, dM, n2,
+                            dW, work, lwork, info));
+        int hinfo = 0;
+        std::vector<double> lam(n2);
+        DD_CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        DD_CK(cudaMemcpyAsync(lam.data(), dW, n2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        DD_CK(cudaStreamSynchronize(c->stream));
+        cusolverDnDestroy(hs);
+        cudaFree(work);
+        if (hinfo != 0) return set_error(DD_ECUDA, "cusolverDnDsygvd info != 0");
+        f.lam_min = lam.front();
+        f.lam_max = lam.back();
+        std::vector<double> w4(n2);
+        for (int j = 0; j < n2; j++) w4[j] = (double)powl((long double)lam[j], -0.25L);
+        DD_CK(cudaMemcpyAsync(dW, w4.data(), n2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        // B = M U Λ^{-1/4} (column-major in dM), then row-major in dA; F = B B^T into the padded layout
+        DD_CK(face_mass_cols(n, hh12, dA, dM, n2, n2, c->stream));
+        DD_CK(cudaMemsetAsync(dA, 0, big * sizeof(double), c->stream));
+        DD_CK(scale_transpose(dM, dW, n2, dA, kp, c->stream));
+        const size_t frows = (size_t)round_up((int)f.NP, 128);
+        DD_CK(dalloc(c, &f.F, frows * (size_t)f.NP));
+        DD_CK(face_gram_scatter(dA, n2, kp, f.F, n, f.ldf, f.NP, c->num_sms, c->stream));
+        DD_CK(cudaStreamSynchronize(c->stream));
+        cudaFree(dA); cudaFree(dM); cudaFree(dW); cudaFree(info);
+    }
+
+    // --- pole systems: [M term if c0 != 0] + [poles with non-zero residue];  (a, b, w): a A + b M
+    struct Sys { double a, b, w, cost; };
+    std::vector<Sys> sys;
+    if (c0[0] != 0.0) sys.push_back({0.0, 1.0, c0[0], 1.0});
+    for (int k = 0; k < c->n_poles; k++) {
+        const double p = poles[k], r = residues[k];
+        if (r == 0.0) continue;
+        sys.push_back({1.0, -p, r, std::sqrt((f.lam_max - p) / (f.lam_min - p))});
+    }
+    f.nsys_total = (int)sys.size();
+    f.rank = dist ? dist->rank : 0;
+    f.world = dist ? dist->world : 1;
+    std::vector<int> mine;
+    if (f.world > 1 && dist->mode == DD_SHARD_POLES) {
+        // balanced by predicted inner-CG cost (longest-processing-time greedy)
+        std::vector<int> order(sys.size());
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return sys[x].cost > sys[y].cost; });
+        std::vector<double> load(f.world, 0.0);
+        std::vector<int> owner(sys.size(), 0);
+        for (int i : order) {
+            int r = 0;
+            for (int q = 1; q < f.world; q++)
+                if (load[q] < load[r]) r = q;
+            owner[i] = r;
+            load[r] += sys[i].cost;
+        }
+        for (int i = 0; i < (int)sys.size(); i++)
+            if (owner[i] == f.rank) mine.push_back(i);
+    } else {
+        for (int i = 0; i < (int)sys.size(); i++) mine.push_back(i);
+    }
+    f.sys_ids = mine;
+    f.nsys = (int)mine.size();
+    const int ns = std::max(1, f.nsys);
+    std::vector<double> sa(ns, 0.0), sb(ns, 1.0), swt(ns, 0.0), pd((size_t)ns * f.NP, 0.0);
+    for (int i = 0; i < f.nsys; i++) {
+        const Sys& s = sys[mine[i]];
+        sa[i] = s.a; sb[i] = s.b; swt[i] = s.w;
+        for (int a = 0; a < n; a++)
+            for (int b = 0; b < n; b++) {
+                const long double ca = 1.0L - 0.5L * sig[a], cb = 1.0L - 0.5L * sig[b];
+                const long double alpha = sig[a] + sig[b];
+                const long double mut = (long double)hh12 * (6.0L + 2.0L * ca + 2.0L * cb + 2.0L * ca * cb);
+                pd[(size_t)i * f.NP + (size_t)a * f.ldf + b] = (double)(1.0L / ((long double)s.a * alpha + (long double)s.b * mut));
+            }
+    }
+    DD_CK(dalloc(c, &f.sys_a, ns));
+    DD_CK(dalloc(c, &f.sys_b, ns));
+    DD_CK(dalloc(c, &f.sys_w, ns));
+    DD_CK(dalloc(c, &f.pdiag, pd.size()));
+    DD_CK(cudaMemcpyAsync(f.sys_a, sa.data(), ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    DD_CK(cudaMemcpyAsync(f.sys_b, sb.data(), ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    DD_CK(cudaMemcpyAsync(f.sys_w, swt.data(), ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    DD_CK(cudaMemcpyAsync(f.pdiag, pd.data(), pd.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+
+    // --- per-parameter K, γ and workspaces
+    DD_CK(dalloc(c, &c->Kp, c->n_param));
+    DD_CK(dalloc(c, &c->gp, c->n_param));
+    DD_CK(cudaMemcpyAsync(c->Kp, K, c->n_param * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    DD_CK(cudaMemcpyAsync(c->gp, mu_inv, c->n_param * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    const int cp8 = round_up(c->max_cols, 8);
+    const size_t vec = (size_t)f.NP * cp8 + slack;
+    for (double** v : {&f.x, &f.r, &f.p, &f.q, &f.z, &f.U1, &f.U2}) DD_CK(dalloc(c, v, vec));
+    const size_t pairs = (size_t)ns * c->max_cols;
+    const size_t pv = (size_t)f.NP * pairs + slack;
+    for (double** v : {&f.ix, &f.ir, &f.ip, &f.iq, &f.iz, &f.T1, &f.T2}) DD_CK(dalloc(c, v, pv));
+    DD_CK(dalloc(c, &f.irho, pairs));
+    DD_CK(dalloc(c, &f.irho0, pairs));
+    DD_CK(dalloc(c, &f.iactive, pairs));
+    DD_CK(dalloc(c, &f.Kcol, cp8));
+    DD_CK(dalloc(c, &f.fx_ws, face_fx_ws_doubles(f.NP, cp8, c->num_sms)));
+    DD_CK(dalloc(c, &f.fx_cnt, face_fx_tiles(f.NP, cp8) + 1));
+    DD_CK(dalloc(c, &c->bst, (size_t)f.n2 * c->max_cols));
+    DD_CK(dalloc(c, &c->xst, (size_t)f.n2 * c->max_cols));
+    DD_CK(dalloc(c, &c->colp_st, c->max_cols));
+    if (const char* it = std::getenv("DD_INNER_MAXIT")) f.inner_maxit = std::max(1, atoi(it));
+
+    // --- NCCL communicator for the pole split (bootstrapped by the caller's unique id)
+    if (f.world > 1 && dist->mode == DD_SHARD_POLES) {
+        if (!dist->nccl_unique_id) return set_error(DD_EINVAL, "pole split needs an ncclUniqueId");
+        ncclUniqueId id;
+        std::memcpy(&id, dist->nccl_unique_id, sizeof(id));
+        ncclComm_t comm = nullptr;
+        NK(ncclCommInitRank(&comm, f.world, id, f.rank));
+        f.nccl = comm;
+    }
+    DD_CK(cudaStreamSynchronize(c->stream));
+    return DD_OK;
+}
+
+void destroy_3d(dd_ctx* c) {
+    if (c->f3.nccl) {
+        ncclCommDestroy(static_cast<ncclComm_t>(c->f3.nccl));
+        c->f3.nccl = nullptr;
+    }
+}
+
+// y = S x on padded face vectors p -> q
+static dd_status schur_core(dd_ctx* c, int ncols, const int* colp, const double* p, double* q) {
+    Face3& f = c->f3;
+    DD_TIMED(DD_KCLASS_OTHER, gather_param(ncols, colp, c->n_param, c->Kp, f.Kcol, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(p, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass_scaled(f.U1, f.U2, ncols, f.n, f.ldf, f.S, f.sw, 0, 1, f.Kcol, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U2, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, f.NP, p, q, f.U2, ncols, colp, c->n_param, c->gp, f.fx_ws, f.fx_cnt,
+                                           c->num_sms, c->stream));
+    return DD_OK;
+}
+
+// z = P_RA r on padded face vectors (rank-local systems, then the allreduce of the pole split)
+static dd_status precond_core(dd_ctx* c, int ncols, const double* r, double* z) {
+    Face3& f = c->f3;
+    if (f.nsys == 0) {
+        DD_CK(cudaMemsetAsync(z, 0, sizeof(double) * (size_t)f.NP * ncols, c->stream));
+    } else {
+        InnerArgs a{};
+        a.n = f.n; a.ldf = f.ldf; a.NP = f.NP;
+        a.npair = f.nsys * ncols; a.C = ncols;
+        a.hh12 = (double)(1.0L / ((long double)c->N * c->N * 12.0L));
+        a.sys_a = f.sys_a; a.sys_b = f.sys_b;
+        a.x = f.ix; a.r = f.ir; a.p = f.ip; a.q = f.iq; a.z = f.iz;
+        a.rho = f.irho; a.rho0 = f.irho0; a.active = f.iactive; a.rtol = f.inner_rtol;
+        auto dst_precond = [&]() -> dd_status {   // z = Q diag(1/(a α + b μ̃)) Q r per pair
+            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.ir, f.T1, a.npair, f.n, f.ldf, f.S, c->stream));
+            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_scaled(f.T1, f.T2, a.npair, f.n, f.ldf, f.S, f.pdiag, f.NP, ncols,
+                                                              nullptr, c->stream));
+            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.T2, f.T1, a.npair, f.n, f.ldf, f.S, c->stream));
+            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.T1, f.iz, a.npair, f.n, f.ldf, f.S, c->stream));
+            return DD_OK;
+        };
+        DD_TIMED(DD_KCLASS_POLESUM, inner_init(a, r, c->stream));
+        dd_status s = dst_precond();
+        if (s != DD_OK) return s;
+        DD_TIMED(DD_KCLASS_POLESUM, inner_start(a, c->stream));
+        int it = 0;
+        for (it = 1; it <= f.inner_maxit; it++) {
+            DD_TIMED(DD_KCLASS_POLESUM, inner_step1(a, c->stream));
+            s = dst_precond();
+            if (s != DD_OK) return s;
+            DD_CK(cudaMemsetAsync(c->ints + 1, 0, sizeof(int), c->stream));
+            DD_TIMED(DD_KCLASS_POLESUM, inner_step2(a, c->ints + 1, c->stream));
+            if (it % 4 == 0 || it == f.inner_maxit) {
+                DD_CK(cudaMemcpyAsync(c->h_ints + 1, c->ints + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+                DD_CK(cudaStreamSynchronize(c->stream));
+                if (c->h_ints[1] == 0) break;
+            }
+        }
+        f.last_inner_iters = std::min(it, f.inner_maxit);
+        DD_TIMED(DD_KCLASS_POLESUM, inner_combine(a, f.sys_w, f.nsys, z, c->stream));
+    }
+    if (f.nccl) {
+        NK(ncclAllReduce(z, z, (size_t)f.NP * ncols, ncclDouble, ncclSum, static_cast<ncclComm_t>(f.nccl), c->stream));
+    }
+    return DD_OK;
+}
+
+dd_status schur_3d(dd_ctx* c, int ncols, const int* colp, const double* xin, double* yout, bool user_layout) {
+    Face3& f = c->f3;
+    if (!user_layout) return schur_core(c, ncols, colp, xin, yout);
+    DD_TIMED(DD_KCLASS_OTHER, face_copy_in(f.n, f.ldf, f.NP, ncols, xin, f.n2, f.p, c->stream));
+    dd_status s = schur_core(c, ncols, colp, f.p, f.q);
+    if (s != DD_OK) return s;
+    DD_TIMED(DD_KCLASS_OTHER, face_copy_out(f.n, f.ldf, f.NP, ncols, f.q, yout, f.n2, c->stream));
+    return DD_OK;
+}
+
+dd_status precond_3d(dd_ctx* c, int ncols, const int* colp, const double* rin, double* zout, bool user_layout) {
+    (void)colp;
+    Face3& f = c->f3;
+    if (!user_layout) return precond_core(c, ncols, rin, zout);
+    DD_TIMED(DD_KCLASS_OTHER, face_copy_in(f.n, f.ldf, f.NP, ncols, rin, f.n2, f.r, c->stream));
+    dd_status s = precond_core(c, ncols, f.r, f.z);
+    if (s != DD_OK) return s;
+    DD_TIMED(DD_KCLASS_OTHER, face_copy_out(f.n, f.ldf, f.NP, ncols, f.z, zout, f.n2, c->stream));
+    return DD_OK;
+}
+
+dd_status pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
+                 int norm_kind) {
+    Face3& f = c->f3;
+    DD_TIMED(DD_KCLASS_OTHER, face_copy_in(f.n, f.ldf, f.NP, ncols, b, f.n2, f.r, c->stream));
+    dd_status s = precond_core(c, ncols, f.r, f.z);
+    if (s != DD_OK) return s;
+    Pcg3 st{};
+    st.NP = f.NP; st.ncols = ncols;
+    st.x = f.x; st.r = f.r; st.p = f.p; st.q = f.q; st.z = f.z;
+    st.rho = c->rho; st.eta0 = c->eta0; st.relres = c->relres; st.active = c->active; st.iters = c->iters;
+    st.hist = c->hist; st.rtol = rtol; st.norm_kind = norm_kind; st.status = c->ints + 4;
+    DD_TIMED(DD_KCLASS_OTHER, pcg3_start(st, c->stream));
+    int k = 0;
+    for (k = 1; k <= maxit; k++) {
+        s = schur_core(c, ncols, colp, f.p, f.q);
+        if (s != DD_OK) return s;
+        DD_TIMED(DD_KCLASS_OTHER, pcg3_alpha(st, c->stream));
+        s = precond_core(c, ncols, f.r, f.z);
+        if (s != DD_OK) return s;
+        DD_CK(cudaMemsetAsync(c->ints + 2, 0, sizeof(int), c->stream));
+        DD_TIMED(DD_KCLASS_OTHER, pcg3_beta(st, k, maxit, c->ints + 2, c->stream));
+        DD_CK(cudaMemcpyAsync(c->h_ints + 2, c->ints + 2, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        DD_CK(cudaStreamSynchronize(c->stream));
+        if (c->h_ints[2] == 0) break;
+    }
+    c->h_ints[0] = std::min(k, maxit);
+    DD_CK(cudaMemcpyAsync(c->ints, c->h_ints, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    DD_CK(cudaStreamSynchronize(c->stream));
+    DD_TIMED(DD_KCLASS_OTHER, face_copy_out(f.n, f.ldf, f.NP, ncols, f.x, x, f.n2, c->stream));
+    return DD_OK;
+}
+
+}  // namespace dd
+
+extern "C" dd_status dd_nccl_unique_id(void* out128) {
+    if (!out128) return dd::set_error(DD_EINVAL, "NULL buffer");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return dd::set_error(DD_ENCCL, ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+    return DD_OK;
+}
+
+extern "C" dd_status dd_inner_iterations(const dd_ctx* c, int* iters) {
+    if (!c || !iters) return dd::set_error(DD_EINVAL, "NULL argument");
+    *iters = c->f3.last_inner_iters;
+    return DD_OK;
+}

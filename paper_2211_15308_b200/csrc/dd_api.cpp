@@ -312,8 +312,10 @@ extern "C" dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K,
             if (!std::isfinite(r)) return fail(DD_EINVAL, "residues must be finite");
         }
     }
-    if (dist && dist->world > 1) return fail(DD_EUNSUPPORTED, "distributed handles: not in this build yet");
-    if (mesh->dim == 3) return fail(DD_EUNSUPPORTED, "3D interfaces: not in this build yet");
+    if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)) return fail(DD_EINVAL, "bad rank/world");
+    if (dist && dist->mode != DD_SHARD_COLUMNS && dist->mode != DD_SHARD_POLES) return fail(DD_EINVAL, "bad dist mode");
+    if (dist && dist->world > 1 && dist->mode == DD_SHARD_POLES && mesh->dim != 3)
+        return fail(DD_EUNSUPPORTED, "pole split is implemented for 3D interfaces (2D shards by columns)");
 
     dd_ctx* c = new dd_ctx();
     c->dim = mesh->dim;
@@ -335,7 +337,8 @@ extern "C" dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K,
     if (const char* ns = std::getenv("DD_NO_SMALL")) c->small_ok = !(ns[0] == '1');
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DD_ECUDA, "cudaSetDevice failed"));
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-    dd_status s = setup_2d(c, K, mu_inv, poles, residues, c0);
+    dd_status s = c->dim == 2 ? setup_2d(c, K, mu_inv, poles, residues, c0)
+                              : setup_3d(c, K, mu_inv, poles, residues, c0, dist);
     if (s != DD_OK) return bail(s);
     c->hist_cap = 4096;
     if (cudaMalloc(&c->rho, sizeof(double) * (3 * (size_t)max_cols + c->hist_cap + 8)) != cudaSuccess)
@@ -403,6 +406,7 @@ extern "C" dd_status dd_apply_schur(dd_ctx* c, int ncols, const int* colp, const
     if (!x || !y) return fail(DD_EINVAL, "x/y NULL");
     CK(cudaSetDevice(c->device));
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
+    if (c->dim == 3) return schur_3d(c, ncols, colp, x, y, true);
     TIMED(DD_KCLASS_OTHER, launch_copy_cols(c->n, ncols, x, c->n, c->xw, c->ldv, c->stream));
     return schur_gemms(c, ncols, colp, c->xw, y, c->n);
 }
@@ -413,8 +417,9 @@ extern "C" dd_status dd_apply_precond(dd_ctx* c, int ncols, const int* colp, con
     if (ncols == 0) return DD_OK;
     if (!r || !z) return fail(DD_EINVAL, "r/z NULL");
     CK(cudaSetDevice(c->device));
-    c->last_ps_warps = polesum_warps(c->geom);
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
+    if (c->dim == 3) return precond_3d(c, ncols, colp, r, z, true);
+    c->last_ps_warps = polesum_warps(c->geom);
     TIMED(DD_KCLASS_POLESUM, launch_precond(ncols, colp, c->geom, c->tabs, r, c->n, z, c->n, c->stream));
     return DD_OK;
 }
@@ -505,7 +510,10 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
     c->last_ps_warps = polesum_warps(c->geom);
     c->last_graph = 0;
     c->last_small = 0;
-    if (c->small_ok && pcg_small_supported(c->n)) {
+    if (c->dim == 3) {
+        dd_status s3 = pcg_3d(c, ncols, colp, b, x, rtol, maxit, norm_kind);
+        if (s3 != DD_OK) return s3;
+    } else if (c->small_ok && pcg_small_supported(c->n)) {
         // whole PCG in one persistent launch (small interfaces)
         c->last_small = 1;
         TIMED(DD_KCLASS_POLESUM, launch_pcg_small(st, c->geom, c->tabs, b, c->n, c->W, c->lda, c->Kpad, c->sw, c->Kp,
@@ -608,6 +616,7 @@ extern "C" dd_status dd_destroy(dd_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    destroy_3d(c);
     for (auto& e : c->solve_ev) if (e) cudaEventDestroy(e);
     for (auto& e : c->ev_pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (auto& e : c->ev_free) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }

@@ -110,4 +110,51 @@ cudaError_t launch_copy_cols(int n, int ncols, const double* src, int lds, doubl
                              cudaStream_t st);
 cudaError_t launch_check_params(int ncols, const int* col_param, int n_param, int* flag, cudaStream_t st);
 
+// ----------------------------------------------------------------------------- 3D face (face3d.cu)
+struct InnerArgs {
+    int n, ldf; long long NP;
+    int npair, C;                 // pairs (= systems x columns), columns
+    double hh12;                  // h^2 / 12
+    const double* sys_a;          // [systems] coefficient of A_Γ (1 for poles, 0 for the mass term)
+    const double* sys_b;          // [systems] coefficient of the mass stencil (-p for poles, 1 for M)
+    double *x, *r, *p, *q, *z;    // [npair][NP]
+    double *rho, *rho0;           // [npair]
+    int* active;                  // [npair]
+    double rtol;
+};
+struct Pcg3 {
+    long long NP; int ncols;
+    double *x, *r, *p, *q, *z;    // padded face vectors [ncols][NP]
+    double *rho, *eta0, *relres;
+    int *active, *iters;
+    double* hist;
+    double rtol; int norm_kind;
+    int* status;
+};
+cudaError_t face_slab_pass(const double* in, double* out, int nslab, int n, int ldf, const double* S, cudaStream_t st);
+cudaError_t face_slab_pass_scaled(const double* in, double* out, int nslab, int n, int ldf, const double* S,
+                                  const double* w, long long sW, int group, const double* colscale, cudaStream_t st);
+size_t face_fx_ws_doubles(long long NP, int ncols, int num_sms);
+int face_fx_tiles(long long NP, int ncols);
+cudaError_t face_fx(const double* F, long long NP, const double* p, double* q, const double* D, int ncols,
+                    const int* col_param, int n_param, const double* gp, double* ws, int* counters, int num_sms,
+                    cudaStream_t st);
+cudaError_t face_gram_scatter(const double* B, int n2, int kp, double* F, int n, int ldf, long long NP, int num_sms,
+                              cudaStream_t st);
+cudaError_t face_copy_in(int n, int ldf, long long NP, int ncols, const double* src, int lds, double* dst, cudaStream_t st);
+cudaError_t face_copy_out(int n, int ldf, long long NP, int ncols, const double* src, double* dst, int ldd,
+                          cudaStream_t st);
+cudaError_t face_dense_pair(int n, double hh12, double* A, double* M, cudaStream_t st);
+cudaError_t face_mass_cols(int n, double hh12, const double* V, double* out, int ncol, int ldo, cudaStream_t st);
+cudaError_t scale_transpose(const double* V, const double* w, int n2, double* out, int kp, cudaStream_t st);
+cudaError_t inner_init(const InnerArgs& a, const double* b, cudaStream_t st);
+cudaError_t inner_start(const InnerArgs& a, cudaStream_t st);
+cudaError_t inner_step1(const InnerArgs& a, cudaStream_t st);
+cudaError_t inner_step2(const InnerArgs& a, int* n_active, cudaStream_t st);
+cudaError_t inner_combine(const InnerArgs& a, const double* w, int nsys, double* zout, cudaStream_t st);
+cudaError_t pcg3_start(const Pcg3& s, cudaStream_t st);
+cudaError_t pcg3_alpha(const Pcg3& s, cudaStream_t st);
+cudaError_t pcg3_beta(const Pcg3& s, int k, int maxit, int* n_active, cudaStream_t st);
+cudaError_t gather_param(int ncols, const int* col_param, int n_param, const double* src, double* dst, cudaStream_t st);
+
 }  // namespace dd

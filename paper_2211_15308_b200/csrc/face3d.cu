@@ -207,17 +207,6 @@ cudaError_t scale_transpose(const double* V, const double* w, int n2, double* ou
 
 // ------------------------------------------------------------------------------------ inner PCG
 // Pair layout: pair q = s * C + c (system s of this rank, column c); vectors NP each.
-struct InnerArgs {
-    int n, ldf; long long NP;
-    int npair, C;                 // pairs, columns
-    double hh12;
-    const double* sys_a;          // [npair / C] coefficient of A (1 for poles, 0 for the mass term)
-    const double* sys_b;          // [npair / C] coefficient of M (-p for poles, 1 for the mass term)
-    double *x, *r, *p, *q, *z;    // [npair][NP]
-    double *rho, *rho0;           // [npair]
-    int* active;                  // [npair]
-    double rtol;
-};
 
 // deterministic block reduction
 __device__ __forceinline__ double block_sum(double a, double* red) {
@@ -339,15 +328,18 @@ cudaError_t inner_combine(const InnerArgs& a, const double* w, int nsys, double*
 }
 
 // ------------------------------------------------------------------------------------ outer PCG (3D)
-struct Pcg3 {
-    long long NP; int ncols;
-    double *x, *r, *p, *q, *z;   // padded face vectors [ncols][NP]
-    double *rho, *eta0, *relres;
-    int *active, *iters;
-    double* hist;
-    double rtol; int norm_kind;
-    int* status;
-};
+__global__ void k_gather_param(int ncols, const int* col_param, int n_param, const double* src, double* dst) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
+        int p = col_param[c];
+        p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
+        dst[c] = src[p];
+    }
+}
+cudaError_t gather_param(int ncols, const int* col_param, int n_param, const double* src, double* dst, cudaStream_t st) {
+    if (ncols <= 0) return cudaSuccess;
+    k_gather_param<<<(ncols + 127) / 128, 128, 0, st>>>(ncols, col_param, n_param, src, dst);
+    return cudaGetLastError();
+}
 // k = 0: r = b (already in r), z given: ρ = r·z, η0, p = z, x = 0
 __global__ void k3_pcg_start(Pcg3 s) {
     __shared__ double red[32];

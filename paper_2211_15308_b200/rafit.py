@@ -136,6 +136,36 @@ def fit_ra(K: float, gamma: float, lam_min: float, lam_max: float, n_poles: int)
     return ra
 
 
+def face_pair(N: int):
+    """Sparse P1 pair of the Kuhn-mesh face Γ = {x=0} with Dirichlet ∂Γ (stencils of SURVEY §8
+    "verified stencils", pinned against element assembly in the oracle tests):
+    A = [4; -1 at (±1,0),(0,±1)],  M = (h^2/12)[6; 1 at (±1,0),(0,±1),(1,1),(-1,-1)]."""
+    import scipy.sparse as sp
+    n = N - 1
+    h = 1.0 / N
+    I = sp.identity(n, format="csr")
+    T = sp.diags([np.ones(n - 1), np.ones(n - 1)], [-1, 1], format="csr")     # neighbours
+    U = sp.diags([np.ones(n - 1)], [1], format="csr")                           # +1 shift
+    A = 4.0 * sp.kron(I, I) - sp.kron(T, I) - sp.kron(I, T)
+    D = sp.kron(U, U) + sp.kron(U.T, U.T)                                       # (1,1) and (-1,-1)
+    M = (h * h / 12.0) * (6.0 * sp.kron(I, I) + sp.kron(T, I) + sp.kron(I, T) + D)
+    return A.tocsc(), M.tocsc()
+
+
+def interval_face(N: int):
+    """Spectral interval [λ_min, λ_max] of the face pair (A_Γ, M_Γ) (3D configs), by ARPACK
+    (shift-invert at 0 for λ_min, largest for λ_max) — host setup data for the RA fit."""
+    import scipy.sparse.linalg as spla
+    A, M = face_pair(N)
+    if A.shape[0] <= 400:
+        import scipy.linalg as sla
+        lam = sla.eigh(A.toarray(), M.toarray(), eigvals_only=True)
+        return float(lam[0]), float(lam[-1])
+    lo = spla.eigsh(A, k=1, M=M, sigma=0.0, which="LM", return_eigenvectors=False, tol=1e-12)[0]
+    hi = spla.eigsh(A, k=1, M=M, which="LA", return_eigenvectors=False, tol=1e-10, maxiter=20000)[0]
+    return float(lo), float(hi * (1.0 + 1e-9))
+
+
 def interval_1d(N: int):
     """Spectral interval of the 1D P1 pair on Γ with Dirichlet ends, closed form
     λ_k = (6/h^2)(1 - cos θ_k)/(2 + cos θ_k), θ_k = kπ/N, k = 1..N-1 (north star)."""
