@@ -46,7 +46,7 @@ def _env_int(k, d):
 
 
 def fit_ras(cfg):
-    lo, hi = rafit.interval_1d(cfg.N)
+    lo, hi = rafit.interval_1d(cfg.N) if cfg.dim == 2 else rafit.interval_face(cfg.N)
     return [rafit.fit_ra(K, g, lo, hi, cfg.n_poles) for K, g in cfg.params]
 
 
@@ -268,11 +268,32 @@ def main():
         g2_ms, g2_n = prof["gemm_schur"]
         g1_ms, g1_n = prof["gemm_dst"]
         ps_ms, ps_n = prof["polesum_pcg"]
-        flops_g2 = 2.0 * n * (2 * n) * C          # [S_dst | F] (n x 2n) times (2n x C), algorithmic
-        flops_g1 = 2.0 * n * n * C
-        ach_g2 = flops_g2 / (g2_ms / g2_n / 1e3) / 1e12 if g2_n else None
-        step_flops = (flops_g1 + flops_g2) * mean_it
         total_prof_ms = sum(v[0] for v in prof.values())
+        if cfg.dim == 2:
+            flops_g2 = 2.0 * n * (2 * n) * C          # [S_dst | F] (n x 2n) times (2n x C), algorithmic
+            flops_g1 = 2.0 * n * n * C
+            ach_g2 = flops_g2 / (g2_ms / g2_n / 1e3) / 1e12 if g2_n else None
+            step_flops = (flops_g1 + flops_g2) * mean_it
+            roof = {"bound": "tensor", "kernel": "gemm_schur ([S_dst|F] x [T; gamma X], DMMA fp64)",
+                    "achieved": round(ach_g2, 3) if ach_g2 else None, "peak": peak, "unit": "TFLOP/s",
+                    "frac": round(ach_g2 / peak, 4) if ach_g2 else None, "peak_source": peak_src,
+                    "flops_per_launch": flops_g2,
+                    "step_fp64_frac": round(step_flops / (total_prof_ms / nprof / 1e3) / 1e12 / peak, 4)}
+        else:
+            # 3D: the dense fractional term F (n_Γ^2 fp64) is streamed once per Schur apply: HBM-bound
+            mp = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+            hbm = float(mp.get("hbm_gbs", 6650.0))
+            bytes_fx = 8.0 * cfg.n_gamma * cfg.n_gamma + 3 * 8.0 * cfg.n_gamma * C
+            ach = bytes_fx / (g2_ms / g2_n / 1e3) / 1e9 if g2_n else None
+            roof = {"bound": "hbm", "kernel": "gemm_schur (gamma F x + sine back-transform, stream-K DMMA, BN=8)",
+                    "achieved": round(ach, 1) if ach else None, "peak": hbm, "unit": "GB/s",
+                    "frac": round(ach / hbm, 4) if ach else None,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if mp else "fallback 6650 GB/s",
+                    "bytes_per_launch": bytes_fx}
+        roof.update({"traffic": traffic_for(cfg.name, "gemm_schur"),
+                     "avg_launch_us": round(g2_ms / g2_n * 1e3, 2) if g2_n else None,
+                     "share_of_step": {k: round(v[0] / total_prof_ms, 4) for k, v in prof.items()},
+                     "avg_us": {k: round(v[0] / v[1] * 1e3, 2) if v[1] else None for k, v in prof.items()}})
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
@@ -285,19 +306,16 @@ def main():
             "precond_applies_per_s": round(pa_per_s, 1),
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
-            "roofline": {"bound": "tensor", "kernel": "gemm_schur ([S_dst|F] x [T; gamma X], DMMA fp64)",
-                         "achieved": round(ach_g2, 3) if ach_g2 else None, "peak": peak, "unit": "TFLOP/s",
-                         "frac": round(ach_g2 / peak, 4) if ach_g2 else None,
-                         "traffic": traffic_for(cfg.name, "gemm_schur"), "peak_source": peak_src,
-                         "flops_per_launch": flops_g2, "avg_launch_us": round(g2_ms / g2_n * 1e3, 2) if g2_n else None,
-                         "step_fp64_frac": round(step_flops / (total_prof_ms / nprof / 1e3) / 1e12 / peak, 4),
-                         "share_of_step": {k: round(v[0] / total_prof_ms, 4) for k, v in prof.items()},
-                         "avg_us": {k: round(v[0] / v[1] * 1e3, 2) if v[1] else None for k, v in prof.items()}},
+            "roofline": roof,
             "launch_config": qc,
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
                     "h2d_bytes_per_step": int(B.nbytes + C * 4), "d2h_bytes_per_step": int(B.nbytes + C * 12)},
         }
-        if not args.no_cpu_baseline and world == 1:
+        if cfg.dim == 3:
+            line["cpu_baseline"] = None
+            line["cpu_baseline_note"] = ("not run: the dense oracle at n_Gamma = 16129 needs ~5e14 flop of elimination "
+                                         "plus a 16129^2 generalised eigensolve (tens of minutes on the host)")
+        elif not args.no_cpu_baseline and world == 1:
             per = max(1, int(os.environ.get("DD_ORACLE_PER_PARAM", "64")))
             solves, secs = oracle_sample(cfg, ras, B, colp, per)
             line["cpu_baseline"] = {"value": round(solves / secs, 4), "unit": UNIT, "cores": cores_used(),
