@@ -149,27 +149,56 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
     }
     f.sys_ids = mine;
     f.nsys = (int)mine.size();
+    // Sine-domain form of every system a A + b M (exact algebra of the Kuhn face pair):
+    //   Q (a A + b M) Q = diag(a α_ab + b μ̃_ab) + (b h^2/24) D̂ ⊗ D̂,
+    //   α_ab = σ_a + σ_b,  μ̃_ab = (h^2/12)(6 + 2c_a + 2c_b + 2 c_a c_b),  D̂ = S D S,  (D v)_j = v_{j+1} - v_{j-1},
+    // since M - M̃ = (h^2/24) D⊗D collects the (1,1)/(-1,-1) couplings minus their symmetrised part.
     const int ns = std::max(1, f.nsys);
-    std::vector<double> sa(ns, 0.0), sb(ns, 1.0), swt(ns, 0.0), pd((size_t)ns * f.NP, 0.0);
+    std::vector<double> sa(ns, 0.0), sb(ns, 1.0), swt(ns, 0.0), cs(ns, 0.0), dg((size_t)ns * f.NP, 0.0),
+        idg((size_t)ns * f.NP, 0.0);
     for (int i = 0; i < f.nsys; i++) {
         const Sys& s = sys[mine[i]];
         sa[i] = s.a; sb[i] = s.b; swt[i] = s.w;
+        cs[i] = (double)((long double)s.b * h * h / 24.0L);
         for (int a = 0; a < n; a++)
             for (int b = 0; b < n; b++) {
                 const long double ca = 1.0L - 0.5L * sig[a], cb = 1.0L - 0.5L * sig[b];
                 const long double alpha = sig[a] + sig[b];
                 const long double mut = (long double)hh12 * (6.0L + 2.0L * ca + 2.0L * cb + 2.0L * ca * cb);
-                pd[(size_t)i * f.NP + (size_t)a * f.ldf + b] = (double)(1.0L / ((long double)s.a * alpha + (long double)s.b * mut));
+                const long double d = (long double)s.a * alpha + (long double)s.b * mut;
+                dg[(size_t)i * f.NP + (size_t)a * f.ldf + b] = (double)d;
+                idg[(size_t)i * f.NP + (size_t)a * f.ldf + b] = (double)(1.0L / d);
             }
     }
+    std::vector<double> Dh((size_t)Srows * f.ldf, 0.0);
+    {
+        std::vector<long double> SL((size_t)n * n);
+        for (int q = 0; q < n; q++)
+            for (int r = 0; r < n; r++) SL[(size_t)q * n + r] = sc * sintab[((long long)(q + 1) * (r + 1)) % (2 * N)];
+        for (int a = 0; a < n; a++)
+            for (int b = 0; b < n; b++) {
+                long double acc = 0.0L;
+                for (int j = 0; j < n; j++) {
+                    const long double dj = (j + 1 < n ? SL[(size_t)(j + 1) * n + b] : 0.0L) - (j >= 1 ? SL[(size_t)(j - 1) * n + b] : 0.0L);
+                    acc += SL[(size_t)a * n + j] * dj;
+                }
+                Dh[(size_t)a * f.ldf + b] = (double)acc;
+            }
+    }
+    DD_CK(dalloc(c, &f.Dh, Dh.size()));
+    DD_CK(cudaMemcpyAsync(f.Dh, Dh.data(), Dh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     DD_CK(dalloc(c, &f.sys_a, ns));
     DD_CK(dalloc(c, &f.sys_b, ns));
     DD_CK(dalloc(c, &f.sys_w, ns));
-    DD_CK(dalloc(c, &f.pdiag, pd.size()));
+    DD_CK(dalloc(c, &f.cs, ns));
+    DD_CK(dalloc(c, &f.dg, dg.size()));
+    DD_CK(dalloc(c, &f.idg, idg.size()));
     DD_CK(cudaMemcpyAsync(f.sys_a, sa.data(), ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     DD_CK(cudaMemcpyAsync(f.sys_b, sb.data(), ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     DD_CK(cudaMemcpyAsync(f.sys_w, swt.data(), ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    DD_CK(cudaMemcpyAsync(f.pdiag, pd.data(), pd.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    DD_CK(cudaMemcpyAsync(f.cs, cs.data(), ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    DD_CK(cudaMemcpyAsync(f.dg, dg.data(), dg.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    DD_CK(cudaMemcpyAsync(f.idg, idg.data(), idg.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
 
     // --- per-parameter K, γ and workspaces
     DD_CK(dalloc(c, &c->Kp, c->n_param));
@@ -239,25 +268,19 @@ static dd_status precond_core(dd_ctx* c, int ncols, const double* r, double* z) 
         a.sys_a = f.sys_a; a.sys_b = f.sys_b;
         a.x = f.ix; a.r = f.ir; a.p = f.ip; a.q = f.iq; a.z = f.iz;
         a.rho = f.irho; a.rho0 = f.irho0; a.active = f.iactive; a.rtol = f.inner_rtol;
-        auto dst_precond = [&]() -> dd_status {   // z = Q diag(1/(a α + b μ̃)) Q r per pair
-            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.ir, f.T1, a.npair, f.n, f.ldf, f.S, c->stream));
-            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_scaled(f.T1, f.T2, a.npair, f.n, f.ldf, f.S, f.pdiag, f.NP, ncols,
-                                                              nullptr, c->stream));
-            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.T2, f.T1, a.npair, f.n, f.ldf, f.S, c->stream));
-            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.T1, f.iz, a.npair, f.n, f.ldf, f.S, c->stream));
-            return DD_OK;
-        };
-        DD_TIMED(DD_KCLASS_POLESUM, inner_init(a, r, c->stream));
-        dd_status s = dst_precond();
-        if (s != DD_OK) return s;
-        DD_TIMED(DD_KCLASS_POLESUM, inner_start(a, c->stream));
+        a.dg = f.dg; a.idg = f.idg; a.cs = f.cs;
+        // r̂_c = Q r_c once per column (2 slab passes)
+        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(r, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
+        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.S, c->stream));
+        DD_TIMED(DD_KCLASS_POLESUM, inner_init_hat(a, f.U2, c->stream));
         int it = 0;
         for (it = 1; it <= f.inner_maxit; it++) {
-            DD_TIMED(DD_KCLASS_POLESUM, inner_step1(a, c->stream));
-            s = dst_precond();
-            if (s != DD_OK) return s;
+            // q̂ = dg ∘ p̂ + cs D̂ p̂ D̂^T on the active pairs, then the fused CG update
+            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_active(f.ip, f.T1, a.npair, f.n, f.ldf, f.Dh, f.iactive, c->stream));
+            DD_TIMED(DD_KCLASS_POLESUM, face_inner_op_pass(f.T1, f.iq, f.ip, a.npair, ncols, f.n, f.ldf, f.Dh, f.dg, f.cs,
+                                                           f.iactive, c->stream));
             DD_CK(cudaMemsetAsync(c->ints + 1, 0, sizeof(int), c->stream));
-            DD_TIMED(DD_KCLASS_POLESUM, inner_step2(a, c->ints + 1, c->stream));
+            DD_TIMED(DD_KCLASS_POLESUM, inner_update_hat(a, c->ints + 1, c->stream));
             if (it % 4 == 0 || it == f.inner_maxit) {
                 DD_CK(cudaMemcpyAsync(c->h_ints + 1, c->ints + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
                 DD_CK(cudaStreamSynchronize(c->stream));
@@ -265,7 +288,10 @@ static dd_status precond_core(dd_ctx* c, int ncols, const double* r, double* z) 
             }
         }
         f.last_inner_iters = std::min(it, f.inner_maxit);
-        DD_TIMED(DD_KCLASS_POLESUM, inner_combine(a, f.sys_w, f.nsys, z, c->stream));
+        // ẑ_c = Σ_s w_s x̂_{s,c} (fixed system order), z_c = Q ẑ_c
+        DD_TIMED(DD_KCLASS_POLESUM, inner_combine(a, f.sys_w, f.nsys, f.U1, c->stream));
+        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.S, c->stream));
+        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.U2, z, ncols, f.n, f.ldf, f.S, c->stream));
     }
     if (f.nccl) {
         NK(ncclAllReduce(z, z, (size_t)f.NP * ncols, ncclDouble, ncclSum, static_cast<ncclComm_t>(f.nccl), c->stream));

@@ -54,7 +54,9 @@ struct Face3 {
     int nsys = 0;                     // systems handled by this rank
     int nsys_total = 0;
     std::vector<int> sys_ids;         // global system ids of this rank
-    double *sys_a = nullptr, *sys_b = nullptr, *sys_w = nullptr, *pdiag = nullptr;   // pdiag [nsys][NP]
+    double *sys_a = nullptr, *sys_b = nullptr, *sys_w = nullptr;
+    double *dg = nullptr, *idg = nullptr, *cs = nullptr;   // sine-domain diagonal / inverse [nsys][NP], D̂ coefficient [nsys]
+    double* Dh = nullptr;             // D̂ = S D S (central difference in the sine basis), like S
     // inner PCG pairs [nsys * max_cols][NP]
     double *ix = nullptr, *ir = nullptr, *ip = nullptr, *iq = nullptr, *iz = nullptr, *T1 = nullptr, *T2 = nullptr;
     double *irho = nullptr, *irho0 = nullptr;

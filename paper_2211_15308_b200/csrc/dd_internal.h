@@ -121,6 +121,9 @@ struct InnerArgs {
     double *rho, *rho0;           // [npair]
     int* active;                  // [npair]
     double rtol;
+    const double* dg;             // [systems][NP] sine-diagonal part a α + b μ̃ (0 on padding)
+    const double* idg;            // [systems][NP] its inverse (0 on padding)
+    const double* cs;             // [systems] coefficient of D̂ v D̂^T: b h^2/24
 };
 struct Pcg3 {
     long long NP; int ncols;
@@ -147,6 +150,12 @@ cudaError_t face_copy_out(int n, int ldf, long long NP, int ncols, const double*
 cudaError_t face_dense_pair(int n, double hh12, double* A, double* M, cudaStream_t st);
 cudaError_t face_mass_cols(int n, double hh12, const double* V, double* out, int ncol, int ldo, cudaStream_t st);
 cudaError_t scale_transpose(const double* V, const double* w, int n2, double* out, int kp, cudaStream_t st);
+cudaError_t face_slab_pass_active(const double* in, double* out, int nslab, int n, int ldf, const double* B,
+                                  const int* active, cudaStream_t st);
+cudaError_t face_inner_op_pass(const double* in, double* q, const double* p, int nslab, int C, int n, int ldf,
+                               const double* B, const double* dg, const double* cs, const int* active, cudaStream_t st);
+cudaError_t inner_init_hat(const InnerArgs& a, const double* bh, cudaStream_t st);
+cudaError_t inner_update_hat(const InnerArgs& a, int* n_active, cudaStream_t st);
 cudaError_t inner_init(const InnerArgs& a, const double* b, cudaStream_t st);
 cudaError_t inner_start(const InnerArgs& a, cudaStream_t st);
 cudaError_t inner_step1(const InnerArgs& a, cudaStream_t st);

@@ -40,6 +40,7 @@ struct DgemmProblem {
     const double* B; int ldb;    // columns readable up to round_up(N, BN)
     long long sA = 0, sB = 0;    // batch strides (elements)
     int batch = 1;
+    const int* active = nullptr; // optional per-slab flag: slabs with active[b] == 0 are skipped
 };
 
 __device__ __forceinline__ void dg_cp_async16(void* smem, const void* gmem) {
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
     double* As = smem;
     double* Bs = smem + C::STAGES * C::BM * C::LDS;
     const int bz = blockIdx.z;
+    if (g.active && !g.active[bz]) return;   // frozen slab (uniform across the cluster)
     g.A += (size_t)bz * g.sA;
     g.B += (size_t)bz * g.sB;
 

@@ -44,6 +44,16 @@ struct EpiSlabScale {          // Out[b] = v * scale(b) * w[b's table][row + col
         out[(size_t)b * sC + i] = v * s;
     }
 };
+struct EpiInnerOp {            // q̂[b] = dg[s] ∘ p̂[b] + cs[s] v,  s = b / C   (sine-domain shifted operator)
+    double* q; const double* p; long long NP; int ldf, C;
+    const double* dg; const double* cs;
+    __device__ __forceinline__ void operator()(int b, int row, int col, double v) const {
+        const int s = b / C;
+        const size_t i = row + (size_t)col * ldf;
+        const size_t o = (size_t)b * NP + i;
+        q[o] = fma(dg[(size_t)s * NP + i], p[o], cs[s] * v);
+    }
+};
 struct EpiFaceFx {             // q[c] = γ_c v + D[c]  (padded face layout)
     double* q; const double* D; long long ldq; const int* col_param; int n_param; const double* gp;
     __device__ __forceinline__ void operator()(int, int row, int col, double v) const {
@@ -77,6 +87,27 @@ cudaError_t face_slab_pass_scaled(const double* in, double* out, int nslab, int 
     g.sB = 0;
     g.batch = nslab;
     return dgemm_launch<CfgSlab>(g, 1, EpiSlabScale{out, (long long)ldf * ldf, ldf, w, sW, group, colscale}, st);
+}
+
+// Out = (Y B^T)^T per active slab (B = D̂ for the sine-domain operator)
+cudaError_t face_slab_pass_active(const double* in, double* out, int nslab, int n, int ldf, const double* B,
+                                  const int* active, cudaStream_t st) {
+    DgemmProblem g{n, n, ldf, in, ldf, B, ldf};
+    g.sA = (long long)ldf * ldf;
+    g.sB = 0;
+    g.batch = nslab;
+    g.active = active;
+    return dgemm_launch<CfgSlab>(g, 1, EpiSlabStore{out, (long long)ldf * ldf, ldf}, st);
+}
+// second pass of q̂ = dg ∘ p̂ + cs D̂ p̂ D̂^T over active pairs
+cudaError_t face_inner_op_pass(const double* in, double* q, const double* p, int nslab, int C, int n, int ldf,
+                               const double* B, const double* dg, const double* cs, const int* active, cudaStream_t st) {
+    DgemmProblem g{n, n, ldf, in, ldf, B, ldf};
+    g.sA = (long long)ldf * ldf;
+    g.sB = 0;
+    g.batch = nslab;
+    g.active = active;
+    return dgemm_launch<CfgSlab>(g, 1, EpiInnerOp{q, p, (long long)ldf * ldf, ldf, C, dg, cs}, st);
 }
 
 // q = γ F p + D over ncols columns (F: NP x NP row-major padded; vectors NP per column).
@@ -220,6 +251,78 @@ __device__ __forceinline__ double block_sum(double a, double* red) {
     for (int w = 0; w < W; w++) s += red[w];
     __syncthreads();
     return s;
+}
+
+// ---- sine-domain inner CG: the operator of system s is  dg_s ∘ v + cs_s D̂ v D̂^T  and the
+// preconditioner is 1/dg_s (the sine-diagonal part), both exact algebra of the face pair
+// (M = M̃ + (h^2/24) D⊗D, D = central difference).
+// init: r̂ = b̂_c, x̂ = 0, ẑ = r̂ / dg, ρ = ρ0 = r̂·ẑ, p̂ = ẑ
+__global__ void k_inner_init_hat(InnerArgs a, const double* __restrict__ bh) {
+    __shared__ double red[32];
+    const int pq = blockIdx.x;
+    const int c = pq % a.C, s = pq / a.C;
+    const size_t off = (size_t)pq * a.NP;
+    const double* idg = a.idg + (size_t)s * a.NP;
+    double rho = 0.0;
+    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) {
+        const double r = bh[(size_t)c * a.NP + i];
+        const double z = r * idg[i];
+        a.r[off + i] = r;
+        a.x[off + i] = 0.0;
+        a.p[off + i] = z;
+        rho = fma(r, z, rho);
+    }
+    rho = block_sum(rho, red);
+    if (threadIdx.x == 0) {
+        a.rho[pq] = rho;
+        a.rho0[pq] = rho;
+        a.active[pq] = rho > 0.0 ? 1 : 0;
+    }
+}
+// given q̂ = Â p̂: α = ρ/(p̂·q̂); x̂ += αp̂; r̂ -= αq̂; ẑ = r̂/dg; ρ' = r̂·ẑ; stop if ρ' <= rtol^2 ρ0;
+// else p̂ = ẑ + (ρ'/ρ) p̂   (one CTA per pair; fixed-order reductions)
+__global__ void k_inner_update_hat(InnerArgs a, int* n_active) {
+    __shared__ double red[32];
+    const int pq = blockIdx.x;
+    if (!a.active[pq]) return;
+    const int s = pq / a.C;
+    const size_t off = (size_t)pq * a.NP;
+    const double* idg = a.idg + (size_t)s * a.NP;
+    double d = 0.0;
+    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) d = fma(a.p[off + i], a.q[off + i], d);
+    d = block_sum(d, red);
+    if (!(d > 0.0)) {
+        if (threadIdx.x == 0) a.active[pq] = 0;
+        return;
+    }
+    const double alpha = a.rho[pq] / d;
+    double rho = 0.0;
+    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) {
+        a.x[off + i] = fma(alpha, a.p[off + i], a.x[off + i]);
+        const double r = fma(-alpha, a.q[off + i], a.r[off + i]);
+        a.r[off + i] = r;
+        rho = fma(r, r * idg[i], rho);
+    }
+    rho = block_sum(rho, red);
+    if (!(rho > a.rtol * a.rtol * a.rho0[pq])) {
+        if (threadIdx.x == 0) a.active[pq] = 0;
+        return;
+    }
+    const double beta = rho / a.rho[pq];
+    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x)
+        a.p[off + i] = fma(beta, a.p[off + i], a.r[off + i] * idg[i]);
+    if (threadIdx.x == 0) {
+        a.rho[pq] = rho;
+        atomicAdd(n_active, 1);
+    }
+}
+cudaError_t inner_init_hat(const InnerArgs& a, const double* bh, cudaStream_t st) {
+    k_inner_init_hat<<<a.npair, 512, 0, st>>>(a, bh);
+    return cudaGetLastError();
+}
+cudaError_t inner_update_hat(const InnerArgs& a, int* n_active, cudaStream_t st) {
+    k_inner_update_hat<<<a.npair, 512, 0, st>>>(a, n_active);
+    return cudaGetLastError();
 }
 
 // init: r = b_c, x = 0 (z, ρ set after the first preconditioner application)
