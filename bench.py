@@ -208,6 +208,7 @@ def main():
             iters_all.append(r.iters.copy())
         torch.cuda.synchronize()
     launches = S.launch_count()
+    qc = S.query_config()              # launch configuration of the timed solves
     if world > 1:
         dist.barrier()
     total_ms = float(sum(step_ms))
@@ -226,7 +227,6 @@ def main():
         step()
     prof = S.profile_read()
     S.profile(False)
-    qc = S.query_config()
 
     # ---- e2e through the host-buffer ABI call (pinned host memory, H2D + D2H inside)
     Bh = torch.as_tensor(B).pin_memory().numpy()

@@ -335,6 +335,8 @@ extern "C" dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K,
     };
     if (const char* ng = std::getenv("DD_NO_GRAPH")) c->graph_ok = !(ng[0] == '1');   // profiling: host loop
     if (const char* ns = std::getenv("DD_NO_SMALL")) c->small_ok = !(ns[0] == '1');
+    const char* pht = std::getenv("DD_PHASE_TIMING");
+    const bool want_dbg = pht && pht[0] == '1';
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DD_ECUDA, "cudaSetDevice failed"));
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     dd_status s = c->dim == 2 ? setup_2d(c, K, mu_inv, poles, residues, c0)
@@ -355,6 +357,7 @@ extern "C" dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K,
     if (cudaMemsetAsync(c->active, 0, sizeof(int) * (2 * (size_t)max_cols + 16), c->stream) != cudaSuccess)
         return bail(fail(DD_ECUDA, "memset"));
     if (cudaMallocHost(&c->h_ints, sizeof(int) * 16) != cudaSuccess) return bail(fail(DD_ENOMEM, "pinned"));
+    if (want_dbg && dalloc(c, &c->dbg, 16) != cudaSuccess) return bail(fail(DD_ENOMEM, "dbg"));
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DD_ECUDA, "setup sync"));
     *out = c;
     return DD_OK;
@@ -437,6 +440,7 @@ static PcgState make_state(dd_ctx* c, int ncols, const int* colp, double* x, dou
     s.done_ctas = c->ints + 3; s.status = c->ints + 4;
     s.rtol = rtol; s.maxit = maxit; s.norm_kind = norm_kind;
     s.cond_handle = 0;
+    s.dbg = c->dbg;
     return s;
 }
 
@@ -570,6 +574,12 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
     CK(cudaMemcpyAsync(c->h_ints, c->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     const int kdone = c->h_ints[0];
+    if (c->dbg) {
+        long long t[8] = {0};
+        CK(cudaMemcpy(t, c->dbg, sizeof(t), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[dd phase cycles] load+pq %lld  update %lld  polesum %lld  dots+p %lld  finish %lld\n",
+                t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
+    }
     if (c->last_graph) c->launches += 3LL * kdone;
     if (hist) {
         // column 0 history: η_0 .. η_{iters[0]}

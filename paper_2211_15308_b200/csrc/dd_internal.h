@@ -89,6 +89,7 @@ struct PcgState {
     int* status;                       // 0 ok, DD_ENOTSPD
     double rtol; int maxit; int norm_kind;
     unsigned long long cond_handle;    // cudaGraphConditionalHandle (0 = none)
+    long long* dbg;                    // optional phase timestamps of CTA 0 (DD_PHASE_TIMING=1)
 };
 
 PoleGeom make_pole_geom(int n);

@@ -339,6 +339,9 @@ __global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_pcg_iter(PcgSta
     if (threadIdx.x == 0) s_work = s.active[c];
     __syncthreads();
     bool still = false;
+#define DD_PHASE(i) \
+    if (s.dbg && blockIdx.x == 0 && threadIdx.x == 0) s.dbg[i] = clock64()
+    DD_PHASE(0);
     if (s_work) {
         const int k = *s.kiter + 1;
         const int param = clamp_param(s.col_param[c], t.n_param);
@@ -358,6 +361,7 @@ __global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_pcg_iter(PcgSta
 #pragma unroll
         for (int j = 0; j < RPT; j++) pq = fma(pv[j], qv[j], pq);
         block_sum2(pq, dummy, red);
+        DD_PHASE(1);
         if (!(pq > 0.0)) {
             if (threadIdx.x == 0) {
                 atomicExch(s.status, (int)DD_ENOTSPD);
@@ -380,7 +384,9 @@ __global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_pcg_iter(PcgSta
             }
             for (int i = threadIdx.x + RPT * NT; i < g.T * g.LL; i += NT) S.R[tpos(i, g)] = 0.0;
             __syncthreads();
+            DD_PHASE(2);
             block_polesum<LMAX, G, NG>(t, g, param, S.R, S.Z, S.scratch);
+            DD_PHASE(3);
             double rz = 0.0, zz = 0.0;
             double zv[RPT];
 #pragma unroll
@@ -425,7 +431,10 @@ __global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_pcg_iter(PcgSta
             }
         }
     }
+    DD_PHASE(4);
     finish_iteration(s, still);
+    DD_PHASE(5);
+#undef DD_PHASE
 }
 
 // ---------------------------------------------------------------------------------------------
