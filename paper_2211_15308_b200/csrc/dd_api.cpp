@@ -575,10 +575,12 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
     CK(cudaStreamSynchronize(c->stream));
     const int kdone = c->h_ints[0];
     if (c->dbg) {
-        long long t[8] = {0};
+        long long t[16] = {0};
         CK(cudaMemcpy(t, c->dbg, sizeof(t), cudaMemcpyDeviceToHost));
         fprintf(stderr, "[dd phase cycles] load+pq %lld  update %lld  polesum %lld  dots+p %lld  finish %lld\n",
                 t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
+        fprintf(stderr, "[dd polesum cycles] stage-wait %lld  sys0: fwd %lld bwd %lld pcr %lld  rest-of-systems %lld  combine %lld\n",
+                t[6] - t[2], t[7] - t[6], t[8] - t[7], t[9] - t[8], t[10] - t[9], t[3] - t[10]);
     }
     if (c->last_graph) c->launches += 3LL * kdone;
     if (hist) {

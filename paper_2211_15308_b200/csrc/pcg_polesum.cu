@@ -76,11 +76,15 @@ __device__ __forceinline__ void stage_tables(const PoleTabs& t, const PoleGeom& 
 
 // z = P r for the CTA's column.  R: input (transposed), Z: output (transposed, written by every
 // thread for its own chunk after the fixed-order combine).  sm: scratch (tables already staged).
-template <int LMAX, int G, int NG>
-__device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, const double* R, double* Z,
-                              double* scratch) {
+// FULL: the chunk length equals LMAX at compile time (n + 1 = T * LMAX; all BASELINE configs), so
+// the unrolled sweeps carry no per-row branch and every table / R load hoists off the FMA chain.
+template <int LMAX, int G, int NG, bool FULL>
+__device__ void block_polesum_impl(const PoleTabs& t, const PoleGeom& g, int param, const double* R, double* Z,
+                                   double* scratch, long long* dbg) {
+#define DD_PS(i) \
+    if (dbg && threadIdx.x == 0) dbg[i] = clock64()
     constexpr int T = 32 * G;
-    const int LL = g.LL;
+    const int LL = FULL ? LMAX : g.LL;
     const int tot = LL * (T + 1);
     const int tid = threadIdx.x;
     const int group = tid / T, tau = tid % T;
@@ -96,6 +100,7 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
         if (i < LL) zg[tix(i, tau, T)] = 0.0;
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
+    DD_PS(6);
 
     const int Lr = tau < g.part ? LL - 1 : (tau == g.part ? g.Lr_part : 0);
     const int Lr_next = (tau + 1) < g.part ? LL - 1 : ((tau + 1) == g.part ? g.Lr_part : 0);
@@ -118,26 +123,54 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
         const double pinv = __ldg(&t.pinvb[(pbase + k) * T + tau]);
 
         // forward:  ỹ_i = r_i/b'_i - (e/b'_i) ỹ_{i-1}
+        // (rows in batches of 8: the batch's shared-memory loads issue together, then the chain runs)
+        constexpr int BT = LMAX < 8 ? LMAX : 8;
         double y[LMAX];
         double prev = 0.0, y_last = 0.0;
 #pragma unroll
-        for (int i = 0; i < LMAX; i++) {
-            if (i < LL - 1) {
-                const double v = fma(-cp[i], prev, R[tix(i, tau, T)] * ib[i]);
-                y[i] = i < Lr ? v : 0.0;
-                if (i < Lr) y_last = v;
-                prev = y[i];
-            } else {
-                y[i] = 0.0;
+        for (int i0 = 0; i0 < LMAX; i0 += BT) {
+            double rb[BT], cb[BT];
+#pragma unroll
+            for (int j = 0; j < BT; j++) {
+                const int i = i0 + j;
+                rb[j] = 0.0;
+                cb[j] = 0.0;
+                if (i < LL - 1) {
+                    rb[j] = R[tix(i, tau, T)] * ib[i];
+                    cb[j] = cp[i];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < BT; j++) {
+                const int i = i0 + j;
+                if (i < LL - 1) {
+                    const double v = fma(-cb[j], prev, rb[j]);
+                    y[i] = i < Lr ? v : 0.0;
+                    if (i < Lr) y_last = v;
+                    prev = y[i];
+                } else {
+                    y[i] = 0.0;
+                }
             }
         }
+        if (k == 0) DD_PS(7);
         // backward:  y_i = ỹ_i - (e/b'_i) y_{i+1}
         double next = 0.0;
 #pragma unroll
-        for (int i = LMAX - 1; i >= 0; i--) {
-            if (i < LL - 1) {
-                y[i] = fma(-cp[i], next, y[i]);
-                next = y[i];
+        for (int i0 = LMAX - 1; i0 >= 0; i0 -= BT) {
+            double cb[BT];
+#pragma unroll
+            for (int j = 0; j < BT; j++) {
+                const int i = i0 - j;
+                cb[j] = (i >= 0 && i < LL - 1) ? cp[i] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < BT; j++) {
+                const int i = i0 - j;
+                if (i >= 0 && i < LL - 1) {
+                    y[i] = fma(-cb[j], next, y[i]);
+                    next = y[i];
+                }
             }
         }
         const double y_first = Lr > 0 ? y[0] : 0.0;
@@ -148,6 +181,7 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
             if (Lr > 0) rs -= e * y_last;
             if (tau < T - 1 && Lr_next > 0) rs -= e * y_first_next;
         }
+        if (k == 0) DD_PS(8);
         // parallel cyclic reduction over the T separators
         if constexpr (G == 1) {
 #pragma unroll
@@ -174,15 +208,30 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
             }
             group_sync<G>(group);
         }
+        if (k == 0) DD_PS(9);
         const double gsep = sep_real ? rs * pinv : 0.0;
         const double gleft = group_shift<G>(gsep, -1, tau, xb, group);
         const double eg0 = e * gleft, eg1 = e * gsep;
 #pragma unroll
-        for (int i = 0; i < LMAX; i++) {
-            if (i < LL - 1 && i < Lr) {
-                const double x = y[i] - eg0 * u[i] - eg1 * u[Lr - 1 - i];
-                const int ix = tix(i, tau, T);
-                zg[ix] = fma(wk, x, zg[ix]);
+        for (int i0 = 0; i0 < LMAX; i0 += BT) {
+            double ua[BT], ub[BT], zo[BT];
+#pragma unroll
+            for (int j = 0; j < BT; j++) {
+                const int i = i0 + j;
+                ua[j] = 0.0; ub[j] = 0.0; zo[j] = 0.0;
+                if (i < LL - 1 && i < Lr) {
+                    ua[j] = u[i];
+                    ub[j] = u[Lr - 1 - i];
+                    zo[j] = zg[tix(i, tau, T)];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < BT; j++) {
+                const int i = i0 + j;
+                if (i < LL - 1 && i < Lr) {
+                    const double x = y[i] - eg0 * ua[j] - eg1 * ub[j];
+                    zg[tix(i, tau, T)] = fma(wk, x, zo[j]);
+                }
             }
         }
         if (LL >= 1) {
@@ -191,6 +240,7 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
         }
     }
 
+    DD_PS(10);
     // fixed-order combine of the NG group partials: Z = z_0 + z_1 + ... + z_{NG-1}
     __syncthreads();
     for (int idx = tid; idx < tot; idx += blockDim.x) {
@@ -199,6 +249,14 @@ __device__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, c
         Z[idx] = acc;
     }
     __syncthreads();
+#undef DD_PS
+}
+
+template <int LMAX, int G, int NG>
+__device__ __forceinline__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, const double* R,
+                                              double* Z, double* scratch, long long* dbg = nullptr) {
+    if (g.LL == LMAX) block_polesum_impl<LMAX, G, NG, true>(t, g, param, R, Z, scratch, dbg);
+    else block_polesum_impl<LMAX, G, NG, false>(t, g, param, R, Z, scratch, dbg);
 }
 
 // Deterministic block reduction of two values (fixed tree).
@@ -232,7 +290,7 @@ __device__ __forceinline__ Smem carve(double* sm, const PoleGeom& g) {
 
 // ---------------------------------------------------------------------------- kernels
 template <int LMAX, int G, int NG>
-__global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_precond(int ncols, const int* __restrict__ col_param, PoleGeom g,
+__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_precond(int ncols, const int* __restrict__ col_param, PoleGeom g,
                                                          PoleTabs t, const double* __restrict__ r, int ldr,
                                                          double* __restrict__ z, int ldz) {
     extern __shared__ __align__(16) double sm[];
@@ -275,7 +333,7 @@ __device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_a
 }
 
 template <int LMAX, int G, int NG>
-__global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_pcg_init(PcgState s, PoleGeom g, PoleTabs t,
+__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_pcg_init(PcgState s, PoleGeom g, PoleTabs t,
                                                           const double* __restrict__ b, int ldb) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
@@ -325,7 +383,7 @@ __global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_pcg_init(PcgSta
 
 // rows of thread tid: ρ = tid + j NT, j < RPT (coalesced); RPT = ceil(T LL / NT) <= ceil(LMAX / NG)
 template <int LMAX, int G, int NG>
-__global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
+__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
     constexpr int NT = 32 * G * NG;
     constexpr int RPT = (LMAX + NG - 1) / NG;
     extern __shared__ __align__(16) double sm[];
@@ -385,7 +443,7 @@ __global__ void __launch_bounds__(32 * G * NG, G >= 4 ? 1 : 2) k_pcg_iter(PcgSta
             for (int i = threadIdx.x + RPT * NT; i < g.T * g.LL; i += NT) S.R[tpos(i, g)] = 0.0;
             __syncthreads();
             DD_PHASE(2);
-            block_polesum<LMAX, G, NG>(t, g, param, S.R, S.Z, S.scratch);
+            block_polesum<LMAX, G, NG>(t, g, param, S.R, S.Z, S.scratch, blockIdx.x == 0 ? s.dbg : nullptr);
             DD_PHASE(3);
             double rz = 0.0, zz = 0.0;
             double zv[RPT];
@@ -570,8 +628,10 @@ __global__ void k_check_params(int ncols, const int* col_param, int n_param, int
 PoleGeom make_pole_geom(int n) {
     PoleGeom g{};
     g.n = n;
+    // chunks of <= 16 rows per thread (short Thomas chains, <= 128 registers), widening the
+    // group (G warps, PCR over 32 G separators) as n grows; chunks grow to 32 only past n = 4095
     int G = 1;
-    while (32 * G * 32 < n + 1 && G < 8) G *= 2;
+    while (32 * G * 16 < n + 1 && G < 8) G *= 2;
     g.G = G;
     g.T = 32 * G;
     g.J = 0;
@@ -591,7 +651,7 @@ static int lmax_of(int L) {
 }
 
 int polesum_groups(const PoleGeom& g) {
-    if (g.G >= 8) return 1;
+    if (g.G >= 8) return g.LL <= 16 ? 2 : 1;
     if (g.G == 4) return 2;
     if (g.G == 2) return 4;
     return 8;
@@ -623,9 +683,9 @@ static cudaError_t set_smem(K kern, size_t bytes) {
         else if (_G == 1 && _lm == 4) { constexpr int LM = 4, GG = 1, NGG = 8; __VA_ARGS__; }    \
         else if (_G == 1 && _lm == 8) { constexpr int LM = 8, GG = 1, NGG = 8; __VA_ARGS__; }    \
         else if (_G == 1 && _lm == 16) { constexpr int LM = 16, GG = 1, NGG = 8; __VA_ARGS__; }  \
-        else if (_G == 1) { constexpr int LM = 32, GG = 1, NGG = 8; __VA_ARGS__; }               \
-        else if (_G == 2) { constexpr int LM = 32, GG = 2, NGG = 4; __VA_ARGS__; }               \
-        else if (_G == 4) { constexpr int LM = 32, GG = 4, NGG = 2; __VA_ARGS__; }               \
+        else if (_G == 2) { constexpr int LM = 16, GG = 2, NGG = 4; __VA_ARGS__; }               \
+        else if (_G == 4) { constexpr int LM = 16, GG = 4, NGG = 2; __VA_ARGS__; }               \
+        else if (_lm <= 16) { constexpr int LM = 16, GG = 8, NGG = 2; __VA_ARGS__; }             \
         else { constexpr int LM = 32, GG = 8, NGG = 1; __VA_ARGS__; }                            \
     } while (0)
 
