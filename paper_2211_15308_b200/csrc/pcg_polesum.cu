@@ -54,6 +54,13 @@ __device__ __forceinline__ double group_shift(double v, int d, int tau, double* 
     }
 }
 
+// Read-only global load issued where written (volatile: not sunk towards its first use).
+__device__ __forceinline__ double ldg_early(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
 // Asynchronously stage this parameter set's interior tables (4 contiguous blocks of nsys x LL
 // doubles) into scratch with cp.async (LDGSTS); block_polesum waits for them.  Called at kernel
 // entry so the copies overlap the vector passes.
@@ -102,25 +109,29 @@ __device__ void block_polesum_impl(const PoleTabs& t, const PoleGeom& g, int par
     __syncthreads();
     DD_PS(6);
 
-    const int Lr = tau < g.part ? LL - 1 : (tau == g.part ? g.Lr_part : 0);
-    const int Lr_next = (tau + 1) < g.part ? LL - 1 : ((tau + 1) == g.part ? g.Lr_part : 0);
-    const bool sep_real = tau < g.part;
+    // FULL (n + 1 = T LL): every chunk has LL - 1 interior rows; only the last separator is padding
+    const int Lr = FULL ? LMAX - 1 : (tau < g.part ? LL - 1 : (tau == g.part ? g.Lr_part : 0));
+    const int Lr_next = FULL ? LMAX - 1 : ((tau + 1) < g.part ? LL - 1 : ((tau + 1) == g.part ? g.Lr_part : 0));
+    const bool sep_real = FULL ? (tau < T - 1) : (tau < g.part);
     double* xb = xbuf + (size_t)group * 2 * T;
 
     for (int k = group; k < nsys; k += NG) {
         const double* ib = tab + (size_t)k * LL;
         const double* cp = ib + tstride;
-        const double* u = tau < g.part ? ib + 2 * tstride : ib + 3 * tstride;
-        const double e = __ldg(&t.e[pbase + k]), wk = __ldg(&t.w[pbase + k]);
+        const double* u = (FULL || tau < g.part) ? ib + 2 * tstride : ib + 3 * tstride;
+        // Per-system scalars and this thread's PCR multipliers: issued here (volatile loads are not
+        // sunk by the compiler) so their global latency hides under the Thomas sweeps below.
+        const double e = ldg_early(&t.e[pbase + k]), wk = ldg_early(&t.w[pbase + k]);
         const double* pa = t.pa + (pbase + k) * (size_t)g.J * T;
         const double* pb = t.pb + (pbase + k) * (size_t)g.J * T;
-        double pav[8], pbv[8];
+        constexpr int JM = G == 1 ? 5 : (G == 2 ? 6 : (G == 4 ? 7 : 8));   // log2(32 G)
+        double pav[JM], pbv[JM];
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-            pav[j] = j < g.J ? __ldg(&pa[j * T + tau]) : 0.0;
-            pbv[j] = j < g.J ? __ldg(&pb[j * T + tau]) : 0.0;
+        for (int j = 0; j < JM; j++) {
+            pav[j] = ldg_early(&pa[j * T + tau]);
+            pbv[j] = ldg_early(&pb[j * T + tau]);
         }
-        const double pinv = __ldg(&t.pinvb[(pbase + k) * T + tau]);
+        const double pinv = ldg_early(&t.pinvb[(pbase + k) * T + tau]);
 
         // forward:  ỹ_i = r_i/b'_i - (e/b'_i) ỹ_{i-1}
         // (rows in batches of 8: the batch's shared-memory loads issue together, then the chain runs)
@@ -194,17 +205,16 @@ __device__ void block_polesum_impl(const PoleTabs& t, const PoleGeom& g, int par
                 rs = rs - pav[j] * rm - pbv[j] * rp;
             }
         } else {
+            // double-buffered shared-memory exchange, one named barrier per step
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
-                if (j < g.J) {
-                    const int s = 1 << j;
-                    double* buf = xb + (j & 1) * T;
-                    buf[tau] = rs;
-                    group_sync<G>(group);
-                    const double rm = (tau >= s) ? buf[tau - s] : 0.0;
-                    const double rp = (tau + s < T) ? buf[tau + s] : 0.0;
-                    rs = rs - pav[j] * rm - pbv[j] * rp;
-                }
+            for (int j = 0; j < JM; j++) {
+                const int s = 1 << j;
+                double* buf = xb + (j & 1) * T;
+                buf[tau] = rs;
+                group_sync<G>(group);
+                const double rm = (tau >= s) ? buf[tau - s] : 0.0;
+                const double rp = (tau + s < T) ? buf[tau + s] : 0.0;
+                rs = rs - pav[j] * rm - pbv[j] * rp;
             }
             group_sync<G>(group);
         }
@@ -212,34 +222,35 @@ __device__ void block_polesum_impl(const PoleTabs& t, const PoleGeom& g, int par
         const double gsep = sep_real ? rs * pinv : 0.0;
         const double gleft = group_shift<G>(gsep, -1, tau, xb, group);
         const double eg0 = e * gleft, eg1 = e * gsep;
+        {
 #pragma unroll
-        for (int i0 = 0; i0 < LMAX; i0 += BT) {
-            double ua[BT], ub[BT], zo[BT];
+            for (int i0 = 0; i0 < LMAX; i0 += BT) {
+                double ua[BT], ub[BT], zo[BT];
 #pragma unroll
-            for (int j = 0; j < BT; j++) {
-                const int i = i0 + j;
-                ua[j] = 0.0; ub[j] = 0.0; zo[j] = 0.0;
-                if (i < LL - 1 && i < Lr) {
-                    ua[j] = u[i];
-                    ub[j] = u[Lr - 1 - i];
-                    zo[j] = zg[tix(i, tau, T)];
+                for (int j = 0; j < BT; j++) {
+                    const int i = i0 + j;
+                    ua[j] = 0.0; ub[j] = 0.0; zo[j] = 0.0;
+                    if (i < LL - 1 && i < Lr) {
+                        ua[j] = u[i];
+                        ub[j] = u[Lr - 1 - i];
+                        zo[j] = zg[tix(i, tau, T)];
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < BT; j++) {
+                    const int i = i0 + j;
+                    if (i < LL - 1 && i < Lr) {
+                        const double x = y[i] - eg0 * ua[j] - eg1 * ub[j];
+                        zg[tix(i, tau, T)] = fma(wk, x, zo[j]);
+                    }
                 }
             }
-#pragma unroll
-            for (int j = 0; j < BT; j++) {
-                const int i = i0 + j;
-                if (i < LL - 1 && i < Lr) {
-                    const double x = y[i] - eg0 * ua[j] - eg1 * ub[j];
-                    zg[tix(i, tau, T)] = fma(wk, x, zo[j]);
-                }
+            if (LL >= 1) {
+                const int ix = tix(LL - 1, tau, T);
+                zg[ix] = fma(wk, gsep, zg[ix]);
             }
-        }
-        if (LL >= 1) {
-            const int ix = tix(LL - 1, tau, T);
-            zg[ix] = fma(wk, gsep, zg[ix]);
         }
     }
-
     DD_PS(10);
     // fixed-order combine of the NG group partials: Z = z_0 + z_1 + ... + z_{NG-1}
     __syncthreads();
@@ -255,7 +266,7 @@ __device__ void block_polesum_impl(const PoleTabs& t, const PoleGeom& g, int par
 template <int LMAX, int G, int NG>
 __device__ __forceinline__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, const double* R,
                                               double* Z, double* scratch, long long* dbg = nullptr) {
-    if (g.LL == LMAX) block_polesum_impl<LMAX, G, NG, true>(t, g, param, R, Z, scratch, dbg);
+    if (g.LL == LMAX && g.n + 1 == g.T * g.LL) block_polesum_impl<LMAX, G, NG, true>(t, g, param, R, Z, scratch, dbg);
     else block_polesum_impl<LMAX, G, NG, false>(t, g, param, R, Z, scratch, dbg);
 }
 
