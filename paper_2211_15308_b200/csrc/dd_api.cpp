@@ -335,6 +335,7 @@ extern "C" dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K,
     };
     if (const char* ng = std::getenv("DD_NO_GRAPH")) c->graph_ok = !(ng[0] == '1');   // profiling: host loop
     if (const char* ns = std::getenv("DD_NO_SMALL")) c->small_ok = !(ns[0] == '1');
+    if (const char* np = std::getenv("DD_NO_PDL")) c->pdl = !(np[0] == '1');
     const char* pht = std::getenv("DD_PHASE_TIMING");
     const bool want_dbg = pht && pht[0] == '1';
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DD_ECUDA, "cudaSetDevice failed"));
@@ -380,6 +381,7 @@ static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double
     g1.C = c->Z; g1.ldc = 2 * c->Kpad;
     g1.splitk = sk1; g1.ws = c->gws; g1.counters = c->gcnt; g1.num_sms = c->num_sms;
     g1.epi = EPI_SCHUR_DST;
+    g1.pdl = c->pdl; g1.a_static = 1;
     g1.n_param = c->n_param;
     g1.col_param = colp; g1.Kp = c->Kp; g1.gp = c->gp; g1.s = c->sw;
     g1.X = xin; g1.ldx = c->ldv; g1.Zlow = c->Z + c->Kpad;
@@ -391,6 +393,7 @@ static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double
     g2.C = y; g2.ldc = ldy;
     g2.splitk = sk2; g2.ws = c->gws; g2.counters = c->gcnt; g2.num_sms = c->num_sms;
     g2.epi = EPI_STORE;
+    g2.pdl = c->pdl; g2.a_static = 1;
     TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(g2, c->stream));
     return DD_OK;
 }
@@ -423,7 +426,7 @@ extern "C" dd_status dd_apply_precond(dd_ctx* c, int ncols, const int* colp, con
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
     if (c->dim == 3) return precond_3d(c, ncols, colp, r, z, true);
     c->last_ps_warps = polesum_warps(c->geom);
-    TIMED(DD_KCLASS_POLESUM, launch_precond(ncols, colp, c->geom, c->tabs, r, c->n, z, c->n, c->stream));
+    TIMED(DD_KCLASS_POLESUM, launch_precond(ncols, colp, c->geom, c->tabs, r, c->n, z, c->n, c->stream, c->pdl));
     return DD_OK;
 }
 
@@ -448,7 +451,7 @@ static dd_status iteration_body(dd_ctx* c, const PcgState& s) {
     dd_status st = schur_gemms(c, s.ncols, s.col_param, c->p, c->q, c->ldv);
     if (st != DD_OK) return st;
     c->last_ps_warps = polesum_warps(c->geom);
-    TIMED(DD_KCLASS_POLESUM, launch_pcg_iter(s, c->geom, c->tabs, c->stream));
+    TIMED(DD_KCLASS_POLESUM, launch_pcg_iter(s, c->geom, c->tabs, c->stream, c->pdl));
     return DD_OK;
 }
 

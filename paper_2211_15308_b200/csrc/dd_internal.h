@@ -30,6 +30,8 @@ struct GemmArgs {
     double* ws;                  // stream-K partials (gemm_ws_doubles)
     int* counters;               // [tiles], zero on entry, left zero on exit
     int epi;
+    int pdl;                     // launch with programmatic stream serialisation (follows a kernel)
+    int a_static;                // A is constant (prefetched before griddepcontrol.wait)
     int n_param;
     // EPI_SCHUR_DST
     const int* col_param; const double* Kp; const double* gp; const double* s;
@@ -99,9 +101,9 @@ int polesum_warps(const PoleGeom& g);
 size_t polesum_smem(const PoleGeom& g, int max_sys);
 cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b,
                             int ldb, cudaStream_t st);
-cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st);
+cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st, bool pdl = false);
 cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, const PoleTabs& t,
-                           const double* r, int ldr, double* z, int ldz, cudaStream_t st);
+                           const double* r, int ldr, double* z, int ldz, cudaStream_t st, bool pdl = false);
 // whole PCG in one launch for n <= 63 (one CTA per column, operators in shared memory)
 bool pcg_small_supported(int n);
 cudaError_t launch_pcg_small(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b, int ldb,

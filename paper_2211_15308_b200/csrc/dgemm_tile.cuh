@@ -6,10 +6,16 @@
 // (mma.sync.aligned.m16n8k4 .f64 -> SASS DMMA.8x8x4; tcgen05 has no f64 kind).  Operands are
 // staged by a STAGES-deep cp.async (LDGSTS) ring in padded smem rows (BK+4 doubles: the
 // fragment loads of a warp hit distinct bank pairs).  Split-K: gridDim.y = S CTAs of one output
-// tile form a thread-block cluster (1, S, 1); after the main loop each CTA parks its
-// accumulators in its own shared memory and, after a cluster barrier, CTA q reduces the
-// accumulator registers r ≡ q (mod S) of all S CTAs over DSMEM in fixed order s = 0..S-1
-// (bitwise deterministic, no global partials, no serial tail) and runs the epilogue on them.
+// tile form a thread-block cluster (1, S, 1) (S = 1, 2, 4, 8, a template parameter).  After its
+// main loop each CTA q PUSHES accumulator register r into slot [q] of CTA (r mod S)'s reduction
+// buffer with st.shared::cluster (a region of its own, so pushes may land while the owner is
+// still in its main loop); one cluster barrier (arrive.release / wait.acquire); each CTA then sums
+// its S slots from local shared memory in fixed order q = 0..S-1 (bitwise deterministic, no
+// global partials, no remote loads) and runs the epilogue on its registers r ≡ rank (mod S).
+// Programmatic dependent launch: every kernel lets its dependents launch at entry
+// (griddepcontrol.launch_dependents) and waits for its prerequisite grid (griddepcontrol.wait)
+// only before touching data the preceding kernel may write; with `a_static` the first A stages
+// (a constant operand, e.g. the sine matrix) are prefetched before that wait.
 #pragma once
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -41,7 +47,21 @@ struct DgemmProblem {
     long long sA = 0, sB = 0;    // batch strides (elements)
     int batch = 1;
     const int* active = nullptr; // optional per-slab flag: slabs with active[b] == 0 are skipped
+    unsigned long long* ts = nullptr;   // optional per-CTA phase timestamps (lab instrumentation)
+    int a_static = 0;            // A is not written by the preceding kernel: prefetch it before griddepcontrol.wait
 };
+
+// Programmatic dependent launch (no-ops when the launch did not opt in)
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long dg_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define DG_TS(i) \
+    if (g.ts && threadIdx.x == 0) g.ts[(size_t)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 8 + (i)] = dg_gtime()
 
 __device__ __forceinline__ void dg_cp_async16(void* smem, const void* gmem) {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -71,8 +91,7 @@ __device__ __forceinline__ void dg_coord(int r, int tid, int& row, int& col) {
 
 // Issue the cp.async copies of one K-stage (A: BM rows, B: BN columns of BK doubles each).
 template <class C>
-__device__ __forceinline__ void dg_load_stage(double* As, double* Bs, const double* A, int lda, const double* B, int ldb,
-                                              int m0, int n0, int k0, int tid) {
+__device__ __forceinline__ void dg_load_A(double* As, const double* A, int lda, int m0, int k0, int tid) {
 #pragma unroll
     for (int j = 0; j < (C::ACH + C::THREADS - 1) / C::THREADS; j++) {
         const int c = tid + C::THREADS * j;
@@ -81,6 +100,9 @@ __device__ __forceinline__ void dg_load_stage(double* As, double* Bs, const doub
             dg_cp_async16(&As[row * C::LDS + kc], A + (size_t)(m0 + row) * lda + k0 + kc);
         }
     }
+}
+template <class C>
+__device__ __forceinline__ void dg_load_B(double* Bs, const double* B, int ldb, int n0, int k0, int tid) {
 #pragma unroll
     for (int j = 0; j < (C::BCH + C::THREADS - 1) / C::THREADS; j++) {
         const int c = tid + C::THREADS * j;
@@ -90,31 +112,54 @@ __device__ __forceinline__ void dg_load_stage(double* As, double* Bs, const doub
         }
     }
 }
+template <class C>
+__device__ __forceinline__ void dg_load_stage(double* As, double* Bs, const double* A, int lda, const double* B, int ldb,
+                                              int m0, int n0, int k0, int tid) {
+    dg_load_A<C>(As, A, lda, m0, k0, tid);
+    dg_load_B<C>(Bs, B, ldb, n0, k0, tid);
+}
+
+// Shared memory of the split-K tile kernel: the pipeline ring plus (S > 1) a separate
+// reduction buffer [S][ceil(NREG/S)][THREADS].
+template <class C, int S>
+constexpr size_t dg_tile_smem() {
+    return C::SMEM_PIPE + (S > 1 ? size_t(S) * ((C::NREG + S - 1) / S) * C::THREADS * sizeof(double) : 0);
+}
 
 // Epi: functor  __device__ void operator()(int b, int row, int col, double v) const
 // (b = batch index; row < M, col < N checked)
-template <class C, class Epi>
+template <class C, class Epi, int S>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem g, Epi epi) {
     extern __shared__ __align__(16) double smem[];
     double* As = smem;
     double* Bs = smem + C::STAGES * C::BM * C::LDS;
+    pdl_launch_dependents();
     const int bz = blockIdx.z;
-    if (g.active && !g.active[bz]) return;   // frozen slab (uniform across the cluster)
-    g.A += (size_t)bz * g.sA;
-    g.B += (size_t)bz * g.sB;
-
     const int tiles_m = (g.M + C::BM - 1) / C::BM;
     const int m0 = (blockIdx.x % tiles_m) * C::BM;
     const int n0 = (blockIdx.x / tiles_m) * C::BN;
-    const int S = gridDim.y, split = blockIdx.y;
+    const int split = S > 1 ? (int)blockIdx.y : 0;
     const int ktiles = g.K / C::BK;
     const int per = (ktiles + S - 1) / S;
     const int kt0 = split * per;
     const int nkt = max(0, min(per, ktiles - kt0));
-
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wm = warp % C::WM, wn = warp / C::WM;
     const int gq = lane >> 2, tq = lane & 3;
+
+    // prologue: constant A stages may be fetched before the prerequisite grid has finished
+    const bool pre_a = g.a_static && !g.active;
+    const double* A0 = g.A + (size_t)bz * g.sA;
+    if (pre_a) {
+#pragma unroll
+        for (int s = 0; s < C::STAGES - 1; s++)
+            if (s < nkt) dg_load_A<C>(As + s * C::BM * C::LDS, A0, g.lda, m0, (kt0 + s) * C::BK, tid);
+    }
+    pdl_wait();
+    if (g.active && !g.active[bz]) return;   // frozen slab (uniform across the cluster)
+    DG_TS(0);
+    g.A = A0;
+    g.B += (size_t)bz * g.sB;
 
     double acc[C::MI][C::NI][4];
 #pragma unroll
@@ -124,21 +169,21 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
 #pragma unroll
             for (int r = 0; r < 4; r++) acc[i][j][r] = 0.0;
 
-    auto load_stage = [&](int stage, int kt) {
-        dg_load_stage<C>(As + stage * C::BM * C::LDS, Bs + stage * C::BN * C::LDS, g.A, g.lda, g.B, g.ldb, m0, n0,
-                         kt * C::BK, tid);
-    };
-
 #pragma unroll
     for (int s = 0; s < C::STAGES - 1; s++) {
-        if (s < nkt) load_stage(s, kt0 + s);
+        if (s < nkt) {
+            if (!pre_a) dg_load_A<C>(As + s * C::BM * C::LDS, g.A, g.lda, m0, (kt0 + s) * C::BK, tid);
+            dg_load_B<C>(Bs + s * C::BN * C::LDS, g.B, g.ldb, n0, (kt0 + s) * C::BK, tid);
+        }
         dg_cp_commit();
     }
     for (int it = 0; it < nkt; it++) {
         dg_cp_wait<C::STAGES - 2>();
         __syncthreads();
         const int nk = it + C::STAGES - 1;
-        if (nk < nkt) load_stage(nk % C::STAGES, kt0 + nk);
+        if (nk < nkt)
+            dg_load_stage<C>(As + (nk % C::STAGES) * C::BM * C::LDS, Bs + (nk % C::STAGES) * C::BN * C::LDS, g.A, g.lda,
+                             g.B, g.ldb, m0, n0, (kt0 + nk) * C::BK, tid);
         dg_cp_commit();
         const double* as = As + (it % C::STAGES) * C::BM * C::LDS + (wm * C::TM + gq) * C::LDS + tq;
         const double* bs = Bs + (it % C::STAGES) * C::BN * C::LDS + (wn * C::TN + gq) * C::LDS + tq;
@@ -159,8 +204,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
         }
     }
     dg_cp_wait<0>();
+    DG_TS(1);
 
-    if (S == 1) {
+    if constexpr (S == 1) {
 #pragma unroll
         for (int mi = 0; mi < C::MI; mi++)
 #pragma unroll
@@ -172,46 +218,47 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
                     row += m0; col += n0;
                     if (row < g.M && col < g.N) epi(bz, row, col, acc[mi][ni][q]);
                 }
-        return;
-    }
-
-    // ---- split-K: deterministic reduction across the cluster over DSMEM
-    cg::cluster_group cluster = cg::this_cluster();
-    __syncthreads();   // pipeline smem is free now
-    double* red = smem;
+    } else {
+        // ---- split-K: push partials into the owners' reduction buffers over DSMEM, one barrier
+        constexpr int JP = (C::NREG + S - 1) / S;
+        double* red = smem + C::SMEM_PIPE / sizeof(double);
+        const unsigned lred = static_cast<unsigned>(__cvta_generic_to_shared(red));
+        unsigned rbase[S];
 #pragma unroll
-    for (int mi = 0; mi < C::MI; mi++)
+        for (int o = 0; o < S; o++) asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbase[o]) : "r"(lred), "r"(o));
 #pragma unroll
-        for (int ni = 0; ni < C::NI; ni++)
+        for (int mi = 0; mi < C::MI; mi++)
 #pragma unroll
-            for (int q = 0; q < 4; q++) red[((mi * C::NI + ni) * 4 + q) * C::THREADS + tid] = acc[mi][ni][q];
-    cluster.sync();
-    const int rank = (int)cluster.block_rank();
-    // CTA `rank` owns registers r = rank + j*S; source-CTA-outer / register-inner so the DSMEM
-    // loads of one source are in flight together; the sum order over sources is fixed.
-    constexpr int JMAX = C::NREG;
-    double v[JMAX];
+            for (int ni = 0; ni < C::NI; ni++)
 #pragma unroll
-    for (int j = 0; j < JMAX; j++) v[j] = 0.0;
-    for (int s = 0; s < S; s++) {
-        const double* rs = cluster.map_shared_rank(red, s);
+                for (int q = 0; q < 4; q++) {
+                    const int r = (mi * C::NI + ni) * 4 + q;
+                    const unsigned dst = rbase[r % S] + (unsigned)(((split * JP + r / S) * C::THREADS + tid) * sizeof(double));
+                    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dst), "d"(acc[mi][ni][q]) : "memory");
+                }
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        DG_TS(2);
+        double v[JP];
 #pragma unroll
-        for (int j = 0; j < JMAX; j++) {
-            const int r = rank + j * S;
-            if (r < C::NREG) v[j] += rs[r * C::THREADS + tid];
+        for (int j = 0; j < JP; j++) v[j] = 0.0;
+#pragma unroll
+        for (int q = 0; q < S; q++)
+#pragma unroll
+            for (int j = 0; j < JP; j++)
+                if (split + j * S < C::NREG) v[j] += red[(q * JP + j) * C::THREADS + tid];
+        DG_TS(3);
+#pragma unroll
+        for (int j = 0; j < JP; j++) {
+            const int r = split + j * S;
+            if (r < C::NREG) {
+                int row, col;
+                dg_coord<C>(r, tid, row, col);
+                row += m0; col += n0;
+                if (row < g.M && col < g.N) epi(bz, row, col, v[j]);
+            }
         }
+        DG_TS(4);
     }
-#pragma unroll
-    for (int j = 0; j < JMAX; j++) {
-        const int r = rank + j * S;
-        if (r < C::NREG) {
-            int row, col;
-            dg_coord<C>(r, tid, row, col);
-            row += m0; col += n0;
-            if (row < g.M && col < g.N) epi(bz, row, col, v[j]);
-        }
-    }
-    cluster.sync();   // keep every CTA's smem alive until all remote reads are done
 }
 
 // ----------------------------------------------------------------------------------- stream-K
@@ -243,6 +290,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProb
     double* As = smem;
     double* Bs = smem + C::STAGES * C::BM * C::LDS;
     __shared__ int s_last;
+    pdl_launch_dependents();
+    pdl_wait();
 
     const int tiles_m = (g.M + C::BM - 1) / C::BM;
     const int tiles = tiles_m * ((g.N + C::BN - 1) / C::BN);
@@ -396,8 +445,18 @@ inline size_t dgemm_streamk_ws_doubles(int M, int N, int G) {
     return (size_t(G) + 2 * tiles + 2) * C::BM * C::BN;
 }
 
+// PDL launch attribute (programmatic stream serialisation) for launches that follow a kernel
+inline void dg_set_pdl(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, bool pdl) {
+    if (pdl) {
+        at[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+        cfg.numAttrs++;
+    }
+}
+
 template <class C, class Epi>
-inline cudaError_t dgemm_launch_streamk(const DgemmProblem& g, int G, const StreamK& sk, const Epi& epi, cudaStream_t st) {
+inline cudaError_t dgemm_launch_streamk(const DgemmProblem& g, int G, const StreamK& sk, const Epi& epi, cudaStream_t st,
+                                        bool pdl = false) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_dgemm_streamk<C, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -407,8 +466,16 @@ inline cudaError_t dgemm_launch_streamk(const DgemmProblem& g, int G, const Stre
     if (g.M <= 0 || g.N <= 0) return cudaSuccess;
     StreamK s = sk;
     s.G = G;
-    k_dgemm_streamk<C, Epi><<<G, C::THREADS, C::SMEM, st>>>(g, epi, s);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G, 1, 1);
+    cfg.blockDim = dim3(C::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    cfg.attrs = at;
+    cfg.numAttrs = 0;
+    dg_set_pdl(cfg, at, pdl);
+    return cudaLaunchKernelEx(&cfg, k_dgemm_streamk<C, Epi>, g, epi, s);
 }
 
 template <class C>
@@ -416,31 +483,43 @@ inline int dgemm_tiles(int M, int N) {
     return ((M + C::BM - 1) / C::BM) * ((N + C::BN - 1) / C::BN);
 }
 
-template <class C, class Epi>
-inline cudaError_t dgemm_launch(const DgemmProblem& g, int splitk, const Epi& epi, cudaStream_t st) {
+template <class C, class Epi, int S>
+inline cudaError_t dgemm_launch_s(const DgemmProblem& g, const Epi& epi, cudaStream_t st, bool pdl) {
+    constexpr size_t smem = dg_tile_smem<C, S>();
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_dgemm_tile<C, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_dgemm_tile<C, Epi, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        if (C::SMEM > 100 * 1024) cudaFuncSetAttribute(k_dgemm_tile<C, Epi>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (smem > 100 * 1024) cudaFuncSetAttribute(k_dgemm_tile<C, Epi, S>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
     }
-    if (g.M <= 0 || g.N <= 0) return cudaSuccess;
-    if (splitk < 1) splitk = 1;
-    if (splitk > 8) splitk = 8;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(dgemm_tiles<C>(g.M, g.N), splitk, g.batch < 1 ? 1 : g.batch);
+    cfg.gridDim = dim3(dgemm_tiles<C>(g.M, g.N), S, g.batch < 1 ? 1 : g.batch);
     cfg.blockDim = dim3(C::THREADS, 1, 1);
-    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1;
-    at[0].val.clusterDim.y = splitk;
-    at[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute at[2];
     cfg.attrs = at;
-    cfg.numAttrs = splitk > 1 ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_dgemm_tile<C, Epi>, g, epi);
+    cfg.numAttrs = 0;
+    if (S > 1) {
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 1;
+        at[0].val.clusterDim.y = S;
+        at[0].val.clusterDim.z = 1;
+        cfg.numAttrs = 1;
+    }
+    dg_set_pdl(cfg, at, pdl);
+    return cudaLaunchKernelEx(&cfg, k_dgemm_tile<C, Epi, S>, g, epi);
+}
+
+// split-K S is rounded down to a power of two (1, 2, 4, 8)
+template <class C, class Epi>
+inline cudaError_t dgemm_launch(const DgemmProblem& g, int splitk, const Epi& epi, cudaStream_t st, bool pdl = false) {
+    if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+    if (splitk >= 8) return dgemm_launch_s<C, Epi, 8>(g, epi, st, pdl);
+    if (splitk >= 4) return dgemm_launch_s<C, Epi, 4>(g, epi, st, pdl);
+    if (splitk >= 2) return dgemm_launch_s<C, Epi, 2>(g, epi, st, pdl);
+    return dgemm_launch_s<C, Epi, 1>(g, epi, st, pdl);
 }
 
 // Pick split-K S (1..8) for a tile count so that S * tiles fills the SM slots evenly.
@@ -451,7 +530,7 @@ inline int dgemm_pick_splitk(int M, int N, int K, int num_sms, int ctas_per_sm) 
     const int slots = num_sms * ctas_per_sm;
     int best = 1;
     double best_t = 1e30;
-    for (int s = 1; s <= 8; s++) {
+    for (int s = 1; s <= 8; s *= 2) {
         if (s > 1 && ktiles / s < 4) break;
         const int ctas = tiles * s;
         // time ~ (work per CTA) x (CTAs on the busiest SM) / (SM efficiency at that residency):

@@ -56,11 +56,13 @@ size_t gemm_ws_doubles(int M, int N, int num_sms) {
 template <class Epi>
 static cudaError_t launch(const GemmArgs& a, const Epi& e, cudaStream_t st) {
     DgemmProblem g{a.M, a.N, a.K, a.A, a.lda, a.B, a.ldb};
+    g.a_static = a.a_static;
     if (a.splitk == 0) {
         StreamK sk{a.ws, a.counters, 0};
-        return dgemm_launch_streamk<CfgS>(g, dgemm_streamk_grid<CfgS>(a.M, a.N, a.K, a.num_sms, OCC_S), sk, e, st);
+        return dgemm_launch_streamk<CfgS>(g, dgemm_streamk_grid<CfgS>(a.M, a.N, a.K, a.num_sms, OCC_S), sk, e, st,
+                                          a.pdl != 0);
     }
-    return dgemm_launch<CfgC>(g, a.splitk, e, st);
+    return dgemm_launch<CfgC>(g, a.splitk, e, st, a.pdl != 0);
 }
 
 cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {

@@ -23,6 +23,26 @@
 
 namespace dd {
 
+// Programmatic dependent launch (no-ops unless the launch opted in): dependents may launch at
+// entry; the wait precedes every read of data an earlier kernel of the stream writes.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_prior() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename Kern, typename... Args>
+static cudaError_t launch_ex(Kern k, int grid, int block, size_t smem, cudaStream_t st, bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(block, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // transposed, padded layout of a column in shared memory: [row-in-chunk i][thread τ], stride T+1
 __device__ __forceinline__ int tix(int i, int tau, int T) { return i * (T + 1) + tau; }
 __device__ __forceinline__ int clamp_param(int p, int n_param) { return p < 0 ? 0 : (p >= n_param ? n_param - 1 : p); }
@@ -307,10 +327,12 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     extern __shared__ __align__(16) double sm[];
     const int c = blockIdx.x;
     if (c >= ncols) return;
+    pdl_trigger();
     Smem S = carve(sm, g);
     const int npad = g.T * g.LL;
     const int param = clamp_param(col_param[c], t.n_param);
     stage_tables(t, g, param, S.scratch);
+    pdl_wait_prior();
     for (int i = threadIdx.x; i < npad; i += blockDim.x) S.R[tpos(i, g)] = i < g.n ? r[(size_t)c * ldr + i] : 0.0;
     __syncthreads();
     block_polesum<LMAX, G, NG>(t, g, param, S.R, S.Z, S.scratch);
@@ -350,10 +372,12 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     __shared__ double red[64];
     const int c = blockIdx.x;
     const int n = g.n, npad = g.T * g.LL;
+    pdl_trigger();
     Smem S = carve(sm, g);
     const size_t off = (size_t)c * s.ldv;
     const int param = clamp_param(s.col_param[c], t.n_param);
     stage_tables(t, g, param, S.scratch);
+    pdl_wait_prior();
     for (int i = threadIdx.x; i < npad; i += blockDim.x) {
         const double v = i < n ? b[(size_t)c * ldb + i] : 0.0;
         S.R[tpos(i, g)] = v;
@@ -405,16 +429,20 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     Smem S = carve(sm, g);
     const size_t off = (size_t)c * s.ldv;
     const size_t offx = (size_t)c * s.ldx;
+    pdl_trigger();
+    // constant inputs (column parameter, pole tables) before the wait on the preceding GEMM
+    const int param = clamp_param(s.col_param[c], t.n_param);
+    stage_tables(t, g, param, S.scratch);
+    pdl_wait_prior();
     if (threadIdx.x == 0) s_work = s.active[c];
     __syncthreads();
     bool still = false;
 #define DD_PHASE(i) \
     if (s.dbg && blockIdx.x == 0 && threadIdx.x == 0) s.dbg[i] = clock64()
     DD_PHASE(0);
+    if (!s_work) asm volatile("cp.async.wait_all;\n" ::);
     if (s_work) {
         const int k = *s.kiter + 1;
-        const int param = clamp_param(s.col_param[c], t.n_param);
-        stage_tables(t, g, param, S.scratch);
         // one pass over p, q, x, r: all loads in flight together
         double pv[RPT], qv[RPT], xv[RPT], rv[RPT];
 #pragma unroll
@@ -712,26 +740,25 @@ cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st) {
+cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st, bool pdl) {
     if (s.ncols <= 0) return cudaSuccess;
     const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
     DD_POLE_SWITCH(g, {
         e = set_smem(k_pcg_iter<LM, GG, NGG>, smem);
-        if (e == cudaSuccess) k_pcg_iter<LM, GG, NGG><<<s.ncols, 32 * GG * NGG, smem, st>>>(s, g, t);
+        if (e == cudaSuccess) e = launch_ex(k_pcg_iter<LM, GG, NGG>, s.ncols, 32 * GG * NGG, smem, st, pdl, s, g, t);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, const PoleTabs& t, const double* r,
-                           int ldr, double* z, int ldz, cudaStream_t st) {
+                           int ldr, double* z, int ldz, cudaStream_t st, bool pdl) {
     if (ncols <= 0) return cudaSuccess;
     const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
     DD_POLE_SWITCH(g, {
         e = set_smem(k_precond<LM, GG, NGG>, smem);
-        if (e == cudaSuccess)
-            k_precond<LM, GG, NGG><<<ncols, 32 * GG * NGG, smem, st>>>(ncols, col_param, g, t, r, ldr, z, ldz);
+        if (e == cudaSuccess) e = launch_ex(k_precond<LM, GG, NGG>, ncols, 32 * GG * NGG, smem, st, pdl, ncols, col_param, g, t, r, ldr, z, ldz);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
 }

@@ -31,8 +31,8 @@ template <class C>
 void run_variant(const char* name, int M, int N, int K, const double* A, const double* B, double* Cm, const double* Cref,
                  int sms, int splitk_force) {
     int occ = 0;
-    cudaFuncSetAttribute(k_dgemm_tile<C, StoreEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dgemm_tile<C, StoreEpi>, C::THREADS, C::SMEM);
+    cudaFuncSetAttribute(k_dgemm_tile<C, StoreEpi, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dgemm_tile<C, StoreEpi, 1>, C::THREADS, C::SMEM);
     DgemmProblem g{M, N, K, A, K, B, K};
     StoreEpi epi{Cm, M};
     int sks[9] = {0};
@@ -103,9 +103,11 @@ void run_streamk(const char* name, int M, int N, int K, const double* A, const d
 int main(int argc, char** argv) {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cublasHandle_t hb; cublasCreate(&hb);
-    struct Shape { int M, N, K; } shapes[] = {{1023, 256, 1024}, {1023, 256, 2048}, {2046, 256, 1024}, {2047, 512, 2048},
+    struct Shape { int M, N, K; } all_shapes[] = {{1023, 256, 1024}, {1023, 256, 2048}, {2046, 256, 1024}, {2047, 512, 2048},
                                               {2047, 512, 4096}, {4094, 512, 2048}, {4095, 128, 4096}, {4095, 128, 8192},
                                               {8190, 128, 4096}};
+    const int nshapes = argc > 1 ? atoi(argv[1]) : 9;   // first n shapes (3 = config-2 shapes only)
+    std::vector<Shape> shapes(all_shapes, all_shapes + nshapes);
     for (auto s : shapes) {
         const int M = s.M, N = s.N, K = s.K;
         const int Mp = (M + 255) / 256 * 256, Np = (N + 255) / 256 * 256;
@@ -133,6 +135,11 @@ int main(int argc, char** argv) {
         run_variant<DgemmCfg<64, 64, 16, 2, 2, 4, 2>>("64x64k16_w2x2_s4", M, N, K, A, B, C, Cr, sms, f);
         run_variant<DgemmCfg<64, 64, 16, 2, 2, 3, 3>>("64x64k16_w2x2_s3", M, N, K, A, B, C, Cr, sms, f);
         run_variant<DgemmCfg<64, 64, 32, 2, 2, 3, 2>>("64x64k32_w2x2_s3", M, N, K, A, B, C, Cr, sms, f);
+        run_variant<DgemmCfg<128, 64, 16, 4, 2, 3, 2>>("128x64k16_w4x2_s3", M, N, K, A, B, C, Cr, sms, f);
+        run_variant<DgemmCfg<64, 128, 16, 2, 4, 3, 2>>("64x128k16_w2x4_s3", M, N, K, A, B, C, Cr, sms, f);
+        run_variant<DgemmCfg<128, 64, 16, 2, 2, 3, 2>>("128x64k16_w2x2_s3", M, N, K, A, B, C, Cr, sms, f);
+        run_variant<DgemmCfg<64, 64, 16, 2, 2, 6, 2>>("64x64k16_w2x2_s6", M, N, K, A, B, C, Cr, sms, f);
+        run_variant<DgemmCfg<32, 64, 16, 1, 2, 4, 4>>("32x64k16_w1x2_s4", M, N, K, A, B, C, Cr, sms, f);
         cudaFree(A); cudaFree(B); cudaFree(C); cudaFree(Cr);
     }
     return 0;
