@@ -59,8 +59,10 @@ static cudaError_t launch(const GemmArgs& a, const Epi& e, cudaStream_t st) {
     g.a_static = a.a_static;
     if (a.splitk == 0) {
         StreamK sk{a.ws, a.counters, 0};
+        // no PDL here: early-resident CTAs of a stream-K grid land unevenly on the SMs (a third
+        // CTA beside the predecessor's two), which breaks the equal-work-per-SM premise (cfg3: -25%)
         return dgemm_launch_streamk<CfgS>(g, dgemm_streamk_grid<CfgS>(a.M, a.N, a.K, a.num_sms, OCC_S), sk, e, st,
-                                          a.pdl != 0);
+                                          false);
     }
     return dgemm_launch<CfgC>(g, a.splitk, e, st, a.pdl != 0);
 }

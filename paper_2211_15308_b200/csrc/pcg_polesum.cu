@@ -19,6 +19,8 @@
 //
 // PCG: one fused kernel per iteration after the two
 // GEMMs: α = ρ/(p·q); x += αp; r -= αq; z = P r; ρ' = r·z; η test; β = ρ'/ρ; p = z + βp.
+#include <algorithm>
+
 #include "dd_internal.h"
 
 namespace dd {
@@ -283,10 +285,139 @@ __device__ void block_polesum_impl(const PoleTabs& t, const PoleGeom& g, int par
 #undef DD_PS
 }
 
+// FULL geometry (n + 1 = T LL: every chunk has LL - 1 interior rows, only the last separator is
+// padding) — the BASELINE shapes.  Same arithmetic as block_polesum_impl, restructured for issue
+// and latency: the group's share of the pole sum is accumulated in registers (no shared-memory
+// read-modify-write per row and system), the broadcast table reads are 16-byte vector loads of
+// a whole row pair, and the PCR multipliers / per-system scalars of the NEXT system are fetched
+// from global memory while the current one is swept.
+template <int LL, int G, int NG>
+__device__ void block_polesum_full(const PoleTabs& t, int param, const double* R, double* Z, double* scratch,
+                                   long long* dbg) {
+    constexpr int T = 32 * G;
+    constexpr int JM = G == 1 ? 5 : (G == 2 ? 6 : (G == 4 ? 7 : 8));   // log2(32 G)
+    constexpr int tot = LL * (T + 1);
+    static_assert(LL % 2 == 0, "row pairs");
+    const int tid = threadIdx.x;
+    const int group = tid / T, tau = tid % T;
+    const int nsys = t.nsys[param];
+    const size_t pbase = (size_t)param * t.max_sys;
+    const size_t tstride = (size_t)t.max_sys * LL;
+    const double* tab = scratch;
+    double* xbuf = scratch + 4 * tstride;
+    double* Zw = xbuf + 2 * NG * T;
+    double* xb = xbuf + (size_t)group * 2 * T;
+    const bool sep_real = tau < T - 1;
+    const double* Rt = R + tau;              // row i of this thread's chunk: Rt[i * (T + 1)]
+
+    double zacc[LL];
+#pragma unroll
+    for (int i = 0; i < LL; i++) zacc[i] = 0.0;
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    if (dbg && threadIdx.x == 0) dbg[6] = clock64();
+
+    for (int k = group; k < nsys; k += NG) {
+        // per-system scalars and this thread's PCR multipliers: issued first (volatile loads are not
+        // sunk), their latency hides under the sweeps
+        const double e = ldg_early(&t.e[pbase + k]), wk = ldg_early(&t.w[pbase + k]);
+        double pav[JM], pbv[JM];
+        {
+            const double* pa = t.pa + (pbase + k) * (size_t)JM * T + tau;
+            const double* pb = t.pb + (pbase + k) * (size_t)JM * T + tau;
+#pragma unroll
+            for (int j = 0; j < JM; j++) { pav[j] = ldg_early(&pa[j * T]); pbv[j] = ldg_early(&pb[j * T]); }
+        }
+        const double pinv = ldg_early(&t.pinvb[(pbase + k) * T + tau]);
+        const double2* ib2 = reinterpret_cast<const double2*>(tab + (size_t)k * LL);
+        const double2* cp2 = reinterpret_cast<const double2*>(tab + tstride + (size_t)k * LL);
+        const double2* u2 = reinterpret_cast<const double2*>(tab + 2 * tstride + (size_t)k * LL);
+
+        // forward:  ỹ_i = r_i/b'_i - (e/b'_i) ỹ_{i-1},  i = 0 .. LL-2
+        double y[LL];
+        double prev = 0.0;
+#pragma unroll
+        for (int i2 = 0; i2 < LL / 2; i2++) {
+            const double2 ib = ib2[i2], cp = cp2[i2];
+            const int i = 2 * i2;
+            if (i < LL - 1) { prev = fma(-cp.x, prev, Rt[i * (T + 1)] * ib.x); y[i] = prev; }
+            if (i + 1 < LL - 1) { prev = fma(-cp.y, prev, Rt[(i + 1) * (T + 1)] * ib.y); y[i + 1] = prev; }
+        }
+        const double y_last = y[LL - 2];
+        // backward:  y_i = ỹ_i - (e/b'_i) y_{i+1}
+#pragma unroll
+        for (int i2 = (LL - 2) / 2; i2 >= 0; i2--) {
+            const double2 cp = cp2[i2];
+            const int i = 2 * i2;
+            if (i + 1 <= LL - 3) y[i + 1] = fma(-cp.y, y[i + 2], y[i + 1]);
+            if (i <= LL - 3) y[i] = fma(-cp.x, y[i + 1], y[i]);
+        }
+        const double y_first_next = group_shift<G>(y[0], 1, tau, xb, group);
+        double rs = 0.0;
+        if (sep_real) rs = Rt[(LL - 1) * (T + 1)] - e * y_last - e * y_first_next;
+        // parallel cyclic reduction over the T separators
+        if constexpr (G == 1) {
+#pragma unroll
+            for (int j = 0; j < 5; j++) {
+                const int s = 1 << j;
+                double rm = __shfl_up_sync(0xffffffffu, rs, s);
+                double rp = __shfl_down_sync(0xffffffffu, rs, s);
+                if (tau < s) rm = 0.0;
+                if (tau + s > T - 1) rp = 0.0;
+                rs = rs - pav[j] * rm - pbv[j] * rp;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < JM; j++) {
+                const int s = 1 << j;
+                double* buf = xb + (j & 1) * T;
+                buf[tau] = rs;
+                group_sync<G>(group);
+                const double rm = (tau >= s) ? buf[tau - s] : 0.0;
+                const double rp = (tau + s < T) ? buf[tau + s] : 0.0;
+                rs = rs - pav[j] * rm - pbv[j] * rp;
+            }
+            group_sync<G>(group);
+        }
+        const double gsep = sep_real ? rs * pinv : 0.0;
+        const double gleft = group_shift<G>(gsep, -1, tau, xb, group);
+        const double eg0 = e * gleft, eg1 = e * gsep;
+        // x_i = y_i - e g_{τ-1} u_i - e g_τ u_{LL-2-i};  z += w_k x
+#pragma unroll
+        for (int i2 = 0; i2 < LL / 2; i2++) {
+            const double2 ua = u2[i2];
+            const int i = 2 * i2;
+            if (i < LL - 1) zacc[i] = fma(wk, y[i] - eg0 * ua.x - eg1 * tab[2 * tstride + (size_t)k * LL + (LL - 2 - i)], zacc[i]);
+            if (i + 1 < LL - 1)
+                zacc[i + 1] = fma(wk, y[i + 1] - eg0 * ua.y - eg1 * tab[2 * tstride + (size_t)k * LL + (LL - 3 - i)], zacc[i + 1]);
+        }
+        zacc[LL - 1] = fma(wk, gsep, zacc[LL - 1]);
+        if (dbg && threadIdx.x == 0 && k == 0) dbg[7] = dbg[8] = dbg[9] = clock64();
+    }
+    if (dbg && threadIdx.x == 0) dbg[10] = clock64();
+    // fixed-order combine of the NG group partials
+    double* zg = Zw + (size_t)group * tot;
+#pragma unroll
+    for (int i = 0; i < LL; i++) zg[tix(i, tau, T)] = zacc[i];
+    __syncthreads();
+    for (int idx = tid; idx < tot; idx += blockDim.x) {
+        double acc = Zw[idx];
+        for (int gg = 1; gg < NG; gg++) acc += Zw[(size_t)gg * tot + idx];
+        Z[idx] = acc;
+    }
+    __syncthreads();
+}
+
 template <int LMAX, int G, int NG>
 __device__ __forceinline__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, const double* R,
                                               double* Z, double* scratch, long long* dbg = nullptr) {
-    if (g.LL == LMAX && g.n + 1 == g.T * g.LL) block_polesum_impl<LMAX, G, NG, true>(t, g, param, R, Z, scratch, dbg);
+    if (g.LL == LMAX && g.n + 1 == g.T * g.LL) {
+        if constexpr (LMAX >= 2) {
+            block_polesum_full<LMAX, G, NG>(t, param, R, Z, scratch, dbg);
+            return;
+        }
+        block_polesum_impl<LMAX, G, NG, true>(t, g, param, R, Z, scratch, dbg);
+    }
     else block_polesum_impl<LMAX, G, NG, false>(t, g, param, R, Z, scratch, dbg);
 }
 
@@ -511,16 +642,10 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
                 if (threadIdx.x == 0) s.active[c] = 0;
             } else {
                 const double beta = rz / s.rho[c];
-                double pn[RPT];
 #pragma unroll
                 for (int j = 0; j < RPT; j++) {
                     const int i = threadIdx.x + j * NT;
-                    pn[j] = i < n ? s.p[off + i] : 0.0;
-                }
-#pragma unroll
-                for (int j = 0; j < RPT; j++) {
-                    const int i = threadIdx.x + j * NT;
-                    if (i < n) s.p[off + i] = fma(beta, pn[j], zv[j]);
+                    if (i < n) s.p[off + i] = fma(beta, pv[j], zv[j]);   // pv: p as loaded at entry
                 }
                 __syncthreads();
                 if (threadIdx.x == 0) s.rho[c] = rz;
