@@ -69,6 +69,33 @@ typedef struct {
 typedef struct dd_ctx dd_ctx;
 
 /*
+ * dd_frac — the fractional perturbation, generalising Eq.(2)'s γ(-Δ_Γ)^{-1/2} to Eq.(9)'s
+ * γ L^t:
+ *   t         exponent, -1 < t < 1 (Eq.(2): t = -1/2)
+ *   shifted   0: L = -Δ_Γ, the pair (A_Γ, M_Γ) (Eq.(2));  1: L = -Δ_Γ + I_Γ, i.e. (A_Γ + M_Γ, M_Γ)
+ *             (Eq.(9))
+ *   mode      DD_FRAC_DENSE: F = (M U)(Λ_L)^t (M U)^T formed once at setup (Eq.(7));
+ *             DD_FRAC_RA: F x ≈ M r_F(L) M x through a second rational approximation
+ *             r_F(λ) = fc0 + Σ fc_k/(λ - fp_k) ≈ λ^t applied as a pole sum (Remark 1,
+ *             PAPER.md:274-288): linear memory and work, no dense n_Γ² block
+ *   fc0, n_fpoles, fpoles, fresidues   r_F for DD_FRAC_RA (host; ignored for DENSE); fp_k < 0
+ *             are poles of the unshifted pair (A_Γ, M_Γ), like dd_setup's `poles`
+ * The preconditioner's RA (dd_setup's poles/residues) must then approximate
+ * (K λ_L^{1/2} + γ λ_L^t)^-1 in λ of the pair (A_Γ, M_Γ) — the library only applies it.
+ */
+typedef struct {
+    double t;
+    int shifted;
+    int mode;
+    double fc0;
+    int n_fpoles;
+    const double* fpoles;
+    const double* fresidues;
+} dd_frac;
+#define DD_FRAC_DENSE 0
+#define DD_FRAC_RA 1
+
+/*
  * dd_setup — build a handle for one mesh and n_param parameter sets.
  *   K[n_param], mu_inv[n_param]   host; K > 0, mu_inv >= 0   (γ = mu_inv)
  *   poles, residues               host [n_param * n_poles]; parameter set j uses entries
@@ -87,6 +114,14 @@ dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K, const doub
                    int n_poles, const double* poles, const double* residues, const double* c0,
                    int max_cols, int device, void* cuda_stream, const dd_dist* dist,
                    dd_ctx** out);
+
+/* dd_setup with a general fractional perturbation (dd_frac above; NULL = Eq.(2): t = -1/2,
+ * unshifted, dense F).  Extra DD_EINVAL cases: t not in (-1, 1), shifted not in {0, 1},
+ * mode unknown, DD_FRAC_RA with a pole >= 0 / non-finite coefficient. */
+dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n_param, const double* K,
+                      const double* mu_inv, int n_poles, const double* poles, const double* residues,
+                      const double* c0, int max_cols, int device, void* cuda_stream,
+                      const dd_dist* dist, dd_ctx** out);
 
 /* n_Γ = N-1 (2D) or (N-1)^2 (3D); -1 for a NULL handle. */
 int dd_interface_size(const dd_ctx* ctx);

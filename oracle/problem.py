@@ -21,12 +21,15 @@ from . import fem, ra, schur, spectral
 
 
 class DenseProblem:
-    def __init__(self, dim: int, N: int, method: str = "layers"):
-        self.dim, self.N = dim, N
+    """t, sigma: the perturbation γ L^t with L = -Δ_Γ + σ I_Γ (Eq.(2): t = -1/2, σ = 0;
+    Eq.(9), PAPER.md:208-216: general -1 < t < 1 and σ = 1)."""
+
+    def __init__(self, dim: int, N: int, method: str = "layers", t: float = -0.5, sigma: float = 0.0):
+        self.dim, self.N, self.t, self.sigma = dim, N, t, sigma
         self.S_unit = schur.schur_layers(dim, N) if method == "layers" else schur.schur_bruteforce(dim, N)
         self.A_g, self.M_g = fem.trace_pair(dim, N)
         self.gevp = spectral.GEVP(self.A_g, self.M_g)
-        self.F = self.gevp.power(-0.5)
+        self.F = self.gevp.power(t, sigma)
         self.n_gamma = self.S_unit.shape[0]
 
     def S(self, K, gamma):
@@ -39,7 +42,7 @@ class DenseProblem:
         return ra.apply_ra(self.A_g, self.M_g, c0, poles, residues, X)
 
     def apply_P_exact(self, K, gamma, X):
-        return ra.apply_exact_precond(self.gevp, K, gamma, X)
+        return ra.apply_exact_precond(self.gevp, K, gamma, X, self.t, self.sigma)
 
     def apply_P_ra_eigen(self, c0, poles, residues, X):
         return ra.apply_ra_eigen(self.gevp, c0, poles, residues, X)
@@ -49,8 +52,8 @@ class DenseProblem:
 
 
 class ModeProblem2D:
-    def __init__(self, N: int):
-        self.dim, self.N = 2, N
+    def __init__(self, N: int, t: float = -0.5, sigma: float = 0.0):
+        self.dim, self.N, self.t, self.sigma = 2, N, t, sigma
         n = N - 1
         self.n_gamma = n
         a_d, a_o, m_d, m_o = fem.trace_pair_1d(N)
@@ -63,7 +66,7 @@ class ModeProblem2D:
         self.mu = m_d[0] + 2.0 * mo * c             # M_Γ mode values
         self.lam = self.alpha / self.mu             # generalised eigenvalues of (A_Γ, M_Γ)
         self.s = schur.schur_modes_2d(N)            # S_unit mode values
-        self.f = self.mu * self.lam ** -0.5         # F mode values: (MU) Λ^-1/2 (MU)^T
+        self.f = self.mu * (self.lam + sigma) ** t  # F mode values: (MU) (Λ+σ)^t (MU)^T
         self.band = (a_d, a_o, m_d, m_o)
 
     def apply_S(self, K, gamma, X):
@@ -85,7 +88,8 @@ class ModeProblem2D:
 
     def apply_P_exact(self, K, gamma, X):
         Xh = schur.dst_ortho(X, axis=0)
-        w = 1.0 / (self.mu * (K * self.lam ** 0.5 + gamma * self.lam ** -0.5))
+        x = self.lam + self.sigma
+        w = 1.0 / (self.mu * (K * x ** 0.5 + gamma * x ** self.t))
         return schur.dst_ortho(w[:, None] * Xh if X.ndim == 2 else w * Xh, axis=0)
 
     def spectrum(self):

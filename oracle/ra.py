@@ -22,10 +22,12 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 
-def f_target(x, K: float, gamma: float):
-    """f(x) = 1/(K x^{1/2} + γ x^{-1/2})  (with α=K, s=1/2, β=γ, t=-1/2)."""
-    x = np.asarray(x, dtype=np.float64)
-    return 1.0 / (K * np.sqrt(x) + gamma / np.sqrt(x))
+def f_target(x, K: float, gamma: float, t: float = -0.5, sigma: float = 0.0):
+    """f(x) = 1/(K x^{1/2} + γ x^{-1/2})  (PAPER.md:193, with α=K, s=1/2, β=γ, t=-1/2);
+    generally 1/(K (x+σ)^{1/2} + γ (x+σ)^t) — Eq.(9)'s S_Γ = K L^{1/2} + γ L^t with
+    L = -Δ_Γ + σ I_Γ, as a function of the eigenvalue x of the pair (A_Γ, M_Γ)."""
+    x = np.asarray(x, dtype=np.float64) + sigma
+    return 1.0 / (K * np.sqrt(x) + gamma * x ** t)
 
 
 def r_eval(x, c0: float, poles, residues):
@@ -37,10 +39,10 @@ def r_eval(x, c0: float, poles, residues):
     return out
 
 
-def ra_rel_error(c0, poles, residues, K, gamma, xs) -> float:
+def ra_rel_error(c0, poles, residues, K, gamma, xs, t: float = -0.5, sigma: float = 0.0) -> float:
     """max_x |r(x)/f(x) - 1| over the points xs (pointwise relative error, reading A10)."""
     xs = np.asarray(xs, dtype=np.float64)
-    return float(np.max(np.abs(r_eval(xs, c0, poles, residues) / f_target(xs, K, gamma) - 1.0)))
+    return float(np.max(np.abs(r_eval(xs, c0, poles, residues) / f_target(xs, K, gamma, t, sigma) - 1.0)))
 
 
 def cancellation_factor(c0, poles, residues, K, gamma, xs) -> float:
@@ -100,6 +102,8 @@ def apply_ra_eigen(gevp, c0, poles, residues, B: np.ndarray) -> np.ndarray:
     return gevp.apply_function(r_eval(gevp.lam, c0, poles, residues), B)
 
 
-def apply_exact_precond(gevp, K: float, gamma: float, B: np.ndarray) -> np.ndarray:
-    """Exact S_Γ^-1 B = U diag(1/(K λ^{1/2} + γ λ^{-1/2})) U^T B  (Eq.(6)/(7))."""
-    return gevp.apply_sum_inverse([(K, 0.5), (gamma, -0.5)], B)
+def apply_exact_precond(gevp, K: float, gamma: float, B: np.ndarray, t: float = -0.5,
+                        sigma: float = 0.0) -> np.ndarray:
+    """Exact S_Γ^-1 B = U diag(1/(K λ^{1/2} + γ λ^{-1/2})) U^T B  (Eq.(6)/(7)); generally
+    S_Γ = K L^{1/2} + γ L^t with L = A + σM (Eq.(9))."""
+    return gevp.apply_sum_inverse([(K, 0.5), (gamma, t)], B, sigma)

@@ -26,19 +26,20 @@ class GEVP:
         self.lam, self.U, self.M, self.L = lam, U, M, L
         self.MU = M @ U
 
-    def power(self, s: float) -> np.ndarray:
-        """L^s_h = (M U) Λ^s (M U)^T  (Eq.(7))."""
-        return (self.MU * self.lam ** s) @ self.MU.T
+    def power(self, s: float, sigma: float = 0.0) -> np.ndarray:
+        """L^s_h = (M U) Λ^s (M U)^T  (Eq.(7)); with sigma, of L + σM (same U, eigenvalues
+        λ + σ) — Eq.(9)'s shifted L = -Δ_Γ + I_Γ for σ = 1."""
+        return (self.MU * (self.lam + sigma) ** s) @ self.MU.T
 
     def apply_power(self, s: float, X: np.ndarray) -> np.ndarray:
         return self.MU @ _scale_rows(self.lam ** s, self.MU.T @ X)
 
-    def apply_sum_inverse(self, terms, B: np.ndarray) -> np.ndarray:
-        """x = U diag(Σ_i α_i λ^{s_i})^{-1} U^T b: the exact inverse of Σ_i α_i L^{s_i}
-        in the Eq.(7) calculus (inverse of the Schur preconditioner Eq.(6))."""
+    def apply_sum_inverse(self, terms, B: np.ndarray, sigma: float = 0.0) -> np.ndarray:
+        """x = U diag(Σ_i α_i (λ+σ)^{s_i})^{-1} U^T b: the exact inverse of Σ_i α_i L^{s_i}
+        in the Eq.(7) calculus (inverse of the Schur preconditioner Eq.(6), L = A + σM)."""
         w = np.zeros_like(self.lam)
         for alpha, s in terms:
-            w = w + alpha * self.lam ** s
+            w = w + alpha * (self.lam + sigma) ** s
         return self.U @ _scale_rows(1.0 / w, self.U.T @ B)
 
     def apply_function(self, fvals: np.ndarray, B: np.ndarray) -> np.ndarray:

@@ -21,7 +21,7 @@ DD_OK, DD_EINVAL, DD_ECUDA, DD_ENOMEM, DD_ENOTSPD, DD_ENOCONV, DD_ENCCL, DD_EUNS
 STATUS_NAMES = ["DD_OK", "DD_EINVAL", "DD_ECUDA", "DD_ENOMEM", "DD_ENOTSPD", "DD_ENOCONV", "DD_ENCCL", "DD_EUNSUPPORTED"]
 KCLASS = ["gemm_dst", "gemm_schur", "polesum_pcg", "other"]
 
-EXPORTS = ["dd_setup", "dd_interface_size", "dd_apply_schur", "dd_apply_precond", "dd_pcg_solve",
+EXPORTS = ["dd_setup", "dd_setup_ex", "dd_interface_size", "dd_apply_schur", "dd_apply_precond", "dd_pcg_solve",
            "dd_pcg_solve_host", "dd_destroy", "dd_last_error", "dd_profile_enable", "dd_profile_read",
            "dd_launch_count", "dd_query_config", "dd_test_dgemm", "dd_last_solve_ms", "dd_nccl_unique_id",
            "dd_inner_iterations"]
@@ -42,6 +42,24 @@ class _Dist(ctypes.Structure):
                 ("mode", ctypes.c_int)]
 
 
+class _Frac(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_double), ("shifted", ctypes.c_int), ("mode", ctypes.c_int), ("fc0", ctypes.c_double),
+                ("n_fpoles", ctypes.c_int), ("fpoles", ctypes.c_void_p), ("fresidues", ctypes.c_void_p)]
+
+
+DD_FRAC_DENSE, DD_FRAC_RA = 0, 1
+
+
+@dataclass
+class Frac:
+    """Fractional perturbation γ L^t (dd_frac): t in (-1, 1); shifted: L = -Δ_Γ + I_Γ;
+    mode 'dense' (F formed at setup) or 'ra' (F x = M r_F(L) M x, r_F = fra ≈ λ^t, Remark 1)."""
+    t: float = -0.5
+    shifted: bool = False
+    mode: str = "dense"
+    fra: object = None           # RationalApprox-like (c0, poles, residues) in the pair (A_Γ, M_Γ) convention
+
+
 _lib = None
 
 
@@ -56,6 +74,9 @@ def load():
     P, I, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
     lib.dd_setup.argtypes = [ctypes.POINTER(_Mesh), I, P, P, I, P, P, P, I, I, P, ctypes.POINTER(_Dist), ctypes.POINTER(P)]
     lib.dd_setup.restype = I
+    lib.dd_setup_ex.argtypes = [ctypes.POINTER(_Mesh), ctypes.POINTER(_Frac), I, P, P, I, P, P, P, I, I, P,
+                                ctypes.POINTER(_Dist), ctypes.POINTER(P)]
+    lib.dd_setup_ex.restype = I
     lib.dd_interface_size.argtypes = [P]; lib.dd_interface_size.restype = I
     lib.dd_apply_schur.argtypes = [P, I, P, P, P]; lib.dd_apply_schur.restype = I
     lib.dd_apply_precond.argtypes = [P, I, P, P, P]; lib.dd_apply_precond.restype = I
@@ -106,9 +127,11 @@ class Solver:
     zero residues).
     """
 
-    def __init__(self, dim: int, N: int, params, ras, max_cols: int, device: int = 0, stream=None, dist=None):
+    def __init__(self, dim: int, N: int, params, ras, max_cols: int, device: int = 0, stream=None, dist=None,
+                 frac: Frac = None):
         """dist: None, or (rank, world, mode, unique_id_bytes) with mode DD_SHARD_COLUMNS (0) or
-        DD_SHARD_POLES (1); the 128-byte unique id comes from nccl_unique_id() on rank 0."""
+        DD_SHARD_POLES (1); the 128-byte unique id comes from nccl_unique_id() on rank 0.
+        frac: None (Eq.(2): t = -1/2, unshifted, dense F) or a Frac."""
         import torch
         self._torch = torch
         lib = load()
@@ -131,9 +154,18 @@ class Solver:
             self._uid = ctypes.create_string_buffer(bytes(uid) if uid is not None else bytes(128), 128)
             self._dist = _Dist(int(rank), int(world), ctypes.cast(self._uid, ctypes.c_void_p), int(mode))
             dptr = ctypes.byref(self._dist)
-        st = lib.dd_setup(ctypes.byref(mesh), self.n_param, K.ctypes.data, mu.ctypes.data, m, poles.ctypes.data,
-                          res.ctypes.data, c0.ctypes.data, int(max_cols), int(device),
-                          ctypes.c_void_p(self.stream.cuda_stream), dptr, ctypes.byref(h))
+        fr = frac if frac is not None else Frac()
+        self.frac = fr
+        fpol = _f64(fr.fra.poles if fr.fra is not None else [])
+        fres = _f64(fr.fra.residues if fr.fra is not None else [])
+        self._fkeep = (fpol, fres)
+        mode = {"dense": DD_FRAC_DENSE, "ra": DD_FRAC_RA}.get(fr.mode, -1)
+        cfr = _Frac(float(fr.t), int(bool(fr.shifted)), mode,
+                    float(fr.fra.c0) if fr.fra is not None else 0.0, int(fpol.size),
+                    fpol.ctypes.data if fpol.size else None, fres.ctypes.data if fres.size else None)
+        st = lib.dd_setup_ex(ctypes.byref(mesh), ctypes.byref(cfr), self.n_param, K.ctypes.data, mu.ctypes.data, m,
+                             poles.ctypes.data, res.ctypes.data, c0.ctypes.data, int(max_cols), int(device),
+                             ctypes.c_void_p(self.stream.cuda_stream), dptr, ctypes.byref(h))
         _check(st)
         self._h = h
         self.max_cols = int(max_cols)

@@ -102,7 +102,9 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
         f.lam_min = lam.front();
         f.lam_max = lam.back();
         std::vector<double> w4(n2);
-        for (int j = 0; j < n2; j++) w4[j] = (double)powl((long double)lam[j], -0.25L);
+        // F = (M U)(Λ + σ)^t (M U)^T = B B^T with B = M U (Λ + σ)^{t/2}  (Eq.(7); dd_frac)
+        for (int j = 0; j < n2; j++)
+            w4[j] = (double)powl((long double)lam[j] + (long double)c->frac_sigma, 0.5L * (long double)c->frac_t);
         DD_CK(cudaMemcpyAsync(dW, w4.data(), n2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         // B = M U Λ^{-1/4} (column-major in dM), then row-major in dA; F = B B^T into the padded layout
         DD_CK(face_mass_cols(n, hh12, dA, dM, n2, n2, c->stream));

@@ -159,13 +159,14 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
         }
         swh[b] = (double)((1.0L + 0.5L * sig[b]) - g);
     }
-    // F = S diag(μ_b λ_b^{-1/2}) S  (Eq.(7) in closed form for the 1D pair, t = -1/2):
+    // F = S diag(μ_b (λ_b + σ)^t) S  (Eq.(7) in closed form for the 1D pair; Eq.(2): t = -1/2,
+    // σ = 0; Eq.(9)'s shifted L = A_Γ + M_Γ has eigenvalues λ_b + 1 with the same vectors):
     // μ_b = (h/6)(6 - σ_b),  λ_b = 6 σ_b / (h^2 (6 - σ_b))
     std::vector<double> Bh((size_t)c->Kpad * round_up(n, GEMM_BN), 0.0);
     for (int k = 0; k < n; k++) {
         const long double mu = h / 6.0L * (6.0L - sig[k]);
         const long double lam = 6.0L * sig[k] / (h * h * (6.0L - sig[k]));
-        const long double f = mu / sqrtl(lam);
+        const long double f = mu * powl(lam + (long double)c->frac_sigma, (long double)c->frac_t);
         for (int j = 0; j < n; j++) Bh[(size_t)j * c->Kpad + k] = (double)(f * (long double)Wh[(size_t)k * c->lda + j]);
     }
     CK(dalloc(c, &c->W, (size_t)c->Mpad * c->lda));
@@ -293,7 +294,28 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
 extern "C" dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K, const double* mu_inv, int n_poles,
                               const double* poles, const double* residues, const double* c0, int max_cols, int device,
                               void* cuda_stream, const dd_dist* dist, dd_ctx** out) {
+    return dd_setup_ex(mesh, nullptr, n_param, K, mu_inv, n_poles, poles, residues, c0, max_cols, device, cuda_stream,
+                       dist, out);
+}
+
+extern "C" dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n_param, const double* K,
+                                 const double* mu_inv, int n_poles, const double* poles, const double* residues,
+                                 const double* c0, int max_cols, int device, void* cuda_stream, const dd_dist* dist,
+                                 dd_ctx** out) {
     if (!out) return fail(DD_EINVAL, "out is NULL");
+    dd_frac fr{-0.5, 0, DD_FRAC_DENSE, 0.0, 0, nullptr, nullptr};
+    if (frac) fr = *frac;
+    if (!(fr.t > -1.0 && fr.t < 1.0)) return fail(DD_EINVAL, "fractional exponent t must lie in (-1, 1)");
+    if (fr.shifted != 0 && fr.shifted != 1) return fail(DD_EINVAL, "shifted must be 0 or 1");
+    if (fr.mode != DD_FRAC_DENSE && fr.mode != DD_FRAC_RA) return fail(DD_EINVAL, "unknown fractional mode");
+    if (fr.mode == DD_FRAC_RA) {
+        if (fr.n_fpoles < 0 || (fr.n_fpoles > 0 && (!fr.fpoles || !fr.fresidues)) || !std::isfinite(fr.fc0))
+            return fail(DD_EINVAL, "bad RA of the fractional term");
+        for (int k = 0; k < fr.n_fpoles; k++)
+            if (!(fr.fpoles[k] < 0.0) || !std::isfinite(fr.fpoles[k]) || !std::isfinite(fr.fresidues[k]))
+                return fail(DD_EINVAL, "fractional-term poles must be < 0 and finite");
+        if (mesh && mesh->dim == 3) return fail(DD_EUNSUPPORTED, "RA-evaluated fractional term: 2D interfaces only");
+    }
     *out = nullptr;
     if (!mesh) return fail(DD_EINVAL, "mesh is NULL");
     if (mesh->dim != 2 && mesh->dim != 3) return fail(DD_EINVAL, "dim must be 2 or 3");
@@ -325,6 +347,14 @@ extern "C" dd_status dd_setup(const dd_mesh* mesh, int n_param, const double* K,
     c->n_param = n_param;
     c->n_poles = n_poles;
     c->max_cols = max_cols;
+    c->frac_t = fr.t;
+    c->frac_sigma = fr.shifted ? 1.0 : 0.0;
+    c->frac_mode = fr.mode;
+    if (fr.mode == DD_FRAC_RA) {
+        c->fra_c0 = fr.fc0;
+        c->fra_poles.assign(fr.fpoles, fr.fpoles + fr.n_fpoles);
+        c->fra_res.assign(fr.fresidues, fr.fresidues + fr.n_fpoles);
+    }
     c->device = device;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
     auto bail = [&](dd_status s) {

@@ -78,6 +78,11 @@ struct dd_ctx {
     int n_param = 0, n_poles = 0, max_cols = 0, cols_pad = 0, device = 0, num_sms = 148;
     cudaStream_t stream = nullptr;
     std::vector<void*> allocs;
+    // fractional perturbation (dd_frac): γ L^t, L = A_Γ + σ M_Γ; mode DENSE or RA (Remark 1)
+    double frac_t = -0.5, frac_sigma = 0.0;
+    int frac_mode = 0;
+    double fra_c0 = 0.0;
+    std::vector<double> fra_poles, fra_res;
     // operator data (2D)
     double* W = nullptr;      // Mpad x 2 Kpad row-major: [S_dst | 0 | F | 0]
     double* sw = nullptr;     // Schur weights s_b

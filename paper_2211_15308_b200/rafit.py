@@ -37,6 +37,9 @@ class RationalApprox:
     n_zolo: int
     rel_err: float = float("nan")      # max |r/f - 1| on a 2e4-point geometric grid
     cancel: float = float("nan")       # κ_c of reading A11
+    t: float = -0.5                    # fractional exponent of f (dd_frac.t)
+    sigma: float = 0.0                 # shift of L (dd_frac.shifted): eigenvalues λ + σ
+    method: str = "zolotarev"
 
     @property
     def m(self) -> int:
@@ -53,7 +56,8 @@ class RationalApprox:
         return {"c0": self.c0, "poles": list(map(float, self.poles)),
                 "residues": list(map(float, self.residues)), "lam_min": self.lam_min,
                 "lam_max": self.lam_max, "K": self.K, "gamma": self.gamma,
-                "n_zolo": self.n_zolo, "rel_err": self.rel_err, "cancel": self.cancel}
+                "n_zolo": self.n_zolo, "rel_err": self.rel_err, "cancel": self.cancel, "t": self.t,
+                "sigma": self.sigma, "method": self.method}
 
 
 def _zolotarev_invsqrt(kappa: float, n: int, dps: int = 50):
@@ -98,12 +102,88 @@ def _zolotarev_invsqrt(kappa: float, n: int, dps: int = 50):
         return d0, q, r
 
 
-def fit_ra(K: float, gamma: float, lam_min: float, lam_max: float, n_poles: int) -> RationalApprox:
-    """RA of f(x) = 1/(K x^{1/2} + γ x^{-1/2}) on [lam_min, lam_max] with `n_poles` poles in
-    total (n_poles - 1 from the Zolotarev fit of x^{-1/2}, plus -γ/K when γ > 0)."""
-    import mpmath as mp
+def f_general(lam, K: float, gamma: float, t: float = -0.5, sigma: float = 0.0):
+    """f(λ) = 1/(K (λ+σ)^{1/2} + γ (λ+σ)^t)  (Eq.(6)/(9): S_Γ = K L^{1/2} + γ L^t, L = A_Γ + σ M_Γ)."""
+    x = np.asarray(lam, dtype=np.float64) + sigma
+    return 1.0 / (K * np.sqrt(x) + gamma * x ** t)
+
+
+def _finish(ra: RationalApprox, fvals) -> RationalApprox:
+    xs = np.geomspace(ra.lam_min, ra.lam_max, 20000)
+    f = fvals(xs)
+    ra.rel_err = float(np.max(np.abs(ra(xs) / f - 1.0)))
+    acc = np.full_like(xs, abs(ra.c0))
+    for p, c in zip(ra.poles, ra.residues):
+        acc += np.abs(c / (xs - p))
+    ra.cancel = float(np.max(acc / f))
+    return ra
+
+
+def _relative_refit(xs, fv, poles):
+    """c0, c_k minimising max-ish relative error: least squares of (c0 + Σ c_k/(x-p_k))/f(x) = 1."""
+    A = np.column_stack([np.ones_like(xs)] + [1.0 / (xs - p) for p in poles]) / fv[:, None]
+    sc = np.linalg.norm(A, axis=0)
+    c, *_ = np.linalg.lstsq(A / sc, np.ones_like(xs), rcond=None)
+    c = c / sc
+    return float(c[0]), np.asarray(c[1:], dtype=np.float64)
+
+
+def fit_function_aaa(fx, x_lo: float, x_hi: float, n_poles: int):
+    """Rational approximation c0 + Σ c_k/(x - q_k) of a positive function fx on [x_lo, x_hi]
+    with real negative poles q_k (host setup data; PAPER.md:196-198 leaves the construction to the
+    references).  AAA (scipy) proposes poles for several degrees <= n_poles; complex or
+    non-negative ones are dropped, the coefficients are refitted for relative accuracy, and the
+    candidate with the smallest relative error on a dense geometric grid wins."""
+    import warnings
+    from scipy.interpolate import AAA
+    xs = np.geomspace(x_lo, x_hi, 3000)
+    fv = fx(xs)
+    xe = np.geomspace(x_lo, x_hi, 20000)
+    fe = fx(xe)
+    best = None
+    for deg in range(max(1, n_poles - 6), n_poles + 1):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            r = AAA(xs, fv, max_terms=deg + 1, rtol=0.0)
+            q = np.asarray(r.poles())
+        q = q[(np.abs(q.imag) <= 1e-8 * np.abs(q)) & (q.real < 0)].real
+        q = np.sort(q)[::-1][:n_poles]
+        c0, c = _relative_refit(xs, fv, q)
+        val = np.full_like(xe, c0)
+        for qk, ck in zip(q, c):
+            val += ck / (xe - qk)
+        err = float(np.max(np.abs(val / fe - 1.0)))
+        if np.isfinite(err) and (best is None or err < best[0]):
+            best = (err, c0, q, c)
+    if best is None:
+        raise ValueError("no valid rational approximation with real negative poles")
+    return best[1], best[2], best[3]
+
+
+def fit_ra(K: float, gamma: float, lam_min: float, lam_max: float, n_poles: int, t: float = -0.5,
+           sigma: float = 0.0) -> RationalApprox:
+    """RA of f(λ) = 1/(K (λ+σ)^{1/2} + γ (λ+σ)^t) on [lam_min, lam_max] (λ: eigenvalues of the
+    pair (A_Γ, M_Γ)) with `n_poles` poles in total, returned in the library convention
+    r(λ) = c0 + Σ c_k/(λ - p_k) (the shift is folded into the poles: p_k = q_k - σ).
+    t = -1/2 (Eq.(2), Eq.(6)): n_poles - 1 from the Zolotarev fit of x^{-1/2}, plus -γ/K.
+    Other t (Eq.(9) sweep, NEXT-3): AAA with real negative poles (fit_function_aaa)."""
     if not (K > 0 and gamma >= 0 and 0 < lam_min < lam_max and np.isfinite(lam_max)):
         raise ValueError("need K > 0, gamma >= 0, 0 < lam_min < lam_max")
+    if not (-1.0 < t < 1.0) or sigma < 0:
+        raise ValueError("need -1 < t < 1 and sigma >= 0")
+    if t != -0.5:
+        fx = lambda x: 1.0 / (K * np.sqrt(x) + gamma * x ** t)
+        c0, q, c = fit_function_aaa(fx, lam_min + sigma, lam_max + sigma, n_poles)
+        order = np.argsort(-q)
+        ra = RationalApprox(c0, q[order] - sigma, c[order], float(lam_min), float(lam_max), float(K), float(gamma),
+                            0, t=float(t), sigma=float(sigma), method="aaa")
+        return _finish(ra, lambda lam: f_general(lam, K, gamma, t, sigma))
+    if sigma != 0.0:
+        base = fit_ra(K, gamma, lam_min + sigma, lam_max + sigma, n_poles)
+        ra = RationalApprox(base.c0, base.poles - sigma, base.residues, float(lam_min), float(lam_max), float(K),
+                            float(gamma), base.n_zolo, t=-0.5, sigma=float(sigma))
+        return _finish(ra, lambda lam: f_general(lam, K, gamma, -0.5, sigma))
+    import mpmath as mp
     nz = n_poles - 1 if gamma > 0 else n_poles
     if nz < 1:
         raise ValueError("n_poles too small")
@@ -126,14 +206,7 @@ def fit_ra(K: float, gamma: float, lam_min: float, lam_max: float, n_poles: int)
         ra = RationalApprox(float(c0), np.array([float(poles[i]) for i in order]),
                             np.array([float(res[i]) for i in order]), float(lam_min),
                             float(lam_max), float(K), float(gamma), nz)
-    xs = np.geomspace(lam_min, lam_max, 20000)
-    f = 1.0 / (K * np.sqrt(xs) + gamma / np.sqrt(xs))
-    ra.rel_err = float(np.max(np.abs(ra(xs) / f - 1.0)))
-    acc = np.full_like(xs, abs(ra.c0))
-    for p, c in zip(ra.poles, ra.residues):
-        acc += np.abs(c / (xs - p))
-    ra.cancel = float(np.max(acc / f))
-    return ra
+    return _finish(ra, lambda lam: f_general(lam, K, gamma))
 
 
 def face_pair(N: int):
