@@ -264,6 +264,9 @@ def main():
         n = cfg.n
         its = np.concatenate(iters_all)
         mean_it = float(its.mean())
+        last = iters_all[-1]
+        by_param = [[K, g, int(last[colp == p].max()), round(float(last[colp == p].mean()), 2)]
+                    for p, (K, g) in enumerate(cfg.params)]
         peak, peak_src = fp64_peak()
         g2_ms, g2_n = prof["gemm_schur"]
         g1_ms, g1_n = prof["gemm_dst"]
@@ -302,7 +305,8 @@ def main():
                        "param_sets": len(cfg.params), "rhs_per_param": cfg.rhs_per_param, "solves_per_step": C,
                        "poles": cfg.n_poles, "rtol": cfg.rtol, "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": f"columns sharded, {world} rank(s), no collective",
-                       "mean_pcg_iters": round(mean_it, 3), "max_pcg_iters": int(its.max())},
+                       "mean_pcg_iters": round(mean_it, 3), "max_pcg_iters": int(its.max()),
+                       "iters_by_param": {"fields": ["K", "mu_inv", "max", "mean"], "rows": by_param}},
             "precond_applies_per_s": round(pa_per_s, 1),
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -46,5 +46,16 @@ CONFIGS = (
     Config("cfg5_2d_N2048_darcy", 2, 2048, _grid([1e-6, 1e-4, 1e-2, 1.0], [1.0, 1e2, 1e4, 1e6]), 20, 32),
 )
 
-BY_NAME = {c.name: c for c in CONFIGS}
+# NEXT-4: the same kernels as the inexact Riesz-map block of the Darcy-Stokes
+# preconditioner — PCG on the config-5 sweep at the paper's inner tolerances (PAPER.md:372-373
+# "relative tolerance of 10^-4"; Appendix, "10^-5"), reported as max / mean
+# inner iteration counts per (K, μ) point (Fig. 7's ○ / × markers).
+INEXACT = (
+    Config("cfg5i_2d_N2048_darcy_rtol1e-5", 2, 2048, _grid([1e-6, 1e-4, 1e-2, 1.0], [1.0, 1e2, 1e4, 1e6]), 20, 32,
+           rtol=1e-5),
+    Config("cfg5i_2d_N2048_darcy_rtol1e-4", 2, 2048, _grid([1e-6, 1e-4, 1e-2, 1.0], [1.0, 1e2, 1e4, 1e6]), 20, 32,
+           rtol=1e-4),
+)
+
+BY_NAME = {c.name: c for c in CONFIGS + INEXACT}
 HEADLINE = CONFIGS[1]

@@ -480,3 +480,27 @@ def test_ra_fit_general_t(t, sigma):
         _, it_ra, *_ = pcg.pcg(lambda v: Mo.apply_S(K, g, v),
                                lambda v: Mo.apply_P_ra(fit.c0, fit.poles, fit.residues, v), b)
         assert abs(it_ra - it_ex) <= 1, (K, g, it_ex, it_ra)
+
+
+# --------------------------------------------------------------------------- inexact inner PCG (NEXT-4)
+def test_inexact_inner_pcg_iteration_bound():
+    # the Darcy pressure Riesz map is approximated by PCG at relative
+    # tolerance 1e-4 / 1e-5.  With the preconditioned spectrum in [1, √6] (closed form above),
+    # η_k/η_0 <= 2 ρ^k √κ with ρ = (κ^½-1)/(κ^½+1) bounds the count for EVERY (K, μ, h):
+    # 7 at 1e-4, 9 at 1e-5 (16 at 1e-10).  Checked on the config-5 (K, μ) grid, several meshes.
+    kap = np.sqrt(6.0)
+    rho = (np.sqrt(kap) - 1) / (np.sqrt(kap) + 1)
+    bound = {tol: int(np.ceil(np.log(tol / (2 * np.sqrt(kap))) / np.log(rho))) for tol in (1e-4, 1e-5, 1e-10)}
+    assert bound == {1e-4: 7, 1e-5: 9, 1e-10: 16}
+    for N in (64, 512, 2048):
+        Mo = problem.ModeProblem2D(N)
+        B = np.random.default_rng(N).uniform(-1, 1, (N - 1, 4))
+        for K in (1e-6, 1e-4, 1e-2, 1.0):
+            for mu_inv in (1.0, 1e2, 1e4, 1e6):
+                prev = -1
+                for tol in (1e-4, 1e-5, 1e-10):
+                    X, its, rel, _ = pcg.pcg_batch(lambda V, c: Mo.apply_S(K, mu_inv, V),
+                                                   lambda V, c: Mo.apply_P_exact(K, mu_inv, V), B, rtol=tol)
+                    assert its.max() <= bound[tol] and np.all(rel <= tol)
+                    assert its.min() >= prev      # tighter tolerance never needs fewer iterations
+                    prev = its.max()
