@@ -114,7 +114,7 @@ class BulkProblem:
     def __init__(self, dim: int, N: int):
         self.dim, self.N = dim, N
         coords, cells = (square_mesh(N) if dim == 2 else cube_mesh(N))
-        K, _ = _assemble(coords.shape[0], cells, coords)
+        K, Mfull = _assemble(coords.shape[0], cells, coords)
         idx = np.rint(coords * N).astype(np.int64)          # integer lattice coordinates
         i = idx[:, 0]
         others = idx[:, 1:]
@@ -130,6 +130,7 @@ class BulkProblem:
         g_ids, i_ids = order(gamma), order(inner)
         perm = np.concatenate([g_ids, i_ids])
         self.A = K[perm][:, perm].tocsr()
+        self.M = Mfull[perm][:, perm].tocsr()     # consistent P1 mass on the free nodes (same order)
         self.n_gamma, self.n_int = len(g_ids), len(i_ids)
         self.layer_of = idx[perm, 0]
         self.coords = coords[perm]

@@ -656,6 +656,91 @@ extern "C" dd_status dd_pcg_solve_host(dd_ctx* c, int ncols, const int* colp_h, 
     return r;
 }
 
+// ------------------------------------------------------------------------------------ bulk solve
+// Full DD solve on a bulk right-hand side (2D; bulk2d.cu has the algebra).
+extern "C" dd_status dd_bulk_solve(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol,
+                                   int maxit, int norm_kind, int* iters, double* rel_res) {
+    dd_status s = check_cols(c, ncols, colp);
+    if (s != DD_OK) return s;
+    if (c->dim != 2) return fail(DD_EUNSUPPORTED, "bulk solve: 2D handles only");
+    if (ncols > 0 && (!b || !x)) return fail(DD_EINVAL, "b/x NULL");
+    if (!(rtol >= 0.0) || maxit < 0 || (norm_kind != 0 && norm_kind != 1)) return fail(DD_EINVAL, "rtol/maxit/norm_kind");
+    if (ncols == 0) return DD_OK;
+    CK(cudaSetDevice(c->device));
+    const int n = c->n, ldf = c->Kpad;
+    const long long NP = (long long)ldf * ldf;
+    if (!c->bulk_a) {
+        // workspaces (first use): two slab buffers, 1/(σ_a + σ_b), skinny vectors
+        // + 64 padded rows: the slab GEMM reads A rows up to round_up(n, 64) of the last slab
+        const size_t slab_tot = (size_t)NP * c->max_cols + (size_t)64 * ldf;
+        CK(dalloc(c, &c->bulk_a, slab_tot));
+        CK(dalloc(c, &c->bulk_b, slab_tot));
+        CK(dalloc(c, &c->bulk_sinv, (size_t)NP));
+        CK(dalloc(c, &c->bulk_g, (size_t)ldf * c->cols_pad));
+        CK(dalloc(c, &c->bulk_w, (size_t)ldf * c->cols_pad));
+        CK(dalloc(c, &c->bulk_gv, (size_t)n * c->max_cols));
+        CK(dalloc(c, &c->bulk_xg, (size_t)n * c->max_cols));
+        CK(cudaMemsetAsync(c->bulk_a, 0, sizeof(double) * slab_tot, c->stream));
+        CK(cudaMemsetAsync(c->bulk_b, 0, sizeof(double) * slab_tot, c->stream));
+        CK(cudaMemsetAsync(c->bulk_g, 0, sizeof(double) * (size_t)ldf * c->cols_pad, c->stream));
+        CK(cudaMemsetAsync(c->bulk_w, 0, sizeof(double) * (size_t)ldf * c->cols_pad, c->stream));
+        const long double PI = 3.141592653589793238462643383279502884L;
+        std::vector<long double> sig(n);
+        for (int a = 0; a < n; a++) {
+            const long double sh = sinl(PI * (a + 1) / (2.0L * c->N));
+            sig[a] = 4.0L * sh * sh;                      // 5-point mode value 2 - 2cos θ
+        }
+        std::vector<double> h((size_t)NP, 0.0);
+        for (int a = 0; a < n; a++)
+            for (int bb = 0; bb < n; bb++) h[(size_t)a * ldf + bb] = (double)(1.0L / (sig[a] + sig[bb]));
+        CK(cudaMemcpyAsync(c->bulk_sinv, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    const long long nb = (long long)n * n + n;
+    const double* S = c->W;               // S_dst: rows of W, row stride lda
+    const double* s1 = c->W;              // S[1, :]
+    TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
+    // Ŷ = (S B0 S) / Σ,  bΓ -> bulk_g
+    TIMED(DD_KCLASS_OTHER, bulk_in(n, ldf, ncols, b, nb, c->bulk_a, c->bulk_g, ldf, c->stream));
+    TIMED(DD_KCLASS_GEMM_DST, bulk_slab_pass(c->bulk_a, c->bulk_b, ncols, n, ldf, S, c->lda, nullptr, c->stream));
+    TIMED(DD_KCLASS_GEMM_DST, bulk_slab_pass(c->bulk_b, c->bulk_a, ncols, n, ldf, S, c->lda, c->bulk_sinv, c->stream));
+    // g = bΓ + [L00^-1 b0]_{i=1} = bΓ + S w,  w_b = Σ_a s1_a Ŷ_ab
+    TIMED(DD_KCLASS_OTHER, bulk_row1(n, ldf, ncols, c->bulk_a, s1, c->bulk_w, ldf, c->stream));
+    {
+        GemmArgs ga{};
+        ga.M = n; ga.N = ncols; ga.K = ldf;
+        ga.A = S; ga.lda = c->lda;
+        ga.B = c->bulk_w; ga.ldb = ldf;
+        ga.C = c->bulk_gv; ga.ldc = n;
+        ga.X = c->bulk_g; ga.ldx = ldf;
+        ga.splitk = gemm_pick_splitk(n, ncols, ldf, c->num_sms); ga.ws = c->gws; ga.counters = c->gcnt;
+        ga.num_sms = c->num_sms; ga.epi = EPI_ADD;
+        TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(ga, c->stream));
+    }
+    // xΓ = S^-1 g   (the Schur PCG)
+    dd_status ps = dd_pcg_solve(c, ncols, colp, c->bulk_gv, c->bulk_xg, rtol, maxit, norm_kind, iters, rel_res, nullptr);
+    if (ps != DD_OK && ps != DD_ENOCONV) return ps;
+    // u = S xΓ;  x̂0 = Ŷ / K + (s1 ⊗ u) / Σ;  x0 = S x̂0 S
+    TIMED(DD_KCLASS_OTHER, launch_copy_cols(n, ncols, c->bulk_xg, n, c->bulk_g, ldf, c->stream));
+    {
+        GemmArgs ga{};
+        ga.M = n; ga.N = ncols; ga.K = ldf;
+        ga.A = S; ga.lda = c->lda;
+        ga.B = c->bulk_g; ga.ldb = ldf;
+        ga.C = c->bulk_w; ga.ldc = ldf;
+        ga.splitk = gemm_pick_splitk(n, ncols, ldf, c->num_sms); ga.ws = c->gws; ga.counters = c->gcnt;
+        ga.num_sms = c->num_sms; ga.epi = EPI_STORE;
+        TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(ga, c->stream));
+    }
+    TIMED(DD_KCLASS_OTHER, bulk_update(n, ldf, ncols, c->bulk_a, s1, c->bulk_w, ldf, c->bulk_sinv, colp, c->n_param,
+                                       c->Kp, c->stream));
+    TIMED(DD_KCLASS_GEMM_DST, bulk_slab_pass(c->bulk_a, c->bulk_b, ncols, n, ldf, S, c->lda, nullptr, c->stream));
+    TIMED(DD_KCLASS_GEMM_DST, bulk_slab_pass(c->bulk_b, c->bulk_a, ncols, n, ldf, S, c->lda, nullptr, c->stream));
+    TIMED(DD_KCLASS_OTHER, bulk_out(n, ldf, ncols, c->bulk_a, c->bulk_xg, n, x, nb, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return ps;
+}
+
 extern "C" dd_status dd_destroy(dd_ctx* c) {
     if (!c) return DD_OK;
     cudaSetDevice(c->device);

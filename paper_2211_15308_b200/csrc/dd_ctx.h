@@ -83,6 +83,9 @@ struct dd_ctx {
     int frac_mode = 0;
     double fra_c0 = 0.0;
     std::vector<double> fra_poles, fra_res;
+    // full DD bulk solve (2D, dd_bulk_solve; allocated on first use)
+    double *bulk_a = nullptr, *bulk_b = nullptr, *bulk_sinv = nullptr, *bulk_g = nullptr, *bulk_w = nullptr;
+    double *bulk_gv = nullptr, *bulk_xg = nullptr;
     // operator data (2D)
     double* W = nullptr;      // Mpad x 2 Kpad row-major: [S_dst | 0 | F | 0]
     double* sw = nullptr;     // Schur weights s_b

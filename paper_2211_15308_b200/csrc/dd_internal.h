@@ -18,6 +18,7 @@ constexpr size_t GEMM_SMEM = size_t(GEMM_STAGES) * (GEMM_BM + GEMM_BN) * GEMM_LD
 enum EpiKind : int {
     EPI_STORE = 0,      // C[i,c] = acc
     EPI_SCHUR_DST = 1,  // C[i,c] = K_c s_i acc   and   Zlow[i,c] = γ_c X[i,c]   (Schur step a-2/a-3)
+    EPI_ADD = 2,        // C[i,c] = acc + X[i,c]  (X with ldx)
 };
 
 struct GemmArgs {
@@ -112,6 +113,18 @@ cudaError_t launch_pcg_small(const PcgState& s, const PoleGeom& g, const PoleTab
 cudaError_t launch_copy_cols(int n, int ncols, const double* src, int lds, double* dst, int ldd,
                              cudaStream_t st);
 cudaError_t launch_check_params(int ncols, const int* col_param, int n_param, int* flag, cudaStream_t st);
+
+// ----------------------------------------------------------------------------- 2D bulk solve (bulk2d.cu)
+cudaError_t bulk_slab_pass(const double* in, double* out, int nslab, int n, int ldf, const double* S, int lds,
+                           const double* w, cudaStream_t st);
+cudaError_t bulk_in(int n, int ldf, int ncols, const double* b, long long ldb, double* slab, double* gout, int ldg,
+                    cudaStream_t st);
+cudaError_t bulk_row1(int n, int ldf, int ncols, const double* Yh, const double* s1, double* w, int ldw,
+                      cudaStream_t st);
+cudaError_t bulk_update(int n, int ldf, int ncols, double* Yh, const double* s1, const double* u, int ldu,
+                        const double* sinv, const int* col_param, int n_param, const double* Kp, cudaStream_t st);
+cudaError_t bulk_out(int n, int ldf, int ncols, const double* slab, const double* xg, int ldg, double* x, long long ldx,
+                     cudaStream_t st);
 
 // ----------------------------------------------------------------------------- 3D face (face3d.cu)
 struct InnerArgs {

@@ -23,6 +23,13 @@ struct EpiStore {
     __device__ __forceinline__ void operator()(int, int row, int col, double v) const { C[row + (size_t)col * ldc] = v; }
 };
 
+struct EpiAdd {                         // C = v + D   (D column-major, ldd)
+    double* C; int ldc; const double* D; int ldd;
+    __device__ __forceinline__ void operator()(int, int row, int col, double v) const {
+        C[row + (size_t)col * ldc] = v + D[row + (size_t)col * ldd];
+    }
+};
+
 struct EpiSchurDst {
     double* C; int ldc;                 // Z top half (T')
     double* Zlow;                       // Z bottom half (γ X), same ldc
@@ -70,6 +77,7 @@ static cudaError_t launch(const GemmArgs& a, const Epi& e, cudaStream_t st) {
 cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
     if (a.M <= 0 || a.N <= 0) return cudaSuccess;
     if (a.epi == EPI_STORE) return launch(a, EpiStore{a.C, a.ldc}, st);
+    if (a.epi == EPI_ADD) return launch(a, EpiAdd{a.C, a.ldc, a.X, a.ldx}, st);
     return launch(a, EpiSchurDst{a.C, a.ldc, a.Zlow, a.X, a.ldx, a.col_param, a.n_param, a.Kp, a.gp, a.s}, st);
 }
 

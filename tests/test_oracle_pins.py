@@ -504,3 +504,47 @@ def test_inexact_inner_pcg_iteration_bound():
                     assert its.max() <= bound[tol] and np.all(rel <= tol)
                     assert its.min() >= prev      # tighter tolerance never needs fewer iterations
                     prev = its.max()
+
+
+# --------------------------------------------------------------------------- bulk problem (NEXT-1)
+from oracle import bulk as obulk  # noqa: E402
+
+
+@pytest.mark.parametrize("t,sigma", [(-0.5, 0.0), (0.25, 1.0)])
+def test_bulk_block_elimination_identity(t, sigma):
+    # PAPER.md:104-122 Eq.(4) / 123-145 Eq.(5) with exact blocks: the Γ part of the direct bulk
+    # solution equals S^-1 (b_Γ - A^{i0} (A^00)^-1 b_0) with S from the Schur tier, and the
+    # interior part solves A^00 x_0 = b_0 - A^{0i} x_Γ.
+    N = 10
+    Bs = obulk.BulkSystem(2, N, t=t, sigma=sigma)
+    D = problem.DenseProblem(2, N, t=t, sigma=sigma)
+    rng = np.random.default_rng(21)
+    b = rng.uniform(-1, 1, Bs.A.shape[0])
+    g = Bs.g
+    for K, gam in [(1.0, 1e2), (1e-3, 1.0)]:
+        x = Bs.solve(K, gam, b)
+        A = K * Bs.A.toarray()
+        Aii, Ai0, A00 = A[:g, :g], A[:g, g:], A[g:, g:]
+        rhs = b[:g] - Ai0 @ np.linalg.solve(A00, b[g:])
+        xg = np.linalg.solve(D.S(K, gam), rhs)
+        assert np.abs(x[:g] - xg).max() <= 1e-10 * np.abs(xg).max()
+        x0 = np.linalg.solve(A00, b[g:] - Ai0.T @ x[:g])
+        assert np.abs(x[g:] - x0).max() <= 1e-10 * np.abs(x0).max()
+        assert np.linalg.norm(Bs.apply(K, gam, x) - b) <= 1e-10 * np.linalg.norm(b)
+
+
+def test_bulk_manufactured_solution_rate():
+    # -K Δu = f on (0,1)^2, u = 0 on ∂Ω\Γ, natural condition on Γ = {x=0} (γ = 0): with
+    # u = cos(πx/2) sin(πy), f = K (π²/4 + π²) u, the P1 nodal error decays as h² (rate 2).
+    K = 2.0
+    errs = []
+    for N in (8, 16, 32):
+        Bs = obulk.BulkSystem(2, N)
+        P = fem.BulkProblem(2, N)
+        xy = P.coords
+        u = np.cos(np.pi * xy[:, 0] / 2) * np.sin(np.pi * xy[:, 1])
+        b = P.M @ (K * (np.pi ** 2 / 4 + np.pi ** 2) * u)
+        x = Bs.solve(K, 0.0, b)
+        errs.append(np.abs(x - u).max())
+    rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert np.all(rates > 1.8) and errs[-1] < 2e-3, (errs, rates)
