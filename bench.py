@@ -162,6 +162,10 @@ def main():
     ap.add_argument("--config", default=configs.HEADLINE.name)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--frac-mode", default="dense", choices=["dense", "ra"],
+                    help="fractional term: dense F (Eq.(7)) or RA-evaluated (Remark 1, NEXT-2)")
+    ap.add_argument("--mode", default="schur", choices=["schur", "bulk"],
+                    help="schur: interface PCG (headline); bulk: full DD solve on bulk RHS (NEXT-1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = configs.BY_NAME[args.config]
@@ -171,6 +175,8 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args, cfg, world, rank)
+    if args.mode == "bulk":
+        return run_bulk(args, cfg, world, rank)
 
     import torch
     import torch.distributed as dist
@@ -182,7 +188,11 @@ def main():
     ras = fit_ras(cfg)
     B, colp = inputs.batch(cfg.n_gamma, len(cfg.params), cfg.rhs_per_param, seed_offset=rank * len(cfg.params))
     C = B.shape[0]
-    S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local)
+    frac = None
+    if args.frac_mode == "ra":
+        lo, hi = rafit.interval_1d(cfg.N) if cfg.dim == 2 else rafit.interval_face(cfg.N)
+        frac = binding.Frac(mode="ra", fra=rafit.fit_power(-0.5, lo, hi, cfg.n_poles))
+    S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local, frac=frac)
     Bt = torch.as_tensor(B, device=f"cuda:{local}")
     cp = torch.as_tensor(colp.astype(np.int32), device=f"cuda:{local}")
     X = torch.empty_like(Bt)
@@ -273,11 +283,13 @@ def main():
         ps_ms, ps_n = prof["polesum_pcg"]
         total_prof_ms = sum(v[0] for v in prof.values())
         if cfg.dim == 2:
-            flops_g2 = 2.0 * n * (2 * n) * C          # [S_dst | F] (n x 2n) times (2n x C), algorithmic
+            # [S_dst | F] (n x 2n) times (2n x C), algorithmic; RA mode (Remark 1): S_dst T' only
+            flops_g2 = 2.0 * n * (2 * n) * C if args.frac_mode == "dense" else 2.0 * n * n * C
             flops_g1 = 2.0 * n * n * C
             ach_g2 = flops_g2 / (g2_ms / g2_n / 1e3) / 1e12 if g2_n else None
             step_flops = (flops_g1 + flops_g2) * mean_it
-            roof = {"bound": "tensor", "kernel": "gemm_schur ([S_dst|F] x [T; gamma X], DMMA fp64)",
+            roof = {"bound": "tensor", "kernel": "gemm_schur ([S_dst|F] x [T; gamma X], DMMA fp64)" if args.frac_mode == "dense"
+                    else "gemm_schur (S_dst x T' + U, DMMA fp64; U = gamma M r_F M x by pole sum)",
                     "achieved": round(ach_g2, 3) if ach_g2 else None, "peak": peak, "unit": "TFLOP/s",
                     "frac": round(ach_g2 / peak, 4) if ach_g2 else None, "peak_source": peak_src,
                     "flops_per_launch": flops_g2,
@@ -305,6 +317,8 @@ def main():
                        "param_sets": len(cfg.params), "rhs_per_param": cfg.rhs_per_param, "solves_per_step": C,
                        "poles": cfg.n_poles, "rtol": cfg.rtol, "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": f"columns sharded, {world} rank(s), no collective",
+                       "fractional_term": "dense F (Eq.(7))" if args.frac_mode == "dense"
+                       else f"RA-evaluated (Remark 1), {cfg.n_poles} poles",
                        "mean_pcg_iters": round(mean_it, 3), "max_pcg_iters": int(its.max()),
                        "iters_by_param": {"fields": ["K", "mu_inv", "max", "mean"], "rows": by_param}},
             "precond_applies_per_s": round(pa_per_s, 1),
@@ -330,6 +344,61 @@ def main():
     S.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_bulk(args, cfg, world, rank):
+    """NEXT-1: full DD solve on bulk right-hand sides (dd_bulk_solve): metric bulk solves/s;
+    the slab transforms (4 batched n x n x n DMMA GEMMs per RHS) bound it."""
+    import torch
+    from paper_2211_15308_b200 import binding
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    ras = fit_ras(cfg)
+    n = cfg.n
+    C = cfg.n_cols
+    rng = np.random.default_rng(1000 + rank)
+    Bb = rng.uniform(-1.0, 1.0, (C, n * n + n))
+    colp = (np.arange(C) // cfg.rhs_per_param).astype(np.int32)
+    S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local)
+    Bt = torch.as_tensor(Bb, device=f"cuda:{local}")
+    X = torch.empty_like(Bt)
+    cp = torch.as_tensor(colp, device=f"cuda:{local}")
+    for _ in range(args.warmup):
+        S.bulk_solve(Bt, cp, x=X, rtol=cfg.rtol, maxit=cfg.maxit)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(S.stream)
+        for _ in range(args.steps):
+            r = S.bulk_solve(Bt, cp, x=X, rtol=cfg.rtol, maxit=cfg.maxit)
+        e1.record(S.stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    S.profile(True)
+    S.bulk_solve(Bt, cp, x=X, rtol=cfg.rtol, maxit=0)      # maxit 0: gemm_dst holds the 4 slab passes only
+    prof = S.profile_read()
+    S.profile(False)
+    ldf = (n + 15) // 16 * 16
+    pass_ms, pass_n = prof["gemm_dst"]
+    fl_pass = 2.0 * n * n * ldf * C
+    peak, peak_src = fp64_peak()
+    ach = fl_pass / (pass_ms / pass_n / 1e3) / 1e12 if pass_n else None
+    if rank == 0:
+        print(json.dumps({
+            "metric": "DD bulk solves/s", "value": round(C / (ms / 1e3), 3), "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name + "_bulk", "bulk_unknowns_per_solve": n * n + n, "solves_per_step": C,
+                       "mean_pcg_iters": float(np.mean(r.iters)), "l2": "inputs (4.3 GB of fields) exceed L2"},
+            "clocks": clk.summary(),
+            "roofline": {"bound": "tensor", "kernel": "bulk slab pass (S Y per field, batched DMMA)",
+                         "achieved": round(ach, 3) if ach else None, "peak": peak, "unit": "TFLOP/s",
+                         "frac": round(ach / peak, 4) if ach else None, "peak_source": peak_src,
+                         "flops_per_launch": fl_pass, "avg_launch_us": round(pass_ms / pass_n * 1e3, 1) if pass_n else None,
+                         "traffic": None,
+                         "share_of_step": {k: round(v[0] / sum(x[0] for x in prof.values()), 4) for k, v in prof.items()}},
+        }), flush=True)
+    S.close()
 
 
 def run_reference(args, cfg, world, rank):

@@ -24,12 +24,19 @@ class DenseProblem:
     """t, sigma: the perturbation γ L^t with L = -Δ_Γ + σ I_Γ (Eq.(2): t = -1/2, σ = 0;
     Eq.(9), PAPER.md:208-216: general -1 < t < 1 and σ = 1)."""
 
-    def __init__(self, dim: int, N: int, method: str = "layers", t: float = -0.5, sigma: float = 0.0):
+    def __init__(self, dim: int, N: int, method: str = "layers", t: float = -0.5, sigma: float = 0.0,
+                 frac_ra=None):
+        """frac_ra = (c0, poles, residues): the fractional term evaluated by RA (Remark 1,
+        PAPER.md:274-288): F = M (c0 M^-1 + Σ c_k (A - p_k M)^-1) M instead of Eq.(7)."""
         self.dim, self.N, self.t, self.sigma = dim, N, t, sigma
         self.S_unit = schur.schur_layers(dim, N) if method == "layers" else schur.schur_bruteforce(dim, N)
         self.A_g, self.M_g = fem.trace_pair(dim, N)
         self.gevp = spectral.GEVP(self.A_g, self.M_g)
-        self.F = self.gevp.power(t, sigma)
+        if frac_ra is None:
+            self.F = self.gevp.power(t, sigma)
+        else:
+            c0, poles, res = frac_ra
+            self.F = self.M_g @ ra.apply_ra(self.A_g, self.M_g, c0, poles, res, self.M_g)
         self.n_gamma = self.S_unit.shape[0]
 
     def S(self, K, gamma):
@@ -52,7 +59,7 @@ class DenseProblem:
 
 
 class ModeProblem2D:
-    def __init__(self, N: int, t: float = -0.5, sigma: float = 0.0):
+    def __init__(self, N: int, t: float = -0.5, sigma: float = 0.0, frac_ra=None):
         self.dim, self.N, self.t, self.sigma = 2, N, t, sigma
         n = N - 1
         self.n_gamma = n
@@ -67,6 +74,8 @@ class ModeProblem2D:
         self.lam = self.alpha / self.mu             # generalised eigenvalues of (A_Γ, M_Γ)
         self.s = schur.schur_modes_2d(N)            # S_unit mode values
         self.f = self.mu * (self.lam + sigma) ** t  # F mode values: (MU) (Λ+σ)^t (MU)^T
+        if frac_ra is not None:                     # Remark 1: (MU) r_F(Λ) (MU)^T
+            self.f = self.mu * ra.r_eval(self.lam, *frac_ra)
         self.band = (a_d, a_o, m_d, m_o)
 
     def apply_S(self, K, gamma, X):

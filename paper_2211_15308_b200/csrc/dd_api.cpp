@@ -122,6 +122,68 @@ static SysTables build_sys_tables(long double d, long double e, const PoleGeom& 
     return t;
 }
 
+// Pole-sum tables of n_sets parameter sets (RA c0 M^-1 + Σ_k c_k (A_Γ - p_k M_Γ)^-1 each):
+// systems [M term if c0 != 0] + [poles with non-zero residue], in long double (build_sys_tables).
+static dd_status build_pole_tabs(dd_ctx* c, const PoleGeom& g, int n_sets, int n_poles, const double* c0,
+                                 const double* poles, const double* residues, PoleTabs& T) {
+    const long double h = 1.0L / c->N;
+    const int L = g.LL;
+    const size_t JT = (size_t)g.J * g.T;
+    const int max_sys = n_poles + 1;
+    std::vector<int> nsys(n_sets, 0);
+    std::vector<double> w((size_t)n_sets * max_sys, 0.0), dd((size_t)n_sets * max_sys, 1.0),
+        ee((size_t)n_sets * max_sys, 0.0), invb((size_t)n_sets * max_sys * L, 0.0),
+        cpr(invb.size(), 0.0), uf(invb.size(), 0.0), up(invb.size(), 0.0),
+        pa((size_t)n_sets * max_sys * JT, 0.0), pb(pa.size(), 0.0),
+        pinvb((size_t)n_sets * max_sys * g.T, 0.0);
+    for (int pi = 0; pi < n_sets; pi++) {
+        std::vector<std::tuple<double, long double, long double>> sys;   // (weight, d, e)
+        if (c0[pi] != 0.0) sys.emplace_back(c0[pi], 4.0L * h / 6.0L, h / 6.0L);
+        for (int k = 0; k < n_poles; k++) {
+            const double pk = poles[(size_t)pi * n_poles + k], ck = residues[(size_t)pi * n_poles + k];
+            if (ck == 0.0) continue;
+            const long double P = pk;
+            sys.emplace_back(ck, 2.0L / h - P * 4.0L * h / 6.0L, -1.0L / h - P * h / 6.0L);
+        }
+        nsys[pi] = (int)sys.size();
+        for (size_t s = 0; s < sys.size(); s++) {
+            const size_t ps = (size_t)pi * max_sys + s;
+            w[ps] = std::get<0>(sys[s]);
+            dd[ps] = (double)std::get<1>(sys[s]);
+            ee[ps] = (double)std::get<2>(sys[s]);
+            SysTables t = build_sys_tables(std::get<1>(sys[s]), std::get<2>(sys[s]), g);
+            std::memcpy(&invb[ps * L], t.invb.data(), L * sizeof(double));
+            std::memcpy(&cpr[ps * L], t.cpr.data(), L * sizeof(double));
+            std::memcpy(&uf[ps * L], t.uf.data(), L * sizeof(double));
+            std::memcpy(&up[ps * L], t.up.data(), L * sizeof(double));
+            std::memcpy(&pa[ps * JT], t.pa.data(), JT * sizeof(double));
+            std::memcpy(&pb[ps * JT], t.pb.data(), JT * sizeof(double));
+            std::memcpy(&pinvb[ps * g.T], t.pinvb.data(), g.T * sizeof(double));
+        }
+    }
+    auto up_d = [&](const std::vector<double>& v, const double** dst) -> dd_status {
+        double* d = nullptr;
+        CK(dalloc(c, &d, v.size()));
+        CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        *dst = d;
+        return DD_OK;
+    };
+    int* nsys_d = nullptr;
+    CK(dalloc(c, &nsys_d, nsys.size()));
+    CK(cudaMemcpyAsync(nsys_d, nsys.data(), nsys.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    T.max_sys = max_sys;
+    T.n_param = n_sets;
+    T.nsys = nsys_d;
+    dd_status st;
+    if ((st = up_d(w, &T.w)) || (st = up_d(dd, &T.d)) || (st = up_d(ee, &T.e)) || (st = up_d(invb, &T.invb)) ||
+        (st = up_d(cpr, &T.cpr)) || (st = up_d(uf, &T.ufull)) || (st = up_d(up, &T.upart)) || (st = up_d(pa, &T.pa)) ||
+        (st = up_d(pb, &T.pb)) || (st = up_d(pinvb, &T.pinvb)))
+        return st;
+    // the host vectors must outlive the async copies
+    CK(cudaStreamSynchronize(c->stream));
+    return DD_OK;
+}
+
 // ------------------------------------------------------------------------------------ setup
 static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, const double* poles,
                           const double* residues, const double* c0) {
@@ -130,7 +192,8 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
     const long double PI = 3.141592653589793238462643383279502884L;
     c->Kpad = round_up(n, GEMM_BK);
     c->ldv = c->Kpad;
-    c->lda = 2 * c->Kpad;
+    const bool dense_f = c->frac_mode == DD_FRAC_DENSE;
+    c->lda = dense_f ? 2 * c->Kpad : c->Kpad;    // RA mode (Remark 1): no dense F block
     c->Mpad = round_up(n, GEMM_BM);
     c->cols_pad = round_up(c->max_cols, GEMM_BN);
 
@@ -162,8 +225,8 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
     // F = S diag(μ_b (λ_b + σ)^t) S  (Eq.(7) in closed form for the 1D pair; Eq.(2): t = -1/2,
     // σ = 0; Eq.(9)'s shifted L = A_Γ + M_Γ has eigenvalues λ_b + 1 with the same vectors):
     // μ_b = (h/6)(6 - σ_b),  λ_b = 6 σ_b / (h^2 (6 - σ_b))
-    std::vector<double> Bh((size_t)c->Kpad * round_up(n, GEMM_BN), 0.0);
-    for (int k = 0; k < n; k++) {
+    std::vector<double> Bh(dense_f ? (size_t)c->Kpad * round_up(n, GEMM_BN) : 0, 0.0);
+    for (int k = 0; k < n && dense_f; k++) {
         const long double mu = h / 6.0L * (6.0L - sig[k]);
         const long double lam = 6.0L * sig[k] / (h * h * (6.0L - sig[k]));
         const long double f = mu * powl(lam + (long double)c->frac_sigma, (long double)c->frac_t);
@@ -172,9 +235,11 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
     CK(dalloc(c, &c->W, (size_t)c->Mpad * c->lda));
     CK(cudaMemcpyAsync(c->W, Wh.data(), Wh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     double* Bd = nullptr;
-    CK(cudaMalloc(&Bd, Bh.size() * sizeof(double)));
-    CK(cudaMemcpyAsync(Bd, Bh.data(), Bh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    {
+    if (dense_f) {
+        CK(cudaMalloc(&Bd, Bh.size() * sizeof(double)));
+        CK(cudaMemcpyAsync(Bd, Bh.data(), Bh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    }
+    if (dense_f) {
         // one-off setup GEMM F = S_dst · (diag(f) S_dst), written into W's right half
         const int sk = gemm_pick_splitk(n, n, c->Kpad, c->num_sms);
         double* ws = nullptr; int* cnt = nullptr;
@@ -193,67 +258,24 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
         if (ws) cudaFree(ws);
         cudaFree(cnt);
     }
-    cudaFree(Bd);
+    if (Bd) cudaFree(Bd);
+    CK(cudaStreamSynchronize(c->stream));
     CK(dalloc(c, &c->sw, n));
     CK(cudaMemcpyAsync(c->sw, swh.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
 
-    // --- pole tables: systems [M term if c0 != 0] + [poles with non-zero residue]
+    // --- pole tables of the preconditioner; in RA mode also those of the fractional term
     PoleGeom& g = c->geom;
     g = make_pole_geom(n);
     if (!pole_geom_supported(g)) return fail(DD_EUNSUPPORTED, "interface too large for the 1D pole-sum kernels");
-    const int L = g.LL;
-    const size_t JT = (size_t)g.J * g.T;
-    const int max_sys = c->n_poles + 1;
-    std::vector<int> nsys(c->n_param, 0);
-    std::vector<double> w((size_t)c->n_param * max_sys, 0.0), dd((size_t)c->n_param * max_sys, 1.0),
-        ee((size_t)c->n_param * max_sys, 0.0), invb((size_t)c->n_param * max_sys * L, 0.0),
-        cpr(invb.size(), 0.0), uf(invb.size(), 0.0), up(invb.size(), 0.0),
-        pa((size_t)c->n_param * max_sys * JT, 0.0), pb(pa.size(), 0.0),
-        pinvb((size_t)c->n_param * max_sys * g.T, 0.0);
-    for (int pi = 0; pi < c->n_param; pi++) {
-        std::vector<std::tuple<double, long double, long double>> sys;   // (weight, d, e)
-        if (c0[pi] != 0.0) sys.emplace_back(c0[pi], 4.0L * h / 6.0L, h / 6.0L);
-        for (int k = 0; k < c->n_poles; k++) {
-            const double pk = poles[(size_t)pi * c->n_poles + k], ck = residues[(size_t)pi * c->n_poles + k];
-            if (ck == 0.0) continue;
-            const long double P = pk;
-            sys.emplace_back(ck, 2.0L / h - P * 4.0L * h / 6.0L, -1.0L / h - P * h / 6.0L);
-        }
-        nsys[pi] = (int)sys.size();
-        for (size_t s = 0; s < sys.size(); s++) {
-            const size_t ps = (size_t)pi * max_sys + s;
-            w[ps] = std::get<0>(sys[s]);
-            dd[ps] = (double)std::get<1>(sys[s]);
-            ee[ps] = (double)std::get<2>(sys[s]);
-            SysTables t = build_sys_tables(std::get<1>(sys[s]), std::get<2>(sys[s]), g);
-            std::memcpy(&invb[ps * L], t.invb.data(), L * sizeof(double));
-            std::memcpy(&cpr[ps * L], t.cpr.data(), L * sizeof(double));
-            std::memcpy(&uf[ps * L], t.uf.data(), L * sizeof(double));
-            std::memcpy(&up[ps * L], t.up.data(), L * sizeof(double));
-            std::memcpy(&pa[ps * JT], t.pa.data(), JT * sizeof(double));
-            std::memcpy(&pb[ps * JT], t.pb.data(), JT * sizeof(double));
-            std::memcpy(&pinvb[ps * g.T], t.pinvb.data(), g.T * sizeof(double));
+    {
+        dd_status st = build_pole_tabs(c, g, c->n_param, c->n_poles, c0, poles, residues, c->tabs);
+        if (st != DD_OK) return st;
+        if (c->frac_mode == DD_FRAC_RA) {
+            st = build_pole_tabs(c, g, 1, (int)c->fra_poles.size(), &c->fra_c0, c->fra_poles.data(), c->fra_res.data(),
+                                 c->ftabs);
+            if (st != DD_OK) return st;
         }
     }
-    auto up_d = [&](const std::vector<double>& v, const double** dst) -> dd_status {
-        double* d = nullptr;
-        CK(dalloc(c, &d, v.size()));
-        CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        *dst = d;
-        return DD_OK;
-    };
-    int* nsys_d = nullptr;
-    CK(dalloc(c, &nsys_d, nsys.size()));
-    CK(cudaMemcpyAsync(nsys_d, nsys.data(), nsys.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    PoleTabs& T = c->tabs;
-    T.max_sys = max_sys;
-    T.n_param = c->n_param;
-    T.nsys = nsys_d;
-    dd_status st;
-    if ((st = up_d(w, &T.w)) || (st = up_d(dd, &T.d)) || (st = up_d(ee, &T.e)) || (st = up_d(invb, &T.invb)) ||
-        (st = up_d(cpr, &T.cpr)) || (st = up_d(uf, &T.ufull)) || (st = up_d(up, &T.upart)) || (st = up_d(pa, &T.pa)) ||
-        (st = up_d(pb, &T.pb)) || (st = up_d(pinvb, &T.pinvb)))
-        return st;
 
     // --- per-parameter K, γ
     CK(dalloc(c, &c->Kp, c->n_param));
@@ -268,6 +290,10 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
     CK(dalloc(c, &c->r, vec));
     CK(dalloc(c, &c->p, vec));
     CK(dalloc(c, &c->q, vec));
+    if (c->frac_mode == DD_FRAC_RA) {
+        CK(dalloc(c, &c->q_f, vec));
+        c->small_ok = false;      // the persistent small-n kernel applies the dense F
+    }
     CK(dalloc(c, &c->bst, (size_t)n * c->max_cols));
     CK(dalloc(c, &c->xst, (size_t)n * c->max_cols));
     CK(dalloc(c, &c->colp_st, c->max_cols));
@@ -416,6 +442,24 @@ static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double
     g1.col_param = colp; g1.Kp = c->Kp; g1.gp = c->gp; g1.s = c->sw;
     g1.X = xin; g1.ldx = c->ldv; g1.Zlow = c->Z + c->Kpad;
     TIMED(DD_KCLASS_GEMM_DST, launch_dgemm(g1, c->stream));
+    if (c->frac_mode == DD_FRAC_RA) {
+        // Remark 1: U = γ M r_F(L) M X by the pole sum on the F tables, then Y = S_dst T' + U
+        TIMED(DD_KCLASS_POLESUM, launch_frac_ra(ncols, colp, c->n_param, c->gp, c->geom, c->ftabs, xin, c->ldv, c->q_f,
+                                                c->ldv, 1.0 / (6.0 * c->N), c->stream, c->pdl));
+        GemmArgs g2{};
+        g2.M = n; g2.N = ncols; g2.K = c->Kpad;
+        g2.A = c->W; g2.lda = c->lda;
+        g2.B = c->Z; g2.ldb = 2 * c->Kpad;
+        g2.C = y; g2.ldc = ldy;
+        g2.X = c->q_f; g2.ldx = c->ldv;
+        g2.splitk = gemm_pick_splitk(n, ncols, c->Kpad, c->num_sms); g2.ws = c->gws; g2.counters = c->gcnt;
+        g2.num_sms = c->num_sms;
+        g2.epi = EPI_ADD;
+        g2.pdl = c->pdl; g2.a_static = 1;
+        c->last_split2 = g2.splitk;
+        TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(g2, c->stream));
+        return DD_OK;
+    }
     GemmArgs g2{};
     g2.M = n; g2.N = ncols; g2.K = 2 * c->Kpad;
     g2.A = c->W; g2.lda = c->lda;

@@ -93,6 +93,8 @@ struct dd_ctx {
     double* gp = nullptr;     // [n_param]
     dd::PoleGeom geom{};
     dd::PoleTabs tabs{};
+    dd::PoleTabs ftabs{};     // RA of L^t (dd_frac DD_FRAC_RA): one set
+    double* q_f = nullptr;    // fractional-term output U (RA mode), ldv x cols_pad
     // workspaces
     double *xw = nullptr, *Z = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
     double *bst = nullptr, *xst = nullptr;   // host-API staging (ld = n_Γ)

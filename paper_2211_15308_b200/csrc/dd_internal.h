@@ -105,6 +105,10 @@ cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs
 cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st, bool pdl = false);
 cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, const PoleTabs& t,
                            const double* r, int ldr, double* z, int ldz, cudaStream_t st, bool pdl = false);
+// RA-evaluated fractional term u = γ M r_F M x (dd_frac DD_FRAC_RA; t: one-parameter-set F tables)
+cudaError_t launch_frac_ra(int ncols, const int* col_param, int n_param, const double* gp, const PoleGeom& g,
+                           const PoleTabs& t, const double* x, int ldx, double* u, int ldu, double h6, cudaStream_t st,
+                           bool pdl = false);
 // whole PCG in one launch for n <= 63 (one CTA per column, operators in shared memory)
 bool pcg_small_supported(int n);
 cudaError_t launch_pcg_small(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b, int ldb,

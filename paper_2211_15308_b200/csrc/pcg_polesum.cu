@@ -470,6 +470,41 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     for (int i = threadIdx.x; i < g.n; i += blockDim.x) z[(size_t)c * ldz + i] = S.Z[tpos(i, g)];
 }
 
+// RA-evaluated fractional term (Remark 1; dd_frac mode DD_FRAC_RA):
+//   u_c = γ_c M_Γ r_F(L) M_Γ x_c,   r_F(L) = fc0 M_Γ^-1 + Σ_k fc_k (A_Γ - fp_k M_Γ)^-1 ≈ L^t,
+// i.e. the pole sum of block_polesum on the F tables (one parameter set) between two products
+// with the 1D P1 mass M_Γ = (h/6) tridiag(1, 4, 1) (Dirichlet ends).
+template <int LMAX, int G, int NG>
+__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_frac_ra(int ncols, const int* __restrict__ col_param,
+                                                         int n_param, const double* __restrict__ gp, PoleGeom g,
+                                                         PoleTabs t, const double* __restrict__ x, int ldx,
+                                                         double* __restrict__ u, int ldu, double h6) {
+    extern __shared__ __align__(16) double sm[];
+    const int c = blockIdx.x;
+    if (c >= ncols) return;
+    pdl_trigger();
+    Smem S = carve(sm, g);
+    const int npad = g.T * g.LL, n = g.n;
+    stage_tables(t, g, 0, S.scratch);
+    pdl_wait_prior();
+    const double* xc = x + (size_t)c * ldx;
+    for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+        double v = 0.0;
+        if (i < n) v = h6 * ((i > 0 ? xc[i - 1] : 0.0) + 4.0 * xc[i] + (i + 1 < n ? xc[i + 1] : 0.0));
+        S.R[tpos(i, g)] = v;
+    }
+    __syncthreads();
+    block_polesum<LMAX, G, NG>(t, g, 0, S.R, S.Z, S.scratch);
+    int p = col_param[c];
+    p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
+    const double gam = gp[p] * h6;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double zm = i > 0 ? S.Z[tpos(i - 1, g)] : 0.0;
+        const double zp = i + 1 < n ? S.Z[tpos(i + 1, g)] : 0.0;
+        u[(size_t)c * ldu + i] = gam * (zm + 4.0 * S.Z[tpos(i, g)] + zp);
+    }
+}
+
 __device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_active) {
     // grid-wide bookkeeping: count active columns; last CTA publishes and sets the graph condition
     __shared__ int s_last;
@@ -884,6 +919,21 @@ cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, c
     DD_POLE_SWITCH(g, {
         e = set_smem(k_precond<LM, GG, NGG>, smem);
         if (e == cudaSuccess) e = launch_ex(k_precond<LM, GG, NGG>, ncols, 32 * GG * NGG, smem, st, pdl, ncols, col_param, g, t, r, ldr, z, ldz);
+    });
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_frac_ra(int ncols, const int* col_param, int n_param, const double* gp, const PoleGeom& g,
+                           const PoleTabs& t, const double* x, int ldx, double* u, int ldu, double h6, cudaStream_t st,
+                           bool pdl) {
+    if (ncols <= 0) return cudaSuccess;
+    const size_t smem = polesum_smem(g, t.max_sys);
+    cudaError_t e = cudaSuccess;
+    DD_POLE_SWITCH(g, {
+        e = set_smem(k_frac_ra<LM, GG, NGG>, smem);
+        if (e == cudaSuccess)
+            e = launch_ex(k_frac_ra<LM, GG, NGG>, ncols, 32 * GG * NGG, smem, st, pdl, ncols, col_param, n_param, gp, g, t,
+                          x, ldx, u, ldu, h6);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
 }

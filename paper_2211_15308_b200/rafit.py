@@ -209,6 +209,33 @@ def fit_ra(K: float, gamma: float, lam_min: float, lam_max: float, n_poles: int,
     return _finish(ra, lambda lam: f_general(lam, K, gamma))
 
 
+def fit_power(t: float, lam_min: float, lam_max: float, n_poles: int, sigma: float = 0.0) -> RationalApprox:
+    """RA r_F(λ) = c0 + Σ c_k/(λ - p_k) of (λ + σ)^t, -1 < t < 0, on [lam_min, lam_max] — the
+    fractional term evaluated by RA (Remark 1: "action of the perturbation can
+    instead be computed via RA"; dd_frac mode DD_FRAC_RA).  t = -1/2: Zolotarev's best relative
+    approximation of x^{-1/2} (all poles real negative, residues positive); other t: AAA.
+    Returned in the library convention (poles of the pair (A_Γ, M_Γ): p_k = q_k - σ)."""
+    if not (-1.0 < t < 0.0) or sigma < 0 or not (0 < lam_min < lam_max):
+        raise ValueError("need -1 < t < 0, sigma >= 0, 0 < lam_min < lam_max")
+    lo, hi = lam_min + sigma, lam_max + sigma
+    if t == -0.5:
+        import mpmath as mp
+        with mp.workdps(50):
+            d0, q, r = _zolotarev_invsqrt(hi / lo, n_poles)
+            lm = mp.mpf(lo)
+            c0 = float(d0 / mp.sqrt(lm))
+            poles = np.array([float(ql * lm) for ql in q])
+            res = np.array([float(rl * mp.sqrt(lm)) for rl in r])
+        method = "zolotarev"
+    else:
+        c0, poles, res = fit_function_aaa(lambda x: x ** t, lo, hi, n_poles)
+        method = "aaa"
+    order = np.argsort(-poles)
+    ra = RationalApprox(float(c0), poles[order] - sigma, res[order], float(lam_min), float(lam_max), 1.0, 0.0,
+                        n_poles, t=float(t), sigma=float(sigma), method=method)
+    return _finish(ra, lambda lam: (np.asarray(lam, dtype=np.float64) + sigma) ** t)
+
+
 def face_pair(N: int):
     """Sparse P1 pair of the Kuhn-mesh face Γ = {x=0} with Dirichlet ∂Γ (stencils of SURVEY §8
     "verified stencils", pinned against element assembly in the oracle tests):

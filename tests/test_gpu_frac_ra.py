@@ -1,0 +1,70 @@
+"""The fractional term evaluated by rational approximation (Remark 1, PAPER.md:274-288;
+dd_frac mode DD_FRAC_RA): y = K S_unit x + γ M r_F(L) M x with r_F ≈ L^t
+applied as a second pole sum (no dense F).  Parity with the oracle's same-RA operator; closeness
+to the dense Eq.(7) operator within the fit error.  Needs a B200 (-m gpu)."""
+import numpy as np
+import pytest
+
+from helpers import rel_l2_cols
+from oracle import pcg as opcg
+from oracle import problem as oprob
+from paper_2211_15308_b200 import rafit
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2211_15308_b200 import binding
+    binding.load()
+    return binding
+
+
+def _cols(B):
+    return torch.as_tensor(B, device="cuda")
+
+
+@pytest.mark.parametrize("N,t,sigma", [(9, -0.5, 0.0), (64, -0.5, 0.0), (200, -0.25, 1.0), (1024, -0.5, 0.0)])
+def test_ra_operator_parity(lib, N, t, sigma):
+    params = [(1.0, 1e2), (1e-3, 1e4)]
+    lo, hi = rafit.interval_1d(N)
+    ras = [rafit.fit_ra(K, g, lo, hi, 14, t=t, sigma=sigma) for K, g in params]
+    fr = rafit.fit_power(t, lo, hi, 16, sigma)
+    fra = (fr.c0, fr.poles, fr.residues)
+    if N <= 200:
+        O = oprob.DenseProblem(2, N, t=t, sigma=sigma, frac_ra=fra)
+        Oex = oprob.DenseProblem(2, N, t=t, sigma=sigma)
+    else:
+        O = oprob.ModeProblem2D(N, t=t, sigma=sigma, frac_ra=fra)
+        Oex = oprob.ModeProblem2D(N, t=t, sigma=sigma)
+    C = 8
+    B = np.random.default_rng(N).uniform(-1, 1, (C, N - 1))
+    colp = np.arange(C) % 2
+    S = lib.Solver(2, N, params, ras, max_cols=C, frac=lib.Frac(t=t, shifted=bool(sigma), mode="ra", fra=fr))
+    try:
+        y = S.apply_schur(_cols(B), colp).cpu().numpy()
+        ref = np.stack([O.apply_S(*params[colp[c]], B[c]) for c in range(C)])
+        assert rel_l2_cols(y, ref) <= max(1e-10, 1e-15 * fr.cancel * 1e2)
+        ex = np.stack([Oex.apply_S(*params[colp[c]], B[c]) for c in range(C)])
+        assert rel_l2_cols(y, ex) <= 2 * fr.rel_err + 1e-12
+        res = S.pcg_solve(_cols(B), colp)
+        x = res.x.cpu().numpy()
+        for c in range(C):
+            K, g = params[colp[c]]; ra = ras[colp[c]]
+            xo, it, *_ = opcg.pcg(lambda v: O.apply_S(K, g, v),
+                                  lambda v: O.apply_P_ra(ra.c0, ra.poles, ra.residues, v), B[c])
+            assert abs(int(res.iters[c]) - it) <= 1
+            assert np.linalg.norm(x[c] - xo) <= 1e-8 * np.linalg.norm(xo)
+        cfg = S.query_config()
+        assert cfg["graph_while"] != 2          # the dense-F persistent small kernel is not used
+    finally:
+        S.close()
+
+
+def test_ra_mode_rejected_in_3d(lib):
+    lo, hi = rafit.interval_face(6)
+    ras = [rafit.fit_ra(1.0, 1.0, lo, hi, 8)]
+    fr = rafit.fit_power(-0.5, lo, hi, 8)
+    with pytest.raises(lib.DDError):
+        lib.Solver(3, 6, [(1.0, 1.0)], ras, max_cols=1, frac=lib.Frac(mode="ra", fra=fr))

@@ -548,3 +548,31 @@ def test_bulk_manufactured_solution_rate():
         errs.append(np.abs(x - u).max())
     rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     assert np.all(rates > 1.8) and errs[-1] < 2e-3, (errs, rates)
+
+
+# --------------------------------------------------------------------------- RA-evaluated operator (NEXT-2, Remark 1)
+@pytest.mark.parametrize("t,sigma", [(-0.5, 0.0), (-0.25, 1.0)])
+def test_ra_evaluated_fractional_term(t, sigma):
+    # Remark 1: F ≈ M r_F(L) M with r_F ≈ λ^t.  Pins: (i) the oracle's
+    # shifted-solve form equals the explicit sine closed form S diag(μ r_F(λ)) S; (ii) it is within
+    # the fit's relative error of the Eq.(7) F, mode by mode: |r_F(λ)/(λ+σ)^t - 1| <= ε_F.
+    N = 40
+    lo, hi = rafit.interval_1d(N)
+    fr = rafit.fit_power(t, lo, hi, 12, sigma)
+    assert np.all(fr.poles < 0)
+    D = problem.DenseProblem(2, N, t=t, sigma=sigma, frac_ra=(fr.c0, fr.poles, fr.residues))
+    h = 1.0 / N; n = N - 1
+    j = np.arange(1, n + 1)
+    Sd = np.sqrt(2.0 / N) * np.sin(np.outer(j, j) * np.pi / N)
+    th = j * np.pi / N
+    mu = (h / 6) * (4 + 2 * np.cos(th))
+    lam = (6 / h ** 2) * (1 - np.cos(th)) / (2 + np.cos(th))
+    rF = ra.r_eval(lam, fr.c0, fr.poles, fr.residues)
+    assert np.abs(D.F - Sd @ np.diag(mu * rF) @ Sd).max() <= 1e-12 * np.abs(D.F).max()
+    assert np.max(np.abs(rF / (lam + sigma) ** t - 1)) <= 1.01 * fr.rel_err + 1e-15
+    Fex = problem.DenseProblem(2, N, t=t, sigma=sigma).F
+    assert np.abs(D.F - Fex).max() <= 2 * fr.rel_err * np.abs(Fex).max()
+    Mo = problem.ModeProblem2D(N, t=t, sigma=sigma, frac_ra=(fr.c0, fr.poles, fr.residues))
+    X = np.random.default_rng(2).uniform(-1, 1, (n, 3))
+    a, b = D.apply_S(1.0, 1e2, X), Mo.apply_S(1.0, 1e2, X)
+    assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
