@@ -424,7 +424,7 @@ extern "C" int dd_interface_size(const dd_ctx* c) { return c ? c->ng : -1; }
 
 // ------------------------------------------------------------------------------------ applies
 static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double* xin, double* y, int ldy) {
-    // T' = (K_c s) ∘ (S_dst X) -> Z[0:n);  γ_c X -> Z[Kpad:Kpad+n);  Y = [S_dst | F] Z
+    // T' = (K_c s) ∘ (S_dst X) -> Z[0:n);  Y = [S_dst | F] [T' ; γ X]
     const int n = c->n;
     const int sk1 = gemm_pick_splitk(n, ncols, c->Kpad, c->num_sms);
     const int sk2 = gemm_pick_splitk(n, ncols, 2 * c->Kpad, c->num_sms);
@@ -556,6 +556,7 @@ static dd_status build_graph(dd_ctx* c, const PcgState& s0, cudaGraphExec_t* out
     c->prof = false;
     const long long l0 = c->launches;
     dd_status st = iteration_body(c, s);
+    c->graph_iter_launches = c->launches - l0;
     c->launches = l0;
     c->prof = prof;
     cudaGraph_t captured = nullptr;
@@ -659,7 +660,7 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
         fprintf(stderr, "[dd polesum cycles] stage-wait %lld  sys0: fwd %lld bwd %lld pcr %lld  rest-of-systems %lld  combine %lld\n",
                 t[6] - t[2], t[7] - t[6], t[8] - t[7], t[9] - t[8], t[10] - t[9], t[3] - t[10]);
     }
-    if (c->last_graph) c->launches += 3LL * kdone;
+    if (c->last_graph) c->launches += c->graph_iter_launches * kdone;
     if (hist) {
         // column 0 history: η_0 .. η_{iters[0]}
         int it0 = 0;

@@ -117,6 +117,7 @@ struct dd_ctx {
     bool graph_ok = true;
     std::map<dd::GraphKey, cudaGraphExec_t> graphs;
     int last_split1 = 0, last_split2 = 0, last_ps_warps = 0, last_graph = 0, last_small = 0;
+    long long graph_iter_launches = 3;   // kernels per PCG iteration in the captured body
     bool pdl = true;          // programmatic dependent launch between the iteration's kernels (DD_NO_PDL=1 disables)
     bool small_ok = true;     // persistent single-launch PCG for n <= 63 (DD_NO_SMALL=1 disables)
     cudaEvent_t solve_ev[2] = {nullptr, nullptr};
