@@ -238,6 +238,10 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
 }
 
 void destroy_3d(dd_ctx* c) {
+    if (c->f3.inner_exec) {
+        cudaGraphExecDestroy(c->f3.inner_exec);
+        c->f3.inner_exec = nullptr;
+    }
     if (c->f3.nccl) {
         ncclCommDestroy(static_cast<ncclComm_t>(c->f3.nccl));
         c->f3.nccl = nullptr;
@@ -275,21 +279,72 @@ static dd_status precond_core(dd_ctx* c, int ncols, const double* r, double* z) 
         DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(r, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
         DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.S, c->stream));
         DD_TIMED(DD_KCLASS_POLESUM, inner_init_hat(a, f.U2, c->stream));
-        int it = 0;
-        for (it = 1; it <= f.inner_maxit; it++) {
+        auto body = [&](cudaStream_t st, int* n_act) -> dd_status {
             // q̂ = dg ∘ p̂ + cs D̂ p̂ D̂^T on the active pairs, then the fused CG update
-            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_active(f.ip, f.T1, a.npair, f.n, f.ldf, f.Dh, f.iactive, c->stream));
+            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_active(f.ip, f.T1, a.npair, f.n, f.ldf, f.Dh, f.iactive, st));
             DD_TIMED(DD_KCLASS_POLESUM, face_inner_op_pass(f.T1, f.iq, f.ip, a.npair, ncols, f.n, f.ldf, f.Dh, f.dg, f.cs,
-                                                           f.iactive, c->stream));
-            DD_CK(cudaMemsetAsync(c->ints + 1, 0, sizeof(int), c->stream));
-            DD_TIMED(DD_KCLASS_POLESUM, inner_update_hat(a, c->ints + 1, c->stream));
-            if (it % 4 == 0 || it == f.inner_maxit) {
-                DD_CK(cudaMemcpyAsync(c->h_ints + 1, c->ints + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-                DD_CK(cudaStreamSynchronize(c->stream));
-                if (c->h_ints[1] == 0) break;
+                                                           f.iactive, st));
+            DD_TIMED(DD_KCLASS_POLESUM, inner_update_hat(a, n_act, st));
+            return DD_OK;
+        };
+        if (c->graph_ok && !c->prof) {
+            // the whole inner loop as one conditional WHILE graph (no host round trips)
+            if (!f.inner_exec || f.inner_key != ncols) {
+                if (f.inner_exec) cudaGraphExecDestroy(f.inner_exec);
+                f.inner_exec = nullptr;
+                cudaGraph_t g = nullptr;
+                DD_CK(cudaGraphCreate(&g, 0));
+                cudaGraphConditionalHandle h;
+                DD_CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+                cudaGraphNodeParams cp = {};
+                cp.type = cudaGraphNodeTypeConditional;
+                cp.conditional.handle = h;
+                cp.conditional.type = cudaGraphCondTypeWhile;
+                cp.conditional.size = 1;
+                cudaGraphNode_t node;
+                DD_CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+                cudaStream_t cap = nullptr;
+                DD_CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+                DD_CK(cudaStreamBeginCaptureToGraph(cap, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                    cudaStreamCaptureModeRelaxed));
+                const bool prof = c->prof;
+                c->prof = false;
+                const long long l0 = c->launches;
+                dd_status bs = body(cap, c->ints + 1);
+                cudaError_t ce = inner_cond(c->ints + 1, c->ints + 6, f.inner_maxit, (unsigned long long)h, cap);
+                c->inner_iter_launches = c->launches - l0 + 1;
+                c->launches = l0;
+                c->prof = prof;
+                cudaGraph_t captured = nullptr;
+                cudaError_t ee = cudaStreamEndCapture(cap, &captured);
+                cudaStreamDestroy(cap);
+                if (bs != DD_OK || ce != cudaSuccess || ee != cudaSuccess) {
+                    cudaGraphDestroy(g);
+                    return bs != DD_OK ? bs : set_error(DD_ECUDA, "inner-loop graph capture");
+                }
+                DD_CK(cudaGraphInstantiate(&f.inner_exec, g, 0));
+                cudaGraphDestroy(g);
+                f.inner_key = ncols;
             }
+            DD_CK(cudaMemsetAsync(c->ints + 6, 0, sizeof(int), c->stream));
+            DD_CK(cudaMemsetAsync(c->ints + 1, 0, sizeof(int), c->stream));
+            DD_CK(cudaGraphLaunch(f.inner_exec, c->stream));
+            f.inner_iters_on_device = true;
+        } else {
+            int it = 0;
+            for (it = 1; it <= f.inner_maxit; it++) {
+                DD_CK(cudaMemsetAsync(c->ints + 1, 0, sizeof(int), c->stream));
+                dd_status bs = body(c->stream, c->ints + 1);
+                if (bs != DD_OK) return bs;
+                if (it % 4 == 0 || it == f.inner_maxit) {
+                    DD_CK(cudaMemcpyAsync(c->h_ints + 1, c->ints + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+                    DD_CK(cudaStreamSynchronize(c->stream));
+                    if (c->h_ints[1] == 0) break;
+                }
+            }
+            f.last_inner_iters = std::min(it, f.inner_maxit);
+            f.inner_iters_on_device = false;
         }
-        f.last_inner_iters = std::min(it, f.inner_maxit);
         // ẑ_c = Σ_s w_s x̂_{s,c} (fixed system order), z_c = Q ẑ_c
         DD_TIMED(DD_KCLASS_POLESUM, inner_combine(a, f.sys_w, f.nsys, f.U1, c->stream));
         DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.S, c->stream));
@@ -368,6 +423,15 @@ extern "C" dd_status dd_nccl_unique_id(void* out128) {
 
 extern "C" dd_status dd_inner_iterations(const dd_ctx* c, int* iters) {
     if (!c || !iters) return dd::set_error(DD_EINVAL, "NULL argument");
+    if (c->f3.inner_iters_on_device) {
+        // the WHILE graph counts its iterations on the device (ints[6]); read it synchronously
+        int v = 0;
+        if (cudaSetDevice(c->device) != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess ||
+            cudaMemcpy(&v, c->ints + 6, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return dd::set_error(DD_ECUDA, "reading the inner iteration count");
+        *iters = v;
+        return DD_OK;
+    }
     *iters = c->f3.last_inner_iters;
     return DD_OK;
 }

@@ -840,7 +840,16 @@ extern "C" dd_status dd_last_solve_ms(dd_ctx* c, double* ms) {
 
 extern "C" long long dd_launch_count(dd_ctx* c) {
     if (!c) return -1;
-    const long long v = c->launches;
+    long long v = c->launches;
+    if (c->dim == 3 && c->f3.inner_exec) {
+        // inner-CG iterations run inside a device-side WHILE graph: counted on the device (ints[8])
+        int tot = 0;
+        if (cudaSetDevice(c->device) == cudaSuccess && cudaStreamSynchronize(c->stream) == cudaSuccess &&
+            cudaMemcpy(&tot, c->ints + 8, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess) {
+            v += (long long)tot * c->inner_iter_launches;
+            cudaMemset(c->ints + 8, 0, sizeof(int));
+        }
+    }
     c->launches = 0;
     return v;
 }

@@ -64,6 +64,9 @@ struct Face3 {
     double inner_rtol = 1e-13;        // reading A12
     int inner_maxit = 400;
     int last_inner_iters = 0;
+    cudaGraphExec_t inner_exec = nullptr;   // WHILE graph of the inner CG loop (key: inner_key = columns)
+    int inner_key = -1;
+    bool inner_iters_on_device = false;
     double* fx_ws = nullptr;
     int* fx_cnt = nullptr;
     double lam_min = 0.0, lam_max = 0.0;   // spectrum of the face pair (from the setup gevp)
@@ -118,6 +121,7 @@ struct dd_ctx {
     std::map<dd::GraphKey, cudaGraphExec_t> graphs;
     int last_split1 = 0, last_split2 = 0, last_ps_warps = 0, last_graph = 0, last_small = 0;
     long long graph_iter_launches = 3;   // kernels per PCG iteration in the captured body
+    long long inner_iter_launches = 4;   // kernels per inner-CG iteration (3D WHILE graph)
     bool pdl = true;          // programmatic dependent launch between the iteration's kernels (DD_NO_PDL=1 disables)
     bool small_ok = true;     // persistent single-launch PCG for n <= 63 (DD_NO_SMALL=1 disables)
     cudaEvent_t solve_ev[2] = {nullptr, nullptr};

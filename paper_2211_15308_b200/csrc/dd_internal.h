@@ -177,6 +177,7 @@ cudaError_t face_inner_op_pass(const double* in, double* q, const double* p, int
 cudaError_t inner_init_hat(const InnerArgs& a, const double* bh, cudaStream_t st);
 cudaError_t inner_update_hat(const InnerArgs& a, int* n_active, cudaStream_t st);
 cudaError_t inner_init(const InnerArgs& a, const double* b, cudaStream_t st);
+cudaError_t inner_cond(int* n_active, int* counter, int maxit, unsigned long long handle, cudaStream_t st);
 cudaError_t inner_start(const InnerArgs& a, cudaStream_t st);
 cudaError_t inner_step1(const InnerArgs& a, cudaStream_t st);
 cudaError_t inner_step2(const InnerArgs& a, int* n_active, cudaStream_t st);

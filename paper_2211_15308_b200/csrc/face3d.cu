@@ -316,6 +316,20 @@ __global__ void k_inner_update_hat(InnerArgs a, int* n_active) {
         atomicAdd(n_active, 1);
     }
 }
+// inner-CG WHILE-graph condition: one more iteration while any pair is active and it < maxit
+__global__ void k_inner_cond(int* n_active, int* counter, int maxit, unsigned long long handle) {
+    const int it = *counter + 1;
+    *counter = it;
+    counter[2] += 1;          // cumulative inner iterations (launch accounting; see dd_launch_count)
+    const int na = *n_active;
+    *n_active = 0;
+    cudaGraphSetConditional((cudaGraphConditionalHandle)handle, (na > 0 && it < maxit) ? 1u : 0u);
+}
+cudaError_t inner_cond(int* n_active, int* counter, int maxit, unsigned long long handle, cudaStream_t st) {
+    k_inner_cond<<<1, 1, 0, st>>>(n_active, counter, maxit, handle);
+    return cudaGetLastError();
+}
+
 cudaError_t inner_init_hat(const InnerArgs& a, const double* bh, cudaStream_t st) {
     k_inner_init_hat<<<a.npair, 512, 0, st>>>(a, bh);
     return cudaGetLastError();
