@@ -290,6 +290,7 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
     CK(dalloc(c, &c->r, vec));
     CK(dalloc(c, &c->p, vec));
     CK(dalloc(c, &c->q, vec));
+    CK(dalloc(c, &c->ntl, 2 * (c->cols_pad / GEMM_BN) + 4));
     if (c->frac_mode == DD_FRAC_RA) {
         CK(dalloc(c, &c->q_f, vec));
         c->small_ok = false;      // the persistent small-n kernel applies the dense F
@@ -392,6 +393,7 @@ extern "C" dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n
     if (const char* ng = std::getenv("DD_NO_GRAPH")) c->graph_ok = !(ng[0] == '1');   // profiling: host loop
     if (const char* ns = std::getenv("DD_NO_SMALL")) c->small_ok = !(ns[0] == '1');
     if (const char* np = std::getenv("DD_NO_PDL")) c->pdl = !(np[0] == '1');
+    if (const char* nk = std::getenv("DD_NO_COMPACT")) c->compact = !(nk[0] == '1');
     const char* pht = std::getenv("DD_PHASE_TIMING");
     const bool want_dbg = pht && pht[0] == '1';
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DD_ECUDA, "cudaSetDevice failed"));
@@ -423,7 +425,8 @@ extern "C" dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n
 extern "C" int dd_interface_size(const dd_ctx* c) { return c ? c->ng : -1; }
 
 // ------------------------------------------------------------------------------------ applies
-static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double* xin, double* y, int ldy) {
+static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double* xin, double* y, int ldy,
+                             const int* ntl = nullptr) {
     // T' = (K_c s) ∘ (S_dst X) -> Z[0:n);  Y = [S_dst | F] [T' ; γ X]
     const int n = c->n;
     const int sk1 = gemm_pick_splitk(n, ncols, c->Kpad, c->num_sms);
@@ -441,6 +444,7 @@ static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double
     g1.n_param = c->n_param;
     g1.col_param = colp; g1.Kp = c->Kp; g1.gp = c->gp; g1.s = c->sw;
     g1.X = xin; g1.ldx = c->ldv; g1.Zlow = c->Z + c->Kpad;
+    g1.ntl = ntl;
     TIMED(DD_KCLASS_GEMM_DST, launch_dgemm(g1, c->stream));
     if (c->frac_mode == DD_FRAC_RA) {
         // Remark 1: U = γ M r_F(L) M X by the pole sum on the F tables, then Y = S_dst T' + U
@@ -456,6 +460,7 @@ static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double
         g2.num_sms = c->num_sms;
         g2.epi = EPI_ADD;
         g2.pdl = c->pdl; g2.a_static = 1;
+        g2.ntl = ntl;
         c->last_split2 = g2.splitk;
         TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(g2, c->stream));
         return DD_OK;
@@ -468,6 +473,7 @@ static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double
     g2.splitk = sk2; g2.ws = c->gws; g2.counters = c->gcnt; g2.num_sms = c->num_sms;
     g2.epi = EPI_STORE;
     g2.pdl = c->pdl; g2.a_static = 1;
+    g2.ntl = ntl;
     TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(g2, c->stream));
     return DD_OK;
 }
@@ -518,11 +524,16 @@ static PcgState make_state(dd_ctx* c, int ncols, const int* colp, double* x, dou
     s.rtol = rtol; s.maxit = maxit; s.norm_kind = norm_kind;
     s.cond_handle = 0;
     s.dbg = c->dbg;
+    // Live-tile compaction costs one dependent load at the start of every GEMM CTA (and a warp's
+    // work in the pole-sum tail); it pays for batches of >= 6 column tiles whose parameter sets
+    // converge at different iterations (cfg5: +10.8 %), not for 4 tiles (cfg2: -1.4 %).
+    s.ntl = (c->compact && (ncols + GEMM_BN - 1) / GEMM_BN >= 6) ? c->ntl : nullptr;
+    s.ntl_cnt = c->ntl + c->cols_pad / GEMM_BN + 2;
     return s;
 }
 
 static dd_status iteration_body(dd_ctx* c, const PcgState& s) {
-    dd_status st = schur_gemms(c, s.ncols, s.col_param, c->p, c->q, c->ldv);
+    dd_status st = schur_gemms(c, s.ncols, s.col_param, c->p, c->q, c->ldv, s.ntl);
     if (st != DD_OK) return st;
     c->last_ps_warps = polesum_warps(c->geom);
     TIMED(DD_KCLASS_POLESUM, launch_pcg_iter(s, c->geom, c->tabs, c->stream, c->pdl));
@@ -587,6 +598,7 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
     }
     CK(cudaEventRecord(c->solve_ev[0], c->stream));
     CK(cudaMemsetAsync(c->ints, 0, sizeof(int) * 8, c->stream));
+    if (c->dim == 2) CK(cudaMemsetAsync(c->ntl, 0, sizeof(int) * (2 * (c->cols_pad / GEMM_BN) + 4), c->stream));
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
     PcgState st = make_state(c, ncols, colp, x, rtol, maxit, norm_kind);
     c->last_ps_warps = polesum_warps(c->geom);

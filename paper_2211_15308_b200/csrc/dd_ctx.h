@@ -122,6 +122,8 @@ struct dd_ctx {
     int last_split1 = 0, last_split2 = 0, last_ps_warps = 0, last_graph = 0, last_small = 0;
     long long graph_iter_launches = 3;   // kernels per PCG iteration in the captured body
     long long inner_iter_launches = 4;   // kernels per inner-CG iteration (3D WHILE graph)
+    bool compact = true;      // GEMMs work over live (unconverged) column tiles only (DD_NO_COMPACT=1 disables)
+    int* ntl = nullptr;       // live column tiles [count, ids...], written by the PCG kernels
     bool pdl = true;          // programmatic dependent launch between the iteration's kernels (DD_NO_PDL=1 disables)
     bool small_ok = true;     // persistent single-launch PCG for n <= 63 (DD_NO_SMALL=1 disables)
     cudaEvent_t solve_ev[2] = {nullptr, nullptr};

@@ -33,6 +33,7 @@ struct GemmArgs {
     int epi;
     int pdl;                     // launch with programmatic stream serialisation (follows a kernel)
     int a_static;                // A is constant (prefetched before griddepcontrol.wait)
+    const int* ntl;              // live column tiles [count, ids...] (BN = 64): work over these only (or null)
     int n_param;
     // EPI_SCHUR_DST
     const int* col_param; const double* Kp; const double* gp; const double* s;
@@ -93,6 +94,8 @@ struct PcgState {
     double rtol; int maxit; int norm_kind;
     unsigned long long cond_handle;    // cudaGraphConditionalHandle (0 = none)
     long long* dbg;                    // optional phase timestamps of CTA 0 (DD_PHASE_TIMING=1)
+    int* ntl;                          // live 64-column tiles [count, ids...] for the GEMMs (or null)
+    int* ntl_cnt;                      // active columns per 64-column tile (zeroed before pcg_init)
 };
 
 PoleGeom make_pole_geom(int n);

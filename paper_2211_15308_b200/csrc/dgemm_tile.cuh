@@ -49,6 +49,8 @@ struct DgemmProblem {
     const int* active = nullptr; // optional per-slab flag: slabs with active[b] == 0 are skipped
     unsigned long long* ts = nullptr;   // optional per-CTA phase timestamps (lab instrumentation)
     int a_static = 0;            // A is not written by the preceding kernel: prefetch it before griddepcontrol.wait
+    const int* ntl = nullptr;    // live column tiles [count, tile ids...] (PCG: columns freeze when converged):
+                                 // the tile / stream-K work is laid out over the live tiles only
 };
 
 // Programmatic dependent launch (no-ops when the launch did not opt in)
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
     const int bz = blockIdx.z;
     const int tiles_m = (g.M + C::BM - 1) / C::BM;
     const int m0 = (blockIdx.x % tiles_m) * C::BM;
-    const int n0 = (blockIdx.x / tiles_m) * C::BN;
+    int n0 = (blockIdx.x / tiles_m) * C::BN;
     const int split = S > 1 ? (int)blockIdx.y : 0;
     const int ktiles = g.K / C::BK;
     const int per = (ktiles + S - 1) / S;
@@ -157,6 +159,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
     }
     pdl_wait();
     if (g.active && !g.active[bz]) return;   // frozen slab (uniform across the cluster)
+    if (g.ntl) {                             // live column tiles only (uniform across the cluster)
+        const int nidx = blockIdx.x / tiles_m;
+        if (nidx >= g.ntl[0]) {
+            asm volatile("cp.async.wait_all;\n" ::);   // drain the A prefetch before leaving
+            return;
+        }
+        n0 = g.ntl[1 + nidx] * C::BN;
+    }
     DG_TS(0);
     g.A = A0;
     g.B += (size_t)bz * g.sB;
@@ -294,7 +304,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProb
     pdl_wait();
 
     const int tiles_m = (g.M + C::BM - 1) / C::BM;
-    const int tiles = tiles_m * ((g.N + C::BN - 1) / C::BN);
+    const int tiles = tiles_m * (g.ntl ? g.ntl[0] : (g.N + C::BN - 1) / C::BN);
     const int KT = g.K / C::BK;
     const long long U = (long long)tiles * KT;
     const int b = blockIdx.x;
@@ -310,7 +320,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProb
         const int ks = (int)(u % KT);
         const int ke = (int)min((long long)KT, (long long)ks + (u1 - u));
         const int m0 = (t % tiles_m) * C::BM;
-        const int n0 = (t / tiles_m) * C::BN;
+        const int n0 = (g.ntl ? g.ntl[1 + t / tiles_m] : t / tiles_m) * C::BN;
         const int nkt = ke - ks;
 
         double acc[C::MI][C::NI][4];

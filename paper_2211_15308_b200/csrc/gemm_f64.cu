@@ -64,6 +64,7 @@ template <class Epi>
 static cudaError_t launch(const GemmArgs& a, const Epi& e, cudaStream_t st) {
     DgemmProblem g{a.M, a.N, a.K, a.A, a.lda, a.B, a.ldb};
     g.a_static = a.a_static;
+    g.ntl = a.ntl;
     if (a.splitk == 0) {
         StreamK sk{a.ws, a.counters, 0};
         // no PDL here: early-resident CTAs of a stream-K grid land unevenly on the SMs (a third

@@ -505,20 +505,53 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_f
     }
 }
 
-__device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_active) {
+// Live 64-column tiles of the batch (GEMM output tiles with at least one unconverged column):
+// every CTA keeps its tile's active-column count current (ntl_cnt, +1 at init, -1 when its column
+// freezes); the last-arriving CTA compacts the live tile ids into s.ntl = [count, ids...] and the
+// next iteration's GEMMs partition their work over those tiles only.
+__device__ __forceinline__ void publish_live_tiles(const PcgState& s, int na) {
+    // warp 0 of the last CTA.  All columns active (the common case until the last iterations):
+    // the identity list, no memory round trip; otherwise one L2 round trip per 32 tiles (ballot +
+    // prefix popcount over the per-tile counters).
+    if (!s.ntl || threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const int nt = (s.ncols + 63) / 64;
+    if (na == s.ncols) {
+        for (int j = lane; j < nt; j += 32) s.ntl[1 + j] = j;
+        if (lane == 0) s.ntl[0] = nt;
+        return;
+    }
+    int total = 0;
+    for (int base = 0; base < nt; base += 32) {
+        const int j = base + lane;
+        const bool live = j < nt && __ldcg(&s.ntl_cnt[j]) > 0;
+        const unsigned m = __ballot_sync(0xffffffffu, live);
+        if (live) s.ntl[1 + total + __popc(m & ((1u << lane) - 1u))] = j;
+        total += __popc(m);
+    }
+    if (lane == 0) s.ntl[0] = total;
+}
+
+__device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_active, bool was_active) {
     // grid-wide bookkeeping: count active columns; last CTA publishes and sets the graph condition
     __shared__ int s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
         if (still_active) atomicAdd(s.n_active_next, 1);
+        if (was_active && !still_active && s.ntl) atomicSub(&s.ntl_cnt[blockIdx.x / 64], 1);
         __threadfence();
         const int prev = atomicAdd(s.done_ctas, 1);
-        s_last = (prev == (int)gridDim.x - 1);
+        const bool last = prev == (int)gridDim.x - 1;
+        if (last) __threadfence();       // acquire: every other CTA's counters are visible
+        s_last = last;
     }
     __syncthreads();
-    if (s_last && threadIdx.x == 0) {
-        __threadfence();
-        const int na = atomicAdd(s.n_active_next, 0);
+    if (!s_last || threadIdx.x >= 32) return;
+    int na = 0;
+    if (threadIdx.x == 0) na = atomicAdd(s.n_active_next, 0);
+    na = __shfl_sync(0xffffffffu, na, 0);
+    publish_live_tiles(s, na);
+    if (threadIdx.x == 0) {
         const int k = *s.kiter + 1;
         *s.kiter = k;
         *s.n_active = na;
@@ -536,6 +569,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
                                                           const double* __restrict__ b, int ldb) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
+    __shared__ int s_init_last;
     const int c = blockIdx.x;
     const int n = g.n, npad = g.T * g.LL;
     pdl_trigger();
@@ -570,11 +604,20 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
         s.active[c] = act ? 1 : 0;
         if (c == 0 && s.hist) s.hist[0] = eta0;
         if (act) atomicAdd(s.n_active_next, 1);
+        if (act && s.ntl) atomicAdd(&s.ntl_cnt[c / 64], 1);
         __threadfence();
         const int prev = atomicAdd(s.done_ctas, 1);
-        if (prev == (int)gridDim.x - 1) {
-            __threadfence();
-            *s.n_active = atomicAdd(s.n_active_next, 0);
+        s_init_last = prev == (int)gridDim.x - 1;
+        if (s_init_last) __threadfence();
+    }
+    __syncthreads();
+    if (s_init_last && threadIdx.x < 32) {
+        int na = 0;
+        if (threadIdx.x == 0) na = atomicAdd(s.n_active_next, 0);
+        na = __shfl_sync(0xffffffffu, na, 0);
+        publish_live_tiles(s, na);
+        if (threadIdx.x == 0) {
+            *s.n_active = na;
             *s.n_active_next = 0;
             *s.done_ctas = 0;
             *s.kiter = 0;
@@ -689,7 +732,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
         }
     }
     DD_PHASE(4);
-    finish_iteration(s, still);
+    finish_iteration(s, still, s_work != 0);
     DD_PHASE(5);
 #undef DD_PHASE
 }
