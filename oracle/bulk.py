@@ -58,3 +58,27 @@ class BulkSystem:
     def from_product(self, y):
         y = np.asarray(y)
         return np.concatenate([y[..., self.ni:], y[..., : self.ni]], axis=-1)
+
+    # ----------------------------------------------------------------------- Eq.(5)
+    def _lu00(self, K):
+        key = float(K)
+        if getattr(self, "_lu_key", None) != key:
+            A = (K * self.A).tocsc()
+            g = self.g
+            self._lu = spla.splu(A[g:, g:].tocsc())
+            self._A0i = A[g:, :g].tocsr()
+            self._Ai0 = A[:g, g:].tocsr()
+            self._lu_key = key
+        return self._lu, self._A0i, self._Ai0
+
+    def dd_precond(self, K, apply_SG_inv, r):
+        """𝓑 r of Eq.(5), in BulkProblem order [Γ, interior]:
+        y0 = (A^00)^-1 r0,  zΓ = S_Γ^-1 (rΓ - A^{i0} y0),  z0 = (A^00)^-1 (r0 - A^{0i} zΓ)
+        — the three factors applied right to left; (A^00)^-1 exact (sparse LU)."""
+        lu, A0i, Ai0 = self._lu00(K)
+        g = self.g
+        r = np.asarray(r, dtype=np.float64)
+        y0 = lu.solve(r[g:])
+        zg = apply_SG_inv(r[:g] - Ai0 @ y0)
+        z0 = lu.solve(r[g:] - A0i @ zg)
+        return np.concatenate([zg, z0])

@@ -24,7 +24,7 @@ KCLASS = ["gemm_dst", "gemm_schur", "polesum_pcg", "other"]
 EXPORTS = ["dd_setup", "dd_setup_ex", "dd_interface_size", "dd_apply_schur", "dd_apply_precond", "dd_pcg_solve",
            "dd_pcg_solve_host", "dd_destroy", "dd_last_error", "dd_profile_enable", "dd_profile_read",
            "dd_launch_count", "dd_query_config", "dd_test_dgemm", "dd_last_solve_ms", "dd_nccl_unique_id",
-           "dd_inner_iterations", "dd_bulk_solve"]
+           "dd_inner_iterations", "dd_bulk_solve", "dd_bulk_pcg_solve"]
 
 
 class DDError(RuntimeError):
@@ -92,6 +92,7 @@ def load():
     lib.dd_nccl_unique_id.argtypes = [P]; lib.dd_nccl_unique_id.restype = I
     lib.dd_inner_iterations.argtypes = [P, P]; lib.dd_inner_iterations.restype = I
     lib.dd_bulk_solve.argtypes = [P, I, P, P, P, D, I, I, P, P]; lib.dd_bulk_solve.restype = I
+    lib.dd_bulk_pcg_solve.argtypes = [P, I, P, P, P, D, I, P, P]; lib.dd_bulk_pcg_solve.restype = I
     lib.dd_test_dgemm.argtypes = [I, I, I, P, I, P, I, P, I, I, P]; lib.dd_test_dgemm.restype = I
     _lib = lib
     return lib
@@ -228,6 +229,23 @@ class Solver:
         iters = np.zeros(ncols, dtype=np.int32); rel = np.zeros(ncols)
         st = load().dd_bulk_solve(self._h, ncols, _ptr(cp), _ptr(b), _ptr(x), float(rtol), int(maxit), int(norm_kind),
                                   iters.ctypes.data, rel.ctypes.data)
+        _check(st, allow=(DD_ENOCONV,))
+        return SolveResult(x, iters, rel, None, st)
+
+    def bulk_pcg_solve(self, b, col_param, x=None, rtol=1e-10, maxit=500):
+        """PCG on the bulk system with the Eq.(5) DD preconditioner (dd_bulk_pcg_solve, 2D)."""
+        t = self._torch
+        n = self.N - 1
+        if not isinstance(b, t.Tensor):
+            b = t.as_tensor(_f64(b), device=self.device)
+        assert b.dtype == t.float64 and b.is_contiguous() and b.device == self.device
+        assert b.dim() == 2 and b.shape[1] == n * n + n
+        ncols = b.shape[0]
+        x = t.empty_like(b) if x is None else x
+        cp = self._cols(col_param)
+        iters = np.zeros(ncols, dtype=np.int32); rel = np.zeros(ncols)
+        st = load().dd_bulk_pcg_solve(self._h, ncols, _ptr(cp), _ptr(b), _ptr(x), float(rtol), int(maxit),
+                                      iters.ctypes.data, rel.ctypes.data)
         _check(st, allow=(DD_ENOCONV,))
         return SolveResult(x, iters, rel, None, st)
 

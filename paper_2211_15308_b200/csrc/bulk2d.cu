@@ -139,3 +139,138 @@ cudaError_t bulk_out(int n, int ldf, int ncols, const double* slab, const double
 }
 
 }  // namespace dd
+
+// ------------------------------------------------------------------------------------------------
+// PCG on the bulk system with the DD preconditioner Eq.(5) (the
+// paper's own protocol).  Bulk vectors use the dd_bulk_solve layout
+// (column c at c*nb: interior nodes x-major, then Γ), nb = n^2 + n.
+namespace dd {
+
+// y = 𝒜 x = K A_h x + γ T^T F T x:   interior rows: K (4 x_ij - x_i±1,j - x_i,j±1) (i = 1 couples
+// to the Γ node (0, j)); Γ rows: K (2 x_j - x_j±1 / 2 - x_1j) + γ (F xΓ)_j  (SURVEY §8 verified
+// stencils; Dirichlet elsewhere).  fx: F xΓ (ld ldfx), computed by the GEMM core beforehand.
+__global__ void k_bulk_apply(int n, int ncols, const double* __restrict__ x, long long nb, const double* __restrict__ fx,
+                             int ldfx, const int* __restrict__ col_param, int n_param, const double* __restrict__ Kp,
+                             const double* __restrict__ gp, double* __restrict__ y) {
+    const long long total = nb * ncols;
+    const long long nn = (long long)n * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(idx / nb);
+        const long long r = idx % nb;
+        int p = col_param[c];
+        p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
+        const double* xc = x + (size_t)c * nb;
+        const double* xg = xc + nn;
+        double v;
+        if (r < nn) {
+            const int i = (int)(r / n), j = (int)(r % n);
+            const double up = i > 0 ? xc[r - n] : xg[j];            // i = 1 row couples to Γ node (0, j)
+            const double dn = i + 1 < n ? xc[r + n] : 0.0;
+            const double lf = j > 0 ? xc[r - 1] : 0.0;
+            const double rt = j + 1 < n ? xc[r + 1] : 0.0;
+            v = Kp[p] * (4.0 * xc[r] - up - dn - lf - rt);
+        } else {
+            const int j = (int)(r - nn);
+            const double lf = j > 0 ? xg[j - 1] : 0.0;
+            const double rt = j + 1 < n ? xg[j + 1] : 0.0;
+            v = fma(gp[p], fx[(size_t)c * ldfx + j], Kp[p] * (2.0 * xg[j] - 0.5 * (lf + rt) - xc[j]));
+        }
+        y[(size_t)c * nb + r] = v;
+    }
+}
+
+__device__ __forceinline__ double bpcg_block_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); q++) s += red[q];   // fixed order: deterministic
+    __syncthreads();
+    return s;
+}
+
+// one CTA per column: α = ρ / p·q; x += α p; r -= α q  (active columns)
+__global__ void k_bpcg_a(long long nb, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                         const double* __restrict__ q, const double* __restrict__ rho, int* __restrict__ active,
+                         int* __restrict__ status) {
+    __shared__ double red[32];
+    const int c = blockIdx.x;
+    if (!active[c]) return;
+    const size_t off = (size_t)c * nb;
+    double pq = 0.0;
+    for (long long i = threadIdx.x; i < nb; i += blockDim.x) pq = fma(p[off + i], q[off + i], pq);
+    pq = bpcg_block_sum(pq, red);
+    if (!(pq > 0.0)) {
+        if (threadIdx.x == 0) { atomicExch(status, (int)DD_ENOTSPD); active[c] = 0; }
+        return;
+    }
+    const double alpha = rho[c] / pq;
+    for (long long i = threadIdx.x; i < nb; i += blockDim.x) {
+        x[off + i] = fma(alpha, p[off + i], x[off + i]);
+        r[off + i] = fma(-alpha, q[off + i], r[off + i]);
+    }
+}
+
+// one CTA per column after z = B r:  ρ' = r·z; η test; β = ρ'/ρ; p = z + β p.  init: p = z, η0.
+__global__ void k_bpcg_b(long long nb, const double* __restrict__ r, const double* __restrict__ z, double* __restrict__ p,
+                         double* __restrict__ rho, double* __restrict__ eta0, double* __restrict__ relres,
+                         int* __restrict__ active, int* __restrict__ iters, int k, double rtol, int maxit, int init,
+                         int* __restrict__ n_active, int* __restrict__ status) {
+    __shared__ double red[32];
+    const int c = blockIdx.x;
+    if (!init && !active[c]) return;
+    const size_t off = (size_t)c * nb;
+    double rz = 0.0;
+    for (long long i = threadIdx.x; i < nb; i += blockDim.x) rz = fma(r[off + i], z[off + i], rz);
+    rz = bpcg_block_sum(rz, red);
+    const double eta = sqrt(fmax(rz, 0.0));
+    if (init) {
+        for (long long i = threadIdx.x; i < nb; i += blockDim.x) p[off + i] = z[off + i];
+        if (threadIdx.x == 0) {
+            eta0[c] = eta; rho[c] = rz; iters[c] = 0; relres[c] = eta > 0.0 ? 1.0 : 0.0;
+            if (rz < 0.0) atomicExch(status, (int)DD_ENOTSPD);
+            const bool act = eta > 0.0 && rz >= 0.0;
+            active[c] = act;
+            if (act) atomicAdd(n_active, 1);
+        }
+        return;
+    }
+    const bool conv = eta <= rtol * eta0[c];
+    if (threadIdx.x == 0) {
+        iters[c] = k;
+        relres[c] = eta0[c] > 0.0 ? eta / eta0[c] : 0.0;
+        if (rz < 0.0) atomicExch(status, (int)DD_ENOTSPD);
+    }
+    if (conv || rz < 0.0 || k >= maxit) {
+        if (threadIdx.x == 0) active[c] = 0;
+        return;
+    }
+    const double beta = rz / rho[c];
+    for (long long i = threadIdx.x; i < nb; i += blockDim.x) p[off + i] = fma(beta, p[off + i], z[off + i]);
+    __syncthreads();
+    if (threadIdx.x == 0) { rho[c] = rz; atomicAdd(n_active, 1); }
+}
+
+cudaError_t bulk_apply(int n, int ncols, const double* x, long long nb, const double* fx, int ldfx, const int* col_param,
+                       int n_param, const double* Kp, const double* gp, double* y, cudaStream_t st) {
+    k_bulk_apply<<<grid_for(nb * ncols), 256, 0, st>>>(n, ncols, x, nb, fx, ldfx, col_param, n_param, Kp, gp, y);
+    return cudaGetLastError();
+}
+cudaError_t bpcg_a(int ncols, long long nb, double* x, double* r, const double* p, const double* q, const double* rho,
+                   int* active, int* status, cudaStream_t st) {
+    k_bpcg_a<<<ncols, 1024, 0, st>>>(nb, x, r, p, q, rho, active, status);
+    return cudaGetLastError();
+}
+cudaError_t bpcg_b(int ncols, long long nb, const double* r, const double* z, double* p, double* rho, double* eta0,
+                   double* relres, int* active, int* iters, int k, double rtol, int maxit, int init, int* n_active,
+                   int* status, cudaStream_t st) {
+    k_bpcg_b<<<ncols, 1024, 0, st>>>(nb, r, z, p, rho, eta0, relres, active, iters, k, rtol, maxit, init, n_active,
+                                      status);
+    return cudaGetLastError();
+}
+
+}  // namespace dd

@@ -714,49 +714,48 @@ extern "C" dd_status dd_pcg_solve_host(dd_ctx* c, int ncols, const int* colp_h, 
 }
 
 // ------------------------------------------------------------------------------------ bulk solve
-// Full DD solve on a bulk right-hand side (2D; bulk2d.cu has the algebra).
-extern "C" dd_status dd_bulk_solve(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol,
-                                   int maxit, int norm_kind, int* iters, double* rel_res) {
-    dd_status s = check_cols(c, ncols, colp);
-    if (s != DD_OK) return s;
-    if (c->dim != 2) return fail(DD_EUNSUPPORTED, "bulk solve: 2D handles only");
-    if (ncols > 0 && (!b || !x)) return fail(DD_EINVAL, "b/x NULL");
-    if (!(rtol >= 0.0) || maxit < 0 || (norm_kind != 0 && norm_kind != 1)) return fail(DD_EINVAL, "rtol/maxit/norm_kind");
-    if (ncols == 0) return DD_OK;
-    CK(cudaSetDevice(c->device));
+// Block elimination on bulk vectors (bulk2d.cu has the algebra):
+//   exact = true : x = 𝒜^-1 b with the interface system solved by the Schur PCG (dd_bulk_solve)
+//   exact = false: x = 𝓑 b, the DD preconditioner Eq.(5) with S_Γ^-1 realised by the RA pole sum
+static dd_status bulk_ensure(dd_ctx* c) {
     const int n = c->n, ldf = c->Kpad;
     const long long NP = (long long)ldf * ldf;
-    if (!c->bulk_a) {
-        // workspaces (first use): two slab buffers, 1/(σ_a + σ_b), skinny vectors
-        // + 64 padded rows: the slab GEMM reads A rows up to round_up(n, 64) of the last slab
-        const size_t slab_tot = (size_t)NP * c->max_cols + (size_t)64 * ldf;
-        CK(dalloc(c, &c->bulk_a, slab_tot));
-        CK(dalloc(c, &c->bulk_b, slab_tot));
-        CK(dalloc(c, &c->bulk_sinv, (size_t)NP));
-        CK(dalloc(c, &c->bulk_g, (size_t)ldf * c->cols_pad));
-        CK(dalloc(c, &c->bulk_w, (size_t)ldf * c->cols_pad));
-        CK(dalloc(c, &c->bulk_gv, (size_t)n * c->max_cols));
-        CK(dalloc(c, &c->bulk_xg, (size_t)n * c->max_cols));
-        CK(cudaMemsetAsync(c->bulk_a, 0, sizeof(double) * slab_tot, c->stream));
-        CK(cudaMemsetAsync(c->bulk_b, 0, sizeof(double) * slab_tot, c->stream));
-        CK(cudaMemsetAsync(c->bulk_g, 0, sizeof(double) * (size_t)ldf * c->cols_pad, c->stream));
-        CK(cudaMemsetAsync(c->bulk_w, 0, sizeof(double) * (size_t)ldf * c->cols_pad, c->stream));
-        const long double PI = 3.141592653589793238462643383279502884L;
-        std::vector<long double> sig(n);
-        for (int a = 0; a < n; a++) {
-            const long double sh = sinl(PI * (a + 1) / (2.0L * c->N));
-            sig[a] = 4.0L * sh * sh;                      // 5-point mode value 2 - 2cos θ
-        }
-        std::vector<double> h((size_t)NP, 0.0);
-        for (int a = 0; a < n; a++)
-            for (int bb = 0; bb < n; bb++) h[(size_t)a * ldf + bb] = (double)(1.0L / (sig[a] + sig[bb]));
-        CK(cudaMemcpyAsync(c->bulk_sinv, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+    if (c->bulk_a) return DD_OK;
+    // + 64 padded rows: the slab GEMM reads A rows up to round_up(n, 64) of the last slab
+    const size_t slab_tot = (size_t)NP * c->max_cols + (size_t)64 * ldf;
+    CK(dalloc(c, &c->bulk_a, slab_tot));
+    CK(dalloc(c, &c->bulk_b, slab_tot));
+    CK(dalloc(c, &c->bulk_sinv, (size_t)NP));
+    CK(dalloc(c, &c->bulk_g, (size_t)ldf * c->cols_pad));
+    CK(dalloc(c, &c->bulk_w, (size_t)ldf * c->cols_pad));
+    CK(dalloc(c, &c->bulk_gv, (size_t)n * c->max_cols));
+    CK(dalloc(c, &c->bulk_xg, (size_t)n * c->max_cols));
+    CK(cudaMemsetAsync(c->bulk_a, 0, sizeof(double) * slab_tot, c->stream));
+    CK(cudaMemsetAsync(c->bulk_b, 0, sizeof(double) * slab_tot, c->stream));
+    CK(cudaMemsetAsync(c->bulk_g, 0, sizeof(double) * (size_t)ldf * c->cols_pad, c->stream));
+    CK(cudaMemsetAsync(c->bulk_w, 0, sizeof(double) * (size_t)ldf * c->cols_pad, c->stream));
+    const long double PI = 3.141592653589793238462643383279502884L;
+    std::vector<long double> sig(n);
+    for (int a = 0; a < n; a++) {
+        const long double sh = sinl(PI * (a + 1) / (2.0L * c->N));
+        sig[a] = 4.0L * sh * sh;                      // 5-point mode value 2 - 2cos θ
     }
+    std::vector<double> h((size_t)NP, 0.0);
+    for (int a = 0; a < n; a++)
+        for (int bb = 0; bb < n; bb++) h[(size_t)a * ldf + bb] = (double)(1.0L / (sig[a] + sig[bb]));
+    CK(cudaMemcpyAsync(c->bulk_sinv, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return DD_OK;
+}
+
+static dd_status bulk_eliminate(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, bool exact,
+                                double rtol, int maxit, int norm_kind, int* iters, double* rel_res) {
+    const int n = c->n, ldf = c->Kpad;
+    dd_status es = bulk_ensure(c);
+    if (es != DD_OK) return es;
     const long long nb = (long long)n * n + n;
     const double* S = c->W;               // S_dst: rows of W, row stride lda
     const double* s1 = c->W;              // S[1, :]
-    TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
     // Ŷ = (S B0 S) / Σ,  bΓ -> bulk_g
     TIMED(DD_KCLASS_OTHER, bulk_in(n, ldf, ncols, b, nb, c->bulk_a, c->bulk_g, ldf, c->stream));
     TIMED(DD_KCLASS_GEMM_DST, bulk_slab_pass(c->bulk_a, c->bulk_b, ncols, n, ldf, S, c->lda, nullptr, c->stream));
@@ -774,9 +773,15 @@ extern "C" dd_status dd_bulk_solve(dd_ctx* c, int ncols, const int* colp, const 
         ga.num_sms = c->num_sms; ga.epi = EPI_ADD;
         TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(ga, c->stream));
     }
-    // xΓ = S^-1 g   (the Schur PCG)
-    dd_status ps = dd_pcg_solve(c, ncols, colp, c->bulk_gv, c->bulk_xg, rtol, maxit, norm_kind, iters, rel_res, nullptr);
-    if (ps != DD_OK && ps != DD_ENOCONV) return ps;
+    dd_status ps = DD_OK;
+    if (exact) {
+        // xΓ = S^-1 g   (the Schur PCG)
+        ps = dd_pcg_solve(c, ncols, colp, c->bulk_gv, c->bulk_xg, rtol, maxit, norm_kind, iters, rel_res, nullptr);
+        if (ps != DD_OK && ps != DD_ENOCONV) return ps;
+    } else {
+        // zΓ = P g   (Eq.(5)'s S_Γ^-1 by the RA pole sum, Eq.(8))
+        TIMED(DD_KCLASS_POLESUM, launch_precond(ncols, colp, c->geom, c->tabs, c->bulk_gv, n, c->bulk_xg, n, c->stream));
+    }
     // u = S xΓ;  x̂0 = Ŷ / K + (s1 ⊗ u) / Σ;  x0 = S x̂0 S
     TIMED(DD_KCLASS_OTHER, launch_copy_cols(n, ncols, c->bulk_xg, n, c->bulk_g, ldf, c->stream));
     {
@@ -794,8 +799,95 @@ extern "C" dd_status dd_bulk_solve(dd_ctx* c, int ncols, const int* colp, const 
     TIMED(DD_KCLASS_GEMM_DST, bulk_slab_pass(c->bulk_a, c->bulk_b, ncols, n, ldf, S, c->lda, nullptr, c->stream));
     TIMED(DD_KCLASS_GEMM_DST, bulk_slab_pass(c->bulk_b, c->bulk_a, ncols, n, ldf, S, c->lda, nullptr, c->stream));
     TIMED(DD_KCLASS_OTHER, bulk_out(n, ldf, ncols, c->bulk_a, c->bulk_xg, n, x, nb, c->stream));
+    return ps;
+}
+
+static dd_status bulk_check(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
+                            int norm_kind) {
+    dd_status s = check_cols(c, ncols, colp);
+    if (s != DD_OK) return s;
+    if (c->dim != 2) return fail(DD_EUNSUPPORTED, "bulk solves: 2D handles only");
+    if (ncols > 0 && (!b || !x)) return fail(DD_EINVAL, "b/x NULL");
+    if (!(rtol >= 0.0) || maxit < 0 || (norm_kind != 0 && norm_kind != 1)) return fail(DD_EINVAL, "rtol/maxit/norm_kind");
+    return DD_OK;
+}
+
+extern "C" dd_status dd_bulk_solve(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol,
+                                   int maxit, int norm_kind, int* iters, double* rel_res) {
+    dd_status s = bulk_check(c, ncols, colp, b, x, rtol, maxit, norm_kind);
+    if (s != DD_OK || ncols == 0) return s;
+    CK(cudaSetDevice(c->device));
+    TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
+    dd_status ps = bulk_eliminate(c, ncols, colp, b, x, true, rtol, maxit, norm_kind, iters, rel_res);
+    if (ps != DD_OK && ps != DD_ENOCONV) return ps;
     CK(cudaStreamSynchronize(c->stream));
     return ps;
+}
+
+// PCG on the bulk system 𝒜 x = b preconditioned by 𝓑 (Eq.(5)), x0 = 0, stop on a 1e10-type
+// reduction of the preconditioned residual norm sqrt(r·𝓑r) (reading A1).
+extern "C" dd_status dd_bulk_pcg_solve(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol,
+                                       int maxit, int* iters, double* rel_res) {
+    dd_status s = bulk_check(c, ncols, colp, b, x, rtol, maxit, 0);
+    if (s != DD_OK || ncols == 0) return s;
+    if (c->frac_mode != DD_FRAC_DENSE) return fail(DD_EUNSUPPORTED, "bulk PCG: dense fractional term only");
+    CK(cudaSetDevice(c->device));
+    const int n = c->n, ldf = c->Kpad;
+    const long long nb = (long long)n * n + n;
+    if (!c->bpcg_r) {
+        for (double** v : {&c->bpcg_r, &c->bpcg_p, &c->bpcg_q, &c->bpcg_z}) CK(dalloc(c, v, (size_t)nb * c->max_cols));
+    }
+    CK(cudaMemsetAsync(c->ints, 0, sizeof(int) * 8, c->stream));
+    TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)nb * ncols, c->stream));
+    CK(cudaMemcpyAsync(c->bpcg_r, b, sizeof(double) * (size_t)nb * ncols, cudaMemcpyDeviceToDevice, c->stream));
+    auto apply_A = [&](const double* in, double* out) -> dd_status {
+        // F xΓ through the dense F block of W (padded copy of xΓ first), then the stencil kernel
+        TIMED(DD_KCLASS_OTHER, launch_copy_cols(n, ncols, in + (size_t)n * n, (int)nb, c->bulk_g, ldf, c->stream));
+        GemmArgs ga{};
+        ga.M = n; ga.N = ncols; ga.K = ldf;
+        ga.A = c->W + ldf; ga.lda = c->lda;
+        ga.B = c->bulk_g; ga.ldb = ldf;
+        ga.C = c->bulk_w; ga.ldc = ldf;
+        ga.splitk = gemm_pick_splitk(n, ncols, ldf, c->num_sms); ga.ws = c->gws; ga.counters = c->gcnt;
+        ga.num_sms = c->num_sms; ga.epi = EPI_STORE;
+        TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(ga, c->stream));
+        TIMED(DD_KCLASS_OTHER, bulk_apply(n, ncols, in, nb, c->bulk_w, ldf, colp, c->n_param, c->Kp, c->gp, out,
+                                          c->stream));
+        return DD_OK;
+    };
+    dd_status st;
+    if ((st = bulk_ensure(c)) != DD_OK) return st;
+    if ((st = bulk_eliminate(c, ncols, colp, c->bpcg_r, c->bpcg_z, false, 0, 0, 0, nullptr, nullptr)) != DD_OK) return st;
+    TIMED(DD_KCLASS_OTHER, bpcg_b(ncols, nb, c->bpcg_r, c->bpcg_z, c->bpcg_p, c->rho, c->eta0, c->relres, c->active,
+                                  c->iters, 0, rtol, maxit, 1, c->ints + 1, c->ints + 4, c->stream));
+    int k = 0;
+    for (k = 1; k <= maxit; k++) {
+        if ((st = apply_A(c->bpcg_p, c->bpcg_q)) != DD_OK) return st;
+        TIMED(DD_KCLASS_OTHER, bpcg_a(ncols, nb, x, c->bpcg_r, c->bpcg_p, c->bpcg_q, c->rho, c->active, c->ints + 4,
+                                      c->stream));
+        if ((st = bulk_eliminate(c, ncols, colp, c->bpcg_r, c->bpcg_z, false, 0, 0, 0, nullptr, nullptr)) != DD_OK)
+            return st;
+        CK(cudaMemsetAsync(c->ints + 1, 0, sizeof(int), c->stream));
+        TIMED(DD_KCLASS_OTHER, bpcg_b(ncols, nb, c->bpcg_r, c->bpcg_z, c->bpcg_p, c->rho, c->eta0, c->relres, c->active,
+                                      c->iters, k, rtol, maxit, 0, c->ints + 1, c->ints + 4, c->stream));
+        CK(cudaMemcpyAsync(c->h_ints, c->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (c->h_ints[1] == 0 || c->h_ints[4] != 0) break;
+    }
+    if (iters) CK(cudaMemcpyAsync(iters, c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c->stream));
+    if (rel_res) CK(cudaMemcpyAsync(rel_res, c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_ints, c->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->h_ints[5]) return fail(DD_EINVAL, "col_param entry out of range (clamped; outputs undefined)");
+    if (c->h_ints[4] == DD_ENOTSPD) return fail(DD_ENOTSPD, "p.Ap <= 0 or r.Br < 0 in the bulk PCG");
+    std::vector<int> itv(ncols);
+    std::vector<double> rr(ncols);
+    CK(cudaMemcpy(itv.data(), c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rr.data(), c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < ncols; i++)
+        if (itv[i] >= maxit && !(rr[i] <= rtol)) return fail(DD_ENOCONV, "maxit reached");
+    return DD_OK;
 }
 
 extern "C" dd_status dd_destroy(dd_ctx* c) {

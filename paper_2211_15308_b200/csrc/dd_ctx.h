@@ -89,6 +89,7 @@ struct dd_ctx {
     // full DD bulk solve (2D, dd_bulk_solve; allocated on first use)
     double *bulk_a = nullptr, *bulk_b = nullptr, *bulk_sinv = nullptr, *bulk_g = nullptr, *bulk_w = nullptr;
     double *bulk_gv = nullptr, *bulk_xg = nullptr;
+    double *bpcg_r = nullptr, *bpcg_p = nullptr, *bpcg_q = nullptr, *bpcg_z = nullptr;   // bulk PCG vectors
     // operator data (2D)
     double* W = nullptr;      // Mpad x 2 Kpad row-major: [S_dst | 0 | F | 0]
     double* sw = nullptr;     // Schur weights s_b

@@ -133,6 +133,14 @@ cudaError_t bulk_update(int n, int ldf, int ncols, double* Yh, const double* s1,
 cudaError_t bulk_out(int n, int ldf, int ncols, const double* slab, const double* xg, int ldg, double* x, long long ldx,
                      cudaStream_t st);
 
+cudaError_t bulk_apply(int n, int ncols, const double* x, long long nb, const double* fx, int ldfx, const int* col_param,
+                       int n_param, const double* Kp, const double* gp, double* y, cudaStream_t st);
+cudaError_t bpcg_a(int ncols, long long nb, double* x, double* r, const double* p, const double* q, const double* rho,
+                   int* active, int* status, cudaStream_t st);
+cudaError_t bpcg_b(int ncols, long long nb, const double* r, const double* z, double* p, double* rho, double* eta0,
+                   double* relres, int* active, int* iters, int k, double rtol, int maxit, int init, int* n_active,
+                   int* status, cudaStream_t st);
+
 // ----------------------------------------------------------------------------- 3D face (face3d.cu)
 struct InnerArgs {
     int n, ldf; long long NP;

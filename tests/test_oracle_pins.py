@@ -576,3 +576,32 @@ def test_ra_evaluated_fractional_term(t, sigma):
     X = np.random.default_rng(2).uniform(-1, 1, (n, 3))
     a, b = D.apply_S(1.0, 1e2, X), Mo.apply_S(1.0, 1e2, X)
     assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
+
+
+def test_bulk_pcg_dd_preconditioner():
+    # Eq.(5), the paper's protocol (PCG on the bulk system):
+    # (i) with S_Γ = the exact Schur complement, 𝓑 = 𝒜^-1 and PCG converges in ONE iteration
+    # (SPEC.md acceptance 1); (ii) with the RA S_Γ^-1, the bulk PCG iteration count equals the
+    # interface (Schur) PCG's ±1 (the preconditioned spectrum is {1} ∪ spec(P S)) and the solution
+    # is the direct one.
+    N = 12
+    Bs = obulk.BulkSystem(2, N)
+    D = problem.DenseProblem(2, N)
+    lo, hi = rafit.interval_1d(N)
+    b = np.random.default_rng(31).uniform(-1, 1, Bs.A.shape[0])
+    for K, gam in [(1.0, 1e2), (1e-3, 1.0)]:
+        Sd = D.S(K, gam)
+        x, it, rel, hist, conv = pcg.pcg(lambda v: Bs.apply(K, gam, v),
+                                         lambda v: Bs.dd_precond(K, lambda w: np.linalg.solve(Sd, w), v), b)
+        assert conv and it == 1
+        xd = Bs.solve(K, gam, b)
+        assert np.linalg.norm(x - xd) <= 1e-10 * np.linalg.norm(xd)
+        fit = rafit.fit_ra(K, gam, lo, hi, 10)
+        P = lambda w: D.apply_P_ra(fit.c0, fit.poles, fit.residues, w)
+        x, it, rel, hist, conv = pcg.pcg(lambda v: Bs.apply(K, gam, v), lambda v: Bs.dd_precond(K, P, v), b)
+        assert conv and np.linalg.norm(x - xd) <= 1e-8 * np.linalg.norm(xd)
+        # interface PCG on the reduced right-hand side g = bΓ - A^{i0} (A^00)^-1 b0
+        lu, A0i, Ai0 = Bs._lu00(K)
+        gvec = b[:Bs.g] - Ai0 @ lu.solve(b[Bs.g:])
+        _, its, *_ = pcg.pcg(lambda v: D.apply_S(K, gam, v), P, gvec)
+        assert abs(it - its) <= 1, (it, its)
