@@ -60,7 +60,10 @@ typedef struct {
 
 typedef struct {
     int rank, world;              /* this process's rank / number of ranks                 */
-    const void* nccl_unique_id;   /* 128-byte ncclUniqueId (broadcast by the caller)         */
+    const void* nccl_unique_id;   /* 128-byte ncclUniqueId (broadcast by the caller); NULL with
+                                     DD_SHARD_POLES: no communicator — dd_apply_precond returns
+                                     this rank's partial pole sum (emulating ranks in one process
+                                     for tests; dd_pcg_solve then is NOT the global solve)     */
     int mode;                     /* DD_SHARD_COLUMNS or DD_SHARD_POLES                      */
 } dd_dist;
 #define DD_SHARD_COLUMNS 0        /* each rank passes its own columns; no collective        */

@@ -153,8 +153,10 @@ class Solver:
         dptr = None
         if dist is not None:
             rank, world, mode, uid = dist
-            self._uid = ctypes.create_string_buffer(bytes(uid) if uid is not None else bytes(128), 128)
-            self._dist = _Dist(int(rank), int(world), ctypes.cast(self._uid, ctypes.c_void_p), int(mode))
+            # uid None: no communicator (pole split: this rank's partial sums; see dd_api.h dd_dist)
+            self._uid = ctypes.create_string_buffer(bytes(uid), 128) if uid is not None else None
+            self._dist = _Dist(int(rank), int(world),
+                               ctypes.cast(self._uid, ctypes.c_void_p) if uid is not None else None, int(mode))
             dptr = ctypes.byref(self._dist)
         fr = frac if frac is not None else Frac()
         self.frac = fr

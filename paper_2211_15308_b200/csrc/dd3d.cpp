@@ -225,8 +225,7 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
     if (const char* it = std::getenv("DD_INNER_MAXIT")) f.inner_maxit = std::max(1, atoi(it));
 
     // --- NCCL communicator for the pole split (bootstrapped by the caller's unique id)
-    if (f.world > 1 && dist->mode == DD_SHARD_POLES) {
-        if (!dist->nccl_unique_id) return set_error(DD_EINVAL, "pole split needs an ncclUniqueId");
+    if (f.world > 1 && dist->mode == DD_SHARD_POLES && dist->nccl_unique_id) {
         ncclUniqueId id;
         std::memcpy(&id, dist->nccl_unique_id, sizeof(id));
         ncclComm_t comm = nullptr;

@@ -114,3 +114,28 @@ def test_full_size_3d_properties(lib):
 def test_nccl_unique_id(lib):
     a = lib.nccl_unique_id(); b = lib.nccl_unique_id()
     assert len(a) == 128 and a != b
+
+
+def test_pole_split_partials_sum_to_full(lib):
+    """Row a-6: the pole split assigns every RA system to exactly one rank
+    (LPT by predicted inner-CG cost); with no communicator (nccl_unique_id NULL) each rank's handle
+    returns its partial pole sum, and the partials of ranks 0..W-1 add up to the single-GPU
+    preconditioner — the allreduce's input, emulated in one process without waiting kernels."""
+    N = 16; n = N - 1
+    params = [(1.0, 1e4)]
+    ras = _fit(N, params, 10)
+    B = torch.as_tensor(np.random.default_rng(8).uniform(-1, 1, (2, n * n)), device="cuda")
+    full = lib.Solver(3, N, params, ras, max_cols=2, device=0)
+    try:
+        zf = full.apply_precond(B, [0, 0]).cpu().numpy()
+    finally:
+        full.close()
+    for world in (2, 3):
+        acc = np.zeros_like(zf)
+        for rank in range(world):
+            S = lib.Solver(3, N, params, ras, max_cols=2, device=0, dist=(rank, world, 1, None))
+            try:
+                acc += S.apply_precond(B, [0, 0]).cpu().numpy()
+            finally:
+                S.close()
+        assert rel_l2_cols(acc, zf) <= 1e-12 * max(1.0, ras[0].cancel)
