@@ -66,11 +66,14 @@ class ModeProblem2D:
         a_d, a_o, m_d, m_o = fem.trace_pair_1d(N)
         # uniform mesh: constant Toeplitz entries; mode value = diag + 2 off cos θ_b
         assert np.allclose(a_d, a_d[0]) and np.allclose(m_d, m_d[0])
-        c = schur._cos_theta(n)
+        k = np.arange(1, n + 1)
+        cm1 = -2.0 * np.sin(0.5 * np.pi * k / (n + 1)) ** 2     # cos θ_b - 1 without cancellation (A18)
         ao = a_o[0] if n > 1 else 0.0
         mo = m_o[0] if n > 1 else 0.0
-        self.alpha = a_d[0] + 2.0 * ao * c          # A_Γ mode values
-        self.mu = m_d[0] + 2.0 * mo * c             # M_Γ mode values
+        # mode value diag + 2 off cos θ written as (diag + 2 off) + 2 off (cos θ - 1): for A_Γ the first
+        # bracket vanishes and the low modes keep full relative precision (reading A26)
+        self.alpha = (a_d[0] + 2.0 * ao) + 2.0 * ao * cm1   # A_Γ mode values
+        self.mu = (m_d[0] + 2.0 * mo) + 2.0 * mo * cm1      # M_Γ mode values
         self.lam = self.alpha / self.mu             # generalised eigenvalues of (A_Γ, M_Γ)
         self.s = schur.schur_modes_2d(N)            # S_unit mode values
         self.f = self.mu * (self.lam + sigma) ** t  # F mode values: (MU) (Λ+σ)^t (MU)^T

@@ -77,17 +77,20 @@ def schur_modes_2d(N: int) -> np.ndarray:
     """Eigenvalues s_b of S_unit in the orthonormal sine basis along Γ (2D, K = 1).
 
     Stiffness blocks of the Freudenthal P1 mesh in sine mode b (checked against element
-    assembly in tests): interior layer diagonal 4 - 2cos θ_b, inter-layer coupling -1,
-    Γ-row diagonal 2 - cos θ_b.  Layer elimination from the far layer:
-    d <- (4 - 2cos θ_b) - 1/d, starting at d = 4 - 2cos θ_b, N-2 times; s_b = (2 - cos θ_b) - 1/d.
+    assembly in tests): interior layer diagonal 4 - 2cos θ_b = 2 + σ_b, inter-layer coupling -1,
+    Γ-row diagonal 2 - cos θ_b = 1 + σ_b/2.  Layer elimination from the far layer:
+    d <- (2 + σ_b) - 1/d, starting at d = 2 + σ_b, N-2 times; s_b = (1 + σ_b/2) - 1/d.
+    The recursion is carried for e = d - 1 (e <- σ_b + e/(1+e), s_b = σ_b/2 + e/(1+e)), the same
+    elimination without the cancellation d ≈ 1 + √σ_b causes for the low modes (DESIGN.md
+    reading A26: the plain form loses 4.7e-10 in s_1 at N = 8192); σ_b = 4 sin²(θ_b/2) (A18).
     """
     n = N - 1
-    c = _cos_theta(n)
-    diag = 4.0 - 2.0 * c
-    d = diag.copy()
+    k = np.arange(1, n + 1)
+    sig = 4.0 * np.sin(0.5 * np.pi * k / (n + 1)) ** 2
+    e = 1.0 + sig
     for _ in range(N - 2):
-        d = diag - 1.0 / d
-    return (2.0 - c) - 1.0 / d
+        e = sig + e / (1.0 + e)
+    return 0.5 * sig + e / (1.0 + e)
 
 
 def schur_modes_3d(N: int) -> np.ndarray:

@@ -288,3 +288,35 @@ def test_inexact_inner_pcg_parity(lib, cfg):
                 assert np.linalg.norm(x[c] - X[:, j]) <= tol * np.linalg.norm(X[:, j])
     finally:
         S.close()
+
+
+def test_maximum_1d_interface(lib):
+    """The largest 1D interface the pole-sum kernels take (n = 8191: 8-warp groups with 32-row
+    chunks, the LL = 32 instantiation) against the oracle's mode tier."""
+    N = 8192
+    params = [(1.0, 1e2), (1e-4, 1e6)]
+    ras = fit_all(N, params, 20)
+    Mo = oprob.ModeProblem2D(N)
+    C = 4
+    B = np.random.default_rng(81).uniform(-1, 1, (C, N - 1))
+    colp = np.arange(C) % 2
+    S = _solver(lib, N, params, ras, max_cols=C)
+    try:
+        y = S.apply_schur(_cols(B), colp).cpu().numpy()
+        ref_y = np.stack([Mo.apply_S(*params[colp[c]], B[c]) for c in range(C)])
+        assert rel_l2_cols(y, ref_y) <= 1e-10
+        z = S.apply_precond(_cols(B), colp).cpu().numpy()
+        ra = lambda c: ras[colp[c]]
+        zb = np.stack([Mo.apply_P_ra(ra(c).c0, ra(c).poles, ra(c).residues, B[c]) for c in range(C)])
+        ze = np.stack([Mo.apply_P_ra_eigen(ra(c).c0, ra(c).poles, ra(c).residues, B[c]) for c in range(C)])
+        check_precond(z, zb, ze, ras)
+        res = S.pcg_solve(_cols(B), colp)
+        x = res.x.cpu().numpy()
+        for c in range(C):
+            K, g = params[colp[c]]
+            xo, it, *_ = opcg.pcg(lambda v: Mo.apply_S(K, g, v),
+                                  lambda v: Mo.apply_P_ra(ra(c).c0, ra(c).poles, ra(c).residues, v), B[c])
+            assert abs(int(res.iters[c]) - it) <= 1
+            assert np.linalg.norm(x[c] - xo) <= 1e-8 * np.linalg.norm(xo)
+    finally:
+        S.close()
