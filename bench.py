@@ -45,9 +45,9 @@ def _env_int(k, d):
         return d
 
 
-def fit_ras(cfg):
+def fit_ras(cfg, t=-0.5, sigma=0.0):
     lo, hi = rafit.interval_1d(cfg.N) if cfg.dim == 2 else rafit.interval_face(cfg.N)
-    return [rafit.fit_ra(K, g, lo, hi, cfg.n_poles) for K, g in cfg.params]
+    return [rafit.fit_ra(K, g, lo, hi, cfg.n_poles, t=t, sigma=sigma) for K, g in cfg.params]
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -102,12 +102,12 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle
-def oracle_sample(cfg, ras, B, colp, per_param: int):
+def oracle_sample(cfg, ras, B, colp, per_param: int, t: float = -0.5, sigma: float = 0.0):
     """Time the CPU oracle (mode tier: scipy DST + LAPACK banded Cholesky pole solves, PCG per
     column) on `per_param` columns of every parameter set.  Returns (solves, seconds)."""
     from oracle import pcg as opcg
     from oracle import problem as oprob
-    Mo = oprob.ModeProblem2D(cfg.N)
+    Mo = oprob.ModeProblem2D(cfg.N, t=t, sigma=sigma)
     t0 = time.perf_counter()
     solves = 0
     for p, (K, g) in enumerate(cfg.params):
@@ -164,6 +164,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--frac-mode", default="dense", choices=["dense", "ra"],
                     help="fractional term: dense F (Eq.(7)) or RA-evaluated (Remark 1, NEXT-2)")
+    ap.add_argument("--t", type=float, default=-0.5, help="fractional exponent t of γ L^t (Eq.(9); NEXT-3)")
+    ap.add_argument("--shifted", action="store_true", help="L = -Δ_Γ + I_Γ (Eq.(9); NEXT-3)")
     ap.add_argument("--mode", default="schur", choices=["schur", "bulk", "bulk-pcg"],
                     help="schur: interface PCG (headline); bulk: full DD solve on bulk RHS (NEXT-1); "
                          "bulk-pcg: PCG on the bulk system with the Eq.(5) DD preconditioner (the paper's protocol)")
@@ -186,13 +188,15 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    ras = fit_ras(cfg)
+    sigma = 1.0 if args.shifted else 0.0
+    ras = fit_ras(cfg, args.t, sigma)
     B, colp = inputs.batch(cfg.n_gamma, len(cfg.params), cfg.rhs_per_param, seed_offset=rank * len(cfg.params))
     C = B.shape[0]
-    frac = None
+    frac = binding.Frac(t=args.t, shifted=args.shifted)
     if args.frac_mode == "ra":
         lo, hi = rafit.interval_1d(cfg.N) if cfg.dim == 2 else rafit.interval_face(cfg.N)
-        frac = binding.Frac(mode="ra", fra=rafit.fit_power(-0.5, lo, hi, cfg.n_poles))
+        frac = binding.Frac(t=args.t, shifted=args.shifted, mode="ra",
+                            fra=rafit.fit_power(args.t, lo, hi, cfg.n_poles, sigma))
     S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local, frac=frac)
     Bt = torch.as_tensor(B, device=f"cuda:{local}")
     cp = torch.as_tensor(colp.astype(np.int32), device=f"cuda:{local}")
@@ -320,6 +324,8 @@ def main():
                        "parallelism": f"columns sharded, {world} rank(s), no collective",
                        "fractional_term": "dense F (Eq.(7))" if args.frac_mode == "dense"
                        else f"RA-evaluated (Remark 1), {cfg.n_poles} poles",
+                       "t": args.t, "L": "-Δ_Γ + I" if args.shifted else "-Δ_Γ",
+                       "ra_max_rel_err": max(r.rel_err for r in ras),
                        "mean_pcg_iters": round(mean_it, 3), "max_pcg_iters": int(its.max()),
                        "iters_by_param": {"fields": ["K", "mu_inv", "max", "mean"], "rows": by_param}},
             "precond_applies_per_s": round(pa_per_s, 1),
@@ -336,7 +342,7 @@ def main():
                                          "plus a 16129^2 generalised eigensolve (tens of minutes on the host)")
         elif not args.no_cpu_baseline and world == 1:
             per = max(1, int(os.environ.get("DD_ORACLE_PER_PARAM", "64")))
-            solves, secs = oracle_sample(cfg, ras, B, colp, per)
+            solves, secs = oracle_sample(cfg, ras, B, colp, per, args.t, 1.0 if args.shifted else 0.0)
             line["cpu_baseline"] = {"value": round(solves / secs, 4), "unit": UNIT, "cores": cores_used(),
                                     "kind": "oracle",
                                     "sample": f"{solves} of the {C} solves ({per} per parameter set), oracle mode tier "
