@@ -299,6 +299,12 @@ def main():
                     "frac": round(ach_g2 / peak, 4) if ach_g2 else None, "peak_source": peak_src,
                     "flops_per_launch": flops_g2,
                     "step_fp64_frac": round(step_flops / (total_prof_ms / nprof / 1e3) / 1e12 / peak, 4)}
+        elif args.frac_mode == "ra":
+            # 3D, Remark 1: no dense F; the step is the face inner CG (slab DMMA passes + vector updates)
+            roof = {"bound": "tensor", "kernel": "3D RA mode: face inner-CG slab passes + updates (class polesum_pcg)",
+                    "achieved": None, "peak": fp64_peak()[0], "unit": "TFLOP/s", "frac": None,
+                    "peak_source": fp64_peak()[1],
+                    "note": "no single dominant kernel: inner-CG GEMM passes and memory-bound updates share the step"}
         else:
             # 3D: the dense fractional term F (n_Γ^2 fp64) is streamed once per Schur apply: HBM-bound
             mp = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}

@@ -69,7 +69,11 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
     DD_CK(cudaMemcpyAsync(f.sw, swh.data(), swh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
 
     // --- dense fractional term via the generalised eigenproblem A_Γ U = M_Γ U Λ, U^T M U = I
-    {
+    //     (RA mode, Remark 1: no dense F and no eigensolve; the interval only steers the pole split)
+    if (c->frac_mode != DD_FRAC_DENSE) {
+        f.lam_min = (double)(2.0L * PI_L * PI_L);
+        f.lam_max = (double)(25.85L / (h * h));
+    } else {
         const int n2 = f.n2;
         const int kp = round_up(n2, 16);
         const size_t big = (size_t)round_up(n2, 64) * kp + 1024;
@@ -202,6 +206,43 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
     DD_CK(cudaMemcpyAsync(f.dg, dg.data(), dg.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     DD_CK(cudaMemcpyAsync(f.idg, idg.data(), idg.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
 
+    // --- RA mode: the r_F systems (fc0 M + Σ_k fc_k (A - fp_k M)^-1 ≈ L^t) in the same sine-domain form
+    if (c->frac_mode == DD_FRAC_RA) {
+        std::vector<Sys> fsys;
+        if (c->fra_c0 != 0.0) fsys.push_back({0.0, 1.0, c->fra_c0, 1.0});
+        for (size_t k = 0; k < c->fra_poles.size(); k++)
+            if (c->fra_res[k] != 0.0) fsys.push_back({1.0, -c->fra_poles[k], c->fra_res[k], 1.0});
+        FSet& F = f.fs;
+        F.nsys = (int)fsys.size();
+        const int nf = std::max(1, F.nsys);
+        std::vector<double> fa(nf, 0.0), fb(nf, 1.0), fw(nf, 0.0), fcs(nf, 0.0), fdg((size_t)nf * f.NP, 0.0),
+            fidg((size_t)nf * f.NP, 0.0);
+        for (int i = 0; i < F.nsys; i++) {
+            const Sys& sy = fsys[i];
+            fa[i] = sy.a; fb[i] = sy.b; fw[i] = sy.w;
+            fcs[i] = (double)((long double)sy.b * h * h / 24.0L);
+            for (int a = 0; a < n; a++)
+                for (int b = 0; b < n; b++) {
+                    const long double ca = 1.0L - 0.5L * sig[a], cb = 1.0L - 0.5L * sig[b];
+                    const long double alpha = sig[a] + sig[b];
+                    const long double mut = (long double)hh12 * (6.0L + 2.0L * ca + 2.0L * cb + 2.0L * ca * cb);
+                    const long double d = (long double)sy.a * alpha + (long double)sy.b * mut;
+                    fdg[(size_t)i * f.NP + (size_t)a * f.ldf + b] = (double)d;
+                    fidg[(size_t)i * f.NP + (size_t)a * f.ldf + b] = (double)(1.0L / d);
+                }
+        }
+        for (double** v : {&F.sys_a, &F.sys_b, &F.sys_w, &F.cs}) DD_CK(dalloc(c, v, nf));
+        DD_CK(dalloc(c, &F.dg, fdg.size()));
+        DD_CK(dalloc(c, &F.idg, fidg.size()));
+        DD_CK(cudaMemcpyAsync(F.sys_a, fa.data(), nf * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(F.sys_b, fb.data(), nf * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(F.sys_w, fw.data(), nf * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(F.cs, fcs.data(), nf * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(F.dg, fdg.data(), fdg.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(F.idg, fidg.data(), fidg.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaStreamSynchronize(c->stream));
+    }
+
     // --- per-parameter K, γ and workspaces
     DD_CK(dalloc(c, &c->Kp, c->n_param));
     DD_CK(dalloc(c, &c->gp, c->n_param));
@@ -213,6 +254,16 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
     const size_t pairs = (size_t)ns * c->max_cols;
     const size_t pv = (size_t)f.NP * pairs + slack;
     for (double** v : {&f.ix, &f.ir, &f.ip, &f.iq, &f.iz, &f.T1, &f.T2}) DD_CK(dalloc(c, v, pv));
+    if (c->frac_mode == DD_FRAC_RA) {
+        FSet& F = f.fs;
+        const size_t fpv = (size_t)f.NP * std::max(1, F.nsys) * c->max_cols + slack;
+        for (double** v : {&F.ix, &F.ir, &F.ip, &F.iq, &F.iz, &F.T1}) DD_CK(dalloc(c, v, fpv));
+        DD_CK(dalloc(c, &F.irho, (size_t)std::max(1, F.nsys) * c->max_cols));
+        DD_CK(dalloc(c, &F.irho0, (size_t)std::max(1, F.nsys) * c->max_cols));
+        DD_CK(dalloc(c, &F.iactive, (size_t)std::max(1, F.nsys) * c->max_cols));
+        for (double** v : {&F.V1, &F.V2, &F.W1, &F.W2}) DD_CK(dalloc(c, v, vec));
+        DD_CK(dalloc(c, &F.gcol, cp8));
+    }
     DD_CK(dalloc(c, &f.irho, pairs));
     DD_CK(dalloc(c, &f.irho0, pairs));
     DD_CK(dalloc(c, &f.iactive, pairs));
@@ -237,6 +288,10 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
 }
 
 void destroy_3d(dd_ctx* c) {
+    if (c->f3.fs.exec) {
+        cudaGraphExecDestroy(c->f3.fs.exec);
+        c->f3.fs.exec = nullptr;
+    }
     if (c->f3.inner_exec) {
         cudaGraphExecDestroy(c->f3.inner_exec);
         c->f3.inner_exec = nullptr;
@@ -247,16 +302,121 @@ void destroy_3d(dd_ctx* c) {
     }
 }
 
-// y = S x on padded face vectors p -> q
-static dd_status schur_core(dd_ctx* c, int ncols, const int* colp, const double* p, double* q) {
+// One set of shifted face systems Σ_s w_s (a_s A + b_s M)^-1 applied by the batched sine-domain CG:
+// the preconditioner's RA systems (Eq.(8)) or, in RA mode, the fractional term's r_F systems
+// (Remark 1).  W1, W2: NP x ncols scratch for the transforms.
+struct InnerView {
+    int nsys;
+    double *sys_a, *sys_b, *sys_w, *cs, *dg, *idg;
+    double *ix, *ir, *ip, *iq, *iz, *T1, *irho, *irho0;
+    int* iactive;
+    cudaGraphExec_t* exec;
+    int* key;
+    bool* on_dev;
+    int* last_iters;
+    int slot_act, slot_cnt;        // ints[] slots: active-pair counter, iteration counter (+2: total)
+    long long* iter_launches;
+};
+
+static InnerView view_P(Face3& f, dd_ctx* c) {
+    return InnerView{f.nsys, f.sys_a, f.sys_b, f.sys_w, f.cs, f.dg, f.idg, f.ix, f.ir, f.ip, f.iq, f.iz, f.T1,
+                     f.irho, f.irho0, f.iactive, &f.inner_exec, &f.inner_key, &f.inner_iters_on_device,
+                     &f.last_inner_iters, 1, 6, &c->inner_iter_launches};
+}
+static InnerView view_F(Face3& f, dd_ctx* c) {
+    FSet& s = f.fs;
+    return InnerView{s.nsys, s.sys_a, s.sys_b, s.sys_w, s.cs, s.dg, s.idg, s.ix, s.ir, s.ip, s.iq, s.iz, s.T1,
+                     s.irho, s.irho0, s.iactive, &s.exec, &s.key, &s.on_dev, &s.last_iters, 11, 12,
+                     &c->f_inner_iter_launches};
+}
+
+static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const double* r, double* z, double* W1,
+                             double* W2) {
     Face3& f = c->f3;
-    DD_TIMED(DD_KCLASS_OTHER, gather_param(ncols, colp, c->n_param, c->Kp, f.Kcol, c->stream));
-    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(p, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
-    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass_scaled(f.U1, f.U2, ncols, f.n, f.ldf, f.S, f.sw, 0, 1, f.Kcol, c->stream));
-    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U2, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
-    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.S, c->stream));
-    DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, f.NP, p, q, f.U2, ncols, colp, c->n_param, c->gp, f.fx_ws, f.fx_cnt,
-                                           c->num_sms, c->stream));
+    InnerArgs a{};
+    a.n = f.n; a.ldf = f.ldf; a.NP = f.NP;
+    a.npair = v.nsys * ncols; a.C = ncols;
+    a.hh12 = (double)(1.0L / ((long double)c->N * c->N * 12.0L));
+    a.sys_a = v.sys_a; a.sys_b = v.sys_b;
+    a.x = v.ix; a.r = v.ir; a.p = v.ip; a.q = v.iq; a.z = v.iz;
+    a.rho = v.irho; a.rho0 = v.irho0; a.active = v.iactive; a.rtol = f.inner_rtol;
+    a.dg = v.dg; a.idg = v.idg; a.cs = v.cs;
+    int* n_act_slot = c->ints + v.slot_act;
+    int* cnt_slot = c->ints + v.slot_cnt;
+    // r̂_c = Q r_c once per column (2 slab passes)
+    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(r, W1, ncols, f.n, f.ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W1, W2, ncols, f.n, f.ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_POLESUM, inner_init_hat(a, W2, c->stream));
+    auto body = [&](cudaStream_t st, int* n_act) -> dd_status {
+        // q̂ = dg ∘ p̂ + cs D̂ p̂ D̂^T on the active pairs, then the fused CG update
+        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_active(v.ip, v.T1, a.npair, f.n, f.ldf, f.Dh, v.iactive, st));
+        DD_TIMED(DD_KCLASS_POLESUM, face_inner_op_pass(v.T1, v.iq, v.ip, a.npair, ncols, f.n, f.ldf, f.Dh, v.dg, v.cs,
+                                                       v.iactive, st));
+        DD_TIMED(DD_KCLASS_POLESUM, inner_update_hat(a, n_act, st));
+        return DD_OK;
+    };
+    if (c->graph_ok && !c->prof) {
+        // the whole inner loop as one conditional WHILE graph (no host round trips)
+        if (!*v.exec || *v.key != ncols) {
+            if (*v.exec) cudaGraphExecDestroy(*v.exec);
+            *v.exec = nullptr;
+            cudaGraph_t g = nullptr;
+            DD_CK(cudaGraphCreate(&g, 0));
+            cudaGraphConditionalHandle h;
+            DD_CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t node;
+            DD_CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+            cudaStream_t cap = nullptr;
+            DD_CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            DD_CK(cudaStreamBeginCaptureToGraph(cap, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                cudaStreamCaptureModeRelaxed));
+            const bool prof = c->prof;
+            c->prof = false;
+            const long long l0 = c->launches;
+            dd_status bs = body(cap, n_act_slot);
+            cudaError_t ce = inner_cond(n_act_slot, cnt_slot, f.inner_maxit, (unsigned long long)h, cap);
+            *v.iter_launches = c->launches - l0 + 1;
+            c->launches = l0;
+            c->prof = prof;
+            cudaGraph_t captured = nullptr;
+            cudaError_t ee = cudaStreamEndCapture(cap, &captured);
+            cudaStreamDestroy(cap);
+            if (bs != DD_OK || ce != cudaSuccess || ee != cudaSuccess) {
+                cudaGraphDestroy(g);
+                return bs != DD_OK ? bs : set_error(DD_ECUDA, "inner-loop graph capture");
+            }
+            DD_CK(cudaGraphInstantiate(v.exec, g, 0));
+            cudaGraphDestroy(g);
+            *v.key = ncols;
+        }
+        DD_CK(cudaMemsetAsync(cnt_slot, 0, sizeof(int), c->stream));
+        DD_CK(cudaMemsetAsync(n_act_slot, 0, sizeof(int), c->stream));
+        DD_CK(cudaGraphLaunch(*v.exec, c->stream));
+        *v.on_dev = true;
+    } else {
+        int it = 0;
+        for (it = 1; it <= f.inner_maxit; it++) {
+            DD_CK(cudaMemsetAsync(n_act_slot, 0, sizeof(int), c->stream));
+            dd_status bs = body(c->stream, n_act_slot);
+            if (bs != DD_OK) return bs;
+            if (it % 4 == 0 || it == f.inner_maxit) {
+                DD_CK(cudaMemcpyAsync(c->h_ints + v.slot_act, n_act_slot, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+                DD_CK(cudaStreamSynchronize(c->stream));
+                if (c->h_ints[v.slot_act] == 0) break;
+            }
+        }
+        *v.last_iters = std::min(it, f.inner_maxit);
+        *v.on_dev = false;
+    }
+    // ẑ_c = Σ_s w_s x̂_{s,c} (fixed system order), z_c = Q ẑ_c
+    DD_TIMED(DD_KCLASS_POLESUM, inner_combine(a, v.sys_w, v.nsys, W1, c->stream));
+    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W1, W2, ncols, f.n, f.ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W2, z, ncols, f.n, f.ldf, f.S, c->stream));
     return DD_OK;
 }
 
@@ -266,92 +426,38 @@ static dd_status precond_core(dd_ctx* c, int ncols, const double* r, double* z) 
     if (f.nsys == 0) {
         DD_CK(cudaMemsetAsync(z, 0, sizeof(double) * (size_t)f.NP * ncols, c->stream));
     } else {
-        InnerArgs a{};
-        a.n = f.n; a.ldf = f.ldf; a.NP = f.NP;
-        a.npair = f.nsys * ncols; a.C = ncols;
-        a.hh12 = (double)(1.0L / ((long double)c->N * c->N * 12.0L));
-        a.sys_a = f.sys_a; a.sys_b = f.sys_b;
-        a.x = f.ix; a.r = f.ir; a.p = f.ip; a.q = f.iq; a.z = f.iz;
-        a.rho = f.irho; a.rho0 = f.irho0; a.active = f.iactive; a.rtol = f.inner_rtol;
-        a.dg = f.dg; a.idg = f.idg; a.cs = f.cs;
-        // r̂_c = Q r_c once per column (2 slab passes)
-        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(r, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
-        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.S, c->stream));
-        DD_TIMED(DD_KCLASS_POLESUM, inner_init_hat(a, f.U2, c->stream));
-        auto body = [&](cudaStream_t st, int* n_act) -> dd_status {
-            // q̂ = dg ∘ p̂ + cs D̂ p̂ D̂^T on the active pairs, then the fused CG update
-            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_active(f.ip, f.T1, a.npair, f.n, f.ldf, f.Dh, f.iactive, st));
-            DD_TIMED(DD_KCLASS_POLESUM, face_inner_op_pass(f.T1, f.iq, f.ip, a.npair, ncols, f.n, f.ldf, f.Dh, f.dg, f.cs,
-                                                           f.iactive, st));
-            DD_TIMED(DD_KCLASS_POLESUM, inner_update_hat(a, n_act, st));
-            return DD_OK;
-        };
-        if (c->graph_ok && !c->prof) {
-            // the whole inner loop as one conditional WHILE graph (no host round trips)
-            if (!f.inner_exec || f.inner_key != ncols) {
-                if (f.inner_exec) cudaGraphExecDestroy(f.inner_exec);
-                f.inner_exec = nullptr;
-                cudaGraph_t g = nullptr;
-                DD_CK(cudaGraphCreate(&g, 0));
-                cudaGraphConditionalHandle h;
-                DD_CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
-                cudaGraphNodeParams cp = {};
-                cp.type = cudaGraphNodeTypeConditional;
-                cp.conditional.handle = h;
-                cp.conditional.type = cudaGraphCondTypeWhile;
-                cp.conditional.size = 1;
-                cudaGraphNode_t node;
-                DD_CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
-                cudaStream_t cap = nullptr;
-                DD_CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-                DD_CK(cudaStreamBeginCaptureToGraph(cap, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                                    cudaStreamCaptureModeRelaxed));
-                const bool prof = c->prof;
-                c->prof = false;
-                const long long l0 = c->launches;
-                dd_status bs = body(cap, c->ints + 1);
-                cudaError_t ce = inner_cond(c->ints + 1, c->ints + 6, f.inner_maxit, (unsigned long long)h, cap);
-                c->inner_iter_launches = c->launches - l0 + 1;
-                c->launches = l0;
-                c->prof = prof;
-                cudaGraph_t captured = nullptr;
-                cudaError_t ee = cudaStreamEndCapture(cap, &captured);
-                cudaStreamDestroy(cap);
-                if (bs != DD_OK || ce != cudaSuccess || ee != cudaSuccess) {
-                    cudaGraphDestroy(g);
-                    return bs != DD_OK ? bs : set_error(DD_ECUDA, "inner-loop graph capture");
-                }
-                DD_CK(cudaGraphInstantiate(&f.inner_exec, g, 0));
-                cudaGraphDestroy(g);
-                f.inner_key = ncols;
-            }
-            DD_CK(cudaMemsetAsync(c->ints + 6, 0, sizeof(int), c->stream));
-            DD_CK(cudaMemsetAsync(c->ints + 1, 0, sizeof(int), c->stream));
-            DD_CK(cudaGraphLaunch(f.inner_exec, c->stream));
-            f.inner_iters_on_device = true;
-        } else {
-            int it = 0;
-            for (it = 1; it <= f.inner_maxit; it++) {
-                DD_CK(cudaMemsetAsync(c->ints + 1, 0, sizeof(int), c->stream));
-                dd_status bs = body(c->stream, c->ints + 1);
-                if (bs != DD_OK) return bs;
-                if (it % 4 == 0 || it == f.inner_maxit) {
-                    DD_CK(cudaMemcpyAsync(c->h_ints + 1, c->ints + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-                    DD_CK(cudaStreamSynchronize(c->stream));
-                    if (c->h_ints[1] == 0) break;
-                }
-            }
-            f.last_inner_iters = std::min(it, f.inner_maxit);
-            f.inner_iters_on_device = false;
-        }
-        // ẑ_c = Σ_s w_s x̂_{s,c} (fixed system order), z_c = Q ẑ_c
-        DD_TIMED(DD_KCLASS_POLESUM, inner_combine(a, f.sys_w, f.nsys, f.U1, c->stream));
-        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.S, c->stream));
-        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(f.U2, z, ncols, f.n, f.ldf, f.S, c->stream));
+        dd_status s = inner_apply(c, view_P(f, c), ncols, r, z, f.U1, f.U2);
+        if (s != DD_OK) return s;
     }
     if (f.nccl) {
         NK(ncclAllReduce(z, z, (size_t)f.NP * ncols, ncclDouble, ncclSum, static_cast<ncclComm_t>(f.nccl), c->stream));
     }
+    return DD_OK;
+}
+
+// y = S x on padded face vectors p -> q
+static dd_status schur_core(dd_ctx* c, int ncols, const int* colp, const double* p, double* q) {
+    Face3& f = c->f3;
+    DD_TIMED(DD_KCLASS_OTHER, gather_param(ncols, colp, c->n_param, c->Kp, f.Kcol, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(p, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass_scaled(f.U1, f.U2, ncols, f.n, f.ldf, f.S, f.sw, 0, 1, f.Kcol, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U2, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.S, c->stream));
+    if (c->frac_mode == DD_FRAC_RA) {
+        // Remark 1: γ F p ≈ γ M r_F(L) M p — the face pole sum of the r_F systems
+        // between two consistent-mass products, no dense F
+        const double hh12 = (double)(1.0L / ((long double)c->N * c->N * 12.0L));
+        DD_TIMED(DD_KCLASS_OTHER, gather_param(ncols, colp, c->n_param, c->gp, f.fs.gcol, c->stream));
+        DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_mass_axpy(f.n, f.ldf, f.NP, ncols, hh12, p, nullptr, nullptr, f.fs.V1,
+                                                      c->stream));
+        dd_status s = inner_apply(c, view_F(f, c), ncols, f.fs.V1, f.fs.V2, f.fs.W1, f.fs.W2);
+        if (s != DD_OK) return s;
+        DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_mass_axpy(f.n, f.ldf, f.NP, ncols, hh12, f.fs.V2, f.fs.gcol, f.U2, q,
+                                                      c->stream));
+        return DD_OK;
+    }
+    DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, f.NP, p, q, f.U2, ncols, colp, c->n_param, c->gp, f.fx_ws, f.fx_cnt,
+                                           c->num_sms, c->stream));
     return DD_OK;
 }
 

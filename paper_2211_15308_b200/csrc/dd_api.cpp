@@ -341,7 +341,6 @@ extern "C" dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n
         for (int k = 0; k < fr.n_fpoles; k++)
             if (!(fr.fpoles[k] < 0.0) || !std::isfinite(fr.fpoles[k]) || !std::isfinite(fr.fresidues[k]))
                 return fail(DD_EINVAL, "fractional-term poles must be < 0 and finite");
-        if (mesh && mesh->dim == 3) return fail(DD_EUNSUPPORTED, "RA-evaluated fractional term: 2D interfaces only");
     }
     *out = nullptr;
     if (!mesh) return fail(DD_EINVAL, "mesh is NULL");
@@ -945,13 +944,15 @@ extern "C" dd_status dd_last_solve_ms(dd_ctx* c, double* ms) {
 extern "C" long long dd_launch_count(dd_ctx* c) {
     if (!c) return -1;
     long long v = c->launches;
-    if (c->dim == 3 && c->f3.inner_exec) {
-        // inner-CG iterations run inside a device-side WHILE graph: counted on the device (ints[8])
-        int tot = 0;
+    if (c->dim == 3 && (c->f3.inner_exec || c->f3.fs.exec)) {
+        // inner-CG iterations run inside device-side WHILE graphs: counted on the device
+        // (ints[8]: preconditioner systems, ints[14]: RA-evaluated fractional term)
+        int tot[16] = {0};
         if (cudaSetDevice(c->device) == cudaSuccess && cudaStreamSynchronize(c->stream) == cudaSuccess &&
-            cudaMemcpy(&tot, c->ints + 8, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess) {
-            v += (long long)tot * c->inner_iter_launches;
+            cudaMemcpy(tot, c->ints, sizeof(int) * 16, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            v += (long long)tot[8] * c->inner_iter_launches + (long long)tot[14] * c->f_inner_iter_launches;
             cudaMemset(c->ints + 8, 0, sizeof(int));
+            cudaMemset(c->ints + 14, 0, sizeof(int));
         }
     }
     c->launches = 0;

@@ -41,6 +41,21 @@ struct GraphKey {
 };
 
 // 3D (face interface) state
+// RA-evaluated fractional term in 3D (dd_frac DD_FRAC_RA): the r_F systems' sine-domain tables,
+// inner-CG state and scratch (V1 = M p, V2 = r_F(L) V1, W1/W2 transform scratch, gcol = γ per column)
+struct FSet {
+    int nsys = 0;
+    double *sys_a = nullptr, *sys_b = nullptr, *sys_w = nullptr, *cs = nullptr, *dg = nullptr, *idg = nullptr;
+    double *ix = nullptr, *ir = nullptr, *ip = nullptr, *iq = nullptr, *iz = nullptr, *T1 = nullptr;
+    double *irho = nullptr, *irho0 = nullptr;
+    int* iactive = nullptr;
+    double *V1 = nullptr, *V2 = nullptr, *W1 = nullptr, *W2 = nullptr, *gcol = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int key = -1;
+    bool on_dev = false;
+    int last_iters = 0;
+};
+
 struct Face3 {
     int n = 0, n2 = 0, ldf = 0;
     long long NP = 0;                 // padded face size ldf^2
@@ -71,6 +86,7 @@ struct Face3 {
     int* fx_cnt = nullptr;
     double lam_min = 0.0, lam_max = 0.0;   // spectrum of the face pair (from the setup gevp)
     void* nccl = nullptr;             // ncclComm_t when the poles are split across ranks
+    FSet fs;                          // RA-evaluated fractional term (Remark 1), RA mode only
     int rank = 0, world = 1;
 };
 
@@ -123,6 +139,7 @@ struct dd_ctx {
     int last_split1 = 0, last_split2 = 0, last_ps_warps = 0, last_graph = 0, last_small = 0;
     long long graph_iter_launches = 3;   // kernels per PCG iteration in the captured body
     long long inner_iter_launches = 4;   // kernels per inner-CG iteration (3D WHILE graph)
+    long long f_inner_iter_launches = 4; // same for the RA-evaluated fractional term's inner CG
     bool compact = true;      // GEMMs work over live (unconverged) column tiles only (DD_NO_COMPACT=1 disables)
     int* ntl = nullptr;       // live column tiles [count, ids...], written by the PCG kernels
     bool pdl = true;          // programmatic dependent launch between the iteration's kernels (DD_NO_PDL=1 disables)

@@ -180,6 +180,8 @@ cudaError_t face_copy_out(int n, int ldf, long long NP, int ncols, const double*
                           cudaStream_t st);
 cudaError_t face_dense_pair(int n, double hh12, double* A, double* M, cudaStream_t st);
 cudaError_t face_mass_cols(int n, double hh12, const double* V, double* out, int ncol, int ldo, cudaStream_t st);
+cudaError_t face_mass_axpy(int n, int ldf, long long NP, int ncols, double hh12, const double* v, const double* scale,
+                           const double* add, double* out, cudaStream_t st);
 cudaError_t scale_transpose(const double* V, const double* w, int n2, double* out, int kp, cudaStream_t st);
 cudaError_t face_slab_pass_active(const double* in, double* out, int nslab, int n, int ldf, const double* B,
                                   const int* active, cudaStream_t st);

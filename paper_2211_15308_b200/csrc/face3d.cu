@@ -177,6 +177,32 @@ __device__ __forceinline__ double face_op(const double* v, int j, int k, int n, 
     return a * (4.0 * c - nb) + bm * (6.0 * c + nb + dg);
 }
 
+// out_c = s_c M_Γ v_c (+ add_c) on padded face vectors (s: per-column scale or null = 1; add or null)
+__global__ void k_face_mass_axpy(int n, int ldf, long long NP, int ncols, double hh12, const double* __restrict__ v,
+                                 const double* __restrict__ scale, const double* __restrict__ add, double* __restrict__ out) {
+    const long long total = NP * ncols;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(idx / NP);
+        const int r = (int)(idx % NP);
+        const int j = r / ldf, k = r % ldf;
+        double y = 0.0;
+        if (j < n && k < n) {
+            y = face_op(v + (size_t)c * NP, j, k, n, ldf, 0.0, hh12);
+            if (scale) y *= scale[c];
+            if (add) y += add[idx];
+        }
+        out[idx] = y;
+    }
+}
+cudaError_t face_mass_axpy(int n, int ldf, long long NP, int ncols, double hh12, const double* v, const double* scale,
+                           const double* add, double* out, cudaStream_t st) {
+    long long blocks = (NP * ncols + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_face_mass_axpy<<<(int)blocks, 256, 0, st>>>(n, ldf, NP, ncols, hh12, v, scale, add, out);
+    return cudaGetLastError();
+}
+
 // M applied to the columns of a dense column-major n2 x ncol matrix (setup: B = M V).
 __global__ void k_face_mass_cols(int n, double hh12, const double* __restrict__ V, double* __restrict__ out, int n2,
                                  int ncol, int ldo) {

@@ -62,9 +62,43 @@ def test_ra_operator_parity(lib, N, t, sigma):
         S.close()
 
 
-def test_ra_mode_rejected_in_3d(lib):
+def test_ra_mode_rejects_bad_fit(lib):
     lo, hi = rafit.interval_face(6)
     ras = [rafit.fit_ra(1.0, 1.0, lo, hi, 8)]
-    fr = rafit.fit_power(-0.5, lo, hi, 8)
+
+    class Bad:
+        c0 = 1.0; poles = np.array([0.5]); residues = np.array([1.0])
     with pytest.raises(lib.DDError):
-        lib.Solver(3, 6, [(1.0, 1.0)], ras, max_cols=1, frac=lib.Frac(mode="ra", fra=fr))
+        lib.Solver(3, 6, [(1.0, 1.0)], ras, max_cols=1, frac=lib.Frac(mode="ra", fra=Bad()))
+
+
+@pytest.mark.parametrize("N", [8, 13])
+def test_ra_operator_3d(lib, N):
+    """Remark 1 on a 3D face (the survey's motivation for NEXT-2: no dense n_Γ^2 F): y = K S_unit x
+    + γ M r_F(L) M x with r_F's face systems solved by the batched sine-domain CG, against the
+    oracle's same-RA operator; and within the fit error of the Eq.(7) operator."""
+    n = N - 1
+    params = [(1.0, 1e2)]
+    lo, hi = rafit.interval_face(N)
+    ras = [rafit.fit_ra(K, g, lo, hi, 10) for K, g in params]
+    fr = rafit.fit_power(-0.5, lo, hi, 12)
+    fra = (fr.c0, fr.poles, fr.residues)
+    O = oprob.DenseProblem(3, N, frac_ra=fra)
+    Oex = oprob.DenseProblem(3, N)
+    B = np.random.default_rng(N).uniform(-1, 1, (3, n * n))
+    S = lib.Solver(3, N, params, ras, max_cols=3, frac=lib.Frac(mode="ra", fra=fr))
+    try:
+        y = S.apply_schur(_cols(B), [0] * 3).cpu().numpy()
+        ref = O.apply_S(*params[0], B.T).T
+        assert rel_l2_cols(y, ref) <= 1e-10 + 2e-12 * fr.cancel
+        ex = Oex.apply_S(*params[0], B.T).T
+        assert rel_l2_cols(y, ex) <= 2 * fr.rel_err + 1e-10
+        res = S.pcg_solve(_cols(B), [0] * 3)
+        ra = ras[0]
+        for c in range(3):
+            xo, it, *_ = opcg.pcg(lambda v: O.apply_S(*params[0], v),
+                                  lambda v: O.apply_P_ra(ra.c0, ra.poles, ra.residues, v), B[c])
+            assert abs(int(res.iters[c]) - it) <= 1
+            assert np.linalg.norm(res.x.cpu().numpy()[c] - xo) <= 1e-8 * np.linalg.norm(xo)
+    finally:
+        S.close()
