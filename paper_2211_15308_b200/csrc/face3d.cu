@@ -18,6 +18,7 @@
 //   partial sums are added by one NCCL allreduce (row a-6, in dd_api.cpp).
 #include "dd_internal.h"
 #include "dgemm_tile.cuh"
+#include <cooperative_groups.h>
 
 namespace dd {
 
@@ -44,14 +45,13 @@ struct EpiSlabScale {          // Out[b] = v * scale(b) * w[b's table][row + col
         out[(size_t)b * sC + i] = v * s;
     }
 };
-struct EpiInnerOp {            // q̂[b] = dg[s] ∘ p̂[b] + cs[s] v,  s = b / C   (sine-domain shifted operator)
-    double* q; const double* p; long long NP; int ldf, C;
-    const double* dg; const double* cs;
+struct EpiInnerOp {            // q̂_part[b] = cs[s] v,  s = b / C: the D̂ ⊗ D̂ part of the sine-domain operator; the
+    double* q; const double* p; long long NP; int ldf, C;   // diagonal part dg ∘ p̂ is added where q̂ is
+    const double* dg; const double* cs;                     // consumed (k_inner_update_cl), coalesced
     __device__ __forceinline__ void operator()(int b, int row, int col, double v) const {
         const int s = b / C;
         const size_t i = row + (size_t)col * ldf;
-        const size_t o = (size_t)b * NP + i;
-        q[o] = fma(dg[(size_t)s * NP + i], p[o], cs[s] * v);
+        q[(size_t)b * NP + i] = cs[s] * v;
     }
 };
 struct EpiFaceFx {             // q[c] = γ_c v + D[c]  (padded face layout)
@@ -307,37 +307,62 @@ __global__ void k_inner_init_hat(InnerArgs a, const double* __restrict__ bh) {
 }
 // given q̂ = Â p̂: α = ρ/(p̂·q̂); x̂ += αp̂; r̂ -= αq̂; ẑ = r̂/dg; ρ' = r̂·ẑ; stop if ρ' <= rtol^2 ρ0;
 // else p̂ = ẑ + (ρ'/ρ) p̂   (one CTA per pair; fixed-order reductions)
-__global__ void k_inner_update_hat(InnerArgs a, int* n_active) {
+// CG update of one (system, column) pair by a cluster of ICL CTAs, each owning NP/ICL of the
+// pair's entries; the two dot products are reduced over DSMEM in fixed rank order (deterministic):
+//   q̂ = dg ∘ p̂ + q̂_part;  α = ρ/p̂·q̂;  x̂ += α p̂;  r̂ -= α q̂;  ρ' = r̂·(idg ∘ r̂);  p̂ = idg ∘ r̂ + β p̂
+constexpr int ICL = 4;
+__device__ __forceinline__ double cluster_allsum(double v, double* red, double* slot) {
+    // block sum -> this CTA's slot; cluster barrier; every CTA sums the ICL slots in rank order
+    v = block_sum(v, red);
+    cg::cluster_group cl = cg::this_cluster();
+    if (threadIdx.x == 0) *slot = v;
+    cl.sync();
+    double s = 0.0;
+    for (int q = 0; q < ICL; q++) s += *cl.map_shared_rank(slot, q);
+    cl.sync();                                   // nobody leaves / overwrites before all have read
+    return s;
+}
+__global__ void __cluster_dims__(ICL, 1, 1) k_inner_update_cl(InnerArgs a, int* n_active) {
     __shared__ double red[32];
-    const int pq = blockIdx.x;
-    if (!a.active[pq]) return;
+    __shared__ double slot;
+    const int pq = blockIdx.y;
+    const int rank = blockIdx.x;                 // cluster rank (cluster spans blockIdx.x)
+    if (!a.active[pq]) return;                   // uniform across the cluster
     const int s = pq / a.C;
+    const long long chunk = (a.NP + ICL - 1) / ICL;
+    const long long i0 = rank * chunk, i1 = min(a.NP, i0 + chunk);
     const size_t off = (size_t)pq * a.NP;
+    const double* dg = a.dg + (size_t)s * a.NP;
     const double* idg = a.idg + (size_t)s * a.NP;
     double d = 0.0;
-    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) d = fma(a.p[off + i], a.q[off + i], d);
-    d = block_sum(d, red);
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const double pv = a.p[off + i];
+        const double qv = fma(dg[i], pv, a.q[off + i]);
+        a.q[off + i] = qv;
+        d = fma(pv, qv, d);
+    }
+    d = cluster_allsum(d, red, &slot);
     if (!(d > 0.0)) {
-        if (threadIdx.x == 0) a.active[pq] = 0;
+        if (rank == 0 && threadIdx.x == 0) a.active[pq] = 0;
         return;
     }
     const double alpha = a.rho[pq] / d;
     double rho = 0.0;
-    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) {
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
         a.x[off + i] = fma(alpha, a.p[off + i], a.x[off + i]);
         const double r = fma(-alpha, a.q[off + i], a.r[off + i]);
         a.r[off + i] = r;
         rho = fma(r, r * idg[i], rho);
     }
-    rho = block_sum(rho, red);
+    rho = cluster_allsum(rho, red, &slot);
     if (!(rho > a.rtol * a.rtol * a.rho0[pq])) {
-        if (threadIdx.x == 0) a.active[pq] = 0;
+        if (rank == 0 && threadIdx.x == 0) a.active[pq] = 0;
         return;
     }
     const double beta = rho / a.rho[pq];
-    for (long long i = threadIdx.x; i < a.NP; i += blockDim.x)
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x)
         a.p[off + i] = fma(beta, a.p[off + i], a.r[off + i] * idg[i]);
-    if (threadIdx.x == 0) {
+    if (rank == 0 && threadIdx.x == 0) {
         a.rho[pq] = rho;
         atomicAdd(n_active, 1);
     }
@@ -361,7 +386,7 @@ cudaError_t inner_init_hat(const InnerArgs& a, const double* bh, cudaStream_t st
     return cudaGetLastError();
 }
 cudaError_t inner_update_hat(const InnerArgs& a, int* n_active, cudaStream_t st) {
-    k_inner_update_hat<<<a.npair, 512, 0, st>>>(a, n_active);
+    k_inner_update_cl<<<dim3(ICL, a.npair), 512, 0, st>>>(a, n_active);
     return cudaGetLastError();
 }
 
