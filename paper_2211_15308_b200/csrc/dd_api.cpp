@@ -704,10 +704,10 @@ extern "C" dd_status dd_pcg_solve_host(dd_ctx* c, int ncols, const int* colp_h, 
         if (colp_h[i] < 0 || colp_h[i] >= c->n_param) return fail(DD_EINVAL, "col_param out of range");
     CK(cudaSetDevice(c->device));
     CK(cudaMemcpyAsync(c->colp_st, colp_h, sizeof(int) * ncols, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->bst, b_h, sizeof(double) * (size_t)c->n * ncols, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->bst, b_h, sizeof(double) * (size_t)c->ng * ncols, cudaMemcpyHostToDevice, c->stream));
     dd_status r = dd_pcg_solve(c, ncols, c->colp_st, c->bst, c->xst, rtol, maxit, norm_kind, iters, rel_res, hist);
     if (r != DD_OK && r != DD_ENOCONV && r != DD_ENOTSPD) return r;
-    CK(cudaMemcpyAsync(x_h, c->xst, sizeof(double) * (size_t)c->n * ncols, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(x_h, c->xst, sizeof(double) * (size_t)c->ng * ncols, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return r;
 }

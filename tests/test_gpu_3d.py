@@ -75,6 +75,15 @@ def test_pcg_parity_3d(case3):
     assert res.hist[0] > 0 and len(res.hist) == res.iters[0] + 1
 
 
+def test_host_api_3d(case3):
+    # the host-buffer entry point stages whole faces ((N-1)^2 per column): same bits as the device call
+    N, params, ras, D, S, B = case3
+    a = S.pcg_solve(torch.as_tensor(B, device="cuda"), [0] * B.shape[0], rtol=1e-10, maxit=200)
+    h = S.pcg_solve_host(B, [0] * B.shape[0], rtol=1e-10, maxit=200)
+    assert np.array_equal(h.x, a.x.cpu().numpy())
+    assert np.array_equal(h.iters, a.iters)
+
+
 def test_full_size_3d_properties(lib):
     """Config 4 (N = 128, n_Γ = 16129) at full size: (i) on sine modes of the face the bulk part is
     K s_ab (oracle's mode-wise elimination); (ii) the fractional term satisfies

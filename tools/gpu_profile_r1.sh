@@ -14,3 +14,7 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/p
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/p_plain.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
   --log-file gpurun_out/p_launches_cfg2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/p_ncu_launch.log 2>&1; echo ncu1=$?
+# NEXT rows: RA-evaluated F in 3D, bulk PCG with the Eq.(5) preconditioner, general t
+timeout 900 python bench.py --config cfg4_3d_N128 --frac-mode ra --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/p_bench_cfg4_ra.json 2>&1; echo cfg4ra=$?
+timeout 900 python bench.py --mode bulk-pcg --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/p_bench_cfg2_bulkpcg.json 2>&1; echo bpcg=$?
+timeout 600 python bench.py --t 0.25 --shifted --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/p_bench_cfg2_t025.json 2>&1; echo t025=$?
