@@ -184,6 +184,9 @@ def main():
     ap.add_argument("--mode", default="schur", choices=["schur", "bulk", "bulk-pcg"],
                     help="schur: interface PCG (headline); bulk: full DD solve on bulk RHS (NEXT-1); "
                          "bulk-pcg: PCG on the bulk system with the Eq.(5) DD preconditioner (the paper's protocol)")
+    ap.add_argument("--schur", default="assembled", choices=["assembled", "factored"],
+                    help="2D Schur apply: one [F|G] GEMM (G = S_unit formed at setup) or per-apply fast "
+                         "diagonalisation K1 + K2 (dd_set_schur_mode)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = configs.BY_NAME[args.config]
@@ -213,6 +216,8 @@ def main():
         frac = binding.Frac(t=args.t, shifted=args.shifted, mode="ra",
                             fra=rafit.fit_power(args.t, lo, hi, cfg.n_poles, sigma))
     S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local, frac=frac)
+    if cfg.dim == 2:
+        S.set_schur_mode(args.schur)
     Bt = torch.as_tensor(B, device=f"cuda:{local}")
     cp = torch.as_tensor(colp.astype(np.int32), device=f"cuda:{local}")
     X = torch.empty_like(Bt)
@@ -309,12 +314,19 @@ def main():
             # over those columns (the profiled solves repeat the timed ones: same inputs, same iters).
             cols_per_apply = live_columns(last, compact=(os.environ.get("DD_NO_COMPACT", "0")[:1] != "1"))
             c_eff = float(np.mean(cols_per_apply))
+            assembled = qc["splitk_dst"] == -1          # one GEMM per apply, no K1 (dd_set_schur_mode)
             flops_g2 = 2.0 * n * (2 * n) * c_eff if args.frac_mode == "dense" else 2.0 * n * n * c_eff
-            flops_g1 = 2.0 * n * n * c_eff
+            flops_g1 = 0.0 if assembled else 2.0 * n * n * c_eff
             ach_g2 = flops_g2 / (g2_ms / g2_n / 1e3) / 1e12 if g2_n else None
             step_flops = (flops_g1 + flops_g2) * len(cols_per_apply)
-            roof = {"bound": "tensor", "kernel": "gemm_schur ([S_dst|F] x [T; gamma X], DMMA fp64)" if args.frac_mode == "dense"
-                    else "gemm_schur (S_dst x T' + U, DMMA fp64; U = gamma M r_F M x by pole sum)",
+            if assembled:
+                kname = ("gemm_schur ([F|G] x [gamma X; K X], DMMA fp64; G = S_unit formed at setup)"
+                         if args.frac_mode == "dense" else
+                         "gemm_schur (G x K X + U, DMMA fp64; U = gamma M r_F M x by pole sum)")
+            else:
+                kname = ("gemm_schur ([S_dst|F] x [T; gamma X], DMMA fp64)" if args.frac_mode == "dense"
+                         else "gemm_schur (S_dst x T' + U, DMMA fp64; U = gamma M r_F M x by pole sum)")
+            roof = {"bound": "tensor", "kernel": kname, "schur_mode": "assembled" if assembled else "factored",
                     "achieved": round(ach_g2, 3) if ach_g2 else None, "peak": peak, "unit": "TFLOP/s",
                     "frac": round(ach_g2 / peak, 4) if ach_g2 else None, "peak_source": peak_src,
                     "flops_per_launch": flops_g2, "mean_live_columns": round(c_eff, 2),
@@ -348,6 +360,7 @@ def main():
             "config": {"workload": cfg.name, "dim": cfg.dim, "cells_per_side": cfg.N, "n_gamma": cfg.n_gamma,
                        "param_sets": len(cfg.params), "rhs_per_param": cfg.rhs_per_param, "solves_per_step": C,
                        "poles": cfg.n_poles, "rtol": cfg.rtol, "l2": "flushed (512 MiB write) between timed steps",
+                       "schur_apply": args.schur if cfg.dim == 2 else "factored (3D)",
                        "parallelism": f"columns sharded, {world} rank(s), no collective",
                        "fractional_term": "dense F (Eq.(7))" if args.frac_mode == "dense"
                        else f"RA-evaluated (Remark 1), {cfg.n_poles} poles",

@@ -203,11 +203,26 @@ dd_status dd_nccl_unique_id(void* out128);
 /* 3D handles: inner (shifted face system) CG iterations of the last preconditioner apply. */
 dd_status dd_inner_iterations(const dd_ctx* ctx, int* iters);
 
+/* 2D handles: how dd_apply_schur and the PCG apply S = K_c S_unit + γ_c F (
+ * SURVEY §8(a) rows a-2, a-3).  Both give the same operator up to rounding order:
+ *   DD_SCHUR_FACTORED (0): per apply, the interior solve by fast diagonalisation,
+ *        T' = (K_c s) ∘ (S_dst X) then Y = [S_dst | F] [T' ; γ X]   (6 n^2 flops per column);
+ *   DD_SCHUR_ASSEMBLED (1, default): the parameter-independent interior solve is applied once at
+ *        setup to the identity, G = S_dst diag(s) S_dst = S_unit (n x n, beside F in the handle),
+ *        and each apply is one GEMM  Y = [F | G] [γ X ; K X]          (4 n^2 flops per column);
+ *        in DD_FRAC_RA mode Y = G (K X) + γ M r_F(L) M X.
+ * mode outside {0,1} or a 3D handle: DD_EINVAL (3D always applies the interior solve per apply:
+ * its S_unit would be another n_Γ^2 = 2 GB stream).  DD_SCHUR_FACTORED is also forced by the
+ * environment variable DD_SCHUR_FACTORED=1 at setup. */
+#define DD_SCHUR_FACTORED 0
+#define DD_SCHUR_ASSEMBLED 1
+dd_status dd_set_schur_mode(dd_ctx* ctx, int mode);
+
 /* ---------------------------------------------------------------- instrumentation
  * Per-kernel-class device time (CUDA events on the handle's stream, recorded around each
  * launch while enabled; graphs are bypassed while enabled).  Classes: */
-#define DD_KCLASS_GEMM_DST 0      /* K1: T = S_dst X with the Schur-weight epilogue        */
-#define DD_KCLASS_GEMM_SCHUR 1    /* K2: Y = [S_dst | F] [T ; γX]                           */
+#define DD_KCLASS_GEMM_DST 0      /* K1: T = S_dst X with the Schur-weight epilogue (factored) */
+#define DD_KCLASS_GEMM_SCHUR 1    /* K2: Y = [S_dst | F] [T ; γX]  or assembled [F | G] [γX ; KX] */
 #define DD_KCLASS_POLESUM 2       /* K3 (+K4): fused PCG update + pole sum + dots           */
 #define DD_KCLASS_OTHER 3         /* init / copies / allreduce                              */
 #define DD_NKCLASS 4

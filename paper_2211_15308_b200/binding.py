@@ -24,7 +24,7 @@ KCLASS = ["gemm_dst", "gemm_schur", "polesum_pcg", "other"]
 EXPORTS = ["dd_setup", "dd_setup_ex", "dd_interface_size", "dd_apply_schur", "dd_apply_precond", "dd_pcg_solve",
            "dd_pcg_solve_host", "dd_destroy", "dd_last_error", "dd_profile_enable", "dd_profile_read",
            "dd_launch_count", "dd_query_config", "dd_test_dgemm", "dd_last_solve_ms", "dd_nccl_unique_id",
-           "dd_inner_iterations", "dd_bulk_solve", "dd_bulk_pcg_solve"]
+           "dd_inner_iterations", "dd_bulk_solve", "dd_bulk_pcg_solve", "dd_set_schur_mode"]
 
 
 class DDError(RuntimeError):
@@ -85,6 +85,7 @@ def load():
     lib.dd_destroy.argtypes = [P]; lib.dd_destroy.restype = I
     lib.dd_last_error.argtypes = []; lib.dd_last_error.restype = ctypes.c_char_p
     lib.dd_profile_enable.argtypes = [P, I]; lib.dd_profile_enable.restype = I
+    lib.dd_set_schur_mode.argtypes = [P, I]; lib.dd_set_schur_mode.restype = I
     lib.dd_profile_read.argtypes = [P, P, P]; lib.dd_profile_read.restype = I
     lib.dd_launch_count.argtypes = [P]; lib.dd_launch_count.restype = ctypes.c_longlong
     lib.dd_query_config.argtypes = [P, P, P, P, P]; lib.dd_query_config.restype = I
@@ -261,6 +262,10 @@ class Solver:
                                       int(maxit), int(norm_kind), iters.ctypes.data, rel.ctypes.data, None)
         _check(st, allow=(DD_ENOCONV, DD_ENOTSPD))
         return SolveResult(x, iters, rel, None, st)
+
+    def set_schur_mode(self, mode: str):
+        """2D: "assembled" (default; one GEMM with [F | G]) or "factored" (K1 + K2 per apply)."""
+        _check(load().dd_set_schur_mode(self._h, {"factored": 0, "assembled": 1}.get(mode, -1)))
 
     def profile(self, on: bool):
         _check(load().dd_profile_enable(self._h, 1 if on else 0))

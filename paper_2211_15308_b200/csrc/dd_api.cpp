@@ -193,7 +193,9 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
     c->Kpad = round_up(n, GEMM_BK);
     c->ldv = c->Kpad;
     const bool dense_f = c->frac_mode == DD_FRAC_DENSE;
-    c->lda = dense_f ? 2 * c->Kpad : c->Kpad;    // RA mode (Remark 1): no dense F block
+    // W = [S_dst | F | G]; RA mode (Remark 1): no dense F block, W = [S_dst | G]
+    c->g_off = dense_f ? 2 * c->Kpad : c->Kpad;
+    c->lda = c->g_off + c->Kpad;
     c->Mpad = round_up(n, GEMM_BM);
     c->cols_pad = round_up(c->max_cols, GEMM_BN);
 
@@ -214,35 +216,38 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
     }
     // Schur weights: s_b = (2 - cos θ_b) - Σ_a S[1,a]^2 / (σ_a + σ_b)
     std::vector<double> swh(n);
+    std::vector<long double> swl(n);
     for (int b = 0; b < n; b++) {
         long double g = 0.0L;
         for (int a = 0; a < n; a++) {
             const long double s1 = sintab[(a + 1) % (2 * N)];
             g += (2.0L / N) * s1 * s1 / (sig[a] + sig[b]);
         }
-        swh[b] = (double)((1.0L + 0.5L * sig[b]) - g);
+        swl[b] = (1.0L + 0.5L * sig[b]) - g;
+        swh[b] = (double)swl[b];
     }
     // F = S diag(μ_b (λ_b + σ)^t) S  (Eq.(7) in closed form for the 1D pair; Eq.(2): t = -1/2,
     // σ = 0; Eq.(9)'s shifted L = A_Γ + M_Γ has eigenvalues λ_b + 1 with the same vectors):
     // μ_b = (h/6)(6 - σ_b),  λ_b = 6 σ_b / (h^2 (6 - σ_b))
-    std::vector<double> Bh(dense_f ? (size_t)c->Kpad * round_up(n, GEMM_BN) : 0, 0.0);
+    std::vector<long double> fdiag(dense_f ? n : 0);
     for (int k = 0; k < n && dense_f; k++) {
         const long double mu = h / 6.0L * (6.0L - sig[k]);
         const long double lam = 6.0L * sig[k] / (h * h * (6.0L - sig[k]));
-        const long double f = mu * powl(lam + (long double)c->frac_sigma, (long double)c->frac_t);
-        for (int j = 0; j < n; j++) Bh[(size_t)j * c->Kpad + k] = (double)(f * (long double)Wh[(size_t)k * c->lda + j]);
+        fdiag[k] = mu * powl(lam + (long double)c->frac_sigma, (long double)c->frac_t);
     }
     CK(dalloc(c, &c->W, (size_t)c->Mpad * c->lda));
     CK(cudaMemcpyAsync(c->W, Wh.data(), Wh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    double* Bd = nullptr;
-    if (dense_f) {
+    // one-off setup GEMMs  S_dst · (diag(d) S_dst)  into W's column block `off`:
+    //   F (d = f above) and G (d = s: the unit Schur complement A^ii - A^i0 A00^-1 A^0i, row a-2
+    //   applied once to the identity; the assembled Schur apply is then y = [F | G] [γ x ; K x])
+    auto sandwich = [&](const std::vector<long double>& d, int off) -> dd_status {
+        std::vector<double> Bh((size_t)c->Kpad * round_up(n, GEMM_BN), 0.0);
+        for (int k = 0; k < n; k++)
+            for (int j = 0; j < n; j++) Bh[(size_t)j * c->Kpad + k] = (double)(d[k] * (long double)Wh[(size_t)k * c->lda + j]);
+        double* Bd = nullptr; double* ws = nullptr; int* cnt = nullptr;
         CK(cudaMalloc(&Bd, Bh.size() * sizeof(double)));
         CK(cudaMemcpyAsync(Bd, Bh.data(), Bh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    }
-    if (dense_f) {
-        // one-off setup GEMM F = S_dst · (diag(f) S_dst), written into W's right half
         const int sk = gemm_pick_splitk(n, n, c->Kpad, c->num_sms);
-        double* ws = nullptr; int* cnt = nullptr;
         const size_t wsz = gemm_ws_doubles(n, n, c->num_sms);
         if (wsz) CK(cudaMalloc(&ws, wsz * sizeof(double)));
         CK(cudaMalloc(&cnt, sizeof(int) * (gemm_tiles(n, n) + 1)));
@@ -251,14 +256,23 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
         ga.M = n; ga.N = n; ga.K = c->Kpad;
         ga.A = c->W; ga.lda = c->lda;
         ga.B = Bd; ga.ldb = c->Kpad;
-        ga.C = c->W + c->Kpad; ga.ldc = c->lda;
+        ga.C = c->W + off; ga.ldc = c->lda;
         ga.splitk = sk; ga.ws = ws; ga.counters = cnt; ga.epi = EPI_STORE; ga.num_sms = c->num_sms;
         CK(launch_dgemm(ga, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         if (ws) cudaFree(ws);
         cudaFree(cnt);
+        cudaFree(Bd);
+        return DD_OK;
+    };
+    if (dense_f) {
+        dd_status st = sandwich(fdiag, c->Kpad);
+        if (st != DD_OK) return st;
     }
-    if (Bd) cudaFree(Bd);
+    {
+        dd_status st = sandwich(swl, c->g_off);
+        if (st != DD_OK) return st;
+    }
     CK(cudaStreamSynchronize(c->stream));
     CK(dalloc(c, &c->sw, n));
     CK(cudaMemcpyAsync(c->sw, swh.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -393,6 +407,7 @@ extern "C" dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n
     if (const char* ns = std::getenv("DD_NO_SMALL")) c->small_ok = !(ns[0] == '1');
     if (const char* np = std::getenv("DD_NO_PDL")) c->pdl = !(np[0] == '1');
     if (const char* nk = std::getenv("DD_NO_COMPACT")) c->compact = !(nk[0] == '1');
+    if (const char* sf = std::getenv("DD_SCHUR_FACTORED")) c->schur_mode = sf[0] == '1' ? 0 : 1;
     const char* pht = std::getenv("DD_PHASE_TIMING");
     const bool want_dbg = pht && pht[0] == '1';
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DD_ECUDA, "cudaSetDevice failed"));
@@ -425,9 +440,36 @@ extern "C" int dd_interface_size(const dd_ctx* c) { return c ? c->ng : -1; }
 
 // ------------------------------------------------------------------------------------ applies
 static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double* xin, double* y, int ldy,
-                             const int* ntl = nullptr) {
-    // T' = (K_c s) ∘ (S_dst X) -> Z[0:n);  Y = [S_dst | F] [T' ; γ X]
+                             const int* ntl = nullptr, bool z_ready = false) {
     const int n = c->n;
+    if (c->schur_mode == 1) {
+        // assembled: Z = [γ X ; K X] (written by the PCG kernels with p, z_ready, or here), then
+        //   Y = [F | G] Z                       (dense F; K-dim 2 Kpad)
+        //   Y = G (K X) + γ M r_F(L) M X         (RA mode, Remark 1; K-dim Kpad)
+        if (!z_ready)
+            TIMED(DD_KCLASS_OTHER, launch_schur_operand(n, ncols, colp, c->n_param, c->Kp, c->gp, xin, c->ldv, c->Z,
+                                                        2 * c->Kpad, c->Kpad, c->stream));
+        const bool ra = c->frac_mode == DD_FRAC_RA;
+        if (ra)
+            TIMED(DD_KCLASS_POLESUM, launch_frac_ra(ncols, colp, c->n_param, c->gp, c->geom, c->ftabs, xin, c->ldv,
+                                                    c->q_f, c->ldv, 1.0 / (6.0 * c->N), c->stream, c->pdl));
+        GemmArgs g2{};
+        g2.M = n; g2.N = ncols; g2.K = ra ? c->Kpad : 2 * c->Kpad;
+        g2.A = c->W + (ra ? c->g_off : c->Kpad); g2.lda = c->lda;
+        g2.B = ra ? c->Z + c->Kpad : c->Z; g2.ldb = 2 * c->Kpad;
+        g2.C = y; g2.ldc = ldy;
+        g2.X = c->q_f; g2.ldx = c->ldv;
+        g2.splitk = gemm_pick_splitk(n, ncols, g2.K, c->num_sms); g2.ws = c->gws; g2.counters = c->gcnt;
+        g2.num_sms = c->num_sms;
+        g2.epi = ra ? EPI_ADD : EPI_STORE;
+        g2.pdl = c->pdl; g2.a_static = 1;
+        g2.ntl = ntl;
+        c->last_split1 = -1;
+        c->last_split2 = g2.splitk;
+        TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(g2, c->stream));
+        return DD_OK;
+    }
+    // factored: T' = (K_c s) ∘ (S_dst X) -> Z[0:n);  Y = [S_dst | F] [T' ; γ X]
     const int sk1 = gemm_pick_splitk(n, ncols, c->Kpad, c->num_sms);
     const int sk2 = gemm_pick_splitk(n, ncols, 2 * c->Kpad, c->num_sms);
     c->last_split1 = sk1;
@@ -528,11 +570,15 @@ static PcgState make_state(dd_ctx* c, int ncols, const int* colp, double* x, dou
     // converge at different iterations (cfg5: +10.8 %), not for 4 tiles (cfg2: -1.4 %).
     s.ntl = (c->compact && (ncols + GEMM_BN - 1) / GEMM_BN >= 6) ? c->ntl : nullptr;
     s.ntl_cnt = c->ntl + c->cols_pad / GEMM_BN + 2;
+    if (c->dim == 2 && c->schur_mode == 1) {
+        s.zs = c->Z; s.ldz = 2 * c->Kpad; s.zhalf = c->Kpad;
+        s.Kp = c->Kp; s.gp = c->gp;
+    }
     return s;
 }
 
 static dd_status iteration_body(dd_ctx* c, const PcgState& s) {
-    dd_status st = schur_gemms(c, s.ncols, s.col_param, c->p, c->q, c->ldv, s.ntl);
+    dd_status st = schur_gemms(c, s.ncols, s.col_param, c->p, c->q, c->ldv, s.ntl, s.zs != nullptr);
     if (st != DD_OK) return st;
     c->last_ps_warps = polesum_warps(c->geom);
     TIMED(DD_KCLASS_POLESUM, launch_pcg_iter(s, c->geom, c->tabs, c->stream, c->pdl));
@@ -905,6 +951,19 @@ extern "C" dd_status dd_destroy(dd_ctx* c) {
 }
 
 extern "C" const char* dd_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" dd_status dd_set_schur_mode(dd_ctx* c, int mode) {
+    if (!c) return fail(DD_EINVAL, "NULL handle");
+    if (c->dim != 2) return fail(DD_EINVAL, "schur mode: 2D handles only");
+    if (mode != DD_SCHUR_FACTORED && mode != DD_SCHUR_ASSEMBLED) return fail(DD_EINVAL, "schur mode not in {0,1}");
+    if (mode != c->schur_mode) {
+        CK(cudaStreamSynchronize(c->stream));
+        for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);    // captured with the other operator
+        c->graphs.clear();
+        c->schur_mode = mode;
+    }
+    return DD_OK;
+}
 
 extern "C" dd_status dd_profile_enable(dd_ctx* c, int on) {
     if (!c) return fail(DD_EINVAL, "NULL handle");

@@ -107,7 +107,9 @@ struct dd_ctx {
     double *bulk_gv = nullptr, *bulk_xg = nullptr;
     double *bpcg_r = nullptr, *bpcg_p = nullptr, *bpcg_q = nullptr, *bpcg_z = nullptr;   // bulk PCG vectors
     // operator data (2D)
-    double* W = nullptr;      // Mpad x 2 Kpad row-major: [S_dst | 0 | F | 0]
+    double* W = nullptr;      // 2D: Mpad x lda row-major: [S_dst | F | G] (RA mode: [S_dst | G]), blocks Kpad wide
+    int g_off = 0;            // 2D: column offset of G = S_dst diag(s) S_dst (the unit Schur complement) in W
+    int schur_mode = 1;       // 2D Schur apply: 0 factored (K1 + K2), 1 assembled (one GEMM with [F | G])
     double* sw = nullptr;     // Schur weights s_b
     double* Kp = nullptr;     // [n_param]
     double* gp = nullptr;     // [n_param]

@@ -96,6 +96,9 @@ struct PcgState {
     long long* dbg;                    // optional phase timestamps of CTA 0 (DD_PHASE_TIMING=1)
     int* ntl;                          // live 64-column tiles [count, ids...] for the GEMMs (or null)
     int* ntl_cnt;                      // active columns per 64-column tile (zeroed before pcg_init)
+    // assembled 2D Schur apply: every new p is also written as the GEMM operand [γ_c p ; K_c p]
+    double* zs; int ldz, zhalf;        // Z (column stride ldz), K-half at row zhalf (or zs = null)
+    const double *Kp, *gp;             // per-parameter K, γ
 };
 
 PoleGeom make_pole_geom(int n);
@@ -119,6 +122,10 @@ cudaError_t launch_pcg_small(const PcgState& s, const PoleGeom& g, const PoleTab
                              cudaStream_t st);
 cudaError_t launch_copy_cols(int n, int ncols, const double* src, int lds, double* dst, int ldd,
                              cudaStream_t st);
+// Z[:, c] = [γ_c x_c ; K_c x_c] (rows 0.. and zhalf..): operand of the assembled Schur GEMM
+cudaError_t launch_schur_operand(int n, int ncols, const int* col_param, int n_param, const double* Kp,
+                                 const double* gp, const double* x, int ldx, double* Z, int ldz, int zhalf,
+                                 cudaStream_t st);
 cudaError_t launch_check_params(int ncols, const int* col_param, int n_param, int* flag, cudaStream_t st);
 
 // ----------------------------------------------------------------------------- 2D bulk solve (bulk2d.cu)

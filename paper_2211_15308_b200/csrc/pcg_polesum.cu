@@ -591,6 +591,10 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
         rz += S.R[tpos(i, g)] * zi;
         zz += zi * zi;
         s.p[off + i] = zi;
+        if (s.zs) {
+            s.zs[(size_t)c * s.ldz + i] = s.gp[param] * zi;
+            s.zs[(size_t)c * s.ldz + s.zhalf + i] = s.Kp[param] * zi;
+        }
     }
     block_sum2(rz, zz, red);
     if (threadIdx.x == 0) {
@@ -720,10 +724,26 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
                 if (threadIdx.x == 0) s.active[c] = 0;
             } else {
                 const double beta = rz / s.rho[c];
+                if (s.zs) {
+                    // assembled Schur apply: the next GEMM's operand [γ p ; K p] written with p
+                    const double gc = s.gp[param], Kc = s.Kp[param];
+                    double* zc = s.zs + (size_t)c * s.ldz;
 #pragma unroll
-                for (int j = 0; j < RPT; j++) {
-                    const int i = threadIdx.x + j * NT;
-                    if (i < n) s.p[off + i] = fma(beta, pv[j], zv[j]);   // pv: p as loaded at entry
+                    for (int j = 0; j < RPT; j++) {
+                        const int i = threadIdx.x + j * NT;
+                        if (i < n) {
+                            const double pn = fma(beta, pv[j], zv[j]);
+                            s.p[off + i] = pn;
+                            zc[i] = gc * pn;
+                            zc[s.zhalf + i] = Kc * pn;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < RPT; j++) {
+                        const int i = threadIdx.x + j * NT;
+                        if (i < n) s.p[off + i] = fma(beta, pv[j], zv[j]);   // pv: p as loaded at entry
+                    }
                 }
                 __syncthreads();
                 if (threadIdx.x == 0) s.rho[c] = rz;
@@ -856,6 +876,19 @@ __global__ void k_copy_cols(int n, int ncols, const double* __restrict__ src, in
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
         const size_t c = idx / n, i = idx % n;
         dst[c * ldd + i] = src[c * lds + i];
+    }
+}
+
+__global__ void k_schur_operand(int n, int ncols, const int* __restrict__ col_param, int n_param,
+                                const double* __restrict__ Kp, const double* __restrict__ gp,
+                                const double* __restrict__ x, int ldx, double* __restrict__ Z, int ldz, int zhalf) {
+    const size_t total = (size_t)n * ncols;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t c = idx / n, i = idx % n;
+        const int p = clamp_param(col_param[c], n_param);
+        const double v = x[c * ldx + i];
+        Z[c * ldz + i] = gp[p] * v;
+        Z[c * ldz + zhalf + i] = Kp[p] * v;
     }
 }
 
@@ -1009,6 +1042,17 @@ cudaError_t launch_copy_cols(int n, int ncols, const double* src, int lds, doubl
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
     k_copy_cols<<<blocks, 256, 0, st>>>(n, ncols, src, lds, dst, ldd);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_schur_operand(int n, int ncols, const int* col_param, int n_param, const double* Kp,
+                                 const double* gp, const double* x, int ldx, double* Z, int ldz, int zhalf,
+                                 cudaStream_t st) {
+    if (n <= 0 || ncols <= 0) return cudaSuccess;
+    const size_t total = (size_t)n * ncols;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_schur_operand<<<blocks, 256, 0, st>>>(n, ncols, col_param, n_param, Kp, gp, x, ldx, Z, ldz, zhalf);
     return cudaGetLastError();
 }
 

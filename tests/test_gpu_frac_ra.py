@@ -25,8 +25,9 @@ def _cols(B):
     return torch.as_tensor(B, device="cuda")
 
 
+@pytest.mark.parametrize("mode", ["assembled", "factored"])
 @pytest.mark.parametrize("N,t,sigma", [(9, -0.5, 0.0), (64, -0.5, 0.0), (200, -0.25, 1.0), (1024, -0.5, 0.0)])
-def test_ra_operator_parity(lib, N, t, sigma):
+def test_ra_operator_parity(lib, N, t, sigma, mode):
     params = [(1.0, 1e2), (1e-3, 1e4)]
     lo, hi = rafit.interval_1d(N)
     ras = [rafit.fit_ra(K, g, lo, hi, 14, t=t, sigma=sigma) for K, g in params]
@@ -42,6 +43,7 @@ def test_ra_operator_parity(lib, N, t, sigma):
     B = np.random.default_rng(N).uniform(-1, 1, (C, N - 1))
     colp = np.arange(C) % 2
     S = lib.Solver(2, N, params, ras, max_cols=C, frac=lib.Frac(t=t, shifted=bool(sigma), mode="ra", fra=fr))
+    S.set_schur_mode(mode)
     try:
         y = S.apply_schur(_cols(B), colp).cpu().numpy()
         ref = np.stack([O.apply_S(*params[colp[c]], B[c]) for c in range(C)])

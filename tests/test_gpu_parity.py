@@ -64,9 +64,14 @@ def small_case(request, lib):
     S.close()
 
 
-def test_schur_apply_parity_small(small_case):
+@pytest.mark.parametrize("mode", ["assembled", "factored"])
+def test_schur_apply_parity_small(small_case, mode):
     N, params, ras, D, S, B, colp = small_case
-    y = S.apply_schur(_cols(B), colp).cpu().numpy()
+    S.set_schur_mode(mode)
+    try:
+        y = S.apply_schur(_cols(B), colp).cpu().numpy()
+    finally:
+        S.set_schur_mode("assembled")
     ref = np.stack([D.apply_S(*params[colp[c]], B[c]) for c in range(B.shape[0])])
     assert rel_l2_cols(y, ref) <= 1e-10
 
@@ -167,9 +172,11 @@ def test_small_persistent_kernel_matches_general_path(lib, N, monkeypatch):
         S1.close(); S2.close()
 
 
-def test_profile_and_launch_counts(lib):
+@pytest.mark.parametrize("mode", ["assembled", "factored"])
+def test_profile_and_launch_counts(lib, mode):
     N = 96; params = [(1.0, 1e2)]; ras = fit_all(N, params, 8)
     S = _solver(lib, N, params, ras, max_cols=8)
+    S.set_schur_mode(mode)
     try:
         B = np.random.default_rng(0).uniform(-1, 1, (8, N - 1))
         S.launch_count()
@@ -181,17 +188,24 @@ def test_profile_and_launch_counts(lib):
         prof = S.profile_read()
         S.profile(False)
         assert np.array_equal(r2.x.cpu().numpy(), r.x.cpu().numpy())
-        assert prof["gemm_dst"][1] == k and prof["polesum_pcg"][1] == k
-        assert prof["gemm_schur"][1] == k
-        assert n_launch == 2 + 3 * k            # check_params, init, then K1 + K2 + pole sum per iteration
-        assert all(v[0] > 0 for v in prof.values())
+        assert prof["polesum_pcg"][1] == k and prof["gemm_schur"][1] == k
+        if mode == "factored":
+            assert prof["gemm_dst"][1] == k
+            assert n_launch == 2 + 3 * k        # check_params, init, then K1 + K2 + pole sum per iteration
+            assert all(v[0] > 0 for v in prof.values())
+        else:
+            assert prof["gemm_dst"][1] == 0     # the interior solve lives in G (setup)
+            assert n_launch == 2 + 2 * k        # check_params, init, then [F | G] GEMM + pole sum
+        with pytest.raises(lib.DDError):
+            S.set_schur_mode("bogus")
     finally:
         S.close()
 
 
 # ------------------------------------------------------------------------- ragged large sizes (G = 2, 4 groups)
+@pytest.mark.parametrize("mode", ["assembled", "factored"])
 @pytest.mark.parametrize("N,C", [(1500, 13), (3001, 7), (2049, 3)])
-def test_ragged_large_parity(lib, N, C):
+def test_ragged_large_parity(lib, N, C, mode):
     """Interfaces whose chunking uses 2- and 4-warp groups with a partial last chunk, and column
     counts that leave ragged GEMM tiles; against the oracle's mode tier."""
     params = [(1.0, 1e2), (1e-3, 1e5)]
@@ -201,6 +215,7 @@ def test_ragged_large_parity(lib, N, C):
     B = rng.uniform(-1, 1, (C, N - 1))
     colp = np.arange(C) % 2
     S = _solver(lib, N, params, ras, max_cols=C)
+    S.set_schur_mode(mode)
     try:
         y = S.apply_schur(_cols(B), colp).cpu().numpy()
         z = S.apply_precond(_cols(B), colp).cpu().numpy()
@@ -256,6 +271,29 @@ def test_full_config_parity(lib, cfg):
             assert np.all(np.abs(res.iters[sel] - its) <= 1), (p, res.iters[sel], its)
             assert rel_l2_cols(x[sel], X.T) <= 1e-8
         assert np.all(res.rel_res <= cfg.rtol)
+    finally:
+        S.close()
+
+
+@pytest.mark.parametrize("name", ["cfg2_2d_N1024_sweep", "cfg5_2d_N2048_darcy"])
+def test_schur_modes_agree_full_size(lib, name):
+    """The assembled apply ([F | G] [γX ; KX], G formed at setup) and the factored one (fast
+    diagonalisation per apply) are the same operator: at full config size they agree to rounding
+    and give the same PCG iterates (both are pinned to the oracle above at smaller sizes)."""
+    cfg = configs.BY_NAME[name]
+    ras = fit_all(cfg.N, cfg.params, cfg.n_poles)
+    B, colp = inputs.batch(cfg.n_gamma, len(cfg.params), cfg.rhs_per_param)
+    S = _solver(lib, cfg.N, cfg.params, ras, max_cols=cfg.n_cols)
+    try:
+        Bt = _cols(B)
+        ya = S.apply_schur(Bt, colp).cpu().numpy()
+        ra = S.pcg_solve(Bt, colp, rtol=cfg.rtol, maxit=cfg.maxit)
+        S.set_schur_mode("factored")
+        yf = S.apply_schur(Bt, colp).cpu().numpy()
+        rf = S.pcg_solve(Bt, colp, rtol=cfg.rtol, maxit=cfg.maxit)
+        assert rel_l2_cols(ya, yf) <= 1e-13
+        assert np.all(np.abs(ra.iters - rf.iters) <= 1)
+        assert rel_l2_cols(ra.x.cpu().numpy(), rf.x.cpu().numpy()) <= 1e-8
     finally:
         S.close()
 
