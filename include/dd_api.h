@@ -211,11 +211,20 @@ dd_status dd_inner_iterations(const dd_ctx* ctx, int* iters);
  *        setup to the identity, G = S_dst diag(s) S_dst = S_unit (n x n, beside F in the handle),
  *        and each apply is one GEMM  Y = [F | G] [γ X ; K X]          (4 n^2 flops per column);
  *        in DD_FRAC_RA mode Y = G (K X) + γ M r_F(L) M X.
- * mode outside {0,1} or a 3D handle: DD_EINVAL (3D always applies the interior solve per apply:
- * its S_unit would be another n_Γ^2 = 2 GB stream).  DD_SCHUR_FACTORED is also forced by the
- * environment variable DD_SCHUR_FACTORED=1 at setup. */
+ *   DD_SCHUR_GROUPED (2, default for dense F when the operators fit in 16 GiB): the full Schur
+ *        matrix of each parameter set, H_p = K_p G + γ_p F (n_param x n^2 doubles, formed when
+ *        the mode is selected), and each apply is one grouped GEMM Y[:, c] = H_{p(c)} X[:, c]
+ *        (2 n^2 flops per column) over 32-column tiles.  Needs every 32-column tile of a call
+ *        to hold one parameter set (columns grouped by parameter, groups a multiple of 32 wide);
+ *        otherwise that call computes the assembled product instead (same result, checked on
+ *        the device, no host synchronisation).
+ * mode outside {0,1,2}, a 3D handle, or GROUPED in DD_FRAC_RA mode: DD_EINVAL; GROUPED beyond
+ * 64 GiB of operators: DD_ENOMEM.  (3D always applies the interior solve per apply: its S_unit
+ * would be another n_Γ^2 = 2 GB stream.)  The environment variable DD_SCHUR_MODE=0|1|2 sets
+ * the mode at setup. */
 #define DD_SCHUR_FACTORED 0
 #define DD_SCHUR_ASSEMBLED 1
+#define DD_SCHUR_GROUPED 2
 dd_status dd_set_schur_mode(dd_ctx* ctx, int mode);
 
 /* ---------------------------------------------------------------- instrumentation

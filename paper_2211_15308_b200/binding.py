@@ -264,8 +264,9 @@ class Solver:
         return SolveResult(x, iters, rel, None, st)
 
     def set_schur_mode(self, mode: str):
-        """2D: "assembled" (default; one GEMM with [F | G]) or "factored" (K1 + K2 per apply)."""
-        _check(load().dd_set_schur_mode(self._h, {"factored": 0, "assembled": 1}.get(mode, -1)))
+        """2D: "grouped" (default for dense F; one GEMM with H_p = K_p G + γ_p F per parameter set),
+        "assembled" (one GEMM with [F | G]) or "factored" (K1 + K2 per apply)."""
+        _check(load().dd_set_schur_mode(self._h, {"factored": 0, "assembled": 1, "grouped": 2}.get(mode, -1)))
 
     def profile(self, on: bool):
         _check(load().dd_profile_enable(self._h, 1 if on else 0))

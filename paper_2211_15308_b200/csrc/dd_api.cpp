@@ -196,7 +196,7 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
     // W = [S_dst | F | G]; RA mode (Remark 1): no dense F block, W = [S_dst | G]
     c->g_off = dense_f ? 2 * c->Kpad : c->Kpad;
     c->lda = c->g_off + c->Kpad;
-    c->Mpad = round_up(n, GEMM_BM);
+    c->Mpad = round_up(n, 128);    // rows readable by every GEMM tile height (64; grouped 128)
     c->cols_pad = round_up(c->max_cols, GEMM_BN);
 
     // --- sine matrix S_dst[j,k] = sqrt(2/N) sin(jkπ/N) with integer argument reduction (A18)
@@ -407,7 +407,6 @@ extern "C" dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n
     if (const char* ns = std::getenv("DD_NO_SMALL")) c->small_ok = !(ns[0] == '1');
     if (const char* np = std::getenv("DD_NO_PDL")) c->pdl = !(np[0] == '1');
     if (const char* nk = std::getenv("DD_NO_COMPACT")) c->compact = !(nk[0] == '1');
-    if (const char* sf = std::getenv("DD_SCHUR_FACTORED")) c->schur_mode = sf[0] == '1' ? 0 : 1;
     const char* pht = std::getenv("DD_PHASE_TIMING");
     const bool want_dbg = pht && pht[0] == '1';
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DD_ECUDA, "cudaSetDevice failed"));
@@ -432,6 +431,20 @@ extern "C" dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n
     if (cudaMallocHost(&c->h_ints, sizeof(int) * 16) != cudaSuccess) return bail(fail(DD_ENOMEM, "pinned"));
     if (want_dbg && dalloc(c, &c->dbg, 16) != cudaSuccess) return bail(fail(DD_ENOMEM, "dbg"));
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DD_ECUDA, "setup sync"));
+    if (c->dim == 2) {
+        // default 2D Schur apply: grouped when F is dense and the per-parameter operators fit in
+        // 16 GiB, else assembled; DD_SCHUR_MODE=0|1|2 overrides (dd_set_schur_mode)
+        int want = c->frac_mode == DD_FRAC_DENSE &&
+                           (double)c->Mpad * c->Kpad * c->n_param * sizeof(double) <= 16.0 * (1ull << 30)
+                       ? DD_SCHUR_GROUPED
+                       : DD_SCHUR_ASSEMBLED;
+        if (const char* sm = std::getenv("DD_SCHUR_MODE")) want = sm[0] - '0';
+        c->schur_mode = DD_SCHUR_ASSEMBLED;
+        if (want != DD_SCHUR_ASSEMBLED) {
+            dd_status ms = dd_set_schur_mode(c, want);
+            if (ms != DD_OK) return bail(ms);
+        }
+    }
     *out = c;
     return DD_OK;
 }
@@ -442,6 +455,33 @@ extern "C" int dd_interface_size(const dd_ctx* c) { return c ? c->ng : -1; }
 static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double* xin, double* y, int ldy,
                              const int* ntl = nullptr, bool z_ready = false) {
     const int n = c->n;
+    if (c->schur_mode == 2) {
+        // grouped: Y[:, c] = H_{p(c)} X[:, c], one 32-column tile per GEMM CTA column; a launch
+        // whose tiles mix parameter sets (flag from k_check_tiles) computes [F | G] [γ X ; K X]
+        if (!z_ready) {
+            CK(cudaMemsetAsync(c->ints + 6, 0, sizeof(int), c->stream));
+            TIMED(DD_KCLASS_OTHER, launch_check_tiles(ncols, colp, c->ints + 6, c->stream));
+            TIMED(DD_KCLASS_OTHER, launch_schur_operand(n, ncols, colp, c->n_param, c->Kp, c->gp, xin, c->ldv, c->Z,
+                                                        2 * c->Kpad, c->Kpad, c->stream));
+        }
+        GemmArgs g{};
+        g.M = n; g.N = ncols; g.K = c->Kpad;
+        g.A = c->H; g.lda = c->Kpad;
+        g.B = xin; g.ldb = c->ldv;
+        g.C = y; g.ldc = ldy;
+        g.grouped = 1; g.sG = (long long)c->Mpad * c->Kpad; g.col_param = colp; g.n_param = c->n_param;
+        g.mixed = c->ints + 6;
+        g.alt_A = c->W + c->Kpad; g.alt_lda = c->lda; g.alt_B = c->Z; g.alt_ldb = 2 * c->Kpad; g.alt_K = 2 * c->Kpad;
+        g.splitk = gemm_pick_splitk_grouped(n, ncols, c->Kpad, c->num_sms);
+        g.ws = c->gws; g.counters = c->gcnt; g.num_sms = c->num_sms;
+        g.epi = EPI_STORE;
+        g.pdl = c->pdl;
+        g.ntl = ntl;
+        c->last_split1 = -2;
+        c->last_split2 = g.splitk;
+        TIMED(DD_KCLASS_GEMM_SCHUR, launch_dgemm(g, c->stream));
+        return DD_OK;
+    }
     if (c->schur_mode == 1) {
         // assembled: Z = [γ X ; K X] (written by the PCG kernels with p, z_ready, or here), then
         //   Y = [F | G] Z                       (dense F; K-dim 2 Kpad)
@@ -570,9 +610,10 @@ static PcgState make_state(dd_ctx* c, int ncols, const int* colp, double* x, dou
     // converge at different iterations (cfg5: +10.8 %), not for 4 tiles (cfg2: -1.4 %).
     s.ntl = (c->compact && (ncols + GEMM_BN - 1) / GEMM_BN >= 6) ? c->ntl : nullptr;
     s.ntl_cnt = c->ntl + c->cols_pad / GEMM_BN + 2;
-    if (c->dim == 2 && c->schur_mode == 1) {
+    if (c->dim == 2 && c->schur_mode >= 1) {
         s.zs = c->Z; s.ldz = 2 * c->Kpad; s.zhalf = c->Kpad;
         s.Kp = c->Kp; s.gp = c->gp;
+        s.zmixed = c->schur_mode == 2 ? c->ints + 6 : nullptr;   // grouped: fallback operand only
     }
     return s;
 }
@@ -645,6 +686,8 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
     CK(cudaMemsetAsync(c->ints, 0, sizeof(int) * 8, c->stream));
     if (c->dim == 2) CK(cudaMemsetAsync(c->ntl, 0, sizeof(int) * (2 * (c->cols_pad / GEMM_BN) + 4), c->stream));
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
+    if (c->dim == 2 && c->schur_mode == 2)
+        TIMED(DD_KCLASS_OTHER, launch_check_tiles(ncols, colp, c->ints + 6, c->stream));
     PcgState st = make_state(c, ncols, colp, x, rtol, maxit, norm_kind);
     c->last_ps_warps = polesum_warps(c->geom);
     c->last_graph = 0;
@@ -955,7 +998,19 @@ extern "C" const char* dd_last_error(void) { return g_last_error.c_str(); }
 extern "C" dd_status dd_set_schur_mode(dd_ctx* c, int mode) {
     if (!c) return fail(DD_EINVAL, "NULL handle");
     if (c->dim != 2) return fail(DD_EINVAL, "schur mode: 2D handles only");
-    if (mode != DD_SCHUR_FACTORED && mode != DD_SCHUR_ASSEMBLED) return fail(DD_EINVAL, "schur mode not in {0,1}");
+    if (mode != DD_SCHUR_FACTORED && mode != DD_SCHUR_ASSEMBLED && mode != DD_SCHUR_GROUPED)
+        return fail(DD_EINVAL, "schur mode not in {0,1,2}");
+    if (mode == DD_SCHUR_GROUPED && c->frac_mode != DD_FRAC_DENSE)
+        return fail(DD_EINVAL, "grouped schur mode needs the dense F (RA mode applies one n x n GEMM already)");
+    if (mode == DD_SCHUR_GROUPED && !c->H) {
+        const size_t per = (size_t)c->Mpad * c->Kpad;
+        if ((double)per * c->n_param * sizeof(double) > 64.0 * (1ull << 30))
+            return fail(DD_ENOMEM, "grouped schur mode: n_param x n^2 operators exceed 64 GiB");
+        CK(dalloc(c, &c->H, per * c->n_param));
+        CK(launch_group_operators(c->n, c->n_param, c->W, c->lda, c->Kpad, c->g_off, c->Kp, c->gp, c->H, c->Kpad,
+                                  (long long)per, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
     if (mode != c->schur_mode) {
         CK(cudaStreamSynchronize(c->stream));
         for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);    // captured with the other operator

@@ -109,7 +109,9 @@ struct dd_ctx {
     // operator data (2D)
     double* W = nullptr;      // 2D: Mpad x lda row-major: [S_dst | F | G] (RA mode: [S_dst | G]), blocks Kpad wide
     int g_off = 0;            // 2D: column offset of G = S_dst diag(s) S_dst (the unit Schur complement) in W
-    int schur_mode = 1;       // 2D Schur apply: 0 factored (K1 + K2), 1 assembled (one GEMM with [F | G])
+    int schur_mode = 1;       // 2D Schur apply: 0 factored (K1 + K2), 1 assembled (one GEMM with [F | G]),
+                              // 2 grouped (one GEMM with H_p = K_p G + γ_p F per parameter set)
+    double* H = nullptr;      // grouped: n_param blocks of Mpad x Kpad (row-major, row stride Kpad)
     double* sw = nullptr;     // Schur weights s_b
     double* Kp = nullptr;     // [n_param]
     double* gp = nullptr;     // [n_param]

@@ -38,7 +38,13 @@ struct GemmArgs {
     // EPI_SCHUR_DST
     const int* col_param; const double* Kp; const double* gp; const double* s;
     const double* X; int ldx; double* Zlow;
+    // grouped A (EPI_STORE, 32-column tiles): tile [n0, n0+32) multiplies A + col_param[n0] * sG,
+    // unless *mixed (some tile spans two groups): then alt_A (M x alt_K) x alt_B for every tile
+    int grouped; long long sG; const int* mixed;
+    const double* alt_A; int alt_lda; const double* alt_B; int alt_ldb; int alt_K;
 };
+constexpr int GEMM_BN_GROUPED = 32;
+int gemm_pick_splitk_grouped(int M, int N, int K, int num_sms);
 
 int gemm_tiles(int M, int N);
 int gemm_pick_splitk(int M, int N, int K, int num_sms);   // 0 = stream-K
@@ -99,6 +105,7 @@ struct PcgState {
     // assembled 2D Schur apply: every new p is also written as the GEMM operand [γ_c p ; K_c p]
     double* zs; int ldz, zhalf;        // Z (column stride ldz), K-half at row zhalf (or zs = null)
     const double *Kp, *gp;             // per-parameter K, γ
+    const int* zmixed;                 // grouped apply: write zs only if *zmixed (fallback operand)
 };
 
 PoleGeom make_pole_geom(int n);
@@ -122,6 +129,11 @@ cudaError_t launch_pcg_small(const PcgState& s, const PoleGeom& g, const PoleTab
                              cudaStream_t st);
 cudaError_t launch_copy_cols(int n, int ncols, const double* src, int lds, double* dst, int ldd,
                              cudaStream_t st);
+// grouped Schur apply: *mixed = 1 if a 32-column tile holds two parameter sets
+cudaError_t launch_check_tiles(int ncols, const int* col_param, int* mixed, cudaStream_t st);
+// H_p = K_p G + γ_p F (W blocks at f_off, g_off) for all p: n rows, row stride ldh, H + p sH
+cudaError_t launch_group_operators(int n, int n_param, const double* W, int lda, int f_off, int g_off, const double* Kp,
+                                   const double* gp, double* H, int ldh, long long sH, cudaStream_t st);
 // Z[:, c] = [γ_c x_c ; K_c x_c] (rows 0.. and zhalf..): operand of the assembled Schur GEMM
 cudaError_t launch_schur_operand(int n, int ncols, const int* col_param, int n_param, const double* Kp,
                                  const double* gp, const double* x, int ldx, double* Z, int ldz, int zhalf,

@@ -49,9 +49,21 @@ struct DgemmProblem {
     const int* active = nullptr; // optional per-slab flag: slabs with active[b] == 0 are skipped
     unsigned long long* ts = nullptr;   // optional per-CTA phase timestamps (lab instrumentation)
     int a_static = 0;            // A is not written by the preceding kernel: prefetch it before griddepcontrol.wait
-    const int* ntl = nullptr;    // live column tiles [count, tile ids...] (PCG: columns freeze when converged):
+    const int* ntl = nullptr;    // live 64-column tiles [count, tile ids...] (PCG: columns freeze when converged):
                                  // the tile / stream-K work is laid out over the live tiles only
+    // Grouped A (tile kernel only): column tile [n0, n0+BN) multiplies A + col_group[n0] * sG —
+    // every BN-column tile must lie in one group — unless *mixed != 0 (flag written on the device
+    // before this launch), in which case the whole launch computes the fallback product
+    // alt_A (M x alt_K, lda alt_lda) x alt_B (ldb alt_ldb) instead.
+    const int* col_group = nullptr;
+    int n_group = 1;                    // group ids are clamped to [0, n_group)
+    long long sG = 0;
+    const int* mixed = nullptr;
+    const double* alt_A = nullptr; int alt_lda = 0;
+    const double* alt_B = nullptr; int alt_ldb = 0;
+    int alt_K = 0;
 };
+constexpr int DG_NTL_BN = 64;    // width of the live-tile list entries
 
 // Programmatic dependent launch (no-ops when the launch did not opt in)
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -141,17 +153,35 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
     const int m0 = (blockIdx.x % tiles_m) * C::BM;
     int n0 = (blockIdx.x / tiles_m) * C::BN;
     const int split = S > 1 ? (int)blockIdx.y : 0;
-    const int ktiles = g.K / C::BK;
-    const int per = (ktiles + S - 1) / S;
-    const int kt0 = split * per;
-    const int nkt = max(0, min(per, ktiles - kt0));
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wm = warp % C::WM, wn = warp / C::WM;
     const int gq = lane >> 2, tq = lane & 3;
 
-    // prologue: constant A stages may be fetched before the prerequisite grid has finished
-    const bool pre_a = g.a_static && !g.active;
+    // prologue: constant A stages may be fetched before the prerequisite grid has finished.
+    // Grouped A: the group ids and the mixed flag are written before the first PDL launch of
+    // a solve (their producers are launched without PDL), so they may be read here too — unless
+    // a live-tile list (written by the preceding kernel) decides which tile this CTA takes.
+    const bool pre_a = g.a_static && !g.active && !(g.col_group && g.ntl);
     const double* A0 = g.A + (size_t)bz * g.sA;
+    bool resolved = false;
+    auto resolve_group = [&]() {
+        if (g.mixed && *g.mixed) {           // uniform across the grid
+            A0 = g.alt_A; g.lda = g.alt_lda; g.B = g.alt_B; g.ldb = g.alt_ldb; g.K = g.alt_K;
+        } else {
+            int grp = n0 < g.N ? g.col_group[n0] : 0;
+            grp = grp < 0 ? 0 : (grp >= g.n_group ? g.n_group - 1 : grp);
+            A0 = g.A + (size_t)grp * g.sG;
+        }
+        resolved = true;
+    };
+    if (g.col_group && !g.ntl) resolve_group();
+    int nkt, kt0;
+    {
+        const int ktiles = g.K / C::BK;
+        const int per = (ktiles + S - 1) / S;
+        kt0 = split * per;
+        nkt = max(0, min(per, ktiles - kt0));
+    }
     if (pre_a) {
 #pragma unroll
         for (int s = 0; s < C::STAGES - 1; s++)
@@ -160,12 +190,25 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
     pdl_wait();
     if (g.active && !g.active[bz]) return;   // frozen slab (uniform across the cluster)
     if (g.ntl) {                             // live column tiles only (uniform across the cluster)
+        constexpr int SUB = DG_NTL_BN / C::BN;
+        static_assert(DG_NTL_BN % C::BN == 0, "live-tile width");
         const int nidx = blockIdx.x / tiles_m;
-        if (nidx >= g.ntl[0]) {
+        if (nidx / SUB >= g.ntl[0]) {
             asm volatile("cp.async.wait_all;\n" ::);   // drain the A prefetch before leaving
             return;
         }
-        n0 = g.ntl[1 + nidx] * C::BN;
+        n0 = g.ntl[1 + nidx / SUB] * DG_NTL_BN + (nidx % SUB) * C::BN;
+        if (n0 >= g.N) {                     // ragged half of the last live tile
+            asm volatile("cp.async.wait_all;\n" ::);
+            return;
+        }
+    }
+    if (g.col_group && !resolved) {
+        resolve_group();
+        const int ktiles = g.K / C::BK;
+        const int per = (ktiles + S - 1) / S;
+        kt0 = split * per;
+        nkt = max(0, min(per, ktiles - kt0));
     }
     DG_TS(0);
     g.A = A0;
@@ -302,9 +345,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProb
     __shared__ int s_last;
     pdl_launch_dependents();
     pdl_wait();
+    bool grouped = g.col_group != nullptr;
+    if (grouped && g.mixed && *g.mixed) {    // a tile spans two groups: fallback product (uniform)
+        g.A = g.alt_A; g.lda = g.alt_lda; g.B = g.alt_B; g.ldb = g.alt_ldb; g.K = g.alt_K;
+        grouped = false;
+    }
 
     const int tiles_m = (g.M + C::BM - 1) / C::BM;
-    const int tiles = tiles_m * (g.ntl ? g.ntl[0] : (g.N + C::BN - 1) / C::BN);
+    const int tiles = tiles_m * (g.ntl ? g.ntl[0] * (DG_NTL_BN / C::BN) : (g.N + C::BN - 1) / C::BN);
     const int KT = g.K / C::BK;
     const long long U = (long long)tiles * KT;
     const int b = blockIdx.x;
@@ -320,8 +368,16 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProb
         const int ks = (int)(u % KT);
         const int ke = (int)min((long long)KT, (long long)ks + (u1 - u));
         const int m0 = (t % tiles_m) * C::BM;
-        const int n0 = (g.ntl ? g.ntl[1 + t / tiles_m] : t / tiles_m) * C::BN;
+        const int n0 = g.ntl ? g.ntl[1 + (t / tiles_m) / (DG_NTL_BN / C::BN)] * DG_NTL_BN +
+                                   ((t / tiles_m) % (DG_NTL_BN / C::BN)) * C::BN
+                             : (t / tiles_m) * C::BN;
         const int nkt = ke - ks;
+        const double* Aseg = g.A;
+        if (grouped) {
+            int grp = n0 < g.N ? g.col_group[n0] : 0;
+            grp = grp < 0 ? 0 : (grp >= g.n_group ? g.n_group - 1 : grp);
+            Aseg = g.A + (size_t)grp * g.sG;
+        }
 
         double acc[C::MI][C::NI][4];
 #pragma unroll
@@ -332,7 +388,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProb
                 for (int r = 0; r < 4; r++) acc[i][j][r] = 0.0;
 
         auto load_stage = [&](int stage, int kt) {
-            dg_load_stage<C>(As + stage * C::BM * C::LDS, Bs + stage * C::BN * C::LDS, g.A, g.lda, g.B, g.ldb, m0, n0,
+            dg_load_stage<C>(As + stage * C::BM * C::LDS, Bs + stage * C::BN * C::LDS, Aseg, g.lda, g.B, g.ldb, m0, n0,
                              kt * C::BK, tid);
         };
         __syncthreads();   // previous segment's smem reads are finished

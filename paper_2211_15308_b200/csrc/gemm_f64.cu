@@ -8,6 +8,8 @@
 //   * cluster split-K (DSMEM reduction) for small problems (config 2), where stream-K's
 //     segment fix-ups cost more than the imbalance they remove.
 // Both reduce partial sums in a fixed order: results are bitwise reproducible.
+#include <cstdlib>
+
 #include "dd_internal.h"
 #include "dgemm_tile.cuh"
 
@@ -15,7 +17,9 @@ namespace dd {
 
 using CfgC = DgemmCfg<64, 64, 16, 2, 2, 4, 2>;   // cluster split-K: 4-stage ring, 2 CTAs/SM
 using CfgS = DgemmCfg<64, 64, 16, 2, 2, 3, 3>;   // stream-K: 3-stage ring, run at 2 CTAs/SM
-constexpr int OCC_C = 2, OCC_S = 2;
+using CfgG = DgemmCfg<128, 32, 16, 4, 1, 3, 2>; // grouped per-parameter GEMM: 32-column tiles (tools/gemm_lab5.cu)
+constexpr int OCC_C = 2, OCC_S = 2, OCC_G = 2;
+static_assert(CfgG::BN == GEMM_BN_GROUPED, "grouped tile width");
 constexpr int SK_MIN_UNITS = 64;   // below this the segment fix-ups outweigh the balance gain
 
 struct EpiStore {
@@ -44,7 +48,11 @@ struct EpiSchurDst {
     }
 };
 
-int gemm_tiles(int M, int N) { return dgemm_tiles<CfgC>(M, N); }
+int gemm_tiles(int M, int N) {
+    // grouped: live-tile lists address 64-column tiles, i.e. up to round_up(N, 64) / 32 tiles
+    const int a = dgemm_tiles<CfgC>(M, N), b = dgemm_tiles<CfgG>(M, (N + 63) / 64 * 64);
+    return a > b ? a : b;
+}
 
 static bool use_streamk(int M, int N, int K, int num_sms) {
     const long long U = (long long)dgemm_tiles<CfgS>(M, N) * (K / CfgS::BK);
@@ -56,8 +64,18 @@ int gemm_pick_splitk(int M, int N, int K, int num_sms) {
     return dgemm_pick_splitk<CfgC>(M, N, K, num_sms, OCC_C);
 }
 
+int gemm_pick_splitk_grouped(int M, int N, int K, int num_sms) {
+    if (std::getenv("DD_GROUPED_NO_SK") == nullptr || std::getenv("DD_GROUPED_NO_SK")[0] != '1') {
+        const long long U = (long long)dgemm_tiles<CfgG>(M, N) * (K / CfgG::BK);
+        if (U / ((long long)num_sms * OCC_G) >= SK_MIN_UNITS) return 0;   // stream-K
+    }
+    return dgemm_pick_splitk<CfgG>(M, N, K, num_sms, OCC_G);
+}
+
 size_t gemm_ws_doubles(int M, int N, int num_sms) {
-    return dgemm_streamk_ws_doubles<CfgS>(M, N, num_sms * OCC_S);
+    const size_t a = dgemm_streamk_ws_doubles<CfgS>(M, N, num_sms * OCC_S);
+    const size_t b = dgemm_streamk_ws_doubles<CfgG>(M, (N + 63) / 64 * 64, num_sms * OCC_G);
+    return a > b ? a : b;
 }
 
 template <class Epi>
@@ -77,6 +95,19 @@ static cudaError_t launch(const GemmArgs& a, const Epi& e, cudaStream_t st) {
 
 cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
     if (a.M <= 0 || a.N <= 0) return cudaSuccess;
+    if (a.grouped) {
+        DgemmProblem g{a.M, a.N, a.K, a.A, a.lda, a.B, a.ldb};
+        g.ntl = a.ntl;
+        g.col_group = a.col_param; g.n_group = a.n_param; g.sG = a.sG; g.mixed = a.mixed;
+        g.alt_A = a.alt_A; g.alt_lda = a.alt_lda; g.alt_B = a.alt_B; g.alt_ldb = a.alt_ldb; g.alt_K = a.alt_K;
+        if (a.splitk == 0) {
+            // stream-K over the live 32-column tiles; the unit count follows the fallback's K too
+            StreamK sk{a.ws, a.counters, 0};
+            const int G = dgemm_streamk_grid<CfgG>(a.M, a.N, a.K, a.num_sms, OCC_G);
+            return dgemm_launch_streamk<CfgG>(g, G, sk, EpiStore{a.C, a.ldc}, st, false);
+        }
+        return dgemm_launch<CfgG>(g, a.splitk, EpiStore{a.C, a.ldc}, st, a.pdl != 0);
+    }
     if (a.epi == EPI_STORE) return launch(a, EpiStore{a.C, a.ldc}, st);
     if (a.epi == EPI_ADD) return launch(a, EpiAdd{a.C, a.ldc, a.X, a.ldx}, st);
     return launch(a, EpiSchurDst{a.C, a.ldc, a.Zlow, a.X, a.ldx, a.col_param, a.n_param, a.Kp, a.gp, a.s}, st);

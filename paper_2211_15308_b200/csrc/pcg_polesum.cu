@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
         rz += S.R[tpos(i, g)] * zi;
         zz += zi * zi;
         s.p[off + i] = zi;
-        if (s.zs) {
+        if (s.zs && (!s.zmixed || *s.zmixed)) {
             s.zs[(size_t)c * s.ldz + i] = s.gp[param] * zi;
             s.zs[(size_t)c * s.ldz + s.zhalf + i] = s.Kp[param] * zi;
         }
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
                 if (threadIdx.x == 0) s.active[c] = 0;
             } else {
                 const double beta = rz / s.rho[c];
-                if (s.zs) {
+                if (s.zs && (!s.zmixed || *s.zmixed)) {
                     // assembled Schur apply: the next GEMM's operand [γ p ; K p] written with p
                     const double gc = s.gp[param], Kc = s.Kp[param];
                     double* zc = s.zs + (size_t)c * s.ldz;
@@ -892,6 +892,28 @@ __global__ void k_schur_operand(int n, int ncols, const int* __restrict__ col_pa
     }
 }
 
+// Grouped Schur apply: does any 32-column tile hold two parameter sets?  (*mixed |= 1)
+__global__ void k_check_tiles(int ncols, const int* __restrict__ col_param, int* mixed) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
+        const int c0 = c - c % GEMM_BN_GROUPED;
+        if (col_param[c] != col_param[c0]) atomicExch(mixed, 1);
+    }
+}
+
+// H_p = K_p G + γ_p F for every parameter set p (rows of n, row stride ldh; padded entries 0)
+__global__ void k_group_operators(int n, int n_param, const double* __restrict__ W, int lda, int f_off, int g_off,
+                                  const double* __restrict__ Kp, const double* __restrict__ gp, double* __restrict__ H,
+                                  int ldh, long long sH) {
+    const size_t total = (size_t)n * ldh;
+    for (int p = 0; p < n_param; p++) {
+        const double K = Kp[p], g = gp[p];
+        for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+            const size_t i = idx / ldh, k = idx % ldh;
+            H[p * sH + idx] = k < (size_t)n ? fma(K, W[i * lda + g_off + k], g * W[i * lda + f_off + k]) : 0.0;
+        }
+    }
+}
+
 __global__ void k_check_params(int ncols, const int* col_param, int n_param, int* flag) {
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
         const int p = col_param[c];
@@ -1053,6 +1075,19 @@ cudaError_t launch_schur_operand(int n, int ncols, const int* col_param, int n_p
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
     k_schur_operand<<<blocks, 256, 0, st>>>(n, ncols, col_param, n_param, Kp, gp, x, ldx, Z, ldz, zhalf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_tiles(int ncols, const int* col_param, int* mixed, cudaStream_t st) {
+    if (ncols <= 0) return cudaSuccess;
+    k_check_tiles<<<(ncols + 255) / 256, 256, 0, st>>>(ncols, col_param, mixed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_group_operators(int n, int n_param, const double* W, int lda, int f_off, int g_off, const double* Kp,
+                                   const double* gp, double* H, int ldh, long long sH, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_group_operators<<<148 * 8, 256, 0, st>>>(n, n_param, W, lda, f_off, g_off, Kp, gp, H, ldh, sH);
     return cudaGetLastError();
 }
 

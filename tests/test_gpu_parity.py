@@ -64,14 +64,17 @@ def small_case(request, lib):
     S.close()
 
 
-@pytest.mark.parametrize("mode", ["assembled", "factored"])
+MODES = ["grouped", "assembled", "factored"]
+
+
+@pytest.mark.parametrize("mode", MODES)
 def test_schur_apply_parity_small(small_case, mode):
     N, params, ras, D, S, B, colp = small_case
     S.set_schur_mode(mode)
     try:
         y = S.apply_schur(_cols(B), colp).cpu().numpy()
     finally:
-        S.set_schur_mode("assembled")
+        S.set_schur_mode("grouped")
     ref = np.stack([D.apply_S(*params[colp[c]], B[c]) for c in range(B.shape[0])])
     assert rel_l2_cols(y, ref) <= 1e-10
 
@@ -172,7 +175,7 @@ def test_small_persistent_kernel_matches_general_path(lib, N, monkeypatch):
         S1.close(); S2.close()
 
 
-@pytest.mark.parametrize("mode", ["assembled", "factored"])
+@pytest.mark.parametrize("mode", MODES)
 def test_profile_and_launch_counts(lib, mode):
     N = 96; params = [(1.0, 1e2)]; ras = fit_all(N, params, 8)
     S = _solver(lib, N, params, ras, max_cols=8)
@@ -193,9 +196,12 @@ def test_profile_and_launch_counts(lib, mode):
             assert prof["gemm_dst"][1] == k
             assert n_launch == 2 + 3 * k        # check_params, init, then K1 + K2 + pole sum per iteration
             assert all(v[0] > 0 for v in prof.values())
-        else:
+        elif mode == "assembled":
             assert prof["gemm_dst"][1] == 0     # the interior solve lives in G (setup)
             assert n_launch == 2 + 2 * k        # check_params, init, then [F | G] GEMM + pole sum
+        else:
+            assert prof["gemm_dst"][1] == 0
+            assert n_launch == 3 + 2 * k        # + the 32-column tile check, then H_p GEMM + pole sum
         with pytest.raises(lib.DDError):
             S.set_schur_mode("bogus")
     finally:
@@ -203,7 +209,7 @@ def test_profile_and_launch_counts(lib, mode):
 
 
 # ------------------------------------------------------------------------- ragged large sizes (G = 2, 4 groups)
-@pytest.mark.parametrize("mode", ["assembled", "factored"])
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("N,C", [(1500, 13), (3001, 7), (2049, 3)])
 def test_ragged_large_parity(lib, N, C, mode):
     """Interfaces whose chunking uses 2- and 4-warp groups with a partial last chunk, and column
@@ -277,23 +283,60 @@ def test_full_config_parity(lib, cfg):
 
 @pytest.mark.parametrize("name", ["cfg2_2d_N1024_sweep", "cfg5_2d_N2048_darcy"])
 def test_schur_modes_agree_full_size(lib, name):
-    """The assembled apply ([F | G] [γX ; KX], G formed at setup) and the factored one (fast
-    diagonalisation per apply) are the same operator: at full config size they agree to rounding
-    and give the same PCG iterates (both are pinned to the oracle above at smaller sizes)."""
+    """The grouped apply (H_p = K_p G + γ_p F per parameter set), the assembled one ([F | G]
+    [γX ; KX]) and the factored one (fast diagonalisation per apply) are the same operator: at
+    full config size they agree to rounding and give the same PCG iterates (each is pinned to
+    the oracle above at smaller sizes)."""
     cfg = configs.BY_NAME[name]
     ras = fit_all(cfg.N, cfg.params, cfg.n_poles)
     B, colp = inputs.batch(cfg.n_gamma, len(cfg.params), cfg.rhs_per_param)
     S = _solver(lib, cfg.N, cfg.params, ras, max_cols=cfg.n_cols)
     try:
         Bt = _cols(B)
-        ya = S.apply_schur(Bt, colp).cpu().numpy()
-        ra = S.pcg_solve(Bt, colp, rtol=cfg.rtol, maxit=cfg.maxit)
-        S.set_schur_mode("factored")
-        yf = S.apply_schur(Bt, colp).cpu().numpy()
-        rf = S.pcg_solve(Bt, colp, rtol=cfg.rtol, maxit=cfg.maxit)
-        assert rel_l2_cols(ya, yf) <= 1e-13
-        assert np.all(np.abs(ra.iters - rf.iters) <= 1)
-        assert rel_l2_cols(ra.x.cpu().numpy(), rf.x.cpu().numpy()) <= 1e-8
+        out = {}
+        for mode in MODES:
+            S.set_schur_mode(mode)
+            out[mode] = (S.apply_schur(Bt, colp).cpu().numpy(), S.pcg_solve(Bt, colp, rtol=cfg.rtol, maxit=cfg.maxit))
+        yg, rg = out["grouped"]
+        for mode in ("assembled", "factored"):
+            y, r = out[mode]
+            assert rel_l2_cols(y, yg) <= 1e-13
+            assert np.all(np.abs(r.iters - rg.iters) <= 1)
+            assert rel_l2_cols(r.x.cpu().numpy(), rg.x.cpu().numpy()) <= 1e-8
+    finally:
+        S.close()
+
+
+@pytest.mark.parametrize("layout", ["grouped32", "grouped_ragged", "mixed"])
+def test_grouped_layouts(lib, layout):
+    """Grouped apply on column layouts whose 32-column tiles hold one parameter set each (the
+    H_p path, incl. a ragged last group and a multi-tile group) and on an interleaved layout
+    (a tile holds several sets: the device-side fallback to [F | G]); against the oracle."""
+    N = 700
+    params = [(1.0, 1e2), (1e-4, 1e6), (1e-2, 1.0)]
+    ras = fit_all(N, params, 16)
+    Mo = oprob.ModeProblem2D(N)
+    colp = {"grouped32": np.repeat([0, 1, 2], 32),
+            "grouped_ragged": np.concatenate([np.repeat([2], 64), np.repeat([0], 32), np.repeat([1], 7)]),
+            "mixed": np.arange(45) % 3}[layout].astype(np.int32)
+    C = len(colp)
+    B = np.random.default_rng(C).uniform(-1, 1, (C, N - 1))
+    S = _solver(lib, N, params, ras, max_cols=C)
+    try:
+        y = S.apply_schur(_cols(B), colp).cpu().numpy()
+        assert S.query_config()["splitk_dst"] == -2          # grouped is the dense-F default
+        ref = np.stack([Mo.apply_S(*params[colp[c]], B[c]) for c in range(C)])
+        assert rel_l2_cols(y, ref) <= 1e-10
+        res = S.pcg_solve(_cols(B), colp)
+        x = res.x.cpu().numpy()
+        for p in range(len(params)):
+            sel = np.nonzero(colp == p)[0]
+            K, g = params[p]; ra = ras[p]
+            X, its, rel, _ = opcg.pcg_batch(lambda V, cols: Mo.apply_S(K, g, V),
+                                            lambda V, cols: Mo.apply_P_ra(ra.c0, ra.poles, ra.residues, V),
+                                            B[sel].T)
+            assert np.all(np.abs(res.iters[sel] - its) <= 1)
+            assert rel_l2_cols(x[sel], X.T) <= 1e-8
     finally:
         S.close()
 
