@@ -360,7 +360,8 @@ def main():
                     "frac": round(ach / hbm, 4) if ach else None,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if mp else "fallback 6650 GB/s",
                     "bytes_per_launch": bytes_fx}
-        roof.update({"traffic": traffic_for(cfg.name, "gemm_schur"),
+        tkey = "gemm_schur" if cfg.dim == 3 else "gemm_schur_" + roof.get("schur_mode", "factored")
+        roof.update({"traffic": traffic_for(cfg.name, tkey), "traffic_key": tkey,
                      "avg_launch_us": round(g2_ms / g2_n * 1e3, 2) if g2_n else None,
                      "share_of_step": {k: round(v[0] / total_prof_ms, 4) for k, v in prof.items()},
                      "avg_us": {k: round(v[0] / v[1] * 1e3, 2) if v[1] else None for k, v in prof.items()}})
