@@ -429,6 +429,9 @@ extern "C" dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n
     if (cudaMemsetAsync(c->active, 0, sizeof(int) * (2 * (size_t)max_cols + 16), c->stream) != cudaSuccess)
         return bail(fail(DD_ECUDA, "memset"));
     if (cudaMallocHost(&c->h_ints, sizeof(int) * 16) != cudaSuccess) return bail(fail(DD_ENOMEM, "pinned"));
+    if (cudaMallocHost(&c->h_iters, sizeof(int) * (size_t)max_cols) != cudaSuccess ||
+        cudaMallocHost(&c->h_rel, sizeof(double) * (size_t)max_cols) != cudaSuccess)
+        return bail(fail(DD_ENOMEM, "pinned"));
     if (want_dbg && dalloc(c, &c->dbg, 16) != cudaSuccess) return bail(fail(DD_ENOMEM, "dbg"));
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DD_ECUDA, "setup sync"));
     if (c->dim == 2) {
@@ -669,8 +672,17 @@ static dd_status build_graph(dd_ctx* c, const PcgState& s0, cudaGraphExec_t* out
     return DD_OK;
 }
 
+static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol,
+                                int maxit, int norm_kind, int* iters, double* rel_res, double* hist, double* x_host);
+
 extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol,
                                   int maxit, int norm_kind, int* iters, double* rel_res, double* hist) {
+    return pcg_solve_impl(c, ncols, colp, b, x, rtol, maxit, norm_kind, iters, rel_res, hist, nullptr);
+}
+
+// x_host: also copy x (n_Γ x ncols) to this host buffer before the one synchronisation
+static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol,
+                                int maxit, int norm_kind, int* iters, double* rel_res, double* hist, double* x_host) {
     dd_status s = check_cols(c, ncols, colp);
     if (s != DD_OK) return s;
     if (ncols > 0 && (!b || !x)) return fail(DD_EINVAL, "b/x NULL");
@@ -747,10 +759,14 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
     }
     }
     CK(cudaEventRecord(c->solve_ev[1], c->stream));
-    if (iters) CK(cudaMemcpyAsync(iters, c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c->stream));
-    if (rel_res) CK(cudaMemcpyAsync(rel_res, c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost, c->stream));
+    // everything the host needs comes back in one batch before the single synchronisation
+    if (x_host) CK(cudaMemcpyAsync(x_host, x, sizeof(double) * (size_t)c->ng * ncols, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_iters, c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_rel, c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(c->h_ints, c->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if (iters) std::memcpy(iters, c->h_iters, sizeof(int) * ncols);
+    if (rel_res) std::memcpy(rel_res, c->h_rel, sizeof(double) * ncols);
     const int kdone = c->h_ints[0];
     if (c->dbg) {
         long long t[16] = {0};
@@ -763,22 +779,14 @@ extern "C" dd_status dd_pcg_solve(dd_ctx* c, int ncols, const int* colp, const d
     if (c->last_graph) c->launches += c->graph_iter_launches * kdone;
     if (hist) {
         // column 0 history: η_0 .. η_{iters[0]}
-        int it0 = 0;
-        CK(cudaMemcpy(&it0, c->iters, sizeof(int), cudaMemcpyDeviceToHost));
+        const int it0 = c->h_iters[0];
         CK(cudaMemcpy(hist, c->hist, sizeof(double) * (it0 + 1), cudaMemcpyDeviceToHost));
     }
     if (c->h_ints[5]) return fail(DD_EINVAL, "col_param entry out of range (clamped; outputs undefined)");
     if (c->h_ints[4] == DD_ENOTSPD) return fail(DD_ENOTSPD, "p.Sp <= 0 or r.Pr < 0 in PCG");
     // any column still active after maxit iterations?
-    std::vector<int> itv(ncols);
-    if (!iters) {
-        CK(cudaMemcpy(itv.data(), c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost));
-        iters = itv.data();
-    }
-    std::vector<double> rr(ncols);
-    CK(cudaMemcpy(rr.data(), c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost));
     for (int i = 0; i < ncols; i++)
-        if (iters[i] >= maxit && !(rr[i] <= rtol)) return fail(DD_ENOCONV, "maxit reached");
+        if (c->h_iters[i] >= maxit && !(c->h_rel[i] <= rtol)) return fail(DD_ENOCONV, "maxit reached");
     return DD_OK;
 }
 
@@ -794,11 +802,7 @@ extern "C" dd_status dd_pcg_solve_host(dd_ctx* c, int ncols, const int* colp_h, 
     CK(cudaSetDevice(c->device));
     CK(cudaMemcpyAsync(c->colp_st, colp_h, sizeof(int) * ncols, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->bst, b_h, sizeof(double) * (size_t)c->ng * ncols, cudaMemcpyHostToDevice, c->stream));
-    dd_status r = dd_pcg_solve(c, ncols, c->colp_st, c->bst, c->xst, rtol, maxit, norm_kind, iters, rel_res, hist);
-    if (r != DD_OK && r != DD_ENOCONV && r != DD_ENOTSPD) return r;
-    CK(cudaMemcpyAsync(x_h, c->xst, sizeof(double) * (size_t)c->ng * ncols, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    return r;
+    return pcg_solve_impl(c, ncols, c->colp_st, c->bst, c->xst, rtol, maxit, norm_kind, iters, rel_res, hist, x_h);
 }
 
 // ------------------------------------------------------------------------------------ bulk solve
@@ -989,6 +993,8 @@ extern "C" dd_status dd_destroy(dd_ctx* c) {
     for (auto& e : c->ev_free) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (void* p : c->allocs) cudaFree(p);
     if (c->h_ints) cudaFreeHost(c->h_ints);
+    if (c->h_iters) cudaFreeHost(c->h_iters);
+    if (c->h_rel) cudaFreeHost(c->h_rel);
     delete c;
     return DD_OK;
 }

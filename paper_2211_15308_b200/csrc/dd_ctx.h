@@ -131,6 +131,8 @@ struct dd_ctx {
     int hist_cap = 0;
     // pinned host mirrors
     int* h_ints = nullptr;
+    int* h_iters = nullptr;       // pinned staging of the per-column results [max_cols]
+    double* h_rel = nullptr;
     // profiling
     bool prof = false;
     std::vector<dd::EvPair> ev_pending, ev_free;

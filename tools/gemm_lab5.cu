@@ -84,12 +84,17 @@ int main() {
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         printf("{\"variant\": \"cublas_batched\", \"P\": %d, \"M\": %d, \"N\": %d, \"K\": %d, \"us\": %.2f, \"tflops\": %.2f}\n", P,
                M, N, K, ms * 1e3 / 20, 2.0 * M * N * K * P / (ms * 1e3 / 20) / 1e6);
+        if (getenv("LAB_SMALL") && s.P != 4) continue;
         run_variant<DgemmCfg<64, 64, 16, 2, 2, 4, 2>>("64x64k16_w2x2_s4", P, M, N, K, Mp, A, B, C, Cr, sms);
-        run_variant<DgemmCfg<64, 32, 16, 2, 1, 4, 4>>("64x32k16_w2x1_s4", P, M, N, K, Mp, A, B, C, Cr, sms);
         run_variant<DgemmCfg<128, 32, 16, 4, 1, 3, 2>>("128x32k16_w4x1_s3", P, M, N, K, Mp, A, B, C, Cr, sms);
-        run_variant<DgemmCfg<128, 32, 16, 4, 1, 4, 2>>("128x32k16_w4x1_s4", P, M, N, K, Mp, A, B, C, Cr, sms);
-        run_variant<DgemmCfg<64, 32, 16, 2, 1, 6, 4>>("64x32k16_w2x1_s6", P, M, N, K, Mp, A, B, C, Cr, sms);
-        run_variant<DgemmCfg<32, 32, 16, 1, 1, 4, 8>>("32x32k16_w1x1_s4", P, M, N, K, Mp, A, B, C, Cr, sms);
+        run_variant<DgemmCfg<128, 32, 32, 4, 1, 3, 2>>("128x32k32_w4x1_s3", P, M, N, K, Mp, A, B, C, Cr, sms);
+        run_variant<DgemmCfg<128, 32, 32, 4, 1, 2, 2>>("128x32k32_w4x1_s2", P, M, N, K, Mp, A, B, C, Cr, sms);
+        run_variant<DgemmCfg<128, 32, 16, 4, 1, 5, 2>>("128x32k16_w4x1_s5", P, M, N, K, Mp, A, B, C, Cr, sms);
+        run_variant<DgemmCfg<128, 32, 16, 2, 1, 3, 2>>("128x32k16_w2x1_s3", P, M, N, K, Mp, A, B, C, Cr, sms);
+        run_variant<DgemmCfg<64, 32, 32, 2, 1, 3, 4>>("64x32k32_w2x1_s3", P, M, N, K, Mp, A, B, C, Cr, sms);
+        run_variant<DgemmCfg<256, 32, 16, 8, 1, 3, 1>>("256x32k16_w8x1_s3", P, M, N, K, Mp, A, B, C, Cr, sms);
+        run_variant<DgemmCfg<128, 64, 16, 4, 2, 3, 1>>("128x64k16_w4x2_s3", P, M, N, K, Mp, A, B, C, Cr, sms);
+        run_variant<DgemmCfg<64, 64, 32, 2, 2, 3, 2>>("64x64k32_w2x2_s3", P, M, N, K, Mp, A, B, C, Cr, sms);
         cudaFree(A); cudaFree(B); cudaFree(C); cudaFree(Cr);
     }
     return 0;
