@@ -135,6 +135,26 @@ def oracle_sample(cfg, ras, B, colp, per_param: int, t: float = -0.5, sigma: flo
     return solves, time.perf_counter() - t0
 
 
+def host_info():
+    """CPU model, usable cores and BLAS of the host the oracle runs on (SURVEY §8(d) oracle timing)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [f"{i.get('internal_api')} {i.get('version')} x{i.get('num_threads')}" for i in threadpool_info()]
+    except Exception:
+        pass
+    return {"cpu_model": model, "affinity_cores": len(os.sched_getaffinity(0)), "blas": blas}
+
+
 def cores_used():
     try:
         from threadpoolctl import threadpool_info
@@ -399,7 +419,8 @@ def main():
             line["cpu_baseline"] = {"value": round(solves / secs, 4), "unit": UNIT, "cores": cores_used(),
                                     "kind": "oracle",
                                     "sample": f"{solves} of the {C} solves ({per} per parameter set), oracle mode tier "
-                                              f"(scipy DST + LAPACK banded Cholesky), {secs:.1f} s"}
+                                              f"(scipy DST + LAPACK banded Cholesky), {secs:.1f} s",
+                                    "host": host_info()}
         print(json.dumps(line), flush=True)
     S.close()
     if world > 1:
@@ -482,7 +503,8 @@ def run_reference(args, cfg, world, rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "solves_per_step": per * len(cfg.params)},
             "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": cores_used(), "kind": "oracle",
-                             "sample": f"{per} solves per parameter set per step (of {cfg.rhs_per_param}), oracle mode tier"},
+                             "sample": f"{per} solves per parameter set per step (of {cfg.rhs_per_param}), oracle mode tier",
+                             "host": host_info()},
             "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
