@@ -74,6 +74,33 @@ def test_ra_mode_rejects_bad_fit(lib):
         lib.Solver(3, 6, [(1.0, 1.0)], ras, max_cols=1, frac=lib.Frac(mode="ra", fra=Bad()))
 
 
+def test_schur_mode_rules(lib):
+    """dd_set_schur_mode (include/dd_api.h): RA handles default to assembled and refuse grouped
+    (no dense F to fold in); 3D handles refuse every 2D mode switch."""
+    N = 64
+    lo, hi = rafit.interval_1d(N)
+    params = [(1.0, 1e2)]
+    ras = [rafit.fit_ra(K, g, lo, hi, 10) for K, g in params]
+    S = lib.Solver(2, N, params, ras, max_cols=2,
+                   frac=lib.Frac(mode="ra", fra=rafit.fit_power(-0.5, lo, hi, 12, 0.0)))
+    try:
+        S.apply_schur(torch.zeros((2, N - 1), dtype=torch.float64, device="cuda"), [0, 0])
+        assert S.query_config()["splitk_dst"] == -1      # assembled
+        with pytest.raises(lib.DDError):
+            S.set_schur_mode("grouped")
+        S.set_schur_mode("factored")
+    finally:
+        S.close()
+    lo3, hi3 = rafit.interval_face(8)
+    S3 = lib.Solver(3, 8, params, [rafit.fit_ra(1.0, 1e2, lo3, hi3, 10)], max_cols=1)
+    try:
+        for mode in ("factored", "assembled", "grouped"):
+            with pytest.raises(lib.DDError):
+                S3.set_schur_mode(mode)
+    finally:
+        S3.close()
+
+
 @pytest.mark.parametrize("N", [8, 13])
 def test_ra_operator_3d(lib, N):
     """Remark 1 on a 3D face (the survey's motivation for NEXT-2: no dense n_Γ^2 F): y = K S_unit x
