@@ -204,6 +204,10 @@ def main():
     ap.add_argument("--mode", default="schur", choices=["schur", "bulk", "bulk-pcg"],
                     help="schur: interface PCG (headline); bulk: full DD solve on bulk RHS (NEXT-1); "
                          "bulk-pcg: PCG on the bulk system with the Eq.(5) DD preconditioner (the paper's protocol)")
+    ap.add_argument("--pole-split", action="store_true",
+                    help="3D (config 4, SURVEY §8(e)): all ranks solve the same columns, the RA poles are split "
+                         "across ranks and the partial sums allreduced over NCCL each preconditioner apply "
+                         "(strong scaling); default: columns per rank (weak scaling, no collective)")
     ap.add_argument("--schur", default=None, choices=["grouped", "assembled", "factored"],
                     help="2D Schur apply (dd_set_schur_mode): grouped = one GEMM with H_p = K_p G + gamma_p F per "
                          "parameter set (default, dense F); assembled = one [F|G] GEMM (default in RA mode); "
@@ -231,8 +235,18 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     sigma = 1.0 if args.shifted else 0.0
     ras = fit_ras(cfg, args.t, sigma)
-    B, colp = inputs.batch(cfg.n_gamma, len(cfg.params), cfg.rhs_per_param, seed_offset=rank * len(cfg.params))
+    split = bool(args.pole_split and cfg.dim == 3)
+    # pole split: every rank holds the same columns (the exchange is inside the preconditioner)
+    B, colp = inputs.batch(cfg.n_gamma, len(cfg.params), cfg.rhs_per_param,
+                           seed_offset=0 if split else rank * len(cfg.params))
     C = B.shape[0]
+    ddist = None
+    if split:
+        from paper_2211_15308_b200 import dist as ddist_mod
+        uid = binding.nccl_unique_id() if rank == 0 else None
+        if world > 1:
+            uid = ddist_mod.broadcast_bytes(uid, 128, device=f"cuda:{local}")
+        ddist = (rank, world, 1, uid if world > 1 else None)   # DD_SHARD_POLES
     frac = binding.Frac(t=args.t, shifted=args.shifted)
     if args.frac_mode == "ra":
         lo, hi = rafit.interval_1d(cfg.N) if cfg.dim == 2 else rafit.interval_face(cfg.N)
@@ -240,7 +254,7 @@ def main():
                             fra=rafit.fit_power(args.t, lo, hi, cfg.n_poles, sigma))
     torch.cuda.synchronize()
     t_setup = time.perf_counter()
-    S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local, frac=frac)
+    S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local, frac=frac, dist=ddist)
     if cfg.dim == 2:
         S.set_schur_mode(args.schur)
     torch.cuda.synchronize()
@@ -278,7 +292,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    solves_total = C * args.steps * world
+    solves_total = C * args.steps * (1 if split else world)
     value = solves_total / (max_ms / 1e3)
 
     # ---- instrumented pass: per-kernel-class device time (CUDA events on libdd's stream)
@@ -306,7 +320,7 @@ def main():
     te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = C * len(e2e_t) * world / float(te.item())
+    e2e_value = C * len(e2e_t) * (1 if split else world) / float(te.item())
 
     # ---- precond applies/s (secondary metric of BASELINE.json)
     Z = torch.empty_like(Bt)
@@ -320,7 +334,7 @@ def main():
         S.apply_precond(Bt, cp, z=Z)
     e1.record(S.stream)
     torch.cuda.synchronize()
-    pa_per_s = C * reps * world / (e0.elapsed_time(e1) / 1e3)
+    pa_per_s = C * reps * (1 if split else world) / (e0.elapsed_time(e1) / 1e3)
 
     if rank == 0:
         n = cfg.n
@@ -388,13 +402,15 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if split else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "dim": cfg.dim, "cells_per_side": cfg.N, "n_gamma": cfg.n_gamma,
                        "param_sets": len(cfg.params), "rhs_per_param": cfg.rhs_per_param, "solves_per_step": C,
                        "poles": cfg.n_poles, "rtol": cfg.rtol, "l2": "flushed (512 MiB write) between timed steps",
                        "schur_apply": args.schur if cfg.dim == 2 else "factored (3D)",
                        "setup_ms_untimed": round(setup_ms, 1),
-                       "parallelism": f"columns sharded, {world} rank(s), no collective",
+                       "parallelism": (f"RA poles split over {world} rank(s), NCCL allreduce of the partial "
+                                       f"sums per preconditioner apply" if split else
+                                       f"columns sharded, {world} rank(s), no collective"),
                        "fractional_term": "dense F (Eq.(7))" if args.frac_mode == "dense"
                        else f"RA-evaluated (Remark 1), {cfg.n_poles} poles",
                        "t": args.t, "L": "-Δ_Γ + I" if args.shifted else "-Δ_Γ",
