@@ -478,7 +478,7 @@ static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double
         g.splitk = gemm_pick_splitk_grouped(n, ncols, c->Kpad, c->num_sms);
         g.ws = c->gws; g.counters = c->gcnt; g.num_sms = c->num_sms;
         g.epi = EPI_STORE;
-        g.pdl = c->pdl;
+        g.pdl = c->pdl; g.a_static = 1;     // H_p is constant: prefetched before griddepcontrol.wait
         g.ntl = ntl;
         c->last_split1 = -2;
         c->last_split2 = g.splitk;

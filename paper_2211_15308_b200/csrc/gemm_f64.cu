@@ -98,6 +98,7 @@ cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
     if (a.grouped) {
         DgemmProblem g{a.M, a.N, a.K, a.A, a.lda, a.B, a.ldb};
         g.ntl = a.ntl;
+        g.a_static = a.a_static;
         g.col_group = a.col_param; g.n_group = a.n_param; g.sG = a.sG; g.mixed = a.mixed;
         g.alt_A = a.alt_A; g.alt_lda = a.alt_lda; g.alt_B = a.alt_B; g.alt_ldb = a.alt_ldb; g.alt_K = a.alt_K;
         if (a.splitk == 0) {
