@@ -65,7 +65,8 @@ int gemm_pick_splitk(int M, int N, int K, int num_sms) {
 }
 
 int gemm_pick_splitk_grouped(int M, int N, int K, int num_sms) {
-    if (std::getenv("DD_GROUPED_NO_SK") == nullptr || std::getenv("DD_GROUPED_NO_SK")[0] != '1') {
+    static const bool no_sk = std::getenv("DD_GROUPED_NO_SK") && std::getenv("DD_GROUPED_NO_SK")[0] == '1';
+    if (!no_sk) {
         const long long U = (long long)dgemm_tiles<CfgG>(M, N) * (K / CfgG::BK);
         if (U / ((long long)num_sms * OCC_G) >= SK_MIN_UNITS) return 0;   // stream-K
     }
