@@ -114,10 +114,34 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
         DD_CK(face_mass_cols(n, hh12, dA, dM, n2, n2, c->stream));
         DD_CK(cudaMemsetAsync(dA, 0, big * sizeof(double), c->stream));
         DD_CK(scale_transpose(dM, dW, n2, dA, kp, c->stream));
-        const size_t frows = (size_t)round_up((int)f.NP, 128);
-        DD_CK(dalloc(c, &f.F, frows * (size_t)f.NP));
-        DD_CK(face_gram_scatter(dA, n2, kp, f.F, n, f.ldf, f.NP, c->num_sms, c->stream));
+        const size_t frows = (size_t)round_up((int)f.NP, 256);
+        // packed-symmetric F (row a-3 option, half the bytes and half the memory) is opt-in: at 8
+        // columns its per-block cross-warp reduction leaves it latency-bound (423 vs 391 µs per
+        // apply for the full-F stream at 83 % of HBM)
+        const char* fp = std::getenv("DD_FX_PACKED");
+        const bool packed = fx_sym_supported(f.NP) && fp && fp[0] == '1';
+        double* Ffull = nullptr;
+        if (packed) {
+            DD_CK(cudaMalloc(&Ffull, frows * (size_t)f.NP * sizeof(double)));
+            DD_CK(cudaMemsetAsync(Ffull, 0, frows * (size_t)f.NP * sizeof(double), c->stream));
+        } else {
+            DD_CK(dalloc(c, &f.F, frows * (size_t)f.NP));
+            Ffull = f.F;
+        }
+        DD_CK(face_gram_scatter(dA, n2, kp, Ffull, n, f.ldf, f.NP, c->num_sms, c->stream));
+        if (packed) {
+            // F is symmetric (B B^T): keep the upper 128 x 128 blocks only (row a-3, half the bytes)
+            std::vector<int> ij;
+            fx_sym_block_table(f.NP, ij);
+            DD_CK(dalloc(c, &f.fblk, ij.size()));
+            DD_CK(cudaMemcpyAsync(f.fblk, ij.data(), ij.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+            DD_CK(dalloc(c, &f.Fp, fx_sym_packed_doubles(f.NP)));
+            DD_CK(fx_sym_pack(Ffull, f.NP, f.fblk, f.Fp, c->stream));
+            DD_CK(dalloc(c, &f.fxD, fx_sym_partial_doubles(f.NP, c->max_cols)));
+            DD_CK(dalloc(c, &f.fxT, fx_sym_partial_doubles(f.NP, c->max_cols)));
+        }
         DD_CK(cudaStreamSynchronize(c->stream));
+        if (packed) cudaFree(Ffull);
         cudaFree(dA); cudaFree(dM); cudaFree(dW); cudaFree(info);
     }
 
@@ -454,6 +478,11 @@ static dd_status schur_core(dd_ctx* c, int ncols, const int* colp, const double*
         if (s != DD_OK) return s;
         DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_mass_axpy(f.n, f.ldf, f.NP, ncols, hh12, f.fs.V2, f.fs.gcol, f.U2, q,
                                                       c->stream));
+        return DD_OK;
+    }
+    if (f.Fp) {
+        DD_TIMED(DD_KCLASS_GEMM_SCHUR, fx_sym_apply(f.Fp, f.fblk, f.NP, p, q, f.U2, ncols, colp, c->n_param, c->gp,
+                                                    f.fxD, f.fxT, c->num_sms, c->stream));
         return DD_OK;
     }
     DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, f.NP, p, q, f.U2, ncols, colp, c->n_param, c->gp, f.fx_ws, f.fx_cnt,

@@ -61,7 +61,10 @@ struct Face3 {
     long long NP = 0;                 // padded face size ldf^2
     double* S = nullptr;              // sine matrix, round_up(n,64) x ldf row-major, zero padded
     double* sw = nullptr;             // Schur weights s_ab, NP (padded layout)
-    double* F = nullptr;              // dense fractional term, rows round_up(NP,128) x NP row-major
+    double* F = nullptr;              // dense fractional term, rows round_up(NP,256) x NP row-major (DD_FX_FULL=1)
+    double* Fp = nullptr;             // packed-symmetric F: upper 128 x 128 blocks in 16-column slabs (default)
+    int* fblk = nullptr;              // (I, J) of each packed block
+    double *fxD = nullptr, *fxT = nullptr;   // direct / transposed block partials of the packed stream
     double* Kcol = nullptr;           // per-column K (gathered from col_param)
     // outer vectors [cols_pad][NP]
     double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr, *U1 = nullptr, *U2 = nullptr;

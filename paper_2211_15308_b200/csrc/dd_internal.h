@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 #include "../../include/dd_api.h"
 
@@ -187,6 +188,16 @@ struct Pcg3 {
 cudaError_t face_slab_pass(const double* in, double* out, int nslab, int n, int ldf, const double* S, cudaStream_t st);
 cudaError_t face_slab_pass_scaled(const double* in, double* out, int nslab, int n, int ldf, const double* S,
                                   const double* w, long long sW, int group, const double* colscale, cudaStream_t st);
+// packed-symmetric F stream (fx_sym.cu): upper 128 x 128 blocks, one read per block, two products
+int fx_sym_blocks(long long NP);
+size_t fx_sym_packed_doubles(long long NP);
+size_t fx_sym_partial_doubles(long long NP, int max_cols);
+bool fx_sym_supported(long long NP);
+void fx_sym_block_table(long long NP, std::vector<int>& ij);          // (I, J) per packed block
+cudaError_t fx_sym_pack(const double* F, long long NP, const int* blk, double* Fp, cudaStream_t st);
+cudaError_t fx_sym_apply(const double* Fp, const int* blk, long long NP, const double* p, double* q, const double* D,
+                         int ncols, const int* col_param, int n_param, const double* gp, double* Dpart, double* Tpart,
+                         int num_sms, cudaStream_t st);
 size_t face_fx_ws_doubles(long long NP, int ncols, int num_sms);
 int face_fx_tiles(long long NP, int ncols);
 cudaError_t face_fx(const double* F, long long NP, const double* p, double* q, const double* D, int ncols,

@@ -75,6 +75,46 @@ def test_pcg_parity_3d(case3):
     assert res.hist[0] > 0 and len(res.hist) == res.iters[0] + 1
 
 
+def test_packed_symmetric_f_matches_full(lib, monkeypatch):
+    """Row a-3's packed-symmetric F (upper 128 x 128 blocks, each read once for F_IJ x_J and
+    F_IJ^T x_I) against the full-F stream on the same handle inputs: N = 32 (8 block rows),
+    11 columns (two 8-column groups, the second ragged)."""
+    N, C = 32, 11
+    params = [(1.0, 1e4)]                             # one parameter set per 3D handle (A20)
+    ras = _fit(N, params, 10)
+    B = np.random.default_rng(7).uniform(-1, 1, (C, (N - 1) ** 2))
+    colp = np.zeros(C, dtype=np.int32)
+    out = {}
+    for packed in ("0", "1"):
+        monkeypatch.setenv("DD_FX_PACKED", packed)
+        S = lib.Solver(3, N, params, ras, max_cols=C, device=0)
+        try:
+            out[packed] = S.apply_schur(torch.as_tensor(B, device="cuda"), colp).cpu().numpy()
+            x = S.pcg_solve(torch.as_tensor(B, device="cuda"), colp, rtol=1e-10, maxit=200)
+            out[packed + "it"] = x.iters
+        finally:
+            S.close()
+    assert rel_l2_cols(out["0"], out["1"]) <= 1e-13
+    assert np.all(np.abs(out["0it"] - out["1it"]) <= 1)
+
+
+def test_packed_symmetric_f_oracle(lib, monkeypatch):
+    """The packed-symmetric F path against the dense oracle (N = 13: NP = 256, blocks (0,0), (0,1),
+    (1,1) — the transposed product of the off-diagonal block carries half of F)."""
+    monkeypatch.setenv("DD_FX_PACKED", "1")
+    N, C = 13, 5
+    params = [(1.0, 1e2)]
+    ras = _fit(N, params, 12)
+    D = oprob.DenseProblem(3, N)
+    B = np.random.default_rng(N).uniform(-1, 1, (C, (N - 1) ** 2))
+    S = lib.Solver(3, N, params, ras, max_cols=C, device=0)
+    try:
+        y = S.apply_schur(torch.as_tensor(B, device="cuda"), [0] * C).cpu().numpy()
+    finally:
+        S.close()
+    assert rel_l2_cols(y, D.apply_S(*params[0], B.T).T) <= 1e-10
+
+
 def test_host_api_3d(case3):
     # the host-buffer entry point stages whole faces ((N-1)^2 per column): same bits as the device call
     N, params, ras, D, S, B = case3
