@@ -50,7 +50,7 @@ def live_columns(iters, compact: bool, bn: int = 64, min_tiles: int = 6):
     columns of the bn-wide tiles that still hold an active column (iters[j] >= k at apply k)."""
     iters = np.asarray(iters); C = len(iters); kmax = int(iters.max()) if C else 0
     tiles = (C + bn - 1) // bn
-    if not compact or tiles < min_tiles:
+    if not compact or (C + 63) // 64 < min_tiles:        # the library's threshold counts 64-column tiles
         return [C] * kmax
     tile_it = np.array([iters[t * bn:(t + 1) * bn].max() for t in range(tiles)])
     width = np.array([min(bn, C - t * bn) for t in range(tiles)])
@@ -350,13 +350,15 @@ def main():
         total_prof_ms = sum(v[0] for v in prof.values())
         if cfg.dim == 2:
             # [S_dst | F] (n x 2n) times (2n x C), algorithmic; RA mode (Remark 1): S_dst T' only
-            # Live-tile compaction (>= 6 column tiles): the apply at iteration k runs only the 64-column
-            # tiles holding a column with iters >= k, so the algorithmic work per launch is counted
-            # over those columns (the profiled solves repeat the timed ones: same inputs, same iters).
-            cols_per_apply = live_columns(last, compact=(os.environ.get("DD_NO_COMPACT", "0")[:1] != "1"))
-            c_eff = float(np.mean(cols_per_apply))
             assembled = qc["splitk_dst"] in (-1, -2)    # one GEMM per apply, no K1 (dd_set_schur_mode)
             grouped = qc["splitk_dst"] == -2            # K-dim n: H_p = K_p G + gamma_p F
+            # Live-tile compaction (>= 6 tiles of 64 columns): the apply at iteration k runs only the
+            # column tiles (32 wide for the grouped GEMM, else 64) holding a column with iters >= k, so
+            # the algorithmic work per launch is counted over those columns (the profiled solves repeat
+            # the timed ones: same inputs, same iterations).
+            cols_per_apply = live_columns(last, compact=(os.environ.get("DD_NO_COMPACT", "0")[:1] != "1"),
+                                          bn=32 if grouped else 64)
+            c_eff = float(np.mean(cols_per_apply))
             flops_g2 = 2.0 * n * (2 * n) * c_eff if (args.frac_mode == "dense" and not grouped) else 2.0 * n * n * c_eff
             flops_g1 = 0.0 if assembled else 2.0 * n * n * c_eff
             ach_g2 = flops_g2 / (g2_ms / g2_n / 1e3) / 1e12 if g2_n else None

@@ -304,7 +304,7 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
     CK(dalloc(c, &c->r, vec));
     CK(dalloc(c, &c->p, vec));
     CK(dalloc(c, &c->q, vec));
-    CK(dalloc(c, &c->ntl, 2 * (c->cols_pad / GEMM_BN) + 4));
+    CK(dalloc(c, &c->ntl, 2 * (c->cols_pad / GEMM_BN_GROUPED) + 4));   // lists at 32- or 64-column width
     if (c->frac_mode == DD_FRAC_RA) {
         CK(dalloc(c, &c->q_f, vec));
         c->small_ok = false;      // the persistent small-n kernel applies the dense F
@@ -472,6 +472,7 @@ static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double
         g.A = c->H; g.lda = c->Kpad;
         g.B = xin; g.ldb = c->ldv;
         g.C = y; g.ldc = ldy;
+        g.ntl_bn = GEMM_BN_GROUPED;
         g.grouped = 1; g.sG = (long long)c->Mpad * c->Kpad; g.col_param = colp; g.n_param = c->n_param;
         g.mixed = c->ints + 6;
         g.alt_A = c->W + c->Kpad; g.alt_lda = c->lda; g.alt_B = c->Z; g.alt_ldb = 2 * c->Kpad; g.alt_K = 2 * c->Kpad;
@@ -612,7 +613,9 @@ static PcgState make_state(dd_ctx* c, int ncols, const int* colp, double* x, dou
     // work in the pole-sum tail); it pays for batches of >= 6 column tiles whose parameter sets
     // converge at different iterations (cfg5: +10.8 %), not for 4 tiles (cfg2: -1.4 %).
     s.ntl = (c->compact && (ncols + GEMM_BN - 1) / GEMM_BN >= 6) ? c->ntl : nullptr;
-    s.ntl_cnt = c->ntl + c->cols_pad / GEMM_BN + 2;
+    // the grouped GEMM's tiles are 32 columns wide (one parameter set each): finer live list
+    s.ntl_bn = (c->dim == 2 && c->schur_mode == 2) ? GEMM_BN_GROUPED : GEMM_BN;
+    s.ntl_cnt = c->ntl + c->cols_pad / GEMM_BN_GROUPED + 2;
     if (c->dim == 2 && c->schur_mode >= 1) {
         s.zs = c->Z; s.ldz = 2 * c->Kpad; s.zhalf = c->Kpad;
         s.Kp = c->Kp; s.gp = c->gp;
@@ -696,7 +699,7 @@ static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const dou
     }
     CK(cudaEventRecord(c->solve_ev[0], c->stream));
     CK(cudaMemsetAsync(c->ints, 0, sizeof(int) * 8, c->stream));
-    if (c->dim == 2) CK(cudaMemsetAsync(c->ntl, 0, sizeof(int) * (2 * (c->cols_pad / GEMM_BN) + 4), c->stream));
+    if (c->dim == 2) CK(cudaMemsetAsync(c->ntl, 0, sizeof(int) * (2 * (c->cols_pad / GEMM_BN_GROUPED) + 4), c->stream));
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
     if (c->dim == 2 && c->schur_mode == 2)
         TIMED(DD_KCLASS_OTHER, launch_check_tiles(ncols, colp, c->ints + 6, c->stream));

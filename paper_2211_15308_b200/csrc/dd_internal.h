@@ -34,7 +34,8 @@ struct GemmArgs {
     int epi;
     int pdl;                     // launch with programmatic stream serialisation (follows a kernel)
     int a_static;                // A is constant (prefetched before griddepcontrol.wait)
-    const int* ntl;              // live column tiles [count, ids...] (BN = 64): work over these only (or null)
+    const int* ntl;              // live column tiles [count, ids...] of width ntl_bn: work over these only (or null)
+    int ntl_bn;                  // 64 (default when 0) or 32 (grouped)
     int n_param;
     // EPI_SCHUR_DST
     const int* col_param; const double* Kp; const double* gp; const double* s;
@@ -102,7 +103,8 @@ struct PcgState {
     unsigned long long cond_handle;    // cudaGraphConditionalHandle (0 = none)
     long long* dbg;                    // optional phase timestamps of CTA 0 (DD_PHASE_TIMING=1)
     int* ntl;                          // live 64-column tiles [count, ids...] for the GEMMs (or null)
-    int* ntl_cnt;                      // active columns per 64-column tile (zeroed before pcg_init)
+    int* ntl_cnt;                      // active columns per live-list tile (zeroed before pcg_init)
+    int ntl_bn;                        // live-list tile width: 64, or 32 for the grouped Schur GEMM
     // assembled 2D Schur apply: every new p is also written as the GEMM operand [γ_c p ; K_c p]
     double* zs; int ldz, zhalf;        // Z (column stride ldz), K-half at row zhalf (or zs = null)
     const double *Kp, *gp;             // per-parameter K, γ

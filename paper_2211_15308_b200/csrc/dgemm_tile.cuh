@@ -49,8 +49,9 @@ struct DgemmProblem {
     const int* active = nullptr; // optional per-slab flag: slabs with active[b] == 0 are skipped
     unsigned long long* ts = nullptr;   // optional per-CTA phase timestamps (lab instrumentation)
     int a_static = 0;            // A is not written by the preceding kernel: prefetch it before griddepcontrol.wait
-    const int* ntl = nullptr;    // live 64-column tiles [count, tile ids...] (PCG: columns freeze when converged):
-                                 // the tile / stream-K work is laid out over the live tiles only
+    const int* ntl = nullptr;    // live column tiles [count, tile ids...] of width ntl_bn (PCG: columns freeze
+                                 // when converged): the tile / stream-K work is laid out over the live tiles only
+    int ntl_bn = 64;             // live-tile width, a multiple of BN
     // Grouped A (tile kernel only): column tile [n0, n0+BN) multiplies A + col_group[n0] * sG —
     // every BN-column tile must lie in one group — unless *mixed != 0 (flag written on the device
     // before this launch), in which case the whole launch computes the fallback product
@@ -63,7 +64,6 @@ struct DgemmProblem {
     const double* alt_B = nullptr; int alt_ldb = 0;
     int alt_K = 0;
 };
-constexpr int DG_NTL_BN = 64;    // width of the live-tile list entries
 
 // Programmatic dependent launch (no-ops when the launch did not opt in)
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -190,14 +190,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
     pdl_wait();
     if (g.active && !g.active[bz]) return;   // frozen slab (uniform across the cluster)
     if (g.ntl) {                             // live column tiles only (uniform across the cluster)
-        constexpr int SUB = DG_NTL_BN / C::BN;
-        static_assert(DG_NTL_BN % C::BN == 0, "live-tile width");
+        const int SUB = g.ntl_bn / C::BN;
         const int nidx = blockIdx.x / tiles_m;
         if (nidx / SUB >= g.ntl[0]) {
             asm volatile("cp.async.wait_all;\n" ::);   // drain the A prefetch before leaving
             return;
         }
-        n0 = g.ntl[1 + nidx / SUB] * DG_NTL_BN + (nidx % SUB) * C::BN;
+        n0 = g.ntl[1 + nidx / SUB] * g.ntl_bn + (nidx % SUB) * C::BN;
         if (n0 >= g.N) {                     // ragged half of the last live tile
             asm volatile("cp.async.wait_all;\n" ::);
             return;
@@ -352,7 +351,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProb
     }
 
     const int tiles_m = (g.M + C::BM - 1) / C::BM;
-    const int tiles = tiles_m * (g.ntl ? g.ntl[0] * (DG_NTL_BN / C::BN) : (g.N + C::BN - 1) / C::BN);
+    const int tiles = tiles_m * (g.ntl ? g.ntl[0] * (g.ntl_bn / C::BN) : (g.N + C::BN - 1) / C::BN);
     const int KT = g.K / C::BK;
     const long long U = (long long)tiles * KT;
     const int b = blockIdx.x;
@@ -368,8 +367,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_streamk(DgemmProb
         const int ks = (int)(u % KT);
         const int ke = (int)min((long long)KT, (long long)ks + (u1 - u));
         const int m0 = (t % tiles_m) * C::BM;
-        const int n0 = g.ntl ? g.ntl[1 + (t / tiles_m) / (DG_NTL_BN / C::BN)] * DG_NTL_BN +
-                                   ((t / tiles_m) % (DG_NTL_BN / C::BN)) * C::BN
+        const int n0 = g.ntl ? g.ntl[1 + (t / tiles_m) / (g.ntl_bn / C::BN)] * g.ntl_bn +
+                                   ((t / tiles_m) % (g.ntl_bn / C::BN)) * C::BN
                              : (t / tiles_m) * C::BN;
         const int nkt = ke - ks;
         const double* Aseg = g.A;

@@ -84,6 +84,7 @@ static cudaError_t launch(const GemmArgs& a, const Epi& e, cudaStream_t st) {
     DgemmProblem g{a.M, a.N, a.K, a.A, a.lda, a.B, a.ldb};
     g.a_static = a.a_static;
     g.ntl = a.ntl;
+    g.ntl_bn = a.ntl_bn > 0 ? a.ntl_bn : 64;
     if (a.splitk == 0) {
         StreamK sk{a.ws, a.counters, 0};
         // no PDL here: early-resident CTAs of a stream-K grid land unevenly on the SMs (a third
@@ -99,6 +100,7 @@ cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
     if (a.grouped) {
         DgemmProblem g{a.M, a.N, a.K, a.A, a.lda, a.B, a.ldb};
         g.ntl = a.ntl;
+        g.ntl_bn = a.ntl_bn > 0 ? a.ntl_bn : 64;
         g.a_static = a.a_static;
         g.col_group = a.col_param; g.n_group = a.n_param; g.sG = a.sG; g.mixed = a.mixed;
         g.alt_A = a.alt_A; g.alt_lda = a.alt_lda; g.alt_B = a.alt_B; g.alt_ldb = a.alt_ldb; g.alt_K = a.alt_K;

@@ -505,7 +505,8 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_f
     }
 }
 
-// Live 64-column tiles of the batch (GEMM output tiles with at least one unconverged column):
+// Live column tiles of the batch (s.ntl_bn = 64, or 32 for the grouped Schur GEMM; GEMM output
+// tiles with at least one unconverged column):
 // every CTA keeps its tile's active-column count current (ntl_cnt, +1 at init, -1 when its column
 // freezes); the last-arriving CTA compacts the live tile ids into s.ntl = [count, ids...] and the
 // next iteration's GEMMs partition their work over those tiles only.
@@ -515,7 +516,7 @@ __device__ __forceinline__ void publish_live_tiles(const PcgState& s, int na) {
     // prefix popcount over the per-tile counters).
     if (!s.ntl || threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
-    const int nt = (s.ncols + 63) / 64;
+    const int nt = (s.ncols + s.ntl_bn - 1) / s.ntl_bn;
     if (na == s.ncols) {
         for (int j = lane; j < nt; j += 32) s.ntl[1 + j] = j;
         if (lane == 0) s.ntl[0] = nt;
@@ -538,7 +539,7 @@ __device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_a
     __syncthreads();
     if (threadIdx.x == 0) {
         if (still_active) atomicAdd(s.n_active_next, 1);
-        if (was_active && !still_active && s.ntl) atomicSub(&s.ntl_cnt[blockIdx.x / 64], 1);
+        if (was_active && !still_active && s.ntl) atomicSub(&s.ntl_cnt[blockIdx.x / s.ntl_bn], 1);
         __threadfence();
         const int prev = atomicAdd(s.done_ctas, 1);
         const bool last = prev == (int)gridDim.x - 1;
@@ -608,7 +609,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
         s.active[c] = act ? 1 : 0;
         if (c == 0 && s.hist) s.hist[0] = eta0;
         if (act) atomicAdd(s.n_active_next, 1);
-        if (act && s.ntl) atomicAdd(&s.ntl_cnt[c / 64], 1);
+        if (act && s.ntl) atomicAdd(&s.ntl_cnt[c / s.ntl_bn], 1);
         __threadfence();
         const int prev = atomicAdd(s.done_ctas, 1);
         s_init_last = prev == (int)gridDim.x - 1;
