@@ -725,6 +725,12 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
                 if (threadIdx.x == 0) s.active[c] = 0;
             } else {
                 const double beta = rz / s.rho[c];
+                // p as at entry, re-read (L2) rather than held in registers across the pole sum
+#pragma unroll
+                for (int j = 0; j < RPT; j++) {
+                    const int i = threadIdx.x + j * NT;
+                    pv[j] = i < n ? __ldcg(&s.p[off + i]) : 0.0;
+                }
                 if (s.zs && (!s.zmixed || *s.zmixed)) {
                     // assembled Schur apply: the next GEMM's operand [γ p ; K p] written with p
                     const double gc = s.gp[param], Kc = s.Kp[param];
