@@ -308,6 +308,9 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
     if (c->frac_mode == DD_FRAC_RA) {
         CK(dalloc(c, &c->q_f, vec));
         c->small_ok = false;      // the persistent small-n kernel applies the dense F
+        CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     }
     CK(dalloc(c, &c->bst, (size_t)n * c->max_cols));
     CK(dalloc(c, &c->xst, (size_t)n * c->max_cols));
@@ -456,7 +459,7 @@ extern "C" int dd_interface_size(const dd_ctx* c) { return c ? c->ng : -1; }
 
 // ------------------------------------------------------------------------------------ applies
 static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double* xin, double* y, int ldy,
-                             const int* ntl = nullptr, bool z_ready = false) {
+                             const int* ntl = nullptr, bool z_ready = false, bool ra_side = false) {
     const int n = c->n;
     if (c->schur_mode == 2) {
         // grouped: Y[:, c] = H_{p(c)} X[:, c], one 32-column tile per GEMM CTA column; a launch
@@ -494,9 +497,19 @@ static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double
             TIMED(DD_KCLASS_OTHER, launch_schur_operand(n, ncols, colp, c->n_param, c->Kp, c->gp, xin, c->ldv, c->Z,
                                                         2 * c->Kpad, c->Kpad, c->stream));
         const bool ra = c->frac_mode == DD_FRAC_RA;
-        if (ra)
+        if (ra && ra_side) {
+            // PCG body: U = γ M r_F M p on the side stream, concurrent with Y = G (K p); the fused
+            // PCG kernel adds U when it reads q (same sum, same rounding as the EPI_ADD epilogue)
+            CK(cudaEventRecord(c->ev_fork, c->stream));
+            CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+            CK(launch_frac_ra(ncols, colp, c->n_param, c->gp, c->geom, c->ftabs, xin, c->ldv, c->q_f, c->ldv,
+                              1.0 / (6.0 * c->N), c->side, false));
+            c->launches++;
+            CK(cudaEventRecord(c->ev_join, c->side));
+        } else if (ra) {
             TIMED(DD_KCLASS_POLESUM, launch_frac_ra(ncols, colp, c->n_param, c->gp, c->geom, c->ftabs, xin, c->ldv,
                                                     c->q_f, c->ldv, 1.0 / (6.0 * c->N), c->stream, c->pdl));
+        }
         GemmArgs g2{};
         g2.M = n; g2.N = ncols; g2.K = ra ? c->Kpad : 2 * c->Kpad;
         g2.A = c->W + (ra ? c->g_off : c->Kpad); g2.lda = c->lda;
@@ -505,7 +518,7 @@ static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double
         g2.X = c->q_f; g2.ldx = c->ldv;
         g2.splitk = gemm_pick_splitk(n, ncols, g2.K, c->num_sms); g2.ws = c->gws; g2.counters = c->gcnt;
         g2.num_sms = c->num_sms;
-        g2.epi = ra ? EPI_ADD : EPI_STORE;
+        g2.epi = (ra && !ra_side) ? EPI_ADD : EPI_STORE;
         g2.pdl = c->pdl; g2.a_static = 1;
         g2.ntl = ntl;
         c->last_split1 = -1;
@@ -624,11 +637,19 @@ static PcgState make_state(dd_ctx* c, int ncols, const int* colp, double* x, dou
     return s;
 }
 
-static dd_status iteration_body(dd_ctx* c, const PcgState& s) {
-    dd_status st = schur_gemms(c, s.ncols, s.col_param, c->p, c->q, c->ldv, s.ntl, s.zs != nullptr);
+static dd_status iteration_body(dd_ctx* c, const PcgState& s0) {
+    // RA mode: the fractional pole sum on the side stream beside the GEMM (not while profiling:
+    // the per-launch event pairs live on the main stream)
+    const bool side = c->frac_mode == DD_FRAC_RA && c->schur_mode == 1 && c->side && !c->prof;
+    dd_status st = schur_gemms(c, s0.ncols, s0.col_param, c->p, c->q, c->ldv, s0.ntl, s0.zs != nullptr, side);
     if (st != DD_OK) return st;
+    PcgState s = s0;
+    if (side) {
+        CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+        s.qadd = c->q_f;
+    }
     c->last_ps_warps = polesum_warps(c->geom);
-    TIMED(DD_KCLASS_POLESUM, launch_pcg_iter(s, c->geom, c->tabs, c->stream, c->pdl));
+    TIMED(DD_KCLASS_POLESUM, launch_pcg_iter(s, c->geom, c->tabs, c->stream, c->pdl && !side));
     return DD_OK;
 }
 
@@ -997,6 +1018,9 @@ extern "C" dd_status dd_destroy(dd_ctx* c) {
     for (void* p : c->allocs) cudaFree(p);
     if (c->h_ints) cudaFreeHost(c->h_ints);
     if (c->h_iters) cudaFreeHost(c->h_iters);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->side) cudaStreamDestroy(c->side);
     if (c->h_rel) cudaFreeHost(c->h_rel);
     delete c;
     return DD_OK;

@@ -154,6 +154,9 @@ struct dd_ctx {
     bool pdl = true;          // programmatic dependent launch between the iteration's kernels (DD_NO_PDL=1 disables)
     bool small_ok = true;     // persistent single-launch PCG for n <= 63 (DD_NO_SMALL=1 disables)
     cudaEvent_t solve_ev[2] = {nullptr, nullptr};
+    // RA mode (2D): the fractional pole sum runs beside the Schur GEMM on a second stream
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     long long* dbg = nullptr;   // DD_PHASE_TIMING=1: CTA-0 phase timestamps of the last PCG iteration kernel
     // 3D
     dd::Face3 f3;

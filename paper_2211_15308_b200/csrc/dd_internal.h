@@ -109,6 +109,7 @@ struct PcgState {
     double* zs; int ldz, zhalf;        // Z (column stride ldz), K-half at row zhalf (or zs = null)
     const double *Kp, *gp;             // per-parameter K, γ
     const int* zmixed;                 // grouped apply: write zs only if *zmixed (fallback operand)
+    const double* qadd;                // RA mode: q = q + qadd (the fractional term, computed concurrently)
 };
 
 PoleGeom make_pole_geom(int n);

@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
             const int i = threadIdx.x + j * NT;
             const bool ok = i < n;
             pv[j] = ok ? s.p[off + i] : 0.0;
-            qv[j] = ok ? s.q[off + i] : 0.0;
+            qv[j] = ok ? (s.qadd ? s.q[off + i] + s.qadd[off + i] : s.q[off + i]) : 0.0;
             xv[j] = ok ? s.x[offx + i] : 0.0;
             rv[j] = ok ? s.r[off + i] : 0.0;
         }
