@@ -116,7 +116,7 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
         DD_CK(scale_transpose(dM, dW, n2, dA, kp, c->stream));
         const size_t frows = (size_t)round_up((int)f.NP, 256);
         // packed-symmetric F (row a-3 option, half the bytes and half the memory) is opt-in: at 8
-        // columns its per-block cross-warp reduction leaves it latency-bound (423 vs 391 µs per
+        // columns its per-block cross-warp reduction leaves it latency-bound (386 vs 391 µs per
         // apply for the full-F stream at 83 % of HBM)
         const char* fp = std::getenv("DD_FX_PACKED");
         const bool packed = fx_sym_supported(f.NP) && fp && fp[0] == '1';

@@ -169,38 +169,58 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // q[row + c NP] = γ_c (Σ_{J>=I} D_{I,J} + Σ_{J'<I} T_{J',I})[row, c] + Dd[row + c NP]
-__global__ void __launch_bounds__(THREADS)
+// One CTA per (block row I, column group): RCH chunks of the NB contributions (D_{I,I..NB-1} then
+// T_{0..I-1,I}, in that order) are summed by RCH thread groups in parallel, each in its own fixed
+// order, then the chunk sums in chunk order — a fixed tree, bitwise reproducible.
+constexpr int RCH = 4, RTH = 128;             // chunks x threads per chunk; 8 outputs per thread
+__global__ void __launch_bounds__(RCH * RTH)
     k_fx_sym_reduce(const double* __restrict__ Dpart, const double* __restrict__ Tpart, int NB, int nblocks,
                     long long NP, int ncols, const int* __restrict__ col_param, int n_param,
                     const double* __restrict__ gp, const double* __restrict__ Dd, double* __restrict__ q) {
+    __shared__ double4 part[RCH - 1][RTH][2];
     const int I = blockIdx.x, cg = blockIdx.y;
-    const int c = threadIdx.x / 32, r0 = (threadIdx.x % 32) * 4;
-    const int colg = cg * 8 + c;
-    if (colg >= ncols) return;
+    const int ch = threadIdx.x / RTH, t = threadIdx.x % RTH;
+    const int o0 = t * 8;                     // outputs o0..o0+7 of the 1024 = [n][row] of this block row
     const size_t pstride = (size_t)nblocks * BT * 8;
     const double* Dp = Dpart + (size_t)cg * pstride;
     const double* Tp = Tpart + (size_t)cg * pstride;
-    double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
     const long long rowbase = (long long)I * NB - (long long)I * (I - 1) / 2;
-#pragma unroll 8
-    for (int J = I; J < NB; J++) {
-        const double4 v = *reinterpret_cast<const double4*>(Dp + (size_t)(rowbase + (J - I)) * BT * 8 + c * BT + r0);
-        y0 += v.x; y1 += v.y; y2 += v.z; y3 += v.w;
+    // contribution j in [0, NB): j < NB - I -> D_{I, I + j};  else T_{j - (NB - I), I}
+    const int per = (NB + RCH - 1) / RCH, j0 = ch * per, j1 = min(NB, j0 + per);
+    double4 a = make_double4(0, 0, 0, 0), b = make_double4(0, 0, 0, 0);
+#pragma unroll 4
+    for (int j = j0; j < j1; j++) {
+        const double* src;
+        if (j < NB - I) {
+            src = Dp + (size_t)(rowbase + j) * BT * 8;
+        } else {
+            const int J = j - (NB - I);
+            src = Tp + (size_t)((long long)J * NB - (long long)J * (J - 1) / 2 + (I - J)) * BT * 8;
+        }
+        const double4 v0 = *reinterpret_cast<const double4*>(src + o0);
+        const double4 v1 = *reinterpret_cast<const double4*>(src + o0 + 4);
+        a.x += v0.x; a.y += v0.y; a.z += v0.z; a.w += v0.w;
+        b.x += v1.x; b.y += v1.y; b.z += v1.z; b.w += v1.w;
     }
-#pragma unroll 8
-    for (int J = 0; J < I; J++) {
-        const long long bJI = (long long)J * NB - (long long)J * (J - 1) / 2 + (I - J);
-        const double4 v = *reinterpret_cast<const double4*>(Tp + (size_t)bJI * BT * 8 + c * BT + r0);
-        y0 += v.x; y1 += v.y; y2 += v.z; y3 += v.w;
+    if (ch > 0) { part[ch - 1][t][0] = a; part[ch - 1][t][1] = b; }
+    __syncthreads();
+    if (ch != 0) return;
+#pragma unroll
+    for (int k = 0; k < RCH - 1; k++) {
+        const double4 u = part[k][t][0], w = part[k][t][1];
+        a.x += u.x; a.y += u.y; a.z += u.z; a.w += u.w;
+        b.x += w.x; b.y += w.y; b.z += w.z; b.w += w.w;
     }
+    const int n = o0 / BT, r0 = o0 % BT;      // 8 outputs share the column n (BT multiple of 8)
+    const int colg = cg * 8 + n;
+    if (colg >= ncols) return;
     int p = col_param[colg];
     p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
     const double g = gp[p];
     const size_t o = (size_t)colg * NP + (size_t)I * BT + r0;
-    q[o + 0] = fma(g, y0, Dd[o + 0]);
-    q[o + 1] = fma(g, y1, Dd[o + 1]);
-    q[o + 2] = fma(g, y2, Dd[o + 2]);
-    q[o + 3] = fma(g, y3, Dd[o + 3]);
+    const double y[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int k = 0; k < 8; k++) q[o + k] = fma(g, y[k], Dd[o + k]);
 }
 
 // full row-major NP x NP F -> packed upper blocks
@@ -252,7 +272,7 @@ cudaError_t fx_sym_apply(const double* Fp, const int* blk, long long NP, const d
     k_fx_sym<<<dim3(G, ncg), THREADS, SMEM, st>>>(Fp, reinterpret_cast<const int2*>(blk), nb, NP, p, ncols, Dpart, Tpart);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_fx_sym_reduce<<<dim3(NB, ncg), THREADS, 0, st>>>(Dpart, Tpart, NB, nb, NP, ncols, col_param, n_param, gp, D, q);
+    k_fx_sym_reduce<<<dim3(NB, ncg), RCH * RTH, 0, st>>>(Dpart, Tpart, NB, nb, NP, ncols, col_param, n_param, gp, D, q);
     return cudaGetLastError();
 }
 
