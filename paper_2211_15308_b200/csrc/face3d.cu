@@ -16,6 +16,8 @@
 //   SURVEY V10), applied with the same slab transforms.  Converged pairs freeze.
 //   The weighted sum over systems runs in fixed system order; across ranks (pole split) the
 //   partial sums are added by one NCCL allreduce (row a-6, in dd_api.cpp).
+#include <cstdlib>
+
 #include "dd_internal.h"
 #include "dgemm_tile.cuh"
 #include <cooperative_groups.h>
@@ -314,6 +316,7 @@ __global__ void k_inner_init_hat(InnerArgs a, const double* __restrict__ bh) {
 // pair's entries; the two dot products are reduced over DSMEM in fixed rank order (deterministic):
 //   q̂ = dg ∘ p̂ + q̂_part;  α = ρ/p̂·q̂;  x̂ += α p̂;  r̂ -= α q̂;  ρ' = r̂·(idg ∘ r̂);  p̂ = idg ∘ r̂ + β p̂
 constexpr int ICL = 4;
+template <int NCL>
 __device__ __forceinline__ double cluster_allsum(double v, double* red, double* slot) {
     // block sum -> this CTA's slot; cluster barrier; every CTA sums the ICL slots in rank order
     v = block_sum(v, red);
@@ -321,18 +324,19 @@ __device__ __forceinline__ double cluster_allsum(double v, double* red, double* 
     if (threadIdx.x == 0) *slot = v;
     cl.sync();
     double s = 0.0;
-    for (int q = 0; q < ICL; q++) s += *cl.map_shared_rank(slot, q);
+    for (int q = 0; q < NCL; q++) s += *cl.map_shared_rank(slot, q);
     cl.sync();                                   // nobody leaves / overwrites before all have read
     return s;
 }
-__global__ void __cluster_dims__(ICL, 1, 1) k_inner_update_cl(InnerArgs a, int* n_active) {
+template <int NCL>
+__global__ void __cluster_dims__(NCL, 1, 1) k_inner_update_cl(InnerArgs a, int* n_active) {
     __shared__ double red[32];
     __shared__ double slot;
     const int pq = blockIdx.y;
     const int rank = blockIdx.x;                 // cluster rank (cluster spans blockIdx.x)
     if (!a.active[pq]) return;                   // uniform across the cluster
     const int s = pq / a.C;
-    const long long chunk = (a.NP + ICL - 1) / ICL;
+    const long long chunk = (a.NP + NCL - 1) / NCL;
     const long long i0 = rank * chunk, i1 = min(a.NP, i0 + chunk);
     const size_t off = (size_t)pq * a.NP;
     const double* dg = a.dg + (size_t)s * a.NP;
@@ -344,7 +348,7 @@ __global__ void __cluster_dims__(ICL, 1, 1) k_inner_update_cl(InnerArgs a, int* 
         a.q[off + i] = qv;
         d = fma(pv, qv, d);
     }
-    d = cluster_allsum(d, red, &slot);
+    d = cluster_allsum<NCL>(d, red, &slot);
     if (!(d > 0.0)) {
         if (rank == 0 && threadIdx.x == 0) a.active[pq] = 0;
         return;
@@ -357,7 +361,7 @@ __global__ void __cluster_dims__(ICL, 1, 1) k_inner_update_cl(InnerArgs a, int* 
         a.r[off + i] = r;
         rho = fma(r, r * idg[i], rho);
     }
-    rho = cluster_allsum(rho, red, &slot);
+    rho = cluster_allsum<NCL>(rho, red, &slot);
     if (!(rho > a.rtol * a.rtol * a.rho0[pq])) {
         if (rank == 0 && threadIdx.x == 0) a.active[pq] = 0;
         return;
@@ -389,7 +393,9 @@ cudaError_t inner_init_hat(const InnerArgs& a, const double* bh, cudaStream_t st
     return cudaGetLastError();
 }
 cudaError_t inner_update_hat(const InnerArgs& a, int* n_active, cudaStream_t st) {
-    k_inner_update_cl<<<dim3(ICL, a.npair), 512, 0, st>>>(a, n_active);
+    // 4-CTA clusters of 256 threads (cfg4: 203 solves/s vs 197 with 512 threads — one wave of
+    // CTAs instead of 2.3; 2-CTA / 1-CTA clusters and 128 / 1024 threads measured slower)
+    k_inner_update_cl<ICL><<<dim3(ICL, a.npair), 256, 0, st>>>(a, n_active);
     return cudaGetLastError();
 }
 
