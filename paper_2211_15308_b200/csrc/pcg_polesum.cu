@@ -540,11 +540,11 @@ __device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_a
     if (threadIdx.x == 0) {
         if (still_active) atomicAdd(s.n_active_next, 1);
         if (was_active && !still_active && s.ntl) atomicSub(&s.ntl_cnt[blockIdx.x / s.ntl_bn], 1);
-        __threadfence();
-        const int prev = atomicAdd(s.done_ctas, 1);
-        const bool last = prev == (int)gridDim.x - 1;
-        if (last) __threadfence();       // acquire: every other CTA's counters are visible
-        s_last = last;
+        // arrival with acquire-release semantics at GPU scope: this CTA's counter updates (and the
+        // status flag) are ordered before its arrival; the last arriver sees every other CTA's
+        int prev;
+        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(s.done_ctas) : "memory");
+        s_last = prev == (int)gridDim.x - 1;
     }
     __syncthreads();
     if (!s_last || threadIdx.x >= 32) return;
