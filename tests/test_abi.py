@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -52,3 +53,17 @@ def test_setup_validation_without_gpu():
                       c0.ctypes.data, 1, 0, None, None, ctypes.byref(h))
     assert st == binding.DD_EINVAL and b"pole" in lib.dd_last_error()
     assert lib.dd_interface_size(None) == -1
+
+
+def test_bench_live_columns():
+    """bench.py's algorithmic-work count under live-tile compaction (host logic): the apply at
+    iteration k multiplies only the tiles holding a column with iters >= k, once the batch has at
+    least 6 tiles of 64 columns (the library's threshold); otherwise every column every time."""
+    import bench
+    its = np.array([3] * 64 + [5] * 64 + [2] * 300)            # 7 tiles of 64 (last ragged)
+    assert bench.live_columns(its, True) == [428, 428, 128, 64, 64]
+    assert bench.live_columns(its, False) == [428] * 5
+    its32 = np.repeat([4, 2, 3, 1, 4, 4, 2, 1, 1, 1, 1, 1], 32)  # 384 columns: 6 tiles of 64
+    lc = bench.live_columns(its32, True, bn=32)
+    assert lc == [384, 32 * 6, 32 * 4, 32 * 3]
+    assert bench.live_columns(np.array([3] * 256), True, bn=32) == [256] * 3   # 4 tiles of 64: off
