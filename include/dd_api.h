@@ -162,8 +162,11 @@ dd_status dd_pcg_solve(dd_ctx* ctx, int ncols, const int* col_param, const doubl
                        double rtol, int maxit, int norm_kind, int* iters, double* rel_res,
                        double* hist);
 
-/* As dd_pcg_solve but b, x and col_param are HOST pointers: the call copies b and
- * col_param host->device, solves, and copies x device->host (synchronous). */
+/* As dd_pcg_solve but b, x and col_param are HOST pointers: the call copies col_param
+ * host->device, solves, and copies x device->host (synchronous, one synchronisation).  b is
+ * read once, by the solve's first kernel: page-locked (pinned) host memory is read there in
+ * place over PCIe (UVA), overlapping the transfer with that kernel; pageable memory is
+ * staged by a copy first.  (DD_NO_ZERO_COPY=1 forces the copy.) */
 dd_status dd_pcg_solve_host(dd_ctx* ctx, int ncols, const int* col_param_host,
                             const double* b_host, double* x_host, double rtol, int maxit,
                             int norm_kind, int* iters, double* rel_res, double* hist);

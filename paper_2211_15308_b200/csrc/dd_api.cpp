@@ -825,8 +825,20 @@ extern "C" dd_status dd_pcg_solve_host(dd_ctx* c, int ncols, const int* colp_h, 
         if (colp_h[i] < 0 || colp_h[i] >= c->n_param) return fail(DD_EINVAL, "col_param out of range");
     CK(cudaSetDevice(c->device));
     CK(cudaMemcpyAsync(c->colp_st, colp_h, sizeof(int) * ncols, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->bst, b_h, sizeof(double) * (size_t)c->ng * ncols, cudaMemcpyHostToDevice, c->stream));
-    return pcg_solve_impl(c, ncols, c->colp_st, c->bst, c->xst, rtol, maxit, norm_kind, iters, rel_res, hist, x_h);
+    // b is read once, by the PCG's first kernel: pinned (page-locked, UVA-mapped) host memory is
+    // read there directly over PCIe, overlapping the transfer with that kernel's pole sum instead
+    // of a separate copy before it; pageable memory is staged by a copy
+    const double* bdev = c->bst;
+    static const bool no_zc = std::getenv("DD_NO_ZERO_COPY") && std::getenv("DD_NO_ZERO_COPY")[0] == '1';
+    cudaPointerAttributes pa{};
+    if (!no_zc && cudaPointerGetAttributes(&pa, b_h) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer != nullptr) {
+        bdev = static_cast<const double*>(pa.devicePointer);
+    } else {
+        cudaGetLastError();
+        CK(cudaMemcpyAsync(c->bst, b_h, sizeof(double) * (size_t)c->ng * ncols, cudaMemcpyHostToDevice, c->stream));
+    }
+    return pcg_solve_impl(c, ncols, c->colp_st, bdev, c->xst, rtol, maxit, norm_kind, iters, rel_res, hist, x_h);
 }
 
 // ------------------------------------------------------------------------------------ bulk solve
