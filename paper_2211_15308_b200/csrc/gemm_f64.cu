@@ -1,8 +1,10 @@
-// FP64 tensor-core GEMMs of the Schur apply:
-//   K1  T' = (K_c s) ∘ (S_dst X)  and  Zlow = γ_c X     (EPI_SCHUR_DST)
-//   K2  Y  = [S_dst | F] [T' ; γX]                        (EPI_STORE)
+// FP64 tensor-core GEMMs of the Schur apply,
+// in the three 2D modes of dd_set_schur_mode:
+//   grouped    Y[:, c] = H_{p(c)} X[:, c],  H_p = K_p G + γ_p F      (CfgG, A block per 32-column tile)
+//   assembled  Y = [F | G] [γX ; KX]                                 (EPI_STORE; RA mode: G (KX) + U, EPI_ADD)
+//   factored   K1  T' = (K_c s) ∘ (S_dst X), Zlow = γ_c X  (EPI_SCHUR_DST);  K2  Y = [S_dst | F] [T' ; γX]
 // on the DMMA tile template of dgemm_tile.cuh.  Two work decompositions, picked per launch from
-// the work per CTA (tools/gemm_lab.cu measurements, profiles/):
+// the work per CTA (tools/gemm_lab*.cu measurements, profiles/):
 //   * stream-K over 2 CTAs/SM when every CTA gets >= 64 (tile, k-tile) units — balanced to
 //     within one unit on any shape (large configs: 30-32 TFLOP/s, cuBLAS-level);
 //   * cluster split-K (DSMEM reduction) for small problems (config 2), where stream-K's
