@@ -114,6 +114,15 @@ def test_determinism_and_host_api(small_case):
     assert np.array_equal(h.x, a)
 
 
+def test_host_api_pinned_input(small_case):
+    # dd_pcg_solve_host reads a page-locked b in place (zero copy) and stages a pageable one: same bits
+    N, params, ras, D, S, B, colp = small_case
+    pinned = torch.as_tensor(B).pin_memory().numpy()
+    a = S.pcg_solve_host(B, colp)
+    b = S.pcg_solve_host(pinned, colp)
+    assert np.array_equal(a.x, b.x) and np.array_equal(a.iters, b.iters)
+
+
 def test_batch_columns_match_single(small_case):
     # A14: columns freeze individually; each column reproduces its single-column run.
     N, params, ras, D, S, B, colp = small_case
