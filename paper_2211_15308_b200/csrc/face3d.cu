@@ -317,21 +317,23 @@ __global__ void k_inner_init_hat(InnerArgs a, const double* __restrict__ bh) {
 //   q̂ = dg ∘ p̂ + q̂_part;  α = ρ/p̂·q̂;  x̂ += α p̂;  r̂ -= α q̂;  ρ' = r̂·(idg ∘ r̂);  p̂ = idg ∘ r̂ + β p̂
 constexpr int ICL = 4;
 template <int NCL>
-__device__ __forceinline__ double cluster_allsum(double v, double* red, double* slot) {
-    // block sum -> this CTA's slot; cluster barrier; every CTA sums the ICL slots in rank order
+__device__ __forceinline__ double cluster_allsum(double v, double* red, double* slot, bool trailing_sync = true) {
+    // block sum -> this CTA's slot; cluster barrier; every CTA sums the ICL slots in rank order.
+    // trailing_sync = false when the caller's next cluster barrier (or one before exiting) already
+    // orders the slot reads before any overwrite or exit
     v = block_sum(v, red);
     cg::cluster_group cl = cg::this_cluster();
     if (threadIdx.x == 0) *slot = v;
     cl.sync();
     double s = 0.0;
     for (int q = 0; q < NCL; q++) s += *cl.map_shared_rank(slot, q);
-    cl.sync();                                   // nobody leaves / overwrites before all have read
+    if (trailing_sync) cl.sync();                // nobody leaves / overwrites before all have read
     return s;
 }
 template <int NCL>
 __global__ void __cluster_dims__(NCL, 1, 1) k_inner_update_cl(InnerArgs a, int* n_active) {
     __shared__ double red[32];
-    __shared__ double slot;
+    __shared__ double slot[2];                   // one per reduction: the second needs no barrier before reuse
     const int pq = blockIdx.y;
     const int rank = blockIdx.x;                 // cluster rank (cluster spans blockIdx.x)
     if (!a.active[pq]) return;                   // uniform across the cluster
@@ -348,8 +350,9 @@ __global__ void __cluster_dims__(NCL, 1, 1) k_inner_update_cl(InnerArgs a, int* 
         a.q[off + i] = qv;
         d = fma(pv, qv, d);
     }
-    d = cluster_allsum<NCL>(d, red, &slot);
+    d = cluster_allsum<NCL>(d, red, &slot[0], false);
     if (!(d > 0.0)) {
+        cg::this_cluster().sync();               // slot[0] reads done before any CTA exits
         if (rank == 0 && threadIdx.x == 0) a.active[pq] = 0;
         return;
     }
@@ -361,7 +364,7 @@ __global__ void __cluster_dims__(NCL, 1, 1) k_inner_update_cl(InnerArgs a, int* 
         a.r[off + i] = r;
         rho = fma(r, r * idg[i], rho);
     }
-    rho = cluster_allsum<NCL>(rho, red, &slot);
+    rho = cluster_allsum<NCL>(rho, red, &slot[1]);
     if (!(rho > a.rtol * a.rtol * a.rho0[pq])) {
         if (rank == 0 && threadIdx.x == 0) a.active[pq] = 0;
         return;
