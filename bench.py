@@ -395,7 +395,9 @@ def main():
                     "achieved": round(ach, 1) if ach else None, "peak": hbm, "unit": "GB/s",
                     "frac": round(ach / hbm, 4) if ach else None,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if mp else "fallback 6650 GB/s",
-                    "bytes_per_launch": bytes_fx}
+                    "bytes_per_launch": bytes_fx,
+                    # also against the north star's nominal 8.0 TB/s
+                    "frac_vs_nominal_8000gbs": round(ach / 8000.0, 4) if ach else None}
         tkey = "gemm_schur" if cfg.dim == 3 else "gemm_schur_" + roof.get("schur_mode", "factored")
         roof.update({"traffic": traffic_for(cfg.name, tkey), "traffic_key": tkey,
                      "avg_launch_us": round(g2_ms / g2_n * 1e3, 2) if g2_n else None,
