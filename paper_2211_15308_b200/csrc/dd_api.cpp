@@ -719,11 +719,10 @@ static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const dou
         CK(cudaEventCreate(&c->solve_ev[1]));
     }
     CK(cudaEventRecord(c->solve_ev[0], c->stream));
-    CK(cudaMemsetAsync(c->ints, 0, sizeof(int) * 8, c->stream));
-    if (c->dim == 2) CK(cudaMemsetAsync(c->ntl, 0, sizeof(int) * (2 * (c->cols_pad / GEMM_BN_GROUPED) + 4), c->stream));
-    TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
-    if (c->dim == 2 && c->schur_mode == 2)
-        TIMED(DD_KCLASS_OTHER, launch_check_tiles(ncols, colp, c->ints + 6, c->stream));
+    // counters, live-tile list and the parameter checks in one launch
+    TIMED(DD_KCLASS_OTHER, launch_solve_prep(ncols, colp, c->n_param, c->ints, 8, c->ntl,
+                                             c->dim == 2 ? 2 * (c->cols_pad / GEMM_BN_GROUPED) + 4 : 0,
+                                             c->dim == 2 && c->schur_mode == 2, c->stream));
     PcgState st = make_state(c, ncols, colp, x, rtol, maxit, norm_kind);
     c->last_ps_warps = polesum_warps(c->geom);
     c->last_graph = 0;

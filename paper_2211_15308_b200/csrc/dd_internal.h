@@ -133,6 +133,10 @@ cudaError_t launch_pcg_small(const PcgState& s, const PoleGeom& g, const PoleTab
                              cudaStream_t st);
 cudaError_t launch_copy_cols(int n, int ncols, const double* src, int lds, double* dst, int ldd,
                              cudaStream_t st);
+// solve prologue: zero ints[0..nzero) and ntl[0..ntl_len), flag bad parameter ids (ints[5]) and,
+// with check_tiles, 32-column tiles holding two parameter sets (ints[6])
+cudaError_t launch_solve_prep(int ncols, const int* col_param, int n_param, int* ints, int nzero, int* ntl,
+                              int ntl_len, bool check_tiles, cudaStream_t st);
 // grouped Schur apply: *mixed = 1 if a 32-column tile holds two parameter sets
 cudaError_t launch_check_tiles(int ncols, const int* col_param, int* mixed, cudaStream_t st);
 // H_p = K_p G + γ_p F (W blocks at f_off, g_off) for all p: n rows, row stride ldh, H + p sH

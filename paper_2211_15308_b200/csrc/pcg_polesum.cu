@@ -899,6 +899,27 @@ __global__ void k_schur_operand(int n, int ncols, const int* __restrict__ col_pa
     }
 }
 
+// Solve prologue in one launch (one CTA): zero the solve's counters and live-tile list, then
+// flag out-of-range parameter ids (ints[5]) and, for the grouped Schur apply, 32-column tiles
+// that hold two parameter sets (ints[6]).
+__global__ void __launch_bounds__(1024) k_solve_prep(int ncols, const int* __restrict__ col_param, int n_param,
+                                                     int* ints, int nzero, int* ntl, int ntl_len, int check_tiles) {
+    for (int i = threadIdx.x; i < nzero; i += blockDim.x) ints[i] = 0;
+    for (int i = threadIdx.x; i < ntl_len; i += blockDim.x) ntl[i] = 0;
+    int bad = 0, mixed = 0;
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+        const int p = col_param[c];
+        bad |= (p < 0 || p >= n_param) ? 1 : 0;
+        if (check_tiles) mixed |= (p != col_param[c - c % GEMM_BN_GROUPED]) ? 1 : 0;
+    }
+    bad = __syncthreads_or(bad);        // also orders the zeroing above before the flag stores
+    mixed = __syncthreads_or(mixed);
+    if (threadIdx.x == 0) {
+        if (bad) ints[5] = 1;
+        if (mixed) ints[6] = 1;
+    }
+}
+
 // Grouped Schur apply: does any 32-column tile hold two parameter sets?  (*mixed |= 1)
 __global__ void k_check_tiles(int ncols, const int* __restrict__ col_param, int* mixed) {
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
@@ -1082,6 +1103,12 @@ cudaError_t launch_schur_operand(int n, int ncols, const int* col_param, int n_p
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
     k_schur_operand<<<blocks, 256, 0, st>>>(n, ncols, col_param, n_param, Kp, gp, x, ldx, Z, ldz, zhalf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_solve_prep(int ncols, const int* col_param, int n_param, int* ints, int nzero, int* ntl,
+                              int ntl_len, bool check_tiles, cudaStream_t st) {
+    k_solve_prep<<<1, 1024, 0, st>>>(ncols, col_param, n_param, ints, nzero, ntl, ntl_len, check_tiles ? 1 : 0);
     return cudaGetLastError();
 }
 

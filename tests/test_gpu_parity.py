@@ -203,14 +203,14 @@ def test_profile_and_launch_counts(lib, mode):
         assert prof["polesum_pcg"][1] == k and prof["gemm_schur"][1] == k
         if mode == "factored":
             assert prof["gemm_dst"][1] == k
-            assert n_launch == 2 + 3 * k        # check_params, init, then K1 + K2 + pole sum per iteration
+            assert n_launch == 2 + 3 * k        # solve prologue, init, then K1 + K2 + pole sum per iteration
             assert all(v[0] > 0 for v in prof.values())
         elif mode == "assembled":
             assert prof["gemm_dst"][1] == 0     # the interior solve lives in G (setup)
-            assert n_launch == 2 + 2 * k        # check_params, init, then [F | G] GEMM + pole sum
+            assert n_launch == 2 + 2 * k        # solve prologue, init, then [F | G] GEMM + pole sum
         else:
             assert prof["gemm_dst"][1] == 0
-            assert n_launch == 3 + 2 * k        # + the 32-column tile check, then H_p GEMM + pole sum
+            assert n_launch == 2 + 2 * k        # solve prologue (incl. the tile check), init, H_p GEMM + pole sum
         with pytest.raises(lib.DDError):
             S.set_schur_mode("bogus")
     finally:
