@@ -165,6 +165,34 @@ def test_edge_cases(lib):
         lib.Solver(2, 1, params, ras, max_cols=1)
 
 
+@pytest.mark.parametrize("mode", MODES)
+def test_edge_cases_general_path(lib, mode):
+    """The batched path (GEMM + fused PCG kernel in the WHILE graph, n > 63): a zero right-hand side
+    next to live ones, maxit reached (DD_ENOCONV, outputs valid), maxit = 0, an out-of-range
+    parameter id (DD_EINVAL from the device-side check) and a 33-column batch (ragged tiles)."""
+    N = 128; params = [(1.0, 1e2), (1e-3, 1e5)]; ras = fit_all(N, params, 12)
+    S = _solver(lib, N, params, ras, max_cols=40)
+    S.set_schur_mode(mode)
+    try:
+        B = np.random.default_rng(3).uniform(-1, 1, (33, N - 1)); B[5] = 0.0
+        colp = (np.arange(33) // 17).astype(np.int32)
+        r = S.pcg_solve(_cols(B), colp)
+        assert S.query_config()["graph_while"] == 1
+        assert r.iters[5] == 0 and np.all(r.x.cpu().numpy()[5] == 0) and np.all(np.delete(r.iters, 5) > 0)
+        assert np.all(r.rel_res <= 1e-10)
+        r2 = S.pcg_solve(_cols(B), colp, maxit=3)
+        assert r2.status == lib.DD_ENOCONV and r2.iters.max() == 3
+        r0 = S.pcg_solve(_cols(B), colp, maxit=0)
+        assert r0.status == lib.DD_ENOCONV and np.all(r0.iters == 0) and np.all(r0.x.cpu().numpy() == 0)
+        bad = colp.copy(); bad[7] = 9
+        with pytest.raises(lib.DDError):
+            S.pcg_solve(_cols(B), bad)
+        r3 = S.pcg_solve(_cols(B), colp)          # the handle is still usable after the error
+        assert np.array_equal(r3.x.cpu().numpy(), r.x.cpu().numpy())
+    finally:
+        S.close()
+
+
 @pytest.mark.parametrize("N", [32, 48, 64])
 def test_small_persistent_kernel_matches_general_path(lib, N, monkeypatch):
     # n <= 63 runs the whole PCG in one launch (K7); it must agree with the GEMM/graph path.
