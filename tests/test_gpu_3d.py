@@ -124,6 +124,24 @@ def test_host_api_3d(case3):
     assert np.array_equal(h.iters, a.iters)
 
 
+def test_edge_cases_3d(lib):
+    """3D solve: a zero right-hand side beside live ones (0 iterations, x = 0), maxit reached
+    (DD_ENOCONV, outputs valid), an out-of-range parameter id (DD_EINVAL)."""
+    N = 8; params = [(1.0, 1e4)]
+    ras = _fit(N, params, 10)
+    S = lib.Solver(3, N, params, ras, max_cols=3, device=0)
+    try:
+        B = np.random.default_rng(5).uniform(-1, 1, (3, (N - 1) ** 2)); B[1] = 0.0
+        r = S.pcg_solve(torch.as_tensor(B, device="cuda"), [0, 0, 0])
+        assert r.iters[1] == 0 and np.all(r.x.cpu().numpy()[1] == 0) and r.iters[0] > 0 and r.iters[2] > 0
+        r2 = S.pcg_solve(torch.as_tensor(B, device="cuda"), [0, 0, 0], maxit=2)
+        assert r2.status == lib.DD_ENOCONV and r2.iters.max() == 2
+        with pytest.raises(lib.DDError):
+            S.pcg_solve(torch.as_tensor(B, device="cuda"), [0, 3, 0])
+    finally:
+        S.close()
+
+
 def test_full_size_3d_properties(lib):
     """Config 4 (N = 128, n_Γ = 16129) at full size: (i) on sine modes of the face the bulk part is
     K s_ab (oracle's mode-wise elimination); (ii) the fractional term satisfies
