@@ -172,16 +172,18 @@ dd_status dd_pcg_solve_host(dd_ctx* ctx, int ncols, const int* col_param_host,
                             int norm_kind, int* iters, double* rel_res, double* hist);
 
 /*
- * dd_bulk_solve — the full DD solve of the discrete Eq.(2) on a BULK right-hand side (2D
- * handles): block elimination with the exact leading block (PAPER.md:
- * 123-145 Eq.(5), 229-230 "(A^00)^-1 ... computed exactly"):
+ * dd_bulk_solve — the full DD solve of the discrete Eq.(2) on a BULK right-hand side (SURVEY
+ * §8(f) NEXT-1): block elimination with the exact leading block (PAPER.md: 123-145 Eq.(5),
+ * 229-230 "(A^00)^-1 ... computed exactly"):
  *     g = b_Γ - A^{i0}(A^00)^-1 b_0,   x_Γ = S^-1 g (dd_pcg_solve),   x_0 = (A^00)^-1(b_0 - A^{0i} x_Γ)
- * with (A^00)^-1 by full-field fast diagonalisation (DST-I along both axes, batched DMMA).
- *   b, x   DEVICE, column c at c*(n^2 + n): [interior nodes (i h, j h), i, j = 1..n, at
- *          (i-1) n + (j-1)  (x-major);  Γ nodes (0, j h) at n^2 + (j-1)],  n = N - 1
+ * with (A^00)^-1 by full-field fast diagonalisation (DST-I along every axis, batched DMMA).
+ *   b, x   DEVICE.  2D: column c at c*(n^2 + n): [interior nodes (i h, j h), i, j = 1..n, at
+ *          (i-1) n + (j-1)  (x-major);  Γ nodes (0, j h) at n^2 + (j-1)],  n = N - 1.
+ *          3D: column c at c*(n^3 + n^2): [interior (i h, j h, k h) at (i-1) n^2 + (j-1) n + (k-1);
+ *          Γ nodes (0, j h, k h) at n^3 + (j-1) n + (k-1)].
  *   rtol, maxit, norm_kind, iters, rel_res: as dd_pcg_solve (for the interface PCG)
- * Allocates its workspaces (2 max_cols x Kpad^2 fields) on first use.  Returns
- * DD_EUNSUPPORTED for 3D handles; otherwise as dd_pcg_solve.  Synchronous.
+ * Allocates its workspaces on first use (2D: 2 max_cols x Kpad^2 fields; 3D: 3 max_cols x n x
+ * ldf^2 fields and a layer-major copy).  Otherwise as dd_pcg_solve.  Synchronous.
  */
 dd_status dd_bulk_solve(dd_ctx* ctx, int ncols, const int* col_param, const double* b, double* x,
                         double rtol, int maxit, int norm_kind, int* iters, double* rel_res);

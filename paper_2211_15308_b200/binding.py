@@ -218,14 +218,14 @@ class Solver:
         return SolveResult(x, iters, rel, hist, st)
 
     def bulk_solve(self, b, col_param, x=None, rtol=1e-10, maxit=500, norm_kind=0):
-        """Full DD solve on bulk right-hand sides (2D): b is (ncols, n^2 + n) — interior nodes
-        x-major, then the Γ nodes (include/dd_api.h dd_bulk_solve)."""
+        """Full DD solve on bulk right-hand sides: b is (ncols, n^d + n^(d-1)) — interior nodes
+        x-major (2D: (i, j); 3D: (i, j, k)), then the Γ nodes (include/dd_api.h dd_bulk_solve)."""
         t = self._torch
         n = self.N - 1
         if not isinstance(b, t.Tensor):
             b = t.as_tensor(_f64(b), device=self.device)
         assert b.dtype == t.float64 and b.is_contiguous() and b.device == self.device
-        assert b.dim() == 2 and b.shape[1] == n * n + n
+        assert b.dim() == 2 and b.shape[1] == (n * n + n if self.dim == 2 else n ** 3 + n * n)
         ncols = b.shape[0]
         x = t.empty_like(b) if x is None else x
         cp = self._cols(col_param)

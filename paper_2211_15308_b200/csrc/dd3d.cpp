@@ -543,6 +543,55 @@ dd_status pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double*
     return DD_OK;
 }
 
+// Full DD solve on bulk right-hand sides (3D; bulk3d.cu has the algebra)
+dd_status bulk_solve_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
+                        int norm_kind, int* iters, double* rel_res) {
+    Face3& f = c->f3;
+    const int n = f.n, ldf = f.ldf, lk = f.ldf;
+    const long long NP = f.NP;
+    const size_t slack = (size_t)64 * ldf;
+    const size_t field = (size_t)c->max_cols * n * NP + slack, faces = (size_t)c->max_cols * NP + slack;
+    if (!f.b3X) {
+        for (double** v : {&f.b3X, &f.b3T, &f.b3Y}) DD_CK(dalloc(c, v, field));
+        DD_CK(dalloc(c, &f.b3L, (size_t)c->max_cols * NP * lk + slack));
+        for (double** v : {&f.b3G, &f.b3W, &f.b3W2}) DD_CK(dalloc(c, v, faces));
+        DD_CK(dalloc(c, &f.b3g, (size_t)c->max_cols * f.n2));
+        DD_CK(dalloc(c, &f.b3xg, (size_t)c->max_cols * f.n2));
+        std::vector<double> sig(n);
+        const long double PI = 3.141592653589793238462643383279502884L;
+        for (int a = 0; a < n; a++) {
+            const long double sh = sinl(PI * (a + 1) / (2.0L * c->N));
+            sig[a] = (double)(4.0L * sh * sh);
+        }
+        DD_CK(dalloc(c, &f.b3sig, (size_t)n));
+        DD_CK(cudaMemcpyAsync(f.b3sig, sig.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaStreamSynchronize(c->stream));
+    }
+    const long long nb = (long long)n * n * n + (long long)n * n;
+    const double* s1 = f.S;                  // row 1 of Q (the first interior layer)
+    // Ŷ = (Q⊗Q⊗Q b_0) / Σ;  b_Γ -> G
+    DD_TIMED(DD_KCLASS_OTHER, bulk3_in(n, ldf, NP, ncols, b, nb, f.b3X, f.b3G, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, bulk3_forward(n, ldf, lk, NP, ncols, f.S, f.b3sig, f.b3X, f.b3T, f.b3L, f.b3Y,
+                                               c->stream));
+    // g = b_Γ + (L^-1 b_0)|_{i=1} = b_Γ + (Q⊗Q) Σ_a s1_a Ŷ_a
+    DD_TIMED(DD_KCLASS_OTHER, bulk3_layer1(n, NP, ncols, f.b3Y, s1, f.b3W, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.b3W, f.b3W2, ncols, n, ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.b3W2, f.b3W, ncols, n, ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_OTHER, bulk3_g(n, ldf, NP, ncols, f.b3G, f.b3W, f.b3g, c->stream));
+    // x_Γ = S^-1 g  (the interface PCG of this handle)
+    dd_status ps = dd_pcg_solve(c, ncols, colp, f.b3g, f.b3xg, rtol, maxit, norm_kind, iters, rel_res, nullptr);
+    if (ps != DD_OK && ps != DD_ENOCONV) return ps;
+    // x̂_0 = Ŷ / (K h) + s1 ⊗ (Q⊗Q x_Γ) / Σ;  x_0 = Q⊗Q⊗Q x̂_0
+    DD_TIMED(DD_KCLASS_OTHER, bulk3_pad(n, ldf, NP, ncols, f.b3xg, f.b3W2, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.b3W2, f.b3W, ncols, n, ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.b3W, f.b3W2, ncols, n, ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_OTHER, bulk3_combine(n, ldf, NP, ncols, f.b3Y, f.b3W2, s1, f.b3sig, colp, c->n_param, c->Kp,
+                                            1.0 / c->N, c->stream));
+    DD_TIMED(DD_KCLASS_GEMM_DST, bulk3_inverse(n, ldf, lk, NP, ncols, f.S, f.b3Y, f.b3T, f.b3L, f.b3X, c->stream));
+    DD_TIMED(DD_KCLASS_OTHER, bulk3_out(n, ldf, NP, ncols, f.b3X, f.b3xg, x, nb, c->stream));
+    return ps;
+}
+
 }  // namespace dd
 
 extern "C" dd_status dd_nccl_unique_id(void* out128) {

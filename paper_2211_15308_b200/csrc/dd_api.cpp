@@ -933,7 +933,6 @@ static dd_status bulk_check(dd_ctx* c, int ncols, const int* colp, const double*
                             int norm_kind) {
     dd_status s = check_cols(c, ncols, colp);
     if (s != DD_OK) return s;
-    if (c->dim != 2) return fail(DD_EUNSUPPORTED, "bulk solves: 2D handles only");
     if (ncols > 0 && (!b || !x)) return fail(DD_EINVAL, "b/x NULL");
     if (!(rtol >= 0.0) || maxit < 0 || (norm_kind != 0 && norm_kind != 1)) return fail(DD_EINVAL, "rtol/maxit/norm_kind");
     return DD_OK;
@@ -944,6 +943,12 @@ extern "C" dd_status dd_bulk_solve(dd_ctx* c, int ncols, const int* colp, const 
     dd_status s = bulk_check(c, ncols, colp, b, x, rtol, maxit, norm_kind);
     if (s != DD_OK || ncols == 0) return s;
     CK(cudaSetDevice(c->device));
+    if (c->dim == 3) {
+        dd_status ps = bulk_solve_3d(c, ncols, colp, b, x, rtol, maxit, norm_kind, iters, rel_res);
+        if (ps != DD_OK && ps != DD_ENOCONV) return ps;
+        CK(cudaStreamSynchronize(c->stream));
+        return ps;
+    }
     TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
     dd_status ps = bulk_eliminate(c, ncols, colp, b, x, true, rtol, maxit, norm_kind, iters, rel_res);
     if (ps != DD_OK && ps != DD_ENOCONV) return ps;
@@ -957,6 +962,7 @@ extern "C" dd_status dd_bulk_pcg_solve(dd_ctx* c, int ncols, const int* colp, co
                                        int maxit, int* iters, double* rel_res) {
     dd_status s = bulk_check(c, ncols, colp, b, x, rtol, maxit, 0);
     if (s != DD_OK || ncols == 0) return s;
+    if (c->dim != 2) return fail(DD_EUNSUPPORTED, "bulk PCG: 2D handles only");
     if (c->frac_mode != DD_FRAC_DENSE) return fail(DD_EUNSUPPORTED, "bulk PCG: dense fractional term only");
     CK(cudaSetDevice(c->device));
     const int n = c->n, ldf = c->Kpad;

@@ -61,6 +61,10 @@ struct Face3 {
     long long NP = 0;                 // padded face size ldf^2
     double* S = nullptr;              // sine matrix, round_up(n,64) x ldf row-major, zero padded
     double* sw = nullptr;             // Schur weights s_ab, NP (padded layout)
+    // 3D bulk solve (dd_bulk_solve, allocated on first use): fields [col][layer][face] (+ slack),
+    // the layer-major copy [col][face][layer], face buffers [col][face], user-layout Γ vectors, σ
+    double *b3X = nullptr, *b3T = nullptr, *b3L = nullptr, *b3Y = nullptr;
+    double *b3G = nullptr, *b3W = nullptr, *b3W2 = nullptr, *b3g = nullptr, *b3xg = nullptr, *b3sig = nullptr;
     double* F = nullptr;              // dense fractional term, rows round_up(NP,256) x NP row-major (DD_FX_FULL=1)
     double* Fp = nullptr;             // packed-symmetric F: upper 128 x 128 blocks in 16-column slabs (default)
     int* fblk = nullptr;              // (I, J) of each packed block
@@ -194,6 +198,8 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
                    const double* c0, const dd_dist* dist);
 dd_status schur_3d(dd_ctx* c, int ncols, const int* colp, const double* xin, double* yout, bool user_layout);
 dd_status precond_3d(dd_ctx* c, int ncols, const int* colp, const double* rin, double* zout, bool user_layout);
+dd_status bulk_solve_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
+                        int norm_kind, int* iters, double* rel_res);
 dd_status pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
                  int norm_kind);
 void destroy_3d(dd_ctx* c);

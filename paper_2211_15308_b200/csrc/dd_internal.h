@@ -193,6 +193,21 @@ struct Pcg3 {
     int* status;
 };
 cudaError_t face_slab_pass(const double* in, double* out, int nslab, int n, int ldf, const double* S, cudaStream_t st);
+// 3D bulk solve (bulk3d.cu): full-field fast diagonalisation of the interior block
+cudaError_t bulk3_forward(int n, int ldf, int lk, long long NP, int ncols, const double* S, const double* sig,
+                          const double* X, double* T, double* Lk, double* Y, cudaStream_t st);
+cudaError_t bulk3_inverse(int n, int ldf, int lk, long long NP, int ncols, const double* S, const double* Y, double* T,
+                          double* Lk, double* X, cudaStream_t st);
+cudaError_t bulk3_in(int n, int ldf, long long NP, int ncols, const double* b, long long ldb, double* X, double* G,
+                     cudaStream_t st);
+cudaError_t bulk3_layer1(int n, long long NP, int ncols, const double* Y, const double* s1, double* w, cudaStream_t st);
+cudaError_t bulk3_g(int n, int ldf, long long NP, int ncols, const double* G, const double* W, double* g, cudaStream_t st);
+cudaError_t bulk3_pad(int n, int ldf, long long NP, int ncols, const double* xg, double* P, cudaStream_t st);
+cudaError_t bulk3_combine(int n, int ldf, long long NP, int ncols, double* Y, const double* XG, const double* s1,
+                          const double* sig, const int* col_param, int n_param, const double* Kp, double h,
+                          cudaStream_t st);
+cudaError_t bulk3_out(int n, int ldf, long long NP, int ncols, const double* X, const double* xg, double* x, long long ldx,
+                      cudaStream_t st);
 cudaError_t face_slab_pass_scaled(const double* in, double* out, int nslab, int n, int ldf, const double* S,
                                   const double* w, long long sW, int group, const double* colscale, cudaStream_t st);
 // packed-symmetric F stream (fx_sym.cu): upper 128 x 128 blocks, one read per block, two products
