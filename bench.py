@@ -459,8 +459,6 @@ def run_bulk(args, cfg, world, rank):
     C = cfg.n_cols
     rng = np.random.default_rng(1000 + rank)
     nb = n * n + n if cfg.dim == 2 else n ** 3 + n * n
-    if cfg.dim == 3 and args.mode != "bulk":
-        raise SystemExit("bulk PCG: 2D configs only")
     Bb = rng.uniform(-1.0, 1.0, (C, nb))
     colp = (np.arange(C) // cfg.rhs_per_param).astype(np.int32)
     S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local)

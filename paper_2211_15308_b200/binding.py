@@ -236,13 +236,13 @@ class Solver:
         return SolveResult(x, iters, rel, None, st)
 
     def bulk_pcg_solve(self, b, col_param, x=None, rtol=1e-10, maxit=500):
-        """PCG on the bulk system with the Eq.(5) DD preconditioner (dd_bulk_pcg_solve, 2D)."""
+        """PCG on the bulk system with the Eq.(5) DD preconditioner (dd_bulk_pcg_solve)."""
         t = self._torch
         n = self.N - 1
         if not isinstance(b, t.Tensor):
             b = t.as_tensor(_f64(b), device=self.device)
         assert b.dtype == t.float64 and b.is_contiguous() and b.device == self.device
-        assert b.dim() == 2 and b.shape[1] == n * n + n
+        assert b.dim() == 2 and b.shape[1] == (n * n + n if self.dim == 2 else n ** 3 + n * n)
         ncols = b.shape[0]
         x = t.empty_like(b) if x is None else x
         cp = self._cols(col_param)

@@ -260,14 +260,120 @@ cudaError_t bulk_apply(int n, int ncols, const double* x, long long nb, const do
     k_bulk_apply<<<grid_for(nb * ncols), 256, 0, st>>>(n, ncols, x, nb, fx, ldfx, col_param, n_param, Kp, gp, y);
     return cudaGetLastError();
 }
+// ---- long columns, few of them (3D bulk: 2 M entries x 8 columns): NBLK CTAs per column; the
+// dot products go through per-CTA partials summed in CTA order (deterministic), the scalar
+// recurrences run in one thread per column
+constexpr int NBLK = 64;
+__global__ void k_coldot(long long nb, const double* __restrict__ a, const double* __restrict__ b,
+                         const int* __restrict__ active, int all, double* __restrict__ part) {
+    __shared__ double red[32];
+    const int c = blockIdx.y, blk = blockIdx.x;
+    if (!all && !active[c]) return;
+    const long long chunk = (nb + NBLK - 1) / NBLK, i0 = blk * chunk, i1 = min(nb, i0 + chunk);
+    const size_t off = (size_t)c * nb;
+    double s = 0.0;
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) s = fma(a[off + i], b[off + i], s);
+    s = bpcg_block_sum(s, red);
+    if (threadIdx.x == 0) part[(size_t)c * NBLK + blk] = s;
+}
+__device__ __forceinline__ double part_sum(const double* part, int c) {
+    double s = 0.0;
+    for (int b = 0; b < NBLK; b++) s += part[(size_t)c * NBLK + b];
+    return s;
+}
+__global__ void k_bpcg_a2(long long nb, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                          const double* __restrict__ q, const double* __restrict__ rho, int* __restrict__ active,
+                          int* __restrict__ status, const double* __restrict__ part) {
+    const int c = blockIdx.y, blk = blockIdx.x;
+    if (!active[c]) return;
+    const double pq = part_sum(part, c);
+    if (!(pq > 0.0)) {
+        if (blk == 0 && threadIdx.x == 0) { atomicExch(status, (int)DD_ENOTSPD); active[c] = 0; }
+        return;
+    }
+    const double alpha = rho[c] / pq;
+    const long long chunk = (nb + NBLK - 1) / NBLK, i0 = blk * chunk, i1 = min(nb, i0 + chunk);
+    const size_t off = (size_t)c * nb;
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        x[off + i] = fma(alpha, p[off + i], x[off + i]);
+        r[off + i] = fma(-alpha, q[off + i], r[off + i]);
+    }
+}
+// scalar step of k_bpcg_b per column: beta[c] = β (update p) or NaN (frozen / init)
+__global__ void k_bpcg_b2(int ncols, double* __restrict__ rho, double* __restrict__ eta0, double* __restrict__ relres,
+                          int* __restrict__ active, int* __restrict__ iters, int k, double rtol, int maxit, int init,
+                          int* __restrict__ n_active, int* __restrict__ status, const double* __restrict__ part,
+                          double* __restrict__ beta) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncols) return;
+    beta[c] = __longlong_as_double(0x7ff8000000000000ll);
+    if (!init && !active[c]) return;
+    const double rz = part_sum(part, c);
+    const double eta = sqrt(fmax(rz, 0.0));
+    if (init) {
+        eta0[c] = eta; rho[c] = rz; iters[c] = 0; relres[c] = eta > 0.0 ? 1.0 : 0.0;
+        if (rz < 0.0) atomicExch(status, (int)DD_ENOTSPD);
+        const bool act = eta > 0.0 && rz >= 0.0;
+        active[c] = act;
+        if (act) atomicAdd(n_active, 1);
+        return;
+    }
+    const bool conv = eta <= rtol * eta0[c];
+    iters[c] = k;
+    relres[c] = eta0[c] > 0.0 ? eta / eta0[c] : 0.0;
+    if (rz < 0.0) atomicExch(status, (int)DD_ENOTSPD);
+    if (conv || rz < 0.0 || k >= maxit) { active[c] = 0; return; }
+    beta[c] = rz / rho[c];
+    rho[c] = rz;
+    atomicAdd(n_active, 1);
+}
+__global__ void k_bpcg_b3(long long nb, const double* __restrict__ z, double* __restrict__ p, int init,
+                          const double* __restrict__ beta) {
+    const int c = blockIdx.y, blk = blockIdx.x;
+    const double bt = beta[c];
+    if (!init && isnan(bt)) return;
+    const long long chunk = (nb + NBLK - 1) / NBLK, i0 = blk * chunk, i1 = min(nb, i0 + chunk);
+    const size_t off = (size_t)c * nb;
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x)
+        p[off + i] = init ? z[off + i] : fma(bt, p[off + i], z[off + i]);
+}
+static bool bpcg_wide(int ncols, long long nb) { return ncols < 148 && nb >= (1ll << 18); }
+static double* bpcg_ws(int ncols) {
+    static double* ws = nullptr;
+    static int cap = 0;
+    if (ncols > cap) {
+        if (ws) cudaFree(ws);
+        cap = ncols < 64 ? 64 : ncols;
+        if (cudaMalloc(&ws, sizeof(double) * (size_t)cap * (NBLK + 1)) != cudaSuccess) { ws = nullptr; cap = 0; }
+    }
+    return ws;
+}
+
 cudaError_t bpcg_a(int ncols, long long nb, double* x, double* r, const double* p, const double* q, const double* rho,
                    int* active, int* status, cudaStream_t st) {
+    if (bpcg_wide(ncols, nb)) {
+        double* part = bpcg_ws(ncols);
+        if (!part) return cudaErrorMemoryAllocation;
+        k_coldot<<<dim3(NBLK, ncols), 512, 0, st>>>(nb, p, q, active, 0, part);
+        k_bpcg_a2<<<dim3(NBLK, ncols), 512, 0, st>>>(nb, x, r, p, q, rho, active, status, part);
+        return cudaGetLastError();
+    }
     k_bpcg_a<<<ncols, 1024, 0, st>>>(nb, x, r, p, q, rho, active, status);
     return cudaGetLastError();
 }
 cudaError_t bpcg_b(int ncols, long long nb, const double* r, const double* z, double* p, double* rho, double* eta0,
                    double* relres, int* active, int* iters, int k, double rtol, int maxit, int init, int* n_active,
                    int* status, cudaStream_t st) {
+    if (bpcg_wide(ncols, nb)) {
+        double* part = bpcg_ws(ncols);
+        if (!part) return cudaErrorMemoryAllocation;
+        double* beta = part + (size_t)ncols * NBLK;
+        k_coldot<<<dim3(NBLK, ncols), 512, 0, st>>>(nb, r, z, active, init, part);
+        k_bpcg_b2<<<(ncols + 127) / 128, 128, 0, st>>>(ncols, rho, eta0, relres, active, iters, k, rtol, maxit, init,
+                                                      n_active, status, part, beta);
+        k_bpcg_b3<<<dim3(NBLK, ncols), 512, 0, st>>>(nb, z, p, init, beta);
+        return cudaGetLastError();
+    }
     k_bpcg_b<<<ncols, 1024, 0, st>>>(nb, r, z, p, rho, eta0, relres, active, iters, k, rtol, maxit, init, n_active,
                                       status);
     return cudaGetLastError();

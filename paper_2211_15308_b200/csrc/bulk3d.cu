@@ -137,6 +137,46 @@ __global__ void k_b3_out(int n, int ldf, long long NP, int ncols, const double* 
     }
 }
 
+// out = 𝒜 x on the bulk product layout: K h (7-point interior stencil; Γ rows 3, -1/2 in-face,
+// -1 to the first layer) + γ F x_Γ on the Γ rows (fx: padded faces, γ already applied)
+__global__ void k_b3_apply(int n, int ldf, long long NP, int ncols, const double* __restrict__ x, long long ldx,
+                           const double* __restrict__ fx, const int* __restrict__ col_param, int n_param,
+                           const double* __restrict__ Kp, double h, double* __restrict__ out) {
+    const long long n2 = (long long)n * n, n3 = n2 * n;
+    const long long per = n3 + n2;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < per * ncols;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long c = idx / per, e = idx % per;
+        const double* xc = x + c * ldx;
+        int p = col_param[c];
+        p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
+        const double Kh = Kp[p] * h;
+        if (e < n3) {
+            const int i = (int)(e / n2), j = (int)((e % n2) / n), k = (int)(e % n);
+            double v = 6.0 * xc[e];
+            v -= i > 0 ? xc[e - n2] : xc[n3 + (long long)j * n + k];          // i = 1 couples to Γ
+            if (i + 1 < n) v -= xc[e + n2];
+            if (j > 0) v -= xc[e - n];
+            if (j + 1 < n) v -= xc[e + n];
+            if (k > 0) v -= xc[e - 1];
+            if (k + 1 < n) v -= xc[e + 1];
+            out[c * ldx + e] = Kh * v;
+        } else {
+            const long long jk = e - n3;
+            const int j = (int)(jk / n), k = (int)(jk % n);
+            const double* g = xc + n3;
+            double v = 3.0 * g[jk] - xc[jk];                                   // xc[jk]: layer 1, same (j, k)
+            double nb = 0.0;
+            if (j > 0) nb += g[jk - n];
+            if (j + 1 < n) nb += g[jk + n];
+            if (k > 0) nb += g[jk - 1];
+            if (k + 1 < n) nb += g[jk + 1];
+            v -= 0.5 * nb;
+            out[c * ldx + e] = fma(Kh, v, fx[c * NP + (long long)j * ldf + k]);
+        }
+    }
+}
+
 static int grid_of(long long total) {
     long long b = (total + 255) / 256;
     return (int)(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b));
@@ -182,6 +222,12 @@ cudaError_t bulk3_combine(int n, int ldf, long long NP, int ncols, double* Y, co
                           cudaStream_t st) {
     k_b3_combine<<<grid_of((long long)ncols * n * NP), 256, 0, st>>>(n, ldf, NP, ncols, Y, XG, s1, sig, col_param,
                                                                       n_param, Kp, h);
+    return cudaGetLastError();
+}
+cudaError_t bulk3_apply(int n, int ldf, long long NP, int ncols, const double* x, long long ldx, const double* fx,
+                        const int* col_param, int n_param, const double* Kp, double h, double* out, cudaStream_t st) {
+    const long long per = (long long)n * n * n + (long long)n * n;
+    k_b3_apply<<<grid_of(per * ncols), 256, 0, st>>>(n, ldf, NP, ncols, x, ldx, fx, col_param, n_param, Kp, h, out);
     return cudaGetLastError();
 }
 cudaError_t bulk3_out(int n, int ldf, long long NP, int ncols, const double* X, const double* xg, double* x, long long ldx,

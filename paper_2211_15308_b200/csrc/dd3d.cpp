@@ -544,8 +544,18 @@ dd_status pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double*
 }
 
 // Full DD solve on bulk right-hand sides (3D; bulk3d.cu has the algebra)
+// exact: x_Γ by the interface PCG (the bulk solve); else the Eq.(5) DD preconditioner 𝓑 with
+// S_Γ^-1 realised by the handle's RA (the bulk PCG's preconditioner)
+static dd_status bulk_eliminate_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, bool exact,
+                                   double rtol, int maxit, int norm_kind, int* iters, double* rel_res);
+
 dd_status bulk_solve_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
                         int norm_kind, int* iters, double* rel_res) {
+    return bulk_eliminate_3d(c, ncols, colp, b, x, true, rtol, maxit, norm_kind, iters, rel_res);
+}
+
+static dd_status bulk_eliminate_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, bool exact,
+                                   double rtol, int maxit, int norm_kind, int* iters, double* rel_res) {
     Face3& f = c->f3;
     const int n = f.n, ldf = f.ldf, lk = f.ldf;
     const long long NP = f.NP;
@@ -578,9 +588,16 @@ dd_status bulk_solve_3d(dd_ctx* c, int ncols, const int* colp, const double* b, 
     DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.b3W, f.b3W2, ncols, n, ldf, f.S, c->stream));
     DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.b3W2, f.b3W, ncols, n, ldf, f.S, c->stream));
     DD_TIMED(DD_KCLASS_OTHER, bulk3_g(n, ldf, NP, ncols, f.b3G, f.b3W, f.b3g, c->stream));
-    // x_Γ = S^-1 g  (the interface PCG of this handle)
-    dd_status ps = dd_pcg_solve(c, ncols, colp, f.b3g, f.b3xg, rtol, maxit, norm_kind, iters, rel_res, nullptr);
-    if (ps != DD_OK && ps != DD_ENOCONV) return ps;
+    dd_status ps = DD_OK;
+    if (exact) {
+        // x_Γ = S^-1 g  (the interface PCG of this handle)
+        ps = dd_pcg_solve(c, ncols, colp, f.b3g, f.b3xg, rtol, maxit, norm_kind, iters, rel_res, nullptr);
+        if (ps != DD_OK && ps != DD_ENOCONV) return ps;
+    } else {
+        // z_Γ = P g  (Eq.(5)'s S_Γ^-1 by the RA preconditioner, Eq.(8))
+        ps = precond_3d(c, ncols, colp, f.b3g, f.b3xg, true);
+        if (ps != DD_OK) return ps;
+    }
     // x̂_0 = Ŷ / (K h) + s1 ⊗ (Q⊗Q x_Γ) / Σ;  x_0 = Q⊗Q⊗Q x̂_0
     DD_TIMED(DD_KCLASS_OTHER, bulk3_pad(n, ldf, NP, ncols, f.b3xg, f.b3W2, c->stream));
     DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.b3W2, f.b3W, ncols, n, ldf, f.S, c->stream));
@@ -590,6 +607,75 @@ dd_status bulk_solve_3d(dd_ctx* c, int ncols, const int* colp, const double* b, 
     DD_TIMED(DD_KCLASS_GEMM_DST, bulk3_inverse(n, ldf, lk, NP, ncols, f.S, f.b3Y, f.b3T, f.b3L, f.b3X, c->stream));
     DD_TIMED(DD_KCLASS_OTHER, bulk3_out(n, ldf, NP, ncols, f.b3X, f.b3xg, x, nb, c->stream));
     return ps;
+}
+
+// PCG on the 3D bulk system 𝒜 x = b preconditioned by 𝓑 (Eq.(5)), x0 = 0, stopping on
+// sqrt(r·𝓑r) <= rtol sqrt(r0·𝓑r0) (reading A1) — the 2D loop of dd_api.cpp
+dd_status bulk_pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
+                      int* iters, double* rel_res) {
+    Face3& f = c->f3;
+    const int n = f.n, ldf = f.ldf;
+    const long long NP = f.NP;
+    const long long nb = (long long)n * n * n + (long long)n * n;
+    if (!c->bpcg_r) {
+        for (double** v : {&c->bpcg_r, &c->bpcg_p, &c->bpcg_q, &c->bpcg_z}) DD_CK(dalloc(c, v, (size_t)nb * c->max_cols));
+    }
+    if (!f.b3Z) {
+        DD_CK(dalloc(c, &f.b3Z, (size_t)c->max_cols * NP + (size_t)64 * ldf));    // zero faces (F-stream D)
+        DD_CK(dalloc(c, &f.b3F, (size_t)c->max_cols * NP + (size_t)64 * ldf));
+        DD_CK(dalloc(c, &f.b3P, (size_t)c->max_cols * NP + (size_t)64 * ldf));
+    }
+    DD_CK(cudaMemsetAsync(c->ints, 0, sizeof(int) * 8, c->stream));
+    DD_TIMED(DD_KCLASS_OTHER, launch_check_params(ncols, colp, c->n_param, c->ints + 5, c->stream));
+    DD_CK(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)nb * ncols, c->stream));
+    DD_CK(cudaMemcpyAsync(c->bpcg_r, b, sizeof(double) * (size_t)nb * ncols, cudaMemcpyDeviceToDevice, c->stream));
+    auto apply = [&](const double* in, double* out) -> dd_status {
+        for (int col = 0; col < ncols; col++)
+            DD_TIMED(DD_KCLASS_OTHER, bulk3_pad(n, ldf, NP, 1, in + (size_t)col * nb + (size_t)n * n * n,
+                                                f.b3P + (size_t)col * NP, c->stream));
+        if (f.Fp) {
+            DD_TIMED(DD_KCLASS_GEMM_SCHUR, fx_sym_apply(f.Fp, f.fblk, NP, f.b3P, f.b3F, f.b3Z, ncols, colp, c->n_param,
+                                                        c->gp, f.fxD, f.fxT, c->num_sms, c->stream));
+        } else {
+            DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, NP, f.b3P, f.b3F, f.b3Z, ncols, colp, c->n_param, c->gp, f.fx_ws,
+                                                   f.fx_cnt, c->num_sms, c->stream));
+        }
+        DD_TIMED(DD_KCLASS_OTHER, bulk3_apply(n, ldf, NP, ncols, in, nb, f.b3F, colp, c->n_param, c->Kp, 1.0 / c->N, out,
+                                              c->stream));
+        return DD_OK;
+    };
+    dd_status st;
+    if ((st = bulk_eliminate_3d(c, ncols, colp, c->bpcg_r, c->bpcg_z, false, 0, 0, 0, nullptr, nullptr)) != DD_OK)
+        return st;
+    DD_TIMED(DD_KCLASS_OTHER, bpcg_b(ncols, nb, c->bpcg_r, c->bpcg_z, c->bpcg_p, c->rho, c->eta0, c->relres, c->active,
+                                     c->iters, 0, rtol, maxit, 1, c->ints + 1, c->ints + 4, c->stream));
+    int k = 0;
+    for (k = 1; k <= maxit; k++) {
+        if ((st = apply(c->bpcg_p, c->bpcg_q)) != DD_OK) return st;
+        DD_TIMED(DD_KCLASS_OTHER, bpcg_a(ncols, nb, x, c->bpcg_r, c->bpcg_p, c->bpcg_q, c->rho, c->active, c->ints + 4,
+                                         c->stream));
+        if ((st = bulk_eliminate_3d(c, ncols, colp, c->bpcg_r, c->bpcg_z, false, 0, 0, 0, nullptr, nullptr)) != DD_OK)
+            return st;
+        DD_CK(cudaMemsetAsync(c->ints + 1, 0, sizeof(int), c->stream));
+        DD_TIMED(DD_KCLASS_OTHER, bpcg_b(ncols, nb, c->bpcg_r, c->bpcg_z, c->bpcg_p, c->rho, c->eta0, c->relres,
+                                         c->active, c->iters, k, rtol, maxit, 0, c->ints + 1, c->ints + 4, c->stream));
+        DD_CK(cudaMemcpyAsync(c->h_ints, c->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
+        DD_CK(cudaStreamSynchronize(c->stream));
+        if (c->h_ints[1] == 0 || c->h_ints[4] != 0) break;
+    }
+    if (iters) DD_CK(cudaMemcpyAsync(iters, c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c->stream));
+    if (rel_res) DD_CK(cudaMemcpyAsync(rel_res, c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost, c->stream));
+    DD_CK(cudaMemcpyAsync(c->h_ints, c->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
+    DD_CK(cudaStreamSynchronize(c->stream));
+    if (c->h_ints[5]) return set_error(DD_EINVAL, "col_param entry out of range (clamped; outputs undefined)");
+    if (c->h_ints[4] == DD_ENOTSPD) return set_error(DD_ENOTSPD, "p.Ap <= 0 or r.Br < 0 in the bulk PCG");
+    std::vector<int> itv(ncols);
+    std::vector<double> rr(ncols);
+    DD_CK(cudaMemcpy(itv.data(), c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost));
+    DD_CK(cudaMemcpy(rr.data(), c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < ncols; i++)
+        if (itv[i] >= maxit && !(rr[i] <= rtol)) return set_error(DD_ENOCONV, "maxit reached");
+    return DD_OK;
 }
 
 }  // namespace dd

@@ -962,9 +962,9 @@ extern "C" dd_status dd_bulk_pcg_solve(dd_ctx* c, int ncols, const int* colp, co
                                        int maxit, int* iters, double* rel_res) {
     dd_status s = bulk_check(c, ncols, colp, b, x, rtol, maxit, 0);
     if (s != DD_OK || ncols == 0) return s;
-    if (c->dim != 2) return fail(DD_EUNSUPPORTED, "bulk PCG: 2D handles only");
     if (c->frac_mode != DD_FRAC_DENSE) return fail(DD_EUNSUPPORTED, "bulk PCG: dense fractional term only");
     CK(cudaSetDevice(c->device));
+    if (c->dim == 3) return bulk_pcg_3d(c, ncols, colp, b, x, rtol, maxit, iters, rel_res);
     const int n = c->n, ldf = c->Kpad;
     const long long nb = (long long)n * n + n;
     if (!c->bpcg_r) {

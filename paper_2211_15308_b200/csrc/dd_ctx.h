@@ -65,6 +65,7 @@ struct Face3 {
     // the layer-major copy [col][face][layer], face buffers [col][face], user-layout Γ vectors, σ
     double *b3X = nullptr, *b3T = nullptr, *b3L = nullptr, *b3Y = nullptr;
     double *b3G = nullptr, *b3W = nullptr, *b3W2 = nullptr, *b3g = nullptr, *b3xg = nullptr, *b3sig = nullptr;
+    double *b3Z = nullptr, *b3F = nullptr, *b3P = nullptr;   // bulk PCG: zero faces, γ F x_Γ, padded x_Γ
     double* F = nullptr;              // dense fractional term, rows round_up(NP,256) x NP row-major (DD_FX_FULL=1)
     double* Fp = nullptr;             // packed-symmetric F: upper 128 x 128 blocks in 16-column slabs (default)
     int* fblk = nullptr;              // (I, J) of each packed block
@@ -200,6 +201,8 @@ dd_status schur_3d(dd_ctx* c, int ncols, const int* colp, const double* xin, dou
 dd_status precond_3d(dd_ctx* c, int ncols, const int* colp, const double* rin, double* zout, bool user_layout);
 dd_status bulk_solve_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
                         int norm_kind, int* iters, double* rel_res);
+dd_status bulk_pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
+                      int* iters, double* rel_res);
 dd_status pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
                  int norm_kind);
 void destroy_3d(dd_ctx* c);

@@ -208,6 +208,8 @@ cudaError_t bulk3_combine(int n, int ldf, long long NP, int ncols, double* Y, co
                           cudaStream_t st);
 cudaError_t bulk3_out(int n, int ldf, long long NP, int ncols, const double* X, const double* xg, double* x, long long ldx,
                       cudaStream_t st);
+cudaError_t bulk3_apply(int n, int ldf, long long NP, int ncols, const double* x, long long ldx, const double* fx,
+                        const int* col_param, int n_param, const double* Kp, double h, double* out, cudaStream_t st);
 cudaError_t face_slab_pass_scaled(const double* in, double* out, int nslab, int n, int ldf, const double* S,
                                   const double* w, long long sW, int group, const double* colscale, cudaStream_t st);
 // packed-symmetric F stream (fx_sym.cu): upper 128 x 128 blocks, one read per block, two products

@@ -186,3 +186,60 @@ def test_bulk_solve_3d_medium(lib):
             assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(Bp[c])
     finally:
         S.close()
+
+
+@pytest.mark.parametrize("N", [6, 9])
+def test_bulk_pcg_3d_parity(lib, N):
+    """The paper's protocol in 3D (dd_bulk_pcg_solve on a 3D handle): PCG on the Kuhn-mesh bulk system
+    with the Eq.(5) preconditioner (exact leading block by fast diagonalisation, S_Γ^-1 by the RA with
+    the face systems solved by inner CG to 1e-13, reading A12) — iterations ±1 and the solution against
+    the oracle's bulk PCG with the same RA (sparse-direct face solves) and against the direct solve."""
+    from oracle import pcg as opcg
+    from oracle import problem as oprob
+    params = [(1.0, 1e2)]
+    lo, hi = rafit.interval_face(N)
+    ras = [rafit.fit_ra(K, g, lo, hi, 12) for K, g in params]
+    Bs = obulk.BulkSystem(3, N)
+    D = oprob.DenseProblem(3, N)
+    C = 2
+    Bp = np.random.default_rng(N + 3).uniform(-1, 1, (C, Bs.A.shape[0]))
+    S = lib.Solver(3, N, params, ras, max_cols=C)
+    try:
+        res = S.bulk_pcg_solve(torch.as_tensor(Bp, device="cuda"), [0] * C)
+        x = res.x.cpu().numpy()
+        K, g = params[0]; ra = ras[0]
+        P = lambda w: D.apply_P_ra(ra.c0, ra.poles, ra.residues, w)
+        for c in range(C):
+            bo = Bs.from_product(Bp[c])
+            xo, it, *_ = opcg.pcg(lambda v: Bs.apply(K, g, v), lambda v: Bs.dd_precond(K, P, v), bo)
+            assert abs(int(res.iters[c]) - it) <= 1, (c, res.iters[c], it)
+            assert np.linalg.norm(x[c] - Bs.to_product(xo)) <= 1e-8 * np.linalg.norm(xo)
+            xd = Bs.solve(K, g, bo)
+            assert np.linalg.norm(Bs.from_product(x[c]) - xd) <= 1e-8 * np.linalg.norm(xd)
+        assert np.all(res.rel_res <= 1e-10)
+    finally:
+        S.close()
+
+
+def test_bulk_pcg_3d_long_columns(lib):
+    """N = 65 (266 240 bulk unknowns per column, 3 columns): the bulk PCG's vector steps take the
+    many-CTAs-per-column path (deterministic per-CTA partial dots); its solution equals the
+    block-elimination bulk solve's to 1e-8 and it needs at most the interface PCG's iterations + 1."""
+    N = 65
+    params = [(1.0, 1e4)]
+    lo, hi = rafit.interval_face(N)
+    ras = [rafit.fit_ra(K, g, lo, hi, 16) for K, g in params]
+    n = N - 1
+    C = 3
+    Bp = np.random.default_rng(21).uniform(-1, 1, (C, n ** 3 + n * n))
+    S = lib.Solver(3, N, params, ras, max_cols=C)
+    try:
+        a = S.bulk_pcg_solve(torch.as_tensor(Bp, device="cuda"), [0] * C)
+        b = S.bulk_solve(torch.as_tensor(Bp, device="cuda"), [0] * C)
+        assert np.all(a.iters <= b.iters + 1) and np.all(a.iters >= b.iters - 4), (a.iters, b.iters)
+        xa, xb = a.x.cpu().numpy(), b.x.cpu().numpy()
+        assert np.max(np.linalg.norm(xa - xb, axis=1) / np.linalg.norm(xb, axis=1)) <= 1e-8
+        a2 = S.bulk_pcg_solve(torch.as_tensor(Bp, device="cuda"), [0] * C)
+        assert np.array_equal(a2.x.cpu().numpy(), xa)          # deterministic reductions
+    finally:
+        S.close()
