@@ -461,7 +461,12 @@ def run_bulk(args, cfg, world, rank):
     nb = n * n + n if cfg.dim == 2 else n ** 3 + n * n
     Bb = rng.uniform(-1.0, 1.0, (C, nb))
     colp = (np.arange(C) // cfg.rhs_per_param).astype(np.int32)
-    S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local)
+    frac = None
+    if args.frac_mode == "ra":
+        # Remark 1: the operator's fractional term evaluated by RA as well
+        lo, hi = rafit.interval_1d(cfg.N) if cfg.dim == 2 else rafit.interval_face(cfg.N)
+        frac = binding.Frac(mode="ra", fra=rafit.fit_power(-0.5, lo, hi, cfg.n_poles, 0.0))
+    S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=C, device=local, frac=frac)
     Bt = torch.as_tensor(Bb, device=f"cuda:{local}")
     X = torch.empty_like(Bt)
     cp = torch.as_tensor(colp, device=f"cuda:{local}")
@@ -501,7 +506,8 @@ def run_bulk(args, cfg, world, rank):
             "value": round(C / (ms / 1e3), 3), "unit": "solves/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name + ("_bulk" if args.mode == "bulk" else "_bulk_pcg"),
+            "config": {"workload": cfg.name + ("_bulk" if args.mode == "bulk" else "_bulk_pcg")
+                                   + ("_frac_ra" if args.frac_mode == "ra" else ""),
                        "bulk_unknowns_per_solve": nb, "solves_per_step": C,
                        "mean_pcg_iters": float(np.mean(r.iters)),
                        "l2": "inputs (4.3 GB of fields) exceed L2" if cfg.dim == 2 else "fields of 133 MB per 8 columns"},

@@ -193,9 +193,10 @@ dd_status dd_bulk_solve(dd_ctx* ctx, int ncols, const int* col_param, const doub
  * 𝒜 x = b (the discrete Eq.(2) on all free nodes, 𝒜 = K A_h + γ T^T F T) from x0 = 0,
  * preconditioned by the DD preconditioner 𝓑 of Eq.(5) with the leading block
  * exact (fast diagonalisation) and S_Γ^-1 realised by the handle's RA (Eq.(8)); stops when
- * sqrt(r·𝓑r) <= rtol · sqrt(r0·𝓑r0).  Same vector layout as dd_bulk_solve (2D and 3D handles);
- * the dense fractional term only (DD_EUNSUPPORTED in DD_FRAC_RA mode).  iters / rel_res: HOST
- * [ncols] or NULL.  Allocates 4 max_cols x (bulk size) vectors on first use.  Synchronous.
+ * sqrt(r·𝓑r) <= rtol · sqrt(r0·𝓑r0).  Same vector layout as dd_bulk_solve (2D and 3D handles).
+ * In DD_FRAC_RA mode the operator's fractional term is the RA-evaluated γ M r_F(L) M (Remark 1,
+ * operator and preconditioner both by RA).  iters / rel_res: HOST [ncols] or
+ * NULL.  Allocates 4 max_cols x (bulk size) vectors on first use.  Synchronous.
  */
 dd_status dd_bulk_pcg_solve(dd_ctx* ctx, int ncols, const int* col_param, const double* b, double* x,
                             double rtol, int maxit, int* iters, double* rel_res);

@@ -633,7 +633,17 @@ dd_status bulk_pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, do
         for (int col = 0; col < ncols; col++)
             DD_TIMED(DD_KCLASS_OTHER, bulk3_pad(n, ldf, NP, 1, in + (size_t)col * nb + (size_t)n * n * n,
                                                 f.b3P + (size_t)col * NP, c->stream));
-        if (f.Fp) {
+        if (c->frac_mode == DD_FRAC_RA) {
+            // Remark 1: γ F x_Γ ≈ γ M r_F(L) M x_Γ — the operator evaluated by RA too
+            const double hh12 = (double)(1.0L / ((long double)c->N * c->N * 12.0L));
+            DD_TIMED(DD_KCLASS_OTHER, gather_param(ncols, colp, c->n_param, c->gp, f.fs.gcol, c->stream));
+            DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_mass_axpy(f.n, f.ldf, f.NP, ncols, hh12, f.b3P, nullptr, nullptr,
+                                                          f.fs.V1, c->stream));
+            dd_status s = inner_apply(c, view_F(f, c), ncols, f.fs.V1, f.fs.V2, f.fs.W1, f.fs.W2);
+            if (s != DD_OK) return s;
+            DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_mass_axpy(f.n, f.ldf, f.NP, ncols, hh12, f.fs.V2, f.fs.gcol, f.b3Z,
+                                                          f.b3F, c->stream));
+        } else if (f.Fp) {
             DD_TIMED(DD_KCLASS_GEMM_SCHUR, fx_sym_apply(f.Fp, f.fblk, NP, f.b3P, f.b3F, f.b3Z, ncols, colp, c->n_param,
                                                         c->gp, f.fxD, f.fxT, c->num_sms, c->stream));
         } else {

@@ -962,9 +962,13 @@ extern "C" dd_status dd_bulk_pcg_solve(dd_ctx* c, int ncols, const int* colp, co
                                        int maxit, int* iters, double* rel_res) {
     dd_status s = bulk_check(c, ncols, colp, b, x, rtol, maxit, 0);
     if (s != DD_OK || ncols == 0) return s;
-    if (c->frac_mode != DD_FRAC_DENSE) return fail(DD_EUNSUPPORTED, "bulk PCG: dense fractional term only");
     CK(cudaSetDevice(c->device));
     if (c->dim == 3) return bulk_pcg_3d(c, ncols, colp, b, x, rtol, maxit, iters, rel_res);
+    if (c->frac_mode == DD_FRAC_RA && !c->ones) {
+        std::vector<double> one((size_t)c->n_param, 1.0);
+        CK(dalloc(c, &c->ones, (size_t)c->n_param));
+        CK(cudaMemcpy(c->ones, one.data(), sizeof(double) * c->n_param, cudaMemcpyHostToDevice));
+    }
     const int n = c->n, ldf = c->Kpad;
     const long long nb = (long long)n * n + n;
     if (!c->bpcg_r) {
@@ -975,8 +979,16 @@ extern "C" dd_status dd_bulk_pcg_solve(dd_ctx* c, int ncols, const int* colp, co
     CK(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)nb * ncols, c->stream));
     CK(cudaMemcpyAsync(c->bpcg_r, b, sizeof(double) * (size_t)nb * ncols, cudaMemcpyDeviceToDevice, c->stream));
     auto apply_A = [&](const double* in, double* out) -> dd_status {
-        // F xΓ through the dense F block of W (padded copy of xΓ first), then the stencil kernel
+        // F xΓ through the dense F block of W (padded copy of xΓ first), then the stencil kernel;
+        // RA mode (Remark 1): M r_F(L) M xΓ by the fractional pole sum instead (γ applied by the stencil)
         TIMED(DD_KCLASS_OTHER, launch_copy_cols(n, ncols, in + (size_t)n * n, (int)nb, c->bulk_g, ldf, c->stream));
+        if (c->frac_mode == DD_FRAC_RA) {
+            TIMED(DD_KCLASS_POLESUM, launch_frac_ra(ncols, colp, c->n_param, c->ones, c->geom, c->ftabs, c->bulk_g, ldf,
+                                                    c->bulk_w, ldf, 1.0 / (6.0 * c->N), c->stream, false));
+            TIMED(DD_KCLASS_OTHER, bulk_apply(n, ncols, in, nb, c->bulk_w, ldf, colp, c->n_param, c->Kp, c->gp, out,
+                                              c->stream));
+            return DD_OK;
+        }
         GemmArgs ga{};
         ga.M = n; ga.N = ncols; ga.K = ldf;
         ga.A = c->W + ldf; ga.lda = c->lda;

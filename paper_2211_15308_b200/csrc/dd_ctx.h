@@ -117,6 +117,7 @@ struct dd_ctx {
     // operator data (2D)
     double* W = nullptr;      // 2D: Mpad x lda row-major: [S_dst | F | G] (RA mode: [S_dst | G]), blocks Kpad wide
     int g_off = 0;            // 2D: column offset of G = S_dst diag(s) S_dst (the unit Schur complement) in W
+    double* ones = nullptr;   // [n_param] 1.0 (RA-mode bulk PCG: the fractional pole sum without γ)
     int schur_mode = 1;       // 2D Schur apply: 0 factored (K1 + K2), 1 assembled (one GEMM with [F | G]),
                               // 2 grouped (one GEMM with H_p = K_p G + γ_p F per parameter set)
     double* H = nullptr;      // grouped: n_param blocks of Mpad x Kpad (row-major, row stride Kpad)

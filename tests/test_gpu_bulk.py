@@ -243,3 +243,38 @@ def test_bulk_pcg_3d_long_columns(lib):
         assert np.array_equal(a2.x.cpu().numpy(), xa)          # deterministic reductions
     finally:
         S.close()
+
+
+@pytest.mark.parametrize("dim,N", [(2, 24), (3, 8)])
+def test_bulk_pcg_ra_operator(lib, dim, N):
+    """Remark 1's experiment (Fig. 4 left in 3D): bulk PCG with the Eq.(5)
+    preconditioner where BOTH the operator's fractional term and S_Γ^-1 are evaluated by RA
+    (dd_frac mode "ra") — against the oracle's direct solve of the bulk system whose dense block
+    is the RA-evaluated F = M r_F(L) M (oracle DenseProblem(frac_ra)), and iterations ±1 against
+    the oracle's bulk PCG with the same two RAs."""
+    from oracle import pcg as opcg
+    from oracle import problem as oprob
+    params = [(1.0, 1e2)]
+    lo, hi = rafit.interval_1d(N) if dim == 2 else rafit.interval_face(N)
+    ras = [rafit.fit_ra(K, g, lo, hi, 12) for K, g in params]
+    fr = rafit.fit_power(-0.5, lo, hi, 16, 0.0)
+    Bs = obulk.BulkSystem(dim, N)
+    D = oprob.DenseProblem(dim, N, frac_ra=(fr.c0, fr.poles, fr.residues))
+    Bs.F = D.F                                                 # the bulk system with the RA-evaluated block
+    C = 2
+    Bp = np.random.default_rng(N + 5).uniform(-1, 1, (C, Bs.A.shape[0]))
+    S = lib.Solver(dim, N, params, ras, max_cols=C, frac=lib.Frac(mode="ra", fra=fr))
+    try:
+        res = S.bulk_pcg_solve(torch.as_tensor(Bp, device="cuda"), [0] * C)
+        x = res.x.cpu().numpy()
+        K, g = params[0]; ra = ras[0]
+        P = lambda w: D.apply_P_ra(ra.c0, ra.poles, ra.residues, w)
+        for c in range(C):
+            bo = Bs.from_product(Bp[c])
+            xd = Bs.solve(K, g, bo)
+            assert np.linalg.norm(Bs.from_product(x[c]) - xd) <= 1e-8 * np.linalg.norm(xd)
+            xo, it, *_ = opcg.pcg(lambda v: Bs.apply(K, g, v), lambda v: Bs.dd_precond(K, P, v), bo)
+            assert abs(int(res.iters[c]) - it) <= 1, (c, res.iters[c], it)
+        assert np.all(res.rel_res <= 1e-10)
+    finally:
+        S.close()
