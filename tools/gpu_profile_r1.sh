@@ -18,3 +18,7 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --
 timeout 900 python bench.py --config cfg4_3d_N128 --frac-mode ra --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/p_bench_cfg4_ra.json 2>&1; echo cfg4ra=$?
 timeout 900 python bench.py --mode bulk-pcg --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/p_bench_cfg2_bulkpcg.json 2>&1; echo bpcg=$?
 timeout 600 python bench.py --t 0.25 --shifted --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/p_bench_cfg2_t025.json 2>&1; echo t025=$?
+# NEXT-1 in 3D: bulk solves, the bulk PCG, and Remark 1's RA-operator bulk PCG
+timeout 900 python bench.py --config cfg4_3d_N128 --mode bulk --steps 3 --warmup 2 > gpurun_out/p_bench_cfg4_bulk.json 2>&1; echo cfg4bulk=$?
+timeout 900 python bench.py --config cfg4_3d_N128 --mode bulk-pcg --steps 2 --warmup 1 > gpurun_out/p_bench_cfg4_bulkpcg.json 2>&1; echo cfg4bpcg=$?
+timeout 900 python bench.py --config cfg4_3d_N128 --mode bulk-pcg --frac-mode ra --steps 2 --warmup 1 > gpurun_out/p_bench_cfg4_bulkpcg_ra.json 2>&1; echo cfg4bpcgra=$?
