@@ -111,13 +111,14 @@ __global__ void k_b3_g(int n, int ldf, long long NP, int ncols, const double* __
         g[idx] = G[c * NP + f] + W[c * NP + f];
     }
 }
-// x_Γ (user face layout) -> padded faces
-__global__ void k_b3_pad(int n, int ldf, long long NP, int ncols, const double* __restrict__ xg, double* __restrict__ P) {
+// x_Γ (user face layout, column stride lds) -> padded faces
+__global__ void k_b3_pad(int n, int ldf, long long NP, int ncols, const double* __restrict__ xg, long long lds,
+                         double* __restrict__ P) {
     const long long n2 = (long long)n * n;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n2 * ncols;
          idx += (long long)gridDim.x * blockDim.x) {
         const long long c = idx / n2, jk = idx % n2;
-        P[c * NP + (jk / n) * ldf + jk % n] = xg[idx];
+        P[c * NP + (jk / n) * ldf + jk % n] = xg[c * lds + jk];
     }
 }
 // padded x_0 faces and x_Γ -> product layout
@@ -213,8 +214,9 @@ cudaError_t bulk3_g(int n, int ldf, long long NP, int ncols, const double* G, co
     k_b3_g<<<grid_of((long long)n * n * ncols), 256, 0, st>>>(n, ldf, NP, ncols, G, W, g);
     return cudaGetLastError();
 }
-cudaError_t bulk3_pad(int n, int ldf, long long NP, int ncols, const double* xg, double* P, cudaStream_t st) {
-    k_b3_pad<<<grid_of((long long)n * n * ncols), 256, 0, st>>>(n, ldf, NP, ncols, xg, P);
+cudaError_t bulk3_pad(int n, int ldf, long long NP, int ncols, const double* xg, long long lds, double* P,
+                      cudaStream_t st) {
+    k_b3_pad<<<grid_of((long long)n * n * ncols), 256, 0, st>>>(n, ldf, NP, ncols, xg, lds, P);
     return cudaGetLastError();
 }
 cudaError_t bulk3_combine(int n, int ldf, long long NP, int ncols, double* Y, const double* XG, const double* s1,

@@ -599,7 +599,7 @@ static dd_status bulk_eliminate_3d(dd_ctx* c, int ncols, const int* colp, const 
         if (ps != DD_OK) return ps;
     }
     // x̂_0 = Ŷ / (K h) + s1 ⊗ (Q⊗Q x_Γ) / Σ;  x_0 = Q⊗Q⊗Q x̂_0
-    DD_TIMED(DD_KCLASS_OTHER, bulk3_pad(n, ldf, NP, ncols, f.b3xg, f.b3W2, c->stream));
+    DD_TIMED(DD_KCLASS_OTHER, bulk3_pad(n, ldf, NP, ncols, f.b3xg, f.n2, f.b3W2, c->stream));
     DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.b3W2, f.b3W, ncols, n, ldf, f.S, c->stream));
     DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.b3W, f.b3W2, ncols, n, ldf, f.S, c->stream));
     DD_TIMED(DD_KCLASS_OTHER, bulk3_combine(n, ldf, NP, ncols, f.b3Y, f.b3W2, s1, f.b3sig, colp, c->n_param, c->Kp,
@@ -630,9 +630,7 @@ dd_status bulk_pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, do
     DD_CK(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)nb * ncols, c->stream));
     DD_CK(cudaMemcpyAsync(c->bpcg_r, b, sizeof(double) * (size_t)nb * ncols, cudaMemcpyDeviceToDevice, c->stream));
     auto apply = [&](const double* in, double* out) -> dd_status {
-        for (int col = 0; col < ncols; col++)
-            DD_TIMED(DD_KCLASS_OTHER, bulk3_pad(n, ldf, NP, 1, in + (size_t)col * nb + (size_t)n * n * n,
-                                                f.b3P + (size_t)col * NP, c->stream));
+        DD_TIMED(DD_KCLASS_OTHER, bulk3_pad(n, ldf, NP, ncols, in + (size_t)n * n * n, nb, f.b3P, c->stream));
         if (c->frac_mode == DD_FRAC_RA) {
             // Remark 1: γ F x_Γ ≈ γ M r_F(L) M x_Γ — the operator evaluated by RA too
             const double hh12 = (double)(1.0L / ((long double)c->N * c->N * 12.0L));

@@ -202,7 +202,8 @@ cudaError_t bulk3_in(int n, int ldf, long long NP, int ncols, const double* b, l
                      cudaStream_t st);
 cudaError_t bulk3_layer1(int n, long long NP, int ncols, const double* Y, const double* s1, double* w, cudaStream_t st);
 cudaError_t bulk3_g(int n, int ldf, long long NP, int ncols, const double* G, const double* W, double* g, cudaStream_t st);
-cudaError_t bulk3_pad(int n, int ldf, long long NP, int ncols, const double* xg, double* P, cudaStream_t st);
+cudaError_t bulk3_pad(int n, int ldf, long long NP, int ncols, const double* xg, long long lds, double* P,
+                      cudaStream_t st);
 cudaError_t bulk3_combine(int n, int ldf, long long NP, int ncols, double* Y, const double* XG, const double* s1,
                           const double* sig, const int* col_param, int n_param, const double* Kp, double h,
                           cudaStream_t st);
