@@ -30,9 +30,14 @@
  * Streams: apply calls are asynchronous on the handle's stream; dd_pcg_solve synchronises
  * that stream once at the end to fill its host outputs.
  * Thread safety: a handle is not thread-safe; distinct handles are independent.
- * Errors: return codes only; nothing crosses the ABI as an exception.  On DD_EINVAL no
- * output is written.  dd_last_error() returns a thread-local description of the last
- * failure.
+ * Errors: return codes only; nothing crosses the ABI as an exception.  On DD_EINVAL found
+ * by the host-side argument checks no output is written.  Two checks run on the device
+ * instead (no host synchronisation in the asynchronous calls): an out-of-range col_param
+ * entry is CLAMPED to [0, n_param) by the kernels — dd_apply_schur / dd_apply_precond then
+ * return DD_OK with the clamped-parameter outputs (they cannot see the device flag), while
+ * dd_pcg_solve / dd_pcg_solve_host / dd_bulk_* read the flag back and return DD_EINVAL
+ * AFTER x has been written (its contents are then undefined).  dd_last_error() returns a
+ * thread-local description of the last failure.
  */
 #ifndef DD_API_H
 #define DD_API_H
@@ -133,7 +138,8 @@ int dd_interface_size(const dd_ctx* ctx);
  * dd_apply_schur — y = S x per column:
  *   y_c = K_c (A^ii - A^i0 (A^00)^-1 A^0i) x_c + γ_c F x_c,  (K_c, γ_c) = set col_param[c].
  * The interior solve (A^00)^-1 is exact (fast diagonalisation; "exactly").
- *   col_param  DEVICE int[ncols], each in [0, n_param)
+ *   col_param  DEVICE int[ncols], each in [0, n_param) (out-of-range entries are clamped on
+ *              the device and not reported by this asynchronous call; see "Errors" above)
  *   x, y       DEVICE n_Γ x ncols column-major; x and y must not overlap.
  * 0 <= ncols <= max_cols (ncols = 0 is a no-op).
  */
@@ -155,8 +161,10 @@ dd_status dd_apply_precond(dd_ctx* ctx, int ncols, const int* col_param, const d
  *   rel_res    HOST double[ncols]: final η / η0
  *   hist       HOST double[maxit+1] or NULL: η history of column 0 (η0 first); entries
  *              after column 0 converged are left untouched
+ *   maxit      >= 0; with hist != NULL also maxit + 1 <= 4096 (else DD_EINVAL)
  * Returns DD_ENOCONV if any column reached maxit (outputs valid), DD_ENOTSPD on p.Sp <= 0
- * or r.Pr < 0 (outputs are the iterate at that point).
+ * or r.Pr < 0 (outputs are the iterate at that point), DD_EINVAL after the solve when a
+ * col_param entry was out of range (x written, contents undefined).
  */
 dd_status dd_pcg_solve(dd_ctx* ctx, int ncols, const int* col_param, const double* b, double* x,
                        double rtol, int maxit, int norm_kind, int* iters, double* rel_res,
@@ -213,11 +221,12 @@ dd_status dd_inner_iterations(const dd_ctx* ctx, int* iters);
  * SURVEY §8(a) rows a-2, a-3).  Both give the same operator up to rounding order:
  *   DD_SCHUR_FACTORED (0): per apply, the interior solve by fast diagonalisation,
  *        T' = (K_c s) ∘ (S_dst X) then Y = [S_dst | F] [T' ; γ X]   (6 n^2 flops per column);
- *   DD_SCHUR_ASSEMBLED (1, default): the parameter-independent interior solve is applied once at
+ *   DD_SCHUR_ASSEMBLED (1; the default in DD_FRAC_RA mode, or when the grouped operators exceed
+ *        16 GiB): the parameter-independent interior solve is applied once at
  *        setup to the identity, G = S_dst diag(s) S_dst = S_unit (n x n, beside F in the handle),
  *        and each apply is one GEMM  Y = [F | G] [γ X ; K X]          (4 n^2 flops per column);
  *        in DD_FRAC_RA mode Y = G (K X) + γ M r_F(L) M X.
- *   DD_SCHUR_GROUPED (2, default for dense F when the operators fit in 16 GiB): the full Schur
+ *   DD_SCHUR_GROUPED (2; THE DEFAULT for dense F when the operators fit in 16 GiB): the full Schur
  *        matrix of each parameter set, H_p = K_p G + γ_p F (n_param x n^2 doubles, formed when
  *        the mode is selected), and each apply is one grouped GEMM Y[:, c] = H_{p(c)} X[:, c]
  *        (2 n^2 flops per column) over 32-column tiles.  Needs every 32-column tile of a call

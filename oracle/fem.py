@@ -184,3 +184,20 @@ def trace_pair_1d(N: int):
         m_d[e] += Me[0, 0]; m_d[e + 1] += Me[1, 1]; m_o[e] += Me[0, 1]
     # drop the Dirichlet end nodes 0 and N
     return a_d[1:N], a_o[1:N - 1], m_d[1:N], m_o[1:N - 1]
+
+
+def trace_pair_face(N: int):
+    """The 3D trace pair (A_Γ, M_Γ) of `trace_pair(3, N)`, assembled directly on the trace mesh
+    of the face Γ = {x=0} — the facets of the Kuhn tetrahedra on x = 0, which are the triangles
+    of the (y, z) square split along (0,0)->(1,1) — without walking the 6 N^3 bulk cells, so the
+    oracle reaches the config-4 face (N = 128).  Same P1 element integrals (`_p1_element`), same
+    Dirichlet ∂Γ and j-major ordering; equality with `trace_pair(3, N)` is pinned in the tests.
+    Returns sparse CSR (A_Γ, M_Γ)."""
+    if N < 2:
+        raise ValueError("N >= 2")
+    coords, cells = square_mesh(N)          # node (j, k) at (j h, k h) in the face's (y, z) plane
+    K, M = _assemble(coords.shape[0], cells, coords)
+    idx = np.rint(coords * N).astype(np.int64)
+    free = np.all((idx > 0) & (idx < N), axis=1)
+    ids = np.nonzero(free)[0]               # ascending id = j (N+1) + k: j-major
+    return K[ids][:, ids].tocsr(), M[ids][:, ids].tocsr()

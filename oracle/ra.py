@@ -45,13 +45,13 @@ def ra_rel_error(c0, poles, residues, K, gamma, xs, t: float = -0.5, sigma: floa
     return float(np.max(np.abs(r_eval(xs, c0, poles, residues) / f_target(xs, K, gamma, t, sigma) - 1.0)))
 
 
-def cancellation_factor(c0, poles, residues, K, gamma, xs) -> float:
-    """κ_c = max_x (|c0| + Σ|c_k/(x-p_k)|) / f(x)   (reading A11)."""
+def cancellation_factor(c0, poles, residues, K, gamma, xs, t: float = -0.5, sigma: float = 0.0) -> float:
+    """κ_c = max_x (|c0| + Σ|c_k/(x-p_k)|) / f(x)   (reading A11; f of `f_target`)."""
     xs = np.asarray(xs, dtype=np.float64)
     acc = np.full_like(xs, abs(c0))
     for p, c in zip(poles, residues):
         acc += np.abs(c / (xs - p))
-    return float(np.max(acc / f_target(xs, K, gamma)))
+    return float(np.max(acc / f_target(xs, K, gamma, t, sigma)))
 
 
 def _to_band(T: np.ndarray) -> np.ndarray:
@@ -67,14 +67,21 @@ def apply_ra(A: np.ndarray, M: np.ndarray, c0, poles, residues, B: np.ndarray) -
     """Z = c0 M^-1 B + Σ_k c_k (A - p_k M)^-1 B, summed in the fixed order k = 0 (mass), 1..m.
 
     1D Γ (tridiagonal pair): LAPACK banded Cholesky (scipy.linalg.solveh_banded);
-    2D Γ (face pair): sparse direct LU (scipy.sparse.linalg.splu).  B is (n_Γ, C).
+    2D Γ (face pair, dense or scipy.sparse): sparse direct LU (scipy.sparse.linalg.splu).
+    B is (n_Γ, C).
     """
     B = np.asarray(B, dtype=np.float64)
-    tridiag = np.count_nonzero(np.triu(A, 2)) == 0 and np.count_nonzero(np.triu(M, 2)) == 0
-    def solve(T, X):
-        if tridiag:
-            return sla.solveh_banded(_to_band(T), X, lower=False)
-        return spla.splu(sp.csc_matrix(T)).solve(X)
+    if sp.issparse(A) or sp.issparse(M):
+        # sparse pair (the config-4 face, n_Γ = 16129): sparse direct LU per shifted matrix
+        A, M = sp.csc_matrix(A), sp.csc_matrix(M)
+        def solve(T, X):
+            return spla.splu(sp.csc_matrix(T)).solve(X)
+    else:
+        tridiag = np.count_nonzero(np.triu(A, 2)) == 0 and np.count_nonzero(np.triu(M, 2)) == 0
+        def solve(T, X):
+            if tridiag:
+                return sla.solveh_banded(_to_band(T), X, lower=False)
+            return spla.splu(sp.csc_matrix(T)).solve(X)
     Z = np.zeros_like(B)
     if c0 != 0.0:
         Z = Z + c0 * solve(M, B)

@@ -148,18 +148,23 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
     // --- pole systems: [M term if c0 != 0] + [poles with non-zero residue];  (a, b, w): a A + b M
     struct Sys { double a, b, w, cost; };
     std::vector<Sys> sys;
+    // cost: the inner CG is preconditioned by the sine-diagonal part of each system (κ <= 3 for
+    // every shift, ~20 iterations whatever the pole) and batched over (system, column) pairs, so a
+    // rank's share of the pole sum costs in proportion to the NUMBER of its systems — not √κ of
+    // the unpreconditioned system (which would put 1 system on most ranks and 5-6 on the rest)
     if (c0[0] != 0.0) sys.push_back({0.0, 1.0, c0[0], 1.0});
     for (int k = 0; k < c->n_poles; k++) {
         const double p = poles[k], r = residues[k];
         if (r == 0.0) continue;
-        sys.push_back({1.0, -p, r, std::sqrt((f.lam_max - p) / (f.lam_min - p))});
+        sys.push_back({1.0, -p, r, 1.0});
     }
     f.nsys_total = (int)sys.size();
     f.rank = dist ? dist->rank : 0;
     f.world = dist ? dist->world : 1;
     std::vector<int> mine;
     if (f.world > 1 && dist->mode == DD_SHARD_POLES) {
-        // balanced by predicted inner-CG cost (longest-processing-time greedy)
+        // balanced by predicted inner-CG cost (longest-processing-time greedy):
+        // equal costs give contiguous-by-order round robin, e.g. 21 systems on 8 ranks -> 3,3,3,3,3,2,2,2
         std::vector<int> order(sys.size());
         std::iota(order.begin(), order.end(), 0);
         std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return sys[x].cost > sys[y].cost; });
@@ -521,7 +526,7 @@ dd_status pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double*
     st.NP = f.NP; st.ncols = ncols;
     st.x = f.x; st.r = f.r; st.p = f.p; st.q = f.q; st.z = f.z;
     st.rho = c->rho; st.eta0 = c->eta0; st.relres = c->relres; st.active = c->active; st.iters = c->iters;
-    st.hist = c->hist; st.rtol = rtol; st.norm_kind = norm_kind; st.status = c->ints + 4;
+    st.hist = c->hist_on ? c->hist : nullptr; st.rtol = rtol; st.norm_kind = norm_kind; st.status = c->ints + 4;
     DD_TIMED(DD_KCLASS_OTHER, pcg3_start(st, c->stream));
     int k = 0;
     for (k = 1; k <= maxit; k++) {

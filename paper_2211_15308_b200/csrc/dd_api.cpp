@@ -245,6 +245,11 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
         for (int k = 0; k < n; k++)
             for (int j = 0; j < n; j++) Bh[(size_t)j * c->Kpad + k] = (double)(d[k] * (long double)Wh[(size_t)k * c->lda + j]);
         double* Bd = nullptr; double* ws = nullptr; int* cnt = nullptr;
+        // scratch freed on every exit path (the CK early returns included)
+        struct Scratch {
+            void** p[3];
+            ~Scratch() { for (void** q : p) if (*q) cudaFree(*q); }
+        } guard{{reinterpret_cast<void**>(&Bd), reinterpret_cast<void**>(&ws), reinterpret_cast<void**>(&cnt)}};
         CK(cudaMalloc(&Bd, Bh.size() * sizeof(double)));
         CK(cudaMemcpyAsync(Bd, Bh.data(), Bh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         const int sk = gemm_pick_splitk(n, n, c->Kpad, c->num_sms);
@@ -260,9 +265,6 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
         ga.splitk = sk; ga.ws = ws; ga.counters = cnt; ga.epi = EPI_STORE; ga.num_sms = c->num_sms;
         CK(launch_dgemm(ga, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        if (ws) cudaFree(ws);
-        cudaFree(cnt);
-        cudaFree(Bd);
         return DD_OK;
     };
     if (dense_f) {
@@ -616,7 +618,9 @@ static PcgState make_state(dd_ctx* c, int ncols, const int* colp, double* x, dou
     s.r = c->r; s.p = c->p; s.q = c->q;
     s.rho = c->rho; s.eta0 = c->eta0; s.relres = c->relres;
     s.active = c->active; s.iters = c->iters;
-    s.hist = c->hist;
+    // column-0 history only when the caller asked for it: the device buffer holds hist_cap
+    // entries and the kernels write one per iteration up to maxit
+    s.hist = c->hist_on ? c->hist : nullptr;
     s.kiter = c->ints + 0; s.n_active = c->ints + 1; s.n_active_next = c->ints + 2;
     s.done_ctas = c->ints + 3; s.status = c->ints + 4;
     s.rtol = rtol; s.maxit = maxit; s.norm_kind = norm_kind;
@@ -719,6 +723,7 @@ static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const dou
         CK(cudaEventCreate(&c->solve_ev[1]));
     }
     CK(cudaEventRecord(c->solve_ev[0], c->stream));
+    c->hist_on = hist != nullptr;        // maxit + 1 <= hist_cap checked above
     // counters, live-tile list and the parameter checks in one launch
     TIMED(DD_KCLASS_OTHER, launch_solve_prep(ncols, colp, c->n_param, c->ints, 8, c->ntl,
                                              c->dim == 2 ? 2 * (c->cols_pad / GEMM_BN_GROUPED) + 4 : 0,

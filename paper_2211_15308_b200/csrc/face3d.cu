@@ -343,6 +343,9 @@ __global__ void __cluster_dims__(NCL, 1, 1) k_inner_update_cl(InnerArgs a, int* 
     const size_t off = (size_t)pq * a.NP;
     const double* dg = a.dg + (size_t)s * a.NP;
     const double* idg = a.idg + (size_t)s * a.NP;
+    // ρ read once, before the first cluster barrier: rank 0 overwrites it at the end, after the
+    // other CTAs have passed both reductions (no read may follow that store)
+    const double rho_old = a.rho[pq];
     double d = 0.0;
     for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
         const double pv = a.p[off + i];
@@ -356,7 +359,7 @@ __global__ void __cluster_dims__(NCL, 1, 1) k_inner_update_cl(InnerArgs a, int* 
         if (rank == 0 && threadIdx.x == 0) a.active[pq] = 0;
         return;
     }
-    const double alpha = a.rho[pq] / d;
+    const double alpha = rho_old / d;
     double rho = 0.0;
     for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
         a.x[off + i] = fma(alpha, a.p[off + i], a.x[off + i]);
@@ -369,7 +372,7 @@ __global__ void __cluster_dims__(NCL, 1, 1) k_inner_update_cl(InnerArgs a, int* 
         if (rank == 0 && threadIdx.x == 0) a.active[pq] = 0;
         return;
     }
-    const double beta = rho / a.rho[pq];
+    const double beta = rho / rho_old;
     for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x)
         a.p[off + i] = fma(beta, a.p[off + i], a.r[off + i] * idg[i]);
     if (rank == 0 && threadIdx.x == 0) {
@@ -460,6 +463,7 @@ __global__ void k_inner_step2(InnerArgs a, int* n_active) {
     const int pq = blockIdx.x;
     if (!a.active[pq]) return;
     const size_t off = (size_t)pq * a.NP;
+    const double rho_old = a.rho[pq];            // before block_sum's barriers: thread 0 overwrites it below
     double s = 0.0;
     for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) s = fma(a.r[off + i], a.z[off + i], s);
     s = block_sum(s, red);
@@ -467,7 +471,7 @@ __global__ void k_inner_step2(InnerArgs a, int* n_active) {
         if (threadIdx.x == 0) a.active[pq] = 0;
         return;
     }
-    const double beta = s / a.rho[pq];
+    const double beta = s / rho_old;
     for (long long i = threadIdx.x; i < a.NP; i += blockDim.x) a.p[off + i] = fma(beta, a.p[off + i], a.z[off + i]);
     if (threadIdx.x == 0) {
         a.rho[pq] = s;
@@ -568,6 +572,7 @@ __global__ void k3_pcg_beta(Pcg3 s, int k, int maxit, int* n_active) {
     const int c = blockIdx.x;
     if (!s.active[c]) return;
     const size_t off = (size_t)c * s.NP;
+    const double rho_old = s.rho[c];             // before block_sum's barriers: thread 0 overwrites it below
     double rz = 0.0, zz = 0.0;
     for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) {
         const double zi = s.z[off + i];
@@ -588,7 +593,7 @@ __global__ void k3_pcg_beta(Pcg3 s, int k, int maxit, int* n_active) {
         if (threadIdx.x == 0) s.active[c] = 0;
         return;
     }
-    const double beta = rz / s.rho[c];
+    const double beta = rz / rho_old;
     for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) s.p[off + i] = fma(beta, s.p[off + i], s.z[off + i]);
     if (threadIdx.x == 0) {
         s.rho[c] = rz;

@@ -28,6 +28,38 @@ def column_shard(n_param: int, rhs_per_param: int, rank: int, world: int):
     return np.asarray(cols, dtype=np.int64), np.asarray(cp, dtype=np.int32)
 
 
+def column_blocks(n_param: int, rhs_per_param: int, bn: int = 32):
+    """The batch cut into blocks of <= bn consecutive columns of ONE parameter set (columns
+    parameter-major as in `inputs.batch`): [(param, first global column, width), ...].  bn = 32 is
+    the grouped Schur GEMM's column tile (one H_p per tile)."""
+    out = []
+    for p in range(n_param):
+        for j0 in range(0, rhs_per_param, bn):
+            out.append((p, p * rhs_per_param + j0, min(bn, rhs_per_param - j0)))
+    return out
+
+
+def block_shard(n_param: int, rhs_per_param: int, rank: int, world: int, iters, bn: int = 32):
+    """Strong-scaling split of a FIXED batch of independent solves over `world` ranks (SURVEY
+    §8(e); config 5: the 512 solves of the Appendix sweep).  Units are whole
+    bn-column single-parameter blocks (`column_blocks`), so every rank's grouped-GEMM tiles keep
+    one parameter set each; blocks go to ranks by LPT (`pole_partition`) on their predicted work
+    iters[param] x width — the PCG iteration count of the block's parameter set (a pilot solve;
+    counts range 3..16 over the config-5 grid), the GEMM and pole-sum work per live column being
+    the same for every block.  Deterministic: every rank computes the same partition.
+    Returns (global column indices, col_param) of `rank`, blocks in ascending column order."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    blocks = column_blocks(n_param, rhs_per_param, bn)
+    parts = pole_partition([float(iters[p]) * w for p, _, w in blocks], world)
+    cols, cp = [], []
+    for b in parts[rank]:
+        p, c0, w = blocks[b]
+        cols.extend(range(c0, c0 + w))
+        cp.extend([p] * w)
+    return np.asarray(cols, dtype=np.int64), np.asarray(cp, dtype=np.int32)
+
+
 def pole_partition(costs, world: int):
     """Split systems (weights = predicted solve cost) over `world` ranks, balancing total cost
     (longest-processing-time greedy, deterministic ties by index).  Returns a list of sorted
@@ -45,9 +77,18 @@ def pole_partition(costs, world: int):
 
 
 def shifted_cost(lam_min: float, lam_max: float, pole: float) -> float:
-    """Predicted CG iterations for (A - pM) with spectrum [λmin, λmax] of the pair: ∝ sqrt(κ),
-    κ = (λmax - p)/(λmin - p)."""
+    """Predicted iterations of PLAIN CG on (A - pM) with spectrum [λmin, λmax] of the pair: ∝ sqrt(κ),
+    κ = (λmax - p)/(λmin - p).  Not the library's cost model: its inner CG is preconditioned by the
+    sine-diagonal part (κ <= 3 for every shift), see `inner_cost`."""
     return math.sqrt((lam_max - pole) / (lam_min - pole))
+
+
+def inner_cost(lam_min: float, lam_max: float, pole: float) -> float:
+    """Cost model of one shifted face system in libdd (dd3d.cpp): the sine-preconditioned inner CG
+    takes about the same ~20 iterations for every shift (171 iterations over 21
+    systems), batched over (system, column) pairs — a unit cost per system, so the pole split
+    balances the COUNT of systems per rank."""
+    return 1.0
 
 
 def max_over_ranks(value: float, device=None) -> float:

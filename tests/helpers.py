@@ -18,9 +18,19 @@ def rel_l2_cols(a, b):
     return float(np.max(num / den))
 
 
+def kappa_c(r) -> float:
+    """The cancellation factor κ_c of reading A11 computed by the ORACLE (oracle.ra.cancellation_factor)
+    for an RA fit r (its c0/poles/residues, target f(K, γ, t, σ) and spectral interval), on the same
+    2e4-point geometric grid of [λ_min, λ_max] the fit reports on."""
+    from oracle import ra as ora
+    xs = np.geomspace(r.lam_min, r.lam_max, 20000)
+    return ora.cancellation_factor(r.c0, r.poles, r.residues, r.K, r.gamma, xs, t=getattr(r, "t", -0.5),
+                                   sigma=getattr(r, "sigma", 0.0))
+
+
 def precond_tol(ras):
-    # max(1e-10, 1e-15 κ_c) relative ℓ2 (κ_c = cancellation factor, reading A11)
-    return max(1e-10, 1e-15 * max(r.cancel for r in ras))
+    # SURVEY §8(c): max(1e-10, 1e-15 κ_c) relative ℓ2 (κ_c = cancellation factor, reading A11, from the oracle)
+    return max(1e-10, 1e-15 * max(kappa_c(r) for r in ras))
 
 
 def check_precond(z_gpu, z_banded, z_eigen, ras):

@@ -1,0 +1,224 @@
+"""GPU parity, round 2: the norm_kind = 1 stopping rule (reading A1), the DD_ENOTSPD breakdown
+(reading A19), maxit beyond the history buffer, the config-4 full-size solve against the stored
+oracle run, and the pole-split partial sums (row a-6) against the oracle's P_RA.  Needs a B200.
+
+Tolerances (north star): applies 1e-10 relative ℓ2 (preconditioner max(1e-10, 1e-15 κ_c), plus
+the A12 inner-CG allowance in 3D), solutions 1e-8, iteration counts ±1.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import fit_all, kappa_c, rel_l2_cols
+from oracle import pcg as opcg
+from oracle import problem as oprob
+from paper_2211_15308_b200 import inputs, rafit
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cfg4_oracle.npz")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2211_15308_b200 import binding
+    binding.load()
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    return binding
+
+
+class _RA:
+    def __init__(self, c0, poles, residues):
+        self.c0, self.poles, self.residues = float(c0), np.asarray(poles, float), np.asarray(residues, float)
+
+
+def _fit3(N, params, m):
+    lo, hi = rafit.interval_face(N)
+    return [rafit.fit_ra(K, g, lo, hi, m) for K, g in params]
+
+
+# ------------------------------------------------------------------------- norm_kind = 1 (reading A1)
+@pytest.mark.parametrize("N,C", [(33, 3), (200, 37), (1024, 64)], ids=["small-kernel", "graph", "grouped-1024"])
+def test_norm_kind1_parity_2d(lib, N, C):
+    """η = ||P r||_2 on every 2D path (persistent small-n kernel, WHILE graph, grouped GEMM at
+    the config-2 size): iteration counts ±1, x within 1e-8, column-0 history within 1e-8."""
+    params = [(1.0, 1e2), (1e-4, 1e6)]
+    ras = fit_all(N, params, 14)
+    colp = (np.arange(C) * len(params)) // C
+    B = np.random.default_rng(N + 1).uniform(-1, 1, (C, N - 1))
+    D = oprob.DenseProblem(2, N) if N <= 200 else oprob.ModeProblem2D(N)
+    S = lib.Solver(2, N, params, ras, max_cols=C, device=0)
+    try:
+        res = S.pcg_solve(torch.as_tensor(B, device="cuda"), colp, norm_kind=1, want_hist=True)
+        x = res.x.cpu().numpy()
+    finally:
+        S.close()
+    for c in sorted({0, C // 2, C - 1}):
+        K, g = params[colp[c]]; ra = ras[colp[c]]
+        xo, it, rel, hist, conv = opcg.pcg(lambda v: D.apply_S(K, g, v),
+                                           lambda v: D.apply_P_ra(ra.c0, ra.poles, ra.residues, v), B[c], norm_kind=1)
+        assert conv and abs(int(res.iters[c]) - it) <= 1, (c, res.iters[c], it)
+        assert np.linalg.norm(x[c] - xo) <= 1e-8 * np.linalg.norm(xo)
+        assert res.rel_res[c] <= 1e-10
+        if c == 0:
+            k = min(len(hist), len(res.hist))
+            assert np.allclose(res.hist[:k], hist[:k], rtol=1e-8, atol=0)
+
+
+def test_norm_kind1_parity_3d(lib):
+    N, params = 8, [(1.0, 1e4)]
+    ras = _fit3(N, params, 10)
+    D = oprob.DenseProblem(3, N)
+    B = np.random.default_rng(9).uniform(-1, 1, (3, (N - 1) ** 2))
+    S = lib.Solver(3, N, params, ras, max_cols=3, device=0)
+    try:
+        res = S.pcg_solve(torch.as_tensor(B, device="cuda"), [0, 0, 0], norm_kind=1, want_hist=True)
+        x = res.x.cpu().numpy()
+    finally:
+        S.close()
+    K, g = params[0]; ra = ras[0]
+    for c in range(3):
+        xo, it, rel, hist, conv = opcg.pcg(lambda v: D.apply_S(K, g, v),
+                                           lambda v: D.apply_P_ra(ra.c0, ra.poles, ra.residues, v), B[c], norm_kind=1)
+        assert conv and abs(int(res.iters[c]) - it) <= 1
+        assert np.linalg.norm(x[c] - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+# ------------------------------------------------------------------------- DD_ENOTSPD (reading A19)
+@pytest.mark.parametrize("dim,N", [(2, 33), (2, 200), (3, 8)], ids=["2d-small-kernel", "2d-graph", "3d"])
+def test_enotspd_on_indefinite_preconditioner(lib, dim, N):
+    """A 'fit' with r(λ) = -1 < 0 on the whole spectrum (c0 = -1, the one pole switched off by a
+    zero residue): P = -M^-1 is negative definite, r.Pr < 0 at the first step.  The oracle raises
+    NotSPD; the library returns DD_ENOTSPD for every column."""
+    params = [(1.0, 1e2)]
+    ras = [_RA(-1.0, [-1.0], [0.0])]
+    n_g = (N - 1) ** (dim - 1)
+    B = np.random.default_rng(5).uniform(-1, 1, (2, n_g))
+    D = oprob.DenseProblem(dim, N)
+    with pytest.raises(opcg.NotSPD):
+        opcg.pcg(lambda v: D.apply_S(1.0, 1e2, v), lambda v: D.apply_P_ra(-1.0, [-1.0], [0.0], v), B[0])
+    S = lib.Solver(dim, N, params, ras, max_cols=2, device=0)
+    try:
+        res = S.pcg_solve(torch.as_tensor(B, device="cuda"), [0, 0])
+        assert res.status == lib.DD_ENOTSPD
+        assert np.all(res.iters == 0)
+    finally:
+        S.close()
+
+
+# ------------------------------------------------------------------------- maxit beyond the history buffer
+@pytest.mark.parametrize("dim,N,maxit", [(2, 128, 4200), (3, 4, 4110)])
+def test_maxit_beyond_history_buffer(lib, dim, N, maxit):
+    """rtol = 0 and maxit > 4096 with no history requested: the solve runs maxit iterations
+    (DD_ENOCONV, or DD_OK if η reaches exactly 0) without writing past the device history
+    buffer, and the handle still solves correctly afterwards; with a history, maxit + 1 > 4096
+    is DD_EINVAL."""
+    params = [(1.0, 1e2)]
+    ras = fit_all(N, params, 8) if dim == 2 else _fit3(N, params, 8)
+    n_g = (N - 1) ** (dim - 1)
+    B = np.random.default_rng(2).uniform(-1, 1, (2, n_g))
+    S = lib.Solver(dim, N, params, ras, max_cols=2, device=0)
+    try:
+        Bt = torch.as_tensor(B, device="cuda")
+        ref = S.pcg_solve(Bt, [0, 0])
+        r = S.pcg_solve(Bt, [0, 0], rtol=0.0, maxit=maxit)
+        assert r.status in (lib.DD_ENOCONV, lib.DD_OK)
+        assert r.iters.max() <= maxit
+        again = S.pcg_solve(Bt, [0, 0])
+        assert np.array_equal(again.x.cpu().numpy(), ref.x.cpu().numpy())
+        assert np.array_equal(again.iters, ref.iters)
+        with pytest.raises(lib.DDError):
+            S.pcg_solve(Bt, [0, 0], maxit=4096, want_hist=True)
+    finally:
+        S.close()
+
+
+# ------------------------------------------------------------------------- row a-6 vs the oracle
+def test_pole_split_partials_sum_to_oracle(lib):
+    """Row a-6: the rank partials of the pole split (each rank's share of Eq.(8),
+    no communicator: the allreduce's inputs) summed in rank order equal the ORACLE's P_RA
+    (sparse-direct parity form) within the 3D preconditioner bar — for world 2, 3 and 4."""
+    N = 16; n = N - 1
+    params = [(1.0, 1e4)]
+    ras = _fit3(N, params, 10)
+    ra = ras[0]
+    D = oprob.DenseProblem(3, N)
+    B = np.random.default_rng(8).uniform(-1, 1, (2, n * n))
+    zb = D.apply_P_ra(ra.c0, ra.poles, ra.residues, B.T).T
+    ze = D.apply_P_ra_eigen(ra.c0, ra.poles, ra.residues, B.T).T
+    kc = kappa_c(ra)
+    tol = max(1e-10, 1e-15 * kc) + 20e-13 * kc
+    Bt = torch.as_tensor(B, device="cuda")
+    for world in (2, 3, 4):
+        acc = np.zeros_like(B)
+        for rank in range(world):
+            S = lib.Solver(3, N, params, ras, max_cols=2, device=0, dist=(rank, world, 1, None))
+            try:
+                acc += S.apply_precond(Bt, [0, 0]).cpu().numpy()
+            finally:
+                S.close()
+        assert rel_l2_cols(acc, ze) <= tol, world
+        assert rel_l2_cols(acc, zb) <= tol + rel_l2_cols(zb, ze), world
+
+
+# ------------------------------------------------------------------------- config 4 at full size
+@pytest.fixture(scope="module")
+def cfg4(lib):
+    if not os.path.exists(GOLDEN):
+        pytest.skip("tests/golden/cfg4_oracle.npz not generated (tests/golden/make_cfg4_oracle.py)")
+    g = np.load(GOLDEN)
+    N = int(g["N"]); n = N - 1
+    ra = _RA(g["c0"], g["poles"], g["residues"])
+    B, colp = inputs.batch(n * n, 1, 8)
+    return g, N, ra, B, colp
+
+
+def test_cfg4_full_size_parity(lib, cfg4):
+    """BASELINE.json config 4 (3D, N = 128, n_Γ = 16129, K = 1, μ^-1 = 1e4, 20 poles, 8 seeded RHS;
+    PAPER.md:237-240, 258-272) element by element against the stored oracle run (dense gevp F,
+    mode-tier S_unit, sparse-direct P_RA, plain PCG): S x <= 1e-10, P r <= max(1e-10, 1e-15 κ_c) +
+    the A12 inner-CG allowance, iterations ±1, x <= 1e-8 on all 8 columns."""
+    g, N, ra, B, colp = cfg4
+    K, gam = float(g["K"]), float(g["gamma"])
+    kc = float(g["kappa_c"])
+    S = lib.Solver(3, N, [(K, gam)], [ra], max_cols=8, device=0)
+    try:
+        Bt = torch.as_tensor(B, device="cuda")
+        y = S.apply_schur(Bt, colp).cpu().numpy()
+        assert rel_l2_cols(y, g["y"]) <= 1e-10
+        z = S.apply_precond(Bt, colp).cpu().numpy()
+        tol = max(1e-10, 1e-15 * kc) + 20e-13 * kc
+        assert rel_l2_cols(z, g["z_eig"]) <= tol
+        assert rel_l2_cols(z, g["z_par"]) <= tol + rel_l2_cols(g["z_par"], g["z_eig"])
+        res = S.pcg_solve(Bt, colp, rtol=1e-10, maxit=500, want_hist=True)
+        x = res.x.cpu().numpy()
+        assert np.all(np.abs(res.iters - g["iters"]) <= 1), (res.iters, g["iters"])
+        assert rel_l2_cols(x, g["x"]) <= 1e-8
+        assert np.all(res.rel_res <= 1e-10)
+        k = min(len(res.hist), len(g["hist"]))
+        assert np.allclose(res.hist[:k], g["hist"][:k], rtol=1e-7, atol=0)
+        r1 = S.pcg_solve(Bt, colp, rtol=1e-10, maxit=500, norm_kind=1)
+        assert np.all(np.abs(r1.iters - g["iters_norm1"]) <= 1)
+    finally:
+        S.close()
+
+
+def test_cfg4_full_size_pole_split_partials(lib, cfg4):
+    """Row a-6 at the config-4 size: the partial pole sums of a 4-way split (the NCCL allreduce's
+    inputs, balanced by the inner-CG cost model) add up to the oracle's P_RA."""
+    g, N, ra, B, colp = cfg4
+    K, gam = float(g["K"]), float(g["gamma"])
+    kc = float(g["kappa_c"])
+    Bt = torch.as_tensor(B[:2], device="cuda")
+    acc = np.zeros_like(B[:2])
+    world = 4
+    for rank in range(world):
+        S = lib.Solver(3, N, [(K, gam)], [ra], max_cols=2, device=0, dist=(rank, world, 1, None))
+        try:
+            acc += S.apply_precond(Bt, colp[:2]).cpu().numpy()
+        finally:
+            S.close()
+    tol = max(1e-10, 1e-15 * kc) + 20e-13 * kc
+    assert rel_l2_cols(acc, g["z_eig"][:2]) <= tol
