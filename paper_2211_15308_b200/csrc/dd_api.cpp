@@ -122,6 +122,47 @@ static SysTables build_sys_tables(long double d, long double e, const PoleGeom& 
     return t;
 }
 
+// Tables of the merged-interior pole sum (pcg_polesum.cu, block_polesum_v2) for one system
+// (d, e) with weight w, FULL geometry with 16-row chunks (15 interior rows + 1 separator) and T
+// chunks: the first row tf of T_int^-1 (T_int = tridiag(e, d, e) of size 15; by persymmetry its
+// last row is tf reversed, and u = T_int^-1 e_1 = tf), w e tf, and the uniform PCR multipliers of
+// the separator system  δ g_τ + ε (g_τ-1 + g_τ+1) = rs_τ,  δ = d - 2 e^2 tf_0,  ε = -e^2 tf_14,
+// extended antisymmetrically to a circulant of period 2T (so every position has the same
+// multiplier): α_j = a_j / b_j, b_j+1 = b_j - 2 a_j α_j, a_j+1 = -a_j α_j (j = 0..log2(2T)-1),
+// 1/D = 1/(b + 2a) after the last step.  W += w T_int^-1 (the merged interior operator).
+// Long double throughout; rounded once to fp64.
+static void build_v2_record(long double d, long double e, long double w, int T, double* rec, long double* Wacc) {
+    constexpr int m = V2_L - 1;
+    long double inv[m][m];
+    long double bp[m];
+    for (int i = 0; i < m; i++) bp[i] = (i == 0) ? d : d - e * e / bp[i - 1];
+    for (int col = 0; col < m; col++) {                 // T_int^-1 e_col by Thomas
+        long double f[m];                               // forward: f_i = (δ_i,col - e f_i-1) / bp_i
+        for (int i = 0; i < m; i++) f[i] = (((i == col) ? 1.0L : 0.0L) - (i > 0 ? e * f[i - 1] : 0.0L)) / bp[i];
+        long double x[m];
+        for (int i = m - 1; i >= 0; i--) x[i] = f[i] - (i < m - 1 ? (e / bp[i]) * x[i + 1] : 0.0L);
+        for (int i = 0; i < m; i++) inv[i][col] = x[i];
+    }
+    for (int i = 0; i < V2_REC; i++) rec[i] = 0.0;
+    for (int i = 0; i < m; i++) {
+        rec[i] = (double)inv[0][i];
+        rec[16 + i] = (double)(w * e * inv[0][i]);
+        for (int j = 0; j < m; j++) Wacc[i * 16 + j] += w * inv[i][j];
+    }
+    rec[V2_E] = (double)e;
+    rec[V2_WK] = (double)w;
+    long double b = d - 2.0L * e * e * inv[0][0], a = -e * e * inv[m - 1][0];
+    int steps = 0;
+    while ((1 << steps) < 2 * T) steps++;
+    for (int j = 0; j < steps; j++) {
+        const long double al = a / b;
+        rec[V2_AL + j] = (double)al;
+        const long double nb = b - 2.0L * a * al, na = -a * al;
+        b = nb; a = na;
+    }
+    rec[V2_DINV] = (double)(1.0L / (b + 2.0L * a));
+}
+
 // Pole-sum tables of n_sets parameter sets (RA c0 M^-1 + Σ_k c_k (A_Γ - p_k M_Γ)^-1 each):
 // systems [M term if c0 != 0] + [poles with non-zero residue], in long double (build_sys_tables).
 static dd_status build_pole_tabs(dd_ctx* c, const PoleGeom& g, int n_sets, int n_poles, const double* c0,
@@ -136,6 +177,11 @@ static dd_status build_pole_tabs(dd_ctx* c, const PoleGeom& g, int n_sets, int n
         cpr(invb.size(), 0.0), uf(invb.size(), 0.0), up(invb.size(), 0.0),
         pa((size_t)n_sets * max_sys * JT, 0.0), pb(pa.size(), 0.0),
         pinvb((size_t)n_sets * max_sys * g.T, 0.0);
+    // merged-interior pole sum (v2): FULL geometry with 16-row chunks, T = 32..256 separators
+    static const bool v1_only = std::getenv("DD_POLESUM_V1") && std::getenv("DD_POLESUM_V1")[0] == '1';
+    const bool v2 = !v1_only && polesum_v2_supported(g, max_sys);
+    const size_t v2_stride = (size_t)V2_WSZ + (size_t)V2_REC * max_sys;
+    std::vector<double> v2tab(v2 ? (size_t)n_sets * v2_stride : 0, 0.0);
     for (int pi = 0; pi < n_sets; pi++) {
         std::vector<std::tuple<double, long double, long double>> sys;   // (weight, d, e)
         if (c0[pi] != 0.0) sys.emplace_back(c0[pi], 4.0L * h / 6.0L, h / 6.0L);
@@ -146,6 +192,14 @@ static dd_status build_pole_tabs(dd_ctx* c, const PoleGeom& g, int n_sets, int n
             sys.emplace_back(ck, 2.0L / h - P * 4.0L * h / 6.0L, -1.0L / h - P * h / 6.0L);
         }
         nsys[pi] = (int)sys.size();
+        if (v2) {
+            std::vector<long double> Wacc(V2_WSZ, 0.0L);
+            double* blk = &v2tab[(size_t)pi * v2_stride];
+            for (size_t s = 0; s < sys.size(); s++)
+                build_v2_record(std::get<1>(sys[s]), std::get<2>(sys[s]), (long double)std::get<0>(sys[s]), g.T,
+                                blk + V2_WSZ + s * V2_REC, Wacc.data());
+            for (int i = 0; i < V2_WSZ; i++) blk[i] = (double)Wacc[i];
+        }
         for (size_t s = 0; s < sys.size(); s++) {
             const size_t ps = (size_t)pi * max_sys + s;
             w[ps] = std::get<0>(sys[s]);
@@ -179,6 +233,9 @@ static dd_status build_pole_tabs(dd_ctx* c, const PoleGeom& g, int n_sets, int n
         (st = up_d(cpr, &T.cpr)) || (st = up_d(uf, &T.ufull)) || (st = up_d(up, &T.upart)) || (st = up_d(pa, &T.pa)) ||
         (st = up_d(pb, &T.pb)) || (st = up_d(pinvb, &T.pinvb)))
         return st;
+    T.v2 = nullptr;
+    T.v2_stride = (int)v2_stride;
+    if (v2 && (st = up_d(v2tab, &T.v2))) return st;
     // the host vectors must outlive the async copies
     CK(cudaStreamSynchronize(c->stream));
     return DD_OK;
@@ -801,8 +858,12 @@ static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const dou
         CK(cudaMemcpy(t, c->dbg, sizeof(t), cudaMemcpyDeviceToHost));
         fprintf(stderr, "[dd phase cycles] load+pq %lld  update %lld  polesum %lld  dots+p %lld  finish %lld\n",
                 t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
-        fprintf(stderr, "[dd polesum cycles] stage-wait %lld  sys0: fwd %lld bwd %lld pcr %lld  rest-of-systems %lld  combine %lld\n",
-                t[6] - t[2], t[7] - t[6], t[8] - t[7], t[9] - t[8], t[10] - t[9], t[3] - t[10]);
+        if (c->tabs.v2)
+            fprintf(stderr, "[dd polesum v2 cycles] stage-wait %lld  phase A %lld  phase B %lld  phase C %lld  tail %lld\n",
+                    t[6] - t[2], t[7] - t[6], t[8] - t[7], t[9] - t[8], t[3] - t[9]);
+        else
+            fprintf(stderr, "[dd polesum cycles] stage-wait %lld  sys0: fwd %lld bwd %lld pcr %lld  rest-of-systems %lld  combine %lld\n",
+                    t[6] - t[2], t[7] - t[6], t[8] - t[7], t[9] - t[8], t[10] - t[9], t[3] - t[10]);
     }
     if (c->last_graph) c->launches += c->graph_iter_launches * kdone;
     if (hist) {

@@ -83,7 +83,16 @@ struct PoleTabs {
     const double* pa;           // [n_param][max_sys][J][T] PCR multipliers (left)
     const double* pb;           // [n_param][max_sys][J][T] PCR multipliers (right)
     const double* pinvb;        // [n_param][max_sys][T]    final 1/b
+    // merged-interior pole sum (block_polesum_v2; NULL when the geometry does not qualify):
+    // per parameter set a block of v2_stride doubles = W (16 x 16) + max_sys records of V2_REC
+    const double* v2;
+    int v2_stride;
 };
+// v2 pole-sum table layout (dd_api.cpp build_v2_record; pcg_polesum.cu block_polesum_v2)
+constexpr int V2_L = 16;        // rows per chunk: 15 interior + 1 separator
+constexpr int V2_WSZ = 256;     // merged interior operator W = Σ_k w_k T_int,k^-1, 16 x 16 (row/col 15 zero)
+constexpr int V2_REC = 48;      // per system: [0,16) tf, [16,32) w e tf, e, w, 1/D, -, [36,48) PCR α_j
+constexpr int V2_E = 32, V2_WK = 33, V2_DINV = 34, V2_AL = 36;
 
 // PCG state for a batch of columns (device).
 struct PcgState {
@@ -117,6 +126,7 @@ bool pole_geom_supported(const PoleGeom& g);
 int polesum_groups(const PoleGeom& g);
 int polesum_warps(const PoleGeom& g);
 size_t polesum_smem(const PoleGeom& g, int max_sys);
+bool polesum_v2_supported(const PoleGeom& g, int max_sys);
 cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b,
                             int ldb, cudaStream_t st);
 cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st, bool pdl = false);

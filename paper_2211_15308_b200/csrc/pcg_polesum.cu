@@ -84,9 +84,19 @@ __device__ __forceinline__ double ldg_early(const double* p) {
 }
 
 // Asynchronously stage this parameter set's interior tables (4 contiguous blocks of nsys x LL
-// doubles) into scratch with cp.async (LDGSTS); block_polesum waits for them.  Called at kernel
-// entry so the copies overlap the vector passes.
+// doubles; v2: the parameter set's W + records block) into scratch with cp.async (LDGSTS);
+// block_polesum waits for them.  Called at kernel entry so the copies overlap the vector passes.
 __device__ __forceinline__ void stage_tables(const PoleTabs& t, const PoleGeom& g, int param, double* scratch) {
+    if (t.v2) {
+        const double* src = t.v2 + (size_t)param * t.v2_stride;
+        const int cnt = (V2_WSZ + V2_REC * t.nsys[param]) / 2;          // 16-byte pieces
+        for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(scratch + 2 * idx));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 2 * idx));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        return;
+    }
     const int LL = g.LL;
     const int cnt = t.nsys[param] * LL;
     const size_t tstride = (size_t)t.max_sys * LL;
@@ -408,9 +418,165 @@ __device__ void block_polesum_full(const PoleTabs& t, int param, const double* R
     __syncthreads();
 }
 
-template <int LMAX, int G, int NG>
+// Merged-interior pole sum (FULL geometry, 16-row chunks, T = 32 G chunks, NT threads = Q
+// sub-threads per chunk).  Same operator as block_polesum_full, reorganised so that no thread runs
+// a per-system dependent chain or waits on a per-system barrier:
+//   chunk interior of system k:  x_int = T_k^-1 r_int - e_k (g_k,τ-1 u_k + g_k,τ J u_k),  u_k = T_k^-1 e_1
+//   Σ_k w_k x_int = W r_int - Σ_k w_k e_k (g_k,τ-1 u_k + g_k,τ J u_k),   W = Σ_k w_k T_k^-1 (host, long double)
+//   separators: δ_k g_τ + ε_k (g_τ-1 + g_τ+1) = r_sep,τ - e_k (last(T_k^-1 r_int,τ) + first(T_k^-1 r_int,τ+1))
+// Phase A (chunk-parallel): W r_int for the thread's rows and, for its share of the systems, the two
+//   end rows of T_k^-1 r_int (dot products with tf_k = first row of T_k^-1; last row = tf_k reversed);
+// Phase B (one warp per system): the T - 1 separator unknowns by parallel cyclic reduction on the
+//   antisymmetric period-2T extension (g_0 = g_T = 0 by symmetry), whose multipliers are the same at
+//   every position — log2(2T) steps with two scalars per step from the table, exchanges through the
+//   system's own shared-memory rows and __syncwarp only;
+// Phase C (chunk-parallel): the corrections Σ_k w_k e_k (...) and z_sep = Σ_k w_k g_k,τ.
+// Three block barriers per pole sum.  scratch: [tables | hl (max_sys x (T+1)) | yf (same)].
+template <int T, int NT>
+__device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, double* Z, double* scratch,
+                                 long long* dbg = nullptr) {
+    constexpr int Q = NT / T;                    // sub-threads per chunk
+    constexpr int RPT = V2_L / Q;                // output rows per thread
+    constexpr int S = T / 32;                    // separators per lane in phase B
+    constexpr int TP = T + 1;                    // row stride of hl / yf
+    constexpr int NW = NT / 32;
+    constexpr int JS = T == 32 ? 6 : (T == 64 ? 7 : (T == 128 ? 8 : 9));   // log2(2T)
+    static_assert(Q >= 1 && V2_L % Q == 0 && T % 32 == 0, "v2 geometry");
+    const double* tab = scratch;
+    const int nsys = t.nsys[param];
+    double* hl = scratch + t.v2_stride;
+    double* yf = hl + (size_t)t.max_sys * TP;
+    const int tid = threadIdx.x, tau = tid % T, q = tid / T;
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    if (dbg && threadIdx.x == 0) dbg[6] = clock64();
+    // ---- phase A
+    double r[V2_L];
+#pragma unroll
+    for (int i = 0; i < V2_L; i++) r[i] = R[i * (T + 1) + tau];
+    double acc[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; u++) {
+        const int i = q + Q * u;
+        double a = 0.0;
+        if (i < V2_L - 1) {
+            const double2* wr = reinterpret_cast<const double2*>(tab + i * 16);
+#pragma unroll
+            for (int j2 = 0; j2 < 8; j2++) {
+                const double2 wv = wr[j2];
+                a = fma(wv.x, r[2 * j2], a);
+                if (2 * j2 + 1 < V2_L - 1) a = fma(wv.y, r[2 * j2 + 1], a);
+            }
+        }
+        acc[u] = a;
+    }
+    for (int k = q; k < nsys; k += Q) {
+        const double* rec = tab + V2_WSZ + k * V2_REC;
+        const double2* tf2 = reinterpret_cast<const double2*>(rec);
+        double f0 = 0.0, l0 = 0.0, f1 = 0.0, l1 = 0.0;        // two chains each (even / odd terms)
+#pragma unroll
+        for (int j2 = 0; j2 < 8; j2++) {
+            const double2 tv = tf2[j2];
+            const int j = 2 * j2;
+            f0 = fma(tv.x, r[j], f0);
+            l0 = fma(tv.x, r[V2_L - 2 - j], l0);
+            if (j + 1 < V2_L - 1) {
+                f1 = fma(tv.y, r[j + 1], f1);
+                l1 = fma(tv.y, r[V2_L - 3 - j], l1);
+            }
+        }
+        hl[k * TP + tau] = fma(-rec[V2_E], l0 + l1, r[V2_L - 1]);   // r_sep - e last(T^-1 r_int)
+        yf[k * TP + tau] = f0 + f1;                                 // first(T^-1 r_int)
+    }
+    __syncthreads();
+    if (dbg && threadIdx.x == 0) dbg[7] = clock64();
+    // ---- phase B: separators of system k by one warp.  The warp keeps the antisymmetric
+    // period-2T extension explicitly in a halo buffer hb[σ + T], σ in [-T, 2T]: every value v_σ is
+    // stored with its mirrors -v at -σ and 2T - σ (v_0 = v_2T = 0 are written once), so the PCR
+    // reads σ ± s with no index arithmetic; read, __syncwarp, write, __syncwarp per step.
+    {
+        const int warp = tid >> 5, lane = tid & 31;
+        constexpr int NWB = T >= 256 ? (NW < 4 ? NW : 4) : (NW < 8 ? NW : 8);
+        if (warp < NWB) {
+            double* hb = yf + (size_t)t.max_sys * TP + (size_t)warp * (3 * T + 1);
+            if (lane == 0) { hb[T] = 0.0; hb[3 * T] = 0.0; }      // v_0 and v_2T (read by σ = T at s = T)
+            for (int k = warp; k < nsys; k += NWB) {
+                const double* rec = tab + V2_WSZ + k * V2_REC;
+                const double e = rec[V2_E];
+                double* A = hl + k * TP;
+                const double* B = yf + k * TP;
+                double rs[S];
+#pragma unroll
+                for (int sl = 0; sl < S; sl++) {
+                    const int sg = 32 * sl + lane + 1;         // separator σ = τ + 1 in 1..T (σ = T: boundary)
+                    rs[sl] = sg < T ? fma(-e, B[sg], A[sg - 1]) : 0.0;
+                }
+#pragma unroll
+                for (int sl = 0; sl < S; sl++) {
+                    const int sg = 32 * sl + lane + 1;
+                    hb[T + sg] = rs[sl]; hb[T - sg] = -rs[sl]; hb[3 * T - sg] = -rs[sl];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < JS; j++) {
+                    const int st = 1 << j;
+                    const double al = rec[V2_AL + j];
+#pragma unroll
+                    for (int sl = 0; sl < S; sl++) {
+                        const int sg = 32 * sl + lane + 1;
+                        rs[sl] = fma(-al, hb[T + sg - st] + hb[T + sg + st], rs[sl]);   // σ = T stays 0
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int sl = 0; sl < S; sl++) {
+                        const int sg = 32 * sl + lane + 1;
+                        hb[T + sg] = rs[sl]; hb[T - sg] = -rs[sl]; hb[3 * T - sg] = -rs[sl];
+                    }
+                    __syncwarp();
+                }
+                const double dinv = rec[V2_DINV];
+#pragma unroll
+                for (int sl = 0; sl < S; sl++) A[32 * sl + lane + 1] = rs[sl] * dinv;   // g at σ (σ = T: 0)
+                if (lane == 0) A[0] = 0.0;
+            }
+        }
+    }
+    __syncthreads();
+    if (dbg && threadIdx.x == 0) dbg[8] = clock64();
+    // ---- phase C: corrections and separator rows
+    double acc2[RPT];                            // second chain (odd systems)
+#pragma unroll
+    for (int u = 0; u < RPT; u++) acc2[u] = 0.0;
+    for (int k0 = 0; k0 < nsys; k0 += 2) {
+#pragma unroll
+        for (int kk = 0; kk < 2; kk++) {
+            const int k = k0 + kk;
+            if (k < nsys) {
+                const double* rec = tab + V2_WSZ + k * V2_REC;
+                const double gl = hl[k * TP + tau], gr = hl[k * TP + tau + 1];    // g_k,τ-1 and g_k,τ
+                double* a = kk ? acc2 : acc;
+#pragma unroll
+                for (int u = 0; u < RPT; u++) {
+                    const int i = q + Q * u;
+                    if (i < V2_L - 1) a[u] = fma(-gl, rec[16 + i], fma(-gr, rec[16 + V2_L - 2 - i], a[u]));
+                    else a[u] = fma(rec[V2_WK], gr, a[u]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; u++) Z[(q + Q * u) * (T + 1) + tau] = acc[u] + acc2[u];
+    __syncthreads();
+    if (dbg && threadIdx.x == 0) dbg[9] = dbg[10] = clock64();
+}
+
+template <int LMAX, int G, int NG, int V = 0>
 __device__ __forceinline__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, const double* R,
                                               double* Z, double* scratch, long long* dbg = nullptr) {
+    if constexpr (V == 1) {                      // t.v2 set: FULL geometry with 16-row chunks
+        block_polesum_v2<32 * G, 32 * G * NG>(t, param, R, Z, scratch, dbg);
+        return;
+    } else {
     if (g.LL == LMAX && g.n + 1 == g.T * g.LL) {
         if constexpr (LMAX >= 2) {
             block_polesum_full<LMAX, G, NG>(t, param, R, Z, scratch, dbg);
@@ -419,6 +585,7 @@ __device__ __forceinline__ void block_polesum(const PoleTabs& t, const PoleGeom&
         block_polesum_impl<LMAX, G, NG, true>(t, g, param, R, Z, scratch, dbg);
     }
     else block_polesum_impl<LMAX, G, NG, false>(t, g, param, R, Z, scratch, dbg);
+    }
 }
 
 // Deterministic block reduction of two values (fixed tree).
@@ -451,7 +618,7 @@ __device__ __forceinline__ Smem carve(double* sm, const PoleGeom& g) {
 }
 
 // ---------------------------------------------------------------------------- kernels
-template <int LMAX, int G, int NG>
+template <int LMAX, int G, int NG, int V>
 __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_precond(int ncols, const int* __restrict__ col_param, PoleGeom g,
                                                          PoleTabs t, const double* __restrict__ r, int ldr,
                                                          double* __restrict__ z, int ldz) {
@@ -466,7 +633,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     pdl_wait_prior();
     for (int i = threadIdx.x; i < npad; i += blockDim.x) S.R[tpos(i, g)] = i < g.n ? r[(size_t)c * ldr + i] : 0.0;
     __syncthreads();
-    block_polesum<LMAX, G, NG>(t, g, param, S.R, S.Z, S.scratch);
+    block_polesum<LMAX, G, NG, V>(t, g, param, S.R, S.Z, S.scratch);
     for (int i = threadIdx.x; i < g.n; i += blockDim.x) z[(size_t)c * ldz + i] = S.Z[tpos(i, g)];
 }
 
@@ -474,7 +641,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
 //   u_c = γ_c M_Γ r_F(L) M_Γ x_c,   r_F(L) = fc0 M_Γ^-1 + Σ_k fc_k (A_Γ - fp_k M_Γ)^-1 ≈ L^t,
 // i.e. the pole sum of block_polesum on the F tables (one parameter set) between two products
 // with the 1D P1 mass M_Γ = (h/6) tridiag(1, 4, 1) (Dirichlet ends).
-template <int LMAX, int G, int NG>
+template <int LMAX, int G, int NG, int V>
 __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_frac_ra(int ncols, const int* __restrict__ col_param,
                                                          int n_param, const double* __restrict__ gp, PoleGeom g,
                                                          PoleTabs t, const double* __restrict__ x, int ldx,
@@ -494,7 +661,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_f
         S.R[tpos(i, g)] = v;
     }
     __syncthreads();
-    block_polesum<LMAX, G, NG>(t, g, 0, S.R, S.Z, S.scratch);
+    block_polesum<LMAX, G, NG, V>(t, g, 0, S.R, S.Z, S.scratch);
     int p = col_param[c];
     p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
     const double gam = gp[p] * h6;
@@ -533,24 +700,27 @@ __device__ __forceinline__ void publish_live_tiles(const PcgState& s, int na) {
     if (lane == 0) s.ntl[0] = total;
 }
 
-__device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_active, bool was_active) {
-    // grid-wide bookkeeping: count active columns; last CTA publishes and sets the graph condition
-    __shared__ int s_last;
+__device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_active, bool was_active, bool flagged) {
+    // grid-wide bookkeeping: count active columns; last CTA publishes and sets the graph condition.
+    // One 64-bit arrival per CTA on the adjacent counters (n_active_next, done_ctas): low word +=
+    // still-active, high word += 1 — the last arriver reads the total from the returned value.  Only a
+    // CTA that also changed a live-tile counter or the status flag fences before arriving (release);
+    // the last arriver fences after (acquire) before reading those.
+    __shared__ int s_last, s_na;
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (still_active) atomicAdd(s.n_active_next, 1);
-        if (was_active && !still_active && s.ntl) atomicSub(&s.ntl_cnt[blockIdx.x / s.ntl_bn], 1);
-        // arrival with acquire-release semantics at GPU scope: this CTA's counter updates (and the
-        // status flag) are ordered before its arrival; the last arriver sees every other CTA's
-        int prev;
-        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(s.done_ctas) : "memory");
-        s_last = prev == (int)gridDim.x - 1;
+        const bool froze = was_active && !still_active && s.ntl;
+        if (froze) atomicSub(&s.ntl_cnt[blockIdx.x / s.ntl_bn], 1);
+        if (froze || flagged) __threadfence();
+        const unsigned long long old = atomicAdd(reinterpret_cast<unsigned long long*>(s.n_active_next),
+                                                 (1ull << 32) | (still_active ? 1ull : 0ull));
+        s_last = (int)(old >> 32) == (int)gridDim.x - 1;
+        s_na = (int)(old & 0xffffffffull) + (still_active ? 1 : 0);
+        if (s_last) __threadfence();
     }
     __syncthreads();
     if (!s_last || threadIdx.x >= 32) return;
-    int na = 0;
-    if (threadIdx.x == 0) na = atomicAdd(s.n_active_next, 0);
-    na = __shfl_sync(0xffffffffu, na, 0);
+    const int na = s_na;
     publish_live_tiles(s, na);
     if (threadIdx.x == 0) {
         const int k = *s.kiter + 1;
@@ -560,12 +730,12 @@ __device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_a
         *s.done_ctas = 0;
         if (s.cond_handle) {
             cudaGraphSetConditional((cudaGraphConditionalHandle)s.cond_handle,
-                                    (na > 0 && k < s.maxit && *s.status == 0) ? 1u : 0u);
+                                    (na > 0 && k < s.maxit && *(volatile int*)s.status == 0) ? 1u : 0u);
         }
     }
 }
 
-template <int LMAX, int G, int NG>
+template <int LMAX, int G, int NG, int V>
 __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_pcg_init(PcgState s, PoleGeom g, PoleTabs t,
                                                           const double* __restrict__ b, int ldb) {
     extern __shared__ __align__(16) double sm[];
@@ -585,7 +755,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
         if (i < n) { s.r[off + i] = v; s.x[(size_t)c * s.ldx + i] = 0.0; }
     }
     __syncthreads();
-    block_polesum<LMAX, G, NG>(t, g, param, S.R, S.Z, S.scratch);
+    block_polesum<LMAX, G, NG, V>(t, g, param, S.R, S.Z, S.scratch);
     double rz = 0.0, zz = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double zi = S.Z[tpos(i, g)];
@@ -631,13 +801,12 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
 }
 
 // rows of thread tid: ρ = tid + j NT, j < RPT (coalesced); RPT = ceil(T LL / NT) <= ceil(LMAX / NG)
-template <int LMAX, int G, int NG>
+template <int LMAX, int G, int NG, int V>
 __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
     constexpr int NT = 32 * G * NG;
     constexpr int RPT = (LMAX + NG - 1) / NG;
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
-    __shared__ int s_work;
     const int c = blockIdx.x;
     const int n = g.n;
     Smem S = carve(sm, g);
@@ -647,26 +816,41 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     // constant inputs (column parameter, pole tables) before the wait on the preceding GEMM
     const int param = clamp_param(s.col_param[c], t.n_param);
     stage_tables(t, g, param, S.scratch);
+    // Inside the WHILE graph the previous iteration's kernels have all completed when this one
+    // starts (iterations of the conditional body are serialised; only the GEMM before this kernel
+    // overlaps it through PDL), so p, x, r, the active flag and the iteration counter are final:
+    // the v2 kernels load them before waiting on the GEMM and only q after it.
+    const bool early = V == 1 && s.cond_handle != 0;
+    double pv[RPT], qv[RPT], xv[RPT], rv[RPT];
+    int work = 0, k = 0;
+    auto load_pxr = [&]() {
+        work = __ldcg(&s.active[c]);
+        k = __ldcg(s.kiter) + 1;
+        if (work) {
+#pragma unroll
+            for (int j = 0; j < RPT; j++) {
+                const int i = threadIdx.x + j * NT;
+                const bool ok = i < n;
+                pv[j] = ok ? __ldcg(&s.p[off + i]) : 0.0;
+                xv[j] = ok ? __ldcg(&s.x[offx + i]) : 0.0;
+                rv[j] = ok ? __ldcg(&s.r[off + i]) : 0.0;
+            }
+        }
+    };
+    if (early) load_pxr();
     pdl_wait_prior();
-    if (threadIdx.x == 0) s_work = s.active[c];
-    __syncthreads();
+    if (!early) load_pxr();
     bool still = false;
+    bool flagged = false;
 #define DD_PHASE(i) \
     if (s.dbg && blockIdx.x == 0 && threadIdx.x == 0) s.dbg[i] = clock64()
     DD_PHASE(0);
-    if (!s_work) asm volatile("cp.async.wait_all;\n" ::);
-    if (s_work) {
-        const int k = *s.kiter + 1;
-        // one pass over p, q, x, r: all loads in flight together
-        double pv[RPT], qv[RPT], xv[RPT], rv[RPT];
+    if (!work) asm volatile("cp.async.wait_all;\n" ::);
+    if (work) {
 #pragma unroll
         for (int j = 0; j < RPT; j++) {
             const int i = threadIdx.x + j * NT;
-            const bool ok = i < n;
-            pv[j] = ok ? s.p[off + i] : 0.0;
-            qv[j] = ok ? (s.qadd ? s.q[off + i] + s.qadd[off + i] : s.q[off + i]) : 0.0;
-            xv[j] = ok ? s.x[offx + i] : 0.0;
-            rv[j] = ok ? s.r[off + i] : 0.0;
+            qv[j] = i < n ? (s.qadd ? s.q[off + i] + s.qadd[off + i] : s.q[off + i]) : 0.0;
         }
         double pq = 0.0, dummy = 0.0;
 #pragma unroll
@@ -674,6 +858,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
         block_sum2(pq, dummy, red);
         DD_PHASE(1);
         if (!(pq > 0.0)) {
+            flagged = true;
             if (threadIdx.x == 0) {
                 atomicExch(s.status, (int)DD_ENOTSPD);
                 s.active[c] = 0;
@@ -696,7 +881,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
             for (int i = threadIdx.x + RPT * NT; i < g.T * g.LL; i += NT) S.R[tpos(i, g)] = 0.0;
             __syncthreads();
             DD_PHASE(2);
-            block_polesum<LMAX, G, NG>(t, g, param, S.R, S.Z, S.scratch, blockIdx.x == 0 ? s.dbg : nullptr);
+            block_polesum<LMAX, G, NG, V>(t, g, param, S.R, S.Z, S.scratch, blockIdx.x == 0 ? s.dbg : nullptr);
             DD_PHASE(3);
             double rz = 0.0, zz = 0.0;
             double zv[RPT];
@@ -714,6 +899,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
             block_sum2(rz, zz, red);
             const double eta = s.norm_kind == 0 ? sqrt(fmax(rz, 0.0)) : sqrt(zz);
             const bool notspd = rz < 0.0;
+            flagged = notspd;
             const bool conv = eta <= s.rtol * s.eta0[c];
             if (threadIdx.x == 0) {
                 s.iters[c] = k;
@@ -725,11 +911,14 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
                 if (threadIdx.x == 0) s.active[c] = 0;
             } else {
                 const double beta = rz / s.rho[c];
-                // p as at entry, re-read (L2) rather than held in registers across the pole sum
+                if constexpr (V == 0) {
+                    // p as at entry, re-read (L2) rather than held in registers across the pole sum
+                    // (the partitioned pole sum needs every register)
 #pragma unroll
-                for (int j = 0; j < RPT; j++) {
-                    const int i = threadIdx.x + j * NT;
-                    pv[j] = i < n ? __ldcg(&s.p[off + i]) : 0.0;
+                    for (int j = 0; j < RPT; j++) {
+                        const int i = threadIdx.x + j * NT;
+                        pv[j] = i < n ? __ldcg(&s.p[off + i]) : 0.0;
+                    }
                 }
                 if (s.zs && (!s.zmixed || *s.zmixed)) {
                     // assembled Schur apply: the next GEMM's operand [γ p ; K p] written with p
@@ -759,7 +948,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
         }
     }
     DD_PHASE(4);
-    finish_iteration(s, still, s_work != 0);
+    finish_iteration(s, still, work != 0, flagged);
     DD_PHASE(5);
 #undef DD_PHASE
 }
@@ -984,6 +1173,14 @@ int polesum_groups(const PoleGeom& g) {
 
 int polesum_warps(const PoleGeom& g) { return g.G * polesum_groups(g); }
 
+static size_t polesum_v2_doubles(const PoleGeom& g, int max_sys) {
+    const int NW = polesum_warps(g);
+    const int NWB = g.T >= 256 ? std::min(NW, 4) : std::min(NW, 8);
+    return (size_t)V2_WSZ + (size_t)V2_REC * max_sys        // tables
+           + 2 * (size_t)max_sys * (g.T + 1)                // hl, yf
+           + (size_t)NWB * (3 * g.T + 1);                   // phase-B halo buffers
+}
+
 size_t polesum_smem(const PoleGeom& g, int max_sys) {
     const int NG = polesum_groups(g);
     const size_t tot = (size_t)g.LL * (g.T + 1);
@@ -991,7 +1188,16 @@ size_t polesum_smem(const PoleGeom& g, int max_sys) {
                + (size_t)max_sys * 4 * g.LL     // tables
                + 2 * (size_t)NG * g.T           // PCR exchange
                + (size_t)NG * tot;              // group partials
+    if (polesum_v2_supported(g, max_sys)) d = std::max(d, 2 * tot + polesum_v2_doubles(g, max_sys));
     return d * sizeof(double);
+}
+
+bool polesum_v2_supported(const PoleGeom& g, int max_sys) {
+    if (g.LL != V2_L || g.n + 1 != g.T * g.LL || g.T < 32 || g.T > 256) return false;
+    const int NT = 32 * polesum_warps(g);
+    if (NT % g.T != 0 || V2_L % (NT / g.T) != 0) return false;
+    const size_t tot = (size_t)g.LL * (g.T + 1);
+    return (2 * tot + polesum_v2_doubles(g, max_sys)) * sizeof(double) <= 220 * 1024;
 }
 
 template <typename K>
@@ -1000,6 +1206,15 @@ static cudaError_t set_smem(K kern, size_t bytes) {
 }
 
 // Instantiated shapes (LMAX, G, NG): n <= 1023 with G = 1, and LL = 32 chunks with G = 2, 4, 8.
+// V: 1 = merged-interior pole sum (tables t.v2; 16-row chunks only), 0 = partitioned Thomas + PCR
+#define DD_POLE_SWITCH_V(g, t, ...)                                                                \
+    DD_POLE_SWITCH(g, {                                                                          \
+        if constexpr (LM == V2_L) {                                                              \
+            if ((t).v2) { constexpr int VV = 1; __VA_ARGS__; }                                   \
+            else { constexpr int VV = 0; __VA_ARGS__; }                                          \
+        } else { constexpr int VV = 0; __VA_ARGS__; }                                            \
+    })
+
 #define DD_POLE_SWITCH(g, ...)                                                                   \
     do {                                                                                         \
         const int _lm = lmax_of((g).LL), _G = (g).G;                                             \
@@ -1019,9 +1234,9 @@ cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs
     if (s.ncols <= 0) return cudaSuccess;
     const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
-    DD_POLE_SWITCH(g, {
-        e = set_smem(k_pcg_init<LM, GG, NGG>, smem);
-        if (e == cudaSuccess) k_pcg_init<LM, GG, NGG><<<s.ncols, 32 * GG * NGG, smem, st>>>(s, g, t, b, ldb);
+    DD_POLE_SWITCH_V(g, t, {
+        e = set_smem(k_pcg_init<LM, GG, NGG, VV>, smem);
+        if (e == cudaSuccess) k_pcg_init<LM, GG, NGG, VV><<<s.ncols, 32 * GG * NGG, smem, st>>>(s, g, t, b, ldb);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -1030,9 +1245,9 @@ cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs
     if (s.ncols <= 0) return cudaSuccess;
     const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
-    DD_POLE_SWITCH(g, {
-        e = set_smem(k_pcg_iter<LM, GG, NGG>, smem);
-        if (e == cudaSuccess) e = launch_ex(k_pcg_iter<LM, GG, NGG>, s.ncols, 32 * GG * NGG, smem, st, pdl, s, g, t);
+    DD_POLE_SWITCH_V(g, t, {
+        e = set_smem(k_pcg_iter<LM, GG, NGG, VV>, smem);
+        if (e == cudaSuccess) e = launch_ex(k_pcg_iter<LM, GG, NGG, VV>, s.ncols, 32 * GG * NGG, smem, st, pdl, s, g, t);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -1042,9 +1257,9 @@ cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, c
     if (ncols <= 0) return cudaSuccess;
     const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
-    DD_POLE_SWITCH(g, {
-        e = set_smem(k_precond<LM, GG, NGG>, smem);
-        if (e == cudaSuccess) e = launch_ex(k_precond<LM, GG, NGG>, ncols, 32 * GG * NGG, smem, st, pdl, ncols, col_param, g, t, r, ldr, z, ldz);
+    DD_POLE_SWITCH_V(g, t, {
+        e = set_smem(k_precond<LM, GG, NGG, VV>, smem);
+        if (e == cudaSuccess) e = launch_ex(k_precond<LM, GG, NGG, VV>, ncols, 32 * GG * NGG, smem, st, pdl, ncols, col_param, g, t, r, ldr, z, ldz);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -1055,10 +1270,10 @@ cudaError_t launch_frac_ra(int ncols, const int* col_param, int n_param, const d
     if (ncols <= 0) return cudaSuccess;
     const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
-    DD_POLE_SWITCH(g, {
-        e = set_smem(k_frac_ra<LM, GG, NGG>, smem);
+    DD_POLE_SWITCH_V(g, t, {
+        e = set_smem(k_frac_ra<LM, GG, NGG, VV>, smem);
         if (e == cudaSuccess)
-            e = launch_ex(k_frac_ra<LM, GG, NGG>, ncols, 32 * GG * NGG, smem, st, pdl, ncols, col_param, n_param, gp, g, t,
+            e = launch_ex(k_frac_ra<LM, GG, NGG, VV>, ncols, 32 * GG * NGG, smem, st, pdl, ncols, col_param, n_param, gp, g, t,
                           x, ldx, u, ldu, h6);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
