@@ -195,7 +195,8 @@ def traffic_for(cfg_name, kernel):
 
 
 # ----------------------------------------------------------------------------- roofline model
-def step_model_2d(cfg, grouped: bool, assembled: bool, frac_ra: bool, cols_per_apply, n_live_groups, peaks):
+def step_model_2d(cfg, grouped: bool, assembled: bool, frac_ra: bool, cols_per_apply, n_live_groups, peaks,
+                  pair: bool = False):
     """Algorithmic work of one PCG iteration per kernel class, for the live columns:
     Schur GEMM  F = 2 n^2 c (grouped; 4 n^2 c assembled / factored K2, 2 n^2 c more for K1),
                 B = 8 n^2 (per live parameter group for grouped; the [F|G] / [S|F] operand once otherwise)
@@ -209,7 +210,8 @@ def step_model_2d(cfg, grouped: bool, assembled: bool, frac_ra: bool, cols_per_a
     p64, pdf, bw = peaks["dmma"] * 1e12, peaks["dfma"] * 1e12, peaks["hbm"] * 1e9
     if grouped:
         fg = 2.0 * n * n * c
-        bg = 8.0 * n * n * g + 16.0 * n * c
+        # H_p blocks: one n^2 operator per live parameter group; shared-pair kernel: G and F once
+        bg = (16.0 * n * n if pair else 8.0 * n * n * g) + 16.0 * n * c
     else:
         fg = (2.0 if frac_ra else 4.0) * n * n * c
         bg = 8.0 * n * n * (1 if frac_ra else 2) + 24.0 * n * c
@@ -461,14 +463,15 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
     share = {k: round(v[0] / total_prof_ms, 4) for k, v in prof.items()}
     avg_us = {k: round(v[0] / v[1] * 1e3, 2) if v[1] else None for k, v in prof.items()}
     if cfg.dim == 2:
-        assembled = qc["splitk_dst"] in (-1, -2)    # one GEMM per apply, no K1 (dd_set_schur_mode)
-        grouped = qc["splitk_dst"] == -2            # K-dim n: H_p = K_p G + gamma_p F
+        assembled = qc["splitk_dst"] in (-1, -2, -3)    # one GEMM per apply, no K1 (dd_set_schur_mode)
+        grouped = qc["splitk_dst"] in (-2, -3)          # K-dim n: H_p = K_p G + gamma_p F
+        pair = qc["splitk_dst"] == -3                   # ... formed in registers from the shared (G, F)
         compact = os.environ.get("DD_NO_COMPACT", "0")[:1] != "1"
         bn = 32 if grouped else 64
         cols_per_apply = live_columns(last, compact=compact, bn=bn)
         groups = live_columns(last, compact=compact, bn=bn)
         n_groups = [int(np.ceil(c / 32.0)) for c in groups]
-        model = step_model_2d(cfg, grouped, assembled, args.frac_mode == "ra", cols_per_apply, n_groups, pk)
+        model = step_model_2d(cfg, grouped, assembled, args.frac_mode == "ra", cols_per_apply, n_groups, pk, pair)
         iters_per_solve = len(cols_per_apply)
         per_iter_meas = {k: (prof[k][0] / prof[k][1] * 1e-3) if prof[k][1] else 0.0 for k in model}
         classes = {}
@@ -490,7 +493,10 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
             ach = by / t_dom / 1e9 if t_dom else None
             roof = {"bound": "hbm", "achieved": round(ach, 1) if ach else None, "peak": pk["hbm"], "unit": "GB/s",
                     "frac": round(ach / pk["hbm"], 4) if ach else None, "peak_source": pk["hbm_src"]}
-        if grouped:
+        if pair:
+            kname = ("gemm_schur grouped from the shared pair ((K_p G + gamma_p F) x X_p, operator fragments formed "
+                     "in registers from G, F tiles; stream-K DMMA fp64)")
+        elif grouped:
             kname = "gemm_schur grouped (H_p x X_p per parameter set, H_p = K_p G + gamma_p F formed at setup, DMMA fp64)"
         elif assembled:
             kname = ("gemm_schur ([F|G] x [gamma X; K X], DMMA fp64; G = S_unit formed at setup)"
@@ -502,7 +508,8 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
             kname = "polesum_pcg (fused PCG update + RA pole sum + dots, k_pcg_iter)"
         step_roof = sum(v[2] for v in model.values())
         step_meas = sum(per_iter_meas.values())
-        roof.update({"kernel": kname, "class": dom, "schur_mode": "grouped" if grouped else ("assembled" if assembled else "factored"),
+        roof.update({"kernel": kname, "class": dom,
+                     "schur_mode": ("grouped_pair" if pair else "grouped") if grouped else ("assembled" if assembled else "factored"),
                      "flops_per_launch": fl, "bytes_per_launch": by,
                      "mean_live_columns": round(float(np.mean(cols_per_apply)), 2) if cols_per_apply else 0,
                      "applies_per_solve": iters_per_solve,

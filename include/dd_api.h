@@ -221,22 +221,20 @@ dd_status dd_inner_iterations(const dd_ctx* ctx, int* iters);
  * SURVEY §8(a) rows a-2, a-3).  Both give the same operator up to rounding order:
  *   DD_SCHUR_FACTORED (0): per apply, the interior solve by fast diagonalisation,
  *        T' = (K_c s) ∘ (S_dst X) then Y = [S_dst | F] [T' ; γ X]   (6 n^2 flops per column);
- *   DD_SCHUR_ASSEMBLED (1; the default in DD_FRAC_RA mode, or when the grouped operators exceed
- *        16 GiB): the parameter-independent interior solve is applied once at
- *        setup to the identity, G = S_dst diag(s) S_dst = S_unit (n x n, beside F in the handle),
- *        and each apply is one GEMM  Y = [F | G] [γ X ; K X]          (4 n^2 flops per column);
- *        in DD_FRAC_RA mode Y = G (K X) + γ M r_F(L) M X.
- *   DD_SCHUR_GROUPED (2; THE DEFAULT for dense F when the operators fit in 16 GiB): the full Schur
- *        matrix of each parameter set, H_p = K_p G + γ_p F (n_param x n^2 doubles, formed when
- *        the mode is selected), and each apply is one grouped GEMM Y[:, c] = H_{p(c)} X[:, c]
- *        (2 n^2 flops per column) over 32-column tiles.  Needs every 32-column tile of a call
- *        to hold one parameter set (columns grouped by parameter, groups a multiple of 32 wide);
- *        otherwise that call computes the assembled product instead (same result, checked on
- *        the device, no host synchronisation).
- * mode outside {0,1,2}, a 3D handle, or GROUPED in DD_FRAC_RA mode: DD_EINVAL; GROUPED beyond
- * 64 GiB of operators: DD_ENOMEM.  (3D always applies the interior solve per apply: its S_unit
- * would be another n_Γ^2 = 2 GB stream.)  The environment variable DD_SCHUR_MODE=0|1|2 sets
- * the mode at setup. */
+ *   DD_SCHUR_ASSEMBLED (1; the default in DD_FRAC_RA mode): the parameter-independent interior
+ *        solve is applied once at setup to the identity, G = S_dst diag(s) S_dst = S_unit (n x n,
+ *        beside F in the handle), and each apply is one GEMM  Y = [F | G] [γ X ; K X]
+ *        (4 n^2 flops per column); in DD_FRAC_RA mode Y = G (K X) + γ M r_F(L) M X.
+ *   DD_SCHUR_GROUPED (2; THE DEFAULT with the dense F): each apply is one grouped GEMM
+ *        Y[:, c] = (K_p G + γ_p F) X[:, c] (2 n^2 flops per column) over 32-column tiles holding one
+ *        parameter set each.  The per-parameter operators H_p = K_p G + γ_p F (n_param x n^2
+ *        doubles) are formed when the mode is selected if they fit in 16 GiB; otherwise (or with
+ *        DD_GROUPED_PAIR=1) the GEMM forms each tile's operator in registers from the shared pair
+ *        (G, F) (2 n^2 doubles).  A call whose 32-column tiles mix parameter sets computes the
+ *        assembled product instead (same result, checked on the device, no host synchronisation).
+ * mode outside {0,1,2}, a 3D handle, or GROUPED in DD_FRAC_RA mode: DD_EINVAL.  (3D always applies
+ * the interior solve per apply: its S_unit would be another n_Γ^2 = 2 GB stream.)  The environment
+ * variable DD_SCHUR_MODE=0|1|2 sets the mode at setup. */
 #define DD_SCHUR_FACTORED 0
 #define DD_SCHUR_ASSEMBLED 1
 #define DD_SCHUR_GROUPED 2

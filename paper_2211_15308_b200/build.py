@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdd.so")
-SOURCES = ["gemm_f64.cu", "pcg_polesum.cu", "face3d.cu", "fx_sym.cu", "bulk2d.cu", "bulk3d.cu", "dd_api.cpp", "dd3d.cpp"]
+SOURCES = ["gemm_f64.cu", "gemm_pair.cu", "pcg_polesum.cu", "face3d.cu", "fx_sym.cu", "bulk2d.cu", "bulk3d.cu", "dd_api.cpp", "dd3d.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_LIB = "/usr/local/cuda/lib64"
 

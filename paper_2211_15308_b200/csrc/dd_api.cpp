@@ -389,6 +389,8 @@ static dd_status setup_2d(dd_ctx* c, const double* K, const double* mu_inv, cons
         wsmax = std::max(wsmax, std::max(w1, w2));
         cntmax = std::max(cntmax, gemm_tiles(n, c->max_cols));
     }
+    wsmax = std::max(wsmax, gemm_pair_ws_doubles(n, c->max_cols, c->num_sms));
+    cntmax = std::max(cntmax, gemm_pair_tiles(n, c->max_cols));
     if (wsmax) CK(dalloc(c, &c->gws, wsmax));
     CK(dalloc(c, &c->gcnt, cntmax + 1));
     return DD_OK;
@@ -497,12 +499,10 @@ extern "C" dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n
     if (want_dbg && dalloc(c, &c->dbg, 16) != cudaSuccess) return bail(fail(DD_ENOMEM, "dbg"));
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DD_ECUDA, "setup sync"));
     if (c->dim == 2) {
-        // default 2D Schur apply: grouped when F is dense and the per-parameter operators fit in
-        // 16 GiB, else assembled; DD_SCHUR_MODE=0|1|2 overrides (dd_set_schur_mode)
-        int want = c->frac_mode == DD_FRAC_DENSE &&
-                           (double)c->Mpad * c->Kpad * c->n_param * sizeof(double) <= 16.0 * (1ull << 30)
-                       ? DD_SCHUR_GROUPED
-                       : DD_SCHUR_ASSEMBLED;
+        // default 2D Schur apply with the dense F: grouped (per-parameter operators H_p when they fit
+        // in 16 GiB, else formed in registers from the shared pair by gemm_pair.cu); RA mode:
+        // assembled.  DD_SCHUR_MODE=0|1|2 overrides (dd_set_schur_mode)
+        int want = c->frac_mode == DD_FRAC_DENSE ? DD_SCHUR_GROUPED : DD_SCHUR_ASSEMBLED;
         if (const char* sm = std::getenv("DD_SCHUR_MODE")) want = sm[0] - '0';
         c->schur_mode = DD_SCHUR_ASSEMBLED;
         if (want != DD_SCHUR_ASSEMBLED) {
@@ -520,6 +520,30 @@ extern "C" int dd_interface_size(const dd_ctx* c) { return c ? c->ng : -1; }
 static dd_status schur_gemms(dd_ctx* c, int ncols, const int* colp, const double* xin, double* y, int ldy,
                              const int* ntl = nullptr, bool z_ready = false, bool ra_side = false) {
     const int n = c->n;
+    if (c->schur_mode == 2 && c->pair) {
+        // grouped from the shared pair: Y[:, c] = (K_p G + γ_p F) X[:, c] (gemm_pair.cu); a call
+        // whose 32-column tiles mix parameter sets computes F (γ X) + G (K X) from Z instead
+        if (!z_ready) {
+            CK(cudaMemsetAsync(c->ints + 6, 0, sizeof(int), c->stream));
+            TIMED(DD_KCLASS_OTHER, launch_check_tiles(ncols, colp, c->ints + 6, c->stream));
+            TIMED(DD_KCLASS_OTHER, launch_schur_operand(n, ncols, colp, c->n_param, c->Kp, c->gp, xin, c->ldv, c->Z,
+                                                        2 * c->Kpad, c->Kpad, c->stream));
+        }
+        PairArgs pa{};
+        pa.M = n; pa.N = ncols; pa.Kpad = c->Kpad;
+        pa.G = c->W + c->g_off; pa.F = c->W + c->Kpad; pa.lda = c->lda;
+        pa.X = xin; pa.ldx = c->ldv;
+        pa.Z = c->Z; pa.ldz = 2 * c->Kpad; pa.zhalf = c->Kpad;
+        pa.mixed = c->ints + 6;
+        pa.col_param = colp; pa.n_param = c->n_param; pa.Kp = c->Kp; pa.gp = c->gp;
+        pa.ntl = ntl;
+        pa.Y = y; pa.ldy = ldy;
+        pa.ws = c->gws; pa.counters = c->gcnt; pa.num_sms = c->num_sms;
+        c->last_split1 = -3;
+        c->last_split2 = 0;
+        TIMED(DD_KCLASS_GEMM_SCHUR, launch_gemm_pair(pa, c->stream));
+        return DD_OK;
+    }
     if (c->schur_mode == 2) {
         // grouped: Y[:, c] = H_{p(c)} X[:, c], one 32-column tile per GEMM CTA column; a launch
         // whose tiles mix parameter sets (flag from k_check_tiles) computes [F | G] [γ X ; K X]
@@ -1130,10 +1154,24 @@ extern "C" dd_status dd_set_schur_mode(dd_ctx* c, int mode) {
         return fail(DD_EINVAL, "schur mode not in {0,1,2}");
     if (mode == DD_SCHUR_GROUPED && c->frac_mode != DD_FRAC_DENSE)
         return fail(DD_EINVAL, "grouped schur mode needs the dense F (RA mode applies one n x n GEMM already)");
-    if (mode == DD_SCHUR_GROUPED && !c->H) {
+    if (mode == DD_SCHUR_GROUPED) {
+        // the per-parameter operators H_p stream n_param n^2 doubles per apply and are the faster
+        // kernel at the BASELINE sizes (cfg5: 130 vs 145 us, cfg3: 156 vs 172 us); the shared-pair
+        // kernel needs no H_p (2 n^2 doubles whatever n_param) and takes over when the H_p would
+        // exceed 16 GiB; DD_GROUPED_PAIR=0|1 overrides
+        bool pair = (double)c->Mpad * c->Kpad * c->n_param * sizeof(double) > 16.0 * (1ull << 30);
+        if (const char* e = std::getenv("DD_GROUPED_PAIR")) pair = e[0] == '1';
+        if (pair != c->pair) {
+            CK(cudaStreamSynchronize(c->stream));
+            for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+            c->graphs.clear();
+            c->pair = pair;
+        }
+    }
+    if (mode == DD_SCHUR_GROUPED && !c->pair && !c->H) {
         const size_t per = (size_t)c->Mpad * c->Kpad;
         if ((double)per * c->n_param * sizeof(double) > 64.0 * (1ull << 30))
-            return fail(DD_ENOMEM, "grouped schur mode: n_param x n^2 operators exceed 64 GiB");
+            return fail(DD_ENOMEM, "grouped schur mode with H_p: n_param x n^2 operators exceed 64 GiB");
         CK(dalloc(c, &c->H, per * c->n_param));
         CK(launch_group_operators(c->n, c->n_param, c->W, c->lda, c->Kpad, c->g_off, c->Kp, c->gp, c->H, c->Kpad,
                                   (long long)per, c->stream));

@@ -138,7 +138,8 @@ struct dd_ctx {
     double *rho = nullptr, *eta0 = nullptr, *relres = nullptr, *hist = nullptr;
     int *active = nullptr, *iters = nullptr, *ints = nullptr;   // ints: kiter, n_active, n_active_next, done, status, flag
     int hist_cap = 0;
-    bool hist_on = false;               // this solve records column 0's history (hist != NULL)
+    bool hist_on = false;
+    bool pair = false;                  // grouped mode through the shared-pair kernel (no H_p blocks)               // this solve records column 0's history (hist != NULL)
     // pinned host mirrors
     int* h_ints = nullptr;
     int* h_iters = nullptr;       // pinned staging of the per-column results [max_cols]

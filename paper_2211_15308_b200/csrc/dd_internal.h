@@ -46,6 +46,23 @@ struct GemmArgs {
     const double* alt_A; int alt_lda; const double* alt_B; int alt_ldb; int alt_K;
 };
 constexpr int GEMM_BN_GROUPED = 32;
+
+// Grouped Schur apply from the shared pair (gemm_pair.cu): Y[:, c] = (K_p G + γ_p F) X[:, c]
+struct PairArgs {
+    int M, N, Kpad;
+    const double *G, *F; int lda;      // row-major, rows readable up to round_up(M, 64)
+    const double* X; int ldx;          // column-major, columns readable up to round_up(N, 64)
+    const double* Z; int ldz, zhalf;   // mixed-tile fallback operand [γ X ; K X]
+    const int* mixed;                  // device flag
+    const int* col_param; int n_param;
+    const double *Kp, *gp;
+    const int* ntl;                    // live 32-column tiles or null
+    double* Y; int ldy;
+    double* ws; int* counters; int num_sms;
+};
+cudaError_t launch_gemm_pair(const PairArgs& a, cudaStream_t st);
+size_t gemm_pair_ws_doubles(int M, int N, int num_sms);
+int gemm_pair_tiles(int M, int N);
 int gemm_pick_splitk_grouped(int M, int N, int K, int num_sms);
 
 int gemm_tiles(int M, int N);

@@ -20,6 +20,7 @@ namespace dd {
 using CfgC = DgemmCfg<64, 64, 16, 2, 2, 4, 2>;   // cluster split-K: 4-stage ring, 2 CTAs/SM
 using CfgS = DgemmCfg<64, 64, 16, 2, 2, 3, 3>;   // stream-K: 3-stage ring, run at 2 CTAs/SM
 using CfgG = DgemmCfg<128, 32, 16, 4, 1, 3, 2>; // grouped per-parameter GEMM: 32-column tiles (tools/gemm_lab5.cu)
+using CfgG4 = DgemmCfg<128, 32, 16, 4, 1, 4, 2>; // grouped stream-K default: 4-stage ring (DD_GROUPED_STAGES=3|4)
 constexpr int OCC_C = 2, OCC_S = 2, OCC_G = 2;
 static_assert(CfgG::BN == GEMM_BN_GROUPED, "grouped tile width");
 constexpr int SK_MIN_UNITS = 64;   // below this the segment fix-ups outweigh the balance gain
@@ -110,6 +111,9 @@ cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
             // stream-K over the live 32-column tiles; the unit count follows the fallback's K too
             StreamK sk{a.ws, a.counters, 0};
             const int G = dgemm_streamk_grid<CfgG>(a.M, a.N, a.K, a.num_sms, OCC_G);
+            // 4-stage ring (cfg5 136 -> 130 us, cfg3 165 -> 156 us against 3 stages; 5 stages or 3 CTAs/SM lose)
+            static const int stages = std::getenv("DD_GROUPED_STAGES") ? std::atoi(std::getenv("DD_GROUPED_STAGES")) : 4;
+            if (stages == 4) return dgemm_launch_streamk<CfgG4>(g, G, sk, EpiStore{a.C, a.ldc}, st, false);
             return dgemm_launch_streamk<CfgG>(g, G, sk, EpiStore{a.C, a.ldc}, st, false);
         }
         return dgemm_launch<CfgG>(g, a.splitk, EpiStore{a.C, a.ldc}, st, a.pdl != 0);

@@ -222,3 +222,45 @@ def test_cfg4_full_size_pole_split_partials(lib, cfg4):
             S.close()
     tol = max(1e-10, 1e-15 * kc) + 20e-13 * kc
     assert rel_l2_cols(acc, g["z_eig"][:2]) <= tol
+
+
+# ------------------------------------------------------------------------- grouped apply from the shared pair
+@pytest.mark.parametrize("N", [200, 1024])
+def test_grouped_pair_kernel_parity(lib, monkeypatch, N):
+    """The grouped Schur apply through the shared-pair kernel (gemm_pair.cu: each warp forms
+    K_p G + γ_p F from the G, F tiles; forced with DD_GROUPED_PAIR=1 at sizes where it is not the
+    default): group-aligned 32-column tiles, a mixed batch (tiles spanning two parameter sets: the
+    F (γX) + G (KX) fallback) and a ragged batch, against the oracle; PCG parity on the aligned batch."""
+    monkeypatch.setenv("DD_GROUPED_PAIR", "1")
+    params = [(1.0, 1e2), (1e-4, 1e6), (1.0, 0.0)]
+    ras = fit_all(N, params, 14)
+    Mo = oprob.ModeProblem2D(N)
+    C = 96
+    B = np.random.default_rng(N).uniform(-1, 1, (C, N - 1))
+    S = lib.Solver(2, N, params, ras, max_cols=C, device=0)
+    try:
+        cases = {"aligned": np.repeat(np.arange(3), 32), "mixed": np.arange(C) % 3,
+                 "ragged": np.repeat(np.arange(3), 32)[:33]}
+        for name, colp in cases.items():
+            Bc = B[:len(colp)]
+            y = S.apply_schur(torch.as_tensor(Bc, device="cuda"), colp).cpu().numpy()
+            assert S.query_config()["splitk_dst"] == -3, name
+            ref = np.stack([Mo.apply_S(*params[colp[c]], Bc[c]) for c in range(len(colp))])
+            assert rel_l2_cols(y, ref) <= 1e-10, name
+        colp = cases["aligned"]
+        res = S.pcg_solve(torch.as_tensor(B, device="cuda"), colp)
+        x = res.x.cpu().numpy()
+        for c in (0, 40, 95):
+            K, g = params[colp[c]]; ra = ras[colp[c]]
+            xo, it, *_ = opcg.pcg(lambda v: Mo.apply_S(K, g, v),
+                                  lambda v: Mo.apply_P_ra(ra.c0, ra.poles, ra.residues, v), B[c])
+            assert abs(int(res.iters[c]) - it) <= 1 and np.linalg.norm(x[c] - xo) <= 1e-8 * np.linalg.norm(xo)
+        mixed = S.pcg_solve(torch.as_tensor(B, device="cuda"), cases["mixed"])
+        for c in (1, 50):
+            K, g = params[cases["mixed"][c]]; ra = ras[cases["mixed"][c]]
+            xo, it, *_ = opcg.pcg(lambda v: Mo.apply_S(K, g, v),
+                                  lambda v: Mo.apply_P_ra(ra.c0, ra.poles, ra.residues, v), B[c])
+            assert abs(int(mixed.iters[c]) - it) <= 1
+            assert np.linalg.norm(mixed.x.cpu().numpy()[c] - xo) <= 1e-8 * np.linalg.norm(xo)
+    finally:
+        S.close()
