@@ -104,6 +104,7 @@ struct PoleTabs {
     // per parameter set a block of v2_stride doubles = W (16 x 16) + max_sys records of V2_REC
     const double* v2;
     int v2_stride;
+    int v2_skip;                // diagnostics only (DD_V2_SKIP bitmask: 1 phase A, 2 phase B, 4 phase C)
 };
 // v2 pole-sum table layout (dd_api.cpp build_v2_record; pcg_polesum.cu block_polesum_v2)
 constexpr int V2_L = 16;        // rows per chunk: 15 interior + 1 separator

@@ -470,7 +470,7 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
         }
         acc[u] = a;
     }
-    for (int k = q; k < nsys; k += Q) {
+    for (int k = q; k < ((t.v2_skip & 1) ? 0 : nsys); k += Q) {
         const double* rec = tab + V2_WSZ + k * V2_REC;
         const double2* tf2 = reinterpret_cast<const double2*>(rec);
         double f0 = 0.0, l0 = 0.0, f1 = 0.0, l1 = 0.0;        // two chains each (even / odd terms)
@@ -500,7 +500,7 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
         if (warp < NWB) {
             double* hb = yf + (size_t)t.max_sys * TP + (size_t)warp * (3 * T + 1);
             if (lane == 0) { hb[T] = 0.0; hb[3 * T] = 0.0; }      // v_0 and v_2T (read by σ = T at s = T)
-            for (int k = warp; k < nsys; k += NWB) {
+            for (int k = warp; k < ((t.v2_skip & 2) ? 0 : nsys); k += NWB) {
                 const double* rec = tab + V2_WSZ + k * V2_REC;
                 const double e = rec[V2_E];
                 double* A = hl + k * TP;
@@ -547,7 +547,7 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
     double acc2[RPT];                            // second chain (odd systems)
 #pragma unroll
     for (int u = 0; u < RPT; u++) acc2[u] = 0.0;
-    for (int k0 = 0; k0 < nsys; k0 += 2) {
+    for (int k0 = 0; k0 < ((t.v2_skip & 4) ? 0 : nsys); k0 += 2) {
 #pragma unroll
         for (int kk = 0; kk < 2; kk++) {
             const int k = k0 + kk;
