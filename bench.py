@@ -701,26 +701,34 @@ def emulate_ranks(args, cfg, ras, frac, B_all, colp_all, pilot, dev, flush):
         t_schur = e0.elapsed_time(e1) / 5
     finally:
         full.close()
-    per = []
+    per, per_s = [], []
     for rk in range(W):
         S = binding.Solver(3, cfg.N, cfg.params, ras, max_cols=B_all.shape[0], device=torch.device(dev).index,
                            frac=frac, dist=(rk, W, 1, None))
         try:
-            S.apply_precond(Bt, cp)
-            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(S.stream)
-            for _ in range(3):
-                S.apply_precond(Bt, cp)
-            e1.record(S.stream)
-            torch.cuda.synchronize()
-            per.append(e0.elapsed_time(e1) / 3)
+            for what, lst in (("precond", per), ("schur", per_s)):
+                fn = S.apply_precond if what == "precond" else S.apply_schur
+                fn(Bt, cp)
+                e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(S.stream)
+                for _ in range(3):
+                    fn(Bt, cp)
+                e1.record(S.stream)
+                torch.cuda.synchronize()
+                lst.append(e0.elapsed_time(e1) / 3)
         finally:
             S.close()
-    t_step = iters * (t_schur + max(per)) + max(per)
-    out.update({"iters": iters, "schur_apply_ms": round(t_schur, 3), "rank_precond_ms": [round(v, 3) for v in per],
+    # each rank: its F rows (row-sharded stream) + the replicated slab passes, then its share of the
+    # pole sum; the step waits for the slowest rank at each of the two collectives
+    t_step = iters * (max(per_s) + max(per)) + max(per)
+    t_step_repl = iters * (t_schur + max(per)) + max(per)
+    out.update({"iters": iters, "schur_apply_ms_1gpu": round(t_schur, 3), "rank_schur_ms_row_sharded_F": [round(v, 3) for v in per_s],
+                "rank_precond_ms": [round(v, 3) for v in per],
                 "predicted_ms_per_solve_batch": round(t_step, 3), "measured_1gpu_ms": round(t_solve1, 3),
                 "predicted_value": round(B_all.shape[0] / (t_step / 1e3), 3), "unit": UNIT,
-                "excludes": "the NCCL allreduce of 16129 x 8 fp64 per preconditioner apply (1 GPU available)"})
+                "predicted_value_replicated_F": round(B_all.shape[0] / (t_step_repl / 1e3), 3),
+                "excludes": "per PCG iteration the NCCL allreduce of the partial pole sums and the allgather of the "
+                            "F rows (16129 x 8 fp64 each) — one GPU available"})
     return out
 
 

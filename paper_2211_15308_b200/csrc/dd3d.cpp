@@ -120,8 +120,14 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
         // apply for the full-F stream at 83 % of HBM)
         const char* fp = std::getenv("DD_FX_PACKED");
         const bool packed = fx_sym_supported(f.NP) && fp && fp[0] == '1';
+        // row-sharded F under a multi-rank pole split (SURVEY §8(e) option): rank ρ keeps rows
+        // [r0(ρ), r0(ρ+1)) in whole 256-row tiles of the F stream; DD_FX_ROWSHARD=0 keeps all rows
+        const char* rsh = std::getenv("DD_FX_ROWSHARD");
+        const bool shardF = !packed && dist && dist->world > 1 && dist->mode == DD_SHARD_POLES && !(rsh && rsh[0] == '0');
         double* Ffull = nullptr;
-        if (packed) {
+        f.fx_r0 = 0;
+        f.fx_r1 = (int)f.NP;
+        if (packed || shardF) {
             DD_CK(cudaMalloc(&Ffull, frows * (size_t)f.NP * sizeof(double)));
             DD_CK(cudaMemsetAsync(Ffull, 0, frows * (size_t)f.NP * sizeof(double), c->stream));
         } else {
@@ -129,6 +135,25 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
             Ffull = f.F;
         }
         DD_CK(face_gram_scatter(dA, n2, kp, Ffull, n, f.ldf, f.NP, c->num_sms, c->stream));
+        if (shardF) {
+            const int W = dist->world, ntile = (int)((f.NP + 255) / 256);
+            std::vector<int> r0s(W + 1);
+            for (int q = 0; q <= W; q++) r0s[q] = std::min((int)f.NP, (int)((long long)q * ntile / W) * 256);
+            f.fx_r0 = r0s[dist->rank];
+            f.fx_r1 = r0s[dist->rank + 1];
+            for (int q = 0; q < W; q++) f.fx_rows_max = std::max(f.fx_rows_max, r0s[q + 1] - r0s[q]);
+            const size_t rows = (size_t)std::max(1, f.fx_r1 - f.fx_r0);
+            DD_CK(dalloc(c, &f.F, (size_t)round_up((int)rows, 256) * (size_t)f.NP));
+            DD_CK(cudaMemcpyAsync(f.F, Ffull + (size_t)f.fx_r0 * f.NP, (size_t)(f.fx_r1 - f.fx_r0) * f.NP * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, c->stream));
+            DD_CK(dalloc(c, &f.fx_r0s, (size_t)W + 1));
+            DD_CK(cudaMemcpyAsync(f.fx_r0s, r0s.data(), sizeof(int) * (W + 1), cudaMemcpyHostToDevice, c->stream));
+            DD_CK(dalloc(c, &f.fx_send, (size_t)c->max_cols * f.fx_rows_max));
+            DD_CK(dalloc(c, &f.fx_recv, (size_t)W * c->max_cols * f.fx_rows_max));
+            DD_CK(cudaStreamSynchronize(c->stream));
+            cudaFree(Ffull);
+            Ffull = nullptr;
+        }
         if (packed) {
             // F is symmetric (B B^T): keep the upper 128 x 128 blocks only (row a-3, half the bytes)
             std::vector<int> ij;
@@ -465,6 +490,31 @@ static dd_status precond_core(dd_ctx* c, int ncols, const double* r, double* z) 
 }
 
 // y = S x on padded face vectors p -> q
+// q = γ F p + D with the dense F stream (row a-3); a row-sharded F (pole split, §8(e)) computes this
+// rank's rows and gathers the others with one ncclAllGather (without a communicator — ranks emulated
+// in one process — the other rows are zero, so the ranks' outputs add up to the full product)
+static dd_status fx_apply(dd_ctx* c, int ncols, const int* colp, const double* p, double* q, const double* D) {
+    Face3& f = c->f3;
+    const int rows = f.fx_r1 - f.fx_r0;
+    if (rows >= f.NP) {
+        DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, f.NP, p, q, D, ncols, colp, c->n_param, c->gp, f.fx_ws, f.fx_cnt,
+                                               c->num_sms, c->stream));
+        return DD_OK;
+    }
+    if (rows > 0)
+        DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, f.NP, p, q, D, ncols, colp, c->n_param, c->gp, f.fx_ws, f.fx_cnt,
+                                               c->num_sms, c->stream, f.fx_r0, rows));
+    if (f.nccl) {
+        DD_TIMED(DD_KCLASS_OTHER, fx_pack(q, f.NP, ncols, f.fx_r0, rows, f.fx_rows_max, f.fx_send, c->stream));
+        NK(ncclAllGather(f.fx_send, f.fx_recv, (size_t)ncols * f.fx_rows_max, ncclDouble,
+                         static_cast<ncclComm_t>(f.nccl), c->stream));
+        DD_TIMED(DD_KCLASS_OTHER, fx_unpack(f.fx_recv, f.NP, ncols, f.world, f.fx_rows_max, f.fx_r0s, q, c->stream));
+    } else {
+        DD_TIMED(DD_KCLASS_OTHER, fx_zero_outside(f.NP, ncols, f.fx_r0, f.fx_r1, q, c->stream));
+    }
+    return DD_OK;
+}
+
 static dd_status schur_core(dd_ctx* c, int ncols, const int* colp, const double* p, double* q) {
     Face3& f = c->f3;
     DD_TIMED(DD_KCLASS_OTHER, gather_param(ncols, colp, c->n_param, c->Kp, f.Kcol, c->stream));
@@ -490,9 +540,7 @@ static dd_status schur_core(dd_ctx* c, int ncols, const int* colp, const double*
                                                     f.fxD, f.fxT, c->num_sms, c->stream));
         return DD_OK;
     }
-    DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, f.NP, p, q, f.U2, ncols, colp, c->n_param, c->gp, f.fx_ws, f.fx_cnt,
-                                           c->num_sms, c->stream));
-    return DD_OK;
+    return fx_apply(c, ncols, colp, p, q, f.U2);
 }
 
 dd_status schur_3d(dd_ctx* c, int ncols, const int* colp, const double* xin, double* yout, bool user_layout) {
@@ -650,8 +698,8 @@ dd_status bulk_pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, do
             DD_TIMED(DD_KCLASS_GEMM_SCHUR, fx_sym_apply(f.Fp, f.fblk, NP, f.b3P, f.b3F, f.b3Z, ncols, colp, c->n_param,
                                                         c->gp, f.fxD, f.fxT, c->num_sms, c->stream));
         } else {
-            DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, NP, f.b3P, f.b3F, f.b3Z, ncols, colp, c->n_param, c->gp, f.fx_ws,
-                                                   f.fx_cnt, c->num_sms, c->stream));
+            dd_status fs = fx_apply(c, ncols, colp, f.b3P, f.b3F, f.b3Z);
+            if (fs != DD_OK) return fs;
         }
         DD_TIMED(DD_KCLASS_OTHER, bulk3_apply(n, ldf, NP, ncols, in, nb, f.b3F, colp, c->n_param, c->Kp, 1.0 / c->N, out,
                                               c->stream));

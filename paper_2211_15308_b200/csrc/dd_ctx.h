@@ -92,6 +92,12 @@ struct Face3 {
     bool inner_iters_on_device = false;
     double* fx_ws = nullptr;
     int* fx_cnt = nullptr;
+    // row-sharded F under the pole split: this rank holds rows [fx_r0, fx_r1) of F
+    // (F points at row fx_r0); the other rows of γ F p arrive by ncclAllGather (fx_r1 - fx_r0 = NP:
+    // unsharded)
+    int fx_r0 = 0, fx_r1 = 0, fx_rows_max = 0;
+    int* fx_r0s = nullptr;            // device [world + 1]: every rank's first row, then NP
+    double *fx_send = nullptr, *fx_recv = nullptr;
     double lam_min = 0.0, lam_max = 0.0;   // spectrum of the face pair (from the setup gevp)
     void* nccl = nullptr;             // ncclComm_t when the poles are split across ranks
     FSet fs;                          // RA-evaluated fractional term (Remark 1), RA mode only

@@ -255,7 +255,13 @@ size_t face_fx_ws_doubles(long long NP, int ncols, int num_sms);
 int face_fx_tiles(long long NP, int ncols);
 cudaError_t face_fx(const double* F, long long NP, const double* p, double* q, const double* D, int ncols,
                     const int* col_param, int n_param, const double* gp, double* ws, int* counters, int num_sms,
+                    cudaStream_t st,
+                    int row0 = 0, int rows = -1);
+cudaError_t fx_pack(const double* q, long long NP, int ncols, int r0, int rows, int rows_max, double* buf,
                     cudaStream_t st);
+cudaError_t fx_unpack(const double* buf, long long NP, int ncols, int world, int rows_max, const int* r0s, double* q,
+                      cudaStream_t st);
+cudaError_t fx_zero_outside(long long NP, int ncols, int r0, int r1, double* q, cudaStream_t st);
 cudaError_t face_gram_scatter(const double* B, int n2, int kp, double* F, int n, int ldf, long long NP, int num_sms,
                               cudaStream_t st);
 cudaError_t face_copy_in(int n, int ldf, long long NP, int ncols, const double* src, int lds, double* dst, cudaStream_t st);

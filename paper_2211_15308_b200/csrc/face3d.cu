@@ -59,12 +59,12 @@ struct EpiInnerOp {            // q̂_part[b] = cs[s] v,  s = b / C: the D̂ ⊗
         q[(size_t)b * NP + i] = cs[s] * v;
     }
 };
-struct EpiFaceFx {             // q[c] = γ_c v + D[c]  (padded face layout)
-    double* q; const double* D; long long ldq; const int* col_param; int n_param; const double* gp;
+struct EpiFaceFx {             // q[c] = γ_c v + D[c]  (padded face layout; rows offset by row0 for a row shard of F)
+    double* q; const double* D; long long ldq; const int* col_param; int n_param; const double* gp; int row0;
     __device__ __forceinline__ void operator()(int, int row, int col, double v) const {
         int p = col_param[col];
         p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
-        const size_t i = row + (size_t)col * ldq;
+        const size_t i = row0 + row + (size_t)col * ldq;
         q[i] = fma(gp[p], v, D[i]);
     }
 };
@@ -119,13 +119,60 @@ cudaError_t face_inner_op_pass(const double* in, double* q, const double* p, int
 size_t face_fx_ws_doubles(long long NP, int ncols, int num_sms) {
     return dgemm_streamk_ws_doubles<CfgFv>((int)NP, ncols, num_sms * OCC_FV);
 }
+// rows [row0, row0 + rows) of q only, F = those rows of the full operator (row-sharded F, §8(e))
 cudaError_t face_fx(const double* F, long long NP, const double* p, double* q, const double* D, int ncols,
                     const int* col_param, int n_param, const double* gp, double* ws, int* counters, int num_sms,
-                    cudaStream_t st) {
-    DgemmProblem g{(int)NP, ncols, (int)NP, F, (int)NP, p, (int)NP};
+                    cudaStream_t st, int row0, int rows) {
+    if (rows < 0) rows = (int)NP;
+    DgemmProblem g{rows, ncols, (int)NP, F, (int)NP, p, (int)NP};
     StreamK sk{ws, counters, 0};
-    const int G = dgemm_streamk_grid<CfgFv>((int)NP, ncols, (int)NP, num_sms, OCC_FV);
-    return dgemm_launch_streamk<CfgFv>(g, G, sk, EpiFaceFx{q, D, NP, col_param, n_param, gp}, st);
+    const int G = dgemm_streamk_grid<CfgFv>(rows, ncols, (int)NP, num_sms, OCC_FV);
+    return dgemm_launch_streamk<CfgFv>(g, G, sk, EpiFaceFx{q, D, NP, col_param, n_param, gp, row0}, st);
+}
+
+// Row-sharded F: rank rows [r0, r0 + rows) of each column packed contiguously (count rows_max per
+// column, zero padded) for ncclAllGather, and the gathered blocks scattered back into the columns
+__global__ void k_fx_pack(const double* __restrict__ q, long long NP, int ncols, int r0, int rows, int rows_max,
+                          double* __restrict__ buf) {
+    const long long tot = (long long)ncols * rows_max;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot; idx += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(idx / rows_max), i = (int)(idx % rows_max);
+        buf[idx] = i < rows ? q[(size_t)c * NP + r0 + i] : 0.0;
+    }
+}
+__global__ void k_fx_unpack(const double* __restrict__ buf, long long NP, int ncols, int world, int rows_max,
+                            const int* __restrict__ r0s, double* __restrict__ q) {
+    const long long tot = (long long)world * ncols * rows_max;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot; idx += (long long)gridDim.x * blockDim.x) {
+        const int rk = (int)(idx / ((long long)ncols * rows_max));
+        const long long rem = idx % ((long long)ncols * rows_max);
+        const int c = (int)(rem / rows_max), i = (int)(rem % rows_max);
+        const int r0 = r0s[rk], r1 = r0s[rk + 1];
+        if (r0 + i < r1) q[(size_t)c * NP + r0 + i] = buf[idx];
+    }
+}
+// no communicator (ranks emulated in one process): the rows this rank does not own are zero, so
+// the ranks' outputs add up to the full product
+__global__ void k_fx_zero_outside(long long NP, int ncols, int r0, int r1, double* __restrict__ q) {
+    const long long tot = (long long)ncols * NP;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot; idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx % NP);
+        if (i < r0 || i >= r1) q[idx] = 0.0;
+    }
+}
+cudaError_t fx_pack(const double* q, long long NP, int ncols, int r0, int rows, int rows_max, double* buf,
+                    cudaStream_t st) {
+    k_fx_pack<<<592, 256, 0, st>>>(q, NP, ncols, r0, rows, rows_max, buf);
+    return cudaGetLastError();
+}
+cudaError_t fx_unpack(const double* buf, long long NP, int ncols, int world, int rows_max, const int* r0s, double* q,
+                      cudaStream_t st) {
+    k_fx_unpack<<<592, 256, 0, st>>>(buf, NP, ncols, world, rows_max, r0s, q);
+    return cudaGetLastError();
+}
+cudaError_t fx_zero_outside(long long NP, int ncols, int r0, int r1, double* q, cudaStream_t st) {
+    k_fx_zero_outside<<<592, 256, 0, st>>>(NP, ncols, r0, r1, q);
+    return cudaGetLastError();
 }
 int face_fx_tiles(long long NP, int ncols) { return dgemm_tiles<CfgFv>((int)NP, ncols); }
 

@@ -264,3 +264,38 @@ def test_grouped_pair_kernel_parity(lib, monkeypatch, N):
             assert np.linalg.norm(mixed.x.cpu().numpy()[c] - xo) <= 1e-8 * np.linalg.norm(xo)
     finally:
         S.close()
+
+
+# ------------------------------------------------------------------------- row-sharded F (SURVEY §8(e) option)
+def test_row_sharded_f_emulated_ranks(lib):
+    """Config-4 pole split with the F stream row-sharded over the ranks (each rank holds rows
+    [r0, r1) of F; with no communicator its Schur apply returns those rows and zeros elsewhere, the
+    input of the ncclAllGather): the ranks' outputs add up to the single-GPU apply and to the
+    oracle's S x (dense gevp F), for 2 and 3 ranks (N = 32: F has 4 row tiles of 256)."""
+    N = 32; n = N - 1
+    params = [(1.0, 1e4)]
+    ras = _fit3(N, params, 10)
+    D = oprob.DenseProblem(3, N)
+    B = np.random.default_rng(11).uniform(-1, 1, (3, n * n))
+    Bt = torch.as_tensor(B, device="cuda")
+    ref = D.apply_S(*params[0], B.T).T
+    full = lib.Solver(3, N, params, ras, max_cols=3, device=0)
+    try:
+        yf = full.apply_schur(Bt, [0, 0, 0]).cpu().numpy()
+    finally:
+        full.close()
+    assert rel_l2_cols(yf, ref) <= 1e-10
+    for world in (2, 3):
+        acc = np.zeros_like(B)
+        nonzero_ranks = 0
+        for rank in range(world):
+            S = lib.Solver(3, N, params, ras, max_cols=3, device=0, dist=(rank, world, 1, None))
+            try:
+                y = S.apply_schur(Bt, [0, 0, 0]).cpu().numpy()
+            finally:
+                S.close()
+            nonzero_ranks += int(np.any(y != 0))
+            acc += y
+        assert nonzero_ranks == world               # every rank owns rows
+        assert rel_l2_cols(acc, ref) <= 1e-10, world
+        assert rel_l2_cols(acc, yf) <= 1e-13, world
