@@ -497,7 +497,8 @@ extern "C" dd_status dd_setup_ex(const dd_mesh* mesh, const dd_frac* frac, int n
     if (cudaMallocHost(&c->h_iters, sizeof(int) * (size_t)max_cols) != cudaSuccess ||
         cudaMallocHost(&c->h_rel, sizeof(double) * (size_t)max_cols) != cudaSuccess)
         return bail(fail(DD_ENOMEM, "pinned"));
-    if (want_dbg && dalloc(c, &c->dbg, 16) != cudaSuccess) return bail(fail(DD_ENOMEM, "dbg"));
+    // dbg[0..15]: phase stamps of CTA 0; dbg[16 + 2 b], dbg[17 + 2 b]: %globaltimer at entry / exit of CTA b
+    if (want_dbg && dalloc(c, &c->dbg, 16 + 2 * (size_t)max_cols) != cudaSuccess) return bail(fail(DD_ENOMEM, "dbg"));
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DD_ECUDA, "setup sync"));
     if (c->dim == 2) {
         // default 2D Schur apply with the dense F: grouped (per-parameter operators H_p when they fit
@@ -881,6 +882,20 @@ static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const dou
     if (c->dbg) {
         long long t[16] = {0};
         CK(cudaMemcpy(t, c->dbg, sizeof(t), cudaMemcpyDeviceToHost));
+        if (c->dim == 2 && ncols > 0) {
+            // CTA timeline of the last fused PCG launch: entry / exit spread (ns)
+            std::vector<long long> tl(2 * (size_t)ncols);
+            CK(cudaMemcpy(tl.data(), c->dbg + 16, sizeof(long long) * tl.size(), cudaMemcpyDeviceToHost));
+            long long e0 = tl[0], e1 = tl[0], x0 = tl[1], x1 = tl[1];
+            double dur = 0.0;
+            for (int b = 0; b < ncols; b++) {
+                e0 = std::min(e0, tl[2 * b]); e1 = std::max(e1, tl[2 * b]);
+                x0 = std::min(x0, tl[2 * b + 1]); x1 = std::max(x1, tl[2 * b + 1]);
+                dur += (double)(tl[2 * b + 1] - tl[2 * b]);
+            }
+            fprintf(stderr, "[dd cta timeline ns] entry spread %lld  first exit %lld  last exit %lld  mean CTA %.0f\n",
+                    e1 - e0, x0 - e0, x1 - e0, dur / ncols);
+        }
         fprintf(stderr, "[dd phase cycles] load+pq %lld  update %lld  polesum %lld  dots+p %lld  finish %lld\n",
                 t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
         if (c->tabs.v2)

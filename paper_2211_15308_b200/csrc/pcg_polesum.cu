@@ -76,6 +76,12 @@ __device__ __forceinline__ double group_shift(double v, int d, int tau, double* 
     }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // Read-only global load issued where written (volatile: not sunk towards its first use).
 __device__ __forceinline__ double ldg_early(const double* p) {
     double v;
@@ -813,6 +819,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     const size_t off = (size_t)c * s.ldv;
     const size_t offx = (size_t)c * s.ldx;
     pdl_trigger();
+    if (s.dbg && threadIdx.x == 0) s.dbg[16 + 2 * c] = (long long)gtimer();
     // constant inputs (column parameter, pole tables) before the wait on the preceding GEMM
     const int param = clamp_param(s.col_param[c], t.n_param);
     stage_tables(t, g, param, S.scratch);
@@ -950,6 +957,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     DD_PHASE(4);
     finish_iteration(s, still, work != 0, flagged);
     DD_PHASE(5);
+    if (s.dbg && threadIdx.x == 0) s.dbg[17 + 2 * c] = (long long)gtimer();
 #undef DD_PHASE
 }
 
