@@ -517,11 +517,9 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
                     const int sg = 32 * sl + lane + 1;         // separator σ = τ + 1 in 1..T (σ = T: boundary)
                     rs[sl] = sg < T ? fma(-e, B[sg], A[sg - 1]) : 0.0;
                 }
+                // step 0 reads σ ± 1: no mirror is read yet
 #pragma unroll
-                for (int sl = 0; sl < S; sl++) {
-                    const int sg = 32 * sl + lane + 1;
-                    hb[T + sg] = rs[sl]; hb[T - sg] = -rs[sl]; hb[3 * T - sg] = -rs[sl];
-                }
+                for (int sl = 0; sl < S; sl++) hb[T + 32 * sl + lane + 1] = rs[sl];
                 __syncwarp();
 #pragma unroll
                 for (int j = 0; j < JS; j++) {
@@ -530,13 +528,19 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
 #pragma unroll
                     for (int sl = 0; sl < S; sl++) {
                         const int sg = 32 * sl + lane + 1;
-                        rs[sl] = fma(-al, hb[T + sg - st] + hb[T + sg + st], rs[sl]);   // σ = T stays 0
+                        rs[sl] = sg < T ? fma(-al, hb[T + sg - st] + hb[T + sg + st], rs[sl]) : 0.0;
                     }
                     __syncwarp();
+                    // the next step (stride 2s) reads the mirror of σ only where it falls outside
+                    // [1, T - 1]: the left one for σ < 2s, the right one for σ > T - 2s (writing all
+                    // mirrors every step made this phase shared-memory-bandwidth bound)
+                    const int st2 = 2 * st;
 #pragma unroll
                     for (int sl = 0; sl < S; sl++) {
                         const int sg = 32 * sl + lane + 1;
-                        hb[T + sg] = rs[sl]; hb[T - sg] = -rs[sl]; hb[3 * T - sg] = -rs[sl];
+                        hb[T + sg] = rs[sl];
+                        if (sg < st2) hb[T - sg] = -rs[sl];
+                        if (sg > T - st2) hb[3 * T - sg] = -rs[sl];
                     }
                     __syncwarp();
                 }
