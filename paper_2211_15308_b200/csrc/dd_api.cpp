@@ -147,6 +147,7 @@ static void build_v2_record(long double d, long double e, long double w, int T, 
     for (int i = 0; i < m; i++) {
         rec[i] = (double)inv[0][i];
         rec[16 + i] = (double)(w * e * inv[0][i]);
+        rec[V2_WREV + i] = (double)(w * e * inv[0][m - 1 - i]);
         for (int j = 0; j < m; j++) Wacc[i * 16 + j] += w * inv[i][j];
     }
     rec[V2_E] = (double)e;

@@ -109,8 +109,9 @@ struct PoleTabs {
 // v2 pole-sum table layout (dd_api.cpp build_v2_record; pcg_polesum.cu block_polesum_v2)
 constexpr int V2_L = 16;        // rows per chunk: 15 interior + 1 separator
 constexpr int V2_WSZ = 256;     // merged interior operator W = Σ_k w_k T_int,k^-1, 16 x 16 (row/col 15 zero)
-constexpr int V2_REC = 48;      // per system: [0,16) tf, [16,32) w e tf, e, w, 1/D, -, [36,48) PCR α_j
-constexpr int V2_E = 32, V2_WK = 33, V2_DINV = 34, V2_AL = 36;
+constexpr int V2_REC = 64;      // per system: [0,16) tf, [16,32) w e tf, e, w, 1/D, -, [36,48) PCR α_j,
+                                //             [48,64) w e tf reversed (w e tf[14 - i])
+constexpr int V2_E = 32, V2_WK = 33, V2_DINV = 34, V2_AL = 36, V2_WREV = 48;
 
 // PCG state for a batch of columns (device).
 struct PcgState {

@@ -463,7 +463,7 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
     double acc[RPT];
 #pragma unroll
     for (int u = 0; u < RPT; u++) {
-        const int i = q + Q * u;
+        const int i = q * RPT + u;               // contiguous rows per thread (phase C loads pairs)
         double a = 0.0;
         if (i < V2_L - 1) {
             const double2* wr = reinterpret_cast<const double2*>(tab + i * 16);
@@ -557,6 +557,9 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
     double acc2[RPT];                            // second chain (odd systems)
 #pragma unroll
     for (int u = 0; u < RPT; u++) acc2[u] = 0.0;
+    // the thread's rows are contiguous (i = q RPT + u), so the coefficients w e tf_k[i] and their
+    // mirror w e tf_k[14 - i] (stored reversed in the record) load as 16-byte pairs
+    static_assert(RPT % 2 == 0, "row pairs");
     for (int k0 = 0; k0 < ((t.v2_skip & 4) ? 0 : nsys); k0 += 2) {
 #pragma unroll
         for (int kk = 0; kk < 2; kk++) {
@@ -564,18 +567,23 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
             if (k < nsys) {
                 const double* rec = tab + V2_WSZ + k * V2_REC;
                 const double gl = hl[k * TP + tau], gr = hl[k * TP + tau + 1];    // g_k,τ-1 and g_k,τ
+                const double wk = rec[V2_WK];
+                const double2* wf2 = reinterpret_cast<const double2*>(rec + 16 + q * RPT);
+                const double2* wr2 = reinterpret_cast<const double2*>(rec + V2_WREV + q * RPT);
                 double* a = kk ? acc2 : acc;
 #pragma unroll
-                for (int u = 0; u < RPT; u++) {
-                    const int i = q + Q * u;
-                    if (i < V2_L - 1) a[u] = fma(-gl, rec[16 + i], fma(-gr, rec[16 + V2_L - 2 - i], a[u]));
-                    else a[u] = fma(rec[V2_WK], gr, a[u]);
+                for (int v = 0; v < RPT / 2; v++) {
+                    const double2 f = wf2[v], r2 = wr2[v];
+                    const int i = q * RPT + 2 * v;
+                    a[2 * v] = fma(-gl, f.x, fma(-gr, r2.x, a[2 * v]));
+                    a[2 * v + 1] = (i + 1 < V2_L - 1) ? fma(-gl, f.y, fma(-gr, r2.y, a[2 * v + 1]))
+                                                      : fma(wk, gr, a[2 * v + 1]);        // separator row
                 }
             }
         }
     }
 #pragma unroll
-    for (int u = 0; u < RPT; u++) Z[(q + Q * u) * (T + 1) + tau] = acc[u] + acc2[u];
+    for (int u = 0; u < RPT; u++) Z[(q * RPT + u) * (T + 1) + tau] = acc[u] + acc2[u];
     __syncthreads();
     if (dbg && threadIdx.x == 0) dbg[9] = dbg[10] = clock64();
 }
