@@ -28,6 +28,62 @@ static const long double PI_L = 3.141592653589793238462643383279502884L;
         if (_r != ncclSuccess) return set_error(DD_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));   \
     } while (0)
 
+// Chebyshev semi-iteration tables for systems a A + b M of the face pair (reading A12'):
+// preconditioned by P = T_{a α + b m̃} (the sine-diagonal part), every eigenvalue of P^-1 (a A + b M)
+// lies in 1 ± δ with δ = sup_θ |b (m - m̃)| / (a α + b m̃) — a bound on the Rayleigh quotient of
+// these two-level Toeplitz matrices by the ratio of their stencil symbols
+//   α = 4 - 2c1 - 2c2,  m = (h²/12)(6 + 2c1 + 2c2 + 2cos(θ1 + θ2)),  m̃ = (h²/12)(6 + 2c1 + 2c2 + 2c1c2)
+// (m - m̃ = -(h²/6) s1 s2; for a = 0 the sup is (√3 - 1)/2).  δ from a 1024² grid of θ in [0, π]²,
+// widened by 2 %; step count K = ceil(ln(2 √κ / ε) / ln(1/q)), q = (√κ - 1)/(√κ + 1),
+// κ = (1 + δ)/(1 - δ): an energy-norm reduction of ε; coefficients of x += d, r -= A d,
+// d = c1[k] d + c2[k] P^-1 r (centre 1, half-width δ).
+static void build_cheb(const std::vector<std::pair<double, double>>& ab, long double hh12, double eps,
+                       std::vector<double>& c1, std::vector<double>& c2, std::vector<int>& K, int& kmax_all) {
+    const int ns = std::max(1, (int)ab.size());
+    c1.assign((size_t)ns * CHEB_KMAX, 0.0);
+    c2.assign((size_t)ns * CHEB_KMAX, 0.0);
+    K.assign(ns, 0);
+    kmax_all = 0;
+    const int G = 1024;
+    std::vector<long double> cs(G + 1), sn(G + 1);
+    for (int i = 0; i <= G; i++) {
+        const long double t = 3.141592653589793238462643383279502884L * i / G;
+        cs[i] = cosl(t);
+        sn[i] = sinl(t);
+    }
+    for (size_t k = 0; k < ab.size(); k++) {
+        const long double a = ab[k].first, b = ab[k].second;
+        long double dmax = 0.0L;
+        for (int i = 0; i <= G; i++)
+            for (int j = 0; j <= G; j++) {
+                const long double den = a * (4.0L - 2.0L * cs[i] - 2.0L * cs[j]) +
+                                        b * hh12 * (6.0L + 2.0L * cs[i] + 2.0L * cs[j] + 2.0L * cs[i] * cs[j]);
+                if (den <= 0.0L) continue;
+                const long double v = 2.0L * b * hh12 * sn[i] * sn[j] / den;
+                if (v > dmax) dmax = v;
+            }
+        const long double d = std::min(0.999L, dmax * 1.02L);
+        int steps = 1;
+        if (d > 1e-300L) {
+            const long double kap = (1.0L + d) / (1.0L - d), sq = sqrtl(kap);
+            const long double qf = (sq - 1.0L) / (sq + 1.0L);
+            steps = qf > 0.0L ? (int)ceill(logl(2.0L * sq / (long double)eps) / logl(1.0L / qf)) : 1;
+        }
+        steps = std::max(1, std::min(CHEB_KMAX, steps));
+        K[k] = steps;
+        kmax_all = std::max(kmax_all, steps);
+        // ρ_0 = 1/σ = δ (θ = 1), ρ_{j+1} = 1/(2σ - ρ_j); c1 = ρ_{j+1} ρ_j, c2 = 2 ρ_{j+1}/δ
+        const long double dd = std::max(d, 1e-300L), sig = 1.0L / dd;
+        long double rho = dd;
+        for (int j = 0; j < steps; j++) {
+            const long double rn = 1.0L / (2.0L * sig - rho);
+            c1[k * CHEB_KMAX + j] = (double)(rn * rho);
+            c2[k * CHEB_KMAX + j] = (double)(2.0L * rn / dd);
+            rho = rn;
+        }
+    }
+}
+
 dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const double* poles, const double* residues,
                    const double* c0, const dd_dist* dist) {
     (void)K; (void)mu_inv;
@@ -259,6 +315,22 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
     DD_CK(cudaMemcpyAsync(f.cs, cs.data(), ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     DD_CK(cudaMemcpyAsync(f.dg, dg.data(), dg.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     DD_CK(cudaMemcpyAsync(f.idg, idg.data(), idg.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    {
+        const char* icg = std::getenv("DD_INNER_CG");
+        f.inner_cheb = !(icg && icg[0] == '1');
+        std::vector<std::pair<double, double>> ab;
+        for (int i = 0; i < f.nsys; i++) ab.emplace_back(sa[i], sb[i]);
+        std::vector<double> c1, c2;
+        std::vector<int> K;
+        build_cheb(ab, hh12, f.inner_rtol, c1, c2, K, f.kmax_all);
+        DD_CK(dalloc(c, &f.cc1, c1.size()));
+        DD_CK(dalloc(c, &f.cc2, c2.size()));
+        DD_CK(dalloc(c, &f.kmax, K.size()));
+        DD_CK(cudaMemcpyAsync(f.cc1, c1.data(), c1.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(f.cc2, c2.data(), c2.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(f.kmax, K.data(), K.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaStreamSynchronize(c->stream));
+    }
 
     // --- RA mode: the r_F systems (fc0 M + Σ_k fc_k (A - fp_k M)^-1 ≈ L^t) in the same sine-domain form
     if (c->frac_mode == DD_FRAC_RA) {
@@ -294,6 +366,17 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
         DD_CK(cudaMemcpyAsync(F.cs, fcs.data(), nf * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         DD_CK(cudaMemcpyAsync(F.dg, fdg.data(), fdg.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         DD_CK(cudaMemcpyAsync(F.idg, fidg.data(), fidg.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        std::vector<std::pair<double, double>> fab;
+        for (int i = 0; i < F.nsys; i++) fab.emplace_back(fa[i], fb[i]);
+        std::vector<double> c1, c2;
+        std::vector<int> K;
+        build_cheb(fab, hh12, f.inner_rtol, c1, c2, K, F.kmax_all);
+        DD_CK(dalloc(c, &F.cc1, c1.size()));
+        DD_CK(dalloc(c, &F.cc2, c2.size()));
+        DD_CK(dalloc(c, &F.kmax, K.size()));
+        DD_CK(cudaMemcpyAsync(F.cc1, c1.data(), c1.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(F.cc2, c2.data(), c2.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(F.kmax, K.data(), K.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
         DD_CK(cudaStreamSynchronize(c->stream));
     }
 
@@ -370,18 +453,21 @@ struct InnerView {
     int* last_iters;
     int slot_act, slot_cnt;        // ints[] slots: active-pair counter, iteration counter (+2: total)
     long long* iter_launches;
+    const double *cc1, *cc2;       // Chebyshev tables (reading A12')
+    const int* kmax;
+    int kmax_all;
 };
 
 static InnerView view_P(Face3& f, dd_ctx* c) {
     return InnerView{f.nsys, f.sys_a, f.sys_b, f.sys_w, f.cs, f.dg, f.idg, f.ix, f.ir, f.ip, f.iq, f.iz, f.T1,
                      f.irho, f.irho0, f.iactive, &f.inner_exec, &f.inner_key, &f.inner_iters_on_device,
-                     &f.last_inner_iters, 1, 6, &c->inner_iter_launches};
+                     &f.last_inner_iters, 1, 6, &c->inner_iter_launches, f.cc1, f.cc2, f.kmax, f.kmax_all};
 }
 static InnerView view_F(Face3& f, dd_ctx* c) {
     FSet& s = f.fs;
     return InnerView{s.nsys, s.sys_a, s.sys_b, s.sys_w, s.cs, s.dg, s.idg, s.ix, s.ir, s.ip, s.iq, s.iz, s.T1,
                      s.irho, s.irho0, s.iactive, &s.exec, &s.key, &s.on_dev, &s.last_iters, 11, 12,
-                     &c->f_inner_iter_launches};
+                     &c->f_inner_iter_launches, s.cc1, s.cc2, s.kmax, s.kmax_all};
 }
 
 static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const double* r, double* z, double* W1,
@@ -400,13 +486,18 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
     // r̂_c = Q r_c once per column (2 slab passes)
     DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(r, W1, ncols, f.n, f.ldf, f.S, c->stream));
     DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W1, W2, ncols, f.n, f.ldf, f.S, c->stream));
-    DD_TIMED(DD_KCLASS_POLESUM, inner_init_hat(a, W2, c->stream));
+    const bool cheb = f.inner_cheb && v.cc1;
+    a.cc1 = v.cc1; a.cc2 = v.cc2; a.kmax = v.kmax; a.kstride = CHEB_KMAX; a.kiter = cnt_slot;
+    const int loop_max = cheb ? std::min(f.inner_maxit, v.kmax_all) : f.inner_maxit;
+    if (cheb) DD_TIMED(DD_KCLASS_POLESUM, inner_init_cheb(a, W2, c->stream));
+    else DD_TIMED(DD_KCLASS_POLESUM, inner_init_hat(a, W2, c->stream));
     auto body = [&](cudaStream_t st, int* n_act) -> dd_status {
-        // q̂ = dg ∘ p̂ + cs D̂ p̂ D̂^T on the active pairs, then the fused CG update
+        // q̂ = dg ∘ p̂ + cs D̂ p̂ D̂^T on the active pairs, then the update (Chebyshev step or fused CG)
         DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_active(v.ip, v.T1, a.npair, f.n, f.ldf, f.Dh, v.iactive, st));
         DD_TIMED(DD_KCLASS_POLESUM, face_inner_op_pass(v.T1, v.iq, v.ip, a.npair, ncols, f.n, f.ldf, f.Dh, v.dg, v.cs,
                                                        v.iactive, st));
-        DD_TIMED(DD_KCLASS_POLESUM, inner_update_hat(a, n_act, st));
+        if (cheb) DD_TIMED(DD_KCLASS_POLESUM, inner_update_cheb(a, n_act, st));
+        else DD_TIMED(DD_KCLASS_POLESUM, inner_update_hat(a, n_act, st));
         return DD_OK;
     };
     if (c->graph_ok && !c->prof) {
@@ -433,7 +524,7 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
             c->prof = false;
             const long long l0 = c->launches;
             dd_status bs = body(cap, n_act_slot);
-            cudaError_t ce = inner_cond(n_act_slot, cnt_slot, f.inner_maxit, (unsigned long long)h, cap);
+            cudaError_t ce = inner_cond(n_act_slot, cnt_slot, loop_max, (unsigned long long)h, cap);
             *v.iter_launches = c->launches - l0 + 1;
             c->launches = l0;
             c->prof = prof;
@@ -454,17 +545,19 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
         *v.on_dev = true;
     } else {
         int it = 0;
-        for (it = 1; it <= f.inner_maxit; it++) {
+        DD_CK(cudaMemsetAsync(cnt_slot, 0, sizeof(int), c->stream));
+        for (it = 1; it <= loop_max; it++) {
             DD_CK(cudaMemsetAsync(n_act_slot, 0, sizeof(int), c->stream));
             dd_status bs = body(c->stream, n_act_slot);
             if (bs != DD_OK) return bs;
-            if (it % 4 == 0 || it == f.inner_maxit) {
+            if (cheb) DD_CK(inner_tick(cnt_slot, c->stream));   // the Chebyshev step counter
+            if (it % 4 == 0 || it == loop_max) {
                 DD_CK(cudaMemcpyAsync(c->h_ints + v.slot_act, n_act_slot, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
                 DD_CK(cudaStreamSynchronize(c->stream));
                 if (c->h_ints[v.slot_act] == 0) break;
             }
         }
-        *v.last_iters = std::min(it, f.inner_maxit);
+        *v.last_iters = std::min(it, loop_max);
         *v.on_dev = false;
     }
     // ẑ_c = Σ_s w_s x̂_{s,c} (fixed system order), z_c = Q ẑ_c

@@ -54,6 +54,9 @@ struct FSet {
     int key = -1;
     bool on_dev = false;
     int last_iters = 0;
+    double *cc1 = nullptr, *cc2 = nullptr;   // Chebyshev tables (see Face3)
+    int* kmax = nullptr;
+    int kmax_all = 0;
 };
 
 struct Face3 {
@@ -85,6 +88,10 @@ struct Face3 {
     double *irho = nullptr, *irho0 = nullptr;
     int* iactive = nullptr;
     double inner_rtol = 1e-13;        // reading A12
+    bool inner_cheb = true;           // reading A12': Chebyshev semi-iteration (DD_INNER_CG=1: the CG of round 1)
+    double *cc1 = nullptr, *cc2 = nullptr;   // Chebyshev coefficients [nsys][CHEB_KMAX]
+    int* kmax = nullptr;                     // a-priori step count per system
+    int kmax_all = 0;                        // max over this rank's systems
     int inner_maxit = 400;
     int last_inner_iters = 0;
     cudaGraphExec_t inner_exec = nullptr;   // WHILE graph of the inner CG loop (key: inner_key = columns)

@@ -211,7 +211,14 @@ struct InnerArgs {
     const double* dg;             // [systems][NP] sine-diagonal part a α + b μ̃ (0 on padding)
     const double* idg;            // [systems][NP] its inverse (0 on padding)
     const double* cs;             // [systems] coefficient of D̂ v D̂^T: b h^2/24
+    // Chebyshev inner solver (reading A12'): per system the step count and the recurrence
+    // coefficients d <- c1[k] d + c2[k] P^-1 r of step k (kstride entries per system)
+    const double *cc1 = nullptr, *cc2 = nullptr;
+    const int* kmax = nullptr;
+    int kstride = 0;
+    const int* kiter = nullptr;   // device: the current step k (the loop's counter)
 };
+constexpr int CHEB_KMAX = 40;     // upper bound on the a-priori Chebyshev step counts
 struct Pcg3 {
     long long NP; int ncols;
     double *x, *r, *p, *q, *z;    // padded face vectors [ncols][NP]
@@ -278,6 +285,9 @@ cudaError_t face_slab_pass_active(const double* in, double* out, int nslab, int 
 cudaError_t face_inner_op_pass(const double* in, double* q, const double* p, int nslab, int C, int n, int ldf,
                                const double* B, const double* dg, const double* cs, const int* active, cudaStream_t st);
 cudaError_t inner_init_hat(const InnerArgs& a, const double* bh, cudaStream_t st);
+cudaError_t inner_init_cheb(const InnerArgs& a, const double* bh, cudaStream_t st);
+cudaError_t inner_tick(int* counter, cudaStream_t st);
+cudaError_t inner_update_cheb(const InnerArgs& a, int* n_active, cudaStream_t st);
 cudaError_t inner_update_hat(const InnerArgs& a, int* n_active, cudaStream_t st);
 cudaError_t inner_init(const InnerArgs& a, const double* b, cudaStream_t st);
 cudaError_t inner_cond(int* n_active, int* counter, int maxit, unsigned long long handle, cudaStream_t st);

@@ -427,14 +427,76 @@ __global__ void __cluster_dims__(NCL, 1, 1) k_inner_update_cl(InnerArgs a, int* 
         atomicAdd(n_active, 1);
     }
 }
-// inner-CG WHILE-graph condition: one more iteration while any pair is active and it < maxit
+// inner-loop WHILE-graph condition: one more iteration while any pair is active and it < maxit
+// (handle 0: the host-driven loop, counter only)
 __global__ void k_inner_cond(int* n_active, int* counter, int maxit, unsigned long long handle) {
     const int it = *counter + 1;
     *counter = it;
     counter[2] += 1;          // cumulative inner iterations (launch accounting; see dd_launch_count)
     const int na = *n_active;
     *n_active = 0;
-    cudaGraphSetConditional((cudaGraphConditionalHandle)handle, (na > 0 && it < maxit) ? 1u : 0u);
+    if (handle) cudaGraphSetConditional((cudaGraphConditionalHandle)handle, (na > 0 && it < maxit) ? 1u : 0u);
+}
+
+// ---- Chebyshev semi-iteration for the shifted face systems (reading A12'): with the rigorous
+// spectral bounds 1 -/+ δ_s of the sine-diagonal preconditioned system (centre 1), x_0 = 0,
+// r_0 = b, d_0 = P^-1 r_0 and per step k: x += d; r -= A d; d = c1[k] d + c2[k] P^-1 r.  No inner
+// products: the update is one elementwise pass and a pair stops after its a-priori step count.
+__global__ void k_inner_init_cheb(InnerArgs a, const double* __restrict__ bh) {
+    const int pq = blockIdx.y;
+    const int c = pq % a.C, s = pq / a.C;
+    const size_t off = (size_t)pq * a.NP;
+    const double* idg = a.idg + (size_t)s * a.NP;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.NP; i += (long long)gridDim.x * blockDim.x) {
+        const double r = bh[(size_t)c * a.NP + i];
+        a.r[off + i] = r;
+        a.x[off + i] = 0.0;
+        a.p[off + i] = r * idg[i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.active[pq] = a.kmax[s] > 0 ? 1 : 0;
+}
+// step k = *kiter of every pair with k < K_s:  q̂ = dg ∘ d + q̂_part;  x̂ += d;  r̂ -= q̂;  d = c1 d + c2 idg ∘ r̂
+__global__ void k_inner_update_cheb(InnerArgs a, int* n_active) {
+    const int pq = blockIdx.y;
+    const int s = pq / a.C;
+    const int k = *a.kiter;
+    const int K = a.kmax[s];
+    if (k >= K) return;                          // this pair finished (uniform across the grid row)
+    const size_t off = (size_t)pq * a.NP;
+    const double* dg = a.dg + (size_t)s * a.NP;
+    const double* idg = a.idg + (size_t)s * a.NP;
+    const double c1 = a.cc1[(size_t)s * a.kstride + k], c2 = a.cc2[(size_t)s * a.kstride + k];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.NP; i += (long long)gridDim.x * blockDim.x) {
+        const double d = a.p[off + i];
+        const double q = fma(dg[i], d, a.q[off + i]);
+        a.x[off + i] += d;
+        const double r = a.r[off + i] - q;
+        a.r[off + i] = r;
+        a.p[off + i] = fma(c1, d, c2 * (r * idg[i]));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const bool more = k + 1 < K;
+        a.active[pq] = more ? 1 : 0;             // read by the next step's operator passes
+        if (more) atomicAdd(n_active, 1);
+    }
+}
+// host-driven loop: advance the step counter (and the cumulative count) without touching the
+// active-pair counter the host polls
+__global__ void k_inner_tick(int* counter) {
+    counter[0] += 1;
+    counter[2] += 1;
+}
+cudaError_t inner_tick(int* counter, cudaStream_t st) {
+    k_inner_tick<<<1, 1, 0, st>>>(counter);
+    return cudaGetLastError();
+}
+cudaError_t inner_init_cheb(const InnerArgs& a, const double* bh, cudaStream_t st) {
+    k_inner_init_cheb<<<dim3(8, a.npair), 256, 0, st>>>(a, bh);
+    return cudaGetLastError();
+}
+cudaError_t inner_update_cheb(const InnerArgs& a, int* n_active, cudaStream_t st) {
+    k_inner_update_cheb<<<dim3(8, a.npair), 256, 0, st>>>(a, n_active);
+    return cudaGetLastError();
 }
 cudaError_t inner_cond(int* n_active, int* counter, int maxit, unsigned long long handle, cudaStream_t st) {
     k_inner_cond<<<1, 1, 0, st>>>(n_active, counter, maxit, handle);

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/x_build.log 2>&1; echo build=$?
+DD_NO_GRAPH=1 timeout 1500 python -m pytest tests/test_gpu_3d.py tests/test_gpu_r2.py -x -q -p no:cacheprovider -k "3d or cfg4" > gpurun_out/x_pytest.log 2>&1; echo pytest=$?
+tail -3 gpurun_out/x_pytest.log
+timeout 900 python bench.py --config cfg4_3d_N128 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/x_bench_cfg4.json 2> gpurun_out/x_bench_cfg4.err; echo bench4=$?
