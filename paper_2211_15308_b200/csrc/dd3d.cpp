@@ -269,6 +269,27 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
     //   Q (a A + b M) Q = diag(a α_ab + b μ̃_ab) + (b h^2/24) D̂ ⊗ D̂,
     //   α_ab = σ_a + σ_b,  μ̃_ab = (h^2/12)(6 + 2c_a + 2c_b + 2 c_a c_b),  D̂ = S D S,  (D v)_j = v_{j+1} - v_{j-1},
     // since M - M̃ = (h^2/24) D⊗D collects the (1,1)/(-1,-1) couplings minus their symmetrised part.
+    // parity order of the sine index (dd_ctx.h: Face3::Sp): 0-based a = 0, 2, 4, .. then 1, 3, ..
+    std::vector<int> perm, ipos(n);
+    for (int a = 0; a < n; a += 2) perm.push_back(a);
+    const int ne = (int)perm.size();
+    for (int a = 1; a < n; a += 2) perm.push_back(a);
+    for (int i = 0; i < n; i++) ipos[perm[i]] = i;
+    {
+        const char* nk = std::getenv("DD_NO_KPAR");
+        f.kpar = (ne % 64 == 0 && ne < f.ldf && !(nk && nk[0] == '1')) ? ne : 0;
+        std::vector<double> Sp((size_t)Srows * f.ldf, 0.0), SpT((size_t)Srows * f.ldf, 0.0);
+        for (int i = 0; i < n; i++)
+            for (int col = 0; col < n; col++) {
+                Sp[(size_t)i * f.ldf + col] = Sh[(size_t)perm[i] * f.ldf + col];
+                SpT[(size_t)col * f.ldf + i] = Sh[(size_t)perm[i] * f.ldf + col];
+            }
+        DD_CK(dalloc(c, &f.Sp, Sp.size()));
+        DD_CK(dalloc(c, &f.SpT, SpT.size()));
+        DD_CK(cudaMemcpyAsync(f.Sp, Sp.data(), Sp.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(f.SpT, SpT.data(), SpT.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaStreamSynchronize(c->stream));
+    }
     const int ns = std::max(1, f.nsys);
     std::vector<double> sa(ns, 0.0), sb(ns, 1.0), swt(ns, 0.0), cs(ns, 0.0), dg((size_t)ns * f.NP, 0.0),
         idg((size_t)ns * f.NP, 0.0);
@@ -282,8 +303,9 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
                 const long double alpha = sig[a] + sig[b];
                 const long double mut = (long double)hh12 * (6.0L + 2.0L * ca + 2.0L * cb + 2.0L * ca * cb);
                 const long double d = (long double)s.a * alpha + (long double)s.b * mut;
-                dg[(size_t)i * f.NP + (size_t)a * f.ldf + b] = (double)d;
-                idg[(size_t)i * f.NP + (size_t)a * f.ldf + b] = (double)(1.0L / d);
+                const size_t e = (size_t)ipos[a] * f.ldf + ipos[b];
+                dg[(size_t)i * f.NP + e] = (double)d;
+                idg[(size_t)i * f.NP + e] = (double)(1.0L / d);
             }
     }
     std::vector<double> Dh((size_t)Srows * f.ldf, 0.0);
@@ -298,7 +320,9 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
                     const long double dj = (j + 1 < n ? SL[(size_t)(j + 1) * n + b] : 0.0L) - (j >= 1 ? SL[(size_t)(j - 1) * n + b] : 0.0L);
                     acc += SL[(size_t)a * n + j] * dj;
                 }
-                Dh[(size_t)a * f.ldf + b] = (double)acc;
+                // parity order; D̂_ab = 0 exactly when a + b is even (Σ_j sin(j a θ) cos(j b θ) over
+                // a sum of even frequencies vanishes), stored as an exact zero
+                Dh[(size_t)ipos[a] * f.ldf + ipos[b]] = (a + b) % 2 == 0 ? 0.0 : (double)acc;
             }
     }
     DD_CK(dalloc(c, &f.Dh, Dh.size()));
@@ -353,8 +377,9 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
                     const long double alpha = sig[a] + sig[b];
                     const long double mut = (long double)hh12 * (6.0L + 2.0L * ca + 2.0L * cb + 2.0L * ca * cb);
                     const long double d = (long double)sy.a * alpha + (long double)sy.b * mut;
-                    fdg[(size_t)i * f.NP + (size_t)a * f.ldf + b] = (double)d;
-                    fidg[(size_t)i * f.NP + (size_t)a * f.ldf + b] = (double)(1.0L / d);
+                    const size_t e = (size_t)ipos[a] * f.ldf + ipos[b];
+                    fdg[(size_t)i * f.NP + e] = (double)d;
+                    fidg[(size_t)i * f.NP + e] = (double)(1.0L / d);
                 }
         }
         for (double** v : {&F.sys_a, &F.sys_b, &F.sys_w, &F.cs}) DD_CK(dalloc(c, v, nf));
@@ -483,24 +508,40 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
     a.dg = v.dg; a.idg = v.idg; a.cs = v.cs;
     int* n_act_slot = c->ints + v.slot_act;
     int* cnt_slot = c->ints + v.slot_cnt;
-    // r̂_c = Q r_c once per column (2 slab passes)
-    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(r, W1, ncols, f.n, f.ldf, f.S, c->stream));
-    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W1, W2, ncols, f.n, f.ldf, f.S, c->stream));
+    // r̂_c = Q r_c once per column (2 slab passes, into the parity-ordered sine domain)
+    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(r, W1, ncols, f.n, f.ldf, f.Sp, c->stream));
+    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W1, W2, ncols, f.n, f.ldf, f.Sp, c->stream));
     const bool cheb = f.inner_cheb && v.cc1;
     a.cc1 = v.cc1; a.cc2 = v.cc2; a.kmax = v.kmax; a.kstride = CHEB_KMAX; a.kiter = cnt_slot;
-    const int loop_max = cheb ? std::min(f.inner_maxit, v.kmax_all) : f.inner_maxit;
+    // Chebyshev: step 1 is the init (x̂_1 = P^-1 b̂), the loop runs the other K_s - 1
+    const int loop_max = cheb ? std::min(f.inner_maxit, v.kmax_all - 1) : f.inner_maxit;
     if (cheb) DD_TIMED(DD_KCLASS_POLESUM, inner_init_cheb(a, W2, c->stream));
     else DD_TIMED(DD_KCLASS_POLESUM, inner_init_hat(a, W2, c->stream));
     auto body = [&](cudaStream_t st, int* n_act) -> dd_status {
-        // q̂ = dg ∘ p̂ + cs D̂ p̂ D̂^T on the active pairs, then the update (Chebyshev step or fused CG)
-        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_active(v.ip, v.T1, a.npair, f.n, f.ldf, f.Dh, v.iactive, st));
+        if (cheb) {
+            // T = D̂ x̂ (active pairs), then r, d and x̂ in the second pass's epilogue
+            DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_active(v.ix, v.T1, a.npair, f.n, f.ldf, f.Dh, v.iactive, f.kpar,
+                                                              st));
+            DD_TIMED(DD_KCLASS_POLESUM, face_inner_cheb_pass(v.T1, a, W2, f.Dh, f.kpar, st));
+            return DD_OK;
+        }
+        // q̂ = dg ∘ p̂ + cs D̂ p̂ D̂^T on the active pairs, then the fused CG update
+        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_active(v.ip, v.T1, a.npair, f.n, f.ldf, f.Dh, v.iactive, f.kpar, st));
         DD_TIMED(DD_KCLASS_POLESUM, face_inner_op_pass(v.T1, v.iq, v.ip, a.npair, ncols, f.n, f.ldf, f.Dh, v.dg, v.cs,
-                                                       v.iactive, st));
-        if (cheb) DD_TIMED(DD_KCLASS_POLESUM, inner_update_cheb(a, n_act, st));
-        else DD_TIMED(DD_KCLASS_POLESUM, inner_update_hat(a, n_act, st));
+                                                       v.iactive, f.kpar, st));
+        DD_TIMED(DD_KCLASS_POLESUM, inner_update_hat(a, n_act, st));
         return DD_OK;
     };
-    if (c->graph_ok && !c->prof) {
+    auto cond = [&](cudaStream_t st, unsigned long long h) -> cudaError_t {
+        return cheb ? inner_cond_cheb(a, n_act_slot, cnt_slot, loop_max, h, st)
+                    : inner_cond(n_act_slot, cnt_slot, loop_max, h, st);
+    };
+    if (cheb && loop_max <= 0) {
+        // every system is done after the init step
+        DD_CK(cudaMemsetAsync(cnt_slot, 0, sizeof(int), c->stream));
+        *v.last_iters = 0;
+        *v.on_dev = false;
+    } else if (c->graph_ok && !c->prof) {
         // the whole inner loop as one conditional WHILE graph (no host round trips)
         if (!*v.exec || *v.key != ncols) {
             if (*v.exec) cudaGraphExecDestroy(*v.exec);
@@ -524,7 +565,7 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
             c->prof = false;
             const long long l0 = c->launches;
             dd_status bs = body(cap, n_act_slot);
-            cudaError_t ce = inner_cond(n_act_slot, cnt_slot, loop_max, (unsigned long long)h, cap);
+            cudaError_t ce = cond(cap, (unsigned long long)h);
             *v.iter_launches = c->launches - l0 + 1;
             c->launches = l0;
             c->prof = prof;
@@ -547,10 +588,10 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
         int it = 0;
         DD_CK(cudaMemsetAsync(cnt_slot, 0, sizeof(int), c->stream));
         for (it = 1; it <= loop_max; it++) {
-            DD_CK(cudaMemsetAsync(n_act_slot, 0, sizeof(int), c->stream));
+            if (!cheb) DD_CK(cudaMemsetAsync(n_act_slot, 0, sizeof(int), c->stream));
             dd_status bs = body(c->stream, n_act_slot);
             if (bs != DD_OK) return bs;
-            if (cheb) DD_CK(inner_tick(cnt_slot, c->stream));   // the Chebyshev step counter
+            if (cheb) DD_CK(cond(c->stream, 0ull));   // step counter, active flags, *n_active
             if (it % 4 == 0 || it == loop_max) {
                 DD_CK(cudaMemcpyAsync(c->h_ints + v.slot_act, n_act_slot, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
                 DD_CK(cudaStreamSynchronize(c->stream));
@@ -562,8 +603,8 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
     }
     // ẑ_c = Σ_s w_s x̂_{s,c} (fixed system order), z_c = Q ẑ_c
     DD_TIMED(DD_KCLASS_POLESUM, inner_combine(a, v.sys_w, v.nsys, W1, c->stream));
-    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W1, W2, ncols, f.n, f.ldf, f.S, c->stream));
-    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W2, z, ncols, f.n, f.ldf, f.S, c->stream));
+    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W1, W2, ncols, f.n, f.ldf, f.SpT, c->stream));
+    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W2, z, ncols, f.n, f.ldf, f.SpT, c->stream));
     return DD_OK;
 }
 

@@ -82,7 +82,14 @@ struct Face3 {
     std::vector<int> sys_ids;         // global system ids of this rank
     double *sys_a = nullptr, *sys_b = nullptr, *sys_w = nullptr;
     double *dg = nullptr, *idg = nullptr, *cs = nullptr;   // sine-domain diagonal / inverse [nsys][NP], D̂ coefficient [nsys]
-    double* Dh = nullptr;             // D̂ = S D S (central difference in the sine basis), like S
+    double* Dh = nullptr;             // D̂ = S D S (central difference in the sine basis) in the parity order, like S
+    // The shifted systems live in the PARITY-ORDERED sine domain: index i <-> mode perm[i], odd
+    // modes first (kpar of them), then even ones.  D̂ couples modes of opposite parity only, so in
+    // this order it is [[0, E], [E', 0]] and its slab GEMMs skip the zero half of K (kpar != 0
+    // when the block edge is 64-aligned).  Sp = P S (forward), SpT = S P^T (backward transform).
+    double* Sp = nullptr;
+    double* SpT = nullptr;
+    int kpar = 0;
     // inner PCG pairs [nsys * max_cols][NP]
     double *ix = nullptr, *ir = nullptr, *ip = nullptr, *iq = nullptr, *iz = nullptr, *T1 = nullptr, *T2 = nullptr;
     double *irho = nullptr, *irho0 = nullptr;

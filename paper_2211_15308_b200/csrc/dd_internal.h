@@ -281,13 +281,16 @@ cudaError_t face_mass_axpy(int n, int ldf, long long NP, int ncols, double hh12,
                            const double* add, double* out, cudaStream_t st);
 cudaError_t scale_transpose(const double* V, const double* w, int n2, double* out, int kp, cudaStream_t st);
 cudaError_t face_slab_pass_active(const double* in, double* out, int nslab, int n, int ldf, const double* B,
-                                  const int* active, cudaStream_t st);
+                                  const int* active, int kpar, cudaStream_t st);
 cudaError_t face_inner_op_pass(const double* in, double* q, const double* p, int nslab, int C, int n, int ldf,
-                               const double* B, const double* dg, const double* cs, const int* active, cudaStream_t st);
+                               const double* B, const double* dg, const double* cs, const int* active, int kpar,
+                               cudaStream_t st);
+cudaError_t face_inner_cheb_pass(const double* in, const InnerArgs& a, const double* bh, const double* B, int kpar,
+                                 cudaStream_t st);
 cudaError_t inner_init_hat(const InnerArgs& a, const double* bh, cudaStream_t st);
 cudaError_t inner_init_cheb(const InnerArgs& a, const double* bh, cudaStream_t st);
-cudaError_t inner_tick(int* counter, cudaStream_t st);
-cudaError_t inner_update_cheb(const InnerArgs& a, int* n_active, cudaStream_t st);
+cudaError_t inner_cond_cheb(const InnerArgs& a, int* n_active, int* counter, int maxit, unsigned long long handle,
+                            cudaStream_t st);
 cudaError_t inner_update_hat(const InnerArgs& a, int* n_active, cudaStream_t st);
 cudaError_t inner_init(const InnerArgs& a, const double* b, cudaStream_t st);
 cudaError_t inner_cond(int* n_active, int* counter, int maxit, unsigned long long handle, cudaStream_t st);

@@ -63,6 +63,11 @@ struct DgemmProblem {
     const double* alt_A = nullptr; int alt_lda = 0;
     const double* alt_B = nullptr; int alt_ldb = 0;
     int alt_K = 0;
+    // Parity-blocked B (tile kernel, S = 1 slabs; not with ntl / col_group): B = [[0, E], [E', 0]]
+    // with the block edge at kpar (a multiple of BN and BK) — a column tile below kpar only needs
+    // k in [kpar, K), one at or above it k in [0, kpar); the skipped products are exact zeros
+    // (fma(0, a, acc) == acc), so the result is bitwise that of the full K loop.  0: full K.
+    int kpar = 0;
 };
 
 // Programmatic dependent launch (no-ops when the launch did not opt in)
@@ -142,6 +147,20 @@ constexpr size_t dg_tile_smem() {
 
 // Epi: functor  __device__ void operator()(int b, int row, int col, double v) const
 // (b = batch index; row < M, col < N checked)
+//
+// Staged epilogue (tile kernel, S = 1): an Epi with `static constexpr bool kStaged = true` gets the
+// CTA tile through shared memory, transposed to column-contiguous row pairs, and is called as
+//   Blk k = epi.block(b);                       once per CTA (per-slab scalars)
+//   epi.load(b, row, col, k, ctx);              U row pairs (row, row+1) of column col ...
+//   epi.store(b, row, col, pair, k, ctx, v);    ... then their results (pair: row+1 < M)
+// so that a functor whose stores may alias its loads (in-place updates) still issues U
+// independent 16-byte loads per thread before the first store — the per-element form serialises
+// every load behind the previous element's store.  Output addresses of a row pair are
+// contiguous when the epilogue stores transposed (i = row + col * ld), as the slab passes do.
+template <class Epi, class = void>
+struct EpiStaged { static constexpr bool value = false; };
+template <class Epi>
+struct EpiStaged<Epi, decltype(void(Epi::kStaged))> { static constexpr bool value = Epi::kStaged; };
 template <class C, class Epi, int S>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem g, Epi epi) {
     extern __shared__ __align__(16) double smem[];
@@ -177,10 +196,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
     if (g.col_group && !g.ntl) resolve_group();
     int nkt, kt0;
     {
-        const int ktiles = g.K / C::BK;
+        int kb = 0, ke = g.K;
+        if (g.kpar) {
+            if (n0 + C::BN <= g.kpar) kb = g.kpar;
+            else if (n0 >= g.kpar) ke = g.kpar;
+        }
+        const int ktiles = (ke - kb) / C::BK;
         const int per = (ktiles + S - 1) / S;
-        kt0 = split * per;
-        nkt = max(0, min(per, ktiles - kt0));
+        nkt = max(0, min(per, ktiles - split * per));
+        kt0 = kb / C::BK + split * per;
     }
     if (pre_a) {
 #pragma unroll
@@ -258,7 +282,44 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) k_dgemm_tile(DgemmProblem
     dg_cp_wait<0>();
     DG_TS(1);
 
-    if constexpr (S == 1) {
+    if constexpr (S == 1 && EpiStaged<Epi>::value) {
+        constexpr int TLD = C::BM + 2;                    // smem column stride (even: 16-byte row pairs)
+        static_assert(size_t(C::BN) * TLD * sizeof(double) <= C::SMEM_PIPE, "staged epilogue tile");
+        constexpr int RP = C::BM / 2, TOT = C::BN * RP, U = 4;
+        __syncthreads();                                  // every warp is done with the pipeline ring
+        double* Ts = smem;
+#pragma unroll
+        for (int mi = 0; mi < C::MI; mi++)
+#pragma unroll
+            for (int ni = 0; ni < C::NI; ni++)
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    int row, col;
+                    dg_coord<C>((mi * C::NI + ni) * 4 + q, tid, row, col);
+                    Ts[col * TLD + row] = acc[mi][ni][q];
+                }
+        __syncthreads();
+        const auto blk = epi.block(bz);
+        for (int base = 0; base < TOT; base += C::THREADS * U) {
+            typename Epi::Ctx cx[U];
+            int rr[U], cc[U];
+            bool ok[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int e = base + u * C::THREADS + tid;
+                cc[u] = e / RP;
+                rr[u] = 2 * (e % RP);
+                ok[u] = e < TOT && m0 + rr[u] < g.M && n0 + cc[u] < g.N;
+                if (ok[u]) epi.load(bz, m0 + rr[u], n0 + cc[u], blk, cx[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (ok[u]) {
+                    const double2 v = *reinterpret_cast<const double2*>(&Ts[cc[u] * TLD + rr[u]]);
+                    epi.store(bz, m0 + rr[u], n0 + cc[u], m0 + rr[u] + 1 < g.M, blk, cx[u], v);
+                }
+        }
+    } else if constexpr (S == 1) {
 #pragma unroll
         for (int mi = 0; mi < C::MI; mi++)
 #pragma unroll

@@ -32,10 +32,20 @@ using CfgFv = DgemmCfg<256, 8, 32, 8, 1, 3, 1>;
 constexpr int OCC_FV = 1;
 
 // ------------------------------------------------------------------------------------ epilogues
-struct EpiSlabStore {          // Out[b] (col-major, ldc = ldf) = v
+struct EpiSlabStore {          // Out[b] (col-major, ldc = ldf) = v   (staged: 16-byte row-pair stores)
     double* out; long long sC; int ldf;
-    __device__ __forceinline__ void operator()(int b, int row, int col, double v) const {
+    static constexpr bool kStaged = true;
+    struct Blk {};
+    struct Ctx {};
+    __device__ __forceinline__ void operator()(int b, int row, int col, double v) const {   // split-K form
         out[(size_t)b * sC + row + (size_t)col * ldf] = v;
+    }
+    __device__ __forceinline__ Blk block(int) const { return {}; }
+    __device__ __forceinline__ void load(int, int, int, const Blk&, Ctx&) const {}
+    __device__ __forceinline__ void store(int b, int row, int col, bool pair, const Blk&, const Ctx&, double2 v) const {
+        double* o = out + (size_t)b * sC + row + (size_t)col * ldf;
+        if (pair) *reinterpret_cast<double2*>(o) = v;
+        else o[0] = v.x;
     }
 };
 struct EpiSlabScale {          // Out[b] = v * scale(b) * w[b's table][row + col ldf]
@@ -57,6 +67,49 @@ struct EpiInnerOp {            // q̂_part[b] = cs[s] v,  s = b / C: the D̂ ⊗
         const int s = b / C;
         const size_t i = row + (size_t)col * ldf;
         q[(size_t)b * NP + i] = cs[s] * v;
+    }
+};
+struct EpiInnerCheb {          // one Chebyshev step of pair b = s*C + c at element i (v = (D̂ T D̂^T)_i of x̂_j):
+    double* x; double* d; const double* bh; long long NP; int ldf, C;   // r = b̂ - dg∘x̂ - cs v;
+    const double* dg; const double* idg; const double* cs;              // d = c1[j] d + c2[j] idg∘r; x̂ += d
+    const double* c1; const double* c2; int kstride; const int* kiter;
+    static constexpr bool kStaged = true;                              // x̂, d̂ updated in place
+    struct Blk { double cs, c1, c2; size_t e0, t0, b0; };
+    struct Ctx { double2 x, d, b, g, ig; };
+    __device__ __forceinline__ void operator()(int b, int row, int col, double v) const {   // split-K form
+        const Blk k = block(b);
+        const size_t i = row + (size_t)col * ldf;
+        const double xv = x[k.e0 + i];
+        const double r = bh[k.b0 + i] - fma(dg[k.t0 + i], xv, k.cs * v);
+        const double dn = fma(k.c1, d[k.e0 + i], k.c2 * (idg[k.t0 + i] * r));
+        d[k.e0 + i] = dn;
+        x[k.e0 + i] = xv + dn;
+    }
+    __device__ __forceinline__ Blk block(int b) const {
+        const int s = b / C, c = b - s * C;
+        const int j = *kiter;
+        return Blk{cs[s], c1[(size_t)s * kstride + j], c2[(size_t)s * kstride + j], (size_t)b * NP, (size_t)s * NP,
+                   (size_t)c * NP};
+    }
+    __device__ __forceinline__ void load(int, int row, int col, const Blk& k, Ctx& cx) const {
+        const size_t i = row + (size_t)col * ldf;
+        cx.x = *reinterpret_cast<const double2*>(x + k.e0 + i);
+        cx.d = *reinterpret_cast<const double2*>(d + k.e0 + i);
+        cx.b = __ldg(reinterpret_cast<const double2*>(bh + k.b0 + i));
+        cx.g = __ldg(reinterpret_cast<const double2*>(dg + k.t0 + i));
+        cx.ig = __ldg(reinterpret_cast<const double2*>(idg + k.t0 + i));
+    }
+    __device__ __forceinline__ void store(int, int row, int col, bool pair, const Blk& k, const Ctx& cx, double2 v) const {
+        const size_t i = row + (size_t)col * ldf;
+        const double r0 = cx.b.x - fma(cx.g.x, cx.x.x, k.cs * v.x), r1 = cx.b.y - fma(cx.g.y, cx.x.y, k.cs * v.y);
+        const double d0 = fma(k.c1, cx.d.x, k.c2 * (cx.ig.x * r0)), d1 = fma(k.c1, cx.d.y, k.c2 * (cx.ig.y * r1));
+        if (pair) {
+            *reinterpret_cast<double2*>(d + k.e0 + i) = make_double2(d0, d1);
+            *reinterpret_cast<double2*>(x + k.e0 + i) = make_double2(cx.x.x + d0, cx.x.y + d1);
+        } else {
+            d[k.e0 + i] = d0;
+            x[k.e0 + i] = cx.x.x + d0;
+        }
     }
 };
 struct EpiFaceFx {             // q[c] = γ_c v + D[c]  (padded face layout; rows offset by row0 for a row shard of F)
@@ -94,25 +147,42 @@ cudaError_t face_slab_pass_scaled(const double* in, double* out, int nslab, int 
     return dgemm_launch<CfgSlab>(g, 1, EpiSlabScale{out, (long long)ldf * ldf, ldf, w, sW, group, colscale}, st);
 }
 
-// Out = (Y B^T)^T per active slab (B = D̂ for the sine-domain operator)
+// Out = (Y B^T)^T per active slab (B = D̂ for the sine-domain operator; kpar: its parity-block
+// edge, see DgemmProblem::kpar)
 cudaError_t face_slab_pass_active(const double* in, double* out, int nslab, int n, int ldf, const double* B,
-                                  const int* active, cudaStream_t st) {
+                                  const int* active, int kpar, cudaStream_t st) {
     DgemmProblem g{n, n, ldf, in, ldf, B, ldf};
     g.sA = (long long)ldf * ldf;
     g.sB = 0;
     g.batch = nslab;
     g.active = active;
+    g.kpar = kpar;
     return dgemm_launch<CfgSlab>(g, 1, EpiSlabStore{out, (long long)ldf * ldf, ldf}, st);
 }
 // second pass of q̂ = dg ∘ p̂ + cs D̂ p̂ D̂^T over active pairs
 cudaError_t face_inner_op_pass(const double* in, double* q, const double* p, int nslab, int C, int n, int ldf,
-                               const double* B, const double* dg, const double* cs, const int* active, cudaStream_t st) {
+                               const double* B, const double* dg, const double* cs, const int* active, int kpar,
+                               cudaStream_t st) {
     DgemmProblem g{n, n, ldf, in, ldf, B, ldf};
     g.sA = (long long)ldf * ldf;
     g.sB = 0;
     g.batch = nslab;
     g.active = active;
+    g.kpar = kpar;
     return dgemm_launch<CfgSlab>(g, 1, EpiInnerOp{q, p, (long long)ldf * ldf, ldf, C, dg, cs}, st);
+}
+// second pass of the Chebyshev step: the operator's D̂ ⊗ D̂ part of x̂_j, the residual and both
+// updates in the epilogue (EpiInnerCheb)
+cudaError_t face_inner_cheb_pass(const double* in, const InnerArgs& a, const double* bh, const double* B, int kpar,
+                                 cudaStream_t st) {
+    DgemmProblem g{a.n, a.n, a.ldf, in, a.ldf, B, a.ldf};
+    g.sA = a.NP;
+    g.sB = 0;
+    g.batch = a.npair;
+    g.active = a.active;
+    g.kpar = kpar;
+    return dgemm_launch<CfgSlab>(g, 1, EpiInnerCheb{a.x, a.p, bh, a.NP, a.ldf, a.C, a.dg, a.idg, a.cs, a.cc1, a.cc2,
+                                                    a.kstride, a.kiter}, st);
 }
 
 // q = γ F p + D over ncols columns (F: NP x NP row-major padded; vectors NP per column).
@@ -439,63 +509,51 @@ __global__ void k_inner_cond(int* n_active, int* counter, int maxit, unsigned lo
 }
 
 // ---- Chebyshev semi-iteration for the shifted face systems (reading A12'): with the rigorous
-// spectral bounds 1 -/+ δ_s of the sine-diagonal preconditioned system (centre 1), x_0 = 0,
-// r_0 = b, d_0 = P^-1 r_0 and per step k: x += d; r -= A d; d = c1[k] d + c2[k] P^-1 r.  No inner
-// products: the update is one elementwise pass and a pair stops after its a-priori step count.
+// spectral bounds 1 -/+ δ_s of the sine-diagonal preconditioned system (centre 1), x_0 = 0 and
+// d_0 = P^-1 b, x_1 = d_0; step j = 0.. K_s-2 (face_inner_cheb_pass):
+//   r = b - A x_{j+1},  d_{j+1} = c1[j] d_j + c2[j] P^-1 r,  x_{j+2} = x_{j+1} + d_{j+1}
+// — the three-term recurrence written with the true residual, so the state is (x̂, d̂) only and
+// K_s steps cost K_s - 1 operator applications.  No inner products: a pair stops after its
+// a-priori step count K_s.
 __global__ void k_inner_init_cheb(InnerArgs a, const double* __restrict__ bh) {
     const int pq = blockIdx.y;
     const int c = pq % a.C, s = pq / a.C;
     const size_t off = (size_t)pq * a.NP;
     const double* idg = a.idg + (size_t)s * a.NP;
+    const bool live = a.kmax[s] > 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.NP; i += (long long)gridDim.x * blockDim.x) {
-        const double r = bh[(size_t)c * a.NP + i];
-        a.r[off + i] = r;
-        a.x[off + i] = 0.0;
-        a.p[off + i] = r * idg[i];
+        const double d = live ? bh[(size_t)c * a.NP + i] * idg[i] : 0.0;
+        a.x[off + i] = d;
+        a.p[off + i] = d;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.active[pq] = a.kmax[s] > 0 ? 1 : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.active[pq] = a.kmax[s] > 1 ? 1 : 0;
 }
-// step k = *kiter of every pair with k < K_s:  q̂ = dg ∘ d + q̂_part;  x̂ += d;  r̂ -= q̂;  d = c1 d + c2 idg ∘ r̂
-__global__ void k_inner_update_cheb(InnerArgs a, int* n_active) {
-    const int pq = blockIdx.y;
-    const int s = pq / a.C;
-    const int k = *a.kiter;
-    const int K = a.kmax[s];
-    if (k >= K) return;                          // this pair finished (uniform across the grid row)
-    const size_t off = (size_t)pq * a.NP;
-    const double* dg = a.dg + (size_t)s * a.NP;
-    const double* idg = a.idg + (size_t)s * a.NP;
-    const double c1 = a.cc1[(size_t)s * a.kstride + k], c2 = a.cc2[(size_t)s * a.kstride + k];
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.NP; i += (long long)gridDim.x * blockDim.x) {
-        const double d = a.p[off + i];
-        const double q = fma(dg[i], d, a.q[off + i]);
-        a.x[off + i] += d;
-        const double r = a.r[off + i] - q;
-        a.r[off + i] = r;
-        a.p[off + i] = fma(c1, d, c2 * (r * idg[i]));
+// after step j = counter[0]: j + 1 steps done; pair q stays active while j + 3 <= K_s; the WHILE
+// graph continues while any pair is active and j + 1 < maxit (handle 0: host-driven loop, which
+// polls *n_active)
+__global__ void k_inner_cond_cheb(InnerArgs a, int* n_active, int* counter, int maxit, unsigned long long handle) {
+    const int j = counter[0] + 1;
+    int na = 0;
+    for (int pq = threadIdx.x; pq < a.npair; pq += blockDim.x) {
+        const int on = j + 1 < a.kmax[pq / a.C] ? 1 : 0;
+        a.active[pq] = on;
+        na += on;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const bool more = k + 1 < K;
-        a.active[pq] = more ? 1 : 0;             // read by the next step's operator passes
-        if (more) atomicAdd(n_active, 1);
+    na = __syncthreads_count(na > 0);
+    if (threadIdx.x == 0) {
+        counter[0] = j;
+        counter[2] += 1;       // cumulative steps (launch accounting; see dd_launch_count)
+        *n_active = na;
+        if (handle) cudaGraphSetConditional((cudaGraphConditionalHandle)handle, (na > 0 && j < maxit) ? 1u : 0u);
     }
-}
-// host-driven loop: advance the step counter (and the cumulative count) without touching the
-// active-pair counter the host polls
-__global__ void k_inner_tick(int* counter) {
-    counter[0] += 1;
-    counter[2] += 1;
-}
-cudaError_t inner_tick(int* counter, cudaStream_t st) {
-    k_inner_tick<<<1, 1, 0, st>>>(counter);
-    return cudaGetLastError();
 }
 cudaError_t inner_init_cheb(const InnerArgs& a, const double* bh, cudaStream_t st) {
     k_inner_init_cheb<<<dim3(8, a.npair), 256, 0, st>>>(a, bh);
     return cudaGetLastError();
 }
-cudaError_t inner_update_cheb(const InnerArgs& a, int* n_active, cudaStream_t st) {
-    k_inner_update_cheb<<<dim3(8, a.npair), 256, 0, st>>>(a, n_active);
+cudaError_t inner_cond_cheb(const InnerArgs& a, int* n_active, int* counter, int maxit, unsigned long long handle,
+                            cudaStream_t st) {
+    k_inner_cond_cheb<<<1, 256, 0, st>>>(a, n_active, counter, maxit, handle);
     return cudaGetLastError();
 }
 cudaError_t inner_cond(int* n_active, int* counter, int maxit, unsigned long long handle, cudaStream_t st) {

@@ -299,3 +299,31 @@ def test_row_sharded_f_emulated_ranks(lib):
         assert nonzero_ranks == world               # every rank owns rows
         assert rel_l2_cols(acc, ref) <= 1e-10, world
         assert rel_l2_cols(acc, yf) <= 1e-13, world
+
+
+# ------------------------------------------------------------------------- parity-blocked D̂ (K-half skip)
+@pytest.mark.parametrize("inner_cg", ["0", "1"])
+def test_cfg4_parity_blocked_dhat_bitwise(lib, cfg4, monkeypatch, inner_cg):
+    """In the parity-ordered sine domain D̂ = [[0, E], [E', 0]] (D̂_ab = 0 for a + b even); the slab
+    GEMMs skip the zero half of K at N = 128 (block edge 64).  The skipped products are exact zeros,
+    so P r and S x through the RA-mode Schur operator (r_F systems, same passes) must be BITWISE
+    those of the full-K loop (DD_NO_KPAR=1), for the Chebyshev and the CG inner solver."""
+    g, N, ra, B, colp = cfg4
+    K, gam = float(g["K"]), float(g["gamma"])
+    lo, hi = rafit.interval_face(N)
+    fr = rafit.fit_power(-0.5, lo, hi, 16, 0.0)
+    monkeypatch.setenv("DD_INNER_CG", inner_cg)
+    Bt = torch.as_tensor(B[:3], device="cuda")
+    out = {}
+    for nk in ("0", "1"):
+        monkeypatch.setenv("DD_NO_KPAR", nk)
+        S = lib.Solver(3, N, [(K, gam)], [ra], max_cols=3, device=0, frac=lib.Frac(mode="ra", fra=fr))
+        try:
+            out[nk] = (S.apply_precond(Bt, colp[:3]).cpu().numpy(), S.apply_schur(Bt, colp[:3]).cpu().numpy())
+        finally:
+            S.close()
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert np.array_equal(out["0"][1], out["1"][1])
+    z = out["0"][0]
+    tol = max(1e-10, 1e-15 * float(g["kappa_c"])) + 20e-13 * float(g["kappa_c"])
+    assert rel_l2_cols(z, g["z_eig"][:3]) <= tol
