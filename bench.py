@@ -527,19 +527,26 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
         ps_ms, ps_n = prof["polesum_pcg"]
         ach = bytes_fx / (g2_ms / g2_n / 1e3) / 1e9 if g2_n else None
         iters_solve = float(np.max(last)) if len(last) else 0.0
-        # inner CG (polesum_pcg class): per inner iteration and (system, column) pair the operator pass
-        # (two 127x127x127 DMMA GEMMs, D̂ V D̂^T) and the update (~7 x 8 B per face entry)
+        # inner solver (polesum_pcg class), per operator application and (system, column) pair: the
+        # two slab passes of D̂ V D̂^T with D̂ = [[0, E], [E', 0]] in the parity-ordered sine domain —
+        # n^2 outputs x n/2 nonzero terms x 2 flops each, 2 n^3 algorithmic flops — and the vector
+        # traffic: Chebyshev (default) x̂ read + T written (pass 1), T, x̂, d̂ read + x̂, d̂ written
+        # (pass 2, fused step) = 7 x 8 B per face entry; CG (DD_INNER_CG=1) 2 passes + the 3-sweep
+        # update = 16 x 8 B per entry
+        cheb = os.environ.get("DD_INNER_CG", "0") != "1"
         nsys = len(ras[0].poles) + 1
         applies = iters_solve + 1
         npair = nsys * C / (world if split else 1)
-        f_in = (inner_its or 0) * npair * (4.0 * n ** 3) * applies
-        b_in = (inner_its or 0) * npair * (56.0 * n * n) * applies
+        f_in = (inner_its or 0) * npair * (2.0 * n ** 3) * applies
+        b_in = (inner_its or 0) * npair * ((56.0 if cheb else 128.0) * n * n) * applies
         t_in = ps_ms / 1e3 / nprof if ps_n else None
         inner_roof = max(f_in / (pk["dmma"] * 1e12), b_in / (hbm * 1e9))
         classes = {"gemm_schur": {"bound": "hbm", "bytes_per_launch": bytes_fx, "share_of_step": share.get("gemm_schur"),
                                   "frac": round(ach / hbm, 4) if ach else None},
                    "polesum_pcg": {"bound": "tensor" if f_in / (pk["dmma"] * 1e12) >= b_in / (hbm * 1e9) else "hbm",
-                                   "what": "face inner CG (slab DMMA operator passes + vector updates) per solve",
+                                   "what": ("face inner Chebyshev (slab DMMA operator passes, fused step epilogue)" if cheb
+                                            else "face inner CG (slab DMMA operator passes + vector updates)") + " per solve",
+                                   "inner_solver": "chebyshev" if cheb else "cg",
                                    "inner_iterations_per_apply": inner_its, "pairs": npair,
                                    "flops_per_solve": f_in, "bytes_per_solve": b_in,
                                    "roofline_ms_per_solve": round(inner_roof * 1e3, 3),
@@ -549,7 +556,8 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
         dom = max(("gemm_schur", "polesum_pcg"), key=lambda k: prof[k][0])
         if dom == "polesum_pcg" and t_in:
             roof = {"bound": classes["polesum_pcg"]["bound"], "class": "polesum_pcg",
-                    "kernel": "3D face inner CG (sine-preconditioned, batched over (system, column) pairs)",
+                    "kernel": "3D face inner " + ("Chebyshev" if cheb else "CG") +
+                              " (sine-diagonal preconditioned, batched over (system, column) pairs)",
                     "achieved": round(f_in / t_in / 1e12, 3), "peak": pk["dmma"], "unit": "TFLOP/s",
                     "frac": classes["polesum_pcg"]["frac"], "peak_source": pk["dmma_src"]}
         else:

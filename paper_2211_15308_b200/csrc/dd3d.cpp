@@ -325,6 +325,14 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
                 Dh[(size_t)ipos[a] * f.ldf + ipos[b]] = (a + b) % 2 == 0 ? 0.0 : (double)acc;
             }
     }
+    // D̂ = S D S is antisymmetric (S symmetric, D antisymmetric): make the table exactly so, so that
+    // the fused Chebyshev step may use E = D̂[o][e] for both off-diagonal blocks (D̂[e][o] = -E^T)
+    for (int i = 0; i < n; i++)
+        for (int j2 = 0; j2 < i; j2++) Dh[(size_t)i * f.ldf + j2] = -Dh[(size_t)j2 * f.ldf + i];
+    {
+        const char* fz = std::getenv("DD_CHEB_FUSED");
+        f.cheb_fused = cheb_fused_ok(n, f.ldf) && !(fz && fz[0] == '0');
+    }
     DD_CK(dalloc(c, &f.Dh, Dh.size()));
     DD_CK(cudaMemcpyAsync(f.Dh, Dh.data(), Dh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     DD_CK(dalloc(c, &f.sys_a, ns));
@@ -477,6 +485,7 @@ struct InnerView {
     bool* on_dev;
     int* last_iters;
     int slot_act, slot_cnt;        // ints[] slots: active-pair counter, iteration counter (+2: total)
+    int slot_done;                 // ints[] slot: CTA arrival counter of the fused Chebyshev step
     long long* iter_launches;
     const double *cc1, *cc2;       // Chebyshev tables (reading A12')
     const int* kmax;
@@ -486,12 +495,12 @@ struct InnerView {
 static InnerView view_P(Face3& f, dd_ctx* c) {
     return InnerView{f.nsys, f.sys_a, f.sys_b, f.sys_w, f.cs, f.dg, f.idg, f.ix, f.ir, f.ip, f.iq, f.iz, f.T1,
                      f.irho, f.irho0, f.iactive, &f.inner_exec, &f.inner_key, &f.inner_iters_on_device,
-                     &f.last_inner_iters, 1, 6, &c->inner_iter_launches, f.cc1, f.cc2, f.kmax, f.kmax_all};
+                     &f.last_inner_iters, 1, 6, 9, &c->inner_iter_launches, f.cc1, f.cc2, f.kmax, f.kmax_all};
 }
 static InnerView view_F(Face3& f, dd_ctx* c) {
     FSet& s = f.fs;
     return InnerView{s.nsys, s.sys_a, s.sys_b, s.sys_w, s.cs, s.dg, s.idg, s.ix, s.ir, s.ip, s.iq, s.iz, s.T1,
-                     s.irho, s.irho0, s.iactive, &s.exec, &s.key, &s.on_dev, &s.last_iters, 11, 12,
+                     s.irho, s.irho0, s.iactive, &s.exec, &s.key, &s.on_dev, &s.last_iters, 11, 12, 10,
                      &c->f_inner_iter_launches, s.cc1, s.cc2, s.kmax, s.kmax_all};
 }
 
@@ -517,7 +526,12 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
     const int loop_max = cheb ? std::min(f.inner_maxit, v.kmax_all - 1) : f.inner_maxit;
     if (cheb) DD_TIMED(DD_KCLASS_POLESUM, inner_init_cheb(a, W2, c->stream));
     else DD_TIMED(DD_KCLASS_POLESUM, inner_init_hat(a, W2, c->stream));
+    // fused Chebyshev step (n_e = 64): one persistent kernel per step that also evaluates the loop
+    // condition, so it stands in the condition slot and the body is empty
+    const bool fused = cheb && f.cheb_fused;
+    if (fused) a.x1 = v.iz;
     auto body = [&](cudaStream_t st, int* n_act) -> dd_status {
+        if (fused) return DD_OK;
         if (cheb) {
             // T = D̂ x̂ (active pairs), then r, d and x̂ in the second pass's epilogue
             DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass_active(v.ix, v.T1, a.npair, f.n, f.ldf, f.Dh, v.iactive, f.kpar,
@@ -533,6 +547,8 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
         return DD_OK;
     };
     auto cond = [&](cudaStream_t st, unsigned long long h) -> cudaError_t {
+        if (fused)
+            return cheb_step_fused(a, W2, f.Dh, n_act_slot, cnt_slot, c->ints + v.slot_done, loop_max, h, c->num_sms, st);
         return cheb ? inner_cond_cheb(a, n_act_slot, cnt_slot, loop_max, h, st)
                     : inner_cond(n_act_slot, cnt_slot, loop_max, h, st);
     };
@@ -591,7 +607,7 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
             if (!cheb) DD_CK(cudaMemsetAsync(n_act_slot, 0, sizeof(int), c->stream));
             dd_status bs = body(c->stream, n_act_slot);
             if (bs != DD_OK) return bs;
-            if (cheb) DD_CK(cond(c->stream, 0ull));   // step counter, active flags, *n_active
+            if (cheb) DD_TIMED(DD_KCLASS_POLESUM, cond(c->stream, 0ull));   // (fused step +) counter, flags, *n_active
             if (it % 4 == 0 || it == loop_max) {
                 DD_CK(cudaMemcpyAsync(c->h_ints + v.slot_act, n_act_slot, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
                 DD_CK(cudaStreamSynchronize(c->stream));

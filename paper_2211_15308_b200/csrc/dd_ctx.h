@@ -90,6 +90,7 @@ struct Face3 {
     double* Sp = nullptr;
     double* SpT = nullptr;
     int kpar = 0;
+    bool cheb_fused = false;          // n_e = 64: one fused kernel per Chebyshev step (k_cheb_step)
     // inner PCG pairs [nsys * max_cols][NP]
     double *ix = nullptr, *ir = nullptr, *ip = nullptr, *iq = nullptr, *iz = nullptr, *T1 = nullptr, *T2 = nullptr;
     double *irho = nullptr, *irho0 = nullptr;

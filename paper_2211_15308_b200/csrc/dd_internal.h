@@ -217,6 +217,7 @@ struct InnerArgs {
     const int* kmax = nullptr;
     int kstride = 0;
     const int* kiter = nullptr;   // device: the current step k (the loop's counter)
+    double* x1 = nullptr;         // fused Chebyshev step: second x̂ buffer (x̂ ping-pongs x <-> x1 by step parity)
 };
 constexpr int CHEB_KMAX = 40;     // upper bound on the a-priori Chebyshev step counts
 struct Pcg3 {
@@ -289,6 +290,11 @@ cudaError_t face_inner_cheb_pass(const double* in, const InnerArgs& a, const dou
                                  cudaStream_t st);
 cudaError_t inner_init_hat(const InnerArgs& a, const double* bh, cudaStream_t st);
 cudaError_t inner_init_cheb(const InnerArgs& a, const double* bh, cudaStream_t st);
+// fused Chebyshev step (one persistent kernel per step; n_e = 64, ldf = 128 only — cheb_fused_ok):
+// V = D̂ X̂ D̂^T per (pair, 64x64 parity block), the step's epilogue, and the loop condition
+bool cheb_fused_ok(int n, int ldf);
+cudaError_t cheb_step_fused(const InnerArgs& a, const double* bh, const double* Dh, int* n_active, int* counter,
+                            int* done, int maxit, unsigned long long handle, int num_sms, cudaStream_t st);
 cudaError_t inner_cond_cheb(const InnerArgs& a, int* n_active, int* counter, int maxit, unsigned long long handle,
                             cudaStream_t st);
 cudaError_t inner_update_hat(const InnerArgs& a, int* n_active, cudaStream_t st);

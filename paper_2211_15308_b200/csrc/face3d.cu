@@ -16,6 +16,7 @@
 //   SURVEY V10), applied with the same slab transforms.  Converged pairs freeze.
 //   The weighted sum over systems runs in fixed system order; across ranks (pole split) the
 //   partial sums are added by one NCCL allreduce (row a-6, in dd_api.cpp).
+#include <algorithm>
 #include <cstdlib>
 
 #include "dd_internal.h"
@@ -547,6 +548,213 @@ __global__ void k_inner_cond_cheb(InnerArgs a, int* n_active, int* counter, int 
         if (handle) cudaGraphSetConditional((cudaGraphConditionalHandle)handle, (na > 0 && j < maxit) ? 1u : 0u);
     }
 }
+// ---- fused Chebyshev step for n_e = 64 (N = 128: ldf = 128, two 64-wide parity blocks o, e).
+// With D̂ = [[0, E], [-E^T, 0]] (antisymmetric, exact in the table) the operator's D̂ X̂ D̂^T splits
+// into four independent 64x64 blocks, each from ONE block of X̂:
+//   V_AB = L_A X̂_{Ā B̄} M_B^T,  L_o = M_o = E,  L_e = M_e = E^T,  sign -1 when A != B.
+// Work item = (pair, output block AB), 4 per pair, strided over a persistent grid of one CTA per
+// SM with warp-specialised roles (174 KB smem: E, X̂ block, Y, two V buffers):
+//   8 MMA warps   X̂ block (cp.async, the next item's streams in during GEMM 2) -> Y = L X̂ (DMMA,
+//                 K = 64) -> Y to smem -> V = Y M^T (DMMA) -> V to smem buffer t & 1;
+//   8 epilogue    per V buffer: r = b̂ - dg∘x̂ - cs V, d = c1 d + c2 idg∘r, x̂' = x̂ + d over
+//     warps       16-byte row pairs (coalesced, 4 independent loads batches per thread).
+// FULL/EMPTY named barriers (bar.arrive / bar.sync) hand the V buffers over, so item t's
+// epilogue (global-memory latency) overlaps item t+1's GEMMs (tensor pipe).  x̂ ping-pongs
+// between a.x and a.x1 by step parity (the items of one pair read each other's blocks); d̂ is
+// updated in place (read and written by its own item only).  The last CTA to finish advances
+// the step counter, the active flags and the WHILE condition.  Same arithmetic as the two-pass
+// form up to summation order.
+constexpr int CF_LD = 68;                        // smem row stride: conflict-free fragment loads
+constexpr int CF_MMA = 256, CF_EPI = 256, CF_T = CF_MMA + CF_EPI;
+constexpr int CF_NI = 2;                         // MMA warp tile 32 x 16 (2 x 4 warps over the 64x64 block)
+constexpr size_t CF_BLK = size_t(64) * CF_LD;    // doubles per 64x64 smem block
+constexpr size_t CF_SMEM = 5 * CF_BLK * sizeof(double);
+bool cheb_fused_ok(int n, int ldf) { return ldf == 128 && (n + 1) / 2 == 64; }
+
+__device__ __forceinline__ void cf_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void cf_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int NT>
+__device__ __forceinline__ void cf_load_block(double* dst, const double* src, int ldf, int tid) {
+#pragma unroll
+    for (int j = 0; j < 64 * 32 / NT; j++) {
+        const int c = tid + NT * j, row = c >> 5, ch = c & 31;
+        dg_cp_async16(dst + row * CF_LD + 2 * ch, src + (size_t)row * ldf + 2 * ch);
+    }
+}
+// C = L B over K = 64 for this warp's 32 x (8 CF_NI) sub-tile: L[i][k] = Ls[i*l1 + k*l2], B[k][j] = Bs[k*b1 + j*b2]
+__device__ __forceinline__ void cf_gemm(double (&acc)[2][CF_NI][4], const double* Ls, int l1, int l2, const double* Bs,
+                                        int b1, int b2, int wm, int wn, int gq, int tq) {
+#pragma unroll
+    for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+        for (int ni = 0; ni < CF_NI; ni++)
+#pragma unroll
+            for (int r = 0; r < 4; r++) acc[mi][ni][r] = 0.0;
+    const double* la = Ls + (wm * 32 + gq) * l1 + tq * l2;
+    const double* bb = Bs + tq * b1 + (wn * 8 * CF_NI + gq) * b2;
+#pragma unroll 4
+    for (int kk = 0; kk < 64; kk += 4) {
+        double af[2][2], bf[CF_NI];
+#pragma unroll
+        for (int mi = 0; mi < 2; mi++) {
+            af[mi][0] = la[(mi * 16) * l1 + kk * l2];
+            af[mi][1] = la[(mi * 16 + 8) * l1 + kk * l2];
+        }
+#pragma unroll
+        for (int ni = 0; ni < CF_NI; ni++) bf[ni] = bb[kk * b1 + (ni * 8) * b2];
+#pragma unroll
+        for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+            for (int ni = 0; ni < CF_NI; ni++) dg_mma(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+    }
+}
+__device__ __forceinline__ void cf_store_acc(double* Ys, const double (&acc)[2][CF_NI][4], int wm, int wn, int gq, int tq) {
+#pragma unroll
+    for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+        for (int ni = 0; ni < CF_NI; ni++) {
+            const int row = wm * 32 + mi * 16 + gq, col = wn * 8 * CF_NI + ni * 8 + 2 * tq;
+            *reinterpret_cast<double2*>(&Ys[row * CF_LD + col]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+            *reinterpret_cast<double2*>(&Ys[(row + 8) * CF_LD + col]) = make_double2(acc[mi][ni][2], acc[mi][ni][3]);
+        }
+}
+
+__global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double* __restrict__ bh,
+                                                       const double* __restrict__ Dh, int* n_active, int* counter,
+                                                       int* done, int maxit, unsigned long long handle) {
+    extern __shared__ __align__(16) double smem[];
+    double* Es = smem;
+    double* Xs = smem + CF_BLK;
+    double* Ys = smem + 2 * CF_BLK;
+    double* Vs = smem + 3 * CF_BLK;              // two buffers
+    __shared__ int last;
+    const int tid = threadIdx.x;
+    const int j = counter[0];
+    const double* xin = (j & 1) ? a.x1 : a.x;
+    double* xout = (j & 1) ? a.x : a.x1;
+    const int nitem = a.npair * 4;
+    const int ldf = a.ldf;
+    auto next = [&](int it) {
+        while (it < nitem && !a.active[it >> 2]) it += gridDim.x;
+        return it;
+    };
+    int it0 = next(blockIdx.x);
+    if (tid < CF_MMA) {
+        // ------------------------------------------------ MMA warps
+        const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+        const int wm = warp & 1, wn = warp >> 1;
+        auto xblk = [&](int item) {
+            const int q = item >> 2, A = (item >> 1) & 1, B = item & 1;
+            return xin + (size_t)q * a.NP + (size_t)(1 - A) * 64 * ldf + (1 - B) * 64;
+        };
+        cf_load_block<CF_MMA>(Es, Dh + 64, ldf, tid);        // E = D̂[o rows][e cols]
+        if (it0 < nitem) cf_load_block<CF_MMA>(Xs, xblk(it0), ldf, tid);
+        dg_cp_commit();
+        int t = 0;
+        for (int it = it0; it < nitem; t++) {
+            const int A = (it >> 1) & 1, B = it & 1;
+            dg_cp_wait<0>();
+            cf_bar_sync(1, CF_MMA);                           // X̂ block (and E) landed for every MMA warp
+            double acc[2][CF_NI][4];
+            cf_gemm(acc, Es, A ? 1 : CF_LD, A ? CF_LD : 1, Xs, CF_LD, 1, wm, wn, gq, tq);   // Y = L X̂
+            cf_bar_sync(1, CF_MMA);                           // X̂ consumed; previous GEMM 2 done with Ys
+            const int nit = next(it + gridDim.x);
+            if (nit < nitem) cf_load_block<CF_MMA>(Xs, xblk(nit), ldf, tid);
+            dg_cp_commit();
+            cf_store_acc(Ys, acc, wm, wn, gq, tq);
+            cf_bar_sync(1, CF_MMA);
+            cf_gemm(acc, Ys, CF_LD, 1, Es, B ? CF_LD : 1, B ? 1 : CF_LD, wm, wn, gq, tq);   // V = Y M^T
+            const int b = t & 1;
+            if (t >= 2) cf_bar_sync(4 + b, CF_T);             // EMPTY[b]: item t-2's epilogue is done with it
+            cf_store_acc(Vs + b * CF_BLK, acc, wm, wn, gq, tq);
+            cf_bar_arrive(2 + b, CF_T);                       // FULL[b]
+            it = nit;
+        }
+        dg_cp_wait<0>();
+    } else {
+        // ------------------------------------------------ epilogue warps
+        const int et = tid - CF_MMA;
+        int t = 0;
+        for (int it = it0; it < nitem; t++) {
+            const int q = it >> 2, A = (it >> 1) & 1, B = it & 1;
+            const int s = q / a.C, c = q - s * a.C;
+            const int nit = next(it + gridDim.x);
+            const int b = t & 1;
+            const double sg = A == B ? 1.0 : -1.0;
+            const double cs = sg * a.cs[s], c1 = a.cc1[(size_t)s * a.kstride + j], c2 = a.cc2[(size_t)s * a.kstride + j];
+            const size_t e0 = (size_t)q * a.NP, t0 = (size_t)s * a.NP, b0 = (size_t)c * a.NP;
+            const size_t base = (size_t)A * 64 * ldf + B * 64;
+            const double* V = Vs + b * CF_BLK;
+            cf_bar_sync(2 + b, CF_T);                         // FULL[b]
+#pragma unroll 1
+            for (int bb = 0; bb < 64 * 32 / CF_EPI; bb += 4) {
+                double2 xv[4], dv[4], bv[4], gv[4], iv[4];
+                size_t idx[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
+                    idx[u] = base + (size_t)row * ldf + 2 * cp;
+                    xv[u] = *reinterpret_cast<const double2*>(xin + e0 + idx[u]);
+                    dv[u] = *reinterpret_cast<const double2*>(a.p + e0 + idx[u]);
+                    bv[u] = __ldg(reinterpret_cast<const double2*>(bh + b0 + idx[u]));
+                    gv[u] = __ldg(reinterpret_cast<const double2*>(a.dg + t0 + idx[u]));
+                    iv[u] = __ldg(reinterpret_cast<const double2*>(a.idg + t0 + idx[u]));
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
+                    const double2 v = *reinterpret_cast<const double2*>(&V[row * CF_LD + 2 * cp]);
+                    const double r0 = bv[u].x - fma(gv[u].x, xv[u].x, cs * v.x);
+                    const double r1 = bv[u].y - fma(gv[u].y, xv[u].y, cs * v.y);
+                    const double d0 = fma(c1, dv[u].x, c2 * (iv[u].x * r0));
+                    const double d1 = fma(c1, dv[u].y, c2 * (iv[u].y * r1));
+                    *reinterpret_cast<double2*>(a.p + e0 + idx[u]) = make_double2(d0, d1);
+                    *reinterpret_cast<double2*>(xout + e0 + idx[u]) = make_double2(xv[u].x + d0, xv[u].y + d1);
+                }
+            }
+            // EMPTY[b] — only when the MMA warps will wait for it (their item t+2 exists)
+            if (nit < nitem && next(nit + gridDim.x) < nitem) cf_bar_arrive(4 + b, CF_T);
+            it = nit;
+        }
+    }
+    // the last CTA to finish: step counter, active flags, loop condition
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        last = atomicAdd(done, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int jn = j + 1;
+    int na = 0;
+    for (int pq = tid; pq < a.npair; pq += CF_T) {
+        const int on = jn + 1 < a.kmax[pq / a.C] ? 1 : 0;
+        a.active[pq] = on;
+        na += on;
+    }
+    na = __syncthreads_count(na > 0);
+    if (tid == 0) {
+        *done = 0;
+        counter[0] = jn;
+        counter[2] += 1;
+        *n_active = na;
+        if (handle) cudaGraphSetConditional((cudaGraphConditionalHandle)handle, (na > 0 && jn < maxit) ? 1u : 0u);
+    }
+}
+cudaError_t cheb_step_fused(const InnerArgs& a, const double* bh, const double* Dh, int* n_active, int* counter,
+                            int* done, int maxit, unsigned long long handle, int num_sms, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_cheb_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF_SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int G = std::min(num_sms, std::max(1, a.npair * 4));
+    k_cheb_step<<<G, CF_T, CF_SMEM, st>>>(a, bh, Dh, n_active, counter, done, maxit, handle);
+    return cudaGetLastError();
+}
 cudaError_t inner_init_cheb(const InnerArgs& a, const double* bh, cudaStream_t st) {
     k_inner_init_cheb<<<dim3(8, a.npair), 256, 0, st>>>(a, bh);
     return cudaGetLastError();
@@ -652,7 +860,12 @@ __global__ void k_inner_combine(InnerArgs a, const double* __restrict__ w, int n
          idx += (long long)gridDim.x * blockDim.x) {
         const long long c = idx / a.NP, i = idx % a.NP;
         double acc = 0.0;
-        for (int s = 0; s < nsys; s++) acc = fma(w[s], a.x[((size_t)s * a.C + c) * a.NP + i], acc);
+        for (int s = 0; s < nsys; s++) {
+            // fused Chebyshev: x̂ of system s after its min(K_s - 1, J) loop steps is in x1 if that is odd
+            const double* xs = a.x;
+            if (a.x1 && (max(0, min(a.kmax[s] - 1, *a.kiter)) & 1)) xs = a.x1;
+            acc = fma(w[s], xs[((size_t)s * a.C + c) * a.NP + i], acc);
+        }
         zout[idx] = acc;
     }
 }

@@ -313,6 +313,7 @@ def test_cfg4_parity_blocked_dhat_bitwise(lib, cfg4, monkeypatch, inner_cg):
     lo, hi = rafit.interval_face(N)
     fr = rafit.fit_power(-0.5, lo, hi, 16, 0.0)
     monkeypatch.setenv("DD_INNER_CG", inner_cg)
+    monkeypatch.setenv("DD_CHEB_FUSED", "0")             # the two-pass form (slab GEMMs with kpar)
     Bt = torch.as_tensor(B[:3], device="cuda")
     out = {}
     for nk in ("0", "1"):
@@ -327,3 +328,33 @@ def test_cfg4_parity_blocked_dhat_bitwise(lib, cfg4, monkeypatch, inner_cg):
     z = out["0"][0]
     tol = max(1e-10, 1e-15 * float(g["kappa_c"])) + 20e-13 * float(g["kappa_c"])
     assert rel_l2_cols(z, g["z_eig"][:3]) <= tol
+
+
+def test_cfg4_fused_chebyshev_step_matches_two_pass(lib, cfg4, monkeypatch):
+    """The fused Chebyshev step (k_cheb_step: per (pair, 64x64 parity block) V = L X̂ M^T with the
+    step's epilogue and the loop condition in one persistent kernel) against the two-pass form
+    (DD_CHEB_FUSED=0) on the same systems: same arithmetic up to summation order, so P r agrees to
+    rounding (1e-12, the Chebyshev polynomial's stable recurrence), both within the oracle
+    tolerance; in RA mode the r_F systems (S x) run through the same kernel."""
+    g, N, ra, B, colp = cfg4
+    K, gam = float(g["K"]), float(g["gamma"])
+    lo, hi = rafit.interval_face(N)
+    fr = rafit.fit_power(-0.5, lo, hi, 16, 0.0)
+    Bt = torch.as_tensor(B[:4], device="cuda")
+    out = {}
+    for fz in ("1", "0"):
+        monkeypatch.setenv("DD_CHEB_FUSED", fz)
+        S = lib.Solver(3, N, [(K, gam)], [ra], max_cols=4, device=0, frac=lib.Frac(mode="ra", fra=fr))
+        try:
+            z = S.apply_precond(Bt, colp[:4]).cpu().numpy()
+            y = S.apply_schur(Bt, colp[:4]).cpu().numpy()
+            res = S.pcg_solve(Bt, colp[:4], rtol=1e-10, maxit=200)
+            out[fz] = (z, y, res.iters.copy(), res.x.cpu().numpy())
+        finally:
+            S.close()
+    assert rel_l2_cols(out["1"][0], out["0"][0]) <= 1e-12
+    assert rel_l2_cols(out["1"][1], out["0"][1]) <= 1e-12
+    assert np.all(np.abs(out["1"][2] - out["0"][2]) <= 1)
+    assert rel_l2_cols(out["1"][3], out["0"][3]) <= 1e-9
+    tol = max(1e-10, 1e-15 * float(g["kappa_c"])) + 20e-13 * float(g["kappa_c"])
+    assert rel_l2_cols(out["1"][0], g["z_eig"][:4]) <= tol
