@@ -522,7 +522,14 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
         tkey = "gemm_schur_" + roof["schur_mode"] if dom == "gemm_schur" else dom
     else:
         hbm = pk["hbm"]
-        bytes_fx = 8.0 * cfg.n_gamma * cfg.n_gamma + 3 * 8.0 * cfg.n_gamma * C
+        # F stream: the packed-symmetric upper 128 x 128 blocks (default on one rank; DD_FX_PACKED=0 or a
+        # row-sharded multi-rank split streams the full row-major F); padded face length NP = ldf^2
+        ldf = -(-n // 16) * 16
+        NP = ldf * ldf
+        packed = os.environ.get("DD_FX_PACKED", "1") != "0" and not (split and world > 1) and NP % 128 == 0
+        nbk = NP // 128
+        f_elems = nbk * (nbk + 1) // 2 * 128 * 128 if packed else cfg.n_gamma * cfg.n_gamma
+        bytes_fx = 8.0 * f_elems + 3 * 8.0 * cfg.n_gamma * C
         g2_ms, g2_n = prof["gemm_schur"]
         ps_ms, ps_n = prof["polesum_pcg"]
         ach = bytes_fx / (g2_ms / g2_n / 1e3) / 1e9 if g2_n else None
@@ -542,6 +549,7 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
         t_in = ps_ms / 1e3 / nprof if ps_n else None
         inner_roof = max(f_in / (pk["dmma"] * 1e12), b_in / (hbm * 1e9))
         classes = {"gemm_schur": {"bound": "hbm", "bytes_per_launch": bytes_fx, "share_of_step": share.get("gemm_schur"),
+                                  "f_storage": "packed_symmetric" if packed else "full",
                                   "frac": round(ach / hbm, 4) if ach else None},
                    "polesum_pcg": {"bound": "tensor" if f_in / (pk["dmma"] * 1e12) >= b_in / (hbm * 1e9) else "hbm",
                                    "what": ("face inner Chebyshev (slab DMMA operator passes, fused step epilogue)" if cheb
@@ -562,7 +570,9 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
                     "frac": classes["polesum_pcg"]["frac"], "peak_source": pk["dmma_src"]}
         else:
             roof = {"bound": "hbm", "class": "gemm_schur",
-                    "kernel": "gemm_schur (gamma F x + sine back-transform, stream-K DMMA, BN=8)",
+                    "kernel": ("gemm_schur (gamma F x, packed-symmetric F: direct + transposed DMMA per stored block"
+                               " + fixed-order partial reduce)" if packed else
+                               "gemm_schur (gamma F x, full F stream, stream-K DMMA, BN=8)"),
                     "achieved": round(ach, 1) if ach else None, "peak": hbm, "unit": "GB/s",
                     "frac": round(ach / hbm, 4) if ach else None, "peak_source": pk["hbm_src"],
                     "bytes_per_launch": bytes_fx}

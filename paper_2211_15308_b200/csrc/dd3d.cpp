@@ -171,15 +171,15 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
         DD_CK(cudaMemsetAsync(dA, 0, big * sizeof(double), c->stream));
         DD_CK(scale_transpose(dM, dW, n2, dA, kp, c->stream));
         const size_t frows = (size_t)round_up((int)f.NP, 256);
-        // packed-symmetric F (row a-3 option, half the bytes and half the memory) is opt-in: at 8
-        // columns its per-block cross-warp reduction leaves it latency-bound (386 vs 391 µs per
-        // apply for the full-F stream at 83 % of HBM)
-        const char* fp = std::getenv("DD_FX_PACKED");
-        const bool packed = fx_sym_supported(f.NP) && fp && fp[0] == '1';
         // row-sharded F under a multi-rank pole split (SURVEY §8(e) option): rank ρ keeps rows
         // [r0(ρ), r0(ρ+1)) in whole 256-row tiles of the F stream; DD_FX_ROWSHARD=0 keeps all rows
         const char* rsh = std::getenv("DD_FX_ROWSHARD");
-        const bool shardF = !packed && dist && dist->world > 1 && dist->mode == DD_SHARD_POLES && !(rsh && rsh[0] == '0');
+        const bool shardF = dist && dist->world > 1 && dist->mode == DD_SHARD_POLES && !(rsh && rsh[0] == '0');
+        // otherwise the packed-symmetric F (row a-3: upper blocks only, half the bytes and half the
+        // memory; config 4: 214 + 24 µs per apply vs 386 µs for the full-F stream);
+        // DD_FX_PACKED=0 keeps the full row-major F
+        const char* fp = std::getenv("DD_FX_PACKED");
+        const bool packed = !shardF && fx_sym_supported(f.NP) && !(fp && fp[0] == '0');
         double* Ffull = nullptr;
         f.fx_r0 = 0;
         f.fx_r1 = (int)f.NP;

@@ -3,17 +3,22 @@
 //
 //   q[:, c] = γ_c F p[:, c] + D[:, c]       (8 columns per grid row y; padded face layout, NP rows)
 //
-// Storage: F in 128 x 128 blocks (NB = NP/128 block rows), only blocks (I, J) with I <= J, block
-// index b(I, J) = I NB - I(I-1)/2 + (J - I); a block is 8 slabs of 128 rows x 16 columns, each
-// slab row-major and contiguous (16 KB), so the whole packed matrix is one sequential stream.
-// One pass reads every stored block once and uses it twice:
-//   direct      y_I += F_IJ x_J          (all 8 warps, 16 rows each, 4 m16n8k4 DMMA per slab)
-//   transposed  y_J += F_IJ^T x_I  (I<J) (every warp its 16 block rows as the K-range, 4 DMMA
-//               per slab; the 8 warp partials summed in fixed order once per block)
-// Each block's two 128 x 8 contributions go to partial buffers; k_fx_sym_reduce sums, for block
-// row I, D_{I,J} (J = I..NB-1) then T_{J',I} (J' = 0..I-1) in that fixed order and applies the
-// epilogue — bitwise reproducible.  Bytes: 8 NP^2/2 (F) + 2 x 8 KB per block per 8 columns
-// (partials, written once, read once) instead of 8 NP^2.
+// Storage: F in 128 x 128 blocks (NB = NP/128 block rows), only blocks (I, J) with I <= J in
+// row-major block order b(I, J) = I NB - I(I-1)/2 + (J - I); a block is two half-blocks of 64 rows
+// x 128 columns, each row-major and contiguous (64 KB), so the packed matrix is one sequential
+// stream.  CTA g of a one-per-SM grid takes blocks [g nb/G, (g+1) nb/G) and streams their halves
+// through a 3-deep cp.async ring (XOR-swizzled rows: conflict-free fragment loads without
+// padding).  Every stored block is used twice, by warps with fixed roles:
+//   direct      y_I += F_IJ x_J       warps 0-3: 16 block rows of each half, K = 128 columns;
+//               accumulated in registers across the CTA's blocks of one block row
+//   transposed  y_J += F_IJ^T x_I     warps 4-7: 32 block columns, K = the half's 64 rows,
+//     (I < J)   summed over both halves in registers — no cross-warp reduction
+// (x_I, x_J slices staged in smem per block with the ring).
+// (32 MMAs per warp per half either way).  Outputs: one direct partial per (block row, CTA
+// segment) and one transposed partial per off-diagonal block; k_fx_sym_reduce sums, for block row
+// I, the direct segments then T_{J',I} (J' = 0..I-1) in that fixed order and applies the
+// epilogue — bitwise reproducible.  Bytes: 8 NP^2/2 (F) + 8 KB per off-diagonal block per 8
+// columns (partials, written once, read once) instead of 8 NP^2.
 #include <algorithm>
 #include <vector>
 
@@ -22,13 +27,11 @@
 namespace dd {
 
 namespace {
-constexpr int BT = 128, SLAB = 32, NSLAB = BT / SLAB, LDSL = SLAB + 4, STAGES = 3, THREADS = 256;
-constexpr int MT = SLAB / 16;                 // 16-row output tiles of the transposed product per slab
-constexpr int SLAB_ELEMS = BT * SLAB;         // 4096 doubles = 32 KB
+constexpr int BT = 128, HR = 64, STAGES = 3, THREADS = 256;
+constexpr int HALF = HR * BT;                 // 8192 doubles = 64 KB
 constexpr int BLOCK_ELEMS = BT * BT;          // 16384 doubles
-constexpr int XS = 2 * 8 * BT;                 // one block's x_I and x_J slices: [I|J][col][row]
-constexpr int RED = (THREADS / 32) * NSLAB * SLAB * 8;   // per-warp transposed partials of one block
-constexpr size_t SMEM = ((size_t)STAGES * BT * LDSL + RED + 2 * XS) * sizeof(double);
+constexpr int XLD = BT + 4;                   // x-slice row stride (conflict-free fragment loads)
+constexpr size_t SMEM = ((size_t)STAGES * HALF + 2 * 2 * 8 * XLD) * sizeof(double);
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -39,162 +42,167 @@ __device__ __forceinline__ void mma(double (&c)[4], double a0, double a1, double
                  : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
                  : "d"(a0), "d"(a1), "d"(b));
 }
+// swizzled smem index of half-block element (r, c): the column's bits 2-3 XOR the row's bits 0-1
+__device__ __forceinline__ int swz(int r, int c) { return r * BT + (c ^ ((r & 3) << 2)); }
+__host__ __device__ __forceinline__ int seg_b0(int g, int nb, int G) { return (int)((long long)g * nb / G); }
 }  // namespace
 
 __global__ void __launch_bounds__(THREADS, 1)
     k_fx_sym(const double* __restrict__ Fp, const int2* __restrict__ blk, int nblocks, long long NP,
              const double* __restrict__ x, int ncols, double* __restrict__ Dpart, double* __restrict__ Tpart) {
     extern __shared__ __align__(16) double sm[];
-    double* red = sm + (size_t)STAGES * BT * LDSL;          // [warp][slab][n][m]: transposed partials
-    double* xs = red + RED;                                  // [block parity][I|J][col][row], cp.async-staged
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
     const int cg = blockIdx.y;                               // group of 8 columns
-    const int b0 = (int)((long long)blockIdx.x * nblocks / gridDim.x);
-    const int b1 = (int)((long long)(blockIdx.x + 1) * nblocks / gridDim.x);
-    const long long u0 = (long long)b0 * NSLAB, u1 = (long long)b1 * NSLAB;
-    const int col = cg * 8 + gq;                             // this lane's B-fragment column
-    const bool colok = col < ncols;
-    const double* xc = x + (size_t)(colok ? col : 0) * NP;
+    const int b0 = seg_b0(blockIdx.x, nblocks, gridDim.x), b1 = seg_b0(blockIdx.x + 1, nblocks, gridDim.x);
+    const long long u0 = 2LL * b0, u1 = 2LL * b1;            // half-block units
     const size_t pstride = (size_t)nblocks * BT * 8;          // partial buffers per column group
     double* Dp = Dpart + (size_t)cg * pstride;
     double* Tp = Tpart + (size_t)cg * pstride;
+    const bool direct = warp < 4;
+    const int w4 = warp & 3;
 
-    auto load_slab = [&](long long u) {
-        const double* src = Fp + (size_t)u * SLAB_ELEMS;
-        double* dst = sm + (size_t)((u - u0) % STAGES) * BT * LDSL;
+    // x slices of block b: [b & 1][I | J][n][k] (zero columns past ncols), staged with the ring
+    double* xs = sm + (size_t)STAGES * HALF;
+    auto load_x = [&](int b) {                               // 2 x 8 x 128 doubles, 4 chunks per thread
+        const int2 IJ = blk[b];
 #pragma unroll
-        for (int j = 0; j < SLAB_ELEMS / 2 / THREADS; j++) {   // 16-byte chunks
-            const int ch = tid + j * THREADS;
-            const int r = ch / (SLAB / 2), k2 = (ch % (SLAB / 2)) * 2;
-            cp16(dst + r * LDSL + k2, src + (size_t)r * SLAB + k2);
+        for (int j = 0; j < 2 * 8 * BT / 2 / THREADS; j++) {
+            const int ch = tid + j * THREADS, which = ch >> 9, n = (ch >> 6) & 7, k2 = (ch & 63) * 2;
+            double* dst = xs + (((size_t)(b & 1) * 2 + which) * 8 + n) * XLD + k2;
+            if (cg * 8 + n < ncols)
+                cp16(dst, x + (size_t)(cg * 8 + n) * NP + (size_t)(which ? IJ.y : IJ.x) * BT + k2);
+            else
+                dst[0] = dst[1] = 0.0;
         }
     };
-    // x slices of block b (rows of block row I and block column J, 8 columns) -> xs[b & 1], issued
-    // one block ahead inside the slab ring's commit groups (ready when the block's first slab is)
-    auto load_x = [&](int b) {
-        const int2 IJ = blk[b];
-        double* dst = xs + (size_t)(b & 1) * XS;
+    auto load_half = [&](long long u) {
+        const double* src = Fp + (size_t)u * HALF;
+        double* dst = sm + (size_t)((u - u0) % STAGES) * HALF;
 #pragma unroll
-        for (int j = 0; j < XS / 2 / THREADS; j++) {            // 16-byte chunks: 4 per thread
+        for (int j = 0; j < HALF / 2 / THREADS; j++) {       // 16-byte chunks
             const int ch = tid + j * THREADS;
-            const int which = ch >> 9, c = (ch >> 6) & 7, r2 = (ch & 63) * 2;
-            const int cc = cg * 8 + c < ncols ? cg * 8 + c : 0;
-            const size_t row = (size_t)(which ? IJ.y : IJ.x) * BT + r2;
-            cp16(dst + which * 8 * BT + c * BT + r2, x + (size_t)cc * NP + row);
+            const int r = ch >> 6, c2 = (ch & 63) * 2;
+            cp16(dst + swz(r, c2), src + (size_t)r * BT + c2);
         }
     };
 #pragma unroll
     for (int s = 0; s < STAGES - 1; s++) {
-        if (u0 + s < u1) load_slab(u0 + s);
+        if (u0 + s < u1) load_half(u0 + s);
         if (s == 0 && b0 < b1) load_x(b0);
         asm volatile("cp.async.commit_group;\n" ::);
     }
-    for (int b = b0; b < b1; b++) {
-        const int2 IJ = blk[b];
-        const bool offdiag = IJ.x != IJ.y;
-        double bI[4], bJ[NSLAB][SLAB / 4];
-        double* xb = xs + (size_t)(b & 1) * XS;
-        double accD[4] = {0.0, 0.0, 0.0, 0.0};
-        double accT[NSLAB][MT][4];
+    double acc[2][4];                // direct: [half] row-run accumulators; transposed: [mt] block outputs
 #pragma unroll
-        for (int s = 0; s < NSLAB; s++) {
-            const long long u = (long long)b * NSLAB + s;
+    for (int h = 0; h < 2; h++) acc[h][0] = acc[h][1] = acc[h][2] = acc[h][3] = 0.0;
+    int seg_first = b0;              // first block of the current direct segment
+    const int NB = (int)(NP / BT);
+    int2 IJ = b0 < b1 ? blk[b0] : make_int2(0, 0);           // then walked arithmetically (row-major upper blocks)
+    int slot = 0;                                            // ring slot of the current half
+    double bx[32];                                           // the B fragments of this block (x_J or x_I)
+    for (int b = b0; b < b1; b++) {
+        const bool offdiag = IJ.x != IJ.y;
+        if (!direct) {
+#pragma unroll
+            for (int m = 0; m < 2; m++) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.0;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const long long u = 2LL * b + h;
             asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 2));
             __syncthreads();
-            if (u + STAGES - 1 < u1) load_slab(u + STAGES - 1);
-            if (s == 0 && b + 1 < b1) load_x(b + 1);      // completes with slab u + 5 <= next block's slab 0
+            if (u + STAGES - 1 < u1) load_half(u + STAGES - 1);
+            if (h == 0 && b + 1 < b1) load_x(b + 1);          // lands with half 2(b+1), awaited at block b+1
             asm volatile("cp.async.commit_group;\n" ::);
-            if (s == 0) {
-                // this block's x fragments from the staged slices (zero for columns >= ncols)
+            const double* S = sm + (size_t)slot * HALF;
+            slot = slot + 1 == STAGES ? 0 : slot + 1;
+            if (h == 0) {                                     // this block's B fragments from the staged slices
+                const double* xr = xs + (((size_t)(b & 1) * 2 + (direct ? 1 : 0)) * 8 + gq) * XLD + tq;
 #pragma unroll
-                for (int j = 0; j < 4; j++) bI[j] = colok ? xb[gq * BT + warp * 16 + 4 * j + tq] : 0.0;
-#pragma unroll
-                for (int s2 = 0; s2 < NSLAB; s2++)
-#pragma unroll
-                    for (int j = 0; j < SLAB / 4; j++)
-                        bJ[s2][j] = colok ? xb[8 * BT + gq * BT + s2 * SLAB + 4 * j + tq] : 0.0;
+                for (int k = 0; k < 32; k++) bx[k] = xr[4 * k];
             }
-            const double* S = sm + (size_t)((u - u0) % STAGES) * BT * LDSL;
-            // direct: rows 16 warp .. +16 of the block, K = this slab's 16 columns (block column J)
-            const double* a = S + (warp * 16 + gq) * LDSL + tq;
+            if (direct) {
+                // rows 16 w4 + gq (+8) of this half, K = the block's 128 columns
+                const int r = 16 * w4 + gq;
 #pragma unroll
-            for (int kk = 0; kk < SLAB; kk += 4) mma(accD, a[kk], a[8 * LDSL + kk], bJ[s][kk / 4]);
-            // transposed: outputs = the slab's 16 columns (rows J*128 + 16 s + m of y), K = this warp's
-            // 16 block rows (At[m][k] = S[16 warp + k][m]); partial over the warp's K-range
+                for (int kk = 0; kk < BT; kk += 4) mma(acc[h], S[swz(r, kk + tq)], S[swz(r + 8, kk + tq)], bx[kk / 4]);
+            } else if (offdiag) {
+                // outputs: block columns 32 w4 + 16 mt + gq (+8); K = this half's 64 rows
 #pragma unroll
-            for (int mt = 0; mt < MT; mt++) {
-                accT[s][mt][0] = accT[s][mt][1] = accT[s][mt][2] = accT[s][mt][3] = 0.0;
-                if (offdiag) {
-                    const double* at = S + (warp * 16 + tq) * LDSL + mt * 16 + gq;
+                for (int mt = 0; mt < 2; mt++) {
+                    const int m = 32 * w4 + 16 * mt + gq;
 #pragma unroll
-                    for (int j = 0; j < 4; j++) mma(accT[s][mt], at[4 * j * LDSL], at[4 * j * LDSL + 8], bI[j]);
+                    for (int kk = 0; kk < HR; kk += 4)
+                        mma(acc[mt], S[swz(kk + tq, m)], S[swz(kk + tq, m + 8)], bx[(h * HR + kk) / 4]);
                 }
             }
         }
-        // direct partial of block (I, J): rows (16 warp + gq | + 8), columns (2 tq | 2 tq + 1)
-        {
-            double* d = Dp + (size_t)b * BT * 8;
-            const int r = warp * 16 + gq;
-            d[(2 * tq) * BT + r] = accD[0];
-            d[(2 * tq + 1) * BT + r] = accD[1];
-            d[(2 * tq) * BT + r + 8] = accD[2];
-            d[(2 * tq + 1) * BT + r + 8] = accD[3];
-        }
-        if (offdiag) {
-            // sum the 8 warps' K-range partials in fixed warp order
-            // red[warp][n][row of the block's column range] (8 x 128 per warp)
+        if (direct) {
+            // end of this CTA's run of block row I: write the segment's partial (slot = its first block)
+            const bool row_end = b + 1 == b1 || IJ.y + 1 == NB;
+            if (row_end) {
+                double* d = Dp + (size_t)seg_first * BT * 8;
 #pragma unroll
-            for (int s = 0; s < NSLAB; s++)
-#pragma unroll
-                for (int mt = 0; mt < MT; mt++) {
-                    double* rw = red + (size_t)warp * 8 * BT + s * SLAB + mt * 16;
-                    rw[(2 * tq) * BT + gq] = accT[s][mt][0];
-                    rw[(2 * tq + 1) * BT + gq] = accT[s][mt][1];
-                    rw[(2 * tq) * BT + gq + 8] = accT[s][mt][2];
-                    rw[(2 * tq + 1) * BT + gq + 8] = accT[s][mt][3];
+                for (int h = 0; h < 2; h++) {
+                    const int r = h * HR + 16 * w4 + gq;
+                    d[(2 * tq) * BT + r] = acc[h][0];
+                    d[(2 * tq + 1) * BT + r] = acc[h][1];
+                    d[(2 * tq) * BT + r + 8] = acc[h][2];
+                    d[(2 * tq + 1) * BT + r + 8] = acc[h][3];
+                    acc[h][0] = acc[h][1] = acc[h][2] = acc[h][3] = 0.0;
                 }
-            __syncthreads();
-            double* t = Tp + (size_t)b * BT * 8;
+                seg_first = b + 1;
+            }
+        } else if (offdiag) {
+            double* t = Tp + (size_t)b * BT * 8;              // Tp[b][n][row of block column J]
 #pragma unroll
-            for (int j = 0; j < 8 * BT / THREADS; j++) {
-                const int o = tid + j * THREADS;           // output index n * 128 + row
-                double v = 0.0;
-#pragma unroll
-                for (int w = 0; w < THREADS / 32; w++) v += red[(size_t)w * 8 * BT + o];
-                t[o] = v;                                  // Tp[b][n][row]
+            for (int mt = 0; mt < 2; mt++) {
+                const int m = 32 * w4 + 16 * mt + gq;
+                t[(2 * tq) * BT + m] = acc[mt][0];
+                t[(2 * tq + 1) * BT + m] = acc[mt][1];
+                t[(2 * tq) * BT + m + 8] = acc[mt][2];
+                t[(2 * tq + 1) * BT + m + 8] = acc[mt][3];
             }
         }
+        if (++IJ.y == NB) { IJ.x++; IJ.y = IJ.x; }
     }
     asm volatile("cp.async.wait_all;\n" ::);
 }
 
-// q[row + c NP] = γ_c (Σ_{J>=I} D_{I,J} + Σ_{J'<I} T_{J',I})[row, c] + Dd[row + c NP]
-// One CTA per (block row I, column group): RCH chunks of the NB contributions (D_{I,I..NB-1} then
-// T_{0..I-1,I}, in that order) are summed by RCH thread groups in parallel, each in its own fixed
-// order, then the chunk sums in chunk order — a fixed tree, bitwise reproducible.
-constexpr int RCH = 4, RTH = 128;             // chunks x threads per chunk; 8 outputs per thread
+// q[row + c NP] = γ_c (Σ_segments D + Σ_{J'<I} T_{J',I})[row, c] + Dd[row + c NP]
+// One CTA per (block row I, column group, half of the 1024 outputs): the contributions of block row I — its direct segment
+// partials (CTA order) then T_{0..I-1,I} — are split into RCH chunks summed by RCH thread groups in
+// parallel, each in its own fixed order, then the chunk sums in chunk order: a fixed tree,
+// bitwise reproducible.
+constexpr int RCH = 8, RTH = 64, ROUT = 2;    // chunks x threads per chunk (8 outputs each) x output halves
 __global__ void __launch_bounds__(RCH * RTH)
-    k_fx_sym_reduce(const double* __restrict__ Dpart, const double* __restrict__ Tpart, int NB, int nblocks,
+    k_fx_sym_reduce(const double* __restrict__ Dpart, const double* __restrict__ Tpart, int NB, int nblocks, int G,
                     long long NP, int ncols, const int* __restrict__ col_param, int n_param,
                     const double* __restrict__ gp, const double* __restrict__ Dd, double* __restrict__ q) {
     __shared__ double4 part[RCH - 1][RTH][2];
     const int I = blockIdx.x, cg = blockIdx.y;
     const int ch = threadIdx.x / RTH, t = threadIdx.x % RTH;
-    const int o0 = t * 8;                     // outputs o0..o0+7 of the 1024 = [n][row] of this block row
+    const int o0 = (blockIdx.z * RTH + t) * 8; // outputs o0..o0+7 of the 1024 = [n][row] of this block row
     const size_t pstride = (size_t)nblocks * BT * 8;
     const double* Dp = Dpart + (size_t)cg * pstride;
     const double* Tp = Tpart + (size_t)cg * pstride;
-    const long long rowbase = (long long)I * NB - (long long)I * (I - 1) / 2;
-    // contribution j in [0, NB): j < NB - I -> D_{I, I + j};  else T_{j - (NB - I), I}
-    const int per = (NB + RCH - 1) / RCH, j0 = ch * per, j1 = min(NB, j0 + per);
+    const int rb = (int)((long long)I * NB - (long long)I * (I - 1) / 2), re = rb + (NB - I);
+    // the CTAs whose block ranges meet [rb, re): g_first .. g_last
+    int g0 = (int)((long long)rb * G / nblocks);
+    while (g0 > 0 && seg_b0(g0, nblocks, G) > rb) g0--;
+    while (g0 + 1 < G && seg_b0(g0 + 1, nblocks, G) <= rb) g0++;
+    int nseg = 0;
+    for (int g = g0; g < G && seg_b0(g, nblocks, G) < re; g++) nseg++;
+    const int ncon = nseg + I;
+    // contribution j: j < nseg -> direct segment of CTA g0 + j;  else T_{j - nseg, I}
+    const int per = (ncon + RCH - 1) / RCH, j0 = ch * per, j1 = min(ncon, j0 + per);
     double4 a = make_double4(0, 0, 0, 0), b = make_double4(0, 0, 0, 0);
-#pragma unroll 4
     for (int j = j0; j < j1; j++) {
         const double* src;
-        if (j < NB - I) {
-            src = Dp + (size_t)(rowbase + j) * BT * 8;
+        if (j < nseg) {
+            const int slot = max(rb, seg_b0(g0 + j, nblocks, G));
+            src = Dp + (size_t)slot * BT * 8;
         } else {
-            const int J = j - (NB - I);
+            const int J = j - nseg;
             src = Tp + (size_t)((long long)J * NB - (long long)J * (J - 1) / 2 + (I - J)) * BT * 8;
         }
         const double4 v0 = *reinterpret_cast<const double4*>(src + o0);
@@ -223,15 +231,15 @@ __global__ void __launch_bounds__(RCH * RTH)
     for (int k = 0; k < 8; k++) q[o + k] = fma(g, y[k], Dd[o + k]);
 }
 
-// full row-major NP x NP F -> packed upper blocks
+// full row-major NP x NP F -> packed upper blocks (row-major 128 x 128 each: two 64-row halves)
 __global__ void k_fx_pack(const double* __restrict__ F, long long NP, const int2* __restrict__ blk, int nblocks,
                           double* __restrict__ Fp) {
     const size_t total = (size_t)nblocks * BLOCK_ELEMS;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
         const size_t b = idx / BLOCK_ELEMS, e = idx % BLOCK_ELEMS;
-        const int s = (int)(e / SLAB_ELEMS), r = (int)((e % SLAB_ELEMS) / SLAB), k = (int)(e % SLAB);
+        const int r = (int)(e / BT), k = (int)(e % BT);
         const int2 IJ = blk[b];
-        Fp[idx] = F[((size_t)IJ.x * BT + r) * NP + (size_t)IJ.y * BT + s * SLAB + k];
+        Fp[idx] = F[((size_t)IJ.x * BT + r) * NP + (size_t)IJ.y * BT + k];
     }
 }
 
@@ -272,7 +280,8 @@ cudaError_t fx_sym_apply(const double* Fp, const int* blk, long long NP, const d
     k_fx_sym<<<dim3(G, ncg), THREADS, SMEM, st>>>(Fp, reinterpret_cast<const int2*>(blk), nb, NP, p, ncols, Dpart, Tpart);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_fx_sym_reduce<<<dim3(NB, ncg), RCH * RTH, 0, st>>>(Dpart, Tpart, NB, nb, NP, ncols, col_param, n_param, gp, D, q);
+    k_fx_sym_reduce<<<dim3(NB, ncg, ROUT), RCH * RTH, 0, st>>>(Dpart, Tpart, NB, nb, G, NP, ncols, col_param, n_param, gp, D,
+                                                          q);
     return cudaGetLastError();
 }
 
