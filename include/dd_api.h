@@ -148,6 +148,9 @@ dd_status dd_apply_schur(dd_ctx* ctx, int ncols, const int* col_param, const dou
 /*
  * dd_apply_precond — z = P r per column with the column's RA (Eq.(8)),
  * shifted solves summed in the fixed order: M term, then poles in the given order.
+ * 2D handles solve the 1D shifted systems directly (tridiagonal, long-double tables); 3D handles
+ * solve the face systems iteratively to a 1e-13 relative accuracy (reading A12':
+ * Chebyshev semi-iteration with a-priori spectral bounds), so 3D P is exact up to that.
  */
 dd_status dd_apply_precond(dd_ctx* ctx, int ncols, const int* col_param, const double* r, double* z);
 
@@ -214,7 +217,9 @@ const char* dd_last_error(void);
 
 /* 128-byte ncclUniqueId for dd_dist (rank 0 calls it and broadcasts the bytes). */
 dd_status dd_nccl_unique_id(void* out128);
-/* 3D handles: inner (shifted face system) CG iterations of the last preconditioner apply. */
+/* 3D handles: inner iterations of the last preconditioner apply — the shifted face systems'
+ * operator applications (Chebyshev default: max_s K_s - 1, the first step being P^-1 b; with
+ * DD_INNER_CG=1 the inner CG iterations). */
 dd_status dd_inner_iterations(const dd_ctx* ctx, int* iters);
 
 /* 2D handles: how dd_apply_schur and the PCG apply S = K_c S_unit + γ_c F (
