@@ -496,58 +496,75 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
     }
     __syncthreads();
     if (dbg && threadIdx.x == 0) dbg[7] = clock64();
-    // ---- phase B: separators of system k by one warp.  The warp keeps the antisymmetric
-    // period-2T extension explicitly in a halo buffer hb[σ + T], σ in [-T, 2T]: every value v_σ is
-    // stored with its mirrors -v at -σ and 2T - σ (v_0 = v_2T = 0 are written once), so the PCR
-    // reads σ ± s with no index arithmetic; read, __syncwarp, write, __syncwarp per step.
+    // ---- phase B: separators of up to NSI systems per warp, interleaved (independent chains:
+    // the PCR is latency-bound, so a warp advances its systems' steps together).  Each system's
+    // values live in its own hl row (positions 0..T, v_0 = v_T = 0); the antisymmetric period-2T
+    // extension is read through the reflection x -> -x (x < 0), 2T - x (x > T) with the sign
+    // flipped — no halo buffer; read, __syncwarp, write, __syncwarp per step.
     {
         const int warp = tid >> 5, lane = tid & 31;
-        constexpr int NWB = T >= 256 ? (NW < 4 ? NW : 4) : (NW < 8 ? NW : 8);
-        if (warp < NWB) {
-            double* hb = yf + (size_t)t.max_sys * TP + (size_t)warp * (3 * T + 1);
-            if (lane == 0) { hb[T] = 0.0; hb[3 * T] = 0.0; }      // v_0 and v_2T (read by σ = T at s = T)
-            for (int k = warp; k < ((t.v2_skip & 2) ? 0 : nsys); k += NWB) {
-                const double* rec = tab + V2_WSZ + k * V2_REC;
-                const double e = rec[V2_E];
-                double* A = hl + k * TP;
-                const double* B = yf + k * TP;
-                double rs[S];
+        constexpr int NSI = 3;
+        for (int k0 = warp; k0 < ((t.v2_skip & 2) ? 0 : nsys); k0 += NW * NSI) {
+            double rs[NSI][S];
+            double* A[NSI];
 #pragma unroll
-                for (int sl = 0; sl < S; sl++) {
-                    const int sg = 32 * sl + lane + 1;         // separator σ = τ + 1 in 1..T (σ = T: boundary)
-                    rs[sl] = sg < T ? fma(-e, B[sg], A[sg - 1]) : 0.0;
+            for (int i = 0; i < NSI; i++) {
+                const int k = k0 + i * NW;
+                A[i] = hl + (size_t)(k < nsys ? k : 0) * TP;
+                if (k < nsys) {
+                    const double e = tab[V2_WSZ + k * V2_REC + V2_E];
+                    const double* B = yf + k * TP;
+#pragma unroll
+                    for (int sl = 0; sl < S; sl++) {
+                        const int sg = 32 * sl + lane + 1;     // separator σ = τ + 1 in 1..T (σ = T: boundary)
+                        rs[i][sl] = sg < T ? fma(-e, B[sg], A[i][sg - 1]) : 0.0;
+                    }
                 }
-                // step 0 reads σ ± 1: no mirror is read yet
+            }
+            __syncwarp();
 #pragma unroll
-                for (int sl = 0; sl < S; sl++) hb[T + 32 * sl + lane + 1] = rs[sl];
+            for (int i = 0; i < NSI; i++)
+                if (k0 + i * NW < nsys) {
+#pragma unroll
+                    for (int sl = 0; sl < S; sl++) A[i][32 * sl + lane + 1] = rs[i][sl];   // v_T = 0 from σ = T
+                    if (lane == 0) A[i][0] = 0.0;
+                }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < JS; j++) {
+                const int st = 1 << j;
+#pragma unroll
+                for (int i = 0; i < NSI; i++) {
+                    const int k = k0 + i * NW;
+                    if (k < nsys) {
+                        const double al = tab[V2_WSZ + k * V2_REC + V2_AL + j];
+#pragma unroll
+                        for (int sl = 0; sl < S; sl++) {
+                            const int sg = 32 * sl + lane + 1;
+                            const int xl = sg - st, xr = sg + st;
+                            const double vl = xl < 0 ? -A[i][-xl] : A[i][xl];
+                            const double vr = xr > T ? -A[i][2 * T - xr] : A[i][xr];
+                            rs[i][sl] = sg < T ? fma(-al, vl + vr, rs[i][sl]) : 0.0;
+                        }
+                    }
+                }
                 __syncwarp();
 #pragma unroll
-                for (int j = 0; j < JS; j++) {
-                    const int st = 1 << j;
-                    const double al = rec[V2_AL + j];
+                for (int i = 0; i < NSI; i++)
+                    if (k0 + i * NW < nsys) {
 #pragma unroll
-                    for (int sl = 0; sl < S; sl++) {
-                        const int sg = 32 * sl + lane + 1;
-                        rs[sl] = sg < T ? fma(-al, hb[T + sg - st] + hb[T + sg + st], rs[sl]) : 0.0;
+                        for (int sl = 0; sl < S; sl++) A[i][32 * sl + lane + 1] = rs[i][sl];
                     }
-                    __syncwarp();
-                    // the next step (stride 2s) reads the mirror of σ only where it falls outside
-                    // [1, T - 1]: the left one for σ < 2s, the right one for σ > T - 2s (writing all
-                    // mirrors every step made this phase shared-memory-bandwidth bound)
-                    const int st2 = 2 * st;
+                __syncwarp();
+            }
 #pragma unroll
-                    for (int sl = 0; sl < S; sl++) {
-                        const int sg = 32 * sl + lane + 1;
-                        hb[T + sg] = rs[sl];
-                        if (sg < st2) hb[T - sg] = -rs[sl];
-                        if (sg > T - st2) hb[3 * T - sg] = -rs[sl];
-                    }
-                    __syncwarp();
+            for (int i = 0; i < NSI; i++) {
+                const int k = k0 + i * NW;
+                if (k < nsys) {
+                    const double dinv = tab[V2_WSZ + k * V2_REC + V2_DINV];
+#pragma unroll
+                    for (int sl = 0; sl < S; sl++) A[i][32 * sl + lane + 1] = rs[i][sl] * dinv;   // g at σ (σ = T: 0)
                 }
-                const double dinv = rec[V2_DINV];
-#pragma unroll
-                for (int sl = 0; sl < S; sl++) A[32 * sl + lane + 1] = rs[sl] * dinv;   // g at σ (σ = T: 0)
-                if (lane == 0) A[0] = 0.0;
             }
         }
     }
@@ -1194,11 +1211,9 @@ int polesum_groups(const PoleGeom& g) {
 int polesum_warps(const PoleGeom& g) { return g.G * polesum_groups(g); }
 
 static size_t polesum_v2_doubles(const PoleGeom& g, int max_sys) {
-    const int NW = polesum_warps(g);
-    const int NWB = g.T >= 256 ? std::min(NW, 4) : std::min(NW, 8);
+    (void)g;
     return (size_t)V2_WSZ + (size_t)V2_REC * max_sys        // tables
-           + 2 * (size_t)max_sys * (g.T + 1)                // hl, yf
-           + (size_t)NWB * (3 * g.T + 1);                   // phase-B halo buffers
+           + 2 * (size_t)max_sys * (g.T + 1);               // hl, yf (phase B works in the hl rows)
 }
 
 size_t polesum_smem(const PoleGeom& g, int max_sys) {
