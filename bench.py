@@ -579,14 +579,17 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
         roof["classes"] = classes
         roof["f_stream"] = {"achieved_gbs": round(ach, 1) if ach else None, "frac": round(ach / hbm, 4) if ach else None,
                             "frac_vs_nominal_8000gbs": round(ach / 8000.0, 4) if ach else None}
-        tkey = "gemm_schur" if roof["class"] == "gemm_schur" else "inner_update"
+        fkey = "gemm_schur_packed" if packed else "gemm_schur"
+        ikey = ("cheb_step" if os.environ.get("DD_CHEB_FUSED", "1") != "0" and n == 127 else "cheb_two_pass") if cheb \
+            else "inner_update"
+        tkey = fkey if roof["class"] == "gemm_schur" else ikey
         if args.frac_mode == "ra":
-            roof["note"] = "RA mode: no dense F; the face inner CG carries the step"
+            roof["note"] = "RA mode: no dense F; the face inner solver (r_F and P systems) carries the step"
     roof.update({"traffic": traffic_for(cfg.name, tkey), "traffic_key": tkey,
                  "avg_launch_us": avg_us.get(roof.get("class", "gemm_schur")),
                  "share_of_step": share, "avg_us": avg_us})
     if cfg.dim == 3:
-        roof["traffic_f_stream"] = traffic_for(cfg.name, "gemm_schur")
+        roof["traffic_f_stream"] = traffic_for(cfg.name, fkey) if args.frac_mode != "ra" else None
     if split:
         par = f"RA systems split over {world} rank(s), NCCL allreduce of the partial sums per preconditioner apply"
     elif cfg.dim == 2:
