@@ -6,14 +6,15 @@
 A "step" is one dd_pcg_solve over one batch of the workload (every column driven to rtol 1e-10):
 the whole hot path per PCG iteration — the Schur apply (2D default: ONE grouped DMMA GEMM
 Y[:, c] = H_p X[:, c] with H_p = K_p S_unit + γ_p F formed at setup; 3D: the sine slab passes + the
-F stream) and the fused kernel doing the RA pole sum, the PCG updates and the dot products.
+packed-symmetric F stream) and the RA pole sum (2D: the fused kernel doing the pole sum, the PCG
+updates and the dot products; 3D: the face systems' Chebyshev steps, then the PCG updates).
 Default workload: config 5 (2D, 2048 cells/side, the 16-point (K, μ⁻¹) Darcy sweep x 32 RHS = 512
 independent solves per step; the largest single-GPU configuration of BASELINE.json, standing in
 for the Appendix sweep).
 Multi-GPU (torchrun, one rank per GPU): 2D configs split the FIXED batch over the ranks (strong
 scaling, no data-path collective) in 32-column single-parameter blocks balanced by LPT on pilot
 iteration counts; config 4 splits the RA systems over the ranks with one NCCL allreduce per
-preconditioner apply (strong).  value = the job's solves / max-over-ranks device time.
+preconditioner apply and row-shards F with one NCCL allgather per Schur apply (strong).  value = the job's solves / max-over-ranks device time.
 `--emulate-ranks W` (one GPU) adds a PREDICTION of the W-rank value: each rank's shard run alone.
 Timing: W warm-up steps, then K steps each bracketed by CUDA events (recorded inside libdd
 on its stream), with a 512 MiB L2 flush between steps outside the timed spans; barrier +
