@@ -533,7 +533,9 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
         bytes_fx = 8.0 * f_elems + 3 * 8.0 * cfg.n_gamma * C
         g2_ms, g2_n = prof["gemm_schur"]
         ps_ms, ps_n = prof["polesum_pcg"]
-        ach = bytes_fx / (g2_ms / g2_n / 1e3) / 1e9 if g2_n else None
+        # RA mode (Remark 1) has no F stream: its gemm_schur class holds the two consistent-mass
+        # products around the r_F pole sum, not an F read — no bandwidth figure
+        ach = bytes_fx / (g2_ms / g2_n / 1e3) / 1e9 if g2_n and args.frac_mode != "ra" else None
         iters_solve = float(np.max(last)) if len(last) else 0.0
         # inner solver (polesum_pcg class), per operator application and (system, column) pair: the
         # two slab passes of D̂ V D̂^T with D̂ = [[0, E], [E', 0]] in the parity-ordered sine domain —
