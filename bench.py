@@ -551,8 +551,10 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
         b_in = (inner_its or 0) * npair * ((56.0 if cheb else 128.0) * n * n) * applies
         t_in = ps_ms / 1e3 / nprof if ps_n else None
         inner_roof = max(f_in / (pk["dmma"] * 1e12), b_in / (hbm * 1e9))
-        classes = {"gemm_schur": {"bound": "hbm", "bytes_per_launch": bytes_fx, "share_of_step": share.get("gemm_schur"),
-                                  "f_storage": "packed_symmetric" if packed else "full",
+        ra_mode = args.frac_mode == "ra"
+        classes = {"gemm_schur": {"bound": "hbm", "bytes_per_launch": None if ra_mode else bytes_fx,
+                                  "share_of_step": share.get("gemm_schur"),
+                                  "f_storage": "none (RA-evaluated F)" if ra_mode else ("packed_symmetric" if packed else "full"),
                                   "frac": round(ach / hbm, 4) if ach else None},
                    "polesum_pcg": {"bound": "tensor" if f_in / (pk["dmma"] * 1e12) >= b_in / (hbm * 1e9) else "hbm",
                                    "what": ("face inner Chebyshev (slab DMMA operator passes, fused step epilogue)" if cheb

@@ -582,47 +582,53 @@ __device__ __forceinline__ void cf_load_block(double* dst, const double* src, in
         dg_cp_async16(dst + row * CF_LD + 2 * ch, src + (size_t)row * ldf + 2 * ch);
     }
 }
-// C = L B over K = 64 for this warp's 32 x (8 CF_NI) sub-tile: L[i][k] = Ls[i*l1 + k*l2], B[k][j] = Bs[k*b1 + j*b2]
-__device__ __forceinline__ void cf_gemm(double (&acc)[2][CF_NI][4], const double* Ls, int l1, int l2, const double* Bs,
+// C = L B over K = 64 for this warp's (16 MI) x (8 CF_NI) sub-tile: L[i][k] = Ls[i*l1 + k*l2], B[k][j] = Bs[k*b1 + j*b2]
+template <int MI>
+__device__ __forceinline__ void cf_gemm(double (&acc)[MI][CF_NI][4], const double* Ls, int l1, int l2, const double* Bs,
                                         int b1, int b2, int wm, int wn, int gq, int tq) {
 #pragma unroll
-    for (int mi = 0; mi < 2; mi++)
+    for (int mi = 0; mi < MI; mi++)
 #pragma unroll
         for (int ni = 0; ni < CF_NI; ni++)
 #pragma unroll
             for (int r = 0; r < 4; r++) acc[mi][ni][r] = 0.0;
-    const double* la = Ls + (wm * 32 + gq) * l1 + tq * l2;
+    const double* la = Ls + (wm * 16 * MI + gq) * l1 + tq * l2;
     const double* bb = Bs + tq * b1 + (wn * 8 * CF_NI + gq) * b2;
 #pragma unroll 4
     for (int kk = 0; kk < 64; kk += 4) {
-        double af[2][2], bf[CF_NI];
+        double af[MI][2], bf[CF_NI];
 #pragma unroll
-        for (int mi = 0; mi < 2; mi++) {
+        for (int mi = 0; mi < MI; mi++) {
             af[mi][0] = la[(mi * 16) * l1 + kk * l2];
             af[mi][1] = la[(mi * 16 + 8) * l1 + kk * l2];
         }
 #pragma unroll
         for (int ni = 0; ni < CF_NI; ni++) bf[ni] = bb[kk * b1 + (ni * 8) * b2];
 #pragma unroll
-        for (int mi = 0; mi < 2; mi++)
+        for (int mi = 0; mi < MI; mi++)
 #pragma unroll
             for (int ni = 0; ni < CF_NI; ni++) dg_mma(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
     }
 }
-__device__ __forceinline__ void cf_store_acc(double* Ys, const double (&acc)[2][CF_NI][4], int wm, int wn, int gq, int tq) {
+template <int MI>
+__device__ __forceinline__ void cf_store_acc(double* Ys, const double (&acc)[MI][CF_NI][4], int wm, int wn, int gq, int tq) {
 #pragma unroll
-    for (int mi = 0; mi < 2; mi++)
+    for (int mi = 0; mi < MI; mi++)
 #pragma unroll
         for (int ni = 0; ni < CF_NI; ni++) {
-            const int row = wm * 32 + mi * 16 + gq, col = wn * 8 * CF_NI + ni * 8 + 2 * tq;
+            const int row = wm * 16 * MI + mi * 16 + gq, col = wn * 8 * CF_NI + ni * 8 + 2 * tq;
             *reinterpret_cast<double2*>(&Ys[row * CF_LD + col]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
             *reinterpret_cast<double2*>(&Ys[(row + 8) * CF_LD + col]) = make_double2(acc[mi][ni][2], acc[mi][ni][3]);
         }
 }
 
+// HR: output rows per work item — 64 (a whole parity block) or 32 (half a block: twice the items,
+// for batches whose pairs do not fill the SMs, e.g. the ranks of a pole split)
+template <int HR>
 __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double* __restrict__ bh,
                                                        const double* __restrict__ Dh, int* n_active, int* counter,
                                                        int* done, int maxit, unsigned long long handle) {
+    constexpr int NH = 64 / HR, IPP = 4 * NH, MI = HR / 32;      // items per block, per pair; MMA rows / 16 per warp
     extern __shared__ __align__(16) double smem[];
     double* Es = smem;
     double* Xs = smem + CF_BLK;
@@ -633,10 +639,10 @@ __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double
     const int j = counter[0];
     const double* xin = (j & 1) ? a.x1 : a.x;
     double* xout = (j & 1) ? a.x : a.x1;
-    const int nitem = a.npair * 4;
+    const int nitem = a.npair * IPP;
     const int ldf = a.ldf;
     auto next = [&](int it) {
-        while (it < nitem && !a.active[it >> 2]) it += gridDim.x;
+        while (it < nitem && !a.active[it / IPP]) it += gridDim.x;
         return it;
     };
     int it0 = next(blockIdx.x);
@@ -645,7 +651,7 @@ __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double
         const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
         const int wm = warp & 1, wn = warp >> 1;
         auto xblk = [&](int item) {
-            const int q = item >> 2, A = (item >> 1) & 1, B = item & 1;
+            const int q = item / IPP, blk = (item / NH) & 3, A = blk >> 1, B = blk & 1;
             return xin + (size_t)q * a.NP + (size_t)(1 - A) * 64 * ldf + (1 - B) * 64;
         };
         cf_load_block<CF_MMA>(Es, Dh + 64, ldf, tid);        // E = D̂[o rows][e cols]
@@ -653,21 +659,22 @@ __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double
         dg_cp_commit();
         int t = 0;
         for (int it = it0; it < nitem; t++) {
-            const int A = (it >> 1) & 1, B = it & 1;
+            const int blk = (it / NH) & 3, A = blk >> 1, B = blk & 1, h = it % NH;
             dg_cp_wait<0>();
             cf_bar_sync(1, CF_MMA);                           // X̂ block (and E) landed for every MMA warp
-            double acc[2][CF_NI][4];
-            cf_gemm(acc, Es, A ? 1 : CF_LD, A ? CF_LD : 1, Xs, CF_LD, 1, wm, wn, gq, tq);   // Y = L X̂
+            double acc[MI][CF_NI][4];
+            // Y = L X̂ for the item's HR rows of L (= E, or E^T read transposed)
+            cf_gemm<MI>(acc, Es + (A ? h * HR : h * HR * CF_LD), A ? 1 : CF_LD, A ? CF_LD : 1, Xs, CF_LD, 1, wm, wn, gq, tq);
             cf_bar_sync(1, CF_MMA);                           // X̂ consumed; previous GEMM 2 done with Ys
             const int nit = next(it + gridDim.x);
             if (nit < nitem) cf_load_block<CF_MMA>(Xs, xblk(nit), ldf, tid);
             dg_cp_commit();
-            cf_store_acc(Ys, acc, wm, wn, gq, tq);
+            cf_store_acc<MI>(Ys, acc, wm, wn, gq, tq);
             cf_bar_sync(1, CF_MMA);
-            cf_gemm(acc, Ys, CF_LD, 1, Es, B ? CF_LD : 1, B ? 1 : CF_LD, wm, wn, gq, tq);   // V = Y M^T
+            cf_gemm<MI>(acc, Ys, CF_LD, 1, Es, B ? CF_LD : 1, B ? 1 : CF_LD, wm, wn, gq, tq);   // V = Y M^T
             const int b = t & 1;
             if (t >= 2) cf_bar_sync(4 + b, CF_T);             // EMPTY[b]: item t-2's epilogue is done with it
-            cf_store_acc(Vs + b * CF_BLK, acc, wm, wn, gq, tq);
+            cf_store_acc<MI>(Vs + b * CF_BLK, acc, wm, wn, gq, tq);
             cf_bar_arrive(2 + b, CF_T);                       // FULL[b]
             it = nit;
         }
@@ -677,18 +684,18 @@ __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double
         const int et = tid - CF_MMA;
         int t = 0;
         for (int it = it0; it < nitem; t++) {
-            const int q = it >> 2, A = (it >> 1) & 1, B = it & 1;
+            const int q = it / IPP, blk = (it / NH) & 3, A = blk >> 1, B = blk & 1, h = it % NH;
             const int s = q / a.C, c = q - s * a.C;
             const int nit = next(it + gridDim.x);
             const int b = t & 1;
             const double sg = A == B ? 1.0 : -1.0;
             const double cs = sg * a.cs[s], c1 = a.cc1[(size_t)s * a.kstride + j], c2 = a.cc2[(size_t)s * a.kstride + j];
             const size_t e0 = (size_t)q * a.NP, t0 = (size_t)s * a.NP, b0 = (size_t)c * a.NP;
-            const size_t base = (size_t)A * 64 * ldf + B * 64;
+            const size_t base = (size_t)(A * 64 + h * HR) * ldf + B * 64;
             const double* V = Vs + b * CF_BLK;
             cf_bar_sync(2 + b, CF_T);                         // FULL[b]
 #pragma unroll 1
-            for (int bb = 0; bb < 64 * 32 / CF_EPI; bb += 4) {
+            for (int bb = 0; bb < HR * 32 / CF_EPI; bb += 4) {
                 double2 xv[4], dv[4], bv[4], gv[4], iv[4];
                 size_t idx[4];
 #pragma unroll
@@ -747,12 +754,20 @@ cudaError_t cheb_step_fused(const InnerArgs& a, const double* bh, const double* 
                             int* done, int maxit, unsigned long long handle, int num_sms, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_cheb_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF_SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_cheb_step<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF_SMEM);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_cheb_step<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF_SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int G = std::min(num_sms, std::max(1, a.npair * 4));
-    k_cheb_step<<<G, CF_T, CF_SMEM, st>>>(a, bh, Dh, n_active, counter, done, maxit, handle);
+    // whole parity blocks when they give every SM two or more items; half blocks otherwise
+    if (a.npair * 4 >= 2 * num_sms) {
+        const int G = num_sms;
+        k_cheb_step<64><<<G, CF_T, CF_SMEM, st>>>(a, bh, Dh, n_active, counter, done, maxit, handle);
+    } else {
+        const int G = std::min(num_sms, std::max(1, a.npair * 8));
+        k_cheb_step<32><<<G, CF_T, CF_SMEM, st>>>(a, bh, Dh, n_active, counter, done, maxit, handle);
+    }
     return cudaGetLastError();
 }
 cudaError_t inner_init_cheb(const InnerArgs& a, const double* bh, cudaStream_t st) {

@@ -358,3 +358,29 @@ def test_cfg4_fused_chebyshev_step_matches_two_pass(lib, cfg4, monkeypatch):
     assert rel_l2_cols(out["1"][3], out["0"][3]) <= 1e-9
     tol = max(1e-10, 1e-15 * float(g["kappa_c"])) + 20e-13 * float(g["kappa_c"])
     assert rel_l2_cols(out["1"][0], g["z_eig"][:4]) <= tol
+
+
+@pytest.mark.parametrize("ncols,world", [(1, 1), (3, 1), (8, 8)])
+def test_cfg4_fused_step_small_batches(lib, cfg4, monkeypatch, ncols, world):
+    """The fused Chebyshev step with fewer work items than CTAs (1 column: 84 items for one CTA per
+    SM; 3 columns; a W = 8 pole-split rank: 3 systems x 8 columns) against the two-pass form, and
+    the summed partials of all 8 ranks against the oracle's P_RA."""
+    g, N, ra, B, colp = cfg4
+    K, gam = float(g["K"]), float(g["gamma"])
+    kc = float(g["kappa_c"])
+    Bt = torch.as_tensor(B[:ncols], device="cuda")
+    acc = np.zeros_like(B[:ncols])
+    for rank in range(world):
+        out = {}
+        for fz in ("1", "0"):
+            monkeypatch.setenv("DD_CHEB_FUSED", fz)
+            dist = (rank, world, 1, None) if world > 1 else None
+            S = lib.Solver(3, N, [(K, gam)], [ra], max_cols=ncols, device=0, dist=dist)
+            try:
+                out[fz] = S.apply_precond(Bt, colp[:ncols]).cpu().numpy()
+            finally:
+                S.close()
+        assert rel_l2_cols(out["1"], out["0"]) <= 1e-12, rank
+        acc += out["1"]
+    tol = max(1e-10, 1e-15 * kc) + 20e-13 * kc
+    assert rel_l2_cols(acc, g["z_eig"][:ncols]) <= tol
