@@ -942,55 +942,64 @@ __global__ void k3_pcg_start(Pcg3 s) {
         if (c == 0 && s.hist) s.hist[0] = eta0;
     }
 }
-// α = ρ/(p·q); x += αp; r -= αq
-__global__ void k3_pcg_alpha(Pcg3 s) {
+// The per-iteration updates on a cluster of PCL CTAs per column (a column is NP = 16384 entries at
+// config 4; one CTA per column left 8 CTAs streaming it): each CTA owns NP/PCL entries, the dots
+// are reduced over DSMEM in fixed rank order (deterministic), rank 0 writes the scalars.
+constexpr int PCL = 8;
+__global__ void __cluster_dims__(PCL, 1, 1) k3_pcg_alpha_cl(Pcg3 s) {
     __shared__ double red[32];
-    const int c = blockIdx.x;
-    if (!s.active[c]) return;
+    __shared__ double slot[1];
+    const int c = blockIdx.y, rank = blockIdx.x;
+    if (!s.active[c]) return;                    // uniform across the cluster
     const size_t off = (size_t)c * s.NP;
+    const long long chunk = (s.NP + PCL - 1) / PCL;
+    const long long i0 = rank * chunk, i1 = min(s.NP, i0 + chunk);
     double pq = 0.0;
-    for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) pq = fma(s.p[off + i], s.q[off + i], pq);
-    pq = block_sum(pq, red);
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) pq = fma(s.p[off + i], s.q[off + i], pq);
+    pq = cluster_allsum<PCL>(pq, red, &slot[0]);
     if (!(pq > 0.0)) {
-        if (threadIdx.x == 0) { atomicExch(s.status, (int)DD_ENOTSPD); s.active[c] = 0; }
+        if (rank == 0 && threadIdx.x == 0) { atomicExch(s.status, (int)DD_ENOTSPD); s.active[c] = 0; }
         return;
     }
     const double alpha = s.rho[c] / pq;
-    for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) {
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
         s.x[off + i] = fma(alpha, s.p[off + i], s.x[off + i]);
         s.r[off + i] = fma(-alpha, s.q[off + i], s.r[off + i]);
     }
 }
-// ρ' = r·z; η test; β; p = z + βp
-__global__ void k3_pcg_beta(Pcg3 s, int k, int maxit, int* n_active) {
+__global__ void __cluster_dims__(PCL, 1, 1) k3_pcg_beta_cl(Pcg3 s, int k, int maxit, int* n_active) {
     __shared__ double red[32];
-    const int c = blockIdx.x;
-    if (!s.active[c]) return;
+    __shared__ double slot[2];
+    const int c = blockIdx.y, rank = blockIdx.x;
+    if (!s.active[c]) return;                    // uniform across the cluster
     const size_t off = (size_t)c * s.NP;
-    const double rho_old = s.rho[c];             // before block_sum's barriers: thread 0 overwrites it below
+    const long long chunk = (s.NP + PCL - 1) / PCL;
+    const long long i0 = rank * chunk, i1 = min(s.NP, i0 + chunk);
+    // ρ read before the first cluster barrier: rank 0 overwrites it after the last one
+    const double rho_old = s.rho[c];
     double rz = 0.0, zz = 0.0;
-    for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) {
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
         const double zi = s.z[off + i];
         rz = fma(s.r[off + i], zi, rz);
         zz = fma(zi, zi, zz);
     }
-    rz = block_sum(rz, red);
-    zz = block_sum(zz, red);
+    rz = cluster_allsum<PCL>(rz, red, &slot[0]);
+    zz = cluster_allsum<PCL>(zz, red, &slot[1]);
     const double eta = s.norm_kind == 0 ? sqrt(fmax(rz, 0.0)) : sqrt(zz);
     const bool conv = eta <= s.rtol * s.eta0[c];
-    if (threadIdx.x == 0) {
+    if (rank == 0 && threadIdx.x == 0) {
         s.iters[c] = k;
         s.relres[c] = eta / s.eta0[c];
         if (c == 0 && s.hist) s.hist[k] = eta;
         if (rz < 0.0) atomicExch(s.status, (int)DD_ENOTSPD);
     }
     if (conv || rz < 0.0 || k >= maxit) {
-        if (threadIdx.x == 0) s.active[c] = 0;
+        if (rank == 0 && threadIdx.x == 0) s.active[c] = 0;
         return;
     }
     const double beta = rz / rho_old;
-    for (long long i = threadIdx.x; i < s.NP; i += blockDim.x) s.p[off + i] = fma(beta, s.p[off + i], s.z[off + i]);
-    if (threadIdx.x == 0) {
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) s.p[off + i] = fma(beta, s.p[off + i], s.z[off + i]);
+    if (rank == 0 && threadIdx.x == 0) {
         s.rho[c] = rz;
         atomicAdd(n_active, 1);
     }
@@ -1000,11 +1009,13 @@ cudaError_t pcg3_start(const Pcg3& s, cudaStream_t st) {
     return cudaGetLastError();
 }
 cudaError_t pcg3_alpha(const Pcg3& s, cudaStream_t st) {
-    k3_pcg_alpha<<<s.ncols, 512, 0, st>>>(s);
+    if (s.ncols <= 0) return cudaSuccess;
+    k3_pcg_alpha_cl<<<dim3(PCL, s.ncols), 256, 0, st>>>(s);
     return cudaGetLastError();
 }
 cudaError_t pcg3_beta(const Pcg3& s, int k, int maxit, int* n_active, cudaStream_t st) {
-    k3_pcg_beta<<<s.ncols, 512, 0, st>>>(s, k, maxit, n_active);
+    if (s.ncols <= 0) return cudaSuccess;
+    k3_pcg_beta_cl<<<dim3(PCL, s.ncols), 256, 0, st>>>(s, k, maxit, n_active);
     return cudaGetLastError();
 }
 
