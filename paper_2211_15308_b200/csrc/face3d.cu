@@ -131,12 +131,28 @@ struct EpiFaceScatter {        // dense n^2 x n^2 product -> padded NP x NP row-
     }
 };
 
+// split-K for small slab batches: the config-4 Schur apply transforms 8 slabs = 32 output tiles,
+// a quarter of the SMs; split the K range over a cluster so that the tiles x splits reach the SM
+// count (results: partials summed in fixed rank order over DSMEM)
+static int slab_splitk(int nslab, int n) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const long long tiles = (long long)nslab * ((n + CfgSlab::BM - 1) / CfgSlab::BM) * ((n + CfgSlab::BN - 1) / CfgSlab::BN);
+    int sk = 1;
+    while (sk < 8 && tiles * sk * 2 <= sms) sk *= 2;
+    return sk;
+}
 cudaError_t face_slab_pass(const double* in, double* out, int nslab, int n, int ldf, const double* S, cudaStream_t st) {
     DgemmProblem g{n, n, ldf, in, ldf, S, ldf};
     g.sA = (long long)ldf * ldf;
     g.sB = 0;
     g.batch = nslab;
-    return dgemm_launch<CfgSlab>(g, 1, EpiSlabStore{out, (long long)ldf * ldf, ldf}, st);
+    return dgemm_launch<CfgSlab>(g, slab_splitk(nslab, n), EpiSlabStore{out, (long long)ldf * ldf, ldf}, st);
 }
 
 cudaError_t face_slab_pass_scaled(const double* in, double* out, int nslab, int n, int ldf, const double* S,
@@ -145,7 +161,8 @@ cudaError_t face_slab_pass_scaled(const double* in, double* out, int nslab, int 
     g.sA = (long long)ldf * ldf;
     g.sB = 0;
     g.batch = nslab;
-    return dgemm_launch<CfgSlab>(g, 1, EpiSlabScale{out, (long long)ldf * ldf, ldf, w, sW, group, colscale}, st);
+    return dgemm_launch<CfgSlab>(g, slab_splitk(nslab, n), EpiSlabScale{out, (long long)ldf * ldf, ldf, w, sW, group, colscale},
+                                 st);
 }
 
 // Out = (Y B^T)^T per active slab (B = D̂ for the sine-domain operator; kpar: its parity-block
