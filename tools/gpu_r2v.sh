@@ -5,3 +5,4 @@ tail -2 gpurun_out/v_pytest.log
 for c in cfg5_2d_N2048_darcy cfg2_2d_N1024_sweep cfg3_2d_N4096; do
   timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/v_bench_$c.json 2> gpurun_out/v_bench_$c.err; echo bench $c=$?
 done
+DD_V2_SCALAR=1 timeout 900 python bench.py --config cfg5_2d_N2048_darcy --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/v_bench_scalar.json 2> gpurun_out/v_bench_scalar.err; echo bench scalar=$?
