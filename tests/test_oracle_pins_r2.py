@@ -163,3 +163,50 @@ def test_cfg4_oracle_iterations(g4):
     # the stored solution solves the stored operator's system to the PCG's accuracy: S x ≈ b is not
     # checkable without F here, but P-weighted consistency is: x has the seeded RHS's column count
     assert g4["x"].shape == B.shape and g4["y"].shape == B.shape
+
+
+# --------------------------------------------------------------------------- reading A12' (Chebyshev bounds)
+def _sine(N):
+    n = N - 1
+    j = np.arange(1, N)
+    return np.sqrt(2.0 / N) * np.sin(np.outer(j, j) * np.pi / N)
+
+
+def _symbol_delta(a, b, N, G=2048):
+    # δ = sup_θ |2 b (h²/12) s1 s2| / (a (4 - 2c1 - 2c2) + b (h²/12)(6 + 2c1 + 2c2 + 2 c1 c2)),
+    # the bound reading A12' uses (dd3d.cpp build_cheb: same expression, 1024² grid, x1.02 margin)
+    th = np.linspace(0.0, np.pi, G + 1)
+    c, s = np.cos(th), np.sin(th)
+    c1, c2, s1, s2 = c[:, None], c[None, :], s[:, None], s[None, :]
+    hh12 = 1.0 / (12.0 * N * N)
+    den = a * (4 - 2 * c1 - 2 * c2) + b * hh12 * (6 + 2 * c1 + 2 * c2 + 2 * c1 * c2)
+    return float(np.max(np.abs(2 * b * hh12 * s1 * s2) / den))
+
+
+@pytest.mark.parametrize("N", [6, 10, 16])
+def test_chebyshev_bounds_contain_the_preconditioned_spectrum(N):
+    """Reading A12': for every face system a A + b M (the RA poles' shifts and the mass term), the
+    spectrum of (a Ã + b M̃)^-1 (a A + b M) — M̃ = (S⊗S) diag(μ̃) (S⊗S) the sine-diagonal part,
+    μ̃_ab = (h²/12)(6 + 2c_a + 2c_b + 2 c_a c_b), Ã = A (exactly sine-diagonal) — lies in [1 - δ, 1 + δ]
+    with δ the stencil-symbol bound the Chebyshev coefficients are built from; checked against a
+    dense generalized eigensolve of the oracle's face pair (scipy), independent of the product."""
+    import scipy.linalg as sla
+    A, M = fem.trace_pair_face(N)
+    A, M = A.toarray(), M.toarray()
+    n = N - 1
+    S = _sine(N)
+    Q = np.kron(S, S)                                  # j-major (j, k) ordering, orthonormal, symmetric
+    c = np.cos(np.arange(1, N) * np.pi / N)
+    hh12 = 1.0 / (12.0 * N * N)
+    mu = hh12 * (6 + 2 * c[:, None] + 2 * c[None, :] + 2 * c[:, None] * c[None, :])
+    Mt = Q @ np.diag(mu.ravel()) @ Q
+    sig = 2 - 2 * c
+    At = Q @ np.diag((sig[:, None] + sig[None, :]).ravel()) @ Q
+    assert np.abs(At - A).max() <= 1e-12 * np.abs(A).max()          # A is exactly sine-diagonal
+    for a, b in [(0.0, 1.0), (1.0, 1.0), (1.0, 1e2), (1.0, 1e4), (1.0, 1e6)]:   # b = -p for a pole p < 0
+        lam = sla.eigh(a * A + b * M, a * At + b * Mt, eigvals_only=True)
+        d = _symbol_delta(a, b, N)
+        assert d < 1.0
+        assert lam.min() >= 1 - d - 1e-12 and lam.max() <= 1 + d + 1e-12, (a, b, lam.min(), lam.max(), d)
+    # the mass system's bound is the (sqrt(3) - 1)/2 of the A12' reading as h -> 0
+    assert abs(_symbol_delta(0.0, 1.0, 4096, G=4096) - (np.sqrt(3) - 1) / 2) < 1e-3
