@@ -384,3 +384,25 @@ def test_cfg4_fused_step_small_batches(lib, cfg4, monkeypatch, ncols, world):
         acc += out["1"]
     tol = max(1e-10, 1e-15 * kc) + 20e-13 * kc
     assert rel_l2_cols(acc, g["z_eig"][:ncols]) <= tol
+
+
+@pytest.mark.parametrize("cap", ["1", "4", "7"])
+def test_cfg4_fused_step_truncated_loop(lib, cfg4, monkeypatch, cap):
+    """DD_INNER_MAXIT caps the inner loop below the Chebyshev step counts (K_s - 1 = 18): the fused
+    kernel's x̂ ping-pong must hand the combine the buffer of each system's last step
+    (min(K_s - 1, J) parity) — the truncated operator equals the two-pass form's (1e-12)."""
+    g, N, ra, B, colp = cfg4
+    K, gam = float(g["K"]), float(g["gamma"])
+    Bt = torch.as_tensor(B[:2], device="cuda")
+    monkeypatch.setenv("DD_INNER_MAXIT", cap)
+    out = {}
+    for fz in ("1", "0"):
+        monkeypatch.setenv("DD_CHEB_FUSED", fz)
+        S = lib.Solver(3, N, [(K, gam)], [ra], max_cols=2, device=0)
+        try:
+            out[fz] = S.apply_precond(Bt, colp[:2]).cpu().numpy()
+            assert S.inner_iterations() == int(cap)
+        finally:
+            S.close()
+    assert rel_l2_cols(out["1"], out["0"]) <= 1e-12
+    assert np.all(np.isfinite(out["1"])) and np.linalg.norm(out["1"]) > 0
