@@ -632,7 +632,7 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
         a += __shfl_xor_sync(0xffffffffu, a, o);
         b += __shfl_xor_sync(0xffffffffu, b, o);
     }
-    __syncthreads();
+    // no leading barrier: red is used by block_sum2 only, and every call ends with one after its reads
     if (lane == 0) { red[warp] = a; red[32 + warp] = b; }
     __syncthreads();
     double sa = 0.0, sb = 0.0;
@@ -859,9 +859,12 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     const bool early = V == 1 && s.cond_handle != 0;
     double pv[RPT], qv[RPT], xv[RPT], rv[RPT];
     int work = 0, k = 0;
+    double rho_c = 0.0, eta0_c = 0.0;            // the column's ρ and η0 (written by earlier kernels only)
     auto load_pxr = [&]() {
         work = __ldcg(&s.active[c]);
         k = __ldcg(s.kiter) + 1;
+        rho_c = __ldcg(&s.rho[c]);
+        eta0_c = __ldcg(&s.eta0[c]);
         if (work) {
 #pragma unroll
             for (int j = 0; j < RPT; j++) {
@@ -901,7 +904,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
                 s.iters[c] = k;
             }
         } else {
-            const double alpha = s.rho[c] / pq;
+            const double alpha = rho_c / pq;
 #pragma unroll
             for (int j = 0; j < RPT; j++) {
                 const int i = threadIdx.x + j * NT;
@@ -936,17 +939,17 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
             const double eta = s.norm_kind == 0 ? sqrt(fmax(rz, 0.0)) : sqrt(zz);
             const bool notspd = rz < 0.0;
             flagged = notspd;
-            const bool conv = eta <= s.rtol * s.eta0[c];
+            const bool conv = eta <= s.rtol * eta0_c;
             if (threadIdx.x == 0) {
                 s.iters[c] = k;
-                s.relres[c] = eta / s.eta0[c];
+                s.relres[c] = eta / eta0_c;
                 if (c == 0 && s.hist) s.hist[k] = eta;
                 if (notspd) atomicExch(s.status, (int)DD_ENOTSPD);
             }
             if (conv || notspd || k >= s.maxit) {
                 if (threadIdx.x == 0) s.active[c] = 0;
             } else {
-                const double beta = rz / s.rho[c];
+                const double beta = rz / rho_c;
                 if constexpr (V == 0) {
                     // p as at entry, re-read (L2) rather than held in registers across the pole sum
                     // (the partitioned pole sum needs every register)
