@@ -848,7 +848,8 @@ def run_reference(args, cfg, world, rank):
     v = tot_n / tot_s
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_s / args.steps * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            # the same fixed sample whatever the launch width (rank 0 only): strong, like this arm's own line
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "solves_per_step": per * len(cfg.params)},
             "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": cores_used(), "kind": "oracle",
                              "sample": f"{per} solves per parameter set per step (of {cfg.rhs_per_param}), oracle mode tier",
