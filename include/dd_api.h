@@ -237,9 +237,10 @@ dd_status dd_inner_iterations(const dd_ctx* ctx, int* iters);
  *        DD_GROUPED_PAIR=1) the GEMM forms each tile's operator in registers from the shared pair
  *        (G, F) (2 n^2 doubles).  A call whose 32-column tiles mix parameter sets computes the
  *        assembled product instead (same result, checked on the device, no host synchronisation).
- * mode outside {0,1,2}, a 3D handle, or GROUPED in DD_FRAC_RA mode: DD_EINVAL.  (3D always applies
- * the interior solve per apply: its S_unit would be another n_Γ^2 = 2 GB stream.)  The environment
- * variable DD_SCHUR_MODE=0|1|2 sets the mode at setup. */
+ * mode outside {0,1,2}, a 3D handle, or GROUPED in DD_FRAC_RA mode: DD_EINVAL.  (3D with the dense
+ * F folds K S_unit into the packed-symmetric stream at setup, H = γ F + K S_unit — one parameter set
+ * per 3D handle; with RA-evaluated F or a pole-split row shard it applies the interior solve per
+ * apply.)  The environment variable DD_SCHUR_MODE=0|1|2 sets the mode at setup. */
 #define DD_SCHUR_FACTORED 0
 #define DD_SCHUR_ASSEMBLED 1
 #define DD_SCHUR_GROUPED 2

@@ -86,7 +86,6 @@ static void build_cheb(const std::vector<std::pair<double, double>>& ab, long do
 
 dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const double* poles, const double* residues,
                    const double* c0, const dd_dist* dist) {
-    (void)K; (void)mu_inv;
     Face3& f = c->f3;
     const int N = c->N, n = c->n;
     if (c->n_param != 1) return set_error(DD_EUNSUPPORTED, "3D handles take one parameter set");
@@ -220,6 +219,39 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
             DD_CK(fx_sym_pack(Ffull, f.NP, f.fblk, f.Fp, c->stream));
             DD_CK(dalloc(c, &f.fxD, fx_sym_partial_doubles(f.NP, c->max_cols)));
             DD_CK(dalloc(c, &f.fxT, fx_sym_partial_doubles(f.NP, c->max_cols)));
+            // fold the interior solve into the packed stream: H = γ F + K S_unit (one parameter set
+            // per 3D handle), S_unit applied to the identity columns by the same slab passes the
+            // per-apply path runs, row pad(j) of the dense F <- γ F + K S_unit e_j (symmetric)
+            const char* fo = std::getenv("DD_FX_FOLD");
+            if (!(fo && fo[0] == '0')) {
+                const int BC = 256;
+                const size_t slack_s = (size_t)64 * f.ldf;
+                double *X = nullptr, *Y1 = nullptr, *Y2 = nullptr, *Kc = nullptr;
+                DD_CK(cudaMalloc(&X, ((size_t)BC * f.NP + slack_s) * sizeof(double)));
+                DD_CK(cudaMalloc(&Y1, ((size_t)BC * f.NP + slack_s) * sizeof(double)));
+                DD_CK(cudaMalloc(&Y2, ((size_t)BC * f.NP + slack_s) * sizeof(double)));
+                DD_CK(cudaMalloc(&Kc, BC * sizeof(double)));
+                DD_CK(cudaMemsetAsync(X, 0, ((size_t)BC * f.NP + slack_s) * sizeof(double), c->stream));
+                DD_CK(cudaMemsetAsync(Y1, 0, ((size_t)BC * f.NP + slack_s) * sizeof(double), c->stream));
+                DD_CK(cudaMemsetAsync(Y2, 0, ((size_t)BC * f.NP + slack_s) * sizeof(double), c->stream));
+                {
+                    std::vector<double> kh(BC, K[0]);
+                    DD_CK(cudaMemcpyAsync(Kc, kh.data(), BC * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+                    for (int j0 = 0; j0 < n2; j0 += BC) {
+                        const int nb = std::min(BC, n2 - j0);
+                        DD_CK(face_identity_cols(n, f.ldf, f.NP, j0, nb, X, c->stream));
+                        DD_CK(face_slab_pass(X, Y1, nb, n, f.ldf, f.S, c->stream));
+                        DD_CK(face_slab_pass_scaled(Y1, Y2, nb, n, f.ldf, f.S, f.sw, 0, 1, Kc, c->stream));
+                        DD_CK(face_slab_pass(Y2, Y1, nb, n, f.ldf, f.S, c->stream));
+                        DD_CK(face_slab_pass(Y1, Y2, nb, n, f.ldf, f.S, c->stream));
+                        DD_CK(face_fold_rows(Ffull, f.NP, n, f.ldf, j0, nb, mu_inv[0], Y2, c->stream));
+                    }
+                    DD_CK(cudaStreamSynchronize(c->stream));
+                }
+                cudaFree(X); cudaFree(Y1); cudaFree(Y2); cudaFree(Kc);
+                DD_CK(dalloc(c, &f.Hp, fx_sym_packed_doubles(f.NP)));
+                DD_CK(fx_sym_pack(Ffull, f.NP, f.fblk, f.Hp, c->stream));
+            }
         }
         DD_CK(cudaStreamSynchronize(c->stream));
         if (packed) cudaFree(Ffull);
@@ -667,6 +699,12 @@ static dd_status fx_apply(dd_ctx* c, int ncols, const int* colp, const double* p
 
 static dd_status schur_core(dd_ctx* c, int ncols, const int* colp, const double* p, double* q) {
     Face3& f = c->f3;
+    if (f.Hp) {
+        // S = K S_unit + γ F folded at setup: one packed-symmetric stream
+        DD_TIMED(DD_KCLASS_GEMM_SCHUR, fx_sym_apply(f.Hp, f.fblk, f.NP, p, q, nullptr, ncols, colp, c->n_param, nullptr,
+                                                    f.fxD, f.fxT, c->num_sms, c->stream));
+        return DD_OK;
+    }
     DD_TIMED(DD_KCLASS_OTHER, gather_param(ncols, colp, c->n_param, c->Kp, f.Kcol, c->stream));
     DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(p, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
     DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass_scaled(f.U1, f.U2, ncols, f.n, f.ldf, f.S, f.sw, 0, 1, f.Kcol, c->stream));

@@ -70,7 +70,11 @@ struct Face3 {
     double *b3G = nullptr, *b3W = nullptr, *b3W2 = nullptr, *b3g = nullptr, *b3xg = nullptr, *b3sig = nullptr;
     double *b3Z = nullptr, *b3F = nullptr, *b3P = nullptr;   // bulk PCG: zero faces, γ F x_Γ, padded x_Γ
     double* F = nullptr;              // dense fractional term, rows round_up(NP,256) x NP row-major (DD_FX_FULL=1)
-    double* Fp = nullptr;             // packed-symmetric F: upper 128 x 128 blocks in 16-column slabs (default)
+    double* Fp = nullptr;             // packed-symmetric F: upper 128 x 128 blocks as two 64-row halves (default)
+    // packed-symmetric H = γ F + K S_unit (one parameter set per 3D handle): the Schur apply is one
+    // packed stream, no per-apply slab transforms (DD_FX_FOLD=0 keeps transforms + F); Fp stays for
+    // the bulk operator, which needs γ F alone
+    double* Hp = nullptr;
     int* fblk = nullptr;              // (I, J) of each packed block
     double *fxD = nullptr, *fxT = nullptr;   // direct / transposed block partials of the packed stream
     double* Kcol = nullptr;           // per-column K (gathered from col_param)

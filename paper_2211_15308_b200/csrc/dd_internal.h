@@ -257,6 +257,12 @@ size_t fx_sym_partial_doubles(long long NP, int max_cols);
 bool fx_sym_supported(long long NP);
 void fx_sym_block_table(long long NP, std::vector<int>& ij);          // (I, J) per packed block
 cudaError_t fx_sym_pack(const double* F, long long NP, const int* blk, double* Fp, cudaStream_t st);
+// S_unit folded into F at setup (dd3d.cpp): identity columns of the real face nodes j0.. j0+nb-1,
+// and rows pad(j) of the dense F replaced by γ F + Y (Y = K S_unit e_j from the slab passes)
+cudaError_t face_identity_cols(int n, int ldf, long long NP, int j0, int nb, double* X, cudaStream_t st);
+cudaError_t face_fold_rows(double* F, long long NP, int n, int ldf, int j0, int nb, double gamma, const double* Y,
+                           cudaStream_t st);
+// D = NULL: q = γ_c F p;  gp = NULL: γ_c = 1
 cudaError_t fx_sym_apply(const double* Fp, const int* blk, long long NP, const double* p, double* q, const double* D,
                          int ncols, const int* col_param, int n_param, const double* gp, double* Dpart, double* Tpart,
                          int num_sms, cudaStream_t st);

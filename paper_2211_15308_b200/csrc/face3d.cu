@@ -388,6 +388,37 @@ __global__ void k_scale_transpose(const double* __restrict__ V, const double* __
     }
 }
 
+__global__ void k_face_identity_cols(int n, int ldf, long long NP, int j0, int nb, double* __restrict__ X) {
+    const long long tot = (long long)nb * NP;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(e / NP);
+        const long long i = e - (long long)c * NP;
+        const int j = j0 + c;
+        const long long jp = (long long)(j / n) * ldf + j % n;
+        X[e] = i == jp ? 1.0 : 0.0;
+    }
+}
+__global__ void k_face_fold_rows(double* __restrict__ F, long long NP, int n, int ldf, int j0, int nb, double gamma,
+                                 const double* __restrict__ Y) {
+    const long long tot = (long long)nb * NP;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(e / NP);
+        const long long i = e - (long long)c * NP;
+        const int j = j0 + c;
+        const long long jp = (long long)(j / n) * ldf + j % n;
+        double* row = F + jp * NP;
+        row[i] = fma(gamma, row[i], Y[e]);
+    }
+}
+cudaError_t face_identity_cols(int n, int ldf, long long NP, int j0, int nb, double* X, cudaStream_t st) {
+    k_face_identity_cols<<<1184, 256, 0, st>>>(n, ldf, NP, j0, nb, X);
+    return cudaGetLastError();
+}
+cudaError_t face_fold_rows(double* F, long long NP, int n, int ldf, int j0, int nb, double gamma, const double* Y,
+                           cudaStream_t st) {
+    k_face_fold_rows<<<1184, 256, 0, st>>>(F, NP, n, ldf, j0, nb, gamma, Y);
+    return cudaGetLastError();
+}
 cudaError_t face_dense_pair(int n, double hh12, double* A, double* M, cudaStream_t st) {
     k_face_dense<<<1184, 256, 0, st>>>(n, hh12, A, M);
     return cudaGetLastError();

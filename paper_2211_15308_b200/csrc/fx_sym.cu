@@ -224,11 +224,16 @@ __global__ void __launch_bounds__(RCH * RTH)
     if (colg >= ncols) return;
     int p = col_param[colg];
     p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
-    const double g = gp[p];
+    const double g = gp ? gp[p] : 1.0;
     const size_t o = (size_t)colg * NP + (size_t)I * BT + r0;
     const double y[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    if (Dd) {
 #pragma unroll
-    for (int k = 0; k < 8; k++) q[o + k] = fma(g, y[k], Dd[o + k]);
+        for (int k = 0; k < 8; k++) q[o + k] = fma(g, y[k], Dd[o + k]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; k++) q[o + k] = g * y[k];
+    }
 }
 
 // full row-major NP x NP F -> packed upper blocks (row-major 128 x 128 each: two 64-row halves)
