@@ -179,6 +179,39 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
         // DD_FX_PACKED=0 keeps the full row-major F
         const char* fp = std::getenv("DD_FX_PACKED");
         const bool packed = !shardF && fx_sym_supported(f.NP) && !(fp && fp[0] == '0');
+        // fold the interior solve into the dense operator: rows pad(j) of F <- γ F + K S_unit e_j
+        // (one parameter set per 3D handle; S_unit applied to the identity columns by the same slab
+        // passes the per-apply path runs; symmetric), DD_FX_FOLD=0 keeps the per-apply transforms
+        const char* fo = std::getenv("DD_FX_FOLD");
+        const bool fold = !(fo && fo[0] == '0');
+        auto fold_into = [&](double* Fd) -> dd_status {
+            const int BC = 256;
+            const size_t len = (size_t)BC * f.NP + (size_t)64 * f.ldf;   // slab passes read up to 64 rows past a slab
+            struct Bufs {                                                 // freed on every exit path
+                double *X = nullptr, *Y1 = nullptr, *Y2 = nullptr, *Kc = nullptr;
+                ~Bufs() { cudaFree(X); cudaFree(Y1); cudaFree(Y2); cudaFree(Kc); }
+            } b;
+            DD_CK(cudaMalloc(&b.X, len * sizeof(double)));
+            DD_CK(cudaMalloc(&b.Y1, len * sizeof(double)));
+            DD_CK(cudaMalloc(&b.Y2, len * sizeof(double)));
+            DD_CK(cudaMalloc(&b.Kc, BC * sizeof(double)));
+            DD_CK(cudaMemsetAsync(b.Y1, 0, len * sizeof(double), c->stream));
+            DD_CK(cudaMemsetAsync(b.Y2, 0, len * sizeof(double), c->stream));
+            DD_CK(cudaMemsetAsync(b.X, 0, len * sizeof(double), c->stream));
+            const std::vector<double> kh(BC, K[0]);
+            DD_CK(cudaMemcpyAsync(b.Kc, kh.data(), BC * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            for (int j0 = 0; j0 < n2; j0 += BC) {
+                const int nb = std::min(BC, n2 - j0);
+                DD_CK(face_identity_cols(n, f.ldf, f.NP, j0, nb, b.X, c->stream));
+                DD_CK(face_slab_pass(b.X, b.Y1, nb, n, f.ldf, f.S, c->stream));
+                DD_CK(face_slab_pass_scaled(b.Y1, b.Y2, nb, n, f.ldf, f.S, f.sw, 0, 1, b.Kc, c->stream));
+                DD_CK(face_slab_pass(b.Y2, b.Y1, nb, n, f.ldf, f.S, c->stream));
+                DD_CK(face_slab_pass(b.Y1, b.Y2, nb, n, f.ldf, f.S, c->stream));
+                DD_CK(face_fold_rows(Fd, f.NP, n, f.ldf, j0, nb, mu_inv[0], b.Y2, c->stream));
+            }
+            DD_CK(cudaStreamSynchronize(c->stream));   // kh and the buffers outlive the queued work
+            return DD_OK;
+        };
         double* Ffull = nullptr;
         f.fx_r0 = 0;
         f.fx_r1 = (int)f.NP;
@@ -201,6 +234,14 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
             DD_CK(dalloc(c, &f.F, (size_t)round_up((int)rows, 256) * (size_t)f.NP));
             DD_CK(cudaMemcpyAsync(f.F, Ffull + (size_t)f.fx_r0 * f.NP, (size_t)(f.fx_r1 - f.fx_r0) * f.NP * sizeof(double),
                                   cudaMemcpyDeviceToDevice, c->stream));
+            if (fold) {                    // the Schur apply streams this rank's rows of H; F rows stay for bulk
+                dd_status fs = fold_into(Ffull);
+                if (fs != DD_OK) return fs;
+                DD_CK(dalloc(c, &f.Hrows, (size_t)round_up((int)rows, 256) * (size_t)f.NP));
+                DD_CK(cudaMemcpyAsync(f.Hrows, Ffull + (size_t)f.fx_r0 * f.NP,
+                                      (size_t)(f.fx_r1 - f.fx_r0) * f.NP * sizeof(double), cudaMemcpyDeviceToDevice,
+                                      c->stream));
+            }
             DD_CK(dalloc(c, &f.fx_r0s, (size_t)W + 1));
             DD_CK(cudaMemcpyAsync(f.fx_r0s, r0s.data(), sizeof(int) * (W + 1), cudaMemcpyHostToDevice, c->stream));
             DD_CK(dalloc(c, &f.fx_send, (size_t)c->max_cols * f.fx_rows_max));
@@ -219,36 +260,9 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
             DD_CK(fx_sym_pack(Ffull, f.NP, f.fblk, f.Fp, c->stream));
             DD_CK(dalloc(c, &f.fxD, fx_sym_partial_doubles(f.NP, c->max_cols)));
             DD_CK(dalloc(c, &f.fxT, fx_sym_partial_doubles(f.NP, c->max_cols)));
-            // fold the interior solve into the packed stream: H = γ F + K S_unit (one parameter set
-            // per 3D handle), S_unit applied to the identity columns by the same slab passes the
-            // per-apply path runs, row pad(j) of the dense F <- γ F + K S_unit e_j (symmetric)
-            const char* fo = std::getenv("DD_FX_FOLD");
-            if (!(fo && fo[0] == '0')) {
-                const int BC = 256;
-                const size_t slack_s = (size_t)64 * f.ldf;
-                double *X = nullptr, *Y1 = nullptr, *Y2 = nullptr, *Kc = nullptr;
-                DD_CK(cudaMalloc(&X, ((size_t)BC * f.NP + slack_s) * sizeof(double)));
-                DD_CK(cudaMalloc(&Y1, ((size_t)BC * f.NP + slack_s) * sizeof(double)));
-                DD_CK(cudaMalloc(&Y2, ((size_t)BC * f.NP + slack_s) * sizeof(double)));
-                DD_CK(cudaMalloc(&Kc, BC * sizeof(double)));
-                DD_CK(cudaMemsetAsync(X, 0, ((size_t)BC * f.NP + slack_s) * sizeof(double), c->stream));
-                DD_CK(cudaMemsetAsync(Y1, 0, ((size_t)BC * f.NP + slack_s) * sizeof(double), c->stream));
-                DD_CK(cudaMemsetAsync(Y2, 0, ((size_t)BC * f.NP + slack_s) * sizeof(double), c->stream));
-                {
-                    std::vector<double> kh(BC, K[0]);
-                    DD_CK(cudaMemcpyAsync(Kc, kh.data(), BC * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-                    for (int j0 = 0; j0 < n2; j0 += BC) {
-                        const int nb = std::min(BC, n2 - j0);
-                        DD_CK(face_identity_cols(n, f.ldf, f.NP, j0, nb, X, c->stream));
-                        DD_CK(face_slab_pass(X, Y1, nb, n, f.ldf, f.S, c->stream));
-                        DD_CK(face_slab_pass_scaled(Y1, Y2, nb, n, f.ldf, f.S, f.sw, 0, 1, Kc, c->stream));
-                        DD_CK(face_slab_pass(Y2, Y1, nb, n, f.ldf, f.S, c->stream));
-                        DD_CK(face_slab_pass(Y1, Y2, nb, n, f.ldf, f.S, c->stream));
-                        DD_CK(face_fold_rows(Ffull, f.NP, n, f.ldf, j0, nb, mu_inv[0], Y2, c->stream));
-                    }
-                    DD_CK(cudaStreamSynchronize(c->stream));
-                }
-                cudaFree(X); cudaFree(Y1); cudaFree(Y2); cudaFree(Kc);
+            if (fold) {
+                dd_status fs = fold_into(Ffull);
+                if (fs != DD_OK) return fs;
                 DD_CK(dalloc(c, &f.Hp, fx_sym_packed_doubles(f.NP)));
                 DD_CK(fx_sym_pack(Ffull, f.NP, f.fblk, f.Hp, c->stream));
             }
@@ -675,16 +689,18 @@ static dd_status precond_core(dd_ctx* c, int ncols, const double* r, double* z) 
 // q = γ F p + D with the dense F stream (row a-3); a row-sharded F (pole split, §8(e)) computes this
 // rank's rows and gathers the others with one ncclAllGather (without a communicator — ranks emulated
 // in one process — the other rows are zero, so the ranks' outputs add up to the full product)
-static dd_status fx_apply(dd_ctx* c, int ncols, const int* colp, const double* p, double* q, const double* D) {
+// Mat = F (γ per column, + D) or the folded H rows (Mat = f.Hrows, gp = D = NULL)
+static dd_status fx_apply(dd_ctx* c, int ncols, const int* colp, const double* p, double* q, const double* D,
+                          const double* Mat, const double* gp) {
     Face3& f = c->f3;
     const int rows = f.fx_r1 - f.fx_r0;
     if (rows >= f.NP) {
-        DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, f.NP, p, q, D, ncols, colp, c->n_param, c->gp, f.fx_ws, f.fx_cnt,
+        DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(Mat, f.NP, p, q, D, ncols, colp, c->n_param, gp, f.fx_ws, f.fx_cnt,
                                                c->num_sms, c->stream));
         return DD_OK;
     }
     if (rows > 0)
-        DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(f.F, f.NP, p, q, D, ncols, colp, c->n_param, c->gp, f.fx_ws, f.fx_cnt,
+        DD_TIMED(DD_KCLASS_GEMM_SCHUR, face_fx(Mat, f.NP, p, q, D, ncols, colp, c->n_param, gp, f.fx_ws, f.fx_cnt,
                                                c->num_sms, c->stream, f.fx_r0, rows));
     if (f.nccl) {
         DD_TIMED(DD_KCLASS_OTHER, fx_pack(q, f.NP, ncols, f.fx_r0, rows, f.fx_rows_max, f.fx_send, c->stream));
@@ -705,6 +721,7 @@ static dd_status schur_core(dd_ctx* c, int ncols, const int* colp, const double*
                                                     f.fxD, f.fxT, c->num_sms, c->stream));
         return DD_OK;
     }
+    if (f.Hrows) return fx_apply(c, ncols, colp, p, q, nullptr, f.Hrows, nullptr);   // this rank's rows of H
     DD_TIMED(DD_KCLASS_OTHER, gather_param(ncols, colp, c->n_param, c->Kp, f.Kcol, c->stream));
     DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(p, f.U1, ncols, f.n, f.ldf, f.S, c->stream));
     DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass_scaled(f.U1, f.U2, ncols, f.n, f.ldf, f.S, f.sw, 0, 1, f.Kcol, c->stream));
@@ -728,7 +745,7 @@ static dd_status schur_core(dd_ctx* c, int ncols, const int* colp, const double*
                                                     f.fxD, f.fxT, c->num_sms, c->stream));
         return DD_OK;
     }
-    return fx_apply(c, ncols, colp, p, q, f.U2);
+    return fx_apply(c, ncols, colp, p, q, f.U2, f.F, c->gp);
 }
 
 dd_status schur_3d(dd_ctx* c, int ncols, const int* colp, const double* xin, double* yout, bool user_layout) {
@@ -886,7 +903,7 @@ dd_status bulk_pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, do
             DD_TIMED(DD_KCLASS_GEMM_SCHUR, fx_sym_apply(f.Fp, f.fblk, NP, f.b3P, f.b3F, f.b3Z, ncols, colp, c->n_param,
                                                         c->gp, f.fxD, f.fxT, c->num_sms, c->stream));
         } else {
-            dd_status fs = fx_apply(c, ncols, colp, f.b3P, f.b3F, f.b3Z);
+            dd_status fs = fx_apply(c, ncols, colp, f.b3P, f.b3F, f.b3Z, f.F, c->gp);
             if (fs != DD_OK) return fs;
         }
         DD_TIMED(DD_KCLASS_OTHER, bulk3_apply(n, ldf, NP, ncols, in, nb, f.b3F, colp, c->n_param, c->Kp, 1.0 / c->N, out,

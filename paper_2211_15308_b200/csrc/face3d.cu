@@ -119,7 +119,8 @@ struct EpiFaceFx {             // q[c] = γ_c v + D[c]  (padded face layout; row
         int p = col_param[col];
         p = p < 0 ? 0 : (p >= n_param ? n_param - 1 : p);
         const size_t i = row0 + row + (size_t)col * ldq;
-        q[i] = fma(gp[p], v, D[i]);
+        const double g = gp ? gp[p] : 1.0;               // gp = NULL: the folded H (γ inside)
+        q[i] = D ? fma(g, v, D[i]) : g * v;
     }
 };
 struct EpiFaceScatter {        // dense n^2 x n^2 product -> padded NP x NP row-major matrix
