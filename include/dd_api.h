@@ -115,6 +115,10 @@ typedef struct {
  *   dist                          NULL for a single GPU
  * The RA fit itself is not part of the library (PAPER.md:196-198 defers it to the
  * references); the Python package provides one (rafit.py).
+ * 3D (n_param must be 1) with the dense F: setup runs the generalised eigensolve of the face pair
+ * (cuSOLVER, n_Γ = (N-1)^2) and keeps two packed-symmetric operators, F (for the bulk operator) and
+ * H = γ F + K S_unit (the Schur apply) — at N = 128 1.08 GB each, plus a transient dense n_Γ^2
+ * (2.1 GB) during setup; under a pole split each rank keeps its rows of F and H instead.
  * Returns DD_EINVAL for dim not in {2,3}, N < 2, gamma_face != 0, K <= 0, mu_inv < 0,
  * a pole >= 0 or not finite, n_param < 1, n_poles < 0, max_cols < 1.
  */
