@@ -75,14 +75,14 @@ struct EpiInnerCheb {          // one Chebyshev step of pair b = s*C + c at elem
     const double* dg; const double* idg; const double* cs;              // d = c1[j] d + c2[j] idg∘r; x̂ += d
     const double* c1; const double* c2; int kstride; const int* kiter;
     static constexpr bool kStaged = true;                              // x̂, d̂ updated in place
-    struct Blk { double cs, c1, c2; size_t e0, t0, b0; };
+    struct Blk { double cs, c1, c2; size_t e0, t0, b0; bool first; };   // first: step 0, d_0 = x̂_1 (not stored)
     struct Ctx { double2 x, d, b, g, ig; };
     __device__ __forceinline__ void operator()(int b, int row, int col, double v) const {   // split-K form
         const Blk k = block(b);
         const size_t i = row + (size_t)col * ldf;
         const double xv = x[k.e0 + i];
         const double r = bh[k.b0 + i] - fma(dg[k.t0 + i], xv, k.cs * v);
-        const double dn = fma(k.c1, d[k.e0 + i], k.c2 * (idg[k.t0 + i] * r));
+        const double dn = fma(k.c1, k.first ? xv : d[k.e0 + i], k.c2 * (idg[k.t0 + i] * r));
         d[k.e0 + i] = dn;
         x[k.e0 + i] = xv + dn;
     }
@@ -90,12 +90,12 @@ struct EpiInnerCheb {          // one Chebyshev step of pair b = s*C + c at elem
         const int s = b / C, c = b - s * C;
         const int j = *kiter;
         return Blk{cs[s], c1[(size_t)s * kstride + j], c2[(size_t)s * kstride + j], (size_t)b * NP, (size_t)s * NP,
-                   (size_t)c * NP};
+                   (size_t)c * NP, j == 0};
     }
     __device__ __forceinline__ void load(int, int row, int col, const Blk& k, Ctx& cx) const {
         const size_t i = row + (size_t)col * ldf;
         cx.x = *reinterpret_cast<const double2*>(x + k.e0 + i);
-        cx.d = *reinterpret_cast<const double2*>(d + k.e0 + i);
+        cx.d = k.first ? cx.x : *reinterpret_cast<const double2*>(d + k.e0 + i);
         cx.b = __ldg(reinterpret_cast<const double2*>(bh + k.b0 + i));
         cx.g = __ldg(reinterpret_cast<const double2*>(dg + k.t0 + i));
         cx.ig = __ldg(reinterpret_cast<const double2*>(idg + k.t0 + i));
@@ -572,9 +572,7 @@ __global__ void k_inner_init_cheb(InnerArgs a, const double* __restrict__ bh) {
     const double* idg = a.idg + (size_t)s * a.NP;
     const bool live = a.kmax[s] > 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.NP; i += (long long)gridDim.x * blockDim.x) {
-        const double d = live ? bh[(size_t)c * a.NP + i] * idg[i] : 0.0;
-        a.x[off + i] = d;
-        a.p[off + i] = d;
+        a.x[off + i] = live ? bh[(size_t)c * a.NP + i] * idg[i] : 0.0;   // x̂_1 = d_0 (step 0 reads d from x̂)
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) a.active[pq] = a.kmax[s] > 1 ? 1 : 0;
 }
@@ -752,7 +750,7 @@ __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double
                     const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
                     idx[u] = base + (size_t)row * ldf + 2 * cp;
                     xv[u] = *reinterpret_cast<const double2*>(xin + e0 + idx[u]);
-                    dv[u] = *reinterpret_cast<const double2*>(a.p + e0 + idx[u]);
+                    dv[u] = j == 0 ? xv[u] : *reinterpret_cast<const double2*>(a.p + e0 + idx[u]);
                     bv[u] = __ldg(reinterpret_cast<const double2*>(bh + b0 + idx[u]));
                     gv[u] = __ldg(reinterpret_cast<const double2*>(a.dg + t0 + idx[u]));
                     iv[u] = __ldg(reinterpret_cast<const double2*>(a.idg + t0 + idx[u]));
