@@ -598,10 +598,19 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
         return cheb ? inner_cond_cheb(a, n_act_slot, cnt_slot, loop_max, h, st)
                     : inner_cond(n_act_slot, cnt_slot, loop_max, h, st);
     };
+    // fused steps all in one cooperative launch (grid barrier between steps; DD_CHEB_MULTI=0: one launch
+    // per step inside the WHILE graph)
+    static const bool multi_env = !(std::getenv("DD_CHEB_MULTI") && std::getenv("DD_CHEB_MULTI")[0] == '0');
     if (cheb && loop_max <= 0) {
         // every system is done after the init step
         DD_CK(cudaMemsetAsync(cnt_slot, 0, sizeof(int), c->stream));
         *v.last_iters = 0;
+        *v.on_dev = false;
+    } else if (fused && multi_env) {
+        DD_CK(cudaMemsetAsync(cnt_slot, 0, sizeof(int), c->stream));
+        DD_TIMED(DD_KCLASS_POLESUM, cheb_step_fused(a, W2, f.Dh, n_act_slot, cnt_slot, c->ints + v.slot_done, loop_max,
+                                                    0ull, c->num_sms, c->stream, loop_max));
+        *v.last_iters = loop_max;
         *v.on_dev = false;
     } else if (c->graph_ok && !c->prof) {
         // the whole inner loop as one conditional WHILE graph (no host round trips)

@@ -300,7 +300,8 @@ cudaError_t inner_init_cheb(const InnerArgs& a, const double* bh, cudaStream_t s
 // V = D̂ X̂ D̂^T per (pair, 64x64 parity block), the step's epilogue, and the loop condition
 bool cheb_fused_ok(int n, int ldf);
 cudaError_t cheb_step_fused(const InnerArgs& a, const double* bh, const double* Dh, int* n_active, int* counter,
-                            int* done, int maxit, unsigned long long handle, int num_sms, cudaStream_t st);
+                            int* done, int maxit, unsigned long long handle, int num_sms, cudaStream_t st,
+                            int nsteps = 0);
 cudaError_t inner_cond_cheb(const InnerArgs& a, int* n_active, int* counter, int maxit, unsigned long long handle,
                             cudaStream_t st);
 cudaError_t inner_update_hat(const InnerArgs& a, int* n_active, cudaStream_t st);

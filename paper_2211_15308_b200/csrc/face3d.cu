@@ -670,11 +670,15 @@ __device__ __forceinline__ void cf_store_acc(double* Ys, const double (&acc)[MI]
 }
 
 // HR: output rows per work item — 64 (a whole parity block) or 32 (half a block: twice the items,
-// for batches whose pairs do not fill the SMs, e.g. the ranks of a pole split)
-template <int HR>
+// for batches whose pairs do not fill the SMs, e.g. the ranks of a pole split).
+// MULTI = false: one step (j = counter[0]) per launch, the last CTA advances the counter and sets the
+// WHILE condition.  MULTI = true: all nsteps steps in one cooperative launch with a grid-wide
+// barrier between steps — E stays in shared memory and the per-step launch / ramp / tail goes away.
+// An item is active at step j iff j + 1 < K_s of its system (the pair's a-priori step count).
+template <int HR, bool MULTI>
 __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double* __restrict__ bh,
                                                        const double* __restrict__ Dh, int* n_active, int* counter,
-                                                       int* done, int maxit, unsigned long long handle) {
+                                                       int* done, int maxit, unsigned long long handle, int nsteps) {
     constexpr int NH = 64 / HR, IPP = 4 * NH, MI = HR / 32;      // items per block, per pair; MMA rows / 16 per warp
     extern __shared__ __align__(16) double smem[];
     double* Es = smem;
@@ -683,94 +687,113 @@ __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double
     double* Vs = smem + 3 * CF_BLK;              // two buffers
     __shared__ int last;
     const int tid = threadIdx.x;
-    const int j = counter[0];
-    const double* xin = (j & 1) ? a.x1 : a.x;
-    double* xout = (j & 1) ? a.x : a.x1;
+    const int j0 = MULTI ? 0 : counter[0];
+    const int J1 = MULTI ? nsteps : j0 + 1;
     const int nitem = a.npair * IPP;
     const int ldf = a.ldf;
-    auto next = [&](int it) {
-        while (it < nitem && !a.active[it / IPP]) it += gridDim.x;
+    auto next = [&](int it, int j) {
+        while (it < nitem && !(j + 1 < a.kmax[(it / IPP) / a.C])) it += gridDim.x;
         return it;
     };
-    int it0 = next(blockIdx.x);
-    if (tid < CF_MMA) {
-        // ------------------------------------------------ MMA warps
-        const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
-        const int wm = warp & 1, wn = warp >> 1;
-        auto xblk = [&](int item) {
-            const int q = item / IPP, blk = (item / NH) & 3, A = blk >> 1, B = blk & 1;
-            return xin + (size_t)q * a.NP + (size_t)(1 - A) * 64 * ldf + (1 - B) * 64;
-        };
-        cf_load_block<CF_MMA>(Es, Dh + 64, ldf, tid);        // E = D̂[o rows][e cols]
-        if (it0 < nitem) cf_load_block<CF_MMA>(Xs, xblk(it0), ldf, tid);
-        dg_cp_commit();
-        int t = 0;
-        for (int it = it0; it < nitem; t++) {
-            const int blk = (it / NH) & 3, A = blk >> 1, B = blk & 1, h = it % NH;
-            dg_cp_wait<0>();
-            cf_bar_sync(1, CF_MMA);                           // X̂ block (and E) landed for every MMA warp
-            double acc[MI][CF_NI][4];
-            // Y = L X̂ for the item's HR rows of L (= E, or E^T read transposed)
-            cf_gemm<MI>(acc, Es + (A ? h * HR : h * HR * CF_LD), A ? 1 : CF_LD, A ? CF_LD : 1, Xs, CF_LD, 1, wm, wn, gq, tq);
-            cf_bar_sync(1, CF_MMA);                           // X̂ consumed; previous GEMM 2 done with Ys
-            const int nit = next(it + gridDim.x);
-            if (nit < nitem) cf_load_block<CF_MMA>(Xs, xblk(nit), ldf, tid);
+    // this CTA's items over all its steps: the EMPTY hand-over looks two items ahead across steps
+    int T_total = 0;
+    for (int j = j0; j < J1; j++)
+        for (int it = next(blockIdx.x, j); it < nitem; it = next(it + gridDim.x, j)) T_total++;
+    const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+    const int wm = warp & 1, wn = (warp & 7) >> 1;
+    if (tid < CF_MMA) cf_load_block<CF_MMA>(Es, Dh + 64, ldf, tid);        // E = D̂[o rows][e cols], once
+    int t = 0;
+    for (int j = j0; j < J1; j++) {
+        const double* xin = (j & 1) ? a.x1 : a.x;
+        double* xout = (j & 1) ? a.x : a.x1;
+        const int it0 = next(blockIdx.x, j);
+        if (tid < CF_MMA) {
+            // ------------------------------------------------ MMA warps
+            auto xblk = [&](int item) {
+                const int q = item / IPP, blk = (item / NH) & 3, A = blk >> 1, B = blk & 1;
+                return xin + (size_t)q * a.NP + (size_t)(1 - A) * 64 * ldf + (1 - B) * 64;
+            };
+            if (it0 < nitem) cf_load_block<CF_MMA>(Xs, xblk(it0), ldf, tid);
             dg_cp_commit();
-            cf_store_acc<MI>(Ys, acc, wm, wn, gq, tq);
-            cf_bar_sync(1, CF_MMA);
-            cf_gemm<MI>(acc, Ys, CF_LD, 1, Es, B ? CF_LD : 1, B ? 1 : CF_LD, wm, wn, gq, tq);   // V = Y M^T
-            const int b = t & 1;
-            if (t >= 2) cf_bar_sync(4 + b, CF_T);             // EMPTY[b]: item t-2's epilogue is done with it
-            cf_store_acc<MI>(Vs + b * CF_BLK, acc, wm, wn, gq, tq);
-            cf_bar_arrive(2 + b, CF_T);                       // FULL[b]
-            it = nit;
-        }
-        dg_cp_wait<0>();
-    } else {
-        // ------------------------------------------------ epilogue warps
-        const int et = tid - CF_MMA;
-        int t = 0;
-        for (int it = it0; it < nitem; t++) {
-            const int q = it / IPP, blk = (it / NH) & 3, A = blk >> 1, B = blk & 1, h = it % NH;
-            const int s = q / a.C, c = q - s * a.C;
-            const int nit = next(it + gridDim.x);
-            const int b = t & 1;
-            const double sg = A == B ? 1.0 : -1.0;
-            const double cs = sg * a.cs[s], c1 = a.cc1[(size_t)s * a.kstride + j], c2 = a.cc2[(size_t)s * a.kstride + j];
-            const size_t e0 = (size_t)q * a.NP, t0 = (size_t)s * a.NP, b0 = (size_t)c * a.NP;
-            const size_t base = (size_t)(A * 64 + h * HR) * ldf + B * 64;
-            const double* V = Vs + b * CF_BLK;
-            cf_bar_sync(2 + b, CF_T);                         // FULL[b]
-#pragma unroll 1
-            for (int bb = 0; bb < HR * 32 / CF_EPI; bb += 4) {
-                double2 xv[4], dv[4], bv[4], gv[4], iv[4];
-                size_t idx[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
-                    idx[u] = base + (size_t)row * ldf + 2 * cp;
-                    xv[u] = *reinterpret_cast<const double2*>(xin + e0 + idx[u]);
-                    dv[u] = j == 0 ? xv[u] : *reinterpret_cast<const double2*>(a.p + e0 + idx[u]);
-                    bv[u] = __ldg(reinterpret_cast<const double2*>(bh + b0 + idx[u]));
-                    gv[u] = __ldg(reinterpret_cast<const double2*>(a.dg + t0 + idx[u]));
-                    iv[u] = __ldg(reinterpret_cast<const double2*>(a.idg + t0 + idx[u]));
-                }
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
-                    const double2 v = *reinterpret_cast<const double2*>(&V[row * CF_LD + 2 * cp]);
-                    const double r0 = bv[u].x - fma(gv[u].x, xv[u].x, cs * v.x);
-                    const double r1 = bv[u].y - fma(gv[u].y, xv[u].y, cs * v.y);
-                    const double d0 = fma(c1, dv[u].x, c2 * (iv[u].x * r0));
-                    const double d1 = fma(c1, dv[u].y, c2 * (iv[u].y * r1));
-                    *reinterpret_cast<double2*>(a.p + e0 + idx[u]) = make_double2(d0, d1);
-                    *reinterpret_cast<double2*>(xout + e0 + idx[u]) = make_double2(xv[u].x + d0, xv[u].y + d1);
-                }
+            for (int it = it0; it < nitem; t++) {
+                const int blk = (it / NH) & 3, A = blk >> 1, B = blk & 1, h = it % NH;
+                dg_cp_wait<0>();
+                cf_bar_sync(1, CF_MMA);                       // X̂ block (and E) landed for every MMA warp
+                double acc[MI][CF_NI][4];
+                // Y = L X̂ for the item's HR rows of L (= E, or E^T read transposed)
+                cf_gemm<MI>(acc, Es + (A ? h * HR : h * HR * CF_LD), A ? 1 : CF_LD, A ? CF_LD : 1, Xs, CF_LD, 1, wm, wn,
+                            gq, tq);
+                cf_bar_sync(1, CF_MMA);                       // X̂ consumed; previous GEMM 2 done with Ys
+                const int nit = next(it + gridDim.x, j);      // within this step (the next step's X̂ is not final)
+                if (nit < nitem) cf_load_block<CF_MMA>(Xs, xblk(nit), ldf, tid);
+                dg_cp_commit();
+                cf_store_acc<MI>(Ys, acc, wm, wn, gq, tq);
+                cf_bar_sync(1, CF_MMA);
+                cf_gemm<MI>(acc, Ys, CF_LD, 1, Es, B ? CF_LD : 1, B ? 1 : CF_LD, wm, wn, gq, tq);   // V = Y M^T
+                const int b = t & 1;
+                if (t >= 2) cf_bar_sync(4 + b, CF_T);         // EMPTY[b]: item t-2's epilogue is done with it
+                cf_store_acc<MI>(Vs + b * CF_BLK, acc, wm, wn, gq, tq);
+                cf_bar_arrive(2 + b, CF_T);                   // FULL[b]
+                it = nit;
             }
-            // EMPTY[b] — only when the MMA warps will wait for it (their item t+2 exists)
-            if (nit < nitem && next(nit + gridDim.x) < nitem) cf_bar_arrive(4 + b, CF_T);
-            it = nit;
+            dg_cp_wait<0>();
+        } else {
+            // ------------------------------------------------ epilogue warps
+            const int et = tid - CF_MMA;
+            for (int it = it0; it < nitem; t++) {
+                const int q = it / IPP, blk = (it / NH) & 3, A = blk >> 1, B = blk & 1, h = it % NH;
+                const int s = q / a.C, c = q - s * a.C;
+                const int nit = next(it + gridDim.x, j);
+                const int b = t & 1;
+                const double sg = A == B ? 1.0 : -1.0;
+                const double cs = sg * a.cs[s], c1 = a.cc1[(size_t)s * a.kstride + j], c2 = a.cc2[(size_t)s * a.kstride + j];
+                const size_t e0 = (size_t)q * a.NP, t0 = (size_t)s * a.NP, b0 = (size_t)c * a.NP;
+                const size_t base = (size_t)(A * 64 + h * HR) * ldf + B * 64;
+                const double* V = Vs + b * CF_BLK;
+                cf_bar_sync(2 + b, CF_T);                     // FULL[b]
+#pragma unroll 1
+                for (int bb = 0; bb < HR * 32 / CF_EPI; bb += 4) {
+                    double2 xv[4], dv[4], bv[4], gv[4], iv[4];
+                    size_t idx[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
+                        idx[u] = base + (size_t)row * ldf + 2 * cp;
+                        xv[u] = *reinterpret_cast<const double2*>(xin + e0 + idx[u]);
+                        dv[u] = j == 0 ? xv[u] : *reinterpret_cast<const double2*>(a.p + e0 + idx[u]);
+                        bv[u] = __ldg(reinterpret_cast<const double2*>(bh + b0 + idx[u]));
+                        gv[u] = __ldg(reinterpret_cast<const double2*>(a.dg + t0 + idx[u]));
+                        iv[u] = __ldg(reinterpret_cast<const double2*>(a.idg + t0 + idx[u]));
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
+                        const double2 v = *reinterpret_cast<const double2*>(&V[row * CF_LD + 2 * cp]);
+                        const double r0 = bv[u].x - fma(gv[u].x, xv[u].x, cs * v.x);
+                        const double r1 = bv[u].y - fma(gv[u].y, xv[u].y, cs * v.y);
+                        const double d0 = fma(c1, dv[u].x, c2 * (iv[u].x * r0));
+                        const double d1 = fma(c1, dv[u].y, c2 * (iv[u].y * r1));
+                        *reinterpret_cast<double2*>(a.p + e0 + idx[u]) = make_double2(d0, d1);
+                        *reinterpret_cast<double2*>(xout + e0 + idx[u]) = make_double2(xv[u].x + d0, xv[u].y + d1);
+                    }
+                }
+                // EMPTY[b] — only when the MMA warps will wait for it (this CTA's item t+2 exists)
+                if (t + 2 < T_total) cf_bar_arrive(4 + b, CF_T);
+                it = nit;
+            }
         }
+        if (MULTI && j + 1 < J1) {
+            __syncthreads();
+            cg::this_grid().sync();                           // step j's x̂, d̂ final everywhere
+        }
+    }
+    if (MULTI) {
+        if (blockIdx.x == 0 && tid == 0) {
+            counter[0] = J1;
+            counter[2] += J1 - j0;
+            *n_active = 0;
+        }
+        return;
     }
     // the last CTA to finish: step counter, active flags, loop condition
     __syncthreads();
@@ -781,7 +804,7 @@ __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double
     __syncthreads();
     if (!last) return;
     __threadfence();
-    const int jn = j + 1;
+    const int jn = j0 + 1;
     int na = 0;
     for (int pq = tid; pq < a.npair; pq += CF_T) {
         const int on = jn + 1 < a.kmax[pq / a.C] ? 1 : 0;
@@ -797,25 +820,37 @@ __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double
         if (handle) cudaGraphSetConditional((cudaGraphConditionalHandle)handle, (na > 0 && jn < maxit) ? 1u : 0u);
     }
 }
-cudaError_t cheb_step_fused(const InnerArgs& a, const double* bh, const double* Dh, int* n_active, int* counter,
-                            int* done, int maxit, unsigned long long handle, int num_sms, cudaStream_t st) {
+template <int HR, bool MULTI>
+static cudaError_t cheb_launch(int G, const InnerArgs& a, const double* bh, const double* Dh, int* n_active,
+                               int* counter, int* done, int maxit, unsigned long long handle, int nsteps,
+                               cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_cheb_step<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF_SMEM);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_cheb_step<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF_SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_cheb_step<HR, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)CF_SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    if (!MULTI) {
+        k_cheb_step<HR, false><<<G, CF_T, CF_SMEM, st>>>(a, bh, Dh, n_active, counter, done, maxit, handle, nsteps);
+        return cudaGetLastError();
+    }
+    void* args[] = {(void*)&a, (void*)&bh, (void*)&Dh, (void*)&n_active, (void*)&counter, (void*)&done, (void*)&maxit,
+                    (void*)&handle, (void*)&nsteps};
+    return cudaLaunchCooperativeKernel((const void*)k_cheb_step<HR, true>, dim3(G), dim3(CF_T), args, CF_SMEM, st);
+}
+// nsteps > 0: all steps in one cooperative launch (MULTI); nsteps = 0: one step (the WHILE-loop form)
+cudaError_t cheb_step_fused(const InnerArgs& a, const double* bh, const double* Dh, int* n_active, int* counter,
+                            int* done, int maxit, unsigned long long handle, int num_sms, cudaStream_t st, int nsteps) {
     // whole parity blocks when they give every SM two or more items; half blocks otherwise
     if (a.npair * 4 >= 2 * num_sms) {
         const int G = num_sms;
-        k_cheb_step<64><<<G, CF_T, CF_SMEM, st>>>(a, bh, Dh, n_active, counter, done, maxit, handle);
-    } else {
-        const int G = std::min(num_sms, std::max(1, a.npair * 8));
-        k_cheb_step<32><<<G, CF_T, CF_SMEM, st>>>(a, bh, Dh, n_active, counter, done, maxit, handle);
+        return nsteps > 0 ? cheb_launch<64, true>(G, a, bh, Dh, n_active, counter, done, maxit, handle, nsteps, st)
+                          : cheb_launch<64, false>(G, a, bh, Dh, n_active, counter, done, maxit, handle, 0, st);
     }
-    return cudaGetLastError();
+    const int G = std::min(num_sms, std::max(1, a.npair * 8));
+    return nsteps > 0 ? cheb_launch<32, true>(G, a, bh, Dh, n_active, counter, done, maxit, handle, nsteps, st)
+                      : cheb_launch<32, false>(G, a, bh, Dh, n_active, counter, done, maxit, handle, 0, st);
 }
 cudaError_t inner_init_cheb(const InnerArgs& a, const double* bh, cudaStream_t st) {
     k_inner_init_cheb<<<dim3(8, a.npair), 256, 0, st>>>(a, bh);
