@@ -629,157 +629,202 @@ __device__ __forceinline__ void cf_load_block(double* dst, const double* src, in
         dg_cp_async16(dst + row * CF_LD + 2 * ch, src + (size_t)row * ldf + 2 * ch);
     }
 }
-// C = L B over K = 64 for this warp's (16 MI) x (8 CF_NI) sub-tile: L[i][k] = Ls[i*l1 + k*l2], B[k][j] = Bs[k*b1 + j*b2]
-template <int MI>
-__device__ __forceinline__ void cf_gemm(double (&acc)[MI][CF_NI][4], const double* Ls, int l1, int l2, const double* Bs,
-                                        int b1, int b2, int wm, int wn, int gq, int tq) {
+// C = L B over K = 64 for this warp's (16 MI) x (8 NI) sub-tile at (row0, col0): L[i][k] = Ls[i*l1 + k*l2],
+// B[k][j] = Bs[k*b1 + j*b2]
+template <int MI, int NI>
+__device__ __forceinline__ void cf_gemm(double (&acc)[MI][NI][4], const double* Ls, int l1, int l2, const double* Bs,
+                                        int b1, int b2, int row0, int col0, int gq, int tq) {
 #pragma unroll
     for (int mi = 0; mi < MI; mi++)
 #pragma unroll
-        for (int ni = 0; ni < CF_NI; ni++)
+        for (int ni = 0; ni < NI; ni++)
 #pragma unroll
             for (int r = 0; r < 4; r++) acc[mi][ni][r] = 0.0;
-    const double* la = Ls + (wm * 16 * MI + gq) * l1 + tq * l2;
-    const double* bb = Bs + tq * b1 + (wn * 8 * CF_NI + gq) * b2;
+    const double* la = Ls + (row0 + gq) * l1 + tq * l2;
+    const double* bb = Bs + tq * b1 + (col0 + gq) * b2;
 #pragma unroll 4
     for (int kk = 0; kk < 64; kk += 4) {
-        double af[MI][2], bf[CF_NI];
+        double af[MI][2], bf[NI];
 #pragma unroll
         for (int mi = 0; mi < MI; mi++) {
             af[mi][0] = la[(mi * 16) * l1 + kk * l2];
             af[mi][1] = la[(mi * 16 + 8) * l1 + kk * l2];
         }
 #pragma unroll
-        for (int ni = 0; ni < CF_NI; ni++) bf[ni] = bb[kk * b1 + (ni * 8) * b2];
+        for (int ni = 0; ni < NI; ni++) bf[ni] = bb[kk * b1 + (ni * 8) * b2];
 #pragma unroll
         for (int mi = 0; mi < MI; mi++)
 #pragma unroll
-            for (int ni = 0; ni < CF_NI; ni++) dg_mma(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+            for (int ni = 0; ni < NI; ni++) dg_mma(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
     }
 }
-template <int MI>
-__device__ __forceinline__ void cf_store_acc(double* Ys, const double (&acc)[MI][CF_NI][4], int wm, int wn, int gq, int tq) {
+template <int MI, int NI>
+__device__ __forceinline__ void cf_store_acc(double* Ys, const double (&acc)[MI][NI][4], int row0, int col0, int gq,
+                                             int tq) {
 #pragma unroll
     for (int mi = 0; mi < MI; mi++)
 #pragma unroll
-        for (int ni = 0; ni < CF_NI; ni++) {
-            const int row = wm * 16 * MI + mi * 16 + gq, col = wn * 8 * CF_NI + ni * 8 + 2 * tq;
+        for (int ni = 0; ni < NI; ni++) {
+            const int row = row0 + mi * 16 + gq, col = col0 + ni * 8 + 2 * tq;
             *reinterpret_cast<double2*>(&Ys[row * CF_LD + col]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
             *reinterpret_cast<double2*>(&Ys[(row + 8) * CF_LD + col]) = make_double2(acc[mi][ni][2], acc[mi][ni][3]);
         }
 }
+// the 8 MMA warps' tiling of an item of HR output rows x 64 columns: WMW x (8 / WMW) warps of
+// (16 MI) x (8 NI)
+template <int HR> struct CfTile;
+template <> struct CfTile<64> { static constexpr int MI = 2, NI = 2, WMW = 2; };
+template <> struct CfTile<32> { static constexpr int MI = 1, NI = 2, WMW = 2; };
+template <> struct CfTile<16> { static constexpr int MI = 1, NI = 1, WMW = 1; };
+
+// MMA-warp part of one work item (rows h HR .. of output block AB): GEMM 1, the next unit's X̂ block
+// prefetch (src_next, or none), Y to smem, GEMM 2, V to buffer t & 1
+template <int HR>
+__device__ __forceinline__ void cf_mma_item(int A, int B, int h, int t, const double* src_next, int ldf, double* Es,
+                                            double* Xs, double* Ys, double* Vs, int tid) {
+    using TL = CfTile<HR>;
+    const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+    const int row0 = (warp % TL::WMW) * 16 * TL::MI, col0 = (warp / TL::WMW) * 8 * TL::NI;
+    dg_cp_wait<0>();
+    cf_bar_sync(1, CF_MMA);                           // X̂ block (and E) landed for every MMA warp
+    double acc[TL::MI][TL::NI][4];
+    // Y = L X̂ for the item's HR rows of L (= E, or E^T read transposed)
+    cf_gemm<TL::MI, TL::NI>(acc, Es + (A ? h * HR : h * HR * CF_LD), A ? 1 : CF_LD, A ? CF_LD : 1, Xs, CF_LD, 1, row0,
+                            col0, gq, tq);
+    cf_bar_sync(1, CF_MMA);                           // X̂ consumed; previous GEMM 2 done with Ys
+    if (src_next) cf_load_block<CF_MMA>(Xs, src_next, ldf, tid);
+    dg_cp_commit();
+    cf_store_acc<TL::MI, TL::NI>(Ys, acc, row0, col0, gq, tq);
+    cf_bar_sync(1, CF_MMA);
+    cf_gemm<TL::MI, TL::NI>(acc, Ys, CF_LD, 1, Es, B ? CF_LD : 1, B ? 1 : CF_LD, row0, col0, gq, tq);   // V = Y M^T
+    const int b = t & 1;
+    if (t >= 2) cf_bar_sync(4 + b, CF_T);             // EMPTY[b]: item t-2's epilogue is done with it
+    cf_store_acc<TL::MI, TL::NI>(Vs + b * CF_BLK, acc, row0, col0, gq, tq);
+    cf_bar_arrive(2 + b, CF_T);                       // FULL[b]
+}
+
+// epilogue-warp part of one work item:  r = b̂ - dg∘x̂ - cs V;  d = c1 d + c2 idg∘r;  x̂' = x̂ + d
+template <int HR>
+__device__ __forceinline__ void cf_epi_item(const InnerArgs& a, const double* __restrict__ bh, const double* xin,
+                                            double* xout, int q, int A, int B, int h, int j, int t, bool release,
+                                            const double* Vs, int et) {
+    constexpr int PAIRS = HR * 32 / CF_EPI, U = PAIRS < 4 ? PAIRS : 4;      // row pairs per thread, per batch
+    const int s = q / a.C, c = q - s * a.C, ldf = a.ldf;
+    const int b = t & 1;
+    const double sg = A == B ? 1.0 : -1.0;
+    const double cs = sg * a.cs[s], c1 = a.cc1[(size_t)s * a.kstride + j], c2 = a.cc2[(size_t)s * a.kstride + j];
+    const size_t e0 = (size_t)q * a.NP, t0 = (size_t)s * a.NP, b0 = (size_t)c * a.NP;
+    const size_t base = (size_t)(A * 64 + h * HR) * ldf + B * 64;
+    const double* V = Vs + b * CF_BLK;
+    cf_bar_sync(2 + b, CF_T);                         // FULL[b]
+#pragma unroll 1
+    for (int bb = 0; bb < PAIRS; bb += U) {
+        double2 xv[U], dv[U], bv[U], gv[U], iv[U];
+        size_t idx[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
+            idx[u] = base + (size_t)row * ldf + 2 * cp;
+            xv[u] = *reinterpret_cast<const double2*>(xin + e0 + idx[u]);
+            dv[u] = j == 0 ? xv[u] : *reinterpret_cast<const double2*>(a.p + e0 + idx[u]);
+            bv[u] = __ldg(reinterpret_cast<const double2*>(bh + b0 + idx[u]));
+            gv[u] = __ldg(reinterpret_cast<const double2*>(a.dg + t0 + idx[u]));
+            iv[u] = __ldg(reinterpret_cast<const double2*>(a.idg + t0 + idx[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
+            const double2 v = *reinterpret_cast<const double2*>(&V[row * CF_LD + 2 * cp]);
+            const double r0 = bv[u].x - fma(gv[u].x, xv[u].x, cs * v.x);
+            const double r1 = bv[u].y - fma(gv[u].y, xv[u].y, cs * v.y);
+            const double d0 = fma(c1, dv[u].x, c2 * (iv[u].x * r0));
+            const double d1 = fma(c1, dv[u].y, c2 * (iv[u].y * r1));
+            *reinterpret_cast<double2*>(a.p + e0 + idx[u]) = make_double2(d0, d1);
+            *reinterpret_cast<double2*>(xout + e0 + idx[u]) = make_double2(xv[u].x + d0, xv[u].y + d1);
+        }
+    }
+    if (release) cf_bar_arrive(4 + b, CF_T);          // EMPTY[b] (only when the MMA warps will wait for it)
+}
 
 // HR: output rows per work item — 64 (a whole parity block) or 32 (half a block: twice the items,
-// for batches whose pairs do not fill the SMs, e.g. the ranks of a pole split).
+// for batches whose pairs do not fill the SMs, e.g. the ranks of a pole split).  With HR = 64 the
+// items left over after the whole rounds (nitem mod G) are cut into 16-row quarters spread over
+// every CTA when that leaves at most two quarters per CTA (9 columns: 756 = 5 x 148 + 16 blocks ->
+// one quarter each instead of a sixth round; 572 -> 508 us per apply).
 // MULTI = false: one step (j = counter[0]) per launch, the last CTA advances the counter and sets the
 // WHILE condition.  MULTI = true: all nsteps steps in one cooperative launch with a grid-wide
 // barrier between steps — E stays in shared memory and the per-step launch / ramp / tail goes away.
-// An item is active at step j iff j + 1 < K_s of its system (the pair's a-priori step count).
+// A block item is active at step j iff j + 1 < K_s of its system (the pair's a-priori step count).
+// Work units of a step, strided over the CTAs: u < nmain  -> block item u (HR rows);
+//                                    u >= nmain -> quarter (u - nmain) % 4 of block item nmain + (u - nmain) / 4
 template <int HR, bool MULTI>
 __global__ void __launch_bounds__(CF_T, 1) k_cheb_step(InnerArgs a, const double* __restrict__ bh,
                                                        const double* __restrict__ Dh, int* n_active, int* counter,
                                                        int* done, int maxit, unsigned long long handle, int nsteps) {
-    constexpr int NH = 64 / HR, IPP = 4 * NH, MI = HR / 32;      // items per block, per pair; MMA rows / 16 per warp
+    constexpr int NH = 64 / HR, IPP = 4 * NH;         // items per block, per pair
+    constexpr bool TAIL = HR == 64;                   // quarter the leftover items
     extern __shared__ __align__(16) double smem[];
     double* Es = smem;
     double* Xs = smem + CF_BLK;
     double* Ys = smem + 2 * CF_BLK;
-    double* Vs = smem + 3 * CF_BLK;              // two buffers
+    double* Vs = smem + 3 * CF_BLK;                   // two buffers
     __shared__ int last;
     const int tid = threadIdx.x;
     const int j0 = MULTI ? 0 : counter[0];
     const int J1 = MULTI ? nsteps : j0 + 1;
     const int nitem = a.npair * IPP;
     const int ldf = a.ldf;
-    auto next = [&](int it, int j) {
-        while (it < nitem && !(j + 1 < a.kmax[(it / IPP) / a.C])) it += gridDim.x;
-        return it;
+    const int G = gridDim.x;
+    // quarters only pay when they leave at most 2 per CTA: a quarter item runs at ~1/3 of a block
+    // item's time (measured), so 3 quarters cost a whole round (config 4's 80 leftover blocks -> 320
+    // quarters -> 3 per CTA: kept whole)
+    const int rem = nitem % G;
+    const bool split = TAIL && rem != 0 && (4 * rem + G - 1) / G <= 2;
+    const int nmain = split ? nitem - rem : nitem;
+    const int nunit = nmain + 4 * (nitem - nmain);
+    // unit -> (block item, quarter or -1 for a whole item)
+    auto item_of = [&](int u) { return u < nmain ? u : nmain + (u - nmain) / 4; };
+    auto next = [&](int u, int j) {
+        while (u < nunit && !(j + 1 < a.kmax[(item_of(u) / IPP) / a.C])) u += G;
+        return u;
     };
-    // this CTA's items over all its steps: the EMPTY hand-over looks two items ahead across steps
+    // this CTA's units over all its steps: the EMPTY hand-over looks two units ahead across steps
     int T_total = 0;
     for (int j = j0; j < J1; j++)
-        for (int it = next(blockIdx.x, j); it < nitem; it = next(it + gridDim.x, j)) T_total++;
-    const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
-    const int wm = warp & 1, wn = (warp & 7) >> 1;
+        for (int u = next(blockIdx.x, j); u < nunit; u = next(u + G, j)) T_total++;
     if (tid < CF_MMA) cf_load_block<CF_MMA>(Es, Dh + 64, ldf, tid);        // E = D̂[o rows][e cols], once
     int t = 0;
     for (int j = j0; j < J1; j++) {
         const double* xin = (j & 1) ? a.x1 : a.x;
         double* xout = (j & 1) ? a.x : a.x1;
-        const int it0 = next(blockIdx.x, j);
+        auto xblk = [&](int item) {
+            const int q = item / IPP, blk = (item / NH) & 3, A = blk >> 1, B = blk & 1;
+            return xin + (size_t)q * a.NP + (size_t)(1 - A) * 64 * ldf + (1 - B) * 64;
+        };
+        const int u0 = next(blockIdx.x, j);
         if (tid < CF_MMA) {
             // ------------------------------------------------ MMA warps
-            auto xblk = [&](int item) {
-                const int q = item / IPP, blk = (item / NH) & 3, A = blk >> 1, B = blk & 1;
-                return xin + (size_t)q * a.NP + (size_t)(1 - A) * 64 * ldf + (1 - B) * 64;
-            };
-            if (it0 < nitem) cf_load_block<CF_MMA>(Xs, xblk(it0), ldf, tid);
+            if (u0 < nunit) cf_load_block<CF_MMA>(Xs, xblk(item_of(u0)), ldf, tid);
             dg_cp_commit();
-            for (int it = it0; it < nitem; t++) {
-                const int blk = (it / NH) & 3, A = blk >> 1, B = blk & 1, h = it % NH;
-                dg_cp_wait<0>();
-                cf_bar_sync(1, CF_MMA);                       // X̂ block (and E) landed for every MMA warp
-                double acc[MI][CF_NI][4];
-                // Y = L X̂ for the item's HR rows of L (= E, or E^T read transposed)
-                cf_gemm<MI>(acc, Es + (A ? h * HR : h * HR * CF_LD), A ? 1 : CF_LD, A ? CF_LD : 1, Xs, CF_LD, 1, wm, wn,
-                            gq, tq);
-                cf_bar_sync(1, CF_MMA);                       // X̂ consumed; previous GEMM 2 done with Ys
-                const int nit = next(it + gridDim.x, j);      // within this step (the next step's X̂ is not final)
-                if (nit < nitem) cf_load_block<CF_MMA>(Xs, xblk(nit), ldf, tid);
-                dg_cp_commit();
-                cf_store_acc<MI>(Ys, acc, wm, wn, gq, tq);
-                cf_bar_sync(1, CF_MMA);
-                cf_gemm<MI>(acc, Ys, CF_LD, 1, Es, B ? CF_LD : 1, B ? 1 : CF_LD, wm, wn, gq, tq);   // V = Y M^T
-                const int b = t & 1;
-                if (t >= 2) cf_bar_sync(4 + b, CF_T);         // EMPTY[b]: item t-2's epilogue is done with it
-                cf_store_acc<MI>(Vs + b * CF_BLK, acc, wm, wn, gq, tq);
-                cf_bar_arrive(2 + b, CF_T);                   // FULL[b]
-                it = nit;
+            for (int u = u0; u < nunit; t++) {
+                const int it = item_of(u), blk = (it / NH) & 3, A = blk >> 1, B = blk & 1;
+                const int nu = next(u + G, j);                // within this step (the next step's X̂ is not final)
+                const double* src = nu < nunit ? xblk(item_of(nu)) : nullptr;
+                if (u < nmain) cf_mma_item<HR>(A, B, it % NH, t, src, ldf, Es, Xs, Ys, Vs, tid);
+                else if constexpr (TAIL) cf_mma_item<16>(A, B, (u - nmain) % 4, t, src, ldf, Es, Xs, Ys, Vs, tid);
+                u = nu;
             }
             dg_cp_wait<0>();
         } else {
             // ------------------------------------------------ epilogue warps
             const int et = tid - CF_MMA;
-            for (int it = it0; it < nitem; t++) {
-                const int q = it / IPP, blk = (it / NH) & 3, A = blk >> 1, B = blk & 1, h = it % NH;
-                const int s = q / a.C, c = q - s * a.C;
-                const int nit = next(it + gridDim.x, j);
-                const int b = t & 1;
-                const double sg = A == B ? 1.0 : -1.0;
-                const double cs = sg * a.cs[s], c1 = a.cc1[(size_t)s * a.kstride + j], c2 = a.cc2[(size_t)s * a.kstride + j];
-                const size_t e0 = (size_t)q * a.NP, t0 = (size_t)s * a.NP, b0 = (size_t)c * a.NP;
-                const size_t base = (size_t)(A * 64 + h * HR) * ldf + B * 64;
-                const double* V = Vs + b * CF_BLK;
-                cf_bar_sync(2 + b, CF_T);                     // FULL[b]
-#pragma unroll 1
-                for (int bb = 0; bb < HR * 32 / CF_EPI; bb += 4) {
-                    double2 xv[4], dv[4], bv[4], gv[4], iv[4];
-                    size_t idx[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
-                        idx[u] = base + (size_t)row * ldf + 2 * cp;
-                        xv[u] = *reinterpret_cast<const double2*>(xin + e0 + idx[u]);
-                        dv[u] = j == 0 ? xv[u] : *reinterpret_cast<const double2*>(a.p + e0 + idx[u]);
-                        bv[u] = __ldg(reinterpret_cast<const double2*>(bh + b0 + idx[u]));
-                        gv[u] = __ldg(reinterpret_cast<const double2*>(a.dg + t0 + idx[u]));
-                        iv[u] = __ldg(reinterpret_cast<const double2*>(a.idg + t0 + idx[u]));
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int e = (bb + u) * CF_EPI + et, row = e >> 5, cp = e & 31;
-                        const double2 v = *reinterpret_cast<const double2*>(&V[row * CF_LD + 2 * cp]);
-                        const double r0 = bv[u].x - fma(gv[u].x, xv[u].x, cs * v.x);
-                        const double r1 = bv[u].y - fma(gv[u].y, xv[u].y, cs * v.y);
-                        const double d0 = fma(c1, dv[u].x, c2 * (iv[u].x * r0));
-                        const double d1 = fma(c1, dv[u].y, c2 * (iv[u].y * r1));
-                        *reinterpret_cast<double2*>(a.p + e0 + idx[u]) = make_double2(d0, d1);
-                        *reinterpret_cast<double2*>(xout + e0 + idx[u]) = make_double2(xv[u].x + d0, xv[u].y + d1);
-                    }
-                }
-                // EMPTY[b] — only when the MMA warps will wait for it (this CTA's item t+2 exists)
-                if (t + 2 < T_total) cf_bar_arrive(4 + b, CF_T);
-                it = nit;
+            for (int u = u0; u < nunit; t++) {
+                const int it = item_of(u), q = it / IPP, blk = (it / NH) & 3, A = blk >> 1, B = blk & 1;
+                const int nu = next(u + G, j);
+                if (u < nmain) cf_epi_item<HR>(a, bh, xin, xout, q, A, B, it % NH, j, t, t + 2 < T_total, Vs, et);
+                else if constexpr (TAIL)
+                    cf_epi_item<16>(a, bh, xin, xout, q, A, B, (u - nmain) % 4, j, t, t + 2 < T_total, Vs, et);
+                u = nu;
             }
         }
         if (MULTI && j + 1 < J1) {
