@@ -123,6 +123,28 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
     DD_CK(dalloc(c, &f.sw, (size_t)f.NP));
     DD_CK(cudaMemcpyAsync(f.sw, swh.data(), swh.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
 
+    // parity order of the sine index (dd_ctx.h: Face3::Sp): 0-based a = 0, 2, 4, .. then 1, 3, ..
+    std::vector<int> perm, ipos(n);
+    for (int a = 0; a < n; a += 2) perm.push_back(a);
+    const int ne = (int)perm.size();
+    for (int a = 1; a < n; a += 2) perm.push_back(a);
+    for (int i = 0; i < n; i++) ipos[perm[i]] = i;
+    {
+        const char* nk = std::getenv("DD_NO_KPAR");
+        f.kpar = (ne % 64 == 0 && ne < f.ldf && !(nk && nk[0] == '1')) ? ne : 0;
+        std::vector<double> Sp((size_t)Srows * f.ldf, 0.0), SpT((size_t)Srows * f.ldf, 0.0);
+        for (int i = 0; i < n; i++)
+            for (int col = 0; col < n; col++) {
+                Sp[(size_t)i * f.ldf + col] = Sh[(size_t)perm[i] * f.ldf + col];
+                SpT[(size_t)col * f.ldf + i] = Sh[(size_t)perm[i] * f.ldf + col];
+            }
+        DD_CK(dalloc(c, &f.Sp, Sp.size()));
+        DD_CK(dalloc(c, &f.SpT, SpT.size()));
+        DD_CK(cudaMemcpyAsync(f.Sp, Sp.data(), Sp.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaMemcpyAsync(f.SpT, SpT.data(), SpT.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        DD_CK(cudaStreamSynchronize(c->stream));
+    }
+
     // --- dense fractional term via the generalised eigenproblem A_Γ U = M_Γ U Λ, U^T M U = I
     //     (RA mode, Remark 1: no dense F and no eigensolve; the interval only steers the pole split)
     if (c->frac_mode != DD_FRAC_DENSE) {
@@ -212,6 +234,37 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
             DD_CK(cudaStreamSynchronize(c->stream));   // kh and the buffers outlive the queued work
             return DD_OK;
         };
+        // B̃ = T B column by column: eigen columns of B (row-major n2 x kp in Bd) gathered into padded
+        // face vectors, two slab passes with Sp, scattered back
+        auto transform_columns = [&](double* Bd, int n2c, int ldb) -> dd_status {
+            const int BC = 256;
+            const size_t len = (size_t)BC * f.NP + (size_t)64 * f.ldf;
+            struct Bufs {
+                double *X = nullptr, *Y = nullptr;
+                ~Bufs() { cudaFree(X); cudaFree(Y); }
+            } b;
+            DD_CK(cudaMalloc(&b.X, len * sizeof(double)));
+            DD_CK(cudaMalloc(&b.Y, len * sizeof(double)));
+            DD_CK(cudaMemsetAsync(b.X, 0, len * sizeof(double), c->stream));
+            DD_CK(cudaMemsetAsync(b.Y, 0, len * sizeof(double), c->stream));
+            for (int j0 = 0; j0 < n2c; j0 += BC) {
+                const int nb = std::min(BC, n2c - j0);
+                DD_CK(face_gather_cols(Bd, n2c, ldb, j0, nb, n, f.ldf, f.NP, b.X, c->stream));
+                DD_CK(face_slab_pass(b.X, b.Y, nb, n, f.ldf, f.Sp, c->stream));
+                DD_CK(face_slab_pass(b.Y, b.X, nb, n, f.ldf, f.Sp, c->stream));
+                DD_CK(face_scatter_cols(b.X, n2c, ldb, j0, nb, n, f.ldf, f.NP, Bd, c->stream));
+            }
+            DD_CK(cudaStreamSynchronize(c->stream));
+            return DD_OK;
+        };
+        {   // Schur weights in the parity-ordered sine domain: the diagonal of T S_unit T^T
+            std::vector<double> swp(f.NP, 0.0);
+            for (int a2 = 0; a2 < n; a2++)
+                for (int b2 = 0; b2 < n; b2++) swp[(size_t)ipos[a2] * f.ldf + ipos[b2]] = swh[(size_t)a2 * f.ldf + b2];
+            DD_CK(dalloc(c, &f.sw_hat, (size_t)f.NP));
+            DD_CK(cudaMemcpyAsync(f.sw_hat, swp.data(), swp.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            DD_CK(cudaStreamSynchronize(c->stream));
+        }
         double* Ffull = nullptr;
         f.fx_r0 = 0;
         f.fx_r1 = (int)f.NP;
@@ -261,10 +314,18 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
             DD_CK(dalloc(c, &f.fxD, fx_sym_partial_doubles(f.NP, c->max_cols)));
             DD_CK(dalloc(c, &f.fxT, fx_sym_partial_doubles(f.NP, c->max_cols)));
             if (fold) {
-                dd_status fs = fold_into(Ffull);
+                // the PCG runs in the parity-ordered sine domain (T = Sp ⊗ Sp, orthogonal): there
+                // K S_unit is the diagonal K s (permuted) and γ F is B̃ B̃^T with B̃ = T B, so
+                // H̃ = T (γ F + K S_unit) T^T = γ B̃ B̃^T + K diag(s_perm) — the columns of B are
+                // transformed by the slab passes, the Gram product reruns, the diagonal is added
+                dd_status fs = transform_columns(dA, n2, kp);
                 if (fs != DD_OK) return fs;
+                DD_CK(cudaMemsetAsync(Ffull, 0, frows * (size_t)f.NP * sizeof(double), c->stream));
+                DD_CK(face_gram_scatter(dA, n2, kp, Ffull, n, f.ldf, f.NP, c->num_sms, c->stream));
+                DD_CK(face_hat_diag(Ffull, f.NP, n, f.ldf, mu_inv[0], K[0], f.sw_hat, c->stream));
                 DD_CK(dalloc(c, &f.Hp, fx_sym_packed_doubles(f.NP)));
                 DD_CK(fx_sym_pack(Ffull, f.NP, f.fblk, f.Hp, c->stream));
+                f.hat = true;
             }
         }
         DD_CK(cudaStreamSynchronize(c->stream));
@@ -315,27 +376,6 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
     //   Q (a A + b M) Q = diag(a α_ab + b μ̃_ab) + (b h^2/24) D̂ ⊗ D̂,
     //   α_ab = σ_a + σ_b,  μ̃_ab = (h^2/12)(6 + 2c_a + 2c_b + 2 c_a c_b),  D̂ = S D S,  (D v)_j = v_{j+1} - v_{j-1},
     // since M - M̃ = (h^2/24) D⊗D collects the (1,1)/(-1,-1) couplings minus their symmetrised part.
-    // parity order of the sine index (dd_ctx.h: Face3::Sp): 0-based a = 0, 2, 4, .. then 1, 3, ..
-    std::vector<int> perm, ipos(n);
-    for (int a = 0; a < n; a += 2) perm.push_back(a);
-    const int ne = (int)perm.size();
-    for (int a = 1; a < n; a += 2) perm.push_back(a);
-    for (int i = 0; i < n; i++) ipos[perm[i]] = i;
-    {
-        const char* nk = std::getenv("DD_NO_KPAR");
-        f.kpar = (ne % 64 == 0 && ne < f.ldf && !(nk && nk[0] == '1')) ? ne : 0;
-        std::vector<double> Sp((size_t)Srows * f.ldf, 0.0), SpT((size_t)Srows * f.ldf, 0.0);
-        for (int i = 0; i < n; i++)
-            for (int col = 0; col < n; col++) {
-                Sp[(size_t)i * f.ldf + col] = Sh[(size_t)perm[i] * f.ldf + col];
-                SpT[(size_t)col * f.ldf + i] = Sh[(size_t)perm[i] * f.ldf + col];
-            }
-        DD_CK(dalloc(c, &f.Sp, Sp.size()));
-        DD_CK(dalloc(c, &f.SpT, SpT.size()));
-        DD_CK(cudaMemcpyAsync(f.Sp, Sp.data(), Sp.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        DD_CK(cudaMemcpyAsync(f.SpT, SpT.data(), SpT.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        DD_CK(cudaStreamSynchronize(c->stream));
-    }
     const int ns = std::max(1, f.nsys);
     std::vector<double> sa(ns, 0.0), sb(ns, 1.0), swt(ns, 0.0), cs(ns, 0.0), dg((size_t)ns * f.NP, 0.0),
         idg((size_t)ns * f.NP, 0.0);
@@ -550,8 +590,9 @@ static InnerView view_F(Face3& f, dd_ctx* c) {
                      &c->f_inner_iter_launches, s.cc1, s.cc2, s.kmax, s.kmax_all};
 }
 
+// hat_io: r and z already live in the parity-ordered sine domain (the 3D PCG with H̃): no transforms
 static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const double* r, double* z, double* W1,
-                             double* W2) {
+                             double* W2, bool hat_io = false) {
     Face3& f = c->f3;
     InnerArgs a{};
     a.n = f.n; a.ldf = f.ldf; a.NP = f.NP;
@@ -563,9 +604,14 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
     a.dg = v.dg; a.idg = v.idg; a.cs = v.cs;
     int* n_act_slot = c->ints + v.slot_act;
     int* cnt_slot = c->ints + v.slot_cnt;
-    // r̂_c = Q r_c once per column (2 slab passes, into the parity-ordered sine domain)
-    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(r, W1, ncols, f.n, f.ldf, f.Sp, c->stream));
-    DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W1, W2, ncols, f.n, f.ldf, f.Sp, c->stream));
+    // r̂_c = Q r_c once per column (2 slab passes, into the parity-ordered sine domain); hat_io: r̂ given
+    // (copied into W2, the b̂ slot every inner kernel and the captured loop read)
+    if (hat_io) {
+        DD_CK(cudaMemcpyAsync(W2, r, sizeof(double) * (size_t)f.NP * ncols, cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(r, W1, ncols, f.n, f.ldf, f.Sp, c->stream));
+        DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W1, W2, ncols, f.n, f.ldf, f.Sp, c->stream));
+    }
     const bool cheb = f.inner_cheb && v.cc1;
     a.cc1 = v.cc1; a.cc2 = v.cc2; a.kmax = v.kmax; a.kstride = CHEB_KMAX; a.kiter = cnt_slot;
     // Chebyshev: step 1 is the init (x̂_1 = P^-1 b̂), the loop runs the other K_s - 1
@@ -673,6 +719,10 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
         *v.on_dev = false;
     }
     // ẑ_c = Σ_s w_s x̂_{s,c} (fixed system order), z_c = Q ẑ_c
+    if (hat_io) {
+        DD_TIMED(DD_KCLASS_POLESUM, inner_combine(a, v.sys_w, v.nsys, z, c->stream));
+        return DD_OK;
+    }
     DD_TIMED(DD_KCLASS_POLESUM, inner_combine(a, v.sys_w, v.nsys, W1, c->stream));
     DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W1, W2, ncols, f.n, f.ldf, f.SpT, c->stream));
     DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(W2, z, ncols, f.n, f.ldf, f.SpT, c->stream));
@@ -680,12 +730,12 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
 }
 
 // z = P_RA r on padded face vectors (rank-local systems, then the allreduce of the pole split)
-static dd_status precond_core(dd_ctx* c, int ncols, const double* r, double* z) {
+static dd_status precond_core(dd_ctx* c, int ncols, const double* r, double* z, bool hat_io = false) {
     Face3& f = c->f3;
     if (f.nsys == 0) {
         DD_CK(cudaMemsetAsync(z, 0, sizeof(double) * (size_t)f.NP * ncols, c->stream));
     } else {
-        dd_status s = inner_apply(c, view_P(f, c), ncols, r, z, f.U1, f.U2);
+        dd_status s = inner_apply(c, view_P(f, c), ncols, r, z, f.U1, f.U2, hat_io);
         if (s != DD_OK) return s;
     }
     if (f.nccl) {
@@ -722,12 +772,26 @@ static dd_status fx_apply(dd_ctx* c, int ncols, const int* colp, const double* p
     return DD_OK;
 }
 
+// q̂ = H̃ p̂ in the parity-ordered sine domain (the 3D PCG's Schur apply when f.hat)
+static dd_status schur_core_hat(dd_ctx* c, int ncols, const int* colp, const double* p, double* q) {
+    Face3& f = c->f3;
+    DD_TIMED(DD_KCLASS_GEMM_SCHUR, fx_sym_apply(f.Hp, f.fblk, f.NP, p, q, nullptr, ncols, colp, c->n_param, nullptr,
+                                                f.fxD, f.fxT, c->num_sms, c->stream));
+    return DD_OK;
+}
+
 static dd_status schur_core(dd_ctx* c, int ncols, const int* colp, const double* p, double* q) {
     Face3& f = c->f3;
     if (f.Hp) {
-        // S = K S_unit + γ F folded at setup: one packed-symmetric stream
-        DD_TIMED(DD_KCLASS_GEMM_SCHUR, fx_sym_apply(f.Hp, f.fblk, f.NP, p, q, nullptr, ncols, colp, c->n_param, nullptr,
-                                                    f.fxD, f.fxT, c->num_sms, c->stream));
+        // S = K S_unit + γ F folded at setup into one packed-symmetric stream; with f.hat that
+        // operator is T S T^T, so a physical-domain apply transforms in and out
+        if (!f.hat) return schur_core_hat(c, ncols, colp, p, q);
+        DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(p, f.U1, ncols, f.n, f.ldf, f.Sp, c->stream));
+        DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.Sp, c->stream));
+        dd_status st = schur_core_hat(c, ncols, colp, f.U2, f.U1);
+        if (st != DD_OK) return st;
+        DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U1, f.U2, ncols, f.n, f.ldf, f.SpT, c->stream));
+        DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U2, q, ncols, f.n, f.ldf, f.SpT, c->stream));
         return DD_OK;
     }
     if (f.Hrows) return fx_apply(c, ncols, colp, p, q, nullptr, f.Hrows, nullptr);   // this rank's rows of H
@@ -781,8 +845,15 @@ dd_status precond_3d(dd_ctx* c, int ncols, const int* colp, const double* rin, d
 dd_status pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double* x, double rtol, int maxit,
                  int norm_kind) {
     Face3& f = c->f3;
+    // f.hat: the whole PCG in the parity-ordered sine domain (T orthogonal: the same iteration, the
+    // inner products invariant) — b transformed once, x transformed back once, no transforms inside
+    const bool hat = f.hat;
     DD_TIMED(DD_KCLASS_OTHER, face_copy_in(f.n, f.ldf, f.NP, ncols, b, f.n2, f.r, c->stream));
-    dd_status s = precond_core(c, ncols, f.r, f.z);
+    if (hat) {
+        DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.r, f.U1, ncols, f.n, f.ldf, f.Sp, c->stream));
+        DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U1, f.r, ncols, f.n, f.ldf, f.Sp, c->stream));
+    }
+    dd_status s = precond_core(c, ncols, f.r, f.z, hat);
     if (s != DD_OK) return s;
     Pcg3 st{};
     st.NP = f.NP; st.ncols = ncols;
@@ -792,10 +863,10 @@ dd_status pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double*
     DD_TIMED(DD_KCLASS_OTHER, pcg3_start(st, c->stream));
     int k = 0;
     for (k = 1; k <= maxit; k++) {
-        s = schur_core(c, ncols, colp, f.p, f.q);
+        s = hat ? schur_core_hat(c, ncols, colp, f.p, f.q) : schur_core(c, ncols, colp, f.p, f.q);
         if (s != DD_OK) return s;
         DD_TIMED(DD_KCLASS_OTHER, pcg3_alpha(st, c->stream));
-        s = precond_core(c, ncols, f.r, f.z);
+        s = precond_core(c, ncols, f.r, f.z, hat);
         if (s != DD_OK) return s;
         DD_CK(cudaMemsetAsync(c->ints + 2, 0, sizeof(int), c->stream));
         DD_TIMED(DD_KCLASS_OTHER, pcg3_beta(st, k, maxit, c->ints + 2, c->stream));
@@ -806,6 +877,10 @@ dd_status pcg_3d(dd_ctx* c, int ncols, const int* colp, const double* b, double*
     c->h_ints[0] = std::min(k, maxit);
     DD_CK(cudaMemcpyAsync(c->ints, c->h_ints, sizeof(int), cudaMemcpyHostToDevice, c->stream));
     DD_CK(cudaStreamSynchronize(c->stream));
+    if (hat) {
+        DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.x, f.U1, ncols, f.n, f.ldf, f.SpT, c->stream));
+        DD_TIMED(DD_KCLASS_GEMM_DST, face_slab_pass(f.U1, f.x, ncols, f.n, f.ldf, f.SpT, c->stream));
+    }
     DD_TIMED(DD_KCLASS_OTHER, face_copy_out(f.n, f.ldf, f.NP, ncols, f.x, x, f.n2, c->stream));
     return DD_OK;
 }

@@ -75,7 +75,11 @@ struct Face3 {
     // packed stream, no per-apply slab transforms (DD_FX_FOLD=0 keeps transforms + F); Fp stays for
     // the bulk operator, which needs γ F alone
     double* Hp = nullptr;
-    double* Hrows = nullptr;          // the same fold for this rank's rows under a row-sharded pole split (F stays for bulk)
+    double* Hrows = nullptr;
+    // single rank: Hp holds H̃ = T H T^T in the parity-ordered sine domain (T = Sp ⊗ Sp) and the PCG
+    // runs there (no transforms around the preconditioner; dd_apply_schur transforms in and out)
+    bool hat = false;
+    double* sw_hat = nullptr;         // the Schur weights s in the parity order (the diagonal of T S_unit T^T)          // the same fold for this rank's rows under a row-sharded pole split (F stays for bulk)
     int* fblk = nullptr;              // (I, J) of each packed block
     double *fxD = nullptr, *fxT = nullptr;   // direct / transposed block partials of the packed stream
     double* Kcol = nullptr;           // per-column K (gathered from col_param)

@@ -262,6 +262,14 @@ cudaError_t fx_sym_pack(const double* F, long long NP, const int* blk, double* F
 cudaError_t face_identity_cols(int n, int ldf, long long NP, int j0, int nb, double* X, cudaStream_t st);
 cudaError_t face_fold_rows(double* F, long long NP, int n, int ldf, int j0, int nb, double gamma, const double* Y,
                            cudaStream_t st);
+// B (row-major rows x ldb, row = face node j-major) column block j0..j0+nb-1 <-> padded face vectors
+cudaError_t face_gather_cols(const double* B, int rows, int ldb, int j0, int nb, int n, int ldf, long long NP, double* X,
+                             cudaStream_t st);
+cudaError_t face_scatter_cols(const double* X, int rows, int ldb, int j0, int nb, int n, int ldf, long long NP, double* B,
+                              cudaStream_t st);
+// F <- γ F + K diag(w) on the padded NP x NP row-major F (w: padded face table)
+cudaError_t face_hat_diag(double* F, long long NP, int n, int ldf, double gamma, double K, const double* w,
+                          cudaStream_t st);
 // D = NULL: q = γ_c F p;  gp = NULL: γ_c = 1
 cudaError_t fx_sym_apply(const double* Fp, const int* blk, long long NP, const double* p, double* q, const double* D,
                          int ncols, const int* col_param, int n_param, const double* gp, double* Dpart, double* Tpart,

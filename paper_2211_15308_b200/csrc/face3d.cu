@@ -420,6 +420,46 @@ cudaError_t face_fold_rows(double* F, long long NP, int n, int ldf, int j0, int 
     k_face_fold_rows<<<1184, 256, 0, st>>>(F, NP, n, ldf, j0, nb, gamma, Y);
     return cudaGetLastError();
 }
+__global__ void k_face_gather_cols(const double* __restrict__ B, int rows, int ldb, int j0, int nb, int n, int ldf,
+                                   long long NP, double* __restrict__ X) {
+    const long long tot = (long long)rows * nb;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / nb), cc = (int)(e % nb);              // consecutive threads: consecutive columns
+        X[(size_t)cc * NP + (size_t)(i / n) * ldf + i % n] = B[(size_t)i * ldb + j0 + cc];
+    }
+}
+__global__ void k_face_scatter_cols(const double* __restrict__ X, int rows, int ldb, int j0, int nb, int n, int ldf,
+                                    long long NP, double* __restrict__ B) {
+    const long long tot = (long long)rows * nb;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / nb), cc = (int)(e % nb);
+        B[(size_t)i * ldb + j0 + cc] = X[(size_t)cc * NP + (size_t)(i / n) * ldf + i % n];
+    }
+}
+__global__ void k_face_hat_diag(double* __restrict__ F, long long NP, double gamma, double K, const double* __restrict__ w) {
+    const long long tot = NP * NP;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / NP, j = e - i * NP;
+        const double v = gamma * F[e];
+        F[e] = i == j ? fma(K, w[i], v) : v;
+    }
+}
+cudaError_t face_gather_cols(const double* B, int rows, int ldb, int j0, int nb, int n, int ldf, long long NP, double* X,
+                             cudaStream_t st) {
+    k_face_gather_cols<<<1184, 256, 0, st>>>(B, rows, ldb, j0, nb, n, ldf, NP, X);
+    return cudaGetLastError();
+}
+cudaError_t face_scatter_cols(const double* X, int rows, int ldb, int j0, int nb, int n, int ldf, long long NP, double* B,
+                              cudaStream_t st) {
+    k_face_scatter_cols<<<1184, 256, 0, st>>>(X, rows, ldb, j0, nb, n, ldf, NP, B);
+    return cudaGetLastError();
+}
+cudaError_t face_hat_diag(double* F, long long NP, int n, int ldf, double gamma, double K, const double* w,
+                          cudaStream_t st) {
+    (void)n; (void)ldf;
+    k_face_hat_diag<<<1184 * 4, 256, 0, st>>>(F, NP, gamma, K, w);
+    return cudaGetLastError();
+}
 cudaError_t face_dense_pair(int n, double hh12, double* A, double* M, cudaStream_t st) {
     k_face_dense<<<1184, 256, 0, st>>>(n, hh12, A, M);
     return cudaGetLastError();
