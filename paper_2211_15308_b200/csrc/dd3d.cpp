@@ -604,9 +604,15 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
     a.dg = v.dg; a.idg = v.idg; a.cs = v.cs;
     int* n_act_slot = c->ints + v.slot_act;
     int* cnt_slot = c->ints + v.slot_cnt;
-    // r̂_c = Q r_c once per column (2 slab passes, into the parity-ordered sine domain); hat_io: r̂ given
-    // (copied into W2, the b̂ slot every inner kernel and the captured loop read)
-    if (hat_io) {
+    // r̂_c = Q r_c once per column (2 slab passes, into the parity-ordered sine domain); hat_io: r̂ given —
+    // read in place by the cooperative multi-step path, else copied into W2 (the b̂ slot a captured
+    // WHILE loop has baked in)
+    static const bool multi_env = !(std::getenv("DD_CHEB_MULTI") && std::getenv("DD_CHEB_MULTI")[0] == '0');
+    const bool multi = f.inner_cheb && v.cc1 && f.cheb_fused && multi_env;
+    const double* bh = W2;
+    if (hat_io && multi) {
+        bh = r;
+    } else if (hat_io) {
         DD_CK(cudaMemcpyAsync(W2, r, sizeof(double) * (size_t)f.NP * ncols, cudaMemcpyDeviceToDevice, c->stream));
     } else {
         DD_TIMED(DD_KCLASS_POLESUM, face_slab_pass(r, W1, ncols, f.n, f.ldf, f.Sp, c->stream));
@@ -616,7 +622,7 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
     a.cc1 = v.cc1; a.cc2 = v.cc2; a.kmax = v.kmax; a.kstride = CHEB_KMAX; a.kiter = cnt_slot;
     // Chebyshev: step 1 is the init (x̂_1 = P^-1 b̂), the loop runs the other K_s - 1
     const int loop_max = cheb ? std::min(f.inner_maxit, v.kmax_all - 1) : f.inner_maxit;
-    if (cheb) DD_TIMED(DD_KCLASS_POLESUM, inner_init_cheb(a, W2, c->stream));
+    if (cheb) DD_TIMED(DD_KCLASS_POLESUM, inner_init_cheb(a, bh, c->stream));
     else DD_TIMED(DD_KCLASS_POLESUM, inner_init_hat(a, W2, c->stream));
     // fused Chebyshev step (n_e = 64): one persistent kernel per step that also evaluates the loop
     // condition, so it stands in the condition slot and the body is empty
@@ -646,15 +652,14 @@ static dd_status inner_apply(dd_ctx* c, const InnerView& v, int ncols, const dou
     };
     // fused steps all in one cooperative launch (grid barrier between steps; DD_CHEB_MULTI=0: one launch
     // per step inside the WHILE graph)
-    static const bool multi_env = !(std::getenv("DD_CHEB_MULTI") && std::getenv("DD_CHEB_MULTI")[0] == '0');
     if (cheb && loop_max <= 0) {
         // every system is done after the init step
         DD_CK(cudaMemsetAsync(cnt_slot, 0, sizeof(int), c->stream));
         *v.last_iters = 0;
         *v.on_dev = false;
-    } else if (fused && multi_env) {
+    } else if (multi) {
         DD_CK(cudaMemsetAsync(cnt_slot, 0, sizeof(int), c->stream));
-        DD_TIMED(DD_KCLASS_POLESUM, cheb_step_fused(a, W2, f.Dh, n_act_slot, cnt_slot, c->ints + v.slot_done, loop_max,
+        DD_TIMED(DD_KCLASS_POLESUM, cheb_step_fused(a, bh, f.Dh, n_act_slot, cnt_slot, c->ints + v.slot_done, loop_max,
                                                     0ull, c->num_sms, c->stream, loop_max));
         *v.last_iters = loop_max;
         *v.on_dev = false;
