@@ -530,6 +530,12 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
         packed = os.environ.get("DD_FX_PACKED", "1") != "0" and not (split and world > 1) and NP % 128 == 0
         nbk = NP // 128
         f_elems = nbk * (nbk + 1) // 2 * 128 * 128 if packed else cfg.n_gamma * cfg.n_gamma
+        # class-sparse: the folded sine-domain H̃ at ldf = 128 is block-diagonal in the face parity
+        # classes, so each 64-row half of a stored block keeps one 64-column quadrant (half the bytes)
+        class_sparse = (packed and ldf == 128 and (n + 1) // 2 == 64 and os.environ.get("DD_FX_FOLD", "1") != "0"
+                        and os.environ.get("DD_FX_CLASS_SPARSE", "1") != "0")
+        if class_sparse:
+            f_elems //= 2
         bytes_fx = 8.0 * f_elems + 3 * 8.0 * cfg.n_gamma * C
         g2_ms, g2_n = prof["gemm_schur"]
         ps_ms, ps_n = prof["polesum_pcg"]
@@ -554,7 +560,9 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
         ra_mode = args.frac_mode == "ra"
         classes = {"gemm_schur": {"bound": "hbm", "bytes_per_launch": None if ra_mode else bytes_fx,
                                   "share_of_step": share.get("gemm_schur"),
-                                  "f_storage": "none (RA-evaluated F)" if ra_mode else ("packed_symmetric" if packed else "full"),
+                                  "f_storage": "none (RA-evaluated F)" if ra_mode else (
+                                      ("packed_symmetric_class_sparse" if class_sparse else "packed_symmetric")
+                                      if packed else "full"),
                                   "frac": round(ach / hbm, 4) if ach else None},
                    "polesum_pcg": {"bound": "tensor" if f_in / (pk["dmma"] * 1e12) >= b_in / (hbm * 1e9) else "hbm",
                                    "what": ("face inner Chebyshev (slab DMMA operator passes, fused step epilogue)" if cheb
@@ -584,7 +592,7 @@ def schur_line(args, cfg, world, S, ras, B, colp, C, C_all, solves_per_step, spl
         roof["classes"] = classes
         roof["f_stream"] = {"achieved_gbs": round(ach, 1) if ach else None, "frac": round(ach / hbm, 4) if ach else None,
                             "frac_vs_nominal_8000gbs": round(ach / 8000.0, 4) if ach else None}
-        fkey = "gemm_schur_packed" if packed else "gemm_schur"
+        fkey = ("gemm_schur_packed_cs" if class_sparse else "gemm_schur_packed") if packed else "gemm_schur"
         ikey = ("cheb_step" if os.environ.get("DD_CHEB_FUSED", "1") != "0" and n == 127 else "cheb_two_pass") if cheb \
             else "inner_update"
         tkey = fkey if roof["class"] == "gemm_schur" else ikey

@@ -119,8 +119,11 @@ typedef struct {
  * (cuSOLVER, n_Γ = (N-1)^2) and keeps two packed-symmetric operators, F (for the bulk operator) and
  * the Schur operator in the parity-ordered sine domain, T (γ F + K S_unit) T^T with T = Sp ⊗ Sp
  * (the PCG runs in that orthogonal basis; dd_apply_schur / dd_pcg_solve take and return
- * physical-domain vectors) — at N = 128 1.08 GB each, plus a transient dense n_Γ^2 (2.1 GB) during
- * setup; under a pole split each rank keeps its rows of F and of γ F + K S_unit instead.
+ * physical-domain vectors) — at N = 128 1.08 GB for F; the sine-domain operator is block-diagonal
+ * in the face parity classes c(a,b) = par(a) xor par(b) and is stored class-sparse (one 64 x 64
+ * quadrant per stored half block, 0.54 GB; DD_FX_CLASS_SPARSE=0 keeps the full blocks), plus a
+ * transient dense n_Γ^2 (2.1 GB) during setup; under a pole split each rank keeps its rows of F and
+ * of γ F + K S_unit instead.
  * Returns DD_EINVAL for dim not in {2,3}, N < 2, gamma_face != 0, K <= 0, mu_inv < 0,
  * a pole >= 0 or not finite, n_param < 1, n_poles < 0, max_cols < 1.
  */

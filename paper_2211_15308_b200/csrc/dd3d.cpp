@@ -323,8 +323,14 @@ dd_status setup_3d(dd_ctx* c, const double* K, const double* mu_inv, const doubl
                 DD_CK(cudaMemsetAsync(Ffull, 0, frows * (size_t)f.NP * sizeof(double), c->stream));
                 DD_CK(face_gram_scatter(dA, n2, kp, Ffull, n, f.ldf, f.NP, c->num_sms, c->stream));
                 DD_CK(face_hat_diag(Ffull, f.NP, n, f.ldf, mu_inv[0], K[0], f.sw_hat, c->stream));
-                DD_CK(dalloc(c, &f.Hp, fx_sym_packed_doubles(f.NP)));
-                DD_CK(fx_sym_pack(Ffull, f.NP, f.fblk, f.Hp, c->stream));
+                // the face pencil keeps the parity classes c(a,b) = par(a) xor par(b) of the sine modes
+                // (A is sine-diagonal, M - M̃ couples opposite parities in both indices), so H̃ is
+                // block-diagonal in them: at ldf = 128 each 64-row half of a 128 x 128 block has one
+                // nonzero 64-column quadrant (the others are rounding, ~1e-15 relative: dropped)
+                const char* csenv = std::getenv("DD_FX_CLASS_SPARSE");
+                f.hat_cs = cheb_fused_ok(n, f.ldf) && !(csenv && csenv[0] == '0');
+                DD_CK(dalloc(c, &f.Hp, fx_sym_packed_doubles(f.NP, f.hat_cs)));
+                DD_CK(fx_sym_pack(Ffull, f.NP, f.fblk, f.Hp, c->stream, f.hat_cs));
                 f.hat = true;
             }
         }
@@ -781,7 +787,7 @@ static dd_status fx_apply(dd_ctx* c, int ncols, const int* colp, const double* p
 static dd_status schur_core_hat(dd_ctx* c, int ncols, const int* colp, const double* p, double* q) {
     Face3& f = c->f3;
     DD_TIMED(DD_KCLASS_GEMM_SCHUR, fx_sym_apply(f.Hp, f.fblk, f.NP, p, q, nullptr, ncols, colp, c->n_param, nullptr,
-                                                f.fxD, f.fxT, c->num_sms, c->stream));
+                                                f.fxD, f.fxT, c->num_sms, c->stream, f.hat && f.hat_cs));
     return DD_OK;
 }
 

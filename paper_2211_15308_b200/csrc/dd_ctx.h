@@ -79,6 +79,7 @@ struct Face3 {
     // single rank: Hp holds H̃ = T H T^T in the parity-ordered sine domain (T = Sp ⊗ Sp) and the PCG
     // runs there (no transforms around the preconditioner; dd_apply_schur transforms in and out)
     bool hat = false;
+    bool hat_cs = false;              // Hp packed class-sparse (one 64 x 64 quadrant per half block)
     double* sw_hat = nullptr;         // the Schur weights s in the parity order (the diagonal of T S_unit T^T)          // the same fold for this rank's rows under a row-sharded pole split (F stays for bulk)
     int* fblk = nullptr;              // (I, J) of each packed block
     double *fxD = nullptr, *fxT = nullptr;   // direct / transposed block partials of the packed stream

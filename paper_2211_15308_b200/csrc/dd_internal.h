@@ -252,11 +252,14 @@ cudaError_t face_slab_pass_scaled(const double* in, double* out, int nslab, int 
                                   const double* w, long long sW, int group, const double* colscale, cudaStream_t st);
 // packed-symmetric F stream (fx_sym.cu): upper 128 x 128 blocks, one read per block, two products
 int fx_sym_blocks(long long NP);
-size_t fx_sym_packed_doubles(long long NP);
+size_t fx_sym_packed_doubles(long long NP, bool class_sparse = false);
 size_t fx_sym_partial_doubles(long long NP, int max_cols);
 bool fx_sym_supported(long long NP);
 void fx_sym_block_table(long long NP, std::vector<int>& ij);          // (I, J) per packed block
-cudaError_t fx_sym_pack(const double* F, long long NP, const int* blk, double* Fp, cudaStream_t st);
+// class_sparse: keep per half only its nonzero 64-column quadrant (the sine-domain H̃ at ldf = 128,
+// block-diagonal in the face-index parity classes)
+cudaError_t fx_sym_pack(const double* F, long long NP, const int* blk, double* Fp, cudaStream_t st,
+                        bool class_sparse = false);
 // S_unit folded into F at setup (dd3d.cpp): identity columns of the real face nodes j0.. j0+nb-1,
 // and rows pad(j) of the dense F replaced by γ F + Y (Y = K S_unit e_j from the slab passes)
 cudaError_t face_identity_cols(int n, int ldf, long long NP, int j0, int nb, double* X, cudaStream_t st);
@@ -273,7 +276,7 @@ cudaError_t face_hat_diag(double* F, long long NP, int n, int ldf, double gamma,
 // D = NULL: q = γ_c F p;  gp = NULL: γ_c = 1
 cudaError_t fx_sym_apply(const double* Fp, const int* blk, long long NP, const double* p, double* q, const double* D,
                          int ncols, const int* col_param, int n_param, const double* gp, double* Dpart, double* Tpart,
-                         int num_sms, cudaStream_t st);
+                         int num_sms, cudaStream_t st, bool class_sparse = false);
 size_t face_fx_ws_doubles(long long NP, int ncols, int num_sms);
 int face_fx_tiles(long long NP, int ncols);
 cudaError_t face_fx(const double* F, long long NP, const double* p, double* q, const double* D, int ncols,

@@ -27,11 +27,21 @@
 namespace dd {
 
 namespace {
-constexpr int BT = 128, HR = 64, STAGES = 3, THREADS = 256;
-constexpr int HALF = HR * BT;                 // 8192 doubles = 64 KB
+constexpr int BT = 128, HR = 64, THREADS = 256;
 constexpr int BLOCK_ELEMS = BT * BT;          // 16384 doubles
 constexpr int XLD = BT + 4;                   // x-slice row stride (conflict-free fragment loads)
-constexpr size_t SMEM = ((size_t)STAGES * HALF + 2 * 2 * 8 * XLD) * sizeof(double);
+// CS (class-sparse, the sine-domain H̃ at N = 128): each 64-row half of a block holds only its one
+// nonzero 64-column quadrant — half the bytes and the MMAs; a deeper ring of the 32 KB halves
+template <bool CS> struct FxCfg {
+    static constexpr int HW = CS ? 64 : BT;             // stored columns per half
+    static constexpr int HALF = HR * HW;                 // doubles per half (64 KB / 32 KB)
+    static constexpr int STAGES = CS ? 5 : 3;
+    // x slices of block b' ride in the cp.async group of its first half (issued STAGES - 1 halves
+    // ahead), so up to 1 + STAGES / 2 blocks' slices are live at once
+    static constexpr int NXB = 1 + STAGES / 2;
+    static constexpr size_t SMEM = ((size_t)STAGES * HALF + (size_t)NXB * 2 * 8 * XLD) * sizeof(double);
+};
+constexpr size_t SMEM_MAX = FxCfg<false>::SMEM > FxCfg<true>::SMEM ? FxCfg<false>::SMEM : FxCfg<true>::SMEM;
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -42,14 +52,19 @@ __device__ __forceinline__ void mma(double (&c)[4], double a0, double a1, double
                  : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
                  : "d"(a0), "d"(a1), "d"(b));
 }
-// swizzled smem index of half-block element (r, c): the column's bits 2-3 XOR the row's bits 0-1
-__device__ __forceinline__ int swz(int r, int c) { return r * BT + (c ^ ((r & 3) << 2)); }
+// swizzled smem index of half-block element (r, c), rows of HW doubles: the column's bits 2-3 XOR
+// the row's bits 0-1
+template <int HW>
+__device__ __forceinline__ int swz(int r, int c) { return r * HW + (c ^ ((r & 3) << 2)); }
 __host__ __device__ __forceinline__ int seg_b0(int g, int nb, int G) { return (int)((long long)g * nb / G); }
 }  // namespace
 
+template <bool CS>
 __global__ void __launch_bounds__(THREADS, 1)
     k_fx_sym(const double* __restrict__ Fp, const int2* __restrict__ blk, int nblocks, long long NP,
              const double* __restrict__ x, int ncols, double* __restrict__ Dpart, double* __restrict__ Tpart) {
+    using C = FxCfg<CS>;
+    constexpr int HW = C::HW, HALF = C::HALF, STAGES = C::STAGES, NXB = C::NXB;
     extern __shared__ __align__(16) double sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
     const int cg = blockIdx.y;                               // group of 8 columns
@@ -60,47 +75,49 @@ __global__ void __launch_bounds__(THREADS, 1)
     double* Tp = Tpart + (size_t)cg * pstride;
     const bool direct = warp < 4;
     const int w4 = warp & 3;
+    const int NB = (int)(NP / BT);
 
-    // x slices of block b: [b & 1][I | J][n][k] (zero columns past ncols), staged with the ring
+    // x slices of block b: [b % NXB][I | J][n][k] (zero columns past ncols), staged with the ring
     double* xs = sm + (size_t)STAGES * HALF;
     auto load_x = [&](int b) {                               // 2 x 8 x 128 doubles, 4 chunks per thread
         const int2 IJ = blk[b];
 #pragma unroll
         for (int j = 0; j < 2 * 8 * BT / 2 / THREADS; j++) {
             const int ch = tid + j * THREADS, which = ch >> 9, n = (ch >> 6) & 7, k2 = (ch & 63) * 2;
-            double* dst = xs + (((size_t)(b & 1) * 2 + which) * 8 + n) * XLD + k2;
+            double* dst = xs + (((size_t)(b % NXB) * 2 + which) * 8 + n) * XLD + k2;
             if (cg * 8 + n < ncols)
                 cp16(dst, x + (size_t)(cg * 8 + n) * NP + (size_t)(which ? IJ.y : IJ.x) * BT + k2);
             else
                 dst[0] = dst[1] = 0.0;
         }
     };
-    auto load_half = [&](long long u) {
+    auto load_half = [&](long long u) {                      // + the block's x slices with its first half
+        if ((u & 1) == 0) load_x((int)(u >> 1));
         const double* src = Fp + (size_t)u * HALF;
         double* dst = sm + (size_t)((u - u0) % STAGES) * HALF;
 #pragma unroll
         for (int j = 0; j < HALF / 2 / THREADS; j++) {       // 16-byte chunks
             const int ch = tid + j * THREADS;
-            const int r = ch >> 6, c2 = (ch & 63) * 2;
-            cp16(dst + swz(r, c2), src + (size_t)r * BT + c2);
+            const int r = ch / (HW / 2), c2 = (ch % (HW / 2)) * 2;
+            cp16(dst + swz<HW>(r, c2), src + (size_t)r * HW + c2);
         }
     };
 #pragma unroll
     for (int s = 0; s < STAGES - 1; s++) {
         if (u0 + s < u1) load_half(u0 + s);
-        if (s == 0 && b0 < b1) load_x(b0);
         asm volatile("cp.async.commit_group;\n" ::);
     }
-    double acc[2][4];                // direct: [half] row-run accumulators; transposed: [mt] block outputs
+    double acc[2][4];                // direct: [half] row-run accumulators; transposed: [output column half] block outputs
 #pragma unroll
     for (int h = 0; h < 2; h++) acc[h][0] = acc[h][1] = acc[h][2] = acc[h][3] = 0.0;
     int seg_first = b0;              // first block of the current direct segment
-    const int NB = (int)(NP / BT);
     int2 IJ = b0 < b1 ? blk[b0] : make_int2(0, 0);           // then walked arithmetically (row-major upper blocks)
     int slot = 0;                                            // ring slot of the current half
     double bx[32];                                           // the B fragments of this block (x_J or x_I)
     for (int b = b0; b < b1; b++) {
         const bool offdiag = IJ.x != IJ.y;
+        // CS: half h (block rows 64h..) holds the block columns 64 (h ^ cIJ) .. (face row classes of I, J)
+        const int cIJ = CS ? (((IJ.x >= NB / 2) ? 1 : 0) ^ ((IJ.y >= NB / 2) ? 1 : 0)) : 0;
         if (!direct) {
 #pragma unroll
             for (int m = 0; m < 2; m++) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.0;
@@ -111,28 +128,56 @@ __global__ void __launch_bounds__(THREADS, 1)
             asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 2));
             __syncthreads();
             if (u + STAGES - 1 < u1) load_half(u + STAGES - 1);
-            if (h == 0 && b + 1 < b1) load_x(b + 1);          // lands with half 2(b+1), awaited at block b+1
             asm volatile("cp.async.commit_group;\n" ::);
             const double* S = sm + (size_t)slot * HALF;
             slot = slot + 1 == STAGES ? 0 : slot + 1;
             if (h == 0) {                                     // this block's B fragments from the staged slices
-                const double* xr = xs + (((size_t)(b & 1) * 2 + (direct ? 1 : 0)) * 8 + gq) * XLD + tq;
+                const double* xr = xs + (((size_t)(b % NXB) * 2 + (direct ? 1 : 0)) * 8 + gq) * XLD + tq;
 #pragma unroll
                 for (int k = 0; k < 32; k++) bx[k] = xr[4 * k];
             }
+            const int hp = h ^ cIJ;                           // CS: the stored column half
             if (direct) {
-                // rows 16 w4 + gq (+8) of this half, K = the block's 128 columns
+                // rows 16 w4 + gq (+8) of this half, K = its stored columns (block columns 64 hp .. under CS)
                 const int r = 16 * w4 + gq;
+                if constexpr (CS) {
+                    // compile-time register indices on both branches (hp is uniform per block)
+                    if (hp == 0) {
 #pragma unroll
-                for (int kk = 0; kk < BT; kk += 4) mma(acc[h], S[swz(r, kk + tq)], S[swz(r + 8, kk + tq)], bx[kk / 4]);
+                        for (int kk = 0; kk < HW; kk += 4)
+                            mma(acc[h], S[swz<HW>(r, kk + tq)], S[swz<HW>(r + 8, kk + tq)], bx[kk / 4]);
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < HW; kk += 4)
+                            mma(acc[h], S[swz<HW>(r, kk + tq)], S[swz<HW>(r + 8, kk + tq)], bx[16 + kk / 4]);
+                    }
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < BT; kk += 4)
+                        mma(acc[h], S[swz<HW>(r, kk + tq)], S[swz<HW>(r + 8, kk + tq)], bx[kk / 4]);
+                }
             } else if (offdiag) {
-                // outputs: block columns 32 w4 + 16 mt + gq (+8); K = this half's 64 rows
+                if constexpr (CS) {
+                    // outputs: block columns 64 hp + 16 w4 + gq (+8); K = this half's 64 rows
+                    const int m = 16 * w4 + gq;
+                    if (hp == 0) {
 #pragma unroll
-                for (int mt = 0; mt < 2; mt++) {
-                    const int m = 32 * w4 + 16 * mt + gq;
+                        for (int kk = 0; kk < HR; kk += 4)
+                            mma(acc[0], S[swz<HW>(kk + tq, m)], S[swz<HW>(kk + tq, m + 8)], bx[(h * HR + kk) / 4]);
+                    } else {
 #pragma unroll
-                    for (int kk = 0; kk < HR; kk += 4)
-                        mma(acc[mt], S[swz(kk + tq, m)], S[swz(kk + tq, m + 8)], bx[(h * HR + kk) / 4]);
+                        for (int kk = 0; kk < HR; kk += 4)
+                            mma(acc[1], S[swz<HW>(kk + tq, m)], S[swz<HW>(kk + tq, m + 8)], bx[(h * HR + kk) / 4]);
+                    }
+                } else {
+                    // outputs: block columns 32 w4 + 16 mt + gq (+8); K = this half's 64 rows
+#pragma unroll
+                    for (int mt = 0; mt < 2; mt++) {
+                        const int m = 32 * w4 + 16 * mt + gq;
+#pragma unroll
+                        for (int kk = 0; kk < HR; kk += 4)
+                            mma(acc[mt], S[swz<HW>(kk + tq, m)], S[swz<HW>(kk + tq, m + 8)], bx[(h * HR + kk) / 4]);
+                    }
                 }
             }
         }
@@ -156,7 +201,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             double* t = Tp + (size_t)b * BT * 8;              // Tp[b][n][row of block column J]
 #pragma unroll
             for (int mt = 0; mt < 2; mt++) {
-                const int m = 32 * w4 + 16 * mt + gq;
+                const int m = CS ? 64 * mt + 16 * w4 + gq : 32 * w4 + 16 * mt + gq;
                 t[(2 * tq) * BT + m] = acc[mt][0];
                 t[(2 * tq + 1) * BT + m] = acc[mt][1];
                 t[(2 * tq) * BT + m + 8] = acc[mt][2];
@@ -236,6 +281,20 @@ __global__ void __launch_bounds__(RCH * RTH)
     }
 }
 
+// full row-major NP x NP F -> packed upper blocks, class-sparse: per half h of block (I, J) the 64 x 64
+// quadrant at block columns 64 (h ^ c(I) ^ c(J)), c(I) = I >= NB/2 (the face row's parity class)
+__global__ void k_fx_pack_cs(const double* __restrict__ F, long long NP, const int2* __restrict__ blk, int nblocks,
+                             double* __restrict__ Fp) {
+    const int NB = (int)(NP / BT);
+    const size_t total = (size_t)nblocks * BLOCK_ELEMS / 2;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t b = idx / (BLOCK_ELEMS / 2), e = idx % (BLOCK_ELEMS / 2);
+        const int h = (int)(e / (HR * 64)), r = (int)((e / 64) % HR), k = (int)(e % 64);
+        const int2 IJ = blk[b];
+        const int hp = h ^ (IJ.x >= NB / 2 ? 1 : 0) ^ (IJ.y >= NB / 2 ? 1 : 0);
+        Fp[idx] = F[((size_t)IJ.x * BT + h * HR + r) * NP + (size_t)IJ.y * BT + hp * 64 + k];
+    }
+}
 // full row-major NP x NP F -> packed upper blocks (row-major 128 x 128 each: two 64-row halves)
 __global__ void k_fx_pack(const double* __restrict__ F, long long NP, const int2* __restrict__ blk, int nblocks,
                           double* __restrict__ Fp) {
@@ -252,7 +311,9 @@ int fx_sym_blocks(long long NP) {
     const int NB = (int)(NP / BT);
     return NB * (NB + 1) / 2;
 }
-size_t fx_sym_packed_doubles(long long NP) { return (size_t)fx_sym_blocks(NP) * BLOCK_ELEMS; }
+size_t fx_sym_packed_doubles(long long NP, bool class_sparse) {
+    return (size_t)fx_sym_blocks(NP) * BLOCK_ELEMS / (class_sparse ? 2 : 1);
+}
 size_t fx_sym_partial_doubles(long long NP, int max_cols) {
     return (size_t)fx_sym_blocks(NP) * BT * 8 * (size_t)((max_cols + 7) / 8);
 }
@@ -265,24 +326,35 @@ void fx_sym_block_table(long long NP, std::vector<int>& ij) {
         for (int J = I; J < NB; J++) { ij.push_back(I); ij.push_back(J); }
 }
 
-cudaError_t fx_sym_pack(const double* F, long long NP, const int* blk, double* Fp, cudaStream_t st) {
-    k_fx_pack<<<148 * 8, 256, 0, st>>>(F, NP, reinterpret_cast<const int2*>(blk), fx_sym_blocks(NP), Fp);
+cudaError_t fx_sym_pack(const double* F, long long NP, const int* blk, double* Fp, cudaStream_t st, bool class_sparse) {
+    if (class_sparse)
+        k_fx_pack_cs<<<148 * 8, 256, 0, st>>>(F, NP, reinterpret_cast<const int2*>(blk), fx_sym_blocks(NP), Fp);
+    else
+        k_fx_pack<<<148 * 8, 256, 0, st>>>(F, NP, reinterpret_cast<const int2*>(blk), fx_sym_blocks(NP), Fp);
     return cudaGetLastError();
 }
 
 cudaError_t fx_sym_apply(const double* Fp, const int* blk, long long NP, const double* p, double* q, const double* D,
                          int ncols, const int* col_param, int n_param, const double* gp, double* Dpart, double* Tpart,
-                         int num_sms, cudaStream_t st) {
+                         int num_sms, cudaStream_t st, bool class_sparse) {
     if (ncols <= 0) return cudaSuccess;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_fx_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_fx_sym<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)FxCfg<false>::SMEM);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_fx_sym<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FxCfg<true>::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     const int nb = fx_sym_blocks(NP), NB = (int)(NP / BT), ncg = (ncols + 7) / 8;
     const int G = std::min(nb, num_sms);
-    k_fx_sym<<<dim3(G, ncg), THREADS, SMEM, st>>>(Fp, reinterpret_cast<const int2*>(blk), nb, NP, p, ncols, Dpart, Tpart);
+    if (class_sparse)
+        k_fx_sym<true><<<dim3(G, ncg), THREADS, FxCfg<true>::SMEM, st>>>(Fp, reinterpret_cast<const int2*>(blk), nb, NP, p,
+                                                                        ncols, Dpart, Tpart);
+    else
+        k_fx_sym<false><<<dim3(G, ncg), THREADS, FxCfg<false>::SMEM, st>>>(Fp, reinterpret_cast<const int2*>(blk), nb, NP,
+                                                                          p, ncols, Dpart, Tpart);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     k_fx_sym_reduce<<<dim3(NB, ncg, ROUT), RCH * RTH, 0, st>>>(Dpart, Tpart, NB, nb, G, NP, ncols, col_param, n_param, gp, D,

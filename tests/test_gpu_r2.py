@@ -406,3 +406,27 @@ def test_cfg4_fused_step_truncated_loop(lib, cfg4, monkeypatch, cap):
             S.close()
     assert rel_l2_cols(out["1"], out["0"]) <= 1e-12
     assert np.all(np.isfinite(out["1"])) and np.linalg.norm(out["1"]) > 0
+
+
+def test_cfg4_class_sparse_stream_matches_dense_blocks(lib, cfg4, monkeypatch):
+    """The sine-domain H̃ is block-diagonal in the face-index parity classes (A sine-diagonal, M - M̃
+    couples opposite parities in both indices): the class-sparse packed stream (one 64 x 64 quadrant
+    per half block) against the full packed blocks (DD_FX_CLASS_SPARSE=0) — the dropped quadrants
+    are rounding — for S x and the whole PCG."""
+    g, N, ra, B, colp = cfg4
+    K, gam = float(g["K"]), float(g["gamma"])
+    Bt = torch.as_tensor(B[:4], device="cuda")
+    out = {}
+    for cs in ("1", "0"):
+        monkeypatch.setenv("DD_FX_CLASS_SPARSE", cs)
+        S = lib.Solver(3, N, [(K, gam)], [ra], max_cols=4, device=0)
+        try:
+            y = S.apply_schur(Bt, colp[:4]).cpu().numpy()
+            res = S.pcg_solve(Bt, colp[:4], rtol=1e-10, maxit=200)
+            out[cs] = (y, res.iters.copy(), res.x.cpu().numpy())
+        finally:
+            S.close()
+    assert rel_l2_cols(out["1"][0], out["0"][0]) <= 1e-13
+    assert np.all(np.abs(out["1"][1] - out["0"][1]) <= 1)
+    assert rel_l2_cols(out["1"][2], out["0"][2]) <= 1e-10
+    assert rel_l2_cols(out["1"][0], g["y"][:4]) <= 1e-10
