@@ -144,6 +144,8 @@ PoleGeom make_pole_geom(int n);
 bool pole_geom_supported(const PoleGeom& g);
 int polesum_groups(const PoleGeom& g);
 int polesum_warps(const PoleGeom& g);
+bool polesum_compact(const PoleGeom& g, int max_sys);
+size_t polesum_smem_v(const PoleGeom& g, int max_sys, int v);
 size_t polesum_smem(const PoleGeom& g, int max_sys);
 bool polesum_v2_supported(const PoleGeom& g, int max_sys);
 cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b,

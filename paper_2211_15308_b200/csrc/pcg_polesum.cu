@@ -20,6 +20,8 @@
 // PCG: one fused kernel per iteration after the two
 // GEMMs: α = ρ/(p·q); x += αp; r -= αq; z = P r; ρ' = r·z; η test; β = ρ'/ρ; p = z + βp.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "dd_internal.h"
 
@@ -608,7 +610,7 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
 template <int LMAX, int G, int NG, int V = 0>
 __device__ __forceinline__ void block_polesum(const PoleTabs& t, const PoleGeom& g, int param, const double* R,
                                               double* Z, double* scratch, long long* dbg = nullptr) {
-    if constexpr (V == 1) {                      // t.v2 set: FULL geometry with 16-row chunks
+    if constexpr (V >= 1) {                      // t.v2 set: FULL geometry with 16-row chunks
         block_polesum_v2<32 * G, 32 * G * NG>(t, param, R, Z, scratch, dbg);
         return;
     } else {
@@ -651,17 +653,30 @@ __device__ __forceinline__ Smem carve(double* sm, const PoleGeom& g) {
     const int tot = g.LL * (g.T + 1);
     return Smem{sm, sm + tot, sm + 2 * tot};
 }
+// V = 2 (merged-interior pole sum, compact): Z shares the yf rows of block_polesum_v2 (yf is last
+// read at the start of phase B, Z first written in phase C, after a block barrier), so the CTA
+// needs tot + v2_stride + 2 max_sys (T + 1) doubles and three 256-thread CTAs fit on an SM.
+template <int V>
+__device__ __forceinline__ Smem carve_v(double* sm, const PoleGeom& g, const PoleTabs& t) {
+    if constexpr (V == 2) {
+        const int tot = g.LL * (g.T + 1);
+        double* scratch = sm + tot;
+        return Smem{sm, scratch + t.v2_stride + (size_t)t.max_sys * (g.T + 1), scratch};
+    } else {
+        return carve(sm, g);
+    }
+}
 
 // ---------------------------------------------------------------------------- kernels
 template <int LMAX, int G, int NG, int V>
-__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_precond(int ncols, const int* __restrict__ col_param, PoleGeom g,
+__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 3 : 2) : 1) k_precond(int ncols, const int* __restrict__ col_param, PoleGeom g,
                                                          PoleTabs t, const double* __restrict__ r, int ldr,
                                                          double* __restrict__ z, int ldz) {
     extern __shared__ __align__(16) double sm[];
     const int c = blockIdx.x;
     if (c >= ncols) return;
     pdl_trigger();
-    Smem S = carve(sm, g);
+    Smem S = carve_v<V>(sm, g, t);
     const int npad = g.T * g.LL;
     const int param = clamp_param(col_param[c], t.n_param);
     stage_tables(t, g, param, S.scratch);
@@ -677,7 +692,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
 // i.e. the pole sum of block_polesum on the F tables (one parameter set) between two products
 // with the 1D P1 mass M_Γ = (h/6) tridiag(1, 4, 1) (Dirichlet ends).
 template <int LMAX, int G, int NG, int V>
-__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_frac_ra(int ncols, const int* __restrict__ col_param,
+__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 3 : 2) : 1) k_frac_ra(int ncols, const int* __restrict__ col_param,
                                                          int n_param, const double* __restrict__ gp, PoleGeom g,
                                                          PoleTabs t, const double* __restrict__ x, int ldx,
                                                          double* __restrict__ u, int ldu, double h6) {
@@ -685,7 +700,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_f
     const int c = blockIdx.x;
     if (c >= ncols) return;
     pdl_trigger();
-    Smem S = carve(sm, g);
+    Smem S = carve_v<V>(sm, g, t);
     const int npad = g.T * g.LL, n = g.n;
     stage_tables(t, g, 0, S.scratch);
     pdl_wait_prior();
@@ -771,7 +786,7 @@ __device__ __forceinline__ void finish_iteration(const PcgState& s, bool still_a
 }
 
 template <int LMAX, int G, int NG, int V>
-__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_pcg_init(PcgState s, PoleGeom g, PoleTabs t,
+__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 3 : 2) : 1) k_pcg_init(PcgState s, PoleGeom g, PoleTabs t,
                                                           const double* __restrict__ b, int ldb) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
@@ -779,7 +794,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     const int c = blockIdx.x;
     const int n = g.n, npad = g.T * g.LL;
     pdl_trigger();
-    Smem S = carve(sm, g);
+    Smem S = carve_v<V>(sm, g, t);
     const size_t off = (size_t)c * s.ldv;
     const int param = clamp_param(s.col_param[c], t.n_param);
     stage_tables(t, g, param, S.scratch);
@@ -837,14 +852,14 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
 
 // rows of thread tid: ρ = tid + j NT, j < RPT (coalesced); RPT = ceil(T LL / NT) <= ceil(LMAX / NG)
 template <int LMAX, int G, int NG, int V>
-__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
+__global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 3 : 2) : 1) k_pcg_iter(PcgState s, PoleGeom g, PoleTabs t) {
     constexpr int NT = 32 * G * NG;
     constexpr int RPT = (LMAX + NG - 1) / NG;
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
     const int c = blockIdx.x;
     const int n = g.n;
-    Smem S = carve(sm, g);
+    Smem S = carve_v<V>(sm, g, t);
     const size_t off = (size_t)c * s.ldv;
     const size_t offx = (size_t)c * s.ldx;
     pdl_trigger();
@@ -856,7 +871,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
     // starts (iterations of the conditional body are serialised; only the GEMM before this kernel
     // overlaps it through PDL), so p, x, r, the active flag and the iteration counter are final:
     // the v2 kernels load them before waiting on the GEMM and only q after it.
-    const bool early = V == 1 && s.cond_handle != 0;
+    const bool early = V >= 1 && s.cond_handle != 0;
     double pv[RPT], qv[RPT], xv[RPT], rv[RPT];
     int work = 0, k = 0;
     double rho_c = 0.0, eta0_c = 0.0;            // the column's ρ and η0 (written by earlier kernels only)
@@ -950,9 +965,9 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? 2 : 1) k_p
                 if (threadIdx.x == 0) s.active[c] = 0;
             } else {
                 const double beta = rz / rho_c;
-                if constexpr (V == 0) {
+                if constexpr (V != 1) {
                     // p as at entry, re-read (L2) rather than held in registers across the pole sum
-                    // (the partitioned pole sum needs every register)
+                    // (the partitioned pole sum and the 80-register compact layout need every register)
 #pragma unroll
                     for (int j = 0; j < RPT; j++) {
                         const int i = threadIdx.x + j * NT;
@@ -1230,6 +1245,21 @@ size_t polesum_smem(const PoleGeom& g, int max_sys) {
     return d * sizeof(double);
 }
 
+// The compact merged-interior layout (V = 2, three CTAs per SM): 128-chunk geometry (G = 4,
+// 256 threads), at least LL systems (Z fits in the yf rows), within a third of the SM's shared
+// memory.  DD_POLE_COMPACT=0 keeps the two-CTA layout (V = 1).
+bool polesum_compact(const PoleGeom& g, int max_sys) {
+    static const bool off = std::getenv("DD_POLE_COMPACT") && std::getenv("DD_POLE_COMPACT")[0] == '0';
+    if (off || g.G != 4 || polesum_groups(g) != 2 || max_sys < g.LL || !polesum_v2_supported(g, max_sys)) return false;
+    return polesum_smem_v(g, max_sys, 2) <= 74 * 1024;
+}
+
+size_t polesum_smem_v(const PoleGeom& g, int max_sys, int v) {
+    if (v != 2) return polesum_smem(g, max_sys);
+    const size_t tot = (size_t)g.LL * (g.T + 1);
+    return (tot + polesum_v2_doubles(g, max_sys)) * sizeof(double);
+}
+
 bool polesum_v2_supported(const PoleGeom& g, int max_sys) {
     if (g.LL != V2_L || g.n + 1 != g.T * g.LL || g.T < 32 || g.T > 256) return false;
     const int NT = 32 * polesum_warps(g);
@@ -1238,9 +1268,19 @@ bool polesum_v2_supported(const PoleGeom& g, int max_sys) {
     return (2 * tot + polesum_v2_doubles(g, max_sys)) * sizeof(double) <= 220 * 1024;
 }
 
+// Dynamic shared memory of a pole-sum kernel, with the full shared-memory carveout (the layouts
+// are sized for 2 or 3 resident CTAs per SM); DD_OCC_PRINT=1 prints the resident CTAs per SM.
 template <typename K>
-static cudaError_t set_smem(K kern, size_t bytes) {
-    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+static cudaError_t set_smem(K kern, size_t bytes, int threads = 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    static const bool occ_print = std::getenv("DD_OCC_PRINT") && std::getenv("DD_OCC_PRINT")[0] == '1';
+    if (e == cudaSuccess && occ_print && threads > 0) {
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, bytes);
+        fprintf(stderr, "[dd] pole-sum kernel: %d threads, %zu B smem, %d CTAs/SM\n", threads, bytes, nb);
+    }
+    return e;
 }
 
 // Instantiated shapes (LMAX, G, NG): n <= 1023 with G = 1, and LL = 32 chunks with G = 2, 4, 8.
@@ -1248,7 +1288,9 @@ static cudaError_t set_smem(K kern, size_t bytes) {
 #define DD_POLE_SWITCH_V(g, t, ...)                                                                \
     DD_POLE_SWITCH(g, {                                                                          \
         if constexpr (LM == V2_L) {                                                              \
-            if ((t).v2) { constexpr int VV = 1; __VA_ARGS__; }                                   \
+            if ((t).v2 && GG == 4 && polesum_compact(g, (t).max_sys)) {                          \
+                if constexpr (GG == 4) { constexpr int VV = 2; __VA_ARGS__; }                    \
+            } else if ((t).v2) { constexpr int VV = 1; __VA_ARGS__; }                            \
             else { constexpr int VV = 0; __VA_ARGS__; }                                          \
         } else { constexpr int VV = 0; __VA_ARGS__; }                                            \
     })
@@ -1270,10 +1312,10 @@ static cudaError_t set_smem(K kern, size_t bytes) {
 cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs& t, const double* b, int ldb,
                             cudaStream_t st) {
     if (s.ncols <= 0) return cudaSuccess;
-    const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
     DD_POLE_SWITCH_V(g, t, {
-        e = set_smem(k_pcg_init<LM, GG, NGG, VV>, smem);
+        const size_t smem = polesum_smem_v(g, t.max_sys, VV);
+        e = set_smem(k_pcg_init<LM, GG, NGG, VV>, smem, 32 * GG * NGG);
         if (e == cudaSuccess) k_pcg_init<LM, GG, NGG, VV><<<s.ncols, 32 * GG * NGG, smem, st>>>(s, g, t, b, ldb);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
@@ -1281,10 +1323,10 @@ cudaError_t launch_pcg_init(const PcgState& s, const PoleGeom& g, const PoleTabs
 
 cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs& t, cudaStream_t st, bool pdl) {
     if (s.ncols <= 0) return cudaSuccess;
-    const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
     DD_POLE_SWITCH_V(g, t, {
-        e = set_smem(k_pcg_iter<LM, GG, NGG, VV>, smem);
+        const size_t smem = polesum_smem_v(g, t.max_sys, VV);
+        e = set_smem(k_pcg_iter<LM, GG, NGG, VV>, smem, 32 * GG * NGG);
         if (e == cudaSuccess) e = launch_ex(k_pcg_iter<LM, GG, NGG, VV>, s.ncols, 32 * GG * NGG, smem, st, pdl, s, g, t);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
@@ -1293,10 +1335,10 @@ cudaError_t launch_pcg_iter(const PcgState& s, const PoleGeom& g, const PoleTabs
 cudaError_t launch_precond(int ncols, const int* col_param, const PoleGeom& g, const PoleTabs& t, const double* r,
                            int ldr, double* z, int ldz, cudaStream_t st, bool pdl) {
     if (ncols <= 0) return cudaSuccess;
-    const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
     DD_POLE_SWITCH_V(g, t, {
-        e = set_smem(k_precond<LM, GG, NGG, VV>, smem);
+        const size_t smem = polesum_smem_v(g, t.max_sys, VV);
+        e = set_smem(k_precond<LM, GG, NGG, VV>, smem, 32 * GG * NGG);
         if (e == cudaSuccess) e = launch_ex(k_precond<LM, GG, NGG, VV>, ncols, 32 * GG * NGG, smem, st, pdl, ncols, col_param, g, t, r, ldr, z, ldz);
     });
     return e != cudaSuccess ? e : cudaGetLastError();
@@ -1306,10 +1348,10 @@ cudaError_t launch_frac_ra(int ncols, const int* col_param, int n_param, const d
                            const PoleTabs& t, const double* x, int ldx, double* u, int ldu, double h6, cudaStream_t st,
                            bool pdl) {
     if (ncols <= 0) return cudaSuccess;
-    const size_t smem = polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
     DD_POLE_SWITCH_V(g, t, {
-        e = set_smem(k_frac_ra<LM, GG, NGG, VV>, smem);
+        const size_t smem = polesum_smem_v(g, t.max_sys, VV);
+        e = set_smem(k_frac_ra<LM, GG, NGG, VV>, smem, 32 * GG * NGG);
         if (e == cudaSuccess)
             e = launch_ex(k_frac_ra<LM, GG, NGG, VV>, ncols, 32 * GG * NGG, smem, st, pdl, ncols, col_param, n_param, gp, g, t,
                           x, ldx, u, ldu, h6);
