@@ -186,7 +186,11 @@ dd_status dd_pcg_solve(dd_ctx* ctx, int ncols, const int* col_param, const doubl
  * host->device, solves, and copies x device->host (synchronous, one synchronisation).  b is
  * read once, by the solve's first kernel: page-locked (pinned) host memory is read there in
  * place over PCIe (UVA), overlapping the transfer with that kernel; pageable memory is
- * staged by a copy first.  (DD_NO_ZERO_COPY=1 forces the copy.) */
+ * staged by a copy first.  x likewise (2D, n_Γ >= 64): into a page-locked x the kernel that
+ * freezes a column writes that column's final iterate directly, so the device->host transfer
+ * of early-converging columns overlaps the iterations of the others; a pageable x, or a solve
+ * stopped by DD_ENOTSPD / maxit = 0, gets one copy after the loop.  (DD_NO_ZERO_COPY=1 forces
+ * both copies.) */
 dd_status dd_pcg_solve_host(dd_ctx* ctx, int ncols, const int* col_param_host,
                             const double* b_host, double* x_host, double rtol, int maxit,
                             int norm_kind, int* iters, double* rel_res, double* hist);

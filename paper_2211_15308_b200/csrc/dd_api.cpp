@@ -816,6 +816,17 @@ static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const dou
     c->last_ps_warps = polesum_warps(c->geom);
     c->last_graph = 0;
     c->last_small = 0;
+    // 2D fused path with a page-locked, device-mapped host x: the freezing kernel writes each
+    // column's final x to the host buffer directly (DD_NO_ZERO_COPY=1: one copy after the loop)
+    static const bool no_zc = std::getenv("DD_NO_ZERO_COPY") && std::getenv("DD_NO_ZERO_COPY")[0] == '1';
+    if (x_host && !no_zc && c->dim == 2 && !(c->small_ok && pcg_small_supported(c->n))) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, x_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer != nullptr)
+            st.xh = static_cast<double*>(pa.devicePointer);
+        else
+            cudaGetLastError();
+    }
     if (c->dim == 3) {
         dd_status s3 = pcg_3d(c, ncols, colp, b, x, rtol, maxit, norm_kind);
         if (s3 != DD_OK) return s3;
@@ -829,7 +840,7 @@ static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const dou
     if (maxit > 0) {
         bool done = false;
         if (c->graph_ok && !c->prof) {
-            GraphKey key{ncols, colp, x, rtol, maxit, norm_kind};
+            GraphKey key{ncols, colp, x, rtol, maxit, norm_kind, st.xh};
             auto it = c->graphs.find(key);
             cudaGraphExec_t ex = nullptr;
             if (it != c->graphs.end()) {
@@ -872,7 +883,8 @@ static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const dou
     }
     CK(cudaEventRecord(c->solve_ev[1], c->stream));
     // everything the host needs comes back in one batch before the single synchronisation
-    if (x_host) CK(cudaMemcpyAsync(x_host, x, sizeof(double) * (size_t)c->ng * ncols, cudaMemcpyDeviceToHost, c->stream));
+    if (x_host && !st.xh)
+        CK(cudaMemcpyAsync(x_host, x, sizeof(double) * (size_t)c->ng * ncols, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(c->h_iters, c->iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(c->h_rel, c->relres, sizeof(double) * ncols, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(c->h_ints, c->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -880,6 +892,10 @@ static dd_status pcg_solve_impl(dd_ctx* c, int ncols, const int* colp, const dou
     if (iters) std::memcpy(iters, c->h_iters, sizeof(int) * ncols);
     if (rel_res) std::memcpy(rel_res, c->h_rel, sizeof(double) * ncols);
     const int kdone = c->h_ints[0];
+    // columns the kernels did not freeze (no iteration run, or the loop stopped on a DD_ENOTSPD of
+    // another column) have their x on the device only
+    if (st.xh && (maxit == 0 || c->h_ints[4] != 0 || c->h_ints[1] != 0))
+        CK(cudaMemcpy(x_host, x, sizeof(double) * (size_t)c->ng * ncols, cudaMemcpyDeviceToHost));
     if (c->dbg) {
         long long t[16] = {0};
         CK(cudaMemcpy(t, c->dbg, sizeof(t), cudaMemcpyDeviceToHost));

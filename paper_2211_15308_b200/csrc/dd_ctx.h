@@ -34,9 +34,10 @@ struct GraphKey {
     const double* x;
     double rtol;
     int maxit, norm_kind;
+    const double* xh;                  // PcgState::xh (baked into the graph's kernel parameters)
     bool operator<(const GraphKey& o) const {
-        return std::tie(ncols, colp, x, rtol, maxit, norm_kind) <
-               std::tie(o.ncols, o.colp, o.x, o.rtol, o.maxit, o.norm_kind);
+        return std::tie(ncols, colp, x, rtol, maxit, norm_kind, xh) <
+               std::tie(o.ncols, o.colp, o.x, o.rtol, o.maxit, o.norm_kind, o.xh);
     }
 };
 

@@ -138,6 +138,10 @@ struct PcgState {
     const double *Kp, *gp;             // per-parameter K, γ
     const int* zmixed;                 // grouped apply: write zs only if *zmixed (fallback operand)
     const double* qadd;                // RA mode: q = q + qadd (the fractional term, computed concurrently)
+    // dd_pcg_solve_host with a page-locked x: the device alias of the caller's host buffer (n x ncols,
+    // column stride n).  The kernel that freezes a column writes its final x there over PCIe, so the
+    // device-to-host transfer overlaps the iterations of the columns still running (or null).
+    double* xh;
 };
 
 PoleGeom make_pole_geom(int n);

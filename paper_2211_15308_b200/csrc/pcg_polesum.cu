@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 
                                                           const double* __restrict__ b, int ldb) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64];
-    __shared__ int s_init_last;
+    __shared__ int s_init_last, s_act;
     const int c = blockIdx.x;
     const int n = g.n, npad = g.T * g.LL;
     pdl_trigger();
@@ -827,6 +827,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 
         const bool act = eta0 > 0.0 && rz >= 0.0;
         if (rz < 0.0) atomicExch(s.status, (int)DD_ENOTSPD);
         s.active[c] = act ? 1 : 0;
+        s_act = act ? 1 : 0;
         if (c == 0 && s.hist) s.hist[0] = eta0;
         if (act) atomicAdd(s.n_active_next, 1);
         if (act && s.ntl) atomicAdd(&s.ntl_cnt[c / s.ntl_bn], 1);
@@ -836,6 +837,8 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 
         if (s_init_last) __threadfence();
     }
     __syncthreads();
+    if (s.xh && !s_act)                          // frozen at k = 0: x = 0 is final
+        for (int i = threadIdx.x; i < n; i += blockDim.x) s.xh[(size_t)c * n + i] = 0.0;
     if (s_init_last && threadIdx.x < 32) {
         int na = 0;
         if (threadIdx.x == 0) na = atomicAdd(s.n_active_next, 0);
@@ -896,6 +899,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 
     if (!early) load_pxr();
     bool still = false;
     bool flagged = false;
+    bool froze = false;                          // this launch ends the column: x is final
 #define DD_PHASE(i) \
     if (s.dbg && blockIdx.x == 0 && threadIdx.x == 0) s.dbg[i] = clock64()
     DD_PHASE(0);
@@ -913,6 +917,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 
         DD_PHASE(1);
         if (!(pq > 0.0)) {
             flagged = true;
+            froze = true;
             if (threadIdx.x == 0) {
                 atomicExch(s.status, (int)DD_ENOTSPD);
                 s.active[c] = 0;
@@ -962,6 +967,7 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 
                 if (notspd) atomicExch(s.status, (int)DD_ENOTSPD);
             }
             if (conv || notspd || k >= s.maxit) {
+                froze = true;
                 if (threadIdx.x == 0) s.active[c] = 0;
             } else {
                 const double beta = rz / rho_c;
@@ -999,6 +1005,14 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 
                 if (threadIdx.x == 0) s.rho[c] = rz;
                 still = true;
             }
+        }
+    }
+    if (froze && s.xh) {
+        // each thread's own x entries (written above by this thread, or untouched on a p.q <= 0 stop)
+#pragma unroll
+        for (int j = 0; j < RPT; j++) {
+            const int i = threadIdx.x + j * NT;
+            if (i < n) s.xh[(size_t)c * n + i] = s.x[offx + i];
         }
     }
     DD_PHASE(4);

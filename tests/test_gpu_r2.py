@@ -459,3 +459,32 @@ def test_cfg5_geometry_polesum_repeat_bitwise(lib):
         assert np.all(a.rel_res <= 1e-10)
     finally:
         S.close()
+
+
+# ------------------------------------------------------------------------- x written back by the freezing kernel
+@pytest.mark.parametrize("maxit", [0, 3, 200])
+def test_host_api_pinned_output(lib, maxit):
+    """dd_pcg_solve_host with a page-locked x: each column's final x goes to the host buffer from the
+    kernel that freezes it (zero copy, overlapped with the columns still iterating).  Bitwise equal
+    to the device-buffer solve for converged, maxit-stopped (ENOCONV) and never-iterated columns;
+    the buffer starts as NaN, so an entry the kernels skip would show."""
+    N = 512
+    params = [(1.0, 1e6), (1e-4, 1.0), (1.0, 1e2)]          # 3 / 16 / ~11 iterations: staggered freezes
+    ras = fit_all(N, params, 16)
+    B, colp = inputs.batch(N - 1, len(params), 40)
+    B[5] = 0.0                                              # η0 = 0: frozen at k = 0 with x = 0
+    S = lib.Solver(2, N, params, ras, max_cols=B.shape[0], device=0)
+    try:
+        dev = S.pcg_solve(torch.as_tensor(B, device="cuda"), colp, rtol=1e-10, maxit=maxit)
+        xd = dev.x.cpu().numpy()
+        xh = torch.full(B.shape, float("nan"), dtype=torch.float64).pin_memory().numpy()
+        bh = torch.as_tensor(B).pin_memory().numpy()
+        h = S.pcg_solve_host(bh, colp, rtol=1e-10, maxit=maxit, x_out=xh)
+        assert h.status == dev.status
+        assert np.array_equal(h.iters, dev.iters)
+        assert np.array_equal(xh, xd)
+        assert np.all(xh[5] == 0.0)
+        if maxit == 200:
+            assert dev.status == lib.DD_OK and np.all(h.rel_res <= 1e-10)
+    finally:
+        S.close()

@@ -26,3 +26,6 @@ for c in cfg5_2d_N2048_darcy cfg2_2d_N1024_sweep; do
 done
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_cheb_step|k_fx_sym" -s 100 -c 3 \
     -o $O/full_cfg4 -f python tools/prof_step.py --config cfg4_3d_N128 --solves 1 > $O/ncu_cfg4.log 2>&1; echo ncu cfg4=$?
+# per-iteration launch list of one config-5 solve outside the graph (GEMM / fused PCG vs live columns)
+DD_NO_GRAPH=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file $O/launches_cfg5_nograph.csv python tools/prof_step.py --config cfg5_2d_N2048_darcy --solves 2 > $O/ncu_nograph.log 2>&1; echo ncu_nograph=$?
