@@ -942,6 +942,15 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 
             DD_PHASE(2);
             block_polesum<LMAX, G, NG, V>(t, g, param, S.R, S.Z, S.scratch, blockIdx.x == 0 ? s.dbg : nullptr);
             DD_PHASE(3);
+            if constexpr (V == 2) {
+                // compact layout: p re-read from L2 (not held across the pole sum), issued before
+                // the dot products so the round trip overlaps the block reduction
+#pragma unroll
+                for (int j = 0; j < RPT; j++) {
+                    const int i = threadIdx.x + j * NT;
+                    pv[j] = i < n ? __ldcg(&s.p[off + i]) : 0.0;
+                }
+            }
             double rz = 0.0, zz = 0.0;
             double zv[RPT];
 #pragma unroll
@@ -971,9 +980,9 @@ __global__ void __launch_bounds__(32 * G * NG, (32 * G * NG) <= 256 ? (V == 2 ? 
                 if (threadIdx.x == 0) s.active[c] = 0;
             } else {
                 const double beta = rz / rho_c;
-                if constexpr (V != 1) {
+                if constexpr (V == 0) {
                     // p as at entry, re-read (L2) rather than held in registers across the pole sum
-                    // (the partitioned pole sum and the 80-register compact layout need every register)
+                    // (the partitioned pole sum needs every register)
 #pragma unroll
                     for (int j = 0; j < RPT; j++) {
                         const int i = threadIdx.x + j * NT;
