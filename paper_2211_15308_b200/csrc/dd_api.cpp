@@ -237,6 +237,7 @@ static dd_status build_pole_tabs(dd_ctx* c, const PoleGeom& g, int n_sets, int n
     T.v2 = nullptr;
     T.v2_stride = (int)v2_stride;
     T.v2_skip = std::getenv("DD_V2_SKIP") ? std::atoi(std::getenv("DD_V2_SKIP")) : 0;
+    T.pcr_smem = std::getenv("DD_PCR_SMEM") && std::getenv("DD_PCR_SMEM")[0] == '1';
     if (v2 && (st = up_d(v2tab, &T.v2))) return st;
     // the host vectors must outlive the async copies
     CK(cudaStreamSynchronize(c->stream));

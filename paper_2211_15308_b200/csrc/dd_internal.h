@@ -105,6 +105,7 @@ struct PoleTabs {
     const double* v2;
     int v2_stride;
     int v2_skip;                // diagnostics only (DD_V2_SKIP bitmask: 1 phase A, 2 phase B, 4 phase C)
+    int pcr_smem;               // 1: phase B's PCR through the shared-memory rows (DD_PCR_SMEM=1), 0: in registers
 };
 // v2 pole-sum table layout (dd_api.cpp build_v2_record; pcg_polesum.cu block_polesum_v2)
 constexpr int V2_L = 16;        // rows per chunk: 15 interior + 1 separator

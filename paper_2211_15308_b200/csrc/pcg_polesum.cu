@@ -503,7 +503,71 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
     // values live in its own hl row (positions 0..T, v_0 = v_T = 0); the antisymmetric period-2T
     // extension is read through the reflection x -> -x (x < 0), 2T - x (x > T) with the sign
     // flipped — no halo buffer; read, __syncwarp, write, __syncwarp per step.
-    {
+    if (!t.pcr_smem) {
+        // Register form (default): lane owns σ = 32 sl + lane + 1, sl < S, for one system at a
+        // time; distances below 32 by warp shuffles (the S registers shifted by st lanes, the
+        // wrap into the neighbouring register, the reflections at σ < 0 and σ > T), distances
+        // 32 m by register renaming plus a lane reversal where the reflection is read.  Same
+        // operations in the same order as the shared-memory form (bitwise equal), without its
+        // row stores and __syncwarp pairs.
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int k = warp; k < ((t.v2_skip & 2) ? 0 : nsys); k += NW) {
+            const double* rec = tab + V2_WSZ + k * V2_REC;
+            double* A = hl + (size_t)k * TP;
+            const double e = rec[V2_E];
+            double v[S];
+#pragma unroll
+            for (int sl = 0; sl < S; sl++) {
+                const int sg = 32 * sl + lane + 1;
+                v[sl] = sg < T ? fma(-e, yf[k * TP + sg], A[sg - 1]) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < JS; j++) {
+                const int st = 1 << j;
+                const double al = rec[V2_AL + j];
+                double nv[S];
+                if (st < 32) {
+                    double a[S], b[S];
+#pragma unroll
+                    for (int sl = 0; sl < S; sl++) {
+                        a[sl] = __shfl_sync(0xffffffffu, v[sl], (lane - st) & 31);
+                        b[sl] = __shfl_sync(0xffffffffu, v[sl], (lane + st) & 31);
+                    }
+                    const double rl = __shfl_sync(0xffffffffu, v[0], max(st - lane - 2, 0));
+                    const double rr = __shfl_sync(0xffffffffu, v[S - 1], min(max(62 - lane - st, 0), 31));
+                    const double reflL = lane == st - 1 ? 0.0 : -rl;
+#pragma unroll
+                    for (int sl = 0; sl < S; sl++) {
+                        const double left = lane >= st ? a[sl] : (sl >= 1 ? a[sl >= 1 ? sl - 1 : 0] : reflL);
+                        const double right = lane + st <= 31 ? b[sl] : (sl <= S - 2 ? b[sl <= S - 2 ? sl + 1 : 0] : -rr);
+                        nv[sl] = fma(-al, left + right, v[sl]);
+                    }
+                } else {
+                    const int m = st >> 5;
+                    // value at σ = 32 r + 31 - lane (lane 30 - lane of register r; lane 31: its own
+                    // register r - 1, or 0 at σ = 0)
+                    auto rev = [&](int r) {
+                        const double x = __shfl_sync(0xffffffffu, v[r], (30 - lane) & 31);
+                        const double own = r >= 1 ? v[r >= 1 ? r - 1 : 0] : 0.0;
+                        return lane <= 30 ? x : own;
+                    };
+#pragma unroll
+                    for (int sl = 0; sl < S; sl++) {
+                        const double left = sl >= m ? v[sl >= m ? sl - m : 0] : -rev(m - sl - 1);
+                        const double right = sl + m <= S - 1 ? v[sl + m <= S - 1 ? sl + m : 0] : -rev(2 * S - sl - m - 1);
+                        nv[sl] = fma(-al, left + right, v[sl]);
+                    }
+                }
+#pragma unroll
+                for (int sl = 0; sl < S; sl++) v[sl] = (sl == S - 1 && lane == 31) ? 0.0 : nv[sl];   // σ = T stays 0
+            }
+            const double dinv = rec[V2_DINV];
+            __syncwarp();                                   // the prologue's reads of this row precede the writes
+#pragma unroll
+            for (int sl = 0; sl < S; sl++) A[32 * sl + lane + 1] = v[sl] * dinv;   // g at σ (σ = T: 0)
+            if (lane == 0) A[0] = 0.0;
+        }
+    } else {
         const int warp = tid >> 5, lane = tid & 31;
         constexpr int NSI = 3;
         for (int k0 = warp; k0 < ((t.v2_skip & 2) ? 0 : nsys); k0 += NW * NSI) {

@@ -488,3 +488,28 @@ def test_host_api_pinned_output(lib, maxit):
             assert dev.status == lib.DD_OK and np.all(h.rel_res <= 1e-10)
     finally:
         S.close()
+
+
+# ------------------------------------------------------------------------- phase B: registers vs shared memory
+@pytest.mark.parametrize("N", [512, 1024, 2048, 4096])
+def test_pcr_register_form_bitwise(lib, monkeypatch, N):
+    """The separator PCR of the merged-interior pole sum (phase B) in its register / warp-shuffle
+    form (default) performs the same operations in the same order as the shared-memory form
+    (DD_PCR_SMEM=1, read at setup): bitwise equal preconditioner applies for T = 32, 64, 128, 256
+    chunks (S = 1, 2, 4, 8 separators per lane), including the reflections of the antisymmetric
+    extension at both ends; and the PCG result matches bitwise."""
+    params = [(1.0, 1e2), (1e-4, 1e6)]
+    ras = fit_all(N, params, 16)
+    B, colp = inputs.batch(N - 1, len(params), 8)
+    out = {}
+    for smem in ("0", "1"):
+        monkeypatch.setenv("DD_PCR_SMEM", smem)
+        S = lib.Solver(2, N, params, ras, max_cols=B.shape[0], device=0)
+        try:
+            Bt = torch.as_tensor(B, device="cuda")
+            out[smem] = (S.apply_precond(Bt, colp).cpu().numpy(),
+                         S.pcg_solve(Bt, colp, rtol=1e-10, maxit=100).x.cpu().numpy())
+        finally:
+            S.close()
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert np.array_equal(out["0"][1], out["1"][1])
