@@ -24,7 +24,7 @@ for c in cfg5_2d_N2048_darcy cfg2_2d_N1024_sweep; do
   timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_dgemm|k_pcg_iter" -s 8 -c 2 \
       -o $O/full_$c -f python tools/prof_step.py --config $c --solves 2 > $O/ncu_$c.log 2>&1; echo ncu $c=$?
 done
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_cheb_step|k_fx_sym" -s 100 -c 3 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_cheb_step|k_fx_sym" -s 6 -c 3 \
     -o $O/full_cfg4 -f python tools/prof_step.py --config cfg4_3d_N128 --solves 1 > $O/ncu_cfg4.log 2>&1; echo ncu cfg4=$?
 # per-iteration launch list of one config-5 solve outside the graph (GEMM / fused PCG vs live columns)
 DD_NO_GRAPH=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
