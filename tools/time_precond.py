@@ -22,6 +22,7 @@ ras = [rafit.fit_ra(K, g, lo, hi, cfg.n_poles) for K, g in cfg.params]
 B, colp = inputs.batch(cfg.n_gamma, len(cfg.params), cfg.rhs_per_param)
 S = binding.Solver(cfg.dim, cfg.N, cfg.params, ras, max_cols=B.shape[0], device=0)
 Bt = torch.as_tensor(B, device="cuda")
+colp = torch.as_tensor(colp, dtype=torch.int32, device="cuda")   # device col_param: no per-call conversion
 Z = torch.empty_like(Bt)
 for _ in range(5):
     S.apply_precond(Bt, colp, Z)
