@@ -1110,15 +1110,21 @@ __global__ void __launch_bounds__(32 * NG) k_pcg_small(PcgState s, PoleGeom g, P
     const int c = blockIdx.x;
     const int n = g.n, npad = g.T * g.LL;
     const int ldw = 2 * Kpad;
+    const int lws = ldw + 1;                           // smem row stride (odd: rows of a warp hit different banks)
     double* Ws = sm;                                   // n x 2Kpad
-    double* pv = Ws + (size_t)n * ldw;                 // p, T, x : 64 each
+    double* pv = Ws + (((size_t)n * lws + 1) & ~(size_t)1);   // p, T, x, q : 64 each (16-byte aligned)
     double* Tv = pv + 64;
     double* xv = Tv + 64;
-    double* psm = xv + 64;
+    double* Qv = xv + 64;
+    double* psm = Qv + 64;
     Smem S = carve(psm, g);
     const int param = clamp_param(s.col_param[c], t.n_param);
     stage_tables(t, g, param, S.scratch);
-    for (int idx = threadIdx.x; idx < n * ldw; idx += blockDim.x) Ws[idx] = W[(size_t)(idx / ldw) * lda + idx % ldw];
+    for (int idx = threadIdx.x; idx < n * ldw; idx += blockDim.x) Ws[(idx / ldw) * lws + idx % ldw] = W[(size_t)(idx / ldw) * lda + idx % ldw];
+    // matvecs: TPR threads per row (8 for n <= 31, 4 for n <= 63), each a strided share of the
+    // row, combined by a fixed xor-shuffle tree within the row's lane group
+    const int TPR = n <= 31 ? 8 : 4;
+    const int mrow = threadIdx.x / TPR, msub = threadIdx.x % TPR;
     const double Kc = Kp[param], gc = gp[param];
     for (int i = threadIdx.x; i < npad; i += blockDim.x) {
         const double v = i < n ? b[(size_t)c * ldb + i] : 0.0;
@@ -1145,24 +1151,37 @@ __global__ void __launch_bounds__(32 * NG) k_pcg_small(PcgState s, PoleGeom g, P
     while (run && k < s.maxit) {
         k++;
         // q = S_dst (K s ∘ (S_dst p)) + γ F p
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const double* wr = Ws + (size_t)i * ldw;
+        {
             double a = 0.0;
-            for (int j = 0; j < n; j++) a = fma(wr[j], pv[j], a);
-            Tv[i] = Kc * sw[i] * a;
+            if (mrow < n) {
+                const double* wr = Ws + (size_t)mrow * lws;
+                for (int j = msub; j < n; j += TPR) a = fma(wr[j], pv[j], a);
+            }
+            for (int o = TPR / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (mrow < n && msub == 0) Tv[mrow] = Kc * sw[mrow] * a;
+        }
+        __syncthreads();
+        {
+            double a = 0.0, f = 0.0;
+            if (mrow < n) {
+                const double* wr = Ws + (size_t)mrow * lws;
+                for (int j = msub; j < n; j += TPR) {
+                    a = fma(wr[j], Tv[j], a);
+                    f = fma(wr[Kpad + j], pv[j], f);
+                }
+            }
+            for (int o = TPR / 2; o > 0; o >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                f += __shfl_xor_sync(0xffffffffu, f, o);
+            }
+            if (mrow < n && msub == 0) Qv[mrow] = fma(gc, f, a);
         }
         __syncthreads();
         // n <= 63 < blockDim: thread i owns row i
         double pq = 0.0, dummy = 0.0, qi = 0.0;
         const int i = threadIdx.x;
         if (i < n) {
-            const double* wr = Ws + (size_t)i * ldw;
-            double a = 0.0, f = 0.0;
-            for (int j = 0; j < n; j++) {
-                a = fma(wr[j], Tv[j], a);
-                f = fma(wr[Kpad + j], pv[j], f);
-            }
-            qi = fma(gc, f, a);
+            qi = Qv[i];
             pq = pv[i] * qi;
         }
         block_sum2(pq, dummy, red);
@@ -1453,7 +1472,7 @@ cudaError_t launch_pcg_small(const PcgState& s, const PoleGeom& g, const PoleTab
                              cudaStream_t st) {
     if (s.ncols <= 0) return cudaSuccess;
     if (!pcg_small_supported(g.n) || g.G != 1) return cudaErrorInvalidValue;
-    const size_t smem = ((size_t)g.n * 2 * Kpad + 192) * sizeof(double) + polesum_smem(g, t.max_sys);
+    const size_t smem = ((size_t)g.n * (2 * Kpad + 1) + 1 + 256) * sizeof(double) + polesum_smem(g, t.max_sys);
     cudaError_t e = cudaSuccess;
     switch (lmax_of(g.LL)) {
         case 1: {
