@@ -26,11 +26,14 @@ def _cols(B):
 
 
 @pytest.mark.parametrize("mode", ["assembled", "factored"])
-@pytest.mark.parametrize("N,t,sigma", [(9, -0.5, 0.0), (64, -0.5, 0.0), (200, -0.25, 1.0), (1024, -0.5, 0.0)])
+@pytest.mark.parametrize("N,t,sigma", [(9, -0.5, 0.0), (64, -0.5, 0.0), (200, -0.25, 1.0), (1024, -0.5, 0.0),
+                                         (2048, -0.5, 0.0)])
 def test_ra_operator_parity(lib, N, t, sigma, mode):
+    # N = 2048 with 20 preconditioner poles and the 16-pole r_F: both pole sums (k_frac_ra and the
+    # fused PCG kernel) take the compact 3-CTA layout of the 128-chunk geometry
     params = [(1.0, 1e2), (1e-3, 1e4)]
     lo, hi = rafit.interval_1d(N)
-    ras = [rafit.fit_ra(K, g, lo, hi, 14, t=t, sigma=sigma) for K, g in params]
+    ras = [rafit.fit_ra(K, g, lo, hi, 20 if N >= 2048 else 14, t=t, sigma=sigma) for K, g in params]
     fr = rafit.fit_power(t, lo, hi, 16, sigma)
     fra = (fr.c0, fr.poles, fr.residues)
     if N <= 200:
