@@ -1121,9 +1121,9 @@ __global__ void __launch_bounds__(32 * NG) k_pcg_small(PcgState s, PoleGeom g, P
     const int param = clamp_param(s.col_param[c], t.n_param);
     stage_tables(t, g, param, S.scratch);
     for (int idx = threadIdx.x; idx < n * ldw; idx += blockDim.x) Ws[(idx / ldw) * lws + idx % ldw] = W[(size_t)(idx / ldw) * lda + idx % ldw];
-    // matvecs: TPR threads per row (8 for n <= 31, 4 for n <= 63), each a strided share of the
+    // matvecs: TPR threads per row (blockDim / 32 for n <= 31, / 64 for n <= 63), each a strided share of the
     // row, combined by a fixed xor-shuffle tree within the row's lane group
-    const int TPR = n <= 31 ? 8 : 4;
+    const int TPR = (int)blockDim.x / (n <= 31 ? 32 : 64);
     const int mrow = threadIdx.x / TPR, msub = threadIdx.x % TPR;
     const double Kc = Kp[param], gc = gp[param];
     for (int i = threadIdx.x; i < npad; i += blockDim.x) {
