@@ -478,6 +478,7 @@ __device__ void block_polesum_v2(const PoleTabs& t, int param, const double* R, 
         }
         acc[u] = a;
     }
+#pragma unroll 2
     for (int k = q; k < ((t.v2_skip & 1) ? 0 : nsys); k += Q) {
         const double* rec = tab + V2_WSZ + k * V2_REC;
         const double2* tf2 = reinterpret_cast<const double2*>(rec);
